@@ -1,0 +1,421 @@
+#!/usr/bin/env python
+"""Benchmark of the MS-LLR data-consistency hot path on B200 (one JSON line on rank 0).
+
+A step is one full data-consistency solve ``mrf_dc_cg`` (rhs = A^H y, r0 = rhs - H x0, then
+n_iter = 10 CG iterations of H = A^H A + mu I, mu = 0.01) over ALL L frames of the MRF-shaped
+workload (BASELINE.json configs[2]: 256 x 256, L = 1000, M = 2048, W = 6, sigma = 2, single
+coil), i.e. every row of SURVEY.md §8(a).  ``value`` is NUFFT non-uniform point-passes per second:
+each forward or adjoint over the L frames processes L*C*M points, and one step does 1 adjoint +
+(n_iter + 1) normal operators = (2 n_iter + 3) passes.  ``ms_per_AHA`` is the time of one normal
+operator over L frames, timed separately.  Frames are sharded contiguously over ranks (strong
+scaling, fixed L); the CG inner products are all-reduced with NCCL.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload mrf|sense|stress|cfg2]
+  python bench.py --impl reference ...    # the float64 CPU oracle on a bounded frame sample
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import synth  # noqa: E402
+
+METRIC = "NUFFT fwd+adj nonuniform pts/s and ms per A^H A (L frames); HBM GB/s vs peak"
+UNIT = "pts/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="mrf", choices=list(synth.CONFIGS))
+    ap.add_argument("--cg-iters", type=int, default=None)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target CPU work of the oracle sample")
+    ap.add_argument("--batch-frames", type=int, default=0)
+    return ap.parse_args()
+
+
+def passes_per_step(n_iter: int) -> int:
+    return 2 * n_iter + 3          # 1 adjoint + (n_iter + 1) normals, each normal = fwd + adj
+
+
+# ------------------------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi sampled every 200 ms during the timed region (B200_PROFILING.md clocks line)."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.proc = None
+        self.lines = []
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits", "-lms", "200",
+                 "-i", str(self.idx)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
+        sm, smax, reasons = [], [], set()
+        names = ["active", "hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, val in zip(names[1:], parts[3:7]):
+                if val.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------------------------ helpers
+def peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {}
+
+
+def fp32_peak_tflops(sm_count: int, mhz: float) -> float:
+    """FP32 CUDA-core peak: SMs x 128 FMA lanes x 2 flop x clock."""
+    return sm_count * 128 * 2 * mhz * 1e6 / 1e12
+
+
+def kernel_flops(cfg, cls: str, frames: int) -> float:
+    """Algorithmic FP32 flops of one kernel class over `frames` frames:
+    FFT 5 n log2 n per length-n transform, N row transforms + G column transforms per (l, c);
+    interp / spread 4 W^2 M per (l, c); deapod/coil (2 + 6C) N^2 per frame."""
+    N, G, C, M, W = cfg.N, cfg.G, cfg.C, cfg.M, cfg.W
+    f1 = 5.0 * G * math.log2(G)
+    if cls in ("fwd_rows", "adj_rows"):
+        return frames * (C * N * f1 + (2 + 6 * C) * N * N)
+    if cls in ("fwd_cols", "adj_cols"):
+        return frames * C * (G * f1 + 4 * W * W * M)
+    return 0.0
+
+
+def step_bytes(cfg, L: int, n_iter: int) -> float:
+    """Compulsory HBM bytes of one dc_cg step (SURVEY.md §8(d) "Algorithmic bytes"): adjoint
+    L(8N^2 + 8CM); each normal L 16 N^2; CG init (r = rhs - q, p = r) 4 image passes; each CG
+    iteration 10 image passes (normal 2 + <p,q> 2 + x,r update 6) -- the minimum is 8."""
+    N, C, M = cfg.N, cfg.C, cfg.M
+    img = 8.0 * N * N * L
+    return L * (8.0 * N * N + 8.0 * C * M) + (n_iter + 1) * 2 * img + 4 * img + n_iter * 8 * img
+
+
+def cpu_count():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def make_inputs(cfg, frames, device, torch):
+    """Images and k-space for this rank's frames (seeded; generated on the host, then copied)."""
+    x = synth.images(cfg, frames)
+    coils = synth.coil_maps(cfg.N, cfg.C, cfg.seed)
+    return torch.from_numpy(x).to(device), coils
+
+
+# ------------------------------------------------------------------------------------ oracle arm
+def oracle_sample(cfg, n_iter: int, target_s: float, nf=None):
+    """Time the float64 oracle's dc_cg on a bounded frame sample of the workload (calibrated so
+    the sample takes about ``target_s`` seconds).  Returns a dict (pts/s, frames, cores, ...)."""
+    from oracle import nufft as on, cg as ocg
+    workers = cpu_count()
+    traj = synth.spiral_trajectory(cfg.M, cfg.R, cfg.turns, cfg.p)
+    coils = synth.coil_maps(cfg.N, cfg.C, cfg.seed)
+    if nf is None:   # calibrate: one normal on `workers` frames
+        cal = list(range(min(cfg.L, workers)))
+        xc = synth.images(cfg, cal)
+        t0 = time.perf_counter()
+        on.normal(xc, traj, coils, cfg.W, mu=cfg.mu, frame_interleaf=synth.frame_interleaf(cal, cfg.R),
+                  workers=workers)
+        per_frame = (time.perf_counter() - t0) / len(cal) * (n_iter + 1.5)
+        nf = int(max(1, min(cfg.L, round(target_s / max(per_frame, 1e-6)))))
+    frames = list(range(nf))
+    fil = synth.frame_interleaf(frames, cfg.R)
+    x = synth.images(cfg, frames)
+    y = on.forward(x, traj, coils, cfg.W, frame_interleaf=fil, workers=workers)
+    t0 = time.perf_counter()
+    H = lambda v: on.normal(v, traj, coils, cfg.W, mu=cfg.mu, frame_interleaf=fil, workers=workers)
+    rhs = ocg.dc_rhs(on.adjoint(y, traj, coils, cfg.N, cfg.W, frame_interleaf=fil, workers=workers), None, cfg.mu)
+    ocg.cg(H, rhs, np.zeros_like(rhs), n_iter)
+    dt = time.perf_counter() - t0
+    pts = nf * cfg.C * cfg.M * passes_per_step(n_iter)
+    desc = (f"oracle dc_cg (float64 numpy/scipy, {n_iter} CG iterations) on frames 0..{nf - 1} of {cfg.L} of the "
+            f"'{cfg.name}' workload ({nf * cfg.C * cfg.M * passes_per_step(n_iter)} point-passes), "
+            f"{workers} ThreadPool workers over frames")
+    return {"value": pts / dt, "frames": nf, "cores": workers, "seconds": dt, "sample": desc}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    cfg = synth.get_config(args.workload)
+    n_iter = args.cg_iters or cfg.cg_iters
+    vals, nf, last = [], None, None
+    per_step = max(2.0, args.cpu_seconds / 2)
+    for i in range(args.warmup + args.steps):
+        last = oracle_sample(cfg, n_iter, per_step, nf=nf)
+        nf = last["frames"]
+        if i >= args.warmup:
+            vals.append(last["value"])
+    value = float(np.median(vals))
+    steps_ms = 1e3 * cfg.L * cfg.C * cfg.M * passes_per_step(n_iter) / value
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": steps_ms, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": cfg.name, "N": cfg.N, "L": cfg.L, "M": cfg.M, "C": cfg.C, "W": cfg.W,
+                   "sigma": cfg.sigma, "cg_iters": n_iter, "mu": cfg.mu,
+                   "step": "oracle dc_cg on a frame sample; ms_per_step extrapolated to all L frames"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": last["cores"], "kind": "oracle",
+                         "sample": last["sample"]},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------------------------ our arm
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+    from paper_2310_05647_b200 import binding
+    from paper_2310_05647_b200.sharding import frame_shard
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    comm = None
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=dev)
+        comm = binding.nccl_comm_create(rank, world, local)
+
+    cfg = synth.get_config(args.workload)
+    n_iter = args.cg_iters or cfg.cg_iters
+    off, L = frame_shard(cfg.L, world, rank)
+    frames = list(range(off, off + L))
+    traj = synth.spiral_trajectory(cfg.M, cfg.R, cfg.turns, cfg.p)
+    x_true, coils = make_inputs(cfg, frames, dev, torch)
+    plan = binding.Plan(cfg.N, traj, L, coils=coils, W=cfg.W, frame_offset=off, device=local, nccl_comm=comm,
+                        batch_frames=args.batch_frames)
+    y = plan.forward(x_true)
+    if cfg.noise > 0:
+        ss = torch.tensor([float((y.abs() ** 2).sum().item()), float(y.numel())], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(ss)
+        sig = cfg.noise * math.sqrt(ss[0].item() / ss[1].item())
+        y += sig * torch.from_numpy(synth.unit_noise(cfg.C, cfg.M, frames, cfg.seed)).to(dev)
+    del x_true
+    xbuf = torch.zeros(plan.x_shape, dtype=torch.complex64, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        xbuf.zero_()
+        plan.dc_cg(y, mu=cfg.mu, n_iter=n_iter, x=xbuf)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(v):
+        if world == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    # ---------------------------------------------------------------- timed region
+    clocks = ClockSampler(local)
+    plan.profile(True)
+    barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(args.steps):
+        step()
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    ms_total = max_over_ranks(ev0.elapsed_time(ev1))
+    clk = clocks.stop()
+    prof = {k: plan.profile_query(k) for k in binding.KERNEL_CLASSES}
+    plan.profile(False)
+    ms_step = ms_total / args.steps
+    pts_step = cfg.L * cfg.C * cfg.M * passes_per_step(n_iter)
+    value = pts_step / (ms_step * 1e-3)
+
+    # ---------------------------------------------------------------- per-operator timings (device)
+    def time_op(fn, reps):
+        for _ in range(2):
+            fn()
+        barrier()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(reps):
+            fn()
+        b.record(stream)
+        torch.cuda.synchronize()
+        return max_over_ranks(a.elapsed_time(b)) / reps
+
+    xin = torch.randn(plan.x_shape, dtype=torch.complex64, device=dev)
+    xout = torch.empty_like(xin)
+    yout = torch.empty(plan.y_shape, dtype=torch.complex64, device=dev)
+    reps = max(3, args.steps)
+    ms_normal = time_op(lambda: plan.normal(xin, mu=cfg.mu, out=xout), reps)
+    ms_fwd = time_op(lambda: plan.forward(xin, y=yout), reps)
+    ms_adj = time_op(lambda: plan.adjoint(y, x=xout), reps)
+    ms_cg_iter = max(0.0, (ms_step - ms_adj - ms_normal) / max(1, n_iter))
+    # cuFFT reference (timing only, never in the product path): batched C2C G x G, L*C transforms
+    cufft_ms = None
+    try:
+        B = max(1, min(64, cfg.L * cfg.C))
+        buf = torch.randn((B, cfg.G, cfg.G), dtype=torch.complex64, device=dev)
+        nchunks = math.ceil(L * cfg.C / B)
+        cufft_ms = time_op(lambda: [torch.fft.fft2(buf) for _ in range(nchunks)], 3)
+        del buf
+    except Exception:
+        cufft_ms = None
+
+    # ---------------------------------------------------------------- e2e through the C-ABI, host buffers
+    e2e = None
+    if not args.no_e2e:
+        y_h = y.cpu().pin_memory()
+        x_h = torch.zeros(plan.x_shape, dtype=torch.complex64).pin_memory()
+        plan.dc_cg(y_h, mu=cfg.mu, n_iter=n_iter, x=x_h)          # warm-up (allocates staging)
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(max(1, min(args.steps, 3))):
+            x_h.zero_()
+            plan.dc_cg(y_h, mu=cfg.mu, n_iter=n_iter, x=x_h)
+        torch.cuda.synchronize()
+        n_e2e = max(1, min(args.steps, 3))
+        ms_e2e = max_over_ranks((time.perf_counter() - t0) * 1e3 / n_e2e)
+        e2e = {"value": pts_step / (ms_e2e * 1e-3), "unit": UNIT, "ms_per_step": ms_e2e,
+               "h2d_bytes_per_step": int(y_h.numel() * 8 + x_h.numel() * 8) * world,
+               "d2h_bytes_per_step": int(x_h.numel() * 8) * world,
+               "note": "host pinned y and x0 copied in, solution x copied out, inside each mrf_dc_cg call"}
+
+    # ---------------------------------------------------------------- roofline of the dominant kernel
+    sm_count = torch.cuda.get_device_properties(dev).multi_processor_count
+    pk = peaks()
+    sm_max = float(pk.get("sm_max_mhz", 1965.0))
+    peak_alu = fp32_peak_tflops(sm_count, sm_max)
+    hbm_peak = float(pk.get("hbm_gbs", 6650.0))
+    cls_ms = {k: v[0] for k, v in prof.items()}
+    dom = max(("fwd_rows", "fwd_cols", "adj_cols", "adj_rows"), key=lambda k: cls_ms[k])
+    dom_ms, dom_n = prof[dom]
+    # frames processed by the dominant class in the timed region: each launch covers a batch
+    frames_per_call = {"fwd_rows": n_iter + 1, "fwd_cols": n_iter + 1, "adj_cols": n_iter + 2, "adj_rows": n_iter + 2}
+    dom_flops_total = kernel_flops(cfg, dom, L) * frames_per_call[dom] * args.steps
+    achieved = dom_flops_total / (dom_ms * 1e-3) / 1e12 if dom_ms > 0 else None
+    roofline = {"bound": "alu", "kernel": dom, "achieved": achieved, "peak": peak_alu, "unit": "TFLOP/s",
+                "frac": (achieved / peak_alu) if achieved else None, "traffic": None,
+                "avg_launch_ms": dom_ms / max(dom_n, 1), "launches": dom_n,
+                "peak_note": f"FP32 CUDA-core peak {sm_count} SMs x 128 x 2 x {sm_max:.0f} MHz (DESIGN.md)"}
+    share = {k: (v / ms_total if ms_total > 0 else None) for k, v in cls_ms.items()}
+    hbm_bytes = step_bytes(cfg, cfg.L, n_iter)
+    hbm_achieved = hbm_bytes / (ms_step * 1e-3) / 1e9
+    gpu_launches = int(sum(prof[k][1] for k in ("fwd_rows", "fwd_cols", "adj_cols", "adj_rows", "cg_vec")))
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        o = oracle_sample(cfg, n_iter, args.cpu_seconds)
+        cpu = {"value": o["value"], "unit": UNIT, "cores": o["cores"], "kind": "oracle", "sample": o["sample"],
+               "seconds": o["seconds"]}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": cfg.name, "N": cfg.N, "L": cfg.L, "M": cfg.M, "C": cfg.C, "R": cfg.R, "W": cfg.W,
+                   "sigma": cfg.sigma, "cg_iters": n_iter, "mu": cfg.mu, "parallelism": f"frames/{world}",
+                   "step": "mrf_dc_cg: 1 adjoint + (n_iter+1) normals + CG vector ops",
+                   "l2": "working set > L2 (x, r, p, q each %.0f MB); no flush" % (cfg.L * cfg.N ** 2 * 8 / 1e6),
+                   "batch_frames": args.batch_frames or "auto"},
+        "ms_per_AHA": ms_normal, "ms_per_forward": ms_fwd, "ms_per_adjoint": ms_adj,
+        "ms_per_cg_iter_est": ms_cg_iter,
+        "fwd_pts_s": cfg.L * cfg.C * cfg.M / (ms_fwd * 1e-3), "adj_pts_s": cfg.L * cfg.C * cfg.M / (ms_adj * 1e-3),
+        "hbm": {"algorithmic_bytes_per_step": hbm_bytes, "achieved_GBs": hbm_achieved, "peak_GBs": hbm_peak,
+                "frac": hbm_achieved / hbm_peak},
+        "cufft_ref_ms_fft2_LC": cufft_ms,
+        "roofline": roofline, "kernel_share": share, "gpu_launches": gpu_launches,
+        "clocks": clk, "e2e": e2e, "cpu_baseline": cpu,
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    plan.close()
+    if comm:
+        binding.nccl_comm_destroy(comm)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,146 @@
+/*
+ * mrfnufft.h -- C-ABI of the B200-native (sm_100a) data-consistency operator of MS-LLR
+ * MR fingerprinting reconstruction (Li, Ji, Hu, arxiv 2310.05647).
+ *
+ * What it computes (the "acquisition operator" of the paper):
+ *   b = A X + n,  A = F_u C                       PAPER.md:56-60 (§II-B, Eq. (1) data_ac)
+ *   X in C^{Nx x Ny x L} image frames, b in C^{Nc x Ns x L} k-space, C = coil sensitivities,
+ *   F_u = per-frame non-Cartesian (spiral) undersampled Fourier transform.
+ *   The paper evaluates F_u with a GPU NUFFT library (§III-D, §V) and
+ *   uses A* in the gradient A*(A X - b) (Eq. (15)) and in the
+ *   initialisation X^0 = A* b (Alg. 1).  BASELINE.json's north_star adds the exact
+ *   data-consistency solve (A^H A + mu I) x = A^H y + mu z by conjugate gradients.
+ *
+ * Conventions:
+ *   - image frame x_l[iy][ix] (x fastest), centred indices n = (ix - N/2, iy - N/2);
+ *   - trajectory k in cycles/pixel, |k| <= 0.5 inclusive (+0.5 == -0.5);
+ *   - A:   y[l][c][j] = (1/N) sum_n S_c[n] x_l[n] exp(-i 2 pi k_{l,j} . n)   (approximated by
+ *          Kaiser-Bessel gridding: width W, oversampling sigma = 2, Beatty beta, open support,
+ *          deapodisation by the kernel's continuous Fourier transform unless
+ *          MRF_DEAPOD_DISCRETE);
+ *   - A^H: the exact transpose of the gridding forward (conj coils, e^{+i}, same taps).
+ *   - frame l (local index) samples interleaf frame_interleaf[l], default
+ *     (frame_offset + l) mod R.
+ *
+ * Memory: every complex array is interleaved complex64 (float real, float imag), C-contiguous:
+ *   x, z, out  [L_local][N][N]     y  [L_local][C][M]     coils [C][N][N]     traj [R][M][2]
+ * Array arguments of the operator calls may be DEVICE pointers (on the plan's device; fully
+ * asynchronous on `stream`, CUDA-graph capturable, no allocation) or HOST pointers (pinned or
+ * pageable; the call stages them through plan-owned device buffers allocated on first use and
+ * returns only after the result is back in host memory).  Device and host pointers may not be
+ * mixed within one call.
+ *
+ * Errors: every call returns an mrf_status; MRF_OK == 0.  mrf_last_error() returns a
+ * thread-local human-readable message for the most recent failure.  On any error the output
+ * buffers are unspecified.
+ */
+#ifndef MRFNUFFT_H
+#define MRFNUFFT_H
+
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct mrf_plan_s* mrf_plan;          /* opaque; owns all derived device data */
+
+typedef enum {
+  MRF_OK = 0,
+  MRF_EINVAL = 1,        /* null required pointer, bad size, |k| > 0.5 or non-finite k, W out of
+                            [2,16], mu < 0, n_iter < 0, mixed host/device pointers            */
+  MRF_ENOMEM = 2,        /* device or host allocation failed                                    */
+  MRF_ECUDA = 3,         /* CUDA runtime error (message in mrf_last_error)                      */
+  MRF_ENCCL = 4,         /* NCCL unavailable or a collective failed                             */
+  MRF_EUNSUPPORTED = 5,  /* sigma != 2 or G = sigma*N not in {64,128,256,512,1024}             */
+  MRF_ENUMERIC = 6       /* CG breakdown: Re<p, (A^H A + mu I) p> <= 0 or non-finite           */
+} mrf_status;
+
+/* flags */
+#define MRF_DEAPOD_ANALYTIC 0u   /* psi = continuous FT of the KB kernel (default)               */
+#define MRF_DEAPOD_DISCRETE 1u   /* psi = DFT of the integer-sampled kernel (exact on-grid)      */
+
+typedef struct {
+  int N;                        /* square image side, even; G = sigma*N must be a supported size */
+  int L_local;                  /* frames held by this plan (this rank's shard), >= 1           */
+  int frame_offset;             /* global index of local frame 0 (default interleaf map)        */
+  int M;                        /* nonuniform points per frame, >= 1                            */
+  int R;                        /* distinct interleaves in traj, >= 1                            */
+  const float* traj;            /* HOST [R][M][2] (kx, ky) cycles/pixel; copied at create       */
+  const int* frame_interleaf;   /* HOST [L_local] in [0,R), or NULL => (frame_offset+l) mod R   */
+  int C;                        /* coils >= 1                                                    */
+  const float* coils;           /* HOST [C][N][N] complex64, or NULL with C == 1 => S = 1       */
+  int W;                        /* Kaiser-Bessel width, 2..16                                    */
+  float sigma;                  /* oversampling factor; 2.0 supported                            */
+  unsigned flags;               /* MRF_DEAPOD_*                                                  */
+  int device;                   /* CUDA device ordinal                                           */
+  void* stream;                 /* cudaStream_t for create-time uploads (NULL = legacy default)  */
+  void* nccl_comm;              /* ncclComm_t shared by all ranks of one solve, or NULL          */
+  int batch_frames;             /* frames per on-chip batch of the gridding pipeline; 0 = auto   */
+} mrf_plan_desc;
+
+/* Validates the descriptor, evaluates the KB kernel/deapodisation constants in float64 on the
+ * host, bins every interleaf's points into column strips of the oversampled grid, uploads
+ * everything and allocates all workspaces.  Caller keeps ownership of desc's host arrays. */
+mrf_status mrf_plan_create(const mrf_plan_desc* desc, mrf_plan* out);
+
+/* y = A x  (Eq. (1) without noise).  x [L][N][N], y [L][C][M]. */
+mrf_status mrf_forward(mrf_plan plan, const void* x, void* y, void* stream);
+
+/* x = A^H y  (the adjoint A* of PAPER.md:221; X^0 = A* b of Alg. 1). */
+mrf_status mrf_adjoint(mrf_plan plan, const void* y, void* x, void* stream);
+
+/* out = A^H A x + mu x  (the normal operator inside A*(A X^n - b), Eq. (15)).
+ * out must not alias x; mu >= 0. */
+mrf_status mrf_normal(mrf_plan plan, const void* x, void* out, float mu, void* stream);
+
+typedef struct {
+  int iters;               /* CG iterations performed                                           */
+  double rel_resid;        /* sqrt(rho_last / rho_0), rho = <r, r> global over all ranks        */
+  double* history;         /* nullable HOST array of length n_iter+1: history[k] = sqrt(rho_k)  */
+} mrf_cg_info;
+
+/* Solves (A^H A + mu I) x = A^H y + mu z by CG from x (in: x0, out: solution), inner products
+ * <a,b> = sum conj(a) b over ALL frames of ALL ranks, accumulated in float64 (and all-reduced
+ * with NCCL when the plan has a communicator: every rank must call with the same mu, n_iter,
+ * tol).  z may be NULL (=> 0).  tol == 0 runs exactly n_iter iterations with no host
+ * synchronisation inside the loop; tol > 0 stops once sqrt(rho_k/rho_0) < tol.  Iteration as in
+ * SURVEY.md §8(c)(ii) step 7.  The call synchronises `stream` once at the end to fill `info`
+ * and check for breakdown. */
+mrf_status mrf_dc_cg(mrf_plan plan, const void* y, const void* z, float mu, int n_iter, float tol,
+                     void* x, mrf_cg_info* info, void* stream);
+
+mrf_status mrf_plan_destroy(mrf_plan plan);
+
+const char* mrf_status_string(mrf_status status);
+const char* mrf_last_error(void);
+
+/* ---- plan introspection ---------------------------------------------------------------- */
+/* Bytes of device memory the plan owns (tables, coils, workspaces, CG vectors). */
+size_t mrf_plan_device_bytes(mrf_plan plan);
+
+/* ---- per-kernel timing (CUDA events on the launching stream) ----------------------------- */
+/* Kernel classes for mrf_profile_query. */
+#define MRF_K_FWD_ROWS      0   /* deapod . coil . pad . row FFT                                */
+#define MRF_K_FWD_COLS      1   /* column FFT + KB gather interpolation                          */
+#define MRF_K_ADJ_COLS      2   /* KB spread + column inverse FFT + row crop                     */
+#define MRF_K_ADJ_ROWS      3   /* row inverse FFT + crop + deapod + conj-coil sum               */
+#define MRF_K_CG_VEC        4   /* CG vector updates and inner products                          */
+#define MRF_K_OTHER         5   /* memsets, reductions                                            */
+#define MRF_K_COUNT         6
+/* enable != 0 brackets every subsequent kernel launch with CUDA events (and resets counters). */
+mrf_status mrf_profile_enable(mrf_plan plan, int enable);
+/* Synchronises the recorded events and returns total milliseconds and launch count of a class. */
+mrf_status mrf_profile_query(mrf_plan plan, int kernel_class, double* total_ms, long long* launches);
+
+/* ---- NCCL helpers (NCCL is loaded at run time; no link-time dependency) ------------------- */
+/* Writes the 128-byte ncclUniqueId into id_out. */
+mrf_status mrf_nccl_get_unique_id(void* id_out128);
+/* Creates an ncclComm_t on the current device; *comm_out receives it. */
+mrf_status mrf_nccl_comm_init(void** comm_out, int nranks, const void* id128, int rank, int device);
+mrf_status mrf_nccl_comm_destroy(void* comm);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MRFNUFFT_H */

@@ -1,0 +1,269 @@
+"""Thin ctypes binding over libmrfnufft.so (include/mrfnufft.h).  Argument marshalling only.
+
+Every operator step runs in the library's sm_100a kernels; there is no CPU or PyTorch fallback.
+If the shared library is missing the import fails loudly (build it with
+``python -m paper_2310_05647_b200.build`` or ``__graft_entry__.build()``).
+
+Arrays are ``torch.complex64`` tensors, C-contiguous.  CUDA tensors must live on the plan's
+device and run asynchronously on the current torch stream; CPU tensors (pinned or pageable) go
+through the library's host path (staged copies inside the call; the call returns when done).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Optional
+
+import numpy as np
+import torch
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libmrfnufft.so")
+
+MRF_DEAPOD_ANALYTIC = 0
+MRF_DEAPOD_DISCRETE = 1
+KERNEL_CLASSES = {"fwd_rows": 0, "fwd_cols": 1, "adj_cols": 2, "adj_rows": 3, "cg_vec": 4, "other": 5}
+STATUS = {0: "MRF_OK", 1: "MRF_EINVAL", 2: "MRF_ENOMEM", 3: "MRF_ECUDA", 4: "MRF_ENCCL",
+          5: "MRF_EUNSUPPORTED", 6: "MRF_ENUMERIC"}
+
+EXPORTED = [
+    "mrf_plan_create", "mrf_forward", "mrf_adjoint", "mrf_normal", "mrf_dc_cg", "mrf_plan_destroy",
+    "mrf_status_string", "mrf_last_error", "mrf_plan_device_bytes", "mrf_profile_enable",
+    "mrf_profile_query", "mrf_nccl_get_unique_id", "mrf_nccl_comm_init", "mrf_nccl_comm_destroy",
+]
+
+
+class MrfError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class PlanDesc(ctypes.Structure):
+    _fields_ = [
+        ("N", ctypes.c_int), ("L_local", ctypes.c_int), ("frame_offset", ctypes.c_int),
+        ("M", ctypes.c_int), ("R", ctypes.c_int),
+        ("traj", ctypes.c_void_p), ("frame_interleaf", ctypes.c_void_p),
+        ("C", ctypes.c_int), ("coils", ctypes.c_void_p),
+        ("W", ctypes.c_int), ("sigma", ctypes.c_float), ("flags", ctypes.c_uint),
+        ("device", ctypes.c_int), ("stream", ctypes.c_void_p), ("nccl_comm", ctypes.c_void_p),
+        ("batch_frames", ctypes.c_int),
+    ]
+
+
+class CGInfo(ctypes.Structure):
+    _fields_ = [("iters", ctypes.c_int), ("rel_resid", ctypes.c_double),
+                ("history", ctypes.POINTER(ctypes.c_double))]
+
+
+def _load() -> ctypes.CDLL:
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is not built: run `python -m paper_2310_05647_b200.build` "
+                          "(there is no CPU fallback)")
+    lib = ctypes.CDLL(LIB_PATH)
+    vp, ci, cf = ctypes.c_void_p, ctypes.c_int, ctypes.c_float
+    sig = {
+        "mrf_plan_create": ([ctypes.POINTER(PlanDesc), ctypes.POINTER(vp)], ci),
+        "mrf_forward": ([vp, vp, vp, vp], ci),
+        "mrf_adjoint": ([vp, vp, vp, vp], ci),
+        "mrf_normal": ([vp, vp, vp, cf, vp], ci),
+        "mrf_dc_cg": ([vp, vp, vp, cf, ci, cf, vp, ctypes.POINTER(CGInfo), vp], ci),
+        "mrf_plan_destroy": ([vp], ci),
+        "mrf_status_string": ([ci], ctypes.c_char_p),
+        "mrf_last_error": ([], ctypes.c_char_p),
+        "mrf_plan_device_bytes": ([vp], ctypes.c_size_t),
+        "mrf_profile_enable": ([vp, ci], ci),
+        "mrf_profile_query": ([vp, ci, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_longlong)], ci),
+        "mrf_nccl_get_unique_id": ([vp], ci),
+        "mrf_nccl_comm_init": ([ctypes.POINTER(vp), ci, vp, ci, ci], ci),
+        "mrf_nccl_comm_destroy": ([vp], ci),
+    }
+    for name, (args, res) in sig.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = res
+    return lib
+
+
+lib = _load()
+
+
+def _check(status: int):
+    if status != 0:
+        raise MrfError(status, lib.mrf_last_error().decode(errors="replace"))
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _as_c64(t, shape, name):
+    if not isinstance(t, torch.Tensor):
+        t = torch.from_numpy(np.ascontiguousarray(np.asarray(t, dtype=np.complex64)))
+    if t.dtype != torch.complex64:
+        raise TypeError(f"{name} must be complex64, got {t.dtype}")
+    if tuple(t.shape) != tuple(shape):
+        raise ValueError(f"{name} must have shape {tuple(shape)}, got {tuple(t.shape)}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    return t
+
+
+class Plan:
+    """One frame shard of the multi-frame, multi-coil KB-gridding NUFFT operator (mrf_plan)."""
+
+    def __init__(self, N: int, traj, L: int, *, coils=None, W: int = 6, sigma: float = 2.0,
+                 frame_interleaf=None, frame_offset: int = 0, deapod: str = "analytic",
+                 device: Optional[int] = None, nccl_comm: Optional[int] = None, batch_frames: int = 0):
+        traj_np = np.ascontiguousarray(np.asarray(traj, dtype=np.float32))
+        if traj_np.ndim != 3 or traj_np.shape[2] != 2:
+            raise ValueError("traj must be [R][M][2] float32")
+        self.N, self.L, self.W, self.sigma = int(N), int(L), int(W), float(sigma)
+        self.R, self.M = traj_np.shape[0], traj_np.shape[1]
+        self.frame_offset = int(frame_offset)
+        coils_np = None
+        if coils is not None:
+            coils_np = np.ascontiguousarray(np.asarray(coils, dtype=np.complex64))
+            if coils_np.ndim != 3 or coils_np.shape[1:] != (self.N, self.N):
+                raise ValueError("coils must be [C][N][N] complex64")
+        self.C = 1 if coils_np is None else coils_np.shape[0]
+        fil_np = None
+        if frame_interleaf is not None:
+            fil_np = np.ascontiguousarray(np.asarray(frame_interleaf, dtype=np.int32))
+            if fil_np.shape != (self.L,):
+                raise ValueError("frame_interleaf must have shape [L]")
+        self.device = torch.cuda.current_device() if device is None else int(device)
+        self._keep = (traj_np, coils_np, fil_np)
+        d = PlanDesc()
+        d.N, d.L_local, d.frame_offset, d.M, d.R = self.N, self.L, self.frame_offset, self.M, self.R
+        d.traj = traj_np.ctypes.data
+        d.frame_interleaf = None if fil_np is None else fil_np.ctypes.data
+        d.C = self.C
+        d.coils = None if coils_np is None else coils_np.ctypes.data
+        d.W, d.sigma = self.W, self.sigma
+        d.flags = {"analytic": MRF_DEAPOD_ANALYTIC, "discrete": MRF_DEAPOD_DISCRETE}[deapod]
+        d.device = self.device
+        d.stream = None
+        d.nccl_comm = nccl_comm
+        d.batch_frames = int(batch_frames)
+        h = ctypes.c_void_p()
+        _check(lib.mrf_plan_create(ctypes.byref(d), ctypes.byref(h)))
+        self._h = h
+
+    # ------------------------------------------------------------------ helpers
+    @property
+    def x_shape(self):
+        return (self.L, self.N, self.N)
+
+    @property
+    def y_shape(self):
+        return (self.L, self.C, self.M)
+
+    def _stream(self, *tensors):
+        if any(t is not None and t.is_cuda for t in tensors):
+            return ctypes.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)
+        return None
+
+    def _like(self, ref: torch.Tensor, shape):
+        if ref.is_cuda:
+            return torch.empty(shape, dtype=torch.complex64, device=ref.device)
+        return torch.empty(shape, dtype=torch.complex64, pin_memory=ref.is_pinned())
+
+    @property
+    def device_bytes(self) -> int:
+        return int(lib.mrf_plan_device_bytes(self._h))
+
+    # ------------------------------------------------------------------ operators
+    def forward(self, x, y=None):
+        """y = A x  (Eq. (1))."""
+        x = _as_c64(x, self.x_shape, "x")
+        y = self._like(x, self.y_shape) if y is None else _as_c64(y, self.y_shape, "y")
+        _check(lib.mrf_forward(self._h, _ptr(x), _ptr(y), self._stream(x, y)))
+        return y
+
+    def adjoint(self, y, x=None):
+        """x = A^H y  (A*)."""
+        y = _as_c64(y, self.y_shape, "y")
+        x = self._like(y, self.x_shape) if x is None else _as_c64(x, self.x_shape, "x")
+        _check(lib.mrf_adjoint(self._h, _ptr(y), _ptr(x), self._stream(x, y)))
+        return x
+
+    def normal(self, x, mu: float = 0.0, out=None):
+        """out = A^H A x + mu x  (A*(A X))."""
+        x = _as_c64(x, self.x_shape, "x")
+        out = self._like(x, self.x_shape) if out is None else _as_c64(out, self.x_shape, "out")
+        _check(lib.mrf_normal(self._h, _ptr(x), _ptr(out), ctypes.c_float(mu), self._stream(x, out)))
+        return out
+
+    def dc_cg(self, y, x0=None, z=None, mu: float = 0.01, n_iter: int = 10, tol: float = 0.0, x=None):
+        """CG solve of (A^H A + mu I) x = A^H y + mu z from x0; returns (x, info dict)."""
+        y = _as_c64(y, self.y_shape, "y")
+        if x is None:
+            x = self._like(y, self.x_shape)
+            if x0 is None:
+                x.zero_()
+            else:
+                x.copy_(_as_c64(x0, self.x_shape, "x0"))
+        else:
+            x = _as_c64(x, self.x_shape, "x")
+            if x0 is not None:
+                x.copy_(_as_c64(x0, self.x_shape, "x0"))
+        if z is not None:
+            z = _as_c64(z, self.x_shape, "z")
+        hist = (ctypes.c_double * (n_iter + 1))()
+        info = CGInfo(0, 0.0, ctypes.cast(hist, ctypes.POINTER(ctypes.c_double)))
+        _check(lib.mrf_dc_cg(self._h, _ptr(y), _ptr(z), ctypes.c_float(mu), int(n_iter), ctypes.c_float(tol),
+                             _ptr(x), ctypes.byref(info), self._stream(x, y, z)))
+        return x, {"iters": info.iters, "rel_resid": info.rel_resid, "history": list(hist)[: info.iters + 1]}
+
+    # ------------------------------------------------------------------ profiling
+    def profile(self, enable: bool = True):
+        _check(lib.mrf_profile_enable(self._h, int(bool(enable))))
+
+    def profile_query(self, cls: str):
+        ms = ctypes.c_double()
+        n = ctypes.c_longlong()
+        _check(lib.mrf_profile_query(self._h, KERNEL_CLASSES[cls], ctypes.byref(ms), ctypes.byref(n)))
+        return ms.value, n.value
+
+    # ------------------------------------------------------------------ lifetime
+    def close(self):
+        if getattr(self, "_h", None):
+            _check(lib.mrf_plan_destroy(self._h))
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+
+# ---------------------------------------------------------------------- NCCL communicator
+def nccl_comm_create(rank: int, world: int, device: int):
+    """ncclComm_t for the CG inner-product all-reduce; the 128-byte id is broadcast over the
+    default torch.distributed process group (any backend)."""
+    import torch.distributed as dist
+    buf = (ctypes.c_ubyte * 128)()
+    if rank == 0:
+        _check(lib.mrf_nccl_get_unique_id(ctypes.cast(buf, ctypes.c_void_p)))
+    t = torch.tensor(list(bytes(buf)), dtype=torch.uint8)
+    if dist.get_backend() == "nccl":
+        t = t.cuda(device)
+    dist.broadcast(t, 0)
+    idb = bytes(t.cpu().tolist())
+    ctypes.memmove(buf, idb, 128)
+    comm = ctypes.c_void_p()
+    _check(lib.mrf_nccl_comm_init(ctypes.byref(comm), int(world), ctypes.cast(buf, ctypes.c_void_p), int(rank),
+                                  int(device)))
+    return comm.value
+
+
+def nccl_comm_destroy(comm):
+    if comm:
+        _check(lib.mrf_nccl_comm_destroy(ctypes.c_void_p(comm)))

@@ -1,0 +1,157 @@
+// fft.cuh -- register-resident DFT building blocks for the hand-written G x G FFTs (sm_100a).
+//
+// The 2D DFT of the oversampled grid (the paper's F_u,
+// PAPER.md:60) is evaluated as row and column passes of length-G 1D DFTs.  Each length-G DFT is
+// a two-stage Cooley-Tukey split G = P * Q executed by T cooperating threads of one warp:
+//
+//   n = Q n1 + n2,  k = k1 + P k2
+//   X[k1 + P k2] = sum_{n2} W_Q^{n2 k2} . W_G^{n2 k1} . sum_{n1} x[Q n1 + n2] W_P^{n1 k1}
+//
+// stage 1: thread t owns n2 in {t + T a}: a P-point DFT per n2 in registers, times W_G^{n2 k1};
+// one exchange through shared memory; stage 2: thread t owns k1 in {t + T b}: a Q-point DFT per
+// k1 in registers.  The P-/Q-point DFTs are unrolled at compile time (radix-4 / radix-2
+// decimation in time) with constant twiddles evaluated by constexpr Taylor series in double.
+#pragma once
+#include <cuda_runtime.h>
+
+namespace mrf {
+
+__host__ __device__ constexpr double c_pi() { return 3.14159265358979323846; }
+
+// constexpr cos / sin for |t| <= pi (alternating Taylor series, 40 terms: < 1e-16 abs error).
+__host__ __device__ constexpr double c_cos(double t) {
+  double term = 1.0, sum = 1.0;
+  for (int i = 1; i < 40; ++i) { term *= -t * t / ((2.0 * i - 1.0) * (2.0 * i)); sum += term; }
+  return sum;
+}
+__host__ __device__ constexpr double c_sin(double t) {
+  double term = t, sum = t;
+  for (int i = 1; i < 40; ++i) { term *= -t * t / ((2.0 * i) * (2.0 * i + 1.0)); sum += term; }
+  return sum;
+}
+
+// W_R^K = exp(SIGN * i * 2 pi K / R), K reduced to (-R/2, R/2].
+template <int R, int K, int SIGN>
+struct Tw {
+  static constexpr int Kr = (K % R) > R / 2 ? (K % R) - R : (K % R);
+  static constexpr double ang = SIGN * 2.0 * c_pi() * double(Kr) / double(R);
+  static constexpr float c = float(c_cos(ang));
+  static constexpr float s = float(c_sin(ang));
+};
+
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ float2 cmul(float2 a, float2 b) {
+  return make_float2(fmaf(a.x, b.x, -a.y * b.y), fmaf(a.x, b.y, a.y * b.x));
+}
+__device__ __forceinline__ float2 cmulc(float2 a, float2 b) {   // a * conj(b)
+  return make_float2(fmaf(a.x, b.x, a.y * b.y), fmaf(a.y, b.x, -a.x * b.y));
+}
+__device__ __forceinline__ float2 cscale(float2 a, float s) { return make_float2(a.x * s, a.y * s); }
+// multiply by SIGN * i
+template <int SIGN>
+__device__ __forceinline__ float2 mul_i(float2 a) {
+  return SIGN > 0 ? make_float2(-a.y, a.x) : make_float2(a.y, -a.x);
+}
+
+// a * W_R^K with the trivial angles special-cased.
+template <int R, int K, int SIGN>
+__device__ __forceinline__ float2 twmul(float2 a) {
+  constexpr int k = ((K % R) + R) % R;
+  if constexpr (k == 0) {
+    return a;
+  } else if constexpr (4 * k == R) {
+    return mul_i<SIGN>(a);
+  } else if constexpr (2 * k == R) {
+    return make_float2(-a.x, -a.y);
+  } else if constexpr (4 * k == 3 * R) {
+    return mul_i<-SIGN>(a);
+  } else {
+    constexpr float c = Tw<R, K, SIGN>::c, s = Tw<R, K, SIGN>::s;
+    return make_float2(fmaf(a.x, c, -a.y * s), fmaf(a.x, s, a.y * c));
+  }
+}
+
+template <int R, int SIGN>
+__device__ __forceinline__ void dft(float2 (&v)[R]);
+
+namespace detail {
+// radix-4 DIT combine: X[k + m R/4] = sum_q W_R^{qk} W_4^{qm} D_q[k]
+template <int R, int SIGN, int K>
+__device__ __forceinline__ void r4_combine(float2 (&v)[R], const float2 (&d0)[R / 4], const float2 (&d1)[R / 4],
+                                           const float2 (&d2)[R / 4], const float2 (&d3)[R / 4]) {
+  if constexpr (K < R / 4) {
+    const float2 a0 = d0[K];
+    const float2 a1 = twmul<R, K, SIGN>(d1[K]);
+    const float2 a2 = twmul<R, 2 * K, SIGN>(d2[K]);
+    const float2 a3 = twmul<R, 3 * K, SIGN>(d3[K]);
+    const float2 s02 = cadd(a0, a2), d02 = csub(a0, a2);
+    const float2 s13 = cadd(a1, a3), d13 = mul_i<SIGN>(csub(a1, a3));
+    v[K] = cadd(s02, s13);
+    v[K + R / 2] = csub(s02, s13);
+    v[K + R / 4] = cadd(d02, d13);
+    v[K + 3 * R / 4] = csub(d02, d13);
+    r4_combine<R, SIGN, K + 1>(v, d0, d1, d2, d3);
+  }
+}
+template <int R, int SIGN, int K>
+__device__ __forceinline__ void r2_combine(float2 (&v)[R], const float2 (&e)[R / 2], const float2 (&o)[R / 2]) {
+  if constexpr (K < R / 2) {
+    const float2 t = twmul<R, K, SIGN>(o[K]);
+    v[K] = cadd(e[K], t);
+    v[K + R / 2] = csub(e[K], t);
+    r2_combine<R, SIGN, K + 1>(v, e, o);
+  }
+}
+}  // namespace detail
+
+// In-place R-point DFT, natural order in and out: v[k] <- sum_n v[n] exp(SIGN i 2 pi n k / R).
+template <int R, int SIGN>
+__device__ __forceinline__ void dft(float2 (&v)[R]) {
+  if constexpr (R == 1) {
+    return;
+  } else if constexpr (R == 2) {
+    const float2 a = v[0], b = v[1];
+    v[0] = cadd(a, b);
+    v[1] = csub(a, b);
+  } else if constexpr (R == 4) {
+    const float2 s02 = cadd(v[0], v[2]), d02 = csub(v[0], v[2]);
+    const float2 s13 = cadd(v[1], v[3]), d13 = mul_i<SIGN>(csub(v[1], v[3]));
+    v[0] = cadd(s02, s13);
+    v[2] = csub(s02, s13);
+    v[1] = cadd(d02, d13);
+    v[3] = csub(d02, d13);
+  } else if constexpr (R == 8) {
+    float2 e[4], o[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) { e[i] = v[2 * i]; o[i] = v[2 * i + 1]; }
+    dft<4, SIGN>(e);
+    dft<4, SIGN>(o);
+    detail::r2_combine<8, SIGN, 0>(v, e, o);
+  } else {
+    static_assert(R % 4 == 0, "R must be a power of two");
+    float2 d0[R / 4], d1[R / 4], d2[R / 4], d3[R / 4];
+#pragma unroll
+    for (int i = 0; i < R / 4; ++i) {
+      d0[i] = v[4 * i];
+      d1[i] = v[4 * i + 1];
+      d2[i] = v[4 * i + 2];
+      d3[i] = v[4 * i + 3];
+    }
+    dft<R / 4, SIGN>(d0);
+    dft<R / 4, SIGN>(d1);
+    dft<R / 4, SIGN>(d2);
+    dft<R / 4, SIGN>(d3);
+    detail::r4_combine<R, SIGN, 0>(v, d0, d1, d2, d3);
+  }
+}
+
+// Two-stage split of the supported grid sizes.  T threads (within one warp) per length-G DFT.
+template <int G> struct FFTShape;
+template <> struct FFTShape<64>   { static constexpr int P = 8,  Q = 8,  T = 8;  };
+template <> struct FFTShape<128>  { static constexpr int P = 8,  Q = 16, T = 8;  };
+template <> struct FFTShape<256>  { static constexpr int P = 16, Q = 16, T = 16; };
+template <> struct FFTShape<512>  { static constexpr int P = 16, Q = 32, T = 16; };
+template <> struct FFTShape<1024> { static constexpr int P = 32, Q = 32, T = 32; };
+
+}  // namespace mrf

@@ -1,0 +1,787 @@
+// mrfnufft.cu -- the C-ABI (include/mrfnufft.h): plan creation, operator drivers, CG solve.
+//
+// Plan creation runs once on the host in float64: Kaiser-Bessel
+// constants, deapodisation, twiddles, per-point taps and weights, and the bin-sort of every
+// interleaf's points into 16-column strips of the oversampled grid.  The operator drivers only
+// launch kernels on the caller's stream (no allocation, no host synchronisation), so forward /
+// adjoint / normal / dc_cg(tol = 0) are CUDA-graph capturable.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/mrfnufft.h"
+#include "kernels.cuh"
+#include "nccl_dl.h"
+
+using namespace mrf;
+
+// ================================================================================== errors
+static thread_local std::string g_err;
+
+static mrf_status fail(mrf_status s, const std::string& msg) {
+  g_err = msg;
+  return s;
+}
+
+#define CUDA_TRY(expr)                                                                           \
+  do {                                                                                           \
+    cudaError_t _e = (expr);                                                                     \
+    if (_e != cudaSuccess) {                                                                     \
+      return fail(MRF_ECUDA, std::string(#expr) + ": " + cudaGetErrorString(_e));               \
+    }                                                                                            \
+  } while (0)
+
+#define MRF_TRY(expr)                                                                            \
+  do {                                                                                           \
+    mrf_status _s = (expr);                                                                      \
+    if (_s != MRF_OK) return _s;                                                                 \
+  } while (0)
+
+// ================================================================================== plan
+namespace {
+
+struct Prof {
+  bool on = false;
+  std::vector<cudaEvent_t> ev[MRF_K_COUNT];   // start/stop pairs
+  size_t used[MRF_K_COUNT] = {0};
+  long long launches[MRF_K_COUNT] = {0};
+};
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+}  // namespace
+
+struct mrf_plan_s {
+  // sizes
+  int N = 0, G = 0, L = 0, M = 0, R = 0, C = 1, W = 0, S = 0, frame_offset = 0;
+  unsigned flags = 0;
+  int device = 0;
+  int bf = 1;               // frames per batch
+  void* nccl_comm = nullptr;
+  // device tables
+  float2* coils = nullptr;
+  float* dap = nullptr;
+  float2* tw = nullptr;
+  float* wts = nullptr;
+  int2* ent = nullptr;
+  int* soff = nullptr;
+  int* fil = nullptr;
+  // workspaces
+  float2* H = nullptr;       // [bf*C][N][G] half grid
+  float2* ybuf = nullptr;    // [bf*C][M]
+  float2* r = nullptr;       // CG vectors [L][N][N]
+  float2* p = nullptr;
+  float2* q = nullptr;
+  double2* part = nullptr;   // [kPartBlocks]
+  CGScalars* sc = nullptr;
+  double* hist = nullptr;    // device [hist_cap]
+  int hist_cap = 0;
+  // host staging (allocated on first host-pointer call)
+  float2* stg_x = nullptr;
+  float2* stg_y = nullptr;
+  float2* stg_z = nullptr;
+  size_t bytes = 0;
+  Prof prof;
+  DevPlan dp() const {
+    DevPlan d;
+    d.N = N; d.G = G; d.M = M; d.R = R; d.C = C; d.W = W; d.S = S;
+    d.coils = coils; d.dap = dap; d.tw = tw; d.wts = wts; d.ent = ent; d.soff = soff; d.fil = fil;
+    return d;
+  }
+};
+
+static constexpr int kPartBlocks = 4 * 148;
+
+// ---------------------------------------------------------------------------- host math (fp64)
+// I0 by its power series sum_k (x^2/4)^k / (k!)^2 (converges for all x; x <= ~40 here).
+static double bessel_i0(double x) {
+  const double q = 0.25 * x * x;
+  double term = 1.0, sum = 1.0;
+  for (int k = 1; k < 500; ++k) {
+    term *= q / ((double)k * (double)k);
+    sum += term;
+    if (term < 1e-17 * sum) break;
+  }
+  return sum;
+}
+
+struct KB {
+  int W;
+  double beta, i0b;
+  KB(int W_, double sigma) : W(W_) {
+    beta = M_PI * std::sqrt((W / sigma) * (W / sigma) * (sigma - 0.5) * (sigma - 0.5) - 0.8);
+    i0b = bessel_i0(beta);
+  }
+  double phi(double u) const {   // open support |u| < W/2, phi(0) = 1
+    if (!(std::fabs(u) < 0.5 * W)) return 0.0;
+    const double t = 1.0 - (2.0 * u / W) * (2.0 * u / W);
+    return bessel_i0(beta * std::sqrt(t)) / i0b;
+  }
+  double psi_analytic(double n, int G) const {
+    const double a = M_PI * W * n / G;
+    const double rad = beta * beta - a * a;
+    double f;
+    if (rad > 0) {
+      const double z = std::sqrt(rad);
+      f = std::sinh(z) / z;
+    } else if (rad < 0) {
+      const double z = std::sqrt(-rad);
+      f = std::sin(z) / z;
+    } else {
+      f = 1.0;
+    }
+    return W * f / i0b;
+  }
+  double psi_discrete(double n, int G) const {
+    double s = 0.0;
+    const int dmax = (W + 1) / 2;
+    for (int d = -dmax; d <= dmax; ++d) s += phi((double)d) * std::cos(2.0 * M_PI * d * n / G);
+    return s;
+  }
+};
+
+static void fft_shape(int G, int* P, int* Q) {
+  switch (G) {
+    case 64: *P = FFTShape<64>::P; *Q = FFTShape<64>::Q; break;
+    case 128: *P = FFTShape<128>::P; *Q = FFTShape<128>::Q; break;
+    case 256: *P = FFTShape<256>::P; *Q = FFTShape<256>::Q; break;
+    case 512: *P = FFTShape<512>::P; *Q = FFTShape<512>::Q; break;
+    default: *P = FFTShape<1024>::P; *Q = FFTShape<1024>::Q; break;
+  }
+}
+
+template <typename T>
+static mrf_status dev_alloc(mrf_plan_s* pl, T** ptr, size_t count) {
+  if (count == 0) count = 1;
+  cudaError_t e = cudaMalloc((void**)ptr, count * sizeof(T));
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(MRF_ENOMEM, std::string("cudaMalloc failed: ") + cudaGetErrorString(e));
+  }
+  pl->bytes += count * sizeof(T);
+  return MRF_OK;
+}
+
+static void free_plan(mrf_plan_s* pl) {
+  if (!pl) return;
+  void* ptrs[] = {pl->coils, pl->dap, pl->tw, pl->wts, pl->ent, pl->soff, pl->fil, pl->H, pl->ybuf,
+                  pl->r, pl->p, pl->q, pl->part, pl->sc, pl->hist, pl->stg_x, pl->stg_y, pl->stg_z};
+  for (void* v : ptrs)
+    if (v) cudaFree(v);
+  for (int k = 0; k < MRF_K_COUNT; ++k)
+    for (cudaEvent_t e : pl->prof.ev[k]) cudaEventDestroy(e);
+  delete pl;
+}
+
+// ================================================================================== launches
+static constexpr size_t kProfCap = 1 << 15;
+
+struct ProfScope {
+  mrf_plan_s* pl;
+  int cls;
+  cudaStream_t st;
+  bool rec = false;
+  size_t slot = 0;
+  ProfScope(mrf_plan_s* p, int c, cudaStream_t s) : pl(p), cls(c), st(s) {
+    if (!pl->prof.on) return;
+    pl->prof.launches[cls]++;
+    Prof& pr = pl->prof;
+    if (pr.used[cls] + 2 > kProfCap) return;
+    while (pr.ev[cls].size() < pr.used[cls] + 2) {
+      cudaEvent_t e;
+      if (cudaEventCreate(&e) != cudaSuccess) return;
+      pr.ev[cls].push_back(e);
+    }
+    slot = pr.used[cls];
+    pr.used[cls] += 2;
+    cudaEventRecord(pr.ev[cls][slot], st);
+    rec = true;
+  }
+  ~ProfScope() {
+    if (rec) cudaEventRecord(pl->prof.ev[cls][slot + 1], st);
+  }
+};
+
+template <int G>
+static mrf_status set_smem_attrs() {
+  static bool done = false;
+  if (done) return MRF_OK;
+  CUDA_TRY(cudaFuncSetAttribute(k_fwd_rows<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rows_smem<G>()));
+  CUDA_TRY(cudaFuncSetAttribute(k_adj_rows<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rows_smem<G>()));
+  CUDA_TRY(cudaFuncSetAttribute(k_fwd_cols<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cols_smem<G>()));
+  CUDA_TRY(cudaFuncSetAttribute(k_adj_cols<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cols_smem<G>()));
+  done = true;
+  return MRF_OK;
+}
+
+static mrf_status check_launch(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(MRF_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+  return MRF_OK;
+}
+
+template <int G>
+static mrf_status launch_fwd_rows(mrf_plan_s* pl, const float2* x, float2* H, int l0, int nb, cudaStream_t st) {
+  constexpr int RPC = 256 / FFTShape<G>::T;
+  ProfScope ps(pl, MRF_K_FWD_ROWS, st);
+  k_fwd_rows<G><<<dim3(pl->N / RPC, nb), 256, rows_smem<G>(), st>>>(pl->dp(), x, H, l0);
+  return check_launch("k_fwd_rows");
+}
+template <int G>
+static mrf_status launch_fwd_cols(mrf_plan_s* pl, const float2* H, float2* y, int l0, int nb, cudaStream_t st) {
+  ProfScope ps(pl, MRF_K_FWD_COLS, st);
+  k_fwd_cols<G><<<dim3(pl->S, nb * pl->C), cols_threads<G>(), cols_smem<G>(), st>>>(pl->dp(), H, y, l0);
+  return check_launch("k_fwd_cols");
+}
+template <int G>
+static mrf_status launch_adj_cols(mrf_plan_s* pl, const float2* y, float2* H, int l0, int nb, cudaStream_t st) {
+  ProfScope ps(pl, MRF_K_ADJ_COLS, st);
+  k_adj_cols<G><<<dim3(pl->S, nb * pl->C), cols_threads<G>(), cols_smem<G>(), st>>>(pl->dp(), y, H, l0);
+  return check_launch("k_adj_cols");
+}
+template <int G>
+static mrf_status launch_adj_rows(mrf_plan_s* pl, const float2* H, float2* out, const float2* xin, float mu, int l0,
+                                  int nb, cudaStream_t st) {
+  constexpr int RPC = 256 / FFTShape<G>::T;
+  ProfScope ps(pl, MRF_K_ADJ_ROWS, st);
+  k_adj_rows<G><<<dim3(pl->N / RPC, nb), 256, rows_smem<G>(), st>>>(pl->dp(), H, out, xin, mu, l0);
+  return check_launch("k_adj_rows");
+}
+
+static mrf_status memset_async(mrf_plan_s* pl, void* ptr, size_t bytes, cudaStream_t st) {
+  ProfScope ps(pl, MRF_K_OTHER, st);
+  CUDA_TRY(cudaMemsetAsync(ptr, 0, bytes, st));
+  return MRF_OK;
+}
+
+// ---------------------------------------------------------------------------- operator drivers
+template <int G>
+static mrf_status run_forward(mrf_plan_s* pl, const float2* x, float2* y, cudaStream_t st) {
+  MRF_TRY(set_smem_attrs<G>());
+  MRF_TRY(memset_async(pl, y, (size_t)pl->L * pl->C * pl->M * sizeof(float2), st));
+  for (int l0 = 0; l0 < pl->L; l0 += pl->bf) {
+    const int nb = std::min(pl->bf, pl->L - l0);
+    MRF_TRY(launch_fwd_rows<G>(pl, x, pl->H, l0, nb, st));
+    MRF_TRY(launch_fwd_cols<G>(pl, pl->H, y + (size_t)l0 * pl->C * pl->M, l0, nb, st));
+  }
+  return MRF_OK;
+}
+
+template <int G>
+static mrf_status run_adjoint(mrf_plan_s* pl, const float2* y, float2* x, cudaStream_t st) {
+  MRF_TRY(set_smem_attrs<G>());
+  for (int l0 = 0; l0 < pl->L; l0 += pl->bf) {
+    const int nb = std::min(pl->bf, pl->L - l0);
+    MRF_TRY(launch_adj_cols<G>(pl, y + (size_t)l0 * pl->C * pl->M, pl->H, l0, nb, st));
+    MRF_TRY(launch_adj_rows<G>(pl, pl->H, x, nullptr, 0.f, l0, nb, st));
+  }
+  return MRF_OK;
+}
+
+template <int G>
+static mrf_status run_normal(mrf_plan_s* pl, const float2* x, float2* out, float mu, cudaStream_t st) {
+  MRF_TRY(set_smem_attrs<G>());
+  for (int l0 = 0; l0 < pl->L; l0 += pl->bf) {
+    const int nb = std::min(pl->bf, pl->L - l0);
+    MRF_TRY(launch_fwd_rows<G>(pl, x, pl->H, l0, nb, st));
+    MRF_TRY(memset_async(pl, pl->ybuf, (size_t)nb * pl->C * pl->M * sizeof(float2), st));
+    MRF_TRY(launch_fwd_cols<G>(pl, pl->H, pl->ybuf, l0, nb, st));
+    MRF_TRY(launch_adj_cols<G>(pl, pl->ybuf, pl->H, l0, nb, st));
+    MRF_TRY(launch_adj_rows<G>(pl, pl->H, out, mu != 0.f ? x : nullptr, mu, l0, nb, st));
+  }
+  return MRF_OK;
+}
+
+#define DISPATCH_G(pl, fn, ...)                               \
+  switch ((pl)->G) {                                          \
+    case 64: return fn<64>(__VA_ARGS__);                      \
+    case 128: return fn<128>(__VA_ARGS__);                    \
+    case 256: return fn<256>(__VA_ARGS__);                    \
+    case 512: return fn<512>(__VA_ARGS__);                    \
+    case 1024: return fn<1024>(__VA_ARGS__);                  \
+    default: return fail(MRF_EUNSUPPORTED, "unsupported G");  \
+  }
+
+static mrf_status do_forward(mrf_plan_s* pl, const float2* x, float2* y, cudaStream_t st) {
+  DISPATCH_G(pl, run_forward, pl, x, y, st);
+}
+static mrf_status do_adjoint(mrf_plan_s* pl, const float2* y, float2* x, cudaStream_t st) {
+  DISPATCH_G(pl, run_adjoint, pl, y, x, st);
+}
+static mrf_status do_normal(mrf_plan_s* pl, const float2* x, float2* out, float mu, cudaStream_t st) {
+  DISPATCH_G(pl, run_normal, pl, x, out, mu, st);
+}
+
+// ---------------------------------------------------------------------------- CG (device scalars)
+static int vec_blocks(size_t n) {
+  const size_t b = (n + kVecThreads - 1) / kVecThreads;
+  return (int)std::max<size_t>(1, std::min<size_t>(b, kPartBlocks));
+}
+
+static mrf_status allreduce2(mrf_plan_s* pl, double2* v, cudaStream_t st) {
+  if (!pl->nccl_comm) return MRF_OK;
+  const char* why = nullptr;
+  const NcclApi* api = nccl_api(&why);
+  if (!api) return fail(MRF_ENCCL, why);
+  ProfScope ps(pl, MRF_K_OTHER, st);
+  int rc = api->AllReduce(v, v, 2, kNcclFloat64, kNcclSum, pl->nccl_comm, st);
+  if (rc != 0) return fail(MRF_ENCCL, std::string("ncclAllReduce: ") + api->GetErrorString(rc));
+  return MRF_OK;
+}
+
+static mrf_status reduce_to(mrf_plan_s* pl, int nblk, double2* dst, cudaStream_t st) {
+  ProfScope ps(pl, MRF_K_CG_VEC, st);
+  k_reduce<<<1, kVecThreads, 0, st>>>(pl->part, nblk, dst);
+  MRF_TRY(check_launch("k_reduce"));
+  return MRF_OK;
+}
+
+static mrf_status run_cg(mrf_plan_s* pl, const float2* y, const float2* z, float mu, int n_iter, float tol,
+                         float2* x, mrf_cg_info* info, cudaStream_t st) {
+  const size_t n = (size_t)pl->L * pl->N * pl->N;
+  const int nblk = vec_blocks(n);
+  if (n_iter + 1 > pl->hist_cap) {
+    if (pl->hist) cudaFree(pl->hist);
+    pl->hist = nullptr;
+    pl->hist_cap = 0;
+    MRF_TRY(dev_alloc(pl, &pl->hist, (size_t)n_iter + 1));
+    pl->hist_cap = n_iter + 1;
+  }
+  // rhs = A^H y + mu z  -> r
+  MRF_TRY(do_adjoint(pl, y, pl->r, st));
+  if (z && mu != 0.f) {
+    ProfScope ps(pl, MRF_K_CG_VEC, st);
+    k_axpy<<<nblk, kVecThreads, 0, st>>>(pl->r, z, mu, n);
+    MRF_TRY(check_launch("k_axpy"));
+  }
+  // r = rhs - H x0 ; p = r ; rho0
+  MRF_TRY(do_normal(pl, x, pl->q, mu, st));
+  {
+    ProfScope ps(pl, MRF_K_CG_VEC, st);
+    k_cg_init<<<nblk, kVecThreads, 0, st>>>(pl->r, pl->q, pl->r, pl->p, n, pl->part);
+    MRF_TRY(check_launch("k_cg_init"));
+  }
+  MRF_TRY(reduce_to(pl, nblk, &pl->sc->rr, st));
+  MRF_TRY(allreduce2(pl, &pl->sc->rr, st));
+  {
+    ProfScope ps(pl, MRF_K_CG_VEC, st);
+    k_cg_start<<<1, 1, 0, st>>>(pl->sc, pl->hist);
+    MRF_TRY(check_launch("k_cg_start"));
+  }
+  double rho0 = -1.0;
+  if (tol > 0.f) {
+    CUDA_TRY(cudaMemcpyAsync(&rho0, &pl->sc->rho0, sizeof(double), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+  }
+  int iters_done = n_iter;
+  for (int k = 0; k < n_iter; ++k) {
+    if (tol > 0.f && rho0 == 0.0) { iters_done = 0; break; }
+    MRF_TRY(do_normal(pl, pl->p, pl->q, mu, st));
+    {
+      ProfScope ps(pl, MRF_K_CG_VEC, st);
+      k_dot<<<nblk, kVecThreads, 0, st>>>(pl->p, pl->q, n, pl->part);
+      MRF_TRY(check_launch("k_dot"));
+    }
+    MRF_TRY(reduce_to(pl, nblk, &pl->sc->pq, st));
+    MRF_TRY(allreduce2(pl, &pl->sc->pq, st));
+    {
+      ProfScope ps(pl, MRF_K_CG_VEC, st);
+      k_cg_alpha<<<1, 1, 0, st>>>(pl->sc);
+    }
+    {
+      ProfScope ps(pl, MRF_K_CG_VEC, st);
+      k_cg_xr<<<nblk, kVecThreads, 0, st>>>(x, pl->r, pl->p, pl->q, n, pl->sc, pl->part);
+      MRF_TRY(check_launch("k_cg_xr"));
+    }
+    MRF_TRY(reduce_to(pl, nblk, &pl->sc->rr, st));
+    MRF_TRY(allreduce2(pl, &pl->sc->rr, st));
+    {
+      ProfScope ps(pl, MRF_K_CG_VEC, st);
+      k_cg_beta<<<1, 1, 0, st>>>(pl->sc, pl->hist, k);
+      MRF_TRY(check_launch("k_cg_beta"));
+    }
+    if (tol > 0.f) {
+      double rho = 0.0;
+      CUDA_TRY(cudaMemcpyAsync(&rho, &pl->sc->rho, sizeof(double), cudaMemcpyDeviceToHost, st));
+      CUDA_TRY(cudaStreamSynchronize(st));
+      if (std::sqrt(rho / rho0) < (double)tol) { iters_done = k + 1; break; }
+    }
+    if (k + 1 < n_iter) {
+      ProfScope ps(pl, MRF_K_CG_VEC, st);
+      k_cg_p<<<nblk, kVecThreads, 0, st>>>(pl->p, pl->r, n, pl->sc);
+      MRF_TRY(check_launch("k_cg_p"));
+    }
+  }
+  CGScalars hs;
+  CUDA_TRY(cudaMemcpyAsync(&hs, pl->sc, sizeof(CGScalars), cudaMemcpyDeviceToHost, st));
+  std::vector<double> hh((size_t)n_iter + 1, 0.0);
+  CUDA_TRY(cudaMemcpyAsync(hh.data(), pl->hist, sizeof(double) * (n_iter + 1), cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  if (hs.rho0 == 0.0) iters_done = 0;
+  if (info) {
+    info->iters = iters_done;
+    info->rel_resid = hs.rho0 > 0.0 ? std::sqrt(hs.rho / hs.rho0) : 0.0;
+    if (info->history) {
+      for (int i = 0; i <= n_iter; ++i) info->history[i] = i <= iters_done ? hh[i] : 0.0;
+    }
+  }
+  if (hs.breakdown) return fail(MRF_ENUMERIC, "CG breakdown: Re<p, (A^H A + mu I) p> <= 0 or non-finite");
+  return MRF_OK;
+}
+
+// ================================================================================== pointers
+// 0 = device memory of the plan's device, 1 = host memory, -1 = other device / invalid
+static int ptr_kind(const void* ptr, int dev) {
+  cudaPointerAttributes at;
+  cudaError_t e = cudaPointerGetAttributes(&at, ptr);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return 1;
+  }
+  if (at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged) return at.device == dev ? 0 : -1;
+  return 1;
+}
+
+static mrf_status classify(mrf_plan_s* pl, std::initializer_list<const void*> ptrs, bool* host) {
+  int kind = -2;
+  for (const void* v : ptrs) {
+    if (!v) continue;
+    const int k = ptr_kind(v, pl->device);
+    if (k < 0) return fail(MRF_EINVAL, "pointer is device memory of another device");
+    if (kind == -2) kind = k;
+    else if (kind != k) return fail(MRF_EINVAL, "host and device pointers mixed in one call");
+  }
+  *host = kind == 1;
+  return MRF_OK;
+}
+
+static mrf_status ensure_staging(mrf_plan_s* pl, bool need_z) {
+  const size_t nx = (size_t)pl->L * pl->N * pl->N, ny = (size_t)pl->L * pl->C * pl->M;
+  if (!pl->stg_x) MRF_TRY(dev_alloc(pl, &pl->stg_x, nx));
+  if (!pl->stg_y) MRF_TRY(dev_alloc(pl, &pl->stg_y, std::max(ny, nx)));   // also 2nd image buffer
+  if (need_z && !pl->stg_z) MRF_TRY(dev_alloc(pl, &pl->stg_z, nx));
+  return MRF_OK;
+}
+
+// ================================================================================== C-ABI
+extern "C" {
+
+const char* mrf_status_string(mrf_status s) {
+  switch (s) {
+    case MRF_OK: return "MRF_OK";
+    case MRF_EINVAL: return "MRF_EINVAL: invalid argument";
+    case MRF_ENOMEM: return "MRF_ENOMEM: out of memory";
+    case MRF_ECUDA: return "MRF_ECUDA: CUDA error";
+    case MRF_ENCCL: return "MRF_ENCCL: NCCL error";
+    case MRF_EUNSUPPORTED: return "MRF_EUNSUPPORTED: unsupported configuration";
+    case MRF_ENUMERIC: return "MRF_ENUMERIC: numerical breakdown";
+  }
+  return "unknown mrf_status";
+}
+
+const char* mrf_last_error(void) { return g_err.c_str(); }
+
+mrf_status mrf_plan_create(const mrf_plan_desc* d, mrf_plan* out) {
+  if (!d || !out) return fail(MRF_EINVAL, "null desc or out");
+  *out = nullptr;
+  if (d->N < 8 || (d->N % 2) != 0) return fail(MRF_EINVAL, "N must be even and >= 8");
+  if (d->L_local < 1 || d->M < 1 || d->R < 1 || d->C < 1) return fail(MRF_EINVAL, "L_local, M, R, C must be >= 1");
+  if (d->frame_offset < 0) return fail(MRF_EINVAL, "frame_offset < 0");
+  if (!d->traj) return fail(MRF_EINVAL, "null traj");
+  if (d->C > 1 && !d->coils) return fail(MRF_EINVAL, "C > 1 requires coils");
+  if (d->W < 2 || d->W > 16) return fail(MRF_EINVAL, "W must be in [2, 16]");
+  if (!(d->sigma > 0.f) || !std::isfinite(d->sigma)) return fail(MRF_EINVAL, "sigma must be positive");
+  if (d->batch_frames < 0) return fail(MRF_EINVAL, "batch_frames < 0");
+  if (d->flags & ~1u) return fail(MRF_EINVAL, "unknown flags");
+  if ((double)d->sigma != 2.0) return fail(MRF_EUNSUPPORTED, "only sigma = 2 is supported");
+  const double Gd = (double)d->sigma * d->N;
+  const int G = (int)std::lround(Gd);
+  if (std::fabs(Gd - G) > 1e-9 || !(G == 64 || G == 128 || G == 256 || G == 512 || G == 1024))
+    return fail(MRF_EUNSUPPORTED, "G = sigma*N must be one of 64, 128, 256, 512, 1024");
+  const int N = d->N, M = d->M, R = d->R, W = d->W, C = d->C, L = d->L_local;
+  // trajectory checks
+  for (size_t i = 0; i < (size_t)R * M * 2; ++i) {
+    const float v = d->traj[i];
+    if (!std::isfinite(v) || std::fabs(v) > 0.5f) return fail(MRF_EINVAL, "trajectory entry non-finite or |k| > 0.5");
+  }
+  std::vector<int> fil(L);
+  for (int l = 0; l < L; ++l) {
+    fil[l] = d->frame_interleaf ? d->frame_interleaf[l] : (int)(((long long)d->frame_offset + l) % R);
+    if (fil[l] < 0 || fil[l] >= R) return fail(MRF_EINVAL, "frame_interleaf entry out of [0, R)");
+  }
+  int ndev = 0;
+  CUDA_TRY(cudaGetDeviceCount(&ndev));
+  if (d->device < 0 || d->device >= ndev) return fail(MRF_EINVAL, "bad device ordinal");
+  DeviceGuard guard(d->device);
+  cudaStream_t st = (cudaStream_t)d->stream;
+
+  mrf_plan_s* pl = new mrf_plan_s();
+  pl->N = N; pl->G = G; pl->L = L; pl->M = M; pl->R = R; pl->C = C; pl->W = W; pl->S = G / SW;
+  pl->frame_offset = d->frame_offset;
+  pl->flags = d->flags;
+  pl->device = d->device;
+  pl->nccl_comm = d->nccl_comm;
+  auto bail = [&](mrf_status s) { free_plan(pl); return s; };
+
+  // ---- constants (float64 host) ------------------------------------------------------------
+  const KB kb(W, d->sigma);
+  std::vector<float> dap(N);
+  for (int i = 0; i < N; ++i) {
+    const double n = (double)(i - N / 2);
+    const double psi = (d->flags & MRF_DEAPOD_DISCRETE) ? kb.psi_discrete(n, G) : kb.psi_analytic(n, G);
+    dap[i] = (float)(1.0 / (psi * std::sqrt((double)N)));
+  }
+  int P = 0, Q = 0;
+  fft_shape(G, &P, &Q);
+  std::vector<float2> tw(G);
+  for (int k1 = 0; k1 < P; ++k1)
+    for (int n2 = 0; n2 < Q; ++n2) {
+      const double a = -2.0 * M_PI * (double)((long long)n2 * k1 % G) / G;
+      tw[k1 * Q + n2] = make_float2((float)std::cos(a), (float)std::sin(a));
+    }
+  // ---- taps, weights, strip bins (a0) ---------------------------------------------------------
+  const int S = G / SW;
+  std::vector<float> wts((size_t)R * M * 2 * W);
+  std::vector<int> m0x((size_t)R * M), m0y((size_t)R * M);
+  for (int r = 0; r < R; ++r)
+    for (int j = 0; j < M; ++j) {
+      const size_t pj = (size_t)r * M + j;
+      for (int ax = 0; ax < 2; ++ax) {
+        const double u = (double)G * (double)d->traj[pj * 2 + ax];
+        const long long m0 = (long long)std::floor(u - 0.5 * W) + 1;
+        for (int t = 0; t < W; ++t) wts[pj * 2 * W + ax * W + t] = (float)kb.phi(u - (double)(m0 + t));
+        const int w0 = (int)(((m0 % G) + G) % G);
+        (ax == 0 ? m0x : m0y)[pj] = w0;
+      }
+    }
+  std::vector<int> soff((size_t)R * (S + 1), 0);
+  std::vector<int2> ent;
+  ent.reserve((size_t)R * M * 2);
+  std::vector<std::vector<int2>> bins(S);
+  for (int r = 0; r < R; ++r) {
+    for (auto& b : bins) b.clear();
+    for (int j = 0; j < M; ++j) {
+      const size_t pj = (size_t)r * M + j;
+      int t = 0;
+      while (t < W) {   // split the W x-taps into runs of consecutive columns within one strip
+        const int col = (m0x[pj] + t) % G;
+        const int s = col / SW;
+        int cnt = 1;
+        while (t + cnt < W && ((m0x[pj] + t + cnt) % G) / SW == s && ((m0x[pj] + t + cnt) % G) == col + cnt) ++cnt;
+        const int packed = m0y[pj] | (t << 11) | (cnt << 16) | ((col - s * SW) << 21);
+        bins[s].push_back(make_int2(j, packed));
+        t += cnt;
+      }
+    }
+    for (int s = 0; s < S; ++s) {
+      soff[(size_t)r * (S + 1) + s] = (int)ent.size();
+      ent.insert(ent.end(), bins[s].begin(), bins[s].end());
+    }
+    soff[(size_t)r * (S + 1) + S] = (int)ent.size();
+  }
+  // ---- batch size: keep the [bf*C][N][G] half grid well inside L2 -------------------------------
+  const size_t per_frame = (size_t)C * N * G * sizeof(float2);
+  int bf = d->batch_frames;
+  if (bf == 0) {
+    const size_t target = 48ull << 20;
+    bf = (int)std::max<size_t>(1, target / per_frame);
+  }
+  bf = std::min(bf, L);
+  pl->bf = bf;
+  // ---- device uploads ---------------------------------------------------------------------------
+  mrf_status s;
+  if ((s = dev_alloc(pl, &pl->dap, N)) || (s = dev_alloc(pl, &pl->tw, G)) || (s = dev_alloc(pl, &pl->wts, wts.size())) ||
+      (s = dev_alloc(pl, &pl->ent, ent.size())) || (s = dev_alloc(pl, &pl->soff, soff.size())) ||
+      (s = dev_alloc(pl, &pl->fil, L)) || (s = dev_alloc(pl, &pl->H, (size_t)bf * C * N * G)) ||
+      (s = dev_alloc(pl, &pl->ybuf, (size_t)bf * C * M)) || (s = dev_alloc(pl, &pl->r, (size_t)L * N * N)) ||
+      (s = dev_alloc(pl, &pl->p, (size_t)L * N * N)) || (s = dev_alloc(pl, &pl->q, (size_t)L * N * N)) ||
+      (s = dev_alloc(pl, &pl->part, kPartBlocks)) || (s = dev_alloc(pl, &pl->sc, 1)))
+    return bail(s);
+  if (d->coils && C >= 1) {
+    if ((s = dev_alloc(pl, &pl->coils, (size_t)C * N * N))) return bail(s);
+  }
+  auto up = [&](void* dst, const void* src, size_t bytes) {
+    return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st);
+  };
+  cudaError_t ce = cudaSuccess;
+  if (!ce) ce = up(pl->dap, dap.data(), dap.size() * sizeof(float));
+  if (!ce) ce = up(pl->tw, tw.data(), tw.size() * sizeof(float2));
+  if (!ce) ce = up(pl->wts, wts.data(), wts.size() * sizeof(float));
+  if (!ce && !ent.empty()) ce = up(pl->ent, ent.data(), ent.size() * sizeof(int2));
+  if (!ce) ce = up(pl->soff, soff.data(), soff.size() * sizeof(int));
+  if (!ce) ce = up(pl->fil, fil.data(), fil.size() * sizeof(int));
+  if (!ce && pl->coils) ce = up(pl->coils, d->coils, (size_t)C * N * N * sizeof(float2));
+  if (!ce) ce = cudaMemsetAsync(pl->sc, 0, sizeof(CGScalars), st);
+  if (!ce) ce = cudaStreamSynchronize(st);
+  if (ce) {
+    free_plan(pl);
+    return fail(MRF_ECUDA, std::string("plan upload: ") + cudaGetErrorString(ce));
+  }
+  *out = pl;
+  return MRF_OK;
+}
+
+mrf_status mrf_plan_destroy(mrf_plan pl) {
+  if (!pl) return fail(MRF_EINVAL, "null plan");
+  DeviceGuard guard(pl->device);
+  cudaDeviceSynchronize();
+  free_plan(pl);
+  return MRF_OK;
+}
+
+size_t mrf_plan_device_bytes(mrf_plan pl) { return pl ? pl->bytes : 0; }
+
+mrf_status mrf_forward(mrf_plan pl, const void* x, void* y, void* stream) {
+  if (!pl || !x || !y) return fail(MRF_EINVAL, "null plan/x/y");
+  DeviceGuard guard(pl->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  bool host = false;
+  MRF_TRY(classify(pl, {x, y}, &host));
+  if (!host) return do_forward(pl, (const float2*)x, (float2*)y, st);
+  MRF_TRY(ensure_staging(pl, false));
+  const size_t bx = (size_t)pl->L * pl->N * pl->N * sizeof(float2), by = (size_t)pl->L * pl->C * pl->M * sizeof(float2);
+  CUDA_TRY(cudaMemcpyAsync(pl->stg_x, x, bx, cudaMemcpyHostToDevice, st));
+  MRF_TRY(do_forward(pl, pl->stg_x, pl->stg_y, st));
+  CUDA_TRY(cudaMemcpyAsync(y, pl->stg_y, by, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  return MRF_OK;
+}
+
+mrf_status mrf_adjoint(mrf_plan pl, const void* y, void* x, void* stream) {
+  if (!pl || !x || !y) return fail(MRF_EINVAL, "null plan/x/y");
+  DeviceGuard guard(pl->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  bool host = false;
+  MRF_TRY(classify(pl, {x, y}, &host));
+  if (!host) return do_adjoint(pl, (const float2*)y, (float2*)x, st);
+  MRF_TRY(ensure_staging(pl, false));
+  const size_t bx = (size_t)pl->L * pl->N * pl->N * sizeof(float2), by = (size_t)pl->L * pl->C * pl->M * sizeof(float2);
+  CUDA_TRY(cudaMemcpyAsync(pl->stg_y, y, by, cudaMemcpyHostToDevice, st));
+  MRF_TRY(do_adjoint(pl, pl->stg_y, pl->stg_x, st));
+  CUDA_TRY(cudaMemcpyAsync(x, pl->stg_x, bx, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  return MRF_OK;
+}
+
+mrf_status mrf_normal(mrf_plan pl, const void* x, void* out, float mu, void* stream) {
+  if (!pl || !x || !out) return fail(MRF_EINVAL, "null plan/x/out");
+  if (x == out) return fail(MRF_EINVAL, "out may not alias x");
+  if (!(mu >= 0.f) || !std::isfinite(mu)) return fail(MRF_EINVAL, "mu must be finite and >= 0");
+  DeviceGuard guard(pl->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  bool host = false;
+  MRF_TRY(classify(pl, {x, out}, &host));
+  if (!host) return do_normal(pl, (const float2*)x, (float2*)out, mu, st);
+  MRF_TRY(ensure_staging(pl, false));
+  const size_t bx = (size_t)pl->L * pl->N * pl->N * sizeof(float2);
+  CUDA_TRY(cudaMemcpyAsync(pl->stg_x, x, bx, cudaMemcpyHostToDevice, st));
+  MRF_TRY(do_normal(pl, pl->stg_x, pl->stg_y, mu, st));
+  CUDA_TRY(cudaMemcpyAsync(out, pl->stg_y, bx, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  return MRF_OK;
+}
+
+mrf_status mrf_dc_cg(mrf_plan pl, const void* y, const void* z, float mu, int n_iter, float tol, void* x,
+                     mrf_cg_info* info, void* stream) {
+  if (!pl || !y || !x) return fail(MRF_EINVAL, "null plan/y/x");
+  if (!(mu >= 0.f) || !std::isfinite(mu)) return fail(MRF_EINVAL, "mu must be finite and >= 0");
+  if (n_iter < 0) return fail(MRF_EINVAL, "n_iter < 0");
+  if (!(tol >= 0.f) || !std::isfinite(tol)) return fail(MRF_EINVAL, "tol must be finite and >= 0");
+  DeviceGuard guard(pl->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  bool host = false;
+  MRF_TRY(classify(pl, {y, z, x}, &host));
+  if (!host) return run_cg(pl, (const float2*)y, (const float2*)z, mu, n_iter, tol, (float2*)x, info, st);
+  MRF_TRY(ensure_staging(pl, z != nullptr));
+  const size_t bx = (size_t)pl->L * pl->N * pl->N * sizeof(float2), by = (size_t)pl->L * pl->C * pl->M * sizeof(float2);
+  CUDA_TRY(cudaMemcpyAsync(pl->stg_y, y, by, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaMemcpyAsync(pl->stg_x, x, bx, cudaMemcpyHostToDevice, st));
+  if (z) CUDA_TRY(cudaMemcpyAsync(pl->stg_z, z, bx, cudaMemcpyHostToDevice, st));
+  mrf_status s = run_cg(pl, pl->stg_y, z ? pl->stg_z : nullptr, mu, n_iter, tol, pl->stg_x, info, st);
+  if (s != MRF_OK && s != MRF_ENUMERIC) return s;
+  CUDA_TRY(cudaMemcpyAsync(x, pl->stg_x, bx, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  return s;
+}
+
+mrf_status mrf_profile_enable(mrf_plan pl, int enable) {
+  if (!pl) return fail(MRF_EINVAL, "null plan");
+  pl->prof.on = enable != 0;
+  for (int k = 0; k < MRF_K_COUNT; ++k) {
+    pl->prof.used[k] = 0;
+    pl->prof.launches[k] = 0;
+  }
+  return MRF_OK;
+}
+
+mrf_status mrf_profile_query(mrf_plan pl, int cls, double* total_ms, long long* launches) {
+  if (!pl || cls < 0 || cls >= MRF_K_COUNT) return fail(MRF_EINVAL, "bad plan or kernel class");
+  DeviceGuard guard(pl->device);
+  double tot = 0.0;
+  Prof& pr = pl->prof;
+  for (size_t i = 0; i + 1 < pr.used[cls]; i += 2) {
+    CUDA_TRY(cudaEventSynchronize(pr.ev[cls][i + 1]));
+    float ms = 0.f;
+    CUDA_TRY(cudaEventElapsedTime(&ms, pr.ev[cls][i], pr.ev[cls][i + 1]));
+    tot += ms;
+  }
+  if (total_ms) *total_ms = tot;
+  if (launches) *launches = (long long)(pr.used[cls] / 2);
+  return MRF_OK;
+}
+
+mrf_status mrf_nccl_get_unique_id(void* id_out) {
+  if (!id_out) return fail(MRF_EINVAL, "null id");
+  const char* why = nullptr;
+  const NcclApi* api = nccl_api(&why);
+  if (!api) return fail(MRF_ENCCL, why);
+  NcclUniqueId id;
+  const int rc = api->GetUniqueId(&id);
+  if (rc != 0) return fail(MRF_ENCCL, std::string("ncclGetUniqueId: ") + api->GetErrorString(rc));
+  std::memcpy(id_out, &id, sizeof(id));
+  return MRF_OK;
+}
+
+mrf_status mrf_nccl_comm_init(void** comm_out, int nranks, const void* id128, int rank, int device) {
+  if (!comm_out || !id128 || nranks < 1 || rank < 0 || rank >= nranks) return fail(MRF_EINVAL, "bad comm args");
+  const char* why = nullptr;
+  const NcclApi* api = nccl_api(&why);
+  if (!api) return fail(MRF_ENCCL, why);
+  DeviceGuard guard(device);
+  cudaSetDevice(device);
+  NcclUniqueId id;
+  std::memcpy(&id, id128, sizeof(id));
+  NcclComm comm = nullptr;
+  const int rc = api->CommInitRank(&comm, nranks, id, rank);
+  if (rc != 0) return fail(MRF_ENCCL, std::string("ncclCommInitRank: ") + api->GetErrorString(rc));
+  *comm_out = comm;
+  return MRF_OK;
+}
+
+mrf_status mrf_nccl_comm_destroy(void* comm) {
+  if (!comm) return fail(MRF_EINVAL, "null comm");
+  const char* why = nullptr;
+  const NcclApi* api = nccl_api(&why);
+  if (!api) return fail(MRF_ENCCL, why);
+  const int rc = api->CommDestroy(comm);
+  if (rc != 0) return fail(MRF_ENCCL, std::string("ncclCommDestroy: ") + api->GetErrorString(rc));
+  return MRF_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,303 @@
+"""GPU parity: the sm_100a path through the C-ABI vs the float64 oracle, element by element.
+
+Tolerances (BASELINE.json north_star): relative L2 <= 1e-5 per operator,
+<= 1e-4 on the CG solution; adjoint identity of the fp32 path <= 1e-6 normalised.
+All inputs come from ``synth`` (seeded); every expected value comes from ``oracle``.
+"""
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import synth
+from oracle import nufft as on
+from oracle import cg as ocg
+
+pytestmark = pytest.mark.gpu
+
+OP_TOL = 1e-5
+CG_TOL = 1e-4
+WORKERS = max(1, min(8, len(os.sched_getaffinity(0))))
+
+
+@pytest.fixture(scope="module")
+def mrf():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2310_05647_b200 import binding
+    return binding
+
+
+def rel(a, b):
+    a = np.asarray(a, dtype=np.complex128)
+    b = np.asarray(b, dtype=np.complex128)
+    return float(np.linalg.norm(a - b) / np.linalg.norm(b))
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def host(t):
+    torch.cuda.synchronize()
+    return t.cpu().numpy()
+
+
+def setup(name, frames=None, **over):
+    cfg = synth.get_config(name, **over)
+    traj = synth.spiral_trajectory(cfg.M, cfg.R, cfg.turns, cfg.p)
+    coils = synth.coil_maps(cfg.N, cfg.C, cfg.seed)
+    frames = list(range(cfg.L)) if frames is None else list(frames)
+    x = synth.images(cfg, frames)
+    return cfg, traj, coils, frames, x
+
+
+def plan_for(mrf, cfg, traj, coils, frames, **kw):
+    fil = synth.frame_interleaf(frames, cfg.R)
+    return mrf.Plan(cfg.N, traj, len(frames), coils=coils, W=cfg.W, frame_interleaf=fil, **kw)
+
+
+# ------------------------------------------------------------------------ operators
+@pytest.mark.parametrize("name", ["pr1", "cfg2"])
+def test_operators_vs_oracle(mrf, name):
+    cfg, traj, coils, frames, x = setup(name)
+    fil = synth.frame_interleaf(frames, cfg.R)
+    pl = plan_for(mrf, cfg, traj, coils, frames)
+    y_gpu = host(pl.forward(dev(x)))
+    y_ref = on.forward(x, traj, coils, cfg.W, frame_interleaf=fil, workers=WORKERS)
+    assert rel(y_gpu, y_ref) <= OP_TOL
+    yr = synth.random_kspace(cfg.C, cfg.M, frames, cfg.seed)
+    xa_gpu = host(pl.adjoint(dev(yr)))
+    xa_ref = on.adjoint(yr, traj, coils, cfg.N, cfg.W, frame_interleaf=fil, workers=WORKERS)
+    assert rel(xa_gpu, xa_ref) <= OP_TOL
+    xn_gpu = host(pl.normal(dev(x), mu=cfg.mu))
+    xn_ref = on.normal(x, traj, coils, cfg.W, mu=cfg.mu, frame_interleaf=fil, workers=WORKERS)
+    assert rel(xn_gpu, xn_ref) <= OP_TOL
+
+
+def test_operators_sense_coils_subset(mrf):
+    """SENSE (8 coils, Gaussian-blob maps) on a frame subset that spans two batches."""
+    cfg, traj, coils, frames, x = setup("sense", frames=range(40, 52))
+    fil = synth.frame_interleaf(frames, cfg.R)
+    pl = plan_for(mrf, cfg, traj, coils, frames, batch_frames=5)
+    y_gpu = host(pl.forward(dev(x)))
+    y_ref = on.forward(x, traj, coils, cfg.W, frame_interleaf=fil, workers=WORKERS)
+    assert rel(y_gpu, y_ref) <= OP_TOL
+    xa_gpu = host(pl.adjoint(dev(y_ref.astype(np.complex64))))
+    xa_ref = on.adjoint(y_ref.astype(np.complex64), traj, coils, cfg.N, cfg.W, frame_interleaf=fil, workers=WORKERS)
+    assert rel(xa_gpu, xa_ref) <= OP_TOL
+    xn_gpu = host(pl.normal(dev(x), mu=cfg.mu))
+    xn_ref = on.normal(x, traj, coils, cfg.W, mu=cfg.mu, frame_interleaf=fil, workers=WORKERS)
+    assert rel(xn_gpu, xn_ref) <= OP_TOL
+
+
+def test_operators_stress_subset(mrf):
+    """Stress spiral (p = 4, W = 8, 16 coils, M = 4096) on 3 frames: worst spreading contention."""
+    cfg, traj, coils, frames, x = setup("stress", frames=[0, 37, 1999])
+    fil = synth.frame_interleaf(frames, cfg.R)
+    pl = plan_for(mrf, cfg, traj, coils, frames)
+    y_gpu = host(pl.forward(dev(x)))
+    y_ref = on.forward(x, traj, coils, cfg.W, frame_interleaf=fil, workers=WORKERS)
+    assert rel(y_gpu, y_ref) <= OP_TOL
+    xa_gpu = host(pl.adjoint(dev(y_ref.astype(np.complex64))))
+    xa_ref = on.adjoint(y_ref.astype(np.complex64), traj, coils, cfg.N, cfg.W, frame_interleaf=fil, workers=WORKERS)
+    assert rel(xa_gpu, xa_ref) <= OP_TOL
+
+
+def test_full_mrf_launch_config_sampled_frames(mrf):
+    """MRF-shaped config at full size (L = 1000, the bench launch configuration): sampled frames
+    of forward / normal vs the oracle computed frame by frame."""
+    cfg = synth.get_config("mrf")
+    traj = synth.spiral_trajectory(cfg.M, cfg.R, cfg.turns, cfg.p)
+    x = synth.images(cfg)
+    pl = mrf.Plan(cfg.N, traj, cfg.L, W=cfg.W)
+    xd = dev(x)
+    y = pl.forward(xd)
+    xn = pl.normal(xd, mu=cfg.mu)
+    sample = [0, 1, 47, 48, 499, 998, 999]
+    y_s = host(y[sample])
+    xn_s = host(xn[sample])
+    y_ref = on.forward(x[sample], traj, None, cfg.W, frame_interleaf=[l % cfg.R for l in sample], workers=WORKERS)
+    xn_ref = on.normal(x[sample], traj, None, cfg.W, mu=cfg.mu, frame_interleaf=[l % cfg.R for l in sample],
+                       workers=WORKERS)
+    for i in range(len(sample)):
+        assert rel(y_s[i], y_ref[i]) <= OP_TOL
+        assert rel(xn_s[i], xn_ref[i]) <= OP_TOL
+
+
+@pytest.mark.parametrize("N,W", [(32, 2), (32, 16), (64, 6), (128, 8), (512, 6)])
+def test_grid_sizes_and_widths(mrf, N, W):
+    """Every supported G (64..1024) and the extreme widths W = 2 and W = 16 (max)."""
+    L, M, R = 3, 700, 2
+    traj = synth.spiral_trajectory(M, R, 5, 1.5)
+    rng_frames = range(L)
+    x = synth.iid_images(N, rng_frames, 99)
+    pl = mrf.Plan(N, traj, L, W=W)
+    y_gpu = host(pl.forward(dev(x)))
+    y_ref = on.forward(x, traj, None, W)
+    assert rel(y_gpu, y_ref) <= OP_TOL
+    yr = synth.random_kspace(1, M, rng_frames, 98)
+    assert rel(host(pl.adjoint(dev(yr))), on.adjoint(yr, traj, None, N, W)) <= OP_TOL
+
+
+def test_edges_wrap_dc_single_point(mrf):
+    """Points exactly at k = +-0.5 (wrap) and at DC, M = 1, L = 1."""
+    N = 32
+    traj = np.array([[[0.5, 0.5]], [[-0.5, 0.25]], [[0.0, 0.0]], [[0.5, -0.5]]], np.float32)
+    for r in range(4):
+        x = synth.iid_images(N, [r], 5)
+        pl = mrf.Plan(N, traj[r:r + 1], 1, W=6)
+        y_gpu = host(pl.forward(dev(x)))
+        y_ref = on.forward(x, traj[r:r + 1], None, 6)
+        assert rel(y_gpu, y_ref) <= OP_TOL
+        yv = np.array([[[1.0 - 2.0j]]], np.complex64)
+        assert rel(host(pl.adjoint(dev(yv))), on.adjoint(yv, traj[r:r + 1], None, N, 6)) <= OP_TOL
+
+
+def test_cartesian_discrete_equals_fft(mrf):
+    """Full Cartesian trajectory with discrete deapodisation: the GPU forward equals the FFT."""
+    N = 32
+    traj = synth.cartesian_trajectory(N)
+    x = synth.iid_images(N, [0, 1], 17)
+    pl = mrf.Plan(N, traj, 2, W=6, deapod="discrete")
+    y_gpu = host(pl.forward(dev(x)))
+    ref = np.stack([np.fft.fftshift(np.fft.fft2(np.fft.ifftshift(x[i].astype(np.complex128)), norm="ortho")).ravel()
+                    for i in range(2)])[:, None, :]
+    assert rel(y_gpu, ref) <= OP_TOL
+    assert rel(host(pl.normal(dev(x))), x) <= OP_TOL      # A^H A = I
+
+
+def test_zero_in_zero_out(mrf):
+    cfg, traj, coils, frames, _ = setup("pr1")
+    pl = plan_for(mrf, cfg, traj, coils, frames)
+    z = torch.zeros(pl.x_shape, dtype=torch.complex64, device="cuda")
+    assert not torch.any(pl.forward(z)).item()
+    assert not torch.any(pl.adjoint(torch.zeros(pl.y_shape, dtype=torch.complex64, device="cuda"))).item()
+
+
+def test_adjoint_identity_fp32(mrf):
+    cfg, traj, coils, frames, x = setup("sense", frames=range(3))
+    pl = plan_for(mrf, cfg, traj, coils, frames)
+    yr = synth.random_kspace(cfg.C, cfg.M, frames, 3)
+    Ax = host(pl.forward(dev(x))).astype(np.complex128)
+    AHy = host(pl.adjoint(dev(yr))).astype(np.complex128)
+    lhs, rhs = np.vdot(Ax, yr), np.vdot(x.astype(np.complex128), AHy)
+    assert abs(lhs - rhs) <= 1e-6 * np.linalg.norm(Ax) * np.linalg.norm(yr)
+
+
+def test_host_pointer_path_matches_device(mrf):
+    cfg, traj, coils, frames, x = setup("pr1")
+    pl = plan_for(mrf, cfg, traj, coils, frames)
+    y_dev = host(pl.forward(dev(x)))
+    y_host = pl.forward(torch.from_numpy(x)).numpy()
+    assert np.array_equal(y_dev, y_host)
+    xp = torch.from_numpy(x).pin_memory()
+    y_pin = pl.forward(xp).numpy()
+    assert np.array_equal(y_dev, y_pin)
+
+
+def test_forward_deterministic(mrf):
+    cfg, traj, coils, frames, x = setup("cfg2", frames=range(30))
+    pl = plan_for(mrf, cfg, traj, coils, frames)
+    xd = dev(x)
+    a, b = host(pl.forward(xd)), host(pl.forward(xd))
+    assert np.array_equal(a, b)
+    yr = dev(synth.random_kspace(1, cfg.M, frames, 1))
+    u, v = host(pl.adjoint(yr)), host(pl.adjoint(yr))
+    assert rel(u, v) <= 1e-6
+
+
+def test_batching_invariance(mrf):
+    """Results do not depend on the frame-batch size (ragged last batch included)."""
+    cfg, traj, coils, frames, x = setup("pr1")
+    outs = []
+    for bf in (1, 3, 8):
+        pl = plan_for(mrf, cfg, traj, coils, frames, batch_frames=bf)
+        outs.append(host(pl.normal(dev(x), mu=0.01)))
+    assert rel(outs[0], outs[2]) <= 1e-6 and rel(outs[1], outs[2]) <= 1e-6
+
+
+# ------------------------------------------------------------------------ CG
+def _cg_case(mrf, name, frames=None, n_iter=None, **over):
+    cfg, traj, coils, frames, x = setup(name, frames=frames, **over)
+    fil = synth.frame_interleaf(frames, cfg.R)
+    y = on.forward(x, traj, coils, cfg.W, frame_interleaf=fil, workers=WORKERS)
+    if cfg.noise > 0:
+        sig = cfg.noise * np.sqrt(np.mean(np.abs(y) ** 2))
+        y = y + sig * synth.unit_noise(cfg.C, cfg.M, frames, cfg.seed)
+    y = y.astype(np.complex64)
+    n_iter = cfg.cg_iters if n_iter is None else n_iter
+    H = lambda v: on.normal(v, traj, coils, cfg.W, mu=cfg.mu, frame_interleaf=fil, workers=WORKERS)
+    rhs = ocg.dc_rhs(on.adjoint(y, traj, coils, cfg.N, cfg.W, frame_interleaf=fil, workers=WORKERS), None, cfg.mu)
+    x_ref, h_ref = ocg.cg(H, rhs, np.zeros_like(rhs), n_iter)
+    pl = plan_for(mrf, cfg, traj, coils, frames)
+    xg, info = pl.dc_cg(dev(y), mu=cfg.mu, n_iter=n_iter)
+    xg = host(xg)
+    assert info["iters"] == n_iter
+    assert rel(xg, x_ref) <= CG_TOL
+    assert np.allclose(info["history"], h_ref, rtol=1e-3, atol=0)
+    return rel(xg, x_ref)
+
+
+def test_cg_pr1(mrf):
+    _cg_case(mrf, "pr1")
+
+
+def test_cg_cfg2(mrf):
+    _cg_case(mrf, "cfg2")
+
+
+def test_cg_sense_subset(mrf):
+    _cg_case(mrf, "sense", frames=range(10))
+
+
+def test_cg_x0_z_and_tol(mrf):
+    cfg, traj, coils, frames, x = setup("pr1")
+    fil = synth.frame_interleaf(frames, cfg.R)
+    y = on.forward(x, traj, None, cfg.W).astype(np.complex64)
+    rng = np.random.default_rng(3)
+    x0 = (0.1 * (rng.standard_normal(x.shape) + 1j * rng.standard_normal(x.shape))).astype(np.complex64)
+    z = (rng.standard_normal(x.shape) + 1j * rng.standard_normal(x.shape)).astype(np.complex64)
+    mu = 0.05
+    H = lambda v: on.normal(v, traj, None, cfg.W, mu=mu)
+    rhs = ocg.dc_rhs(on.adjoint(y, traj, None, cfg.N, cfg.W), z, mu)
+    x_ref, h_ref = ocg.cg(H, rhs, x0, 30, tol=1e-3)
+    pl = plan_for(mrf, cfg, traj, None, frames)
+    xg, info = pl.dc_cg(dev(y), x0=dev(x0), z=dev(z), mu=mu, n_iter=30, tol=1e-3)
+    assert info["iters"] == len(h_ref) - 1
+    assert rel(host(xg), x_ref) <= CG_TOL
+    assert info["rel_resid"] < 1e-3
+
+
+def test_cg_zero_rhs(mrf):
+    cfg, traj, coils, frames, x = setup("pr1")
+    pl = plan_for(mrf, cfg, traj, None, frames)
+    xg, info = pl.dc_cg(torch.zeros(pl.y_shape, dtype=torch.complex64, device="cuda"), mu=0.01, n_iter=4)
+    assert info["iters"] == 0
+    assert not torch.any(xg).item()
+
+
+def test_cg_host_pointers(mrf):
+    cfg, traj, coils, frames, x = setup("pr1")
+    pl = plan_for(mrf, cfg, traj, None, frames)
+    y = on.forward(x, traj, None, cfg.W).astype(np.complex64)
+    xd, _ = pl.dc_cg(dev(y), mu=0.01, n_iter=5)
+    xh, _ = pl.dc_cg(torch.from_numpy(y), mu=0.01, n_iter=5)
+    assert rel(xh.numpy(), host(xd)) <= 1e-6
+
+
+def test_invalid_calls(mrf):
+    cfg, traj, coils, frames, x = setup("pr1")
+    pl = plan_for(mrf, cfg, traj, None, frames)
+    xd = dev(x)
+    with pytest.raises(mrf.MrfError) as e:
+        pl.normal(xd, mu=-1.0)
+    assert e.value.status == 1
+    import ctypes
+    assert mrf.lib.mrf_normal(pl._h, ctypes.c_void_p(xd.data_ptr()), ctypes.c_void_p(xd.data_ptr()),
+                              ctypes.c_float(0.0), None) == 1     # aliasing
+    with pytest.raises(mrf.MrfError):
+        pl.dc_cg(dev(np.zeros(pl.y_shape, np.complex64)), n_iter=-1)
+    with pytest.raises(mrf.MrfError):   # host and device pointers mixed
+        pl.forward(xd, torch.zeros(pl.y_shape, dtype=torch.complex64))
