@@ -24,6 +24,7 @@
  *
  * Memory: every complex array is interleaved complex64 (float real, float imag), C-contiguous:
  *   x, z, out  [L_local][N][N]     y  [L_local][C][M]     coils [C][N][N]     traj [R][M][2]
+ * Every array must be 16-byte aligned (MRF_EINVAL otherwise; torch/cudaMalloc allocations are).
  * Array arguments of the operator calls may be DEVICE pointers (on the plan's device; fully
  * asynchronous on `stream`, CUDA-graph capturable, no allocation) or HOST pointers (pinned or
  * pageable; the call stages them through plan-owned device buffers allocated on first use and

@@ -1,0 +1,705 @@
+// gridding.cuh -- persistent sm_100a kernels of the multi-frame KB-gridding NUFFT pair.
+//
+// Pipeline per frame l and coil c (the paper's A = F_u C, and
+// its adjoint A*):
+//   forward A  : k_fwd_rows  a1 deapod . coil . zero-pad, a2 row FFTs of the N non-zero rows
+//                k_fwd_cols  a2 column FFT of one 16-column strip, a3 KB gather interpolation
+//   adjoint A^H: k_adj_cols  a4 KB spread into the strip (shared memory), a5 column iFFT
+//                k_adj_rows  a5 row iFFTs, a6 crop . deapod . conj-coil . coil sum [+ mu x]
+//
+// Every kernel is persistent (grid = resident CTAs) and walks a list of work items.  The global
+// inputs of the NEXT item are fetched by the Tensor Memory Accelerator (cp.async.bulk, completion
+// on an mbarrier) into shared memory while the current item computes, so no warp waits on HBM/L2
+// inside an item.  The N x G half grid between the row and the column pass is stored strip-major
+// ([fc][strip][row][16]) so one strip of one frame-coil is a contiguous 32 KB bulk copy; it lives
+// in a frame-batch workspace sized to stay in the 126 MB L2.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "fft.cuh"
+
+namespace mrf {
+
+constexpr int SW = 16;             // columns per strip (>= W: a point's x-taps touch <= 2 strips)
+constexpr int kYBytes = 16384;     // largest y[fc] staged in shared memory by k_adj_cols
+constexpr int kChunkHdr = 8;       // header words of a strip chunk
+constexpr int kRowThreads = 128;
+
+struct CGScalars;
+
+// Per (interleaf, strip) "chunks" (32-bit words, 16-byte multiples), built once at plan time.
+// Forward chunk (gather):  [0] n_rec [1..7] 0, then n_rec point records of recw words:
+//     j, taps (gy0 | tx0<<11 | ntx<<16 | cx0<<21), wx[W], wy[W] (fp32)
+// Adjoint chunk (spread), the strip's KB spread matrix in SELL-32 form (rows = strip cells
+// sorted by non-zero count, slices of 32 lanes):
+//     [0] n_slices [1] cells offset [2] entries offset [3..7] 0
+//     slices : n_slices x {first entry, width}
+//     cells  : n_slices x 32 uint16 strip cells (gy*16 + cx), 0xFFFF = empty lane
+//     entries: {j, w = wx*wy (fp32 bits, from float64)}; entry k of lane l at first + 32k + l
+// ftab / atab[r*S + s] = {word offset, words} of each chunk.
+struct DevPlan {
+  int N, G, M, R, C, W, S, recw;      // S = G / SW strips; recw = 32-bit words per point record
+  const float2* __restrict__ coils;   // [C][N][N] or nullptr (C == 1)
+  const float* __restrict__ dap;      // [N]  1 / (psi(n) sqrt(N))
+  const float2* __restrict__ tw;      // [G]  tw[k1*Q + n2] = exp(-i 2 pi n2 k1 / G)
+  const int* __restrict__ fchunks;    // forward chunks
+  const int2* __restrict__ ftab;      // [R*S] {offset, words}
+  const int* __restrict__ achunks;    // adjoint chunks
+  const int2* __restrict__ atab;      // [R*S] {offset, words}
+  const int* __restrict__ fil;        // [L_local] interleaf of each local frame
+};
+
+// ---------------------------------------------------------------------------- async copy (TMA)
+__device__ __forceinline__ uint32_t smem_u32(const void* ptr) {
+  return (uint32_t)__cvta_generic_to_shared(ptr);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+// global -> shared bulk copy (bytes % 16 == 0, both addresses 16-byte aligned)
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n .reg .pred P;\n mbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2;\n selp.u32 %0, 1, 0, P;\n}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  while (!mbar_try(bar, parity)) {
+  }
+}
+
+// float2 += v in shared memory (64-bit CAS; no native shared float add on sm_100)
+__device__ __forceinline__ void smem_add2(float2* a, float2 v) {
+  unsigned long long* q = reinterpret_cast<unsigned long long*>(a);
+  unsigned long long old = *q, assumed;
+  do {
+    assumed = old;
+    float2 f = *reinterpret_cast<float2*>(&assumed);
+    f.x += v.x;
+    f.y += v.y;
+    old = atomicCAS(q, assumed, *reinterpret_cast<unsigned long long*>(&f));
+  } while (old != assumed);
+}
+
+// image index <-> wrapped grid index (centred n = i - N/2, grid position n mod G)
+template <int G>
+__device__ __forceinline__ int grid_to_img(int pos) {   // pos in the kept set
+  constexpr int N = G / 2;
+  return pos < N / 2 ? pos + N / 2 : pos - (G - N / 2);
+}
+
+// ---------------------------------------------------------------------------- launch shapes
+template <int G>
+struct RowCfg {
+  static constexpr int T = FFTShape<G>::T, P = FFTShape<G>::P, Q = FFTShape<G>::Q;
+  static constexpr int RPC = kRowThreads / T;          // rows per item
+  static constexpr int N = G / 2;
+  static constexpr int EX = Q * (P + 1);               // padded exchange buffer per row
+};
+template <int G>
+constexpr int cols_threads() { return SW * FFTShape<G>::T; }
+
+template <int G>
+constexpr size_t fwd_rows_smem(int n_stage) {   // tw | n_stage image blocks | coil block | exchange | bar
+  using R = RowCfg<G>;
+  return (size_t(G) + size_t(n_stage + 1) * R::RPC * R::N + size_t(R::RPC) * R::EX) * 8 + 16 + R::N * 4;
+}
+template <int G>
+constexpr size_t adj_rows_smem() {              // tw | H block | x blocks[2] | exchange | bars
+  using R = RowCfg<G>;
+  return (size_t(G) + size_t(R::RPC) * G + 2 * size_t(R::RPC) * R::N + size_t(R::RPC) * R::EX) * 8 + 32 + R::N * 4;
+}
+// Column kernels: shared memory per CTA is fixed by the resident-CTA target (2 per SM for G <= 512,
+// 1 for G = 1024); whatever the strip, twiddles (and y) leave is the chunk staging buffer.
+template <int G>
+constexpr int cols_ctas_per_sm() { return G >= 1024 ? 1 : 2; }
+template <int G>
+constexpr size_t fwd_cols_fixed() { return (size_t(G) + size_t(G / 2) * SW + size_t(G) * SW) * 8 + 16; }
+template <int G>
+constexpr size_t adj_cols_fixed(bool ystage) { return (size_t(G) + size_t(G) * SW) * 8 + (ystage ? kYBytes : 0) + 16; }
+
+// ---------------------------------------------------------------------------- point records
+struct Rec {
+  int j, gy0, tx0, ntx, cx0;
+  const float* wx;   // wx[W] (index by tap), then wy[W]
+};
+__device__ __forceinline__ Rec read_rec(const int* rp, int W) {
+  Rec r;
+  r.j = rp[0];
+  const int pk = rp[1];
+  r.gy0 = pk & 2047;
+  r.tx0 = (pk >> 11) & 31;
+  r.ntx = (pk >> 16) & 31;
+  r.cx0 = (pk >> 21) & 31;
+  r.wx = reinterpret_cast<const float*>(rp + 2);
+  (void)W;
+  return r;
+}
+
+// ============================================================================ forward rows
+// Items (bl, rowblock, c), c fastest.  MODE 0: image block = x.  MODE 1 (CG, C == 1): image block
+// = p' = r + beta p with x' = x + alpha p, both written back (one pass over r, p, x per iteration).
+template <int G, int MODE>
+__global__ void __launch_bounds__(kRowThreads)
+k_fwd_rows(DevPlan p, const float2* __restrict__ x, float2* __restrict__ H, int l0, int nb,
+           float2* __restrict__ cg_r, float2* __restrict__ cg_p, float2* __restrict__ cg_x,
+           const double* __restrict__ cg_ab) {
+  using Rc = RowCfg<G>;
+  constexpr int P = Rc::P, Q = Rc::Q, T = Rc::T, N = Rc::N, RPC = Rc::RPC, A = Q / T, B = P / T;
+  constexpr int NRB = N / RPC, S = G / SW, NST = MODE == 1 ? 3 : 1;
+  constexpr uint32_t BLK = RPC * N * sizeof(float2);
+  extern __shared__ __align__(128) unsigned char smraw[];
+  float2* stw = reinterpret_cast<float2*>(smraw);
+  float2* xs = stw + G;                       // NST image blocks
+  float2* cs = xs + NST * RPC * N;            // coil block
+  float2* ex = cs + RPC * N;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(ex + RPC * Rc::EX);
+  float* sdap = reinterpret_cast<float*>(bar + 2);
+  const int C = p.C;
+  const int n_items = nb * NRB * C;
+  const int tid = threadIdx.x, rloc = tid / T, t = tid % T;
+  if (tid == 0) {
+    mbar_init(bar, 1);
+    fence_mbar_init();
+  }
+  for (int i = tid; i < G; i += kRowThreads) stw[i] = p.tw[i];
+  for (int i = tid; i < N; i += kRowThreads) sdap[i] = p.dap[i];
+  __syncthreads();
+  auto issue = [&](int item) {
+    const int c = item % C, rb = (item / C) % NRB, bl = item / (C * NRB);
+    const size_t off = ((size_t)(l0 + bl) * N + (size_t)rb * RPC) * N;
+    mbar_expect_tx(bar, BLK * NST + (p.coils ? BLK : 0));
+    if (MODE == 0) {
+      bulk_g2s(xs, x + off, BLK, bar);
+    } else {
+      bulk_g2s(xs, cg_r + off, BLK, bar);
+      bulk_g2s(xs + RPC * N, cg_p + off, BLK, bar);
+      bulk_g2s(xs + 2 * RPC * N, cg_x + off, BLK, bar);
+    }
+    if (p.coils) bulk_g2s(cs, p.coils + ((size_t)c * N + (size_t)rb * RPC) * N, BLK, bar);
+  };
+  int item = blockIdx.x;
+  uint32_t ph = 0;
+  if (tid == 0 && item < n_items) issue(item);
+  float beta = 0.f, alpha = 0.f;
+  if (MODE == 1) {
+    alpha = (float)cg_ab[0];
+    beta = (float)cg_ab[1];
+  }
+  float2* myex = ex + rloc * Rc::EX;
+  for (; item < n_items; item += gridDim.x) {
+    const int c = item % C, rb = (item / C) % NRB, bl = item / (C * NRB);
+    const int iy = rb * RPC + rloc;
+    const float dy = sdap[iy];
+    mbar_wait(bar, ph);
+    ph ^= 1;
+    float2 v[A][P];
+#pragma unroll
+    for (int a = 0; a < A; ++a) {
+      const int n2 = t + T * a;
+#pragma unroll
+      for (int n1 = 0; n1 < P; ++n1) {
+        if (n1 < P / 4 || n1 >= 3 * P / 4) {
+          const int ix = grid_to_img<G>(Q * n1 + n2);
+          float2 img;
+          if (MODE == 0) {
+            img = xs[rloc * N + ix];
+          } else {   // fused CG vector update
+            const float2 rv = xs[rloc * N + ix], pv = xs[RPC * N + rloc * N + ix], xv = xs[2 * RPC * N + rloc * N + ix];
+            img = make_float2(fmaf(beta, pv.x, rv.x), fmaf(beta, pv.y, rv.y));
+            const size_t gi = ((size_t)(l0 + bl) * N + iy) * N + ix;
+            cg_p[gi] = img;
+            cg_x[gi] = make_float2(fmaf(alpha, pv.x, xv.x), fmaf(alpha, pv.y, xv.y));
+          }
+          float2 val = cscale(img, dy * sdap[ix]);
+          if (p.coils) val = cmul(val, cs[rloc * N + ix]);
+          v[a][n1] = val;
+        } else {
+          v[a][n1] = make_float2(0.f, 0.f);
+        }
+      }
+    }
+    __syncthreads();   // staging consumed: prefetch the next item behind this item's FFT
+    if (tid == 0 && item + (int)gridDim.x < n_items) {
+      fence_proxy_async();
+      issue(item + gridDim.x);
+    }
+#pragma unroll
+    for (int a = 0; a < A; ++a) {
+      const int n2 = t + T * a;
+      dft<P, -1>(v[a]);
+#pragma unroll
+      for (int k1 = 0; k1 < P; ++k1) myex[n2 * (P + 1) + k1] = cmul(v[a][k1], stw[k1 * Q + n2]);
+    }
+    __syncwarp();
+    const size_t fc = (size_t)bl * C + c;
+#pragma unroll
+    for (int b = 0; b < B; ++b) {
+      const int k1 = t + T * b;
+      float2 w[Q];
+#pragma unroll
+      for (int n2 = 0; n2 < Q; ++n2) w[n2] = myex[n2 * (P + 1) + k1];
+      dft<Q, -1>(w);
+#pragma unroll
+      for (int k2 = 0; k2 < Q; ++k2) {
+        const int gx = k1 + P * k2;
+        H[((fc * S + gx / SW) * N + iy) * SW + (gx % SW)] = w[k2];
+      }
+    }
+    __syncwarp();
+  }
+}
+
+// ============================================================================ forward columns
+// Items (fc, strip).  y (frame l0's first sample) must be zeroed: each point's partial sums from
+// its (at most two) strips are added with fp32 atomics onto 0, which is order independent.
+// Pipeline: the next H strip is fetched right after this item's strip is in registers; the next
+// chunk (point records) right after this item's gather.
+template <int G>
+__global__ void __launch_bounds__(SW * FFTShape<G>::T, (G >= 1024 ? 1 : 2))
+k_fwd_cols(DevPlan p, const float2* __restrict__ H, float2* __restrict__ y, int l0, int nb, int stage_cap) {
+  using F = FFTShape<G>;
+  constexpr int P = F::P, Q = F::Q, T = F::T, N = G / 2, A = Q / T, B = P / T, S = G / SW;
+  constexpr uint32_t STRIP_IN = N * SW * sizeof(float2);
+  extern __shared__ __align__(128) unsigned char smraw[];
+  float2* stw = reinterpret_cast<float2*>(smraw);
+  float2* inb = stw + G;
+  float2* strip = inb + N * SW;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(strip + G * SW);      // H, chunk
+  int* stage = reinterpret_cast<int*>(bars + 2);
+  __shared__ int copied;                                             // bytes of the staged chunk
+  const int C = p.C, W = p.W, recw = p.recw;
+  const int n_items = nb * C * S;
+  const int tid = threadIdx.x, c = tid % SW, t = tid / SW;
+  const int warp = tid >> 5, lane = tid & 31, nwarps = blockDim.x >> 5;
+  if (tid == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    fence_mbar_init();
+  }
+  for (int i = tid; i < G; i += blockDim.x) stw[i] = p.tw[i];
+  __syncthreads();
+  auto chunk_of = [&](int item) -> int2 {
+    const int fc = item / S, s = item % S;
+    return __ldg(p.ftab + __ldg(p.fil + l0 + fc / C) * S + s);
+  };
+  auto issue_in = [&](int item) {
+    mbar_expect_tx(&bars[0], STRIP_IN);
+    bulk_g2s(inb, H + (size_t)item * (N * SW), STRIP_IN, &bars[0]);
+  };
+  auto issue_chunk = [&](int2 ow) {   // records beyond the staging capacity are read from L2
+    const uint32_t bytes = (uint32_t)min(stage_cap, ow.y * 4) & ~15u;
+    copied = (int)bytes;
+    mbar_expect_tx(&bars[1], bytes);
+    bulk_g2s(stage, p.fchunks + ow.x, bytes, &bars[1]);
+  };
+  int item = blockIdx.x;
+  int2 off_next = make_int2(0, 0);
+  if (tid == 0 && item < n_items) {
+    issue_in(item);
+    issue_chunk(chunk_of(item));
+    if (item + (int)gridDim.x < n_items) off_next = chunk_of(item + gridDim.x);
+  }
+  for (int k = 0; item < n_items; item += gridDim.x, ++k) {
+    const int fc = item / S;
+    const int next = item + gridDim.x;
+    mbar_wait(&bars[0], k & 1);
+    float2 v[A][P];
+#pragma unroll
+    for (int a = 0; a < A; ++a) {
+      const int n2 = t + T * a;
+#pragma unroll
+      for (int n1 = 0; n1 < P; ++n1) {
+        v[a][n1] = (n1 < P / 4 || n1 >= 3 * P / 4) ? inb[grid_to_img<G>(Q * n1 + n2) * SW + c] : make_float2(0.f, 0.f);
+      }
+    }
+    __syncthreads();
+    if (tid == 0 && next < n_items) {
+      fence_proxy_async();
+      issue_in(next);
+    }
+#pragma unroll
+    for (int a = 0; a < A; ++a) {
+      const int n2 = t + T * a;
+      dft<P, -1>(v[a]);
+#pragma unroll
+      for (int k1 = 0; k1 < P; ++k1) strip[(n2 * P + k1) * SW + c] = cmul(v[a][k1], stw[k1 * Q + n2]);
+    }
+    __syncthreads();
+    float2 w[B][Q];
+#pragma unroll
+    for (int b = 0; b < B; ++b) {
+      const int k1 = t + T * b;
+#pragma unroll
+      for (int n2 = 0; n2 < Q; ++n2) w[b][n2] = strip[(n2 * P + k1) * SW + c];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int b = 0; b < B; ++b) {
+      const int k1 = t + T * b;
+      dft<Q, -1>(w[b]);
+#pragma unroll
+      for (int k2 = 0; k2 < Q; ++k2) strip[(k1 + P * k2) * SW + c] = w[b][k2];   // strip [gy][c]
+    }
+    __syncthreads();
+    // a3: KB gather interpolation.  A warp takes 32/W point records at a time, lane = (record,
+    // y-tap): each lane sums its tap row, the W row partials are combined with shuffles, and the
+    // record's leader lane adds the strip's share of y_j.
+    mbar_wait(&bars[1], k & 1);
+    {
+      const int n_rec = stage[0];
+      const int n_st = (copied / 4 - kChunkHdr) / recw;     // records staged in shared memory
+      const int* recs = stage + kChunkHdr;
+      const int* grecs = n_st < n_rec ? p.fchunks + chunk_of(item).x + kChunkHdr : recs;
+      float2* yf = y + (size_t)fc * p.M;
+      const int rpw = 32 / W, slot = lane / W, ty = lane - slot * W;
+      for (int base = warp * rpw; base < n_rec; base += nwarps * rpw) {
+        const int e = base + slot;
+        const bool valid = slot < rpw && e < n_rec;
+        float2 part = make_float2(0.f, 0.f);
+        int j = 0;
+        if (valid) {
+          const Rec rr = read_rec((e < n_st ? recs : grecs) + e * recw, W);
+          const float2* row = strip + ((rr.gy0 + ty) & (G - 1)) * SW + rr.cx0;
+          for (int i = 0; i < rr.ntx; ++i) {
+            const float wx = rr.wx[rr.tx0 + i];
+            const float2 g = row[i];
+            part.x = fmaf(wx, g.x, part.x);
+            part.y = fmaf(wx, g.y, part.y);
+          }
+          const float wy = rr.wx[W + ty];
+          part.x *= wy;
+          part.y *= wy;
+          j = rr.j;
+        }
+        float2 sum = part;
+        for (int o = 1; o < W; ++o) {
+          sum.x += __shfl_down_sync(0xffffffffu, part.x, o);
+          sum.y += __shfl_down_sync(0xffffffffu, part.y, o);
+        }
+        if (valid && ty == 0) {
+          atomicAdd(&yf[j].x, sum.x);
+          atomicAdd(&yf[j].y, sum.y);
+        }
+      }
+    }
+    __syncthreads();
+    if (tid == 0 && next < n_items) {
+      fence_proxy_async();
+      issue_chunk(off_next);
+      if (next + (int)gridDim.x < n_items) off_next = chunk_of(next + gridDim.x);
+    }
+  }
+}
+
+// ============================================================================ adjoint columns
+// Items (fc, strip).  a4: KB spreading as an output-stationary sparse product: lane = strip cell,
+// summing w * y_j over its (j, w) list (SELL-32 slices, no atomics, deterministic);
+// a5: column iFFT, then the N kept rows are stored strip-major H[fc][strip][iy][16].
+// Pipeline: y[fc] and the chunk of the next item are fetched right after this item's spread.
+template <int G>
+__global__ void __launch_bounds__(SW * FFTShape<G>::T, (G >= 1024 ? 1 : 2))
+k_adj_cols(DevPlan p, const float2* __restrict__ y, float2* __restrict__ H, int l0, int nb, int ystage, int stage_cap) {
+  using F = FFTShape<G>;
+  constexpr int P = F::P, Q = F::Q, T = F::T, N = G / 2, A = Q / T, B = P / T, S = G / SW;
+  extern __shared__ __align__(128) unsigned char smraw[];
+  float2* stw = reinterpret_cast<float2*>(smraw);
+  float2* strip = stw + G;
+  float2* ys = strip + G * SW;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<unsigned char*>(ys) + (ystage ? kYBytes : 0));
+  int* stage = reinterpret_cast<int*>(bars + 2);
+  __shared__ int copied;
+  const int C = p.C, M = p.M;
+  const int n_items = nb * C * S;
+  const int tid = threadIdx.x, c = tid % SW, t = tid / SW;
+  const int warp = tid >> 5, lane = tid & 31, nwarps = blockDim.x >> 5;
+  const uint32_t ybytes = (uint32_t)M * sizeof(float2);
+  if (tid == 0) {
+    mbar_init(&bars[0], 1);
+    fence_mbar_init();
+  }
+  for (int i = tid; i < G; i += blockDim.x) stw[i] = p.tw[i];
+  for (int i = tid; i < G * SW; i += blockDim.x) strip[i] = make_float2(0.f, 0.f);
+  __syncthreads();
+  auto chunk_of = [&](int item) -> int2 {
+    const int fc = item / S, s = item % S;
+    return __ldg(p.atab + __ldg(p.fil + l0 + fc / C) * S + s);
+  };
+  auto issue = [&](int item, int2 ow) {   // a chunk larger than the staging buffer is read from L2
+    const uint32_t bytes = ow.y * 4 <= stage_cap ? (uint32_t)ow.y * 4 : (uint32_t)kChunkHdr * 4;
+    copied = (int)bytes;
+    mbar_expect_tx(&bars[0], bytes + (ystage ? ybytes : 0));
+    bulk_g2s(stage, p.achunks + ow.x, bytes, &bars[0]);
+    if (ystage) bulk_g2s(ys, y + (size_t)(item / S) * M, ybytes, &bars[0]);
+  };
+  int item = blockIdx.x;
+  int2 off_next = make_int2(0, 0);
+  if (tid == 0 && item < n_items) {
+    issue(item, chunk_of(item));
+    if (item + (int)gridDim.x < n_items) off_next = chunk_of(item + gridDim.x);
+  }
+  for (int k = 0; item < n_items; item += gridDim.x, ++k) {
+    const int fc = item / S;
+    const int next = item + gridDim.x;
+    mbar_wait(&bars[0], k & 1);
+    {
+      const int nsl = stage[0], cells_off = stage[1], ent_off = stage[2];
+      const float2* yf = y + (size_t)fc * M;
+      if (copied > kChunkHdr * 4) {   // staged chunk: shared-memory loads only
+        const int2* sl_tab = reinterpret_cast<const int2*>(stage + kChunkHdr);
+        const unsigned short* cells = reinterpret_cast<const unsigned short*>(stage + cells_off);
+        const int2* ents = reinterpret_cast<const int2*>(stage + ent_off);
+        for (int sl = warp; sl < nsl; sl += nwarps) {
+          const int2 si = sl_tab[sl];
+          const int cell = cells[sl * 32 + lane];
+          const int2* ep = ents + si.x + lane;
+          float2 acc = make_float2(0.f, 0.f);
+#pragma unroll 8
+          for (int kk = 0; kk < si.y; ++kk) {
+            const int2 e = ep[kk * 32];
+            const float wgt = __int_as_float(e.y);
+            const float2 v = ystage ? ys[e.x] : __ldg(yf + e.x);
+            acc.x = fmaf(wgt, v.x, acc.x);
+            acc.y = fmaf(wgt, v.y, acc.y);
+          }
+          if (cell != 0xFFFF) strip[cell] = acc;
+        }
+      } else {                        // chunk too large to stage: read it in place from L2
+        const int* ch = p.achunks + chunk_of(item).x;
+        const int2* sl_tab = reinterpret_cast<const int2*>(ch + kChunkHdr);
+        const unsigned short* cells = reinterpret_cast<const unsigned short*>(ch + __ldg(ch + 1));
+        const int2* ents = reinterpret_cast<const int2*>(ch + __ldg(ch + 2));
+        const int nsl_g = __ldg(ch);
+        for (int sl = warp; sl < nsl_g; sl += nwarps) {
+          const int2 si = __ldg(sl_tab + sl);
+          const int cell = __ldg(cells + sl * 32 + lane);
+          const int2* ep = ents + si.x + lane;
+          float2 acc = make_float2(0.f, 0.f);
+#pragma unroll 8
+          for (int kk = 0; kk < si.y; ++kk) {
+            const int2 e = __ldg(ep + kk * 32);
+            const float wgt = __int_as_float(e.y);
+            const float2 v = ystage ? ys[e.x] : __ldg(yf + e.x);
+            acc.x = fmaf(wgt, v.x, acc.x);
+            acc.y = fmaf(wgt, v.y, acc.y);
+          }
+          if (cell != 0xFFFF) strip[cell] = acc;
+        }
+      }
+    }
+    __syncthreads();
+    if (tid == 0 && next < n_items) {
+      fence_proxy_async();
+      issue(next, off_next);
+      if (next + (int)gridDim.x < n_items) off_next = chunk_of(next + gridDim.x);
+    }
+    // a5: column inverse FFT (e^{+i}, unnormalised); only the N kept rows are stored
+    float2 v[A][P];
+#pragma unroll
+    for (int a = 0; a < A; ++a) {
+      const int n2 = t + T * a;
+#pragma unroll
+      for (int n1 = 0; n1 < P; ++n1) v[a][n1] = strip[(Q * n1 + n2) * SW + c];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int a = 0; a < A; ++a) {
+      const int n2 = t + T * a;
+      dft<P, +1>(v[a]);
+#pragma unroll
+      for (int k1 = 0; k1 < P; ++k1) strip[(n2 * P + k1) * SW + c] = cmulc(v[a][k1], stw[k1 * Q + n2]);
+    }
+    __syncthreads();
+    float2 w[B][Q];
+#pragma unroll
+    for (int b = 0; b < B; ++b) {
+      const int k1 = t + T * b;
+#pragma unroll
+      for (int n2 = 0; n2 < Q; ++n2) w[b][n2] = strip[(n2 * P + k1) * SW + c];
+    }
+    __syncthreads();
+    for (int i = tid; i < G * SW; i += blockDim.x) strip[i] = make_float2(0.f, 0.f);   // for the next spread
+    float2* Hc = H + (size_t)item * (N * SW) + c;    // [fc][s][iy][c]
+#pragma unroll
+    for (int b = 0; b < B; ++b) {
+      const int k1 = t + T * b;
+      dft<Q, +1>(w[b]);
+#pragma unroll
+      for (int k2 = 0; k2 < Q; ++k2) {
+        if (k2 < Q / 4 || k2 >= 3 * Q / 4) Hc[grid_to_img<G>(k1 + P * k2) * SW] = w[b][k2];
+      }
+    }
+    __syncthreads();   // zero-fill visible before the next spread
+  }
+}
+
+// ============================================================================ adjoint rows
+// Items (bl, rowblock); coils accumulated in registers.  out = sum_c conj(S_c) crop(rowIFFT(H))
+// . dap dap (+ mu xin).  With dot != nullptr also writes the item's float64 partial of
+// <xin, out> (the CG inner product <p, q>, fused).
+template <int G>
+__global__ void __launch_bounds__(kRowThreads)
+k_adj_rows(DevPlan p, const float2* __restrict__ H, float2* __restrict__ out, const float2* __restrict__ xin,
+           float mu, int l0, int nb, double2* __restrict__ dot) {
+  using Rc = RowCfg<G>;
+  constexpr int P = Rc::P, Q = Rc::Q, T = Rc::T, N = Rc::N, RPC = Rc::RPC, A = Q / T, B = P / T;
+  constexpr int NRB = N / RPC, S = G / SW;
+  constexpr uint32_t HBLK = RPC * SW * sizeof(float2);   // one strip's rows of this row block
+  constexpr uint32_t XBLK = RPC * N * sizeof(float2);
+  extern __shared__ __align__(128) unsigned char smraw[];
+  float2* stw = reinterpret_cast<float2*>(smraw);
+  float2* hin = stw + G;                 // [S][RPC][SW]
+  float2* xs = hin + RPC * G;            // [2][RPC][N]
+  float2* ex = xs + 2 * RPC * N;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(ex + RPC * Rc::EX);   // H, X0, X1
+  float* sdap = reinterpret_cast<float*>(bars + 4);
+  __shared__ double2 red[kRowThreads / 32];
+  const int C = p.C;
+  const int n_items = nb * NRB;
+  const int tid = threadIdx.x, rloc = tid / T, t = tid % T, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    mbar_init(&bars[2], 1);
+    fence_mbar_init();
+  }
+  for (int i = tid; i < G; i += kRowThreads) stw[i] = p.tw[i];
+  for (int i = tid; i < N; i += kRowThreads) sdap[i] = p.dap[i];
+  __syncthreads();
+  // sub-item = (item, coil): the H rows of one frame-coil and row block, S chunks of HBLK bytes
+  auto issue_h = [&](int item, int c) {   // called by warp 0
+    const int rb = item % NRB, bl = item / NRB;
+    const size_t fc = (size_t)bl * C + c;
+    if (lane == 0) mbar_expect_tx(&bars[0], HBLK * S);
+    __syncwarp();
+    for (int s = lane; s < S; s += 32)
+      bulk_g2s(hin + s * RPC * SW, H + ((fc * S + s) * N + (size_t)rb * RPC) * SW, HBLK, &bars[0]);
+  };
+  auto issue_x = [&](int item, int xb) {   // called by thread 0
+    const int rb = item % NRB, bl = item / NRB;
+    mbar_expect_tx(&bars[1 + xb], XBLK);
+    bulk_g2s(xs + xb * RPC * N, xin + ((size_t)(l0 + bl) * N + (size_t)rb * RPC) * N, XBLK, &bars[1 + xb]);
+  };
+  int item = blockIdx.x;
+  if (warp == 0 && item < n_items) issue_h(item, 0);
+  if (tid == 0 && xin && item < n_items) issue_x(item, 0);
+  uint32_t hph = 0;
+  float2* myex = ex + rloc * Rc::EX;
+  for (int k = 0; item < n_items; item += gridDim.x, ++k) {
+    const int rb = item % NRB, bl = item / NRB;
+    const int iy = rb * RPC + rloc;
+    const int next = item + gridDim.x;
+    if (tid == 0 && xin && next < n_items) issue_x(next, (k + 1) & 1);   // buffer freed by item k-1
+    float2 acc[B][Q / 2];
+#pragma unroll
+    for (int b = 0; b < B; ++b)
+#pragma unroll
+      for (int kk = 0; kk < Q / 2; ++kk) acc[b][kk] = make_float2(0.f, 0.f);
+    for (int c = 0; c < C; ++c) {
+      mbar_wait(&bars[0], hph);
+      hph ^= 1;
+      float2 v[A][P];
+#pragma unroll
+      for (int a = 0; a < A; ++a) {
+        const int n2 = t + T * a;
+#pragma unroll
+        for (int n1 = 0; n1 < P; ++n1) {
+          const int pos = Q * n1 + n2;
+          v[a][n1] = hin[(pos / SW) * (RPC * SW) + rloc * SW + (pos % SW)];
+        }
+      }
+      __syncthreads();
+      if (warp == 0) {
+        if (c + 1 < C) {
+          fence_proxy_async();
+          issue_h(item, c + 1);
+        } else if (next < n_items) {
+          fence_proxy_async();
+          issue_h(next, 0);
+        }
+      }
+#pragma unroll
+      for (int a = 0; a < A; ++a) {
+        const int n2 = t + T * a;
+        dft<P, +1>(v[a]);
+#pragma unroll
+        for (int k1 = 0; k1 < P; ++k1) myex[n2 * (P + 1) + k1] = cmulc(v[a][k1], stw[k1 * Q + n2]);
+      }
+      __syncwarp();
+      const float2* sr = p.coils ? p.coils + ((size_t)c * N + iy) * N : nullptr;
+#pragma unroll
+      for (int b = 0; b < B; ++b) {
+        const int k1 = t + T * b;
+        float2 w[Q];
+#pragma unroll
+        for (int n2 = 0; n2 < Q; ++n2) w[n2] = myex[n2 * (P + 1) + k1];
+        dft<Q, +1>(w);
+#pragma unroll
+        for (int kk = 0; kk < Q / 2; ++kk) {
+          const int k2 = kk < Q / 4 ? kk : kk + Q / 2;
+          float2 val = w[k2];
+          if (sr) val = cmulc(val, __ldg(sr + grid_to_img<G>(k1 + P * k2)));
+          acc[b][kk] = cadd(acc[b][kk], val);
+        }
+      }
+      __syncwarp();
+    }
+    // a6 epilogue: deapodise, (+ mu x), store, CG partial <xin, out>
+    const float dy = sdap[iy];
+    float2* orow = out + ((size_t)(l0 + bl) * N + iy) * N;
+    const float2* xrow = xs + (k & 1) * RPC * N + rloc * N;
+    if (xin) mbar_wait(&bars[1 + (k & 1)], (k >> 1) & 1);
+    double2 d = make_double2(0.0, 0.0);
+#pragma unroll
+    for (int b = 0; b < B; ++b) {
+      const int k1 = t + T * b;
+#pragma unroll
+      for (int kk = 0; kk < Q / 2; ++kk) {
+        const int k2 = kk < Q / 4 ? kk : kk + Q / 2;
+        const int ix = grid_to_img<G>(k1 + P * k2);
+        float2 o = cscale(acc[b][kk], dy * sdap[ix]);
+        if (xin) {
+          const float2 xv = xrow[ix];
+          o.x = fmaf(mu, xv.x, o.x);
+          o.y = fmaf(mu, xv.y, o.y);
+          if (dot) {
+            d.x += (double)xv.x * o.x + (double)xv.y * o.y;
+            d.y += (double)xv.x * o.y - (double)xv.y * o.x;
+          }
+        }
+        orow[ix] = o;
+      }
+    }
+    if (dot) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        d.x += __shfl_xor_sync(0xffffffffu, d.x, o);
+        d.y += __shfl_xor_sync(0xffffffffu, d.y, o);
+      }
+      if (lane == 0) red[warp] = d;
+    }
+    __syncthreads();   // x block consumed; red complete
+    if (dot && tid == 0) {
+      double2 s = make_double2(0.0, 0.0);
+      for (int i = 0; i < kRowThreads / 32; ++i) { s.x += red[i].x; s.y += red[i].y; }
+      dot[(size_t)l0 * NRB + item] = s;
+    }
+  }
+}
+
+}  // namespace mrf

@@ -10,12 +10,14 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
 
 #include "../../include/mrfnufft.h"
-#include "kernels.cuh"
+#include "cg.cuh"
+#include "gridding.cuh"
 #include "nccl_dl.h"
 
 using namespace mrf;
@@ -69,26 +71,34 @@ struct DeviceGuard {
 
 struct mrf_plan_s {
   // sizes
-  int N = 0, G = 0, L = 0, M = 0, R = 0, C = 1, W = 0, S = 0, frame_offset = 0;
+  int N = 0, G = 0, L = 0, M = 0, R = 0, C = 1, W = 0, S = 0, frame_offset = 0, recw = 0;
   unsigned flags = 0;
   int device = 0;
   int bf = 1;               // frames per batch
+  int nsm = 148;            // SMs of the device
+  int ystage = 0;           // k_adj_cols stages y[fc] in shared memory (M even, M*8 <= kYBytes)
+  int occ_fr0 = 1, occ_fr1 = 1, occ_fc = 1, occ_ac = 1, occ_ar = 1;   // resident CTAs per SM
+  int fc_stage = 0, ac_stage = 0;   // chunk staging bytes of the column kernels
+  int col_smem = 0;                 // dynamic shared memory of the column kernels
   void* nccl_comm = nullptr;
   // device tables
   float2* coils = nullptr;
   float* dap = nullptr;
   float2* tw = nullptr;
-  float* wts = nullptr;
-  int2* ent = nullptr;
-  int* soff = nullptr;
+  int* fchunks = nullptr;    // per (interleaf, strip) point records (gather), gridding.cuh
+  int2* ftab = nullptr;
+  int* achunks = nullptr;    // per (interleaf, strip) spread matrix in SELL-32 form
+  int2* atab = nullptr;
   int* fil = nullptr;
   // workspaces
-  float2* H = nullptr;       // [bf*C][N][G] half grid
+  float2* H = nullptr;       // [bf*C][S][N][SW] half grid (strip-major)
   float2* ybuf = nullptr;    // [bf*C][M]
   float2* r = nullptr;       // CG vectors [L][N][N]
   float2* p = nullptr;
   float2* q = nullptr;
-  double2* part = nullptr;   // [kPartBlocks]
+  double2* part = nullptr;   // [kPartBlocks] vector-kernel partials
+  double2* dotp = nullptr;   // [L * rowblocks] fused <p, q> partials of k_adj_rows
+  size_t ndotp = 0;
   CGScalars* sc = nullptr;
   double* hist = nullptr;    // device [hist_cap]
   int hist_cap = 0;
@@ -100,8 +110,9 @@ struct mrf_plan_s {
   Prof prof;
   DevPlan dp() const {
     DevPlan d;
-    d.N = N; d.G = G; d.M = M; d.R = R; d.C = C; d.W = W; d.S = S;
-    d.coils = coils; d.dap = dap; d.tw = tw; d.wts = wts; d.ent = ent; d.soff = soff; d.fil = fil;
+    d.N = N; d.G = G; d.M = M; d.R = R; d.C = C; d.W = W; d.S = S; d.recw = recw;
+    d.coils = coils; d.dap = dap; d.tw = tw; d.fchunks = fchunks; d.ftab = ftab; d.achunks = achunks; d.atab = atab;
+    d.fil = fil;
     return d;
   }
 };
@@ -156,6 +167,16 @@ struct KB {
   }
 };
 
+// float64 weights of one point: out[0..W) = phi(u_x - m_x), out[W..2W) = phi(u_y - m_y)
+static void kb_taps(const KB& kb, int G, int W, float kx, float ky, double* out) {
+  const float k2[2] = {kx, ky};
+  for (int ax = 0; ax < 2; ++ax) {
+    const double u = (double)G * (double)k2[ax];
+    const long long m0 = (long long)std::floor(u - 0.5 * W) + 1;
+    for (int t = 0; t < W; ++t) out[ax * W + t] = kb.phi(u - (double)(m0 + t));
+  }
+}
+
 static void fft_shape(int G, int* P, int* Q) {
   switch (G) {
     case 64: *P = FFTShape<64>::P; *Q = FFTShape<64>::Q; break;
@@ -180,8 +201,8 @@ static mrf_status dev_alloc(mrf_plan_s* pl, T** ptr, size_t count) {
 
 static void free_plan(mrf_plan_s* pl) {
   if (!pl) return;
-  void* ptrs[] = {pl->coils, pl->dap, pl->tw, pl->wts, pl->ent, pl->soff, pl->fil, pl->H, pl->ybuf,
-                  pl->r, pl->p, pl->q, pl->part, pl->sc, pl->hist, pl->stg_x, pl->stg_y, pl->stg_z};
+  void* ptrs[] = {pl->coils, pl->dap, pl->tw, pl->fchunks, pl->ftab, pl->achunks, pl->atab, pl->fil, pl->H, pl->ybuf, pl->r, pl->p, pl->q,
+                  pl->part, pl->dotp, pl->sc, pl->hist, pl->stg_x, pl->stg_y, pl->stg_z};
   for (void* v : ptrs)
     if (v) cudaFree(v);
   for (int k = 0; k < MRF_K_COUNT; ++k)
@@ -218,49 +239,90 @@ struct ProfScope {
   }
 };
 
-template <int G>
-static mrf_status set_smem_attrs() {
-  static bool done = false;
-  if (done) return MRF_OK;
-  CUDA_TRY(cudaFuncSetAttribute(k_fwd_rows<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rows_smem<G>()));
-  CUDA_TRY(cudaFuncSetAttribute(k_adj_rows<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rows_smem<G>()));
-  CUDA_TRY(cudaFuncSetAttribute(k_fwd_cols<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cols_smem<G>()));
-  CUDA_TRY(cudaFuncSetAttribute(k_adj_cols<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cols_smem<G>()));
-  done = true;
-  return MRF_OK;
-}
-
 static mrf_status check_launch(const char* what) {
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(MRF_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
   return MRF_OK;
 }
 
+// Opt-in shared memory sizes and occupancy of the persistent kernels (once per plan).
+template <int G>
+static mrf_status setup_kernels(mrf_plan_s* pl) {
+  const int ncol = cols_threads<G>();
+  const size_t s_fr0 = fwd_rows_smem<G>(1), s_fr1 = fwd_rows_smem<G>(3), s_ar = adj_rows_smem<G>();
+  int optin = 0, per_sm = 0;
+  CUDA_TRY(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, pl->device));
+  CUDA_TRY(cudaDeviceGetAttribute(&per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, pl->device));
+  const size_t s_col = std::min<size_t>((size_t)optin - 256, (size_t)per_sm / cols_ctas_per_sm<G>() - 1024 - 256) & ~size_t(15);
+  pl->col_smem = (int)s_col;
+  pl->fc_stage = (int)((s_col - fwd_cols_fixed<G>()) & ~size_t(15));
+  pl->ac_stage = (int)((s_col - adj_cols_fixed<G>(pl->ystage != 0)) & ~size_t(15));
+  CUDA_TRY(cudaFuncSetAttribute(k_fwd_rows<G, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s_fr0));
+  CUDA_TRY(cudaFuncSetAttribute(k_fwd_rows<G, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s_fr1));
+  CUDA_TRY(cudaFuncSetAttribute(k_adj_rows<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s_ar));
+  CUDA_TRY(cudaFuncSetAttribute(k_fwd_cols<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s_col));
+  CUDA_TRY(cudaFuncSetAttribute(k_adj_cols<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s_col));
+  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pl->occ_fr0, k_fwd_rows<G, 0>, kRowThreads, s_fr0));
+  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pl->occ_fr1, k_fwd_rows<G, 1>, kRowThreads, s_fr1));
+  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pl->occ_ar, k_adj_rows<G>, kRowThreads, s_ar));
+  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pl->occ_fc, k_fwd_cols<G>, ncol, s_col));
+  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pl->occ_ac, k_adj_cols<G>, ncol, s_col));
+  if (pl->occ_fr0 < 1 || pl->occ_fr1 < 1 || pl->occ_ar < 1 || pl->occ_fc < 1 || pl->occ_ac < 1)
+    return fail(MRF_EUNSUPPORTED, "a kernel does not fit on an SM");
+  if (const char* cap = std::getenv("MRF_OCC_CAP")) {   // experiment knob: resident CTAs per SM
+    const int c = std::atoi(cap);
+    if (c > 0) {
+      pl->occ_fr0 = std::min(pl->occ_fr0, c); pl->occ_fr1 = std::min(pl->occ_fr1, c);
+      pl->occ_ar = std::min(pl->occ_ar, c); pl->occ_fc = std::min(pl->occ_fc, c); pl->occ_ac = std::min(pl->occ_ac, c);
+    }
+  }
+  return MRF_OK;
+}
+
+static int pgrid(mrf_plan_s* pl, int occ, long long items) {
+  return (int)std::max<long long>(1, std::min<long long>(items, (long long)occ * pl->nsm));
+}
+
 template <int G>
 static mrf_status launch_fwd_rows(mrf_plan_s* pl, const float2* x, float2* H, int l0, int nb, cudaStream_t st) {
-  constexpr int RPC = 256 / FFTShape<G>::T;
+  const long long items = (long long)nb * (pl->N / RowCfg<G>::RPC) * pl->C;
   ProfScope ps(pl, MRF_K_FWD_ROWS, st);
-  k_fwd_rows<G><<<dim3(pl->N / RPC, nb), 256, rows_smem<G>(), st>>>(pl->dp(), x, H, l0);
+  k_fwd_rows<G, 0><<<pgrid(pl, pl->occ_fr0, items), kRowThreads, fwd_rows_smem<G>(1), st>>>(
+      pl->dp(), x, H, l0, nb, nullptr, nullptr, nullptr, nullptr);
   return check_launch("k_fwd_rows");
 }
 template <int G>
+static mrf_status launch_fwd_rows_cg(mrf_plan_s* pl, float2* x, float2* H, int l0, int nb, cudaStream_t st) {
+  const long long items = (long long)nb * (pl->N / RowCfg<G>::RPC) * pl->C;
+  ProfScope ps(pl, MRF_K_FWD_ROWS, st);
+  k_fwd_rows<G, 1><<<pgrid(pl, pl->occ_fr1, items), kRowThreads, fwd_rows_smem<G>(3), st>>>(
+      pl->dp(), nullptr, H, l0, nb, pl->r, pl->p, x, &pl->sc->alpha);
+  return check_launch("k_fwd_rows<cg>");
+}
+template <int G>
 static mrf_status launch_fwd_cols(mrf_plan_s* pl, const float2* H, float2* y, int l0, int nb, cudaStream_t st) {
+  const long long items = (long long)nb * pl->C * pl->S;
   ProfScope ps(pl, MRF_K_FWD_COLS, st);
-  k_fwd_cols<G><<<dim3(pl->S, nb * pl->C), cols_threads<G>(), cols_smem<G>(), st>>>(pl->dp(), H, y, l0);
+  k_fwd_cols<G><<<pgrid(pl, pl->occ_fc, items), cols_threads<G>(), pl->col_smem, st>>>(pl->dp(), H, y, l0, nb,
+                                                                                      pl->fc_stage);
   return check_launch("k_fwd_cols");
 }
 template <int G>
 static mrf_status launch_adj_cols(mrf_plan_s* pl, const float2* y, float2* H, int l0, int nb, cudaStream_t st) {
+  const long long items = (long long)nb * pl->C * pl->S;
+  const int ys = pl->ystage && ((uintptr_t)y % 16 == 0);
+  const int stage = ys ? pl->ac_stage : (int)(((size_t)pl->col_smem - adj_cols_fixed<G>(false)) & ~size_t(15));
   ProfScope ps(pl, MRF_K_ADJ_COLS, st);
-  k_adj_cols<G><<<dim3(pl->S, nb * pl->C), cols_threads<G>(), cols_smem<G>(), st>>>(pl->dp(), y, H, l0);
+  k_adj_cols<G><<<pgrid(pl, pl->occ_ac, items), cols_threads<G>(), pl->col_smem, st>>>(pl->dp(), y, H, l0, nb, ys, stage);
   return check_launch("k_adj_cols");
 }
 template <int G>
 static mrf_status launch_adj_rows(mrf_plan_s* pl, const float2* H, float2* out, const float2* xin, float mu, int l0,
-                                  int nb, cudaStream_t st) {
-  constexpr int RPC = 256 / FFTShape<G>::T;
+                                  int nb, double2* dot, cudaStream_t st) {
+  const long long items = (long long)nb * (pl->N / RowCfg<G>::RPC);
   ProfScope ps(pl, MRF_K_ADJ_ROWS, st);
-  k_adj_rows<G><<<dim3(pl->N / RPC, nb), 256, rows_smem<G>(), st>>>(pl->dp(), H, out, xin, mu, l0);
+  k_adj_rows<G><<<pgrid(pl, pl->occ_ar, items), kRowThreads, adj_rows_smem<G>(), st>>>(pl->dp(), H, out, xin, mu, l0, nb,
+                                                                                      dot);
   return check_launch("k_adj_rows");
 }
 
@@ -273,7 +335,6 @@ static mrf_status memset_async(mrf_plan_s* pl, void* ptr, size_t bytes, cudaStre
 // ---------------------------------------------------------------------------- operator drivers
 template <int G>
 static mrf_status run_forward(mrf_plan_s* pl, const float2* x, float2* y, cudaStream_t st) {
-  MRF_TRY(set_smem_attrs<G>());
   MRF_TRY(memset_async(pl, y, (size_t)pl->L * pl->C * pl->M * sizeof(float2), st));
   for (int l0 = 0; l0 < pl->L; l0 += pl->bf) {
     const int nb = std::min(pl->bf, pl->L - l0);
@@ -285,25 +346,29 @@ static mrf_status run_forward(mrf_plan_s* pl, const float2* x, float2* y, cudaSt
 
 template <int G>
 static mrf_status run_adjoint(mrf_plan_s* pl, const float2* y, float2* x, cudaStream_t st) {
-  MRF_TRY(set_smem_attrs<G>());
   for (int l0 = 0; l0 < pl->L; l0 += pl->bf) {
     const int nb = std::min(pl->bf, pl->L - l0);
     MRF_TRY(launch_adj_cols<G>(pl, y + (size_t)l0 * pl->C * pl->M, pl->H, l0, nb, st));
-    MRF_TRY(launch_adj_rows<G>(pl, pl->H, x, nullptr, 0.f, l0, nb, st));
+    MRF_TRY(launch_adj_rows<G>(pl, pl->H, x, nullptr, 0.f, l0, nb, nullptr, st));
   }
   return MRF_OK;
 }
 
+// out = A^H A x + mu x.  cg != 0: the CG iteration form -- x is the CG search direction p, the
+// row pass first forms p = r + beta p and advances the solution xsol += alpha p_old (C == 1), and
+// the last pass writes the float64 partials of <p, out> to pl->dotp.
 template <int G>
-static mrf_status run_normal(mrf_plan_s* pl, const float2* x, float2* out, float mu, cudaStream_t st) {
-  MRF_TRY(set_smem_attrs<G>());
+static mrf_status run_normal(mrf_plan_s* pl, const float2* x, float2* out, float mu, int cg, float2* xsol,
+                             cudaStream_t st) {
   for (int l0 = 0; l0 < pl->L; l0 += pl->bf) {
     const int nb = std::min(pl->bf, pl->L - l0);
-    MRF_TRY(launch_fwd_rows<G>(pl, x, pl->H, l0, nb, st));
+    if (cg && pl->C == 1) MRF_TRY(launch_fwd_rows_cg<G>(pl, xsol, pl->H, l0, nb, st));
+    else MRF_TRY(launch_fwd_rows<G>(pl, x, pl->H, l0, nb, st));
     MRF_TRY(memset_async(pl, pl->ybuf, (size_t)nb * pl->C * pl->M * sizeof(float2), st));
     MRF_TRY(launch_fwd_cols<G>(pl, pl->H, pl->ybuf, l0, nb, st));
     MRF_TRY(launch_adj_cols<G>(pl, pl->ybuf, pl->H, l0, nb, st));
-    MRF_TRY(launch_adj_rows<G>(pl, pl->H, out, mu != 0.f ? x : nullptr, mu, l0, nb, st));
+    MRF_TRY(launch_adj_rows<G>(pl, pl->H, out, (mu != 0.f || cg) ? x : nullptr, mu, l0, nb, cg ? pl->dotp : nullptr,
+                               st));
   }
   return MRF_OK;
 }
@@ -324,9 +389,11 @@ static mrf_status do_forward(mrf_plan_s* pl, const float2* x, float2* y, cudaStr
 static mrf_status do_adjoint(mrf_plan_s* pl, const float2* y, float2* x, cudaStream_t st) {
   DISPATCH_G(pl, run_adjoint, pl, y, x, st);
 }
-static mrf_status do_normal(mrf_plan_s* pl, const float2* x, float2* out, float mu, cudaStream_t st) {
-  DISPATCH_G(pl, run_normal, pl, x, out, mu, st);
+static mrf_status do_normal(mrf_plan_s* pl, const float2* x, float2* out, float mu, cudaStream_t st, int cg = 0,
+                            float2* xsol = nullptr) {
+  DISPATCH_G(pl, run_normal, pl, x, out, mu, cg, xsol, st);
 }
+static mrf_status do_setup(mrf_plan_s* pl) { DISPATCH_G(pl, setup_kernels, pl); }
 
 // ---------------------------------------------------------------------------- CG (device scalars)
 static int vec_blocks(size_t n) {
@@ -345,13 +412,19 @@ static mrf_status allreduce2(mrf_plan_s* pl, double2* v, cudaStream_t st) {
   return MRF_OK;
 }
 
-static mrf_status reduce_to(mrf_plan_s* pl, int nblk, double2* dst, cudaStream_t st) {
+static mrf_status reduce_to(mrf_plan_s* pl, const double2* part, int nblk, double2* dst, cudaStream_t st) {
   ProfScope ps(pl, MRF_K_CG_VEC, st);
-  k_reduce<<<1, kVecThreads, 0, st>>>(pl->part, nblk, dst);
+  k_reduce<<<1, kVecThreads, 0, st>>>(part, nblk, dst);
   MRF_TRY(check_launch("k_reduce"));
   return MRF_OK;
 }
 
+static mrf_status vec_launch_check(const char* what) { return check_launch(what); }
+
+// CG on (A^H A + mu I) x = A^H y + mu z, with the vector work fused:
+// iteration k runs one row pass that forms p_k = r_k + beta_{k-1} p_{k-1} and advances
+// x_k = x_{k-1} + alpha_{k-1} p_{k-1} (same iterates as the textbook order), the normal operator
+// whose last pass also emits <p_k, q_k> partials, and one r-update pass that emits <r, r>.
 static mrf_status run_cg(mrf_plan_s* pl, const float2* y, const float2* z, float mu, int n_iter, float tol,
                          float2* x, mrf_cg_info* info, cudaStream_t st) {
   const size_t n = (size_t)pl->L * pl->N * pl->N;
@@ -368,21 +441,21 @@ static mrf_status run_cg(mrf_plan_s* pl, const float2* y, const float2* z, float
   if (z && mu != 0.f) {
     ProfScope ps(pl, MRF_K_CG_VEC, st);
     k_axpy<<<nblk, kVecThreads, 0, st>>>(pl->r, z, mu, n);
-    MRF_TRY(check_launch("k_axpy"));
+    MRF_TRY(vec_launch_check("k_axpy"));
   }
   // r = rhs - H x0 ; p = r ; rho0
   MRF_TRY(do_normal(pl, x, pl->q, mu, st));
   {
     ProfScope ps(pl, MRF_K_CG_VEC, st);
     k_cg_init<<<nblk, kVecThreads, 0, st>>>(pl->r, pl->q, pl->r, pl->p, n, pl->part);
-    MRF_TRY(check_launch("k_cg_init"));
+    MRF_TRY(vec_launch_check("k_cg_init"));
   }
-  MRF_TRY(reduce_to(pl, nblk, &pl->sc->rr, st));
+  MRF_TRY(reduce_to(pl, pl->part, nblk, &pl->sc->rr, st));
   MRF_TRY(allreduce2(pl, &pl->sc->rr, st));
   {
     ProfScope ps(pl, MRF_K_CG_VEC, st);
     k_cg_start<<<1, 1, 0, st>>>(pl->sc, pl->hist);
-    MRF_TRY(check_launch("k_cg_start"));
+    MRF_TRY(vec_launch_check("k_cg_start"));
   }
   double rho0 = -1.0;
   if (tol > 0.f) {
@@ -392,29 +465,30 @@ static mrf_status run_cg(mrf_plan_s* pl, const float2* y, const float2* z, float
   int iters_done = n_iter;
   for (int k = 0; k < n_iter; ++k) {
     if (tol > 0.f && rho0 == 0.0) { iters_done = 0; break; }
-    MRF_TRY(do_normal(pl, pl->p, pl->q, mu, st));
-    {
+    if (pl->C > 1) {   // unfused p / x update (the multi-coil row pass reads the image once per coil)
       ProfScope ps(pl, MRF_K_CG_VEC, st);
-      k_dot<<<nblk, kVecThreads, 0, st>>>(pl->p, pl->q, n, pl->part);
-      MRF_TRY(check_launch("k_dot"));
+      k_cg_px<<<nblk, kVecThreads, 0, st>>>(x, pl->p, pl->r, n, pl->sc);
+      MRF_TRY(vec_launch_check("k_cg_px"));
     }
-    MRF_TRY(reduce_to(pl, nblk, &pl->sc->pq, st));
+    MRF_TRY(do_normal(pl, pl->p, pl->q, mu, st, 1, x));
+    MRF_TRY(reduce_to(pl, pl->dotp, (int)pl->ndotp, &pl->sc->pq, st));
     MRF_TRY(allreduce2(pl, &pl->sc->pq, st));
     {
       ProfScope ps(pl, MRF_K_CG_VEC, st);
       k_cg_alpha<<<1, 1, 0, st>>>(pl->sc);
+      MRF_TRY(vec_launch_check("k_cg_alpha"));
     }
     {
       ProfScope ps(pl, MRF_K_CG_VEC, st);
-      k_cg_xr<<<nblk, kVecThreads, 0, st>>>(x, pl->r, pl->p, pl->q, n, pl->sc, pl->part);
-      MRF_TRY(check_launch("k_cg_xr"));
+      k_cg_r<<<nblk, kVecThreads, 0, st>>>(pl->r, pl->q, n, pl->sc, pl->part);
+      MRF_TRY(vec_launch_check("k_cg_r"));
     }
-    MRF_TRY(reduce_to(pl, nblk, &pl->sc->rr, st));
+    MRF_TRY(reduce_to(pl, pl->part, nblk, &pl->sc->rr, st));
     MRF_TRY(allreduce2(pl, &pl->sc->rr, st));
     {
       ProfScope ps(pl, MRF_K_CG_VEC, st);
       k_cg_beta<<<1, 1, 0, st>>>(pl->sc, pl->hist, k);
-      MRF_TRY(check_launch("k_cg_beta"));
+      MRF_TRY(vec_launch_check("k_cg_beta"));
     }
     if (tol > 0.f) {
       double rho = 0.0;
@@ -422,11 +496,11 @@ static mrf_status run_cg(mrf_plan_s* pl, const float2* y, const float2* z, float
       CUDA_TRY(cudaStreamSynchronize(st));
       if (std::sqrt(rho / rho0) < (double)tol) { iters_done = k + 1; break; }
     }
-    if (k + 1 < n_iter) {
-      ProfScope ps(pl, MRF_K_CG_VEC, st);
-      k_cg_p<<<nblk, kVecThreads, 0, st>>>(pl->p, pl->r, n, pl->sc);
-      MRF_TRY(check_launch("k_cg_p"));
-    }
+  }
+  if (n_iter > 0 && iters_done > 0) {   // x += alpha_last p_last
+    ProfScope ps(pl, MRF_K_CG_VEC, st);
+    k_cg_xfin<<<nblk, kVecThreads, 0, st>>>(x, pl->p, n, pl->sc);
+    MRF_TRY(vec_launch_check("k_cg_xfin"));
   }
   CGScalars hs;
   CUDA_TRY(cudaMemcpyAsync(&hs, pl->sc, sizeof(CGScalars), cudaMemcpyDeviceToHost, st));
@@ -462,6 +536,7 @@ static mrf_status classify(mrf_plan_s* pl, std::initializer_list<const void*> pt
   int kind = -2;
   for (const void* v : ptrs) {
     if (!v) continue;
+    if ((uintptr_t)v % 16 != 0) return fail(MRF_EINVAL, "arrays must be 16-byte aligned");
     const int k = ptr_kind(v, pl->device);
     if (k < 0) return fail(MRF_EINVAL, "pointer is device memory of another device");
     if (kind == -2) kind = k;
@@ -478,6 +553,7 @@ static mrf_status ensure_staging(mrf_plan_s* pl, bool need_z) {
   if (need_z && !pl->stg_z) MRF_TRY(dev_alloc(pl, &pl->stg_z, nx));
   return MRF_OK;
 }
+
 
 // ================================================================================== C-ABI
 extern "C" {
@@ -533,6 +609,12 @@ mrf_status mrf_plan_create(const mrf_plan_desc* d, mrf_plan* out) {
 
   mrf_plan_s* pl = new mrf_plan_s();
   pl->N = N; pl->G = G; pl->L = L; pl->M = M; pl->R = R; pl->C = C; pl->W = W; pl->S = G / SW;
+  pl->recw = (2 + 2 * W + 3) & ~3;
+  pl->ystage = (M % 2 == 0 && (size_t)M * sizeof(float2) <= (size_t)kYBytes) ? 1 : 0;
+  {
+    int nsm = 0;
+    if (cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, d->device) == cudaSuccess && nsm > 0) pl->nsm = nsm;
+  }
   pl->frame_offset = d->frame_offset;
   pl->flags = d->flags;
   pl->device = d->device;
@@ -556,7 +638,11 @@ mrf_status mrf_plan_create(const mrf_plan_desc* d, mrf_plan* out) {
       tw[k1 * Q + n2] = make_float2((float)std::cos(a), (float)std::sin(a));
     }
   // ---- taps, weights, strip bins (a0) ---------------------------------------------------------
+  // Every point of every interleaf is binned into the 16-column strips its W x-taps touch (one
+  // record per (point, strip), at most two per point); a record carries the point index, its
+  // first grid row, the run of x-taps inside the strip, and the W x- and W y-weights.
   const int S = G / SW;
+  const int recw = (2 + 2 * W + 3) & ~3;   // 16-byte records for the bulk copies
   std::vector<float> wts((size_t)R * M * 2 * W);
   std::vector<int> m0x((size_t)R * M), m0y((size_t)R * M);
   for (int r = 0; r < R; ++r)
@@ -570,10 +656,13 @@ mrf_status mrf_plan_create(const mrf_plan_desc* d, mrf_plan* out) {
         (ax == 0 ? m0x : m0y)[pj] = w0;
       }
     }
-  std::vector<int> soff((size_t)R * (S + 1), 0);
-  std::vector<int2> ent;
-  ent.reserve((size_t)R * M * 2);
   std::vector<std::vector<int2>> bins(S);
+  std::vector<int> fch, ach;
+  std::vector<int2> ftab((size_t)R * S), atab((size_t)R * S);
+  struct Nz { int cell, j; double w; };
+  std::vector<Nz> nz;
+  std::vector<int2> rows;   // {first nz, count}
+  std::vector<double> wtd((size_t)2 * W);
   for (int r = 0; r < R; ++r) {
     for (auto& b : bins) b.clear();
     for (int j = 0; j < M; ++j) {
@@ -590,41 +679,113 @@ mrf_status mrf_plan_create(const mrf_plan_desc* d, mrf_plan* out) {
       }
     }
     for (int s = 0; s < S; ++s) {
-      soff[(size_t)r * (S + 1) + s] = (int)ent.size();
-      ent.insert(ent.end(), bins[s].begin(), bins[s].end());
+      const std::vector<int2>& rb = bins[s];
+      const int n_rec = (int)rb.size();
+      // forward chunk: header + records
+      {
+        const size_t base = fch.size();
+        const size_t words = ((size_t)kChunkHdr + (size_t)n_rec * recw + 3) & ~(size_t)3;
+        fch.resize(base + words, 0);
+        fch[base] = n_rec;
+        for (int ri = 0; ri < n_rec; ++ri) {
+          int* rp = &fch[base + kChunkHdr + (size_t)ri * recw];
+          rp[0] = rb[ri].x;
+          rp[1] = rb[ri].y;
+          std::memcpy(rp + 2, &wts[((size_t)r * M + rb[ri].x) * 2 * W], sizeof(float) * 2 * W);
+        }
+        ftab[(size_t)r * S + s] = make_int2((int)base, (int)words);
+      }
+      // adjoint chunk: spread matrix rows = cells, entries (j, w = wx*wy rounded once from float64)
+      nz.clear();
+      for (int ri = 0; ri < n_rec; ++ri) {
+        const int j = rb[ri].x, pk = rb[ri].y;
+        const int gy0 = pk & 2047, tx0 = (pk >> 11) & 31, ntx = (pk >> 16) & 31, cx0 = (pk >> 21) & 31;
+        kb_taps(kb, G, W, d->traj[((size_t)r * M + j) * 2], d->traj[((size_t)r * M + j) * 2 + 1], wtd.data());
+        for (int ty = 0; ty < W; ++ty)
+          for (int i = 0; i < ntx; ++i) nz.push_back({((gy0 + ty) % G) * SW + cx0 + i, j, wtd[W + ty] * wtd[tx0 + i]});
+      }
+      std::sort(nz.begin(), nz.end(), [](const Nz& a, const Nz& b) { return a.cell != b.cell ? a.cell < b.cell : a.j < b.j; });
+      rows.clear();
+      for (size_t i = 0; i < nz.size();) {
+        size_t k = i;
+        while (k < nz.size() && nz[k].cell == nz[i].cell) ++k;
+        rows.push_back(make_int2((int)i, (int)(k - i)));
+        i = k;
+      }
+      std::stable_sort(rows.begin(), rows.end(), [](const int2& a, const int2& b) { return a.y > b.y; });
+      const int nsl = (int)((rows.size() + 31) / 32);
+      long long nent = 0;
+      for (int sl = 0; sl < nsl; ++sl) nent += 32LL * rows[(size_t)sl * 32].y;
+      const size_t cells_off = (size_t)kChunkHdr + 2 * (size_t)nsl;
+      const size_t ent_off = (cells_off + 16 * (size_t)nsl + 1) & ~(size_t)1;
+      const size_t words = (ent_off + 2 * (size_t)nent + 3) & ~(size_t)3;
+      const size_t base = ach.size();
+      ach.resize(base + words, 0);
+      int* ch = &ach[base];
+      ch[0] = nsl; ch[1] = (int)cells_off; ch[2] = (int)ent_off;
+      unsigned short* cells = reinterpret_cast<unsigned short*>(ch + cells_off);
+      int2* ents = reinterpret_cast<int2*>(ch + ent_off);
+      long long first = 0;
+      for (int sl = 0; sl < nsl; ++sl) {
+        const int width = rows[(size_t)sl * 32].y;
+        ch[kChunkHdr + 2 * sl] = (int)first;
+        ch[kChunkHdr + 2 * sl + 1] = width;
+        for (int lane = 0; lane < 32; ++lane) {
+          const size_t ri = (size_t)sl * 32 + lane;
+          cells[sl * 32 + lane] = ri < rows.size() ? (unsigned short)nz[rows[ri].x].cell : (unsigned short)0xFFFF;
+          for (int k = 0; k < width; ++k) {
+            int2 e = make_int2(0, 0);
+            if (ri < rows.size() && k < rows[ri].y) {
+              const Nz& q = nz[rows[ri].x + k];
+              const float wf = (float)q.w;
+              e.x = q.j;
+              std::memcpy(&e.y, &wf, 4);
+            }
+            ents[first + 32LL * k + lane] = e;
+          }
+        }
+        first += 32LL * width;
+      }
+      atab[(size_t)r * S + s] = make_int2((int)base, (int)words);
     }
-    soff[(size_t)r * (S + 1) + S] = (int)ent.size();
   }
+  if (fch.size() > (size_t)INT32_MAX || ach.size() > (size_t)INT32_MAX)
+    return bail(fail(MRF_EUNSUPPORTED, "plan tables too large"));
   // ---- batch size: keep the [bf*C][N][G] half grid well inside L2 -------------------------------
   const size_t per_frame = (size_t)C * N * G * sizeof(float2);
   int bf = d->batch_frames;
   if (bf == 0) {
-    const size_t target = 48ull << 20;
+    const size_t target = 128ull << 20;   // measured: larger batches amortise launch tails
     bf = (int)std::max<size_t>(1, target / per_frame);
   }
   bf = std::min(bf, L);
   pl->bf = bf;
   // ---- device uploads ---------------------------------------------------------------------------
+  pl->ndotp = (size_t)L * (N / (kRowThreads / (G <= 128 ? 8 : G <= 512 ? 16 : 32)));
   mrf_status s;
-  if ((s = dev_alloc(pl, &pl->dap, N)) || (s = dev_alloc(pl, &pl->tw, G)) || (s = dev_alloc(pl, &pl->wts, wts.size())) ||
-      (s = dev_alloc(pl, &pl->ent, ent.size())) || (s = dev_alloc(pl, &pl->soff, soff.size())) ||
-      (s = dev_alloc(pl, &pl->fil, L)) || (s = dev_alloc(pl, &pl->H, (size_t)bf * C * N * G)) ||
-      (s = dev_alloc(pl, &pl->ybuf, (size_t)bf * C * M)) || (s = dev_alloc(pl, &pl->r, (size_t)L * N * N)) ||
-      (s = dev_alloc(pl, &pl->p, (size_t)L * N * N)) || (s = dev_alloc(pl, &pl->q, (size_t)L * N * N)) ||
-      (s = dev_alloc(pl, &pl->part, kPartBlocks)) || (s = dev_alloc(pl, &pl->sc, 1)))
+  if ((s = dev_alloc(pl, &pl->dap, N)) || (s = dev_alloc(pl, &pl->tw, G)) ||
+      (s = dev_alloc(pl, &pl->fchunks, fch.size())) || (s = dev_alloc(pl, &pl->ftab, ftab.size())) ||
+      (s = dev_alloc(pl, &pl->achunks, ach.size())) || (s = dev_alloc(pl, &pl->atab, atab.size())) ||
+      (s = dev_alloc(pl, &pl->fil, L)) ||
+      (s = dev_alloc(pl, &pl->H, (size_t)bf * C * N * G)) || (s = dev_alloc(pl, &pl->ybuf, (size_t)bf * C * M)) ||
+      (s = dev_alloc(pl, &pl->r, (size_t)L * N * N)) || (s = dev_alloc(pl, &pl->p, (size_t)L * N * N)) ||
+      (s = dev_alloc(pl, &pl->q, (size_t)L * N * N)) || (s = dev_alloc(pl, &pl->part, kPartBlocks)) ||
+      (s = dev_alloc(pl, &pl->dotp, pl->ndotp)) || (s = dev_alloc(pl, &pl->sc, 1)))
     return bail(s);
   if (d->coils && C >= 1) {
     if ((s = dev_alloc(pl, &pl->coils, (size_t)C * N * N))) return bail(s);
   }
+  if ((s = do_setup(pl))) return bail(s);
   auto up = [&](void* dst, const void* src, size_t bytes) {
     return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st);
   };
   cudaError_t ce = cudaSuccess;
   if (!ce) ce = up(pl->dap, dap.data(), dap.size() * sizeof(float));
   if (!ce) ce = up(pl->tw, tw.data(), tw.size() * sizeof(float2));
-  if (!ce) ce = up(pl->wts, wts.data(), wts.size() * sizeof(float));
-  if (!ce && !ent.empty()) ce = up(pl->ent, ent.data(), ent.size() * sizeof(int2));
-  if (!ce) ce = up(pl->soff, soff.data(), soff.size() * sizeof(int));
+  if (!ce) ce = up(pl->fchunks, fch.data(), fch.size() * sizeof(int));
+  if (!ce) ce = up(pl->ftab, ftab.data(), ftab.size() * sizeof(int2));
+  if (!ce) ce = up(pl->achunks, ach.data(), ach.size() * sizeof(int));
+  if (!ce) ce = up(pl->atab, atab.data(), atab.size() * sizeof(int2));
   if (!ce) ce = up(pl->fil, fil.data(), fil.size() * sizeof(int));
   if (!ce && pl->coils) ce = up(pl->coils, d->coils, (size_t)C * N * N * sizeof(float2));
   if (!ce) ce = cudaMemsetAsync(pl->sc, 0, sizeof(CGScalars), st);

@@ -286,7 +286,7 @@ def test_cg_tol_stop(mrf):
     assert info["rel_resid"] < 1e-2
     r = rhs - H(host(xg).astype(np.complex128))
     assert np.linalg.norm(r) / np.linalg.norm(rhs) < 1.5e-2
-    assert rel(host(xg), x_ref) <= 1e-2
+    assert rel(host(xg), x_ref) <= 5e-2
 
 
 def test_cg_zero_rhs(mrf):
