@@ -6,6 +6,8 @@
 //                k_fwd_cols  a2 column FFT of one 16-column strip, a3 KB gather interpolation
 //   adjoint A^H: k_adj_cols  a4 KB spread into the strip (shared memory), a5 column iFFT
 //                k_adj_rows  a5 row iFFTs, a6 crop . deapod . conj-coil . coil sum [+ mu x]
+// The forward half grid is strip-major ([fc][strip][row][16]: one strip = one bulk copy); the
+// adjoint half grid is row-major ([fc][row][G]: one row block = one bulk copy).
 //
 // Every kernel is persistent (grid = resident CTAs) and walks a list of work items.  The global
 // inputs of the NEXT item are fetched by the Tensor Memory Accelerator (cp.async.bulk, completion
@@ -424,6 +426,7 @@ k_adj_cols(DevPlan p, const float2* __restrict__ y, float2* __restrict__ H, int 
   uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<unsigned char*>(ys) + (ystage ? kYBytes : 0));
   int* stage = reinterpret_cast<int*>(bars + 2);
   __shared__ int copied;
+  __shared__ int chunk_off;   // word offset of the staged chunk (for its unstaged tail)
   const int C = p.C, M = p.M;
   const int n_items = nb * C * S;
   const int tid = threadIdx.x, c = tid % SW, t = tid / SW;
@@ -440,9 +443,10 @@ k_adj_cols(DevPlan p, const float2* __restrict__ y, float2* __restrict__ H, int 
     const int fc = item / S, s = item % S;
     return __ldg(p.atab + __ldg(p.fil + l0 + fc / C) * S + s);
   };
-  auto issue = [&](int item, int2 ow) {   // a chunk larger than the staging buffer is read from L2
-    const uint32_t bytes = ow.y * 4 <= stage_cap ? (uint32_t)ow.y * 4 : (uint32_t)kChunkHdr * 4;
+  auto issue = [&](int item, int2 ow) {   // the part of a chunk beyond the staging buffer is read from L2
+    const uint32_t bytes = (uint32_t)min(ow.y * 4, stage_cap) & ~15u;
     copied = (int)bytes;
+    chunk_off = ow.x;
     mbar_expect_tx(&bars[0], bytes + (ystage ? ybytes : 0));
     bulk_g2s(stage, p.achunks + ow.x, bytes, &bars[0]);
     if (ystage) bulk_g2s(ys, y + (size_t)(item / S) * M, ybytes, &bars[0]);
@@ -458,17 +462,21 @@ k_adj_cols(DevPlan p, const float2* __restrict__ y, float2* __restrict__ H, int 
     const int next = item + gridDim.x;
     mbar_wait(&bars[0], k & 1);
     {
+      // Staged prefix of the chunk: header, slice table and cells always fit (checked at plan
+      // time); a slice whose entries lie past the staged prefix reads them from L2.
       const int nsl = stage[0], cells_off = stage[1], ent_off = stage[2];
       const float2* yf = y + (size_t)fc * M;
-      if (copied > kChunkHdr * 4) {   // staged chunk: shared-memory loads only
-        const int2* sl_tab = reinterpret_cast<const int2*>(stage + kChunkHdr);
-        const unsigned short* cells = reinterpret_cast<const unsigned short*>(stage + cells_off);
-        const int2* ents = reinterpret_cast<const int2*>(stage + ent_off);
-        for (int sl = warp; sl < nsl; sl += nwarps) {
-          const int2 si = sl_tab[sl];
-          const int cell = cells[sl * 32 + lane];
+      const int2* sl_tab = reinterpret_cast<const int2*>(stage + kChunkHdr);
+      const unsigned short* cells = reinterpret_cast<const unsigned short*>(stage + cells_off);
+      const int2* ents = reinterpret_cast<const int2*>(stage + ent_off);
+      const int n_staged = (copied / 4 - ent_off) / 2;          // entries in shared memory
+      const int2* gents = reinterpret_cast<const int2*>(p.achunks + chunk_off + ent_off);
+      for (int sl = warp; sl < nsl; sl += nwarps) {
+        const int2 si = sl_tab[sl];
+        const int cell = cells[sl * 32 + lane];
+        float2 acc = make_float2(0.f, 0.f);
+        if (si.x + 32 * si.y <= n_staged) {
           const int2* ep = ents + si.x + lane;
-          float2 acc = make_float2(0.f, 0.f);
 #pragma unroll 8
           for (int kk = 0; kk < si.y; ++kk) {
             const int2 e = ep[kk * 32];
@@ -477,19 +485,8 @@ k_adj_cols(DevPlan p, const float2* __restrict__ y, float2* __restrict__ H, int 
             acc.x = fmaf(wgt, v.x, acc.x);
             acc.y = fmaf(wgt, v.y, acc.y);
           }
-          if (cell != 0xFFFF) strip[cell] = acc;
-        }
-      } else {                        // chunk too large to stage: read it in place from L2
-        const int* ch = p.achunks + chunk_of(item).x;
-        const int2* sl_tab = reinterpret_cast<const int2*>(ch + kChunkHdr);
-        const unsigned short* cells = reinterpret_cast<const unsigned short*>(ch + __ldg(ch + 1));
-        const int2* ents = reinterpret_cast<const int2*>(ch + __ldg(ch + 2));
-        const int nsl_g = __ldg(ch);
-        for (int sl = warp; sl < nsl_g; sl += nwarps) {
-          const int2 si = __ldg(sl_tab + sl);
-          const int cell = __ldg(cells + sl * 32 + lane);
-          const int2* ep = ents + si.x + lane;
-          float2 acc = make_float2(0.f, 0.f);
+        } else {
+          const int2* ep = gents + si.x + lane;
 #pragma unroll 8
           for (int kk = 0; kk < si.y; ++kk) {
             const int2 e = __ldg(ep + kk * 32);
@@ -498,8 +495,8 @@ k_adj_cols(DevPlan p, const float2* __restrict__ y, float2* __restrict__ H, int 
             acc.x = fmaf(wgt, v.x, acc.x);
             acc.y = fmaf(wgt, v.y, acc.y);
           }
-          if (cell != 0xFFFF) strip[cell] = acc;
         }
+        if (cell != 0xFFFF) strip[cell] = acc;
       }
     }
     __syncthreads();
@@ -534,14 +531,14 @@ k_adj_cols(DevPlan p, const float2* __restrict__ y, float2* __restrict__ H, int 
     }
     __syncthreads();
     for (int i = tid; i < G * SW; i += blockDim.x) strip[i] = make_float2(0.f, 0.f);   // for the next spread
-    float2* Hc = H + (size_t)item * (N * SW) + c;    // [fc][s][iy][c]
+    float2* Hc = H + (size_t)fc * N * G + (size_t)(item % S) * SW + c;    // row-major [fc][iy][G]
 #pragma unroll
     for (int b = 0; b < B; ++b) {
       const int k1 = t + T * b;
       dft<Q, +1>(w[b]);
 #pragma unroll
       for (int k2 = 0; k2 < Q; ++k2) {
-        if (k2 < Q / 4 || k2 >= 3 * Q / 4) Hc[grid_to_img<G>(k1 + P * k2) * SW] = w[b][k2];
+        if (k2 < Q / 4 || k2 >= 3 * Q / 4) Hc[(size_t)grid_to_img<G>(k1 + P * k2) * G] = w[b][k2];
       }
     }
     __syncthreads();   // zero-fill visible before the next spread
@@ -558,12 +555,12 @@ k_adj_rows(DevPlan p, const float2* __restrict__ H, float2* __restrict__ out, co
            float mu, int l0, int nb, double2* __restrict__ dot) {
   using Rc = RowCfg<G>;
   constexpr int P = Rc::P, Q = Rc::Q, T = Rc::T, N = Rc::N, RPC = Rc::RPC, A = Q / T, B = P / T;
-  constexpr int NRB = N / RPC, S = G / SW;
-  constexpr uint32_t HBLK = RPC * SW * sizeof(float2);   // one strip's rows of this row block
+  constexpr int NRB = N / RPC;
+  constexpr uint32_t HBLK = RPC * G * sizeof(float2);    // the row block of one frame-coil
   constexpr uint32_t XBLK = RPC * N * sizeof(float2);
   extern __shared__ __align__(128) unsigned char smraw[];
   float2* stw = reinterpret_cast<float2*>(smraw);
-  float2* hin = stw + G;                 // [S][RPC][SW]
+  float2* hin = stw + G;                 // [RPC][G]
   float2* xs = hin + RPC * G;            // [2][RPC][N]
   float2* ex = xs + 2 * RPC * N;
   uint64_t* bars = reinterpret_cast<uint64_t*>(ex + RPC * Rc::EX);   // H, X0, X1
@@ -582,13 +579,13 @@ k_adj_rows(DevPlan p, const float2* __restrict__ H, float2* __restrict__ out, co
   for (int i = tid; i < N; i += kRowThreads) sdap[i] = p.dap[i];
   __syncthreads();
   // sub-item = (item, coil): the H rows of one frame-coil and row block, S chunks of HBLK bytes
-  auto issue_h = [&](int item, int c) {   // called by warp 0
+  auto issue_h = [&](int item, int c) {   // called by warp 0: the row block is one contiguous copy
     const int rb = item % NRB, bl = item / NRB;
     const size_t fc = (size_t)bl * C + c;
-    if (lane == 0) mbar_expect_tx(&bars[0], HBLK * S);
-    __syncwarp();
-    for (int s = lane; s < S; s += 32)
-      bulk_g2s(hin + s * RPC * SW, H + ((fc * S + s) * N + (size_t)rb * RPC) * SW, HBLK, &bars[0]);
+    if (lane == 0) {
+      mbar_expect_tx(&bars[0], HBLK);
+      bulk_g2s(hin, H + (fc * N + (size_t)rb * RPC) * G, HBLK, &bars[0]);
+    }
   };
   auto issue_x = [&](int item, int xb) {   // called by thread 0
     const int rb = item % NRB, bl = item / NRB;
@@ -620,7 +617,7 @@ k_adj_rows(DevPlan p, const float2* __restrict__ H, float2* __restrict__ out, co
 #pragma unroll
         for (int n1 = 0; n1 < P; ++n1) {
           const int pos = Q * n1 + n2;
-          v[a][n1] = hin[(pos / SW) * (RPC * SW) + rloc * SW + (pos % SW)];
+          v[a][n1] = hin[rloc * G + pos];
         }
       }
       __syncthreads();

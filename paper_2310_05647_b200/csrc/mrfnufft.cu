@@ -91,8 +91,13 @@ struct mrf_plan_s {
   int2* atab = nullptr;
   int* fil = nullptr;
   // workspaces
-  float2* H = nullptr;       // [bf*C][S][N][SW] half grid (strip-major)
-  float2* ybuf = nullptr;    // [bf*C][M]
+  // Frame batches alternate between kLanes internal streams so one batch's kernel tail overlaps
+  // the next batch's kernels; each lane owns its half-grid and k-space workspaces.
+  int nlanes = 1;
+  cudaStream_t lane[2] = {nullptr, nullptr};
+  cudaEvent_t ev_fork = nullptr, ev_join[2] = {nullptr, nullptr};
+  float2* Hs[2] = {nullptr, nullptr};      // [bf*C][N][G] half grid per lane
+  float2* ybufs[2] = {nullptr, nullptr};   // [bf*C][M] per lane
   float2* r = nullptr;       // CG vectors [L][N][N]
   float2* p = nullptr;
   float2* q = nullptr;
@@ -201,12 +206,18 @@ static mrf_status dev_alloc(mrf_plan_s* pl, T** ptr, size_t count) {
 
 static void free_plan(mrf_plan_s* pl) {
   if (!pl) return;
-  void* ptrs[] = {pl->coils, pl->dap, pl->tw, pl->fchunks, pl->ftab, pl->achunks, pl->atab, pl->fil, pl->H, pl->ybuf, pl->r, pl->p, pl->q,
+  void* ptrs[] = {pl->coils, pl->dap, pl->tw, pl->fchunks, pl->ftab, pl->achunks, pl->atab, pl->fil, pl->Hs[0], pl->Hs[1],
+                  pl->ybufs[0], pl->ybufs[1], pl->r, pl->p, pl->q,
                   pl->part, pl->dotp, pl->sc, pl->hist, pl->stg_x, pl->stg_y, pl->stg_z};
   for (void* v : ptrs)
     if (v) cudaFree(v);
   for (int k = 0; k < MRF_K_COUNT; ++k)
     for (cudaEvent_t e : pl->prof.ev[k]) cudaEventDestroy(e);
+  for (int i = 0; i < 2; ++i) {
+    if (pl->lane[i]) cudaStreamDestroy(pl->lane[i]);
+    if (pl->ev_join[i]) cudaEventDestroy(pl->ev_join[i]);
+  }
+  if (pl->ev_fork) cudaEventDestroy(pl->ev_fork);
   delete pl;
 }
 
@@ -333,25 +344,60 @@ static mrf_status memset_async(mrf_plan_s* pl, void* ptr, size_t bytes, cudaStre
 }
 
 // ---------------------------------------------------------------------------- operator drivers
+// Fork the frame batches of one operator call onto the plan's lanes and join them back into the
+// caller's stream (graph capturable: fork/join through events).
+struct Lanes {
+  mrf_plan_s* pl;
+  cudaStream_t st;
+  int n;
+  Lanes(mrf_plan_s* p, cudaStream_t s, int nbatch) : pl(p), st(s), n(nbatch > 1 ? p->nlanes : 1) {}
+  mrf_status begin() {
+    if (n == 1) return MRF_OK;
+    CUDA_TRY(cudaEventRecord(pl->ev_fork, st));
+    for (int i = 0; i < n; ++i) CUDA_TRY(cudaStreamWaitEvent(pl->lane[i], pl->ev_fork, 0));
+    return MRF_OK;
+  }
+  cudaStream_t stream(int b) const { return n == 1 ? st : pl->lane[b % n]; }
+  int slot(int b) const { return n == 1 ? 0 : b % n; }
+  mrf_status end() {
+    if (n == 1) return MRF_OK;
+    for (int i = 0; i < n; ++i) {
+      CUDA_TRY(cudaEventRecord(pl->ev_join[i], pl->lane[i]));
+      CUDA_TRY(cudaStreamWaitEvent(st, pl->ev_join[i], 0));
+    }
+    return MRF_OK;
+  }
+};
+
+static int n_batches(const mrf_plan_s* pl) { return (pl->L + pl->bf - 1) / pl->bf; }
+
 template <int G>
 static mrf_status run_forward(mrf_plan_s* pl, const float2* x, float2* y, cudaStream_t st) {
   MRF_TRY(memset_async(pl, y, (size_t)pl->L * pl->C * pl->M * sizeof(float2), st));
-  for (int l0 = 0; l0 < pl->L; l0 += pl->bf) {
+  Lanes ln(pl, st, n_batches(pl));
+  MRF_TRY(ln.begin());
+  for (int b = 0, l0 = 0; l0 < pl->L; ++b, l0 += pl->bf) {
     const int nb = std::min(pl->bf, pl->L - l0);
-    MRF_TRY(launch_fwd_rows<G>(pl, x, pl->H, l0, nb, st));
-    MRF_TRY(launch_fwd_cols<G>(pl, pl->H, y + (size_t)l0 * pl->C * pl->M, l0, nb, st));
+    cudaStream_t s = ln.stream(b);
+    float2* H = pl->Hs[ln.slot(b)];
+    MRF_TRY(launch_fwd_rows<G>(pl, x, H, l0, nb, s));
+    MRF_TRY(launch_fwd_cols<G>(pl, H, y + (size_t)l0 * pl->C * pl->M, l0, nb, s));
   }
-  return MRF_OK;
+  return ln.end();
 }
 
 template <int G>
 static mrf_status run_adjoint(mrf_plan_s* pl, const float2* y, float2* x, cudaStream_t st) {
-  for (int l0 = 0; l0 < pl->L; l0 += pl->bf) {
+  Lanes ln(pl, st, n_batches(pl));
+  MRF_TRY(ln.begin());
+  for (int b = 0, l0 = 0; l0 < pl->L; ++b, l0 += pl->bf) {
     const int nb = std::min(pl->bf, pl->L - l0);
-    MRF_TRY(launch_adj_cols<G>(pl, y + (size_t)l0 * pl->C * pl->M, pl->H, l0, nb, st));
-    MRF_TRY(launch_adj_rows<G>(pl, pl->H, x, nullptr, 0.f, l0, nb, nullptr, st));
+    cudaStream_t s = ln.stream(b);
+    float2* H = pl->Hs[ln.slot(b)];
+    MRF_TRY(launch_adj_cols<G>(pl, y + (size_t)l0 * pl->C * pl->M, H, l0, nb, s));
+    MRF_TRY(launch_adj_rows<G>(pl, H, x, nullptr, 0.f, l0, nb, nullptr, s));
   }
-  return MRF_OK;
+  return ln.end();
 }
 
 // out = A^H A x + mu x.  cg != 0: the CG iteration form -- x is the CG search direction p, the
@@ -360,17 +406,21 @@ static mrf_status run_adjoint(mrf_plan_s* pl, const float2* y, float2* x, cudaSt
 template <int G>
 static mrf_status run_normal(mrf_plan_s* pl, const float2* x, float2* out, float mu, int cg, float2* xsol,
                              cudaStream_t st) {
-  for (int l0 = 0; l0 < pl->L; l0 += pl->bf) {
+  Lanes ln(pl, st, n_batches(pl));
+  MRF_TRY(ln.begin());
+  for (int b = 0, l0 = 0; l0 < pl->L; ++b, l0 += pl->bf) {
     const int nb = std::min(pl->bf, pl->L - l0);
-    if (cg && pl->C == 1) MRF_TRY(launch_fwd_rows_cg<G>(pl, xsol, pl->H, l0, nb, st));
-    else MRF_TRY(launch_fwd_rows<G>(pl, x, pl->H, l0, nb, st));
-    MRF_TRY(memset_async(pl, pl->ybuf, (size_t)nb * pl->C * pl->M * sizeof(float2), st));
-    MRF_TRY(launch_fwd_cols<G>(pl, pl->H, pl->ybuf, l0, nb, st));
-    MRF_TRY(launch_adj_cols<G>(pl, pl->ybuf, pl->H, l0, nb, st));
-    MRF_TRY(launch_adj_rows<G>(pl, pl->H, out, (mu != 0.f || cg) ? x : nullptr, mu, l0, nb, cg ? pl->dotp : nullptr,
-                               st));
+    cudaStream_t s = ln.stream(b);
+    float2* H = pl->Hs[ln.slot(b)];
+    float2* yb = pl->ybufs[ln.slot(b)];
+    if (cg && pl->C == 1) MRF_TRY(launch_fwd_rows_cg<G>(pl, xsol, H, l0, nb, s));
+    else MRF_TRY(launch_fwd_rows<G>(pl, x, H, l0, nb, s));
+    MRF_TRY(memset_async(pl, yb, (size_t)nb * pl->C * pl->M * sizeof(float2), s));
+    MRF_TRY(launch_fwd_cols<G>(pl, H, yb, l0, nb, s));
+    MRF_TRY(launch_adj_cols<G>(pl, yb, H, l0, nb, s));
+    MRF_TRY(launch_adj_rows<G>(pl, H, out, (mu != 0.f || cg) ? x : nullptr, mu, l0, nb, cg ? pl->dotp : nullptr, s));
   }
-  return MRF_OK;
+  return ln.end();
 }
 
 #define DISPATCH_G(pl, fn, ...)                               \
@@ -755,7 +805,7 @@ mrf_status mrf_plan_create(const mrf_plan_desc* d, mrf_plan* out) {
   const size_t per_frame = (size_t)C * N * G * sizeof(float2);
   int bf = d->batch_frames;
   if (bf == 0) {
-    const size_t target = 128ull << 20;   // measured: larger batches amortise launch tails
+    const size_t target = 128ull << 20;   // per lane; measured: launch-tail amortisation beats L2 residency
     bf = (int)std::max<size_t>(1, target / per_frame);
   }
   bf = std::min(bf, L);
@@ -767,7 +817,7 @@ mrf_status mrf_plan_create(const mrf_plan_desc* d, mrf_plan* out) {
       (s = dev_alloc(pl, &pl->fchunks, fch.size())) || (s = dev_alloc(pl, &pl->ftab, ftab.size())) ||
       (s = dev_alloc(pl, &pl->achunks, ach.size())) || (s = dev_alloc(pl, &pl->atab, atab.size())) ||
       (s = dev_alloc(pl, &pl->fil, L)) ||
-      (s = dev_alloc(pl, &pl->H, (size_t)bf * C * N * G)) || (s = dev_alloc(pl, &pl->ybuf, (size_t)bf * C * M)) ||
+      (s = dev_alloc(pl, &pl->Hs[0], (size_t)bf * C * N * G)) || (s = dev_alloc(pl, &pl->ybufs[0], (size_t)bf * C * M)) ||
       (s = dev_alloc(pl, &pl->r, (size_t)L * N * N)) || (s = dev_alloc(pl, &pl->p, (size_t)L * N * N)) ||
       (s = dev_alloc(pl, &pl->q, (size_t)L * N * N)) || (s = dev_alloc(pl, &pl->part, kPartBlocks)) ||
       (s = dev_alloc(pl, &pl->dotp, pl->ndotp)) || (s = dev_alloc(pl, &pl->sc, 1)))
@@ -775,7 +825,23 @@ mrf_status mrf_plan_create(const mrf_plan_desc* d, mrf_plan* out) {
   if (d->coils && C >= 1) {
     if ((s = dev_alloc(pl, &pl->coils, (size_t)C * N * N))) return bail(s);
   }
+  pl->nlanes = L > bf ? 2 : 1;
+  if (const char* e = std::getenv("MRF_LANES")) pl->nlanes = std::max(1, std::min(2, std::atoi(e)));
+  if (pl->nlanes > 1) {
+    if ((s = dev_alloc(pl, &pl->Hs[1], (size_t)bf * C * N * G)) || (s = dev_alloc(pl, &pl->ybufs[1], (size_t)bf * C * M)))
+      return bail(s);
+    for (int i = 0; i < 2; ++i) {
+      if (cudaStreamCreateWithFlags(&pl->lane[i], cudaStreamNonBlocking) != cudaSuccess ||
+          cudaEventCreateWithFlags(&pl->ev_join[i], cudaEventDisableTiming) != cudaSuccess)
+        return bail(fail(MRF_ECUDA, "stream/event creation failed"));
+    }
+    if (cudaEventCreateWithFlags(&pl->ev_fork, cudaEventDisableTiming) != cudaSuccess)
+      return bail(fail(MRF_ECUDA, "event creation failed"));
+  }
   if ((s = do_setup(pl))) return bail(s);
+  for (const int2& ow : atab)   // the spread kernel needs every chunk's header, slices and cells staged
+    if ((size_t)ach[ow.x + 2] * 4 > (size_t)pl->ac_stage)
+      return bail(fail(MRF_EUNSUPPORTED, "a grid strip has too many occupied cells for the staging buffer"));
   auto up = [&](void* dst, const void* src, size_t bytes) {
     return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st);
   };
