@@ -28,12 +28,31 @@ __device__ __forceinline__ double2 block_sum2(double2 v) {
   return s;   // valid in thread 0
 }
 
-// dst = sum of part[0..n) in a fixed order (one block)
-__global__ void __launch_bounds__(kVecThreads) k_reduce(const double2* __restrict__ part, int n, double2* __restrict__ dst) {
-  double2 s = make_double2(0.0, 0.0);
-  for (int i = threadIdx.x; i < n; i += blockDim.x) { s.x += part[i].x; s.y += part[i].y; }
-  s = block_sum2(s);
-  if (threadIdx.x == 0) *dst = s;
+// dst = sum of part[0..n) in a fixed order (one block of kReduceThreads, 4 independent loads in
+// flight per thread)
+constexpr int kReduceThreads = 1024;
+__global__ void __launch_bounds__(kReduceThreads) k_reduce(const double2* __restrict__ part, int n, double2* __restrict__ dst) {
+  __shared__ double2 red[kReduceThreads / 32];
+  double2 s0 = make_double2(0.0, 0.0), s1 = s0, s2 = s0, s3 = s0;
+  int i = threadIdx.x;
+  for (; i + 3 * kReduceThreads < n; i += 4 * kReduceThreads) {
+    const double2 a = part[i], b = part[i + kReduceThreads], c = part[i + 2 * kReduceThreads], d = part[i + 3 * kReduceThreads];
+    s0.x += a.x; s0.y += a.y; s1.x += b.x; s1.y += b.y; s2.x += c.x; s2.y += c.y; s3.x += d.x; s3.y += d.y;
+  }
+  for (; i < n; i += kReduceThreads) { s0.x += part[i].x; s0.y += part[i].y; }
+  double2 v = make_double2((s0.x + s1.x) + (s2.x + s3.x), (s0.y + s1.y) + (s2.y + s3.y));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    v.x += __shfl_xor_sync(0xffffffffu, v.x, o);
+    v.y += __shfl_xor_sync(0xffffffffu, v.y, o);
+  }
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double2 t = make_double2(0.0, 0.0);
+    for (int w = 0; w < kReduceThreads / 32; ++w) { t.x += red[w].x; t.y += red[w].y; }
+    *dst = t;
+  }
 }
 
 // Device-resident CG scalars.

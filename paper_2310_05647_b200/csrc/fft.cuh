@@ -146,6 +146,36 @@ __device__ __forceinline__ void dft(float2 (&v)[R]) {
   }
 }
 
+namespace detail {
+template <int P, int SIGN, int N1>
+__device__ __forceinline__ void halfzero_split(const float2 (&v)[P], float2 (&a)[P / 2], float2 (&b)[P / 2]) {
+  if constexpr (N1 < P / 2) {
+    constexpr int src = N1 < P / 4 ? N1 : N1 + P / 2;      // the one non-zero input of the pair
+    constexpr int tw = N1 < P / 4 ? N1 : N1 + P / 2;       // (x[n] - x[n+P/2]) W^n = z W^{n or n+P/2}
+    a[N1] = v[src];
+    b[N1] = twmul<P, tw, SIGN>(v[src]);
+    halfzero_split<P, SIGN, N1 + 1>(v, a, b);
+  }
+}
+}  // namespace detail
+
+// In-place P-point DFT of an input that is zero at n in [P/4, 3P/4) (the zero-padded half of the
+// oversampled grid).  One decimation-in-frequency step leaves every butterfly
+// with a single non-zero input, so it costs only the odd-branch twiddles, then two P/2-point DFTs
+// give the even and odd outputs.  The values in v[P/4 .. 3P/4) are ignored.
+template <int P, int SIGN>
+__device__ __forceinline__ void dft_halfzero(float2 (&v)[P]) {
+  float2 a[P / 2], b[P / 2];
+  detail::halfzero_split<P, SIGN, 0>(v, a, b);
+  dft<P / 2, SIGN>(a);
+  dft<P / 2, SIGN>(b);
+#pragma unroll
+  for (int k = 0; k < P / 2; ++k) {
+    v[2 * k] = a[k];
+    v[2 * k + 1] = b[k];
+  }
+}
+
 // Two-stage split of the supported grid sizes.  T threads (within one warp) per length-G DFT.
 template <int G> struct FFTShape;
 template <> struct FFTShape<64>   { static constexpr int P = 8,  Q = 8,  T = 8;  };

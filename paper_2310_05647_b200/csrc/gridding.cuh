@@ -98,6 +98,10 @@ __device__ __forceinline__ void smem_add2(float2* a, float2 v) {
   } while (old != assumed);
 }
 
+// Shared-memory strip layout [row][16] with the column XOR-swizzled by the row (row & 15): a
+// record's W tap rows then fall in different banks, and a row is still 16 contiguous slots.
+__host__ __device__ __forceinline__ int sidx(int row, int col) { return row * SW + (col ^ (row & (SW - 1))); }
+
 // image index <-> wrapped grid index (centred n = i - N/2, grid position n mod G)
 template <int G>
 __device__ __forceinline__ int grid_to_img(int pos) {   // pos in the kept set
@@ -244,7 +248,7 @@ k_fwd_rows(DevPlan p, const float2* __restrict__ x, float2* __restrict__ H, int 
 #pragma unroll
     for (int a = 0; a < A; ++a) {
       const int n2 = t + T * a;
-      dft<P, -1>(v[a]);
+      dft_halfzero<P, -1>(v[a]);
 #pragma unroll
       for (int k1 = 0; k1 < P; ++k1) myex[n2 * (P + 1) + k1] = cmul(v[a][k1], stw[k1 * Q + n2]);
     }
@@ -338,7 +342,7 @@ k_fwd_cols(DevPlan p, const float2* __restrict__ H, float2* __restrict__ y, int 
 #pragma unroll
     for (int a = 0; a < A; ++a) {
       const int n2 = t + T * a;
-      dft<P, -1>(v[a]);
+      dft_halfzero<P, -1>(v[a]);
 #pragma unroll
       for (int k1 = 0; k1 < P; ++k1) strip[(n2 * P + k1) * SW + c] = cmul(v[a][k1], stw[k1 * Q + n2]);
     }
@@ -356,7 +360,7 @@ k_fwd_cols(DevPlan p, const float2* __restrict__ H, float2* __restrict__ y, int 
       const int k1 = t + T * b;
       dft<Q, -1>(w[b]);
 #pragma unroll
-      for (int k2 = 0; k2 < Q; ++k2) strip[(k1 + P * k2) * SW + c] = w[b][k2];   // strip [gy][c]
+      for (int k2 = 0; k2 < Q; ++k2) strip[sidx(k1 + P * k2, c)] = w[b][k2];   // strip [gy][c] (swizzled)
     }
     __syncthreads();
     // a3: KB gather interpolation.  A warp takes 32/W point records at a time, lane = (record,
@@ -377,10 +381,10 @@ k_fwd_cols(DevPlan p, const float2* __restrict__ H, float2* __restrict__ y, int 
         int j = 0;
         if (valid) {
           const Rec rr = read_rec((e < n_st ? recs : grecs) + e * recw, W);
-          const float2* row = strip + ((rr.gy0 + ty) & (G - 1)) * SW + rr.cx0;
+          const int gy = (rr.gy0 + ty) & (G - 1);
           for (int i = 0; i < rr.ntx; ++i) {
             const float wx = rr.wx[rr.tx0 + i];
-            const float2 g = row[i];
+            const float2 g = strip[sidx(gy, rr.cx0 + i)];
             part.x = fmaf(wx, g.x, part.x);
             part.y = fmaf(wx, g.y, part.y);
           }
@@ -487,7 +491,7 @@ k_adj_cols(DevPlan p, const float2* __restrict__ y, float2* __restrict__ H, int 
           }
         } else {
           const int2* ep = gents + si.x + lane;
-#pragma unroll 8
+#pragma unroll 16
           for (int kk = 0; kk < si.y; ++kk) {
             const int2 e = __ldg(ep + kk * 32);
             const float wgt = __int_as_float(e.y);
@@ -511,7 +515,7 @@ k_adj_cols(DevPlan p, const float2* __restrict__ y, float2* __restrict__ H, int 
     for (int a = 0; a < A; ++a) {
       const int n2 = t + T * a;
 #pragma unroll
-      for (int n1 = 0; n1 < P; ++n1) v[a][n1] = strip[(Q * n1 + n2) * SW + c];
+      for (int n1 = 0; n1 < P; ++n1) v[a][n1] = strip[sidx(Q * n1 + n2, c)];
     }
     __syncthreads();
 #pragma unroll

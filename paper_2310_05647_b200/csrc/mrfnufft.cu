@@ -464,7 +464,7 @@ static mrf_status allreduce2(mrf_plan_s* pl, double2* v, cudaStream_t st) {
 
 static mrf_status reduce_to(mrf_plan_s* pl, const double2* part, int nblk, double2* dst, cudaStream_t st) {
   ProfScope ps(pl, MRF_K_CG_VEC, st);
-  k_reduce<<<1, kVecThreads, 0, st>>>(part, nblk, dst);
+  k_reduce<<<1, kReduceThreads, 0, st>>>(part, nblk, dst);
   MRF_TRY(check_launch("k_reduce"));
   return MRF_OK;
 }
@@ -782,7 +782,9 @@ mrf_status mrf_plan_create(const mrf_plan_desc* d, mrf_plan* out) {
         ch[kChunkHdr + 2 * sl + 1] = width;
         for (int lane = 0; lane < 32; ++lane) {
           const size_t ri = (size_t)sl * 32 + lane;
-          cells[sl * 32 + lane] = ri < rows.size() ? (unsigned short)nz[rows[ri].x].cell : (unsigned short)0xFFFF;
+          cells[sl * 32 + lane] = ri < rows.size()
+                                      ? (unsigned short)sidx(nz[rows[ri].x].cell / SW, nz[rows[ri].x].cell % SW)
+                                      : (unsigned short)0xFFFF;   // swizzled strip slot
           for (int k = 0; k < width; ++k) {
             int2 e = make_int2(0, 0);
             if (ri < rows.size() && k < rows[ri].y) {
