@@ -10,7 +10,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libmrfnufft.so")
 SOURCES = [os.path.join(CSRC, "mrfnufft.cu"), os.path.join(CSRC, "nccl_dl.cpp")]
-DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("kernels.cuh", "fft.cuh", "nccl_dl.h")] + [
+DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("gridding.cuh", "cg.cuh", "fft.cuh", "nccl_dl.h")] + [
     os.path.join(ROOT, "include", "mrfnufft.h")]
 
 NVCC_FLAGS = [
@@ -36,6 +36,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and up_to_date():
         return LIB
     cmd = [nvcc(), *NVCC_FLAGS, "-o", LIB + ".tmp", *SOURCES, "-ldl"]
+    if os.environ.get("MRF_EXPERIMENTS"):
+        cmd.insert(1, "-DMRF_EXPERIMENTS")
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
         print(" ".join(cmd), flush=True)

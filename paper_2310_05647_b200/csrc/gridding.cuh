@@ -50,6 +50,8 @@ struct DevPlan {
   const int* __restrict__ achunks;    // adjoint chunks
   const int2* __restrict__ atab;      // [R*S] {offset, words}
   const int* __restrict__ fil;        // [L_local] interleaf of each local frame
+  int dbg;                            // experiment bits (0 in production)
+  long long* dbgbuf;                  // phase timer output (experiment bit 2)
 };
 
 // ---------------------------------------------------------------------------- async copy (TMA)
@@ -155,6 +157,78 @@ __device__ __forceinline__ Rec read_rec(const int* rp, int W) {
   r.wx = reinterpret_cast<const float*>(rp + 2);
   (void)W;
   return r;
+}
+
+// Phase timer (experiment bit 2; only compiled with -DMRF_EXPERIMENTS): thread 0 of every CTA
+// accumulates clock64 deltas per phase into p.dbgbuf.
+#ifdef MRF_EXPERIMENTS
+#define MRF_DBG_ON(bit) (p.dbg & (bit))
+struct PhaseTimer {
+  long long acc[10];
+  long long t0;
+  bool on;
+  __device__ __forceinline__ void start(bool enable) {
+    on = enable;
+    if (on) {
+      for (int i = 0; i < 10; ++i) acc[i] = 0;
+      t0 = clock64();
+    }
+  }
+  __device__ __forceinline__ void mark(int i) {
+    if (on) {
+      const long long t = clock64();
+      acc[i] += t - t0;
+      t0 = t;
+    }
+  }
+  __device__ __forceinline__ void report(long long* buf, int items) {
+    if (on && buf) {
+      atomicAdd(reinterpret_cast<unsigned long long*>(buf), (unsigned long long)items);
+      for (int i = 0; i < 10; ++i) atomicAdd(reinterpret_cast<unsigned long long*>(buf + 1 + i), (unsigned long long)acc[i]);
+    }
+  }
+};
+#else
+#define MRF_DBG_ON(bit) false
+struct PhaseTimer {
+  __device__ __forceinline__ void start(bool) {}
+  __device__ __forceinline__ void mark(int) {}
+  __device__ __forceinline__ void report(long long*, int) {}
+};
+#endif
+
+// sum_i wx[tx0 + i] * strip(gy, cx0 + i) over the record's x-taps in this strip.  WT > 0: the
+// width is a compile-time bound, so all taps' loads issue before the FMAs (predicated on ntx).
+template <int WT>
+__device__ __forceinline__ float2 tap_row(const float2* strip, const Rec& rr, int gy) {
+  float2 part = make_float2(0.f, 0.f);
+  if constexpr (WT > 0) {
+    float wx[WT];
+    float2 g[WT];
+#pragma unroll
+    for (int i = 0; i < WT; ++i) {
+      if (i < rr.ntx) {
+        wx[i] = rr.wx[rr.tx0 + i];
+        g[i] = strip[sidx(gy, rr.cx0 + i)];
+      } else {
+        wx[i] = 0.f;
+        g[i] = make_float2(0.f, 0.f);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < WT; ++i) {
+      part.x = fmaf(wx[i], g[i].x, part.x);
+      part.y = fmaf(wx[i], g[i].y, part.y);
+    }
+  } else {
+    for (int i = 0; i < rr.ntx; ++i) {
+      const float wx = rr.wx[rr.tx0 + i];
+      const float2 g = strip[sidx(gy, rr.cx0 + i)];
+      part.x = fmaf(wx, g.x, part.x);
+      part.y = fmaf(wx, g.y, part.y);
+    }
+  }
+  return part;
 }
 
 // ============================================================================ forward rows
@@ -289,6 +363,7 @@ k_fwd_cols(DevPlan p, const float2* __restrict__ H, float2* __restrict__ y, int 
   uint64_t* bars = reinterpret_cast<uint64_t*>(strip + G * SW);      // H, chunk
   int* stage = reinterpret_cast<int*>(bars + 2);
   __shared__ int copied;                                             // bytes of the staged chunk
+  __shared__ int fchunk_off;                                         // word offset of the staged chunk
   const int C = p.C, W = p.W, recw = p.recw;
   const int n_items = nb * C * S;
   const int tid = threadIdx.x, c = tid % SW, t = tid / SW;
@@ -311,11 +386,15 @@ k_fwd_cols(DevPlan p, const float2* __restrict__ H, float2* __restrict__ y, int 
   auto issue_chunk = [&](int2 ow) {   // records beyond the staging capacity are read from L2
     const uint32_t bytes = (uint32_t)min(stage_cap, ow.y * 4) & ~15u;
     copied = (int)bytes;
+    fchunk_off = ow.x;
     mbar_expect_tx(&bars[1], bytes);
     bulk_g2s(stage, p.fchunks + ow.x, bytes, &bars[1]);
   };
   int item = blockIdx.x;
   int2 off_next = make_int2(0, 0);
+  PhaseTimer pt;
+  pt.start(MRF_DBG_ON(2) && tid == 0);
+  int nit = 0;
   if (tid == 0 && item < n_items) {
     issue_in(item);
     issue_chunk(chunk_of(item));
@@ -325,6 +404,8 @@ k_fwd_cols(DevPlan p, const float2* __restrict__ H, float2* __restrict__ y, int 
     const int fc = item / S;
     const int next = item + gridDim.x;
     mbar_wait(&bars[0], k & 1);
+    pt.mark(0);
+    ++nit;
     float2 v[A][P];
 #pragma unroll
     for (int a = 0; a < A; ++a) {
@@ -339,6 +420,7 @@ k_fwd_cols(DevPlan p, const float2* __restrict__ H, float2* __restrict__ y, int 
       fence_proxy_async();
       issue_in(next);
     }
+    pt.mark(1);
 #pragma unroll
     for (int a = 0; a < A; ++a) {
       const int n2 = t + T * a;
@@ -347,6 +429,7 @@ k_fwd_cols(DevPlan p, const float2* __restrict__ H, float2* __restrict__ y, int 
       for (int k1 = 0; k1 < P; ++k1) strip[(n2 * P + k1) * SW + c] = cmul(v[a][k1], stw[k1 * Q + n2]);
     }
     __syncthreads();
+    pt.mark(2);
     float2 w[B][Q];
 #pragma unroll
     for (int b = 0; b < B; ++b) {
@@ -355,6 +438,7 @@ k_fwd_cols(DevPlan p, const float2* __restrict__ H, float2* __restrict__ y, int 
       for (int n2 = 0; n2 < Q; ++n2) w[b][n2] = strip[(n2 * P + k1) * SW + c];
     }
     __syncthreads();
+    pt.mark(3);
 #pragma unroll
     for (int b = 0; b < B; ++b) {
       const int k1 = t + T * b;
@@ -363,54 +447,71 @@ k_fwd_cols(DevPlan p, const float2* __restrict__ H, float2* __restrict__ y, int 
       for (int k2 = 0; k2 < Q; ++k2) strip[sidx(k1 + P * k2, c)] = w[b][k2];   // strip [gy][c] (swizzled)
     }
     __syncthreads();
+    pt.mark(4);
     // a3: KB gather interpolation.  A warp takes 32/W point records at a time, lane = (record,
     // y-tap): each lane sums its tap row, the W row partials are combined with shuffles, and the
     // record's leader lane adds the strip's share of y_j.
     mbar_wait(&bars[1], k & 1);
-    {
+    pt.mark(5);
+    if (!MRF_DBG_ON(1)) {
       const int n_rec = stage[0];
       const int n_st = (copied / 4 - kChunkHdr) / recw;     // records staged in shared memory
       const int* recs = stage + kChunkHdr;
-      const int* grecs = n_st < n_rec ? p.fchunks + chunk_of(item).x + kChunkHdr : recs;
+      const int* grecs = p.fchunks + fchunk_off + kChunkHdr;  // the rest is read from L2
       float2* yf = y + (size_t)fc * p.M;
       const int rpw = 32 / W, slot = lane / W, ty = lane - slot * W;
+      auto row_part = [&](const Rec& rr) -> float2 {
+        const int gy = (rr.gy0 + ty) & (G - 1);
+        float2 part;
+        if (W == 6) part = tap_row<6>(strip, rr, gy);
+        else if (W == 8) part = tap_row<8>(strip, rr, gy);
+        else part = tap_row<0>(strip, rr, gy);
+        const float wy = rr.wx[W + ty];
+        return make_float2(part.x * wy, part.y * wy);
+      };
       for (int base = warp * rpw; base < n_rec; base += nwarps * rpw) {
         const int e = base + slot;
         const bool valid = slot < rpw && e < n_rec;
         float2 part = make_float2(0.f, 0.f);
         int j = 0;
         if (valid) {
-          const Rec rr = read_rec((e < n_st ? recs : grecs) + e * recw, W);
-          const int gy = (rr.gy0 + ty) & (G - 1);
-          for (int i = 0; i < rr.ntx; ++i) {
-            const float wx = rr.wx[rr.tx0 + i];
-            const float2 g = strip[sidx(gy, rr.cx0 + i)];
-            part.x = fmaf(wx, g.x, part.x);
-            part.y = fmaf(wx, g.y, part.y);
+          if (e < n_st) {
+            const Rec rr = read_rec(recs + e * recw, W);
+            part = row_part(rr);
+            j = rr.j;
+          } else {
+            const Rec rr = read_rec(grecs + e * recw, W);
+            part = row_part(rr);
+            j = rr.j;
           }
-          const float wy = rr.wx[W + ty];
-          part.x *= wy;
-          part.y *= wy;
-          j = rr.j;
         }
         float2 sum = part;
-        for (int o = 1; o < W; ++o) {
-          sum.x += __shfl_down_sync(0xffffffffu, part.x, o);
-          sum.y += __shfl_down_sync(0xffffffffu, part.y, o);
+        if (!MRF_DBG_ON(8)) {
+          for (int o = 1; o < W; ++o) {
+            sum.x += __shfl_down_sync(0xffffffffu, part.x, o);
+            sum.y += __shfl_down_sync(0xffffffffu, part.y, o);
+          }
         }
         if (valid && ty == 0) {
-          atomicAdd(&yf[j].x, sum.x);
-          atomicAdd(&yf[j].y, sum.y);
+          if (MRF_DBG_ON(4)) {
+            if (sum.x == 12345.f) yf[j] = sum;
+          } else {
+            atomicAdd(&yf[j].x, sum.x);
+            atomicAdd(&yf[j].y, sum.y);
+          }
         }
       }
     }
+    pt.mark(6);
     __syncthreads();
+    pt.mark(7);
     if (tid == 0 && next < n_items) {
       fence_proxy_async();
       issue_chunk(off_next);
       if (next + (int)gridDim.x < n_items) off_next = chunk_of(next + gridDim.x);
     }
   }
+  pt.report(p.dbgbuf, nit);
 }
 
 // ============================================================================ adjoint columns
@@ -457,6 +558,9 @@ k_adj_cols(DevPlan p, const float2* __restrict__ y, float2* __restrict__ H, int 
   };
   int item = blockIdx.x;
   int2 off_next = make_int2(0, 0);
+  PhaseTimer pt;
+  pt.start(MRF_DBG_ON(2) && tid == 0);
+  int nit = 0;
   if (tid == 0 && item < n_items) {
     issue(item, chunk_of(item));
     if (item + (int)gridDim.x < n_items) off_next = chunk_of(item + gridDim.x);
@@ -465,10 +569,12 @@ k_adj_cols(DevPlan p, const float2* __restrict__ y, float2* __restrict__ H, int 
     const int fc = item / S;
     const int next = item + gridDim.x;
     mbar_wait(&bars[0], k & 1);
+    pt.mark(0);
+    ++nit;
     {
       // Staged prefix of the chunk: header, slice table and cells always fit (checked at plan
       // time); a slice whose entries lie past the staged prefix reads them from L2.
-      const int nsl = stage[0], cells_off = stage[1], ent_off = stage[2];
+      const int nsl = MRF_DBG_ON(1) ? 0 : stage[0], cells_off = stage[1], ent_off = stage[2];
       const float2* yf = y + (size_t)fc * M;
       const int2* sl_tab = reinterpret_cast<const int2*>(stage + kChunkHdr);
       const unsigned short* cells = reinterpret_cast<const unsigned short*>(stage + cells_off);
@@ -503,7 +609,9 @@ k_adj_cols(DevPlan p, const float2* __restrict__ y, float2* __restrict__ H, int 
         if (cell != 0xFFFF) strip[cell] = acc;
       }
     }
+    pt.mark(1);
     __syncthreads();
+    pt.mark(2);
     if (tid == 0 && next < n_items) {
       fence_proxy_async();
       issue(next, off_next);
@@ -518,6 +626,7 @@ k_adj_cols(DevPlan p, const float2* __restrict__ y, float2* __restrict__ H, int 
       for (int n1 = 0; n1 < P; ++n1) v[a][n1] = strip[sidx(Q * n1 + n2, c)];
     }
     __syncthreads();
+    pt.mark(3);
 #pragma unroll
     for (int a = 0; a < A; ++a) {
       const int n2 = t + T * a;
@@ -526,6 +635,7 @@ k_adj_cols(DevPlan p, const float2* __restrict__ y, float2* __restrict__ H, int 
       for (int k1 = 0; k1 < P; ++k1) strip[(n2 * P + k1) * SW + c] = cmulc(v[a][k1], stw[k1 * Q + n2]);
     }
     __syncthreads();
+    pt.mark(4);
     float2 w[B][Q];
 #pragma unroll
     for (int b = 0; b < B; ++b) {
@@ -535,6 +645,7 @@ k_adj_cols(DevPlan p, const float2* __restrict__ y, float2* __restrict__ H, int 
     }
     __syncthreads();
     for (int i = tid; i < G * SW; i += blockDim.x) strip[i] = make_float2(0.f, 0.f);   // for the next spread
+    pt.mark(5);
     float2* Hc = H + (size_t)fc * N * G + (size_t)(item % S) * SW + c;    // row-major [fc][iy][G]
 #pragma unroll
     for (int b = 0; b < B; ++b) {
@@ -545,8 +656,11 @@ k_adj_cols(DevPlan p, const float2* __restrict__ y, float2* __restrict__ H, int 
         if (k2 < Q / 4 || k2 >= 3 * Q / 4) Hc[(size_t)grid_to_img<G>(k1 + P * k2) * G] = w[b][k2];
       }
     }
+    pt.mark(6);
     __syncthreads();   // zero-fill visible before the next spread
+    pt.mark(7);
   }
+  pt.report(p.dbgbuf ? p.dbgbuf + 16 : nullptr, nit);
 }
 
 // ============================================================================ adjoint rows

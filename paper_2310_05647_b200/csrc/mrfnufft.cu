@@ -69,6 +69,9 @@ struct DeviceGuard {
 
 }  // namespace
 
+static constexpr int kMaxLanes = 4;
+static constexpr int kDefaultLanes = 2;
+
 struct mrf_plan_s {
   // sizes
   int N = 0, G = 0, L = 0, M = 0, R = 0, C = 1, W = 0, S = 0, frame_offset = 0, recw = 0;
@@ -79,8 +82,11 @@ struct mrf_plan_s {
   int ystage = 0;           // k_adj_cols stages y[fc] in shared memory (M even, M*8 <= kYBytes)
   int occ_fr0 = 1, occ_fr1 = 1, occ_fc = 1, occ_ac = 1, occ_ar = 1;   // resident CTAs per SM
   int fc_stage = 0, ac_stage = 0;   // chunk staging bytes of the column kernels
-  int col_smem = 0;                 // dynamic shared memory of the column kernels
+  int col_smem = 0;                 // dynamic shared memory of k_fwd_cols
+  int acol_smem = 0;                // dynamic shared memory of k_adj_cols
   void* nccl_comm = nullptr;
+  int dbg = 0;               // MRF_DBG experiment bits (1: skip gather/spread, 2: phase timers)
+  long long* dbgbuf = nullptr;
   // device tables
   float2* coils = nullptr;
   float* dap = nullptr;
@@ -94,10 +100,10 @@ struct mrf_plan_s {
   // Frame batches alternate between kLanes internal streams so one batch's kernel tail overlaps
   // the next batch's kernels; each lane owns its half-grid and k-space workspaces.
   int nlanes = 1;
-  cudaStream_t lane[2] = {nullptr, nullptr};
-  cudaEvent_t ev_fork = nullptr, ev_join[2] = {nullptr, nullptr};
-  float2* Hs[2] = {nullptr, nullptr};      // [bf*C][N][G] half grid per lane
-  float2* ybufs[2] = {nullptr, nullptr};   // [bf*C][M] per lane
+  cudaStream_t lane[kMaxLanes] = {};
+  cudaEvent_t ev_fork = nullptr, ev_join[kMaxLanes] = {};
+  float2* Hs[kMaxLanes] = {};      // [bf*C][N][G] half grid per lane
+  float2* ybufs[kMaxLanes] = {};   // [bf*C][M] per lane
   float2* r = nullptr;       // CG vectors [L][N][N]
   float2* p = nullptr;
   float2* q = nullptr;
@@ -118,6 +124,8 @@ struct mrf_plan_s {
     d.N = N; d.G = G; d.M = M; d.R = R; d.C = C; d.W = W; d.S = S; d.recw = recw;
     d.coils = coils; d.dap = dap; d.tw = tw; d.fchunks = fchunks; d.ftab = ftab; d.achunks = achunks; d.atab = atab;
     d.fil = fil;
+    d.dbg = dbg;
+    d.dbgbuf = dbgbuf;
     return d;
   }
 };
@@ -206,14 +214,29 @@ static mrf_status dev_alloc(mrf_plan_s* pl, T** ptr, size_t count) {
 
 static void free_plan(mrf_plan_s* pl) {
   if (!pl) return;
-  void* ptrs[] = {pl->coils, pl->dap, pl->tw, pl->fchunks, pl->ftab, pl->achunks, pl->atab, pl->fil, pl->Hs[0], pl->Hs[1],
-                  pl->ybufs[0], pl->ybufs[1], pl->r, pl->p, pl->q,
+  if (pl->dbgbuf) {   // phase timer dump (experiment bit 2): cycles summed over CTAs
+    long long h[32];
+    if (cudaMemcpy(h, pl->dbgbuf, sizeof(h), cudaMemcpyDeviceToHost) == cudaSuccess) {
+      const char* nm[2] = {"fwd_cols", "adj_cols"};
+      for (int k = 0; k < 2; ++k) {
+        std::fprintf(stderr, "[phase] %s items=%lld cycles/item:", nm[k], h[16 * k]);
+        for (int i = 1; i <= 10; ++i) std::fprintf(stderr, " %.0f", h[16 * k] ? (double)h[16 * k + i] / h[16 * k] : 0.0);
+        std::fprintf(stderr, "\n");
+      }
+    }
+    cudaFree(pl->dbgbuf);
+  }
+  for (int i = 0; i < kMaxLanes; ++i) {
+    if (pl->Hs[i]) cudaFree(pl->Hs[i]);
+    if (pl->ybufs[i]) cudaFree(pl->ybufs[i]);
+  }
+  void* ptrs[] = {pl->coils, pl->dap, pl->tw, pl->fchunks, pl->ftab, pl->achunks, pl->atab, pl->fil, pl->r, pl->p, pl->q,
                   pl->part, pl->dotp, pl->sc, pl->hist, pl->stg_x, pl->stg_y, pl->stg_z};
   for (void* v : ptrs)
     if (v) cudaFree(v);
   for (int k = 0; k < MRF_K_COUNT; ++k)
     for (cudaEvent_t e : pl->prof.ev[k]) cudaEventDestroy(e);
-  for (int i = 0; i < 2; ++i) {
+  for (int i = 0; i < kMaxLanes; ++i) {
     if (pl->lane[i]) cudaStreamDestroy(pl->lane[i]);
     if (pl->ev_join[i]) cudaEventDestroy(pl->ev_join[i]);
   }
@@ -264,20 +287,26 @@ static mrf_status setup_kernels(mrf_plan_s* pl) {
   int optin = 0, per_sm = 0;
   CUDA_TRY(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, pl->device));
   CUDA_TRY(cudaDeviceGetAttribute(&per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, pl->device));
-  const size_t s_col = std::min<size_t>((size_t)optin - 256, (size_t)per_sm / cols_ctas_per_sm<G>() - 1024 - 256) & ~size_t(15);
+  int actas = 1;   // measured: the adjoint column kernel prefers one CTA per SM with a large chunk stage
+  if (const char* e = std::getenv("MRF_ADJ_CTAS")) actas = std::max(1, std::min(2, std::atoi(e)));
+  int fctas = cols_ctas_per_sm<G>();
+  if (const char* e = std::getenv("MRF_FWD_CTAS")) fctas = std::max(1, std::min(2, std::atoi(e)));
+  const size_t s_col = std::min<size_t>((size_t)optin - 256, (size_t)per_sm / fctas - 1024 - 256) & ~size_t(15);
+  const size_t s_acol = std::min<size_t>((size_t)optin - 256, (size_t)per_sm / actas - 1024 - 256) & ~size_t(15);
   pl->col_smem = (int)s_col;
+  pl->acol_smem = (int)s_acol;
   pl->fc_stage = (int)((s_col - fwd_cols_fixed<G>()) & ~size_t(15));
-  pl->ac_stage = (int)((s_col - adj_cols_fixed<G>(pl->ystage != 0)) & ~size_t(15));
+  pl->ac_stage = (int)((s_acol - adj_cols_fixed<G>(pl->ystage != 0)) & ~size_t(15));
   CUDA_TRY(cudaFuncSetAttribute(k_fwd_rows<G, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s_fr0));
   CUDA_TRY(cudaFuncSetAttribute(k_fwd_rows<G, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s_fr1));
   CUDA_TRY(cudaFuncSetAttribute(k_adj_rows<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s_ar));
   CUDA_TRY(cudaFuncSetAttribute(k_fwd_cols<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s_col));
-  CUDA_TRY(cudaFuncSetAttribute(k_adj_cols<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s_col));
+  CUDA_TRY(cudaFuncSetAttribute(k_adj_cols<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s_acol));
   CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pl->occ_fr0, k_fwd_rows<G, 0>, kRowThreads, s_fr0));
   CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pl->occ_fr1, k_fwd_rows<G, 1>, kRowThreads, s_fr1));
   CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pl->occ_ar, k_adj_rows<G>, kRowThreads, s_ar));
   CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pl->occ_fc, k_fwd_cols<G>, ncol, s_col));
-  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pl->occ_ac, k_adj_cols<G>, ncol, s_col));
+  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pl->occ_ac, k_adj_cols<G>, ncol, s_acol));
   if (pl->occ_fr0 < 1 || pl->occ_fr1 < 1 || pl->occ_ar < 1 || pl->occ_fc < 1 || pl->occ_ac < 1)
     return fail(MRF_EUNSUPPORTED, "a kernel does not fit on an SM");
   if (const char* cap = std::getenv("MRF_OCC_CAP")) {   // experiment knob: resident CTAs per SM
@@ -322,9 +351,9 @@ template <int G>
 static mrf_status launch_adj_cols(mrf_plan_s* pl, const float2* y, float2* H, int l0, int nb, cudaStream_t st) {
   const long long items = (long long)nb * pl->C * pl->S;
   const int ys = pl->ystage && ((uintptr_t)y % 16 == 0);
-  const int stage = ys ? pl->ac_stage : (int)(((size_t)pl->col_smem - adj_cols_fixed<G>(false)) & ~size_t(15));
+  const int stage = ys ? pl->ac_stage : (int)(((size_t)pl->acol_smem - adj_cols_fixed<G>(false)) & ~size_t(15));
   ProfScope ps(pl, MRF_K_ADJ_COLS, st);
-  k_adj_cols<G><<<pgrid(pl, pl->occ_ac, items), cols_threads<G>(), pl->col_smem, st>>>(pl->dp(), y, H, l0, nb, ys, stage);
+  k_adj_cols<G><<<pgrid(pl, pl->occ_ac, items), cols_threads<G>(), pl->acol_smem, st>>>(pl->dp(), y, H, l0, nb, ys, stage);
   return check_launch("k_adj_cols");
 }
 template <int G>
@@ -660,6 +689,11 @@ mrf_status mrf_plan_create(const mrf_plan_desc* d, mrf_plan* out) {
   mrf_plan_s* pl = new mrf_plan_s();
   pl->N = N; pl->G = G; pl->L = L; pl->M = M; pl->R = R; pl->C = C; pl->W = W; pl->S = G / SW;
   pl->recw = (2 + 2 * W + 3) & ~3;
+  if (const char* e = std::getenv("MRF_DBG")) pl->dbg = std::atoi(e);
+  if (pl->dbg & 2) {
+    if (cudaMalloc((void**)&pl->dbgbuf, 32 * sizeof(long long)) != cudaSuccess) return fail(MRF_ENOMEM, "dbgbuf");
+    cudaMemset(pl->dbgbuf, 0, 32 * sizeof(long long));
+  }
   pl->ystage = (M % 2 == 0 && (size_t)M * sizeof(float2) <= (size_t)kYBytes) ? 1 : 0;
   {
     int nsm = 0;
@@ -827,12 +861,13 @@ mrf_status mrf_plan_create(const mrf_plan_desc* d, mrf_plan* out) {
   if (d->coils && C >= 1) {
     if ((s = dev_alloc(pl, &pl->coils, (size_t)C * N * N))) return bail(s);
   }
-  pl->nlanes = L > bf ? 2 : 1;
-  if (const char* e = std::getenv("MRF_LANES")) pl->nlanes = std::max(1, std::min(2, std::atoi(e)));
+  pl->nlanes = std::min(kDefaultLanes, (L + bf - 1) / bf);
+  if (const char* e = std::getenv("MRF_LANES")) pl->nlanes = std::max(1, std::min(kMaxLanes, std::atoi(e)));
   if (pl->nlanes > 1) {
-    if ((s = dev_alloc(pl, &pl->Hs[1], (size_t)bf * C * N * G)) || (s = dev_alloc(pl, &pl->ybufs[1], (size_t)bf * C * M)))
-      return bail(s);
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 1; i < pl->nlanes; ++i)
+      if ((s = dev_alloc(pl, &pl->Hs[i], (size_t)bf * C * N * G)) || (s = dev_alloc(pl, &pl->ybufs[i], (size_t)bf * C * M)))
+        return bail(s);
+    for (int i = 0; i < pl->nlanes; ++i) {
       if (cudaStreamCreateWithFlags(&pl->lane[i], cudaStreamNonBlocking) != cudaSuccess ||
           cudaEventCreateWithFlags(&pl->ev_join[i], cudaEventDisableTiming) != cudaSuccess)
         return bail(fail(MRF_ECUDA, "stream/event creation failed"));

@@ -37,4 +37,5 @@ for _ in range(a.reps):
 if a.cg:
     pl.dc_cg(y, mu=0.01, n_iter=a.cg)
 torch.cuda.synchronize()
+pl.close()
 print("ok", L)
