@@ -320,3 +320,54 @@ def test_invalid_calls(mrf):
         pl.dc_cg(dev(np.zeros(pl.y_shape, np.complex64)), n_iter=-1)
     with pytest.raises(mrf.MrfError):   # host and device pointers mixed
         pl.forward(xd, torch.zeros(pl.y_shape, dtype=torch.complex64))
+
+
+# ------------------------------------------------------------------------ NCCL path, graphs
+def test_cg_with_nccl_communicator_single_rank(mrf):
+    """mrf_dc_cg through a 1-rank NCCL communicator (the all-reduce calls of the multi-GPU path
+    run; with one rank the result must equal the communicator-free solve)."""
+    import ctypes
+    cfg, traj, coils, frames, x = setup("pr1")
+    y = on.forward(x, traj, None, cfg.W).astype(np.complex64)
+    buf = (ctypes.c_ubyte * 128)()
+    assert mrf.lib.mrf_nccl_get_unique_id(ctypes.cast(buf, ctypes.c_void_p)) == 0, mrf.lib.mrf_last_error()
+    comm = ctypes.c_void_p()
+    assert mrf.lib.mrf_nccl_comm_init(ctypes.byref(comm), 1, ctypes.cast(buf, ctypes.c_void_p), 0, 0) == 0, \
+        mrf.lib.mrf_last_error()
+    try:
+        pl_c = plan_for(mrf, cfg, traj, None, frames, nccl_comm=comm.value)
+        pl_0 = plan_for(mrf, cfg, traj, None, frames)
+        xc, ic = pl_c.dc_cg(dev(y), mu=cfg.mu, n_iter=cfg.cg_iters)
+        x0, i0 = pl_0.dc_cg(dev(y), mu=cfg.mu, n_iter=cfg.cg_iters)
+        assert np.array_equal(host(xc), host(x0))
+        assert ic["history"] == i0["history"]
+        pl_c.close()
+    finally:
+        mrf.nccl_comm_destroy(comm.value)
+
+
+def test_operators_graph_capturable(mrf):
+    """forward / adjoint / normal on device pointers allocate nothing and sync nothing, so a CUDA
+    graph of them replays to the same result (multi-batch plan: the fork/join lanes are captured)."""
+    cfg, traj, coils, frames, x = setup("cfg2", frames=range(40))
+    pl = plan_for(mrf, cfg, traj, coils, frames, batch_frames=8)
+    xd = dev(x)
+    y = torch.empty(pl.y_shape, dtype=torch.complex64, device="cuda")
+    xn = torch.empty(pl.x_shape, dtype=torch.complex64, device="cuda")
+    ref_y = host(pl.forward(xd)).copy()
+    ref_n = host(pl.normal(xd, mu=0.01)).copy()
+    s = torch.cuda.Stream()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(s):
+        pl.forward(xd, y=y)          # warm-up on the capture stream
+        pl.normal(xd, mu=0.01, out=xn)
+        with torch.cuda.graph(g, stream=s):
+            pl.forward(xd, y=y)
+            pl.normal(xd, mu=0.01, out=xn)
+    y.zero_()
+    xn.zero_()
+    g.replay()
+    torch.cuda.synchronize()
+    assert np.array_equal(host(y), ref_y)
+    assert rel(host(xn), ref_n) <= 1e-6
