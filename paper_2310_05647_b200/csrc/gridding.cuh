@@ -87,6 +87,12 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   }
 }
 
+// Programmatic dependent launch: the next kernel in the stream may start its prologue while this
+// one drains; every kernel waits for its predecessor's completion before touching global data
+// that a predecessor produces or consumes.
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // float2 += v in shared memory (64-bit CAS; no native shared float add on sm_100)
 __device__ __forceinline__ void smem_add2(float2* a, float2 v) {
   unsigned long long* q = reinterpret_cast<unsigned long long*>(a);
@@ -238,7 +244,7 @@ template <int G, int MODE>
 __global__ void __launch_bounds__(kRowThreads)
 k_fwd_rows(DevPlan p, const float2* __restrict__ x, float2* __restrict__ H, int l0, int nb,
            float2* __restrict__ cg_r, float2* __restrict__ cg_p, float2* __restrict__ cg_x,
-           const double* __restrict__ cg_ab) {
+           const double* __restrict__ cg_ab, float2* __restrict__ yzero, long long nyzero) {
   using Rc = RowCfg<G>;
   constexpr int P = Rc::P, Q = Rc::Q, T = Rc::T, N = Rc::N, RPC = Rc::RPC, A = Q / T, B = P / T;
   constexpr int NRB = N / RPC, S = G / SW, NST = MODE == 1 ? 3 : 1;
@@ -260,6 +266,11 @@ k_fwd_rows(DevPlan p, const float2* __restrict__ x, float2* __restrict__ H, int 
   for (int i = tid; i < G; i += kRowThreads) stw[i] = p.tw[i];
   for (int i = tid; i < N; i += kRowThreads) sdap[i] = p.dap[i];
   __syncthreads();
+  pdl_launch_dependents();
+  pdl_wait();
+  // zero the k-space batch buffer the following column pass accumulates into
+  for (long long i = blockIdx.x * (long long)kRowThreads + tid; i < nyzero; i += (long long)gridDim.x * kRowThreads)
+    yzero[i] = make_float2(0.f, 0.f);
   auto issue = [&](int item) {
     const int c = item % C, rb = (item / C) % NRB, bl = item / (C * NRB);
     const size_t off = ((size_t)(l0 + bl) * N + (size_t)rb * RPC) * N;
@@ -277,7 +288,7 @@ k_fwd_rows(DevPlan p, const float2* __restrict__ x, float2* __restrict__ H, int 
   uint32_t ph = 0;
   if (tid == 0 && item < n_items) issue(item);
   float beta = 0.f, alpha = 0.f;
-  if (MODE == 1) {
+  if (MODE == 1) {   // after pdl_wait: written by the previous CG scalar kernel
     alpha = (float)cg_ab[0];
     beta = (float)cg_ab[1];
   }
@@ -375,6 +386,8 @@ k_fwd_cols(DevPlan p, const float2* __restrict__ H, float2* __restrict__ y, int 
   }
   for (int i = tid; i < G; i += blockDim.x) stw[i] = p.tw[i];
   __syncthreads();
+  pdl_launch_dependents();
+  pdl_wait();
   auto chunk_of = [&](int item) -> int2 {
     const int fc = item / S, s = item % S;
     return __ldg(p.ftab + __ldg(p.fil + l0 + fc / C) * S + s);
@@ -544,6 +557,8 @@ k_adj_cols(DevPlan p, const float2* __restrict__ y, float2* __restrict__ H, int 
   for (int i = tid; i < G; i += blockDim.x) stw[i] = p.tw[i];
   for (int i = tid; i < G * SW; i += blockDim.x) strip[i] = make_float2(0.f, 0.f);
   __syncthreads();
+  pdl_launch_dependents();
+  pdl_wait();
   auto chunk_of = [&](int item) -> int2 {
     const int fc = item / S, s = item % S;
     return __ldg(p.atab + __ldg(p.fil + l0 + fc / C) * S + s);
@@ -696,6 +711,8 @@ k_adj_rows(DevPlan p, const float2* __restrict__ H, float2* __restrict__ out, co
   for (int i = tid; i < G; i += kRowThreads) stw[i] = p.tw[i];
   for (int i = tid; i < N; i += kRowThreads) sdap[i] = p.dap[i];
   __syncthreads();
+  pdl_launch_dependents();
+  pdl_wait();
   // sub-item = (item, coil): the H rows of one frame-coil and row block, S chunks of HBLK bytes
   auto issue_h = [&](int item, int c) {   // called by warp 0: the row block is one contiguous copy
     const int rb = item % NRB, bl = item / NRB;

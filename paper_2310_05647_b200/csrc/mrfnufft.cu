@@ -319,33 +319,57 @@ static mrf_status setup_kernels(mrf_plan_s* pl) {
   return MRF_OK;
 }
 
+// Launch with programmatic stream serialisation (PDL): the kernel's prologue overlaps the
+// predecessor's tail; the kernel itself calls griddepcontrol.wait before touching produced data.
+static bool g_pdl = [] {
+  const char* e = std::getenv("MRF_PDL");
+  return !(e && e[0] == '0');
+}();
+
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_pdl(void (*kern)(KArgs...), int grid, int block, size_t smem, cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = g_pdl ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
 static int pgrid(mrf_plan_s* pl, int occ, long long items) {
   return (int)std::max<long long>(1, std::min<long long>(items, (long long)occ * pl->nsm));
 }
 
 template <int G>
-static mrf_status launch_fwd_rows(mrf_plan_s* pl, const float2* x, float2* H, int l0, int nb, cudaStream_t st) {
+static mrf_status launch_fwd_rows(mrf_plan_s* pl, const float2* x, float2* H, int l0, int nb, cudaStream_t st,
+                                  float2* yzero = nullptr, long long nyzero = 0) {
   const long long items = (long long)nb * (pl->N / RowCfg<G>::RPC) * pl->C;
   ProfScope ps(pl, MRF_K_FWD_ROWS, st);
-  k_fwd_rows<G, 0><<<pgrid(pl, pl->occ_fr0, items), kRowThreads, fwd_rows_smem<G>(1), st>>>(
-      pl->dp(), x, H, l0, nb, nullptr, nullptr, nullptr, nullptr);
-  return check_launch("k_fwd_rows");
+  CUDA_TRY(launch_pdl(k_fwd_rows<G, 0>, pgrid(pl, pl->occ_fr0, items), kRowThreads, fwd_rows_smem<G>(1), st, pl->dp(),
+                      x, H, l0, nb, nullptr, nullptr, nullptr, nullptr, yzero, nyzero));
+  return MRF_OK;
 }
 template <int G>
-static mrf_status launch_fwd_rows_cg(mrf_plan_s* pl, float2* x, float2* H, int l0, int nb, cudaStream_t st) {
+static mrf_status launch_fwd_rows_cg(mrf_plan_s* pl, float2* x, float2* H, int l0, int nb, cudaStream_t st,
+                                     float2* yzero, long long nyzero) {
   const long long items = (long long)nb * (pl->N / RowCfg<G>::RPC) * pl->C;
   ProfScope ps(pl, MRF_K_FWD_ROWS, st);
-  k_fwd_rows<G, 1><<<pgrid(pl, pl->occ_fr1, items), kRowThreads, fwd_rows_smem<G>(3), st>>>(
-      pl->dp(), nullptr, H, l0, nb, pl->r, pl->p, x, &pl->sc->alpha);
-  return check_launch("k_fwd_rows<cg>");
+  CUDA_TRY(launch_pdl(k_fwd_rows<G, 1>, pgrid(pl, pl->occ_fr1, items), kRowThreads, fwd_rows_smem<G>(3), st, pl->dp(),
+                      nullptr, H, l0, nb, pl->r, pl->p, x, &pl->sc->alpha, yzero, nyzero));
+  return MRF_OK;
 }
 template <int G>
 static mrf_status launch_fwd_cols(mrf_plan_s* pl, const float2* H, float2* y, int l0, int nb, cudaStream_t st) {
   const long long items = (long long)nb * pl->C * pl->S;
   ProfScope ps(pl, MRF_K_FWD_COLS, st);
-  k_fwd_cols<G><<<pgrid(pl, pl->occ_fc, items), cols_threads<G>(), pl->col_smem, st>>>(pl->dp(), H, y, l0, nb,
-                                                                                      pl->fc_stage);
-  return check_launch("k_fwd_cols");
+  CUDA_TRY(launch_pdl(k_fwd_cols<G>, pgrid(pl, pl->occ_fc, items), cols_threads<G>(), pl->col_smem, st, pl->dp(), H, y,
+                      l0, nb, pl->fc_stage));
+  return MRF_OK;
 }
 template <int G>
 static mrf_status launch_adj_cols(mrf_plan_s* pl, const float2* y, float2* H, int l0, int nb, cudaStream_t st) {
@@ -353,17 +377,18 @@ static mrf_status launch_adj_cols(mrf_plan_s* pl, const float2* y, float2* H, in
   const int ys = pl->ystage && ((uintptr_t)y % 16 == 0);
   const int stage = ys ? pl->ac_stage : (int)(((size_t)pl->acol_smem - adj_cols_fixed<G>(false)) & ~size_t(15));
   ProfScope ps(pl, MRF_K_ADJ_COLS, st);
-  k_adj_cols<G><<<pgrid(pl, pl->occ_ac, items), cols_threads<G>(), pl->acol_smem, st>>>(pl->dp(), y, H, l0, nb, ys, stage);
-  return check_launch("k_adj_cols");
+  CUDA_TRY(launch_pdl(k_adj_cols<G>, pgrid(pl, pl->occ_ac, items), cols_threads<G>(), pl->acol_smem, st, pl->dp(), y, H,
+                      l0, nb, ys, stage));
+  return MRF_OK;
 }
 template <int G>
 static mrf_status launch_adj_rows(mrf_plan_s* pl, const float2* H, float2* out, const float2* xin, float mu, int l0,
                                   int nb, double2* dot, cudaStream_t st) {
   const long long items = (long long)nb * (pl->N / RowCfg<G>::RPC);
   ProfScope ps(pl, MRF_K_ADJ_ROWS, st);
-  k_adj_rows<G><<<pgrid(pl, pl->occ_ar, items), kRowThreads, adj_rows_smem<G>(), st>>>(pl->dp(), H, out, xin, mu, l0, nb,
-                                                                                      dot);
-  return check_launch("k_adj_rows");
+  CUDA_TRY(launch_pdl(k_adj_rows<G>, pgrid(pl, pl->occ_ar, items), kRowThreads, adj_rows_smem<G>(), st, pl->dp(), H, out,
+                      xin, mu, l0, nb, dot));
+  return MRF_OK;
 }
 
 static mrf_status memset_async(mrf_plan_s* pl, void* ptr, size_t bytes, cudaStream_t st) {
@@ -442,9 +467,9 @@ static mrf_status run_normal(mrf_plan_s* pl, const float2* x, float2* out, float
     cudaStream_t s = ln.stream(b);
     float2* H = pl->Hs[ln.slot(b)];
     float2* yb = pl->ybufs[ln.slot(b)];
-    if (cg && pl->C == 1) MRF_TRY(launch_fwd_rows_cg<G>(pl, xsol, H, l0, nb, s));
-    else MRF_TRY(launch_fwd_rows<G>(pl, x, H, l0, nb, s));
-    MRF_TRY(memset_async(pl, yb, (size_t)nb * pl->C * pl->M * sizeof(float2), s));
+    const long long ny = (long long)nb * pl->C * pl->M;   // zeroed by the row pass for the gather
+    if (cg && pl->C == 1) MRF_TRY(launch_fwd_rows_cg<G>(pl, xsol, H, l0, nb, s, yb, ny));
+    else MRF_TRY(launch_fwd_rows<G>(pl, x, H, l0, nb, s, yb, ny));
     MRF_TRY(launch_fwd_cols<G>(pl, H, yb, l0, nb, s));
     MRF_TRY(launch_adj_cols<G>(pl, yb, H, l0, nb, s));
     MRF_TRY(launch_adj_rows<G>(pl, H, out, (mu != 0.f || cg) ? x : nullptr, mu, l0, nb, cg ? pl->dotp : nullptr, s));
