@@ -24,7 +24,7 @@
 namespace mrf {
 
 constexpr int SW = 16;             // columns per strip (>= W: a point's x-taps touch <= 2 strips)
-constexpr int kYBytes = 16384;     // largest y[fc] staged in shared memory by k_adj_cols
+constexpr int kYBytes = 32768;     // largest y[fc] staged in shared memory by k_adj_cols (M <= 4096)
 constexpr int kChunkHdr = 8;       // header words of a strip chunk
 constexpr int kRowThreads = 128;
 
@@ -755,6 +755,16 @@ k_adj_rows(DevPlan p, const float2* __restrict__ H, float2* __restrict__ out, co
           v[a][n1] = hin[rloc * G + pos];
         }
       }
+      // this coil's sensitivities at the thread's output pixels: loaded now, used after the FFT
+      float2 cv[B][Q / 2];
+      if (p.coils) {
+        const float2* sr = p.coils + ((size_t)c * N + iy) * N;
+#pragma unroll
+        for (int b = 0; b < B; ++b)
+#pragma unroll
+          for (int kk = 0; kk < Q / 2; ++kk)
+            cv[b][kk] = __ldg(sr + grid_to_img<G>(t + T * b + P * (kk < Q / 4 ? kk : kk + Q / 2)));
+      }
       __syncthreads();
       if (warp == 0) {
         if (c + 1 < C) {
@@ -773,7 +783,6 @@ k_adj_rows(DevPlan p, const float2* __restrict__ H, float2* __restrict__ out, co
         for (int k1 = 0; k1 < P; ++k1) myex[n2 * (P + 1) + k1] = cmulc(v[a][k1], stw[k1 * Q + n2]);
       }
       __syncwarp();
-      const float2* sr = p.coils ? p.coils + ((size_t)c * N + iy) * N : nullptr;
 #pragma unroll
       for (int b = 0; b < B; ++b) {
         const int k1 = t + T * b;
@@ -785,7 +794,7 @@ k_adj_rows(DevPlan p, const float2* __restrict__ H, float2* __restrict__ out, co
         for (int kk = 0; kk < Q / 2; ++kk) {
           const int k2 = kk < Q / 4 ? kk : kk + Q / 2;
           float2 val = w[k2];
-          if (sr) val = cmulc(val, __ldg(sr + grid_to_img<G>(k1 + P * k2)));
+          if (p.coils) val = cmulc(val, cv[b][kk]);
           acc[b][kk] = cadd(acc[b][kk], val);
         }
       }
