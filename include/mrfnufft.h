@@ -60,6 +60,12 @@ typedef enum {
 /* flags */
 #define MRF_DEAPOD_ANALYTIC 0u   /* psi = continuous FT of the KB kernel (default)               */
 #define MRF_DEAPOD_DISCRETE 1u   /* psi = DFT of the integer-sampled kernel (exact on-grid)      */
+/* mrf_normal and mrf_dc_cg evaluate A^H A by Toeplitz embedding:
+ * A^H A x = sum_c conj(S_c) crop(IFFT_2N(T_r . FFT_2N(pad(S_c x)))), T_r the real 2N x 2N spectrum of
+ * the exact point-spread function of interleaf r (computed in float64 at plan creation).  This is
+ * the exact (NUDFT) normal operator up to fp32 rounding -- it differs from the gridding A^H(A x) by
+ * the NUFFT approximation error (~1e-5).  forward/adjoint are unchanged.  Costs R*(2N)^2*4 bytes. */
+#define MRF_NORMAL_TOEPLITZ 2u
 
 typedef struct {
   int N;                        /* square image side, even; G = sigma*N must be a supported size */
@@ -73,7 +79,7 @@ typedef struct {
   const float* coils;           /* HOST [C][N][N] complex64, or NULL with C == 1 => S = 1       */
   int W;                        /* Kaiser-Bessel width, 2..16                                    */
   float sigma;                  /* oversampling factor; 2.0 supported                            */
-  unsigned flags;               /* MRF_DEAPOD_*                                                  */
+  unsigned flags;               /* MRF_DEAPOD_* | MRF_NORMAL_TOEPLITZ                            */
   int device;                   /* CUDA device ordinal                                           */
   void* stream;                 /* cudaStream_t for create-time uploads (NULL = legacy default)  */
   void* nccl_comm;              /* ncclComm_t shared by all ranks of one solve, or NULL          */

@@ -21,6 +21,7 @@ LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libmrfnufft
 
 MRF_DEAPOD_ANALYTIC = 0
 MRF_DEAPOD_DISCRETE = 1
+MRF_NORMAL_TOEPLITZ = 2
 KERNEL_CLASSES = {"fwd_rows": 0, "fwd_cols": 1, "adj_cols": 2, "adj_rows": 3, "cg_vec": 4, "other": 5}
 STATUS = {0: "MRF_OK", 1: "MRF_EINVAL", 2: "MRF_ENOMEM", 3: "MRF_ECUDA", 4: "MRF_ENCCL",
           5: "MRF_EUNSUPPORTED", 6: "MRF_ENUMERIC"}
@@ -112,7 +113,7 @@ class Plan:
     """One frame shard of the multi-frame, multi-coil KB-gridding NUFFT operator (mrf_plan)."""
 
     def __init__(self, N: int, traj, L: int, *, coils=None, W: int = 6, sigma: float = 2.0,
-                 frame_interleaf=None, frame_offset: int = 0, deapod: str = "analytic",
+                 frame_interleaf=None, frame_offset: int = 0, deapod: str = "analytic", normal: str = "gridding",
                  device: Optional[int] = None, nccl_comm: Optional[int] = None, batch_frames: int = 0):
         traj_np = np.ascontiguousarray(np.asarray(traj, dtype=np.float32))
         if traj_np.ndim != 3 or traj_np.shape[2] != 2:
@@ -140,7 +141,8 @@ class Plan:
         d.C = self.C
         d.coils = None if coils_np is None else coils_np.ctypes.data
         d.W, d.sigma = self.W, self.sigma
-        d.flags = {"analytic": MRF_DEAPOD_ANALYTIC, "discrete": MRF_DEAPOD_DISCRETE}[deapod]
+        d.flags = {"analytic": MRF_DEAPOD_ANALYTIC, "discrete": MRF_DEAPOD_DISCRETE}[deapod] | \
+            {"gridding": 0, "toeplitz": MRF_NORMAL_TOEPLITZ}[normal]
         d.device = self.device
         d.stream = None
         d.nccl_comm = nccl_comm

@@ -145,6 +145,8 @@ constexpr int cols_ctas_per_sm() { return G >= 1024 ? 1 : 2; }
 template <int G>
 constexpr size_t fwd_cols_fixed() { return (size_t(G) + size_t(G / 2) * SW + size_t(G) * SW) * 8 + 16; }
 template <int G>
+constexpr size_t toep_cols_smem() { return (size_t(G) + size_t(G / 2) * SW + size_t(G) * SW) * 8 + 16; }
+template <int G>
 constexpr size_t adj_cols_fixed(bool ystage) { return (size_t(G) + size_t(G) * SW) * 8 + (ystage ? kYBytes : 0) + 16; }
 
 // ---------------------------------------------------------------------------- point records
@@ -676,6 +678,173 @@ k_adj_cols(DevPlan p, const float2* __restrict__ y, float2* __restrict__ H, int 
     pt.mark(7);
   }
   pt.report(p.dbgbuf ? p.dbgbuf + 16 : nullptr, nit);
+}
+
+// ============================================================================ Toeplitz columns
+// the normal operator A^H A x = sum_c conj(S_c) crop(IFFT(T ⊙ FFT(pad(S_c x))))
+// with T the (real) 2N-point spectrum of the point-spread function of the interleaf
+// (plan-time, see k_psf_*).  Items (fc, strip): forward column FFT of the strip (pruned input),
+// multiply by T in registers, inverse column FFT computed in the transposed split
+// (stage A = Q-point inverse DFTs over k2 on the forward's own output layout, so no exchange is
+// needed between the two transforms; one exchange; stage B = P-point inverse DFTs over k1), and
+// the N kept rows are stored row-major for k_adj_rows.  No gather, no spread, no k-space buffer.
+template <int G>
+__global__ void __launch_bounds__(SW * FFTShape<G>::T, (G >= 1024 ? 1 : 2))
+k_toep_cols(DevPlan p, const float2* __restrict__ Hf, float2* __restrict__ Ha, const float* __restrict__ psf, int l0,
+            int nb) {
+  using F = FFTShape<G>;
+  constexpr int P = F::P, Q = F::Q, T = F::T, N = G / 2, A = Q / T, B = P / T, S = G / SW;
+  constexpr uint32_t STRIP_IN = N * SW * sizeof(float2);
+  extern __shared__ __align__(128) unsigned char smraw[];
+  float2* stw = reinterpret_cast<float2*>(smraw);
+  float2* inb = stw + G;
+  float2* ex = inb + N * SW;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(ex + G * SW);
+  const int C = p.C;
+  const int n_items = nb * C * S;
+  const int tid = threadIdx.x, c = tid % SW, t = tid / SW;
+  if (tid == 0) {
+    mbar_init(bar, 1);
+    fence_mbar_init();
+  }
+  for (int i = tid; i < G; i += blockDim.x) stw[i] = p.tw[i];
+  __syncthreads();
+  pdl_launch_dependents();
+  pdl_wait();
+  auto issue_in = [&](int item) {
+    mbar_expect_tx(bar, STRIP_IN);
+    bulk_g2s(inb, Hf + (size_t)item * (N * SW), STRIP_IN, bar);
+  };
+  int item = blockIdx.x;
+  if (tid == 0 && item < n_items) issue_in(item);
+  for (int k = 0; item < n_items; item += gridDim.x, ++k) {
+    const int fc = item / S, s = item % S;
+    const int next = item + gridDim.x;
+    // PSF values at this thread's forward-output rows k1 + P k2: issued now, used after the FFT
+    const int r = __ldg(p.fil + l0 + fc / C);
+    const float* ps = psf + ((size_t)(r * S + s) * G) * SW + c;
+    float tp[B][Q];
+#pragma unroll
+    for (int b = 0; b < B; ++b)
+#pragma unroll
+      for (int k2 = 0; k2 < Q; ++k2) tp[b][k2] = __ldg(ps + (size_t)(t + T * b + P * k2) * SW);
+    mbar_wait(bar, k & 1);
+    float2 v[A][P];
+#pragma unroll
+    for (int a = 0; a < A; ++a) {
+      const int n2 = t + T * a;
+#pragma unroll
+      for (int n1 = 0; n1 < P; ++n1) {
+        v[a][n1] = (n1 < P / 4 || n1 >= 3 * P / 4) ? inb[grid_to_img<G>(Q * n1 + n2) * SW + c] : make_float2(0.f, 0.f);
+      }
+    }
+    __syncthreads();
+    if (tid == 0 && next < n_items) {
+      fence_proxy_async();
+      issue_in(next);
+    }
+    // forward column FFT
+#pragma unroll
+    for (int a = 0; a < A; ++a) {
+      const int n2 = t + T * a;
+      dft_halfzero<P, -1>(v[a]);
+#pragma unroll
+      for (int k1 = 0; k1 < P; ++k1) ex[(n2 * P + k1) * SW + c] = cmul(v[a][k1], stw[k1 * Q + n2]);
+    }
+    __syncthreads();
+    float2 w[B][Q];
+#pragma unroll
+    for (int b = 0; b < B; ++b) {
+      const int k1 = t + T * b;
+#pragma unroll
+      for (int n2 = 0; n2 < Q; ++n2) w[b][n2] = ex[(n2 * P + k1) * SW + c];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int b = 0; b < B; ++b) {
+      const int k1 = t + T * b;
+      dft<Q, -1>(w[b]);                          // w[b][k2] = X[k1 + P k2]
+#pragma unroll
+      for (int k2 = 0; k2 < Q; ++k2) w[b][k2] = cscale(w[b][k2], tp[b][k2]);
+      dft<Q, +1>(w[b]);                          // stage A of the inverse: index n2
+#pragma unroll
+      for (int n2 = 0; n2 < Q; ++n2) ex[(n2 * P + k1) * SW + c] = cmulc(w[b][n2], stw[k1 * Q + n2]);
+    }
+    __syncthreads();
+    float2* Hc = Ha + (size_t)fc * N * G + (size_t)s * SW + c;    // row-major [fc][iy][G]
+#pragma unroll
+    for (int a = 0; a < A; ++a) {
+      const int n2 = t + T * a;
+      float2 u[P];
+#pragma unroll
+      for (int k1 = 0; k1 < P; ++k1) u[k1] = ex[(n2 * P + k1) * SW + c];
+      dft<P, +1>(u);                             // stage B: index n1, row n2 + Q n1
+#pragma unroll
+      for (int n1 = 0; n1 < P; ++n1) {
+        if (n1 < P / 4 || n1 >= 3 * P / 4) Hc[(size_t)grid_to_img<G>(n2 + Q * n1) * G] = u[n1];
+      }
+    }
+    __syncthreads();   // exchange buffer free for the next item
+  }
+}
+
+// ---------------------------------------------------------------------------- PSF (plan time)
+// T[my][mx] = 1/(G^2 N^2) sum_j D(ky_j - my/G) D(kx_j - mx/G),
+// D(theta) = sum_{d=-(N-1)}^{N-1} e^{i 2 pi d theta} = sin((2N-1) pi theta) / sin(pi theta):
+// the G-point DFT of the circulant embedding of K(d) = 1/N^2 sum_j e^{+i 2 pi k_j . d}, the
+// kernel of A^H A for one coil (K is Hermitian, so T is real).  Float64 throughout.
+__global__ void k_psf_dirichlet(const float* __restrict__ traj, int M, int N, int G, int axis, double* __restrict__ D) {
+  const long long total = (long long)M * G;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
+    const int j = (int)(i / G), m = (int)(i % G);
+    const double th = (double)traj[2 * j + axis] - (double)m / G;
+    const double den = sinpi(th);
+    D[i] = fabs(den) < 1e-12 ? (double)(2 * N - 1) * cospi(th * (2 * N - 2)) : sinpi((2 * N - 1) * th) / den;
+  }
+}
+
+// out[my][mx] = scale * sum_j Dy[j][my] Dx[j][mx]  (64 x 64 tile per 256-thread block)
+__global__ void __launch_bounds__(256) k_psf_gemm(const double* __restrict__ Dy, const double* __restrict__ Dx, int M,
+                                                  int G, double scale, double* __restrict__ out) {
+  __shared__ double sy[16][64], sx[16][64];
+  const int ty = threadIdx.x / 16, tx = threadIdx.x % 16;
+  const int my0 = blockIdx.y * 64, mx0 = blockIdx.x * 64;
+  double acc[4][4] = {};
+  for (int j0 = 0; j0 < M; j0 += 16) {
+    for (int i = threadIdx.x; i < 16 * 64; i += 256) {
+      const int jj = i / 64, mm = i % 64, j = j0 + jj;
+      sy[jj][mm] = (j < M && my0 + mm < G) ? Dy[(size_t)j * G + my0 + mm] : 0.0;
+      sx[jj][mm] = (j < M && mx0 + mm < G) ? Dx[(size_t)j * G + mx0 + mm] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int jj = 0; jj < 16; ++jj) {
+      double a[4], b[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) { a[u] = sy[jj][ty + 16 * u]; b[u] = sx[jj][tx + 16 * u]; }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) acc[u][v] = fma(a[u], b[v], acc[u][v]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int u = 0; u < 4; ++u)
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      const int my = my0 + ty + 16 * u, mx = mx0 + tx + 16 * v;
+      if (my < G && mx < G) out[(size_t)my * G + mx] = scale * acc[u][v];
+    }
+}
+
+// psf[r][s][my][16] (fp32) <- T[my][mx] (fp64), s = mx / 16
+__global__ void k_psf_store(const double* __restrict__ Tm, int G, float* __restrict__ psf_r) {
+  const int total = G * G;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const int my = i / G, mx = i % G;
+    psf_r[((size_t)(mx / SW) * G + my) * SW + (mx % SW)] = (float)Tm[i];
+  }
 }
 
 // ============================================================================ adjoint rows

@@ -82,6 +82,7 @@ struct mrf_plan_s {
   int ystage = 0;           // k_adj_cols stages y[fc] in shared memory (M even, M*8 <= kYBytes)
   int occ_fr0 = 1, occ_fr1 = 1, occ_fc = 1, occ_ac = 1, occ_ar = 1;   // resident CTAs per SM
   int fc_stage = 0, ac_stage = 0;   // chunk staging bytes of the column kernels
+  int occ_tc = 1;
   int col_smem = 0;                 // dynamic shared memory of k_fwd_cols
   int acol_smem = 0;                // dynamic shared memory of k_adj_cols
   void* nccl_comm = nullptr;
@@ -103,6 +104,9 @@ struct mrf_plan_s {
   cudaStream_t lane[kMaxLanes] = {};
   cudaEvent_t ev_fork = nullptr, ev_join[kMaxLanes] = {};
   float2* Hs[kMaxLanes] = {};      // [bf*C][N][G] half grid per lane
+  float2* Has[kMaxLanes] = {};     // Toeplitz plans: the adjoint-side half grid per lane
+  float* psf = nullptr;            // Toeplitz plans: [R][S][G][16] real PSF spectra
+  float* ones = nullptr;           // [N] of 1.0 (the Toeplitz path has no deapodisation)
   float2* ybufs[kMaxLanes] = {};   // [bf*C][M] per lane
   float2* r = nullptr;       // CG vectors [L][N][N]
   float2* p = nullptr;
@@ -226,7 +230,10 @@ static void free_plan(mrf_plan_s* pl) {
     }
     cudaFree(pl->dbgbuf);
   }
+  if (pl->psf) cudaFree(pl->psf);
+  if (pl->ones) cudaFree(pl->ones);
   for (int i = 0; i < kMaxLanes; ++i) {
+    if (pl->Has[i]) cudaFree(pl->Has[i]);
     if (pl->Hs[i]) cudaFree(pl->Hs[i]);
     if (pl->ybufs[i]) cudaFree(pl->ybufs[i]);
   }
@@ -306,6 +313,8 @@ static mrf_status setup_kernels(mrf_plan_s* pl) {
   CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pl->occ_fr1, k_fwd_rows<G, 1>, kRowThreads, s_fr1));
   CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pl->occ_ar, k_adj_rows<G>, kRowThreads, s_ar));
   CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pl->occ_fc, k_fwd_cols<G>, ncol, s_col));
+  CUDA_TRY(cudaFuncSetAttribute(k_toep_cols<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)toep_cols_smem<G>()));
+  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pl->occ_tc, k_toep_cols<G>, ncol, toep_cols_smem<G>()));
   CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pl->occ_ac, k_adj_cols<G>, ncol, s_acol));
   if (pl->occ_fr0 < 1 || pl->occ_fr1 < 1 || pl->occ_ar < 1 || pl->occ_fc < 1 || pl->occ_ac < 1)
     return fail(MRF_EUNSUPPORTED, "a kernel does not fit on an SM");
@@ -388,6 +397,15 @@ static mrf_status launch_adj_rows(mrf_plan_s* pl, const float2* H, float2* out, 
   ProfScope ps(pl, MRF_K_ADJ_ROWS, st);
   CUDA_TRY(launch_pdl(k_adj_rows<G>, pgrid(pl, pl->occ_ar, items), kRowThreads, adj_rows_smem<G>(), st, pl->dp(), H, out,
                       xin, mu, l0, nb, dot));
+  return MRF_OK;
+}
+
+template <int G>
+static mrf_status launch_toep_cols(mrf_plan_s* pl, const float2* Hf, float2* Ha, int l0, int nb, cudaStream_t st) {
+  const long long items = (long long)nb * pl->C * pl->S;
+  ProfScope ps(pl, MRF_K_FWD_COLS, st);
+  CUDA_TRY(launch_pdl(k_toep_cols<G>, pgrid(pl, pl->occ_tc, items), cols_threads<G>(), toep_cols_smem<G>(), st, pl->dp(),
+                      Hf, Ha, pl->psf, l0, nb));
   return MRF_OK;
 }
 
@@ -477,6 +495,32 @@ static mrf_status run_normal(mrf_plan_s* pl, const float2* x, float2* out, float
   return ln.end();
 }
 
+// Toeplitz form of run_normal (plans with MRF_NORMAL_TOEPLITZ): row FFT of pad(S_c x) (no
+// deapodisation), k_toep_cols (column FFT, x PSF spectrum, column iFFT), row iFFT + conj-coil sum.
+template <int G>
+static mrf_status run_normal_toeplitz(mrf_plan_s* pl, const float2* x, float2* out, float mu, int cg, float2* xsol,
+                                      cudaStream_t st) {
+  Lanes ln(pl, st, n_batches(pl));
+  MRF_TRY(ln.begin());
+  float* dap = pl->dap;
+  pl->dap = pl->ones;   // dp() copies: the launches below see unit deapodisation
+  mrf_status rc = MRF_OK;
+  for (int b = 0, l0 = 0; l0 < pl->L && rc == MRF_OK; ++b, l0 += pl->bf) {
+    const int nb = std::min(pl->bf, pl->L - l0);
+    cudaStream_t s = ln.stream(b);
+    float2* Hf = pl->Hs[ln.slot(b)];
+    float2* Ha = pl->Has[ln.slot(b)];
+    if (cg && pl->C == 1) rc = launch_fwd_rows_cg<G>(pl, xsol, Hf, l0, nb, s, nullptr, 0);
+    else rc = launch_fwd_rows<G>(pl, x, Hf, l0, nb, s);
+    if (rc == MRF_OK) rc = launch_toep_cols<G>(pl, Hf, Ha, l0, nb, s);
+    if (rc == MRF_OK)
+      rc = launch_adj_rows<G>(pl, Ha, out, (mu != 0.f || cg) ? x : nullptr, mu, l0, nb, cg ? pl->dotp : nullptr, s);
+  }
+  pl->dap = dap;
+  MRF_TRY(rc);
+  return ln.end();
+}
+
 #define DISPATCH_G(pl, fn, ...)                               \
   switch ((pl)->G) {                                          \
     case 64: return fn<64>(__VA_ARGS__);                      \
@@ -495,6 +539,9 @@ static mrf_status do_adjoint(mrf_plan_s* pl, const float2* y, float2* x, cudaStr
 }
 static mrf_status do_normal(mrf_plan_s* pl, const float2* x, float2* out, float mu, cudaStream_t st, int cg = 0,
                             float2* xsol = nullptr) {
+  if (pl->flags & MRF_NORMAL_TOEPLITZ) {
+    DISPATCH_G(pl, run_normal_toeplitz, pl, x, out, mu, cg, xsol, st);
+  }
   DISPATCH_G(pl, run_normal, pl, x, out, mu, cg, xsol, st);
 }
 static mrf_status do_setup(mrf_plan_s* pl) { DISPATCH_G(pl, setup_kernels, pl); }
@@ -659,6 +706,46 @@ static mrf_status ensure_staging(mrf_plan_s* pl, bool need_z) {
 }
 
 
+// Toeplitz PSF spectra (MRF_NORMAL_TOEPLITZ), float64 on the device, one interleaf at a time:
+// Dirichlet factors D_x, D_y [M][G], T_r = D_y^T D_x / (G^2 N^2) (gridding.cuh k_psf_*), stored fp32.
+static mrf_status build_psf(mrf_plan_s* pl, const float* traj_host, cudaStream_t st) {
+  const int N = pl->N, G = pl->G, M = pl->M, R = pl->R;
+  MRF_TRY(dev_alloc(pl, &pl->psf, (size_t)R * G * G));
+  MRF_TRY(dev_alloc(pl, &pl->ones, (size_t)N));
+  std::vector<float> one((size_t)N, 1.0f);
+  CUDA_TRY(cudaMemcpyAsync(pl->ones, one.data(), N * sizeof(float), cudaMemcpyHostToDevice, st));
+  float* traj = nullptr;
+  double *Dx = nullptr, *Dy = nullptr, *Tm = nullptr;
+  auto cleanup = [&]() {
+    if (traj) cudaFree(traj);
+    if (Dx) cudaFree(Dx);
+    if (Dy) cudaFree(Dy);
+    if (Tm) cudaFree(Tm);
+  };
+  if (cudaMalloc((void**)&traj, (size_t)R * M * 2 * sizeof(float)) != cudaSuccess ||
+      cudaMalloc((void**)&Dx, (size_t)M * G * sizeof(double)) != cudaSuccess ||
+      cudaMalloc((void**)&Dy, (size_t)M * G * sizeof(double)) != cudaSuccess ||
+      cudaMalloc((void**)&Tm, (size_t)G * G * sizeof(double)) != cudaSuccess) {
+    cleanup();
+    cudaGetLastError();
+    return fail(MRF_ENOMEM, "PSF workspace");
+  }
+  cudaError_t e = cudaMemcpyAsync(traj, traj_host, (size_t)R * M * 2 * sizeof(float), cudaMemcpyHostToDevice, st);
+  const double scale = 1.0 / ((double)G * G * (double)N * N);
+  for (int r = 0; r < R && e == cudaSuccess; ++r) {
+    const float* tr = traj + (size_t)r * M * 2;
+    k_psf_dirichlet<<<1184, 256, 0, st>>>(tr, M, N, G, 0, Dx);
+    k_psf_dirichlet<<<1184, 256, 0, st>>>(tr, M, N, G, 1, Dy);
+    k_psf_gemm<<<dim3((G + 63) / 64, (G + 63) / 64), 256, 0, st>>>(Dy, Dx, M, G, scale, Tm);
+    k_psf_store<<<592, 256, 0, st>>>(Tm, G, pl->psf + (size_t)r * G * G);
+    e = cudaGetLastError();
+  }
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  cleanup();
+  if (e != cudaSuccess) return fail(MRF_ECUDA, std::string("PSF precompute: ") + cudaGetErrorString(e));
+  return MRF_OK;
+}
+
 // ================================================================================== C-ABI
 extern "C" {
 
@@ -688,7 +775,7 @@ mrf_status mrf_plan_create(const mrf_plan_desc* d, mrf_plan* out) {
   if (d->W < 2 || d->W > 16) return fail(MRF_EINVAL, "W must be in [2, 16]");
   if (!(d->sigma > 0.f) || !std::isfinite(d->sigma)) return fail(MRF_EINVAL, "sigma must be positive");
   if (d->batch_frames < 0) return fail(MRF_EINVAL, "batch_frames < 0");
-  if (d->flags & ~1u) return fail(MRF_EINVAL, "unknown flags");
+  if (d->flags & ~3u) return fail(MRF_EINVAL, "unknown flags");
   if ((double)d->sigma != 2.0) return fail(MRF_EUNSUPPORTED, "only sigma = 2 is supported");
   const double Gd = (double)d->sigma * d->N;
   const int G = (int)std::lround(Gd);
@@ -901,6 +988,11 @@ mrf_status mrf_plan_create(const mrf_plan_desc* d, mrf_plan* out) {
       return bail(fail(MRF_ECUDA, "event creation failed"));
   }
   if ((s = do_setup(pl))) return bail(s);
+  if (pl->flags & MRF_NORMAL_TOEPLITZ) {
+    if ((s = build_psf(pl, d->traj, st))) return bail(s);
+    for (int i = 0; i < pl->nlanes; ++i)
+      if ((s = dev_alloc(pl, &pl->Has[i], (size_t)bf * C * N * G))) return bail(s);
+  }
   for (const int2& ow : atab)   // the spread kernel needs every chunk's header, slices and cells staged
     if ((size_t)ach[ow.x + 2] * 4 > (size_t)pl->ac_stage)
       return bail(fail(MRF_EUNSUPPORTED, "a grid strip has too many occupied cells for the staging buffer"));

@@ -371,3 +371,42 @@ def test_operators_graph_capturable(mrf):
     torch.cuda.synchronize()
     assert np.array_equal(host(y), ref_y)
     assert rel(host(xn), ref_n) <= 1e-6
+
+
+# ------------------------------------------------------------------------ Toeplitz normal (f1)
+def _nudft_normal(x, traj, coils, fil, mu):
+    """The plain definition A^H A x + mu x with the direct NUDFT (oracle layer (i))."""
+    y = on.nudft_forward(x, traj, coils, frame_interleaf=fil)
+    return on.nudft_adjoint(y, traj, coils, x.shape[1], frame_interleaf=fil) + mu * x.astype(np.complex128)
+
+
+@pytest.mark.parametrize("name,frames,over", [
+    ("pr1", None, {}),
+    ("cfg2", [0, 5, 23, 199], {}),
+    ("sense", [0, 3], {"N": 64, "M": 700, "R": 4}),
+    ("stress", [0, 1], {"N": 64, "M": 1024, "R": 4, "C": 4}),
+])
+def test_toeplitz_normal_vs_nudft(mrf, name, frames, over):
+    """MRF_NORMAL_TOEPLITZ: the exact (NUDFT) normal operator up to fp32 rounding."""
+    cfg, traj, coils, frames, x = setup(name, frames=frames, **over)
+    fil = synth.frame_interleaf(frames, cfg.R)
+    pl = plan_for(mrf, cfg, traj, coils, frames, normal="toeplitz")
+    got = host(pl.normal(dev(x), mu=cfg.mu))
+    ref = _nudft_normal(x, traj, coils, fil, cfg.mu)
+    assert rel(got, ref) <= OP_TOL
+    # the gridding normal differs from the exact one by the NUFFT error only
+    grid = on.normal(x, traj, coils, cfg.W, mu=cfg.mu, frame_interleaf=fil)
+    assert rel(grid, ref) <= 1e-4
+
+
+def test_toeplitz_cg_pr1(mrf):
+    """CG with the Toeplitz normal vs the oracle CG with the exact normal (rhs from A^H y)."""
+    cfg, traj, coils, frames, x = setup("pr1")
+    y = on.forward(x, traj, None, cfg.W).astype(np.complex64)
+    H = lambda v: _nudft_normal(v, traj, None, synth.frame_interleaf(frames, cfg.R), cfg.mu)
+    rhs = ocg.dc_rhs(on.adjoint(y, traj, None, cfg.N, cfg.W), None, cfg.mu)
+    x_ref, h_ref = ocg.cg(H, rhs, np.zeros_like(rhs), cfg.cg_iters)
+    pl = plan_for(mrf, cfg, traj, None, frames, normal="toeplitz")
+    xg, info = pl.dc_cg(dev(y), mu=cfg.mu, n_iter=cfg.cg_iters)
+    assert rel(host(xg), x_ref) <= CG_TOL
+    assert np.allclose(info["history"], h_ref, rtol=1e-3, atol=0)
