@@ -410,3 +410,16 @@ def test_toeplitz_cg_pr1(mrf):
     xg, info = pl.dc_cg(dev(y), mu=cfg.mu, n_iter=cfg.cg_iters)
     assert rel(host(xg), x_ref) <= CG_TOL
     assert np.allclose(info["history"], h_ref, rtol=1e-3, atol=0)
+
+
+@pytest.mark.parametrize("N,M,L,bf", [(32, 300, 5, 2), (64, 500, 3, 0), (512, 64, 1, 0)])
+def test_toeplitz_sizes_and_batches(mrf, N, M, L, bf):
+    """Toeplitz normal for G = 64, 128, 1024, with ragged frame batches."""
+    traj = synth.spiral_trajectory(M, 2, 4, 1.5)
+    frames = list(range(L))
+    x = synth.iid_images(N, frames, 31)
+    fil = synth.frame_interleaf(frames, 2)
+    pl = mrf.Plan(N, traj, L, W=6, frame_interleaf=fil, normal="toeplitz", batch_frames=bf)
+    got = host(pl.normal(dev(x), mu=0.02))
+    ref = _nudft_normal(x, traj, None, fil, 0.02)
+    assert rel(got, ref) <= OP_TOL
