@@ -32,13 +32,15 @@ struct CGScalars;
 
 // Per (interleaf, strip) "chunks" (32-bit words, 16-byte multiples), built once at plan time.
 // Forward chunk (gather):  [0] n_rec [1..7] 0, then n_rec point records of recw words:
-//     j, taps (gy0 | tx0<<11 | ntx<<16 | cx0<<21), wx[W], wy[W] (fp32)
+//     j, taps (gy0 | cx0<<11), wx[W] (the x-weights of the taps inside the strip, starting at strip
+//     column cx0, zero past the strip's last tap), wy[W] (fp32)
 // Adjoint chunk (spread), the strip's KB spread matrix in SELL-32 form (rows = strip cells
 // sorted by non-zero count, slices of 32 lanes):
-//     [0] n_slices [1] cells offset [2] entries offset [3..7] 0
-//     slices : n_slices x {first entry, width}
-//     cells  : n_slices x 32 uint16 strip cells (gy*16 + cx), 0xFFFF = empty lane
-//     entries: {j, w = wx*wy (fp32 bits, from float64)}; entry k of lane l at first + 32k + l
+//     [0] n_slices [1] cells offset [2] entries offset [3] n_multi (slices of width > 1) [4..7] 0
+//     slices : n_slices x {first entry, width}, widths non-increasing
+//     cells  : n_slices x 32 uint16 strip cells (swizzled slot), 0xFFFF = empty lane
+//     entries: {j, w = wx*wy (fp32 bits, from float64)}; entry k of lane l at first + 32k + l;
+//              the width-1 slices' entries come first (one flat run), then the wider slices'.
 // ftab / atab[r*S + s] = {word offset, words} of each chunk.
 struct DevPlan {
   int N, G, M, R, C, W, S, recw;      // S = G / SW strips; recw = 32-bit words per point record
@@ -143,29 +145,11 @@ constexpr size_t adj_rows_smem() {              // tw | H block | x blocks[2] | 
 template <int G>
 constexpr int cols_ctas_per_sm() { return G >= 1024 ? 1 : 2; }
 template <int G>
-constexpr size_t fwd_cols_fixed() { return (size_t(G) + size_t(G / 2) * SW + size_t(G) * SW) * 8 + 16; }
+constexpr size_t fwd_cols_fixed() { return (size_t(G) + size_t(G / 2) * SW + size_t(G + 1) * SW) * 8 + 16; }
 template <int G>
 constexpr size_t toep_cols_smem() { return (size_t(G) + size_t(G / 2) * SW + size_t(G) * SW) * 8 + 16; }
 template <int G>
-constexpr size_t adj_cols_fixed(bool ystage) { return (size_t(G) + size_t(G) * SW) * 8 + (ystage ? kYBytes : 0) + 16; }
-
-// ---------------------------------------------------------------------------- point records
-struct Rec {
-  int j, gy0, tx0, ntx, cx0;
-  const float* wx;   // wx[W] (index by tap), then wy[W]
-};
-__device__ __forceinline__ Rec read_rec(const int* rp, int W) {
-  Rec r;
-  r.j = rp[0];
-  const int pk = rp[1];
-  r.gy0 = pk & 2047;
-  r.tx0 = (pk >> 11) & 31;
-  r.ntx = (pk >> 16) & 31;
-  r.cx0 = (pk >> 21) & 31;
-  r.wx = reinterpret_cast<const float*>(rp + 2);
-  (void)W;
-  return r;
-}
+constexpr size_t adj_cols_fixed(size_t ybytes) { return (size_t(G) + size_t(G) * SW) * 8 + ybytes + 16; }
 
 // Phase timer (experiment bit 2; only compiled with -DMRF_EXPERIMENTS): thread 0 of every CTA
 // accumulates clock64 deltas per phase into p.dbgbuf.
@@ -205,38 +189,61 @@ struct PhaseTimer {
 };
 #endif
 
-// sum_i wx[tx0 + i] * strip(gy, cx0 + i) over the record's x-taps in this strip.  WT > 0: the
-// width is a compile-time bound, so all taps' loads issue before the FMAs (predicated on ntx).
-template <int WT>
-__device__ __forceinline__ float2 tap_row(const float2* strip, const Rec& rr, int gy) {
-  float2 part = make_float2(0.f, 0.f);
-  if constexpr (WT > 0) {
-    float wx[WT];
-    float2 g[WT];
+// a3 for one point record (thread = record): y_j += sum_ty wy[ty] sum_i wx[i] strip(gy0 + ty, cx0 + i).
+// The forward strip is stored [row][16] (unswizzled) and followed by a zero pad row, so the taps
+// past the strip's last column (weight 0 by construction) read finite values.  Each y_j receives
+// at most two strip partials, added with fp32 atomics onto 0 (order independent).
+template <int G, int W, bool GL>
+__device__ __forceinline__ void gather_rec(const int* rp, const float2* strip, float2* __restrict__ yf) {
+  constexpr int RW = (2 + 2 * W + 3) & ~3;
+  int wd[RW];
 #pragma unroll
-    for (int i = 0; i < WT; ++i) {
-      if (i < rr.ntx) {
-        wx[i] = rr.wx[rr.tx0 + i];
-        g[i] = strip[sidx(gy, rr.cx0 + i)];
-      } else {
-        wx[i] = 0.f;
-        g[i] = make_float2(0.f, 0.f);
-      }
-    }
-#pragma unroll
-    for (int i = 0; i < WT; ++i) {
-      part.x = fmaf(wx[i], g[i].x, part.x);
-      part.y = fmaf(wx[i], g[i].y, part.y);
-    }
-  } else {
-    for (int i = 0; i < rr.ntx; ++i) {
-      const float wx = rr.wx[rr.tx0 + i];
-      const float2 g = strip[sidx(gy, rr.cx0 + i)];
-      part.x = fmaf(wx, g.x, part.x);
-      part.y = fmaf(wx, g.y, part.y);
-    }
+  for (int k = 0; k < RW / 4; ++k) {
+    const int4 q = GL ? __ldg(reinterpret_cast<const int4*>(rp) + k) : reinterpret_cast<const int4*>(rp)[k];
+    wd[4 * k] = q.x;
+    wd[4 * k + 1] = q.y;
+    wd[4 * k + 2] = q.z;
+    wd[4 * k + 3] = q.w;
   }
-  return part;
+  const int gy0 = wd[1] & 2047, cx0 = (wd[1] >> 11) & 31;
+  float2 acc = make_float2(0.f, 0.f);
+#pragma unroll
+  for (int ty = 0; ty < W; ++ty) {
+    const float2* row = strip + ((gy0 + ty) & (G - 1)) * SW + cx0;
+    float2 racc = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int i = 0; i < W; ++i) {
+      const float2 g = row[i];
+      const float w = __int_as_float(wd[2 + i]);
+      racc.x = fmaf(w, g.x, racc.x);
+      racc.y = fmaf(w, g.y, racc.y);
+    }
+    const float wy = __int_as_float(wd[2 + W + ty]);
+    acc.x = fmaf(wy, racc.x, acc.x);
+    acc.y = fmaf(wy, racc.y, acc.y);
+  }
+  atomicAdd(&yf[wd[0]].x, acc.x);
+  atomicAdd(&yf[wd[0]].y, acc.y);
+}
+// The same for any W in [2, 16] (run-time loops; rp may point to shared or global memory).
+template <int G>
+__device__ __forceinline__ void gather_rec_any(const int* rp, int W, const float2* strip, float2* __restrict__ yf) {
+  const int gy0 = rp[1] & 2047, cx0 = (rp[1] >> 11) & 31;
+  const float* wx = reinterpret_cast<const float*>(rp + 2);
+  float2 acc = make_float2(0.f, 0.f);
+  for (int ty = 0; ty < W; ++ty) {
+    const float2* row = strip + ((gy0 + ty) & (G - 1)) * SW + cx0;
+    float2 racc = make_float2(0.f, 0.f);
+    for (int i = 0; i < W; ++i) {
+      const float2 g = row[i];
+      racc.x = fmaf(wx[i], g.x, racc.x);
+      racc.y = fmaf(wx[i], g.y, racc.y);
+    }
+    acc.x = fmaf(wx[W + ty], racc.x, acc.x);
+    acc.y = fmaf(wx[W + ty], racc.y, acc.y);
+  }
+  atomicAdd(&yf[rp[0]].x, acc.x);
+  atomicAdd(&yf[rp[0]].y, acc.y);
 }
 
 // ============================================================================ forward rows
@@ -373,20 +380,20 @@ k_fwd_cols(DevPlan p, const float2* __restrict__ H, float2* __restrict__ y, int 
   float2* stw = reinterpret_cast<float2*>(smraw);
   float2* inb = stw + G;
   float2* strip = inb + N * SW;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(strip + G * SW);      // H, chunk
+  uint64_t* bars = reinterpret_cast<uint64_t*>(strip + (G + 1) * SW);   // H, chunk (after the pad row)
   int* stage = reinterpret_cast<int*>(bars + 2);
   __shared__ int copied;                                             // bytes of the staged chunk
   __shared__ int fchunk_off;                                         // word offset of the staged chunk
   const int C = p.C, W = p.W, recw = p.recw;
   const int n_items = nb * C * S;
   const int tid = threadIdx.x, c = tid % SW, t = tid / SW;
-  const int warp = tid >> 5, lane = tid & 31, nwarps = blockDim.x >> 5;
   if (tid == 0) {
     mbar_init(&bars[0], 1);
     mbar_init(&bars[1], 1);
     fence_mbar_init();
   }
   for (int i = tid; i < G; i += blockDim.x) stw[i] = p.tw[i];
+  for (int i = tid; i < SW; i += blockDim.x) strip[G * SW + i] = make_float2(0.f, 0.f);   // pad row
   __syncthreads();
   pdl_launch_dependents();
   pdl_wait();
@@ -459,61 +466,29 @@ k_fwd_cols(DevPlan p, const float2* __restrict__ H, float2* __restrict__ y, int 
       const int k1 = t + T * b;
       dft<Q, -1>(w[b]);
 #pragma unroll
-      for (int k2 = 0; k2 < Q; ++k2) strip[sidx(k1 + P * k2, c)] = w[b][k2];   // strip [gy][c] (swizzled)
+      for (int k2 = 0; k2 < Q; ++k2) strip[(k1 + P * k2) * SW + c] = w[b][k2];   // strip [gy][c]
     }
     __syncthreads();
     pt.mark(4);
-    // a3: KB gather interpolation.  A warp takes 32/W point records at a time, lane = (record,
-    // y-tap): each lane sums its tap row, the W row partials are combined with shuffles, and the
-    // record's leader lane adds the strip's share of y_j.
+    // a3: KB gather interpolation, one thread per point record of the strip (records past the
+    // staging capacity are read from L2).
     mbar_wait(&bars[1], k & 1);
     pt.mark(5);
     if (!MRF_DBG_ON(1)) {
       const int n_rec = stage[0];
       const int n_st = (copied / 4 - kChunkHdr) / recw;     // records staged in shared memory
       const int* recs = stage + kChunkHdr;
-      const int* grecs = p.fchunks + fchunk_off + kChunkHdr;  // the rest is read from L2
+      const int* grecs = p.fchunks + fchunk_off + kChunkHdr;
       float2* yf = y + (size_t)fc * p.M;
-      const int rpw = 32 / W, slot = lane / W, ty = lane - slot * W;
-      auto row_part = [&](const Rec& rr) -> float2 {
-        const int gy = (rr.gy0 + ty) & (G - 1);
-        float2 part;
-        if (W == 6) part = tap_row<6>(strip, rr, gy);
-        else if (W == 8) part = tap_row<8>(strip, rr, gy);
-        else part = tap_row<0>(strip, rr, gy);
-        const float wy = rr.wx[W + ty];
-        return make_float2(part.x * wy, part.y * wy);
-      };
-      for (int base = warp * rpw; base < n_rec; base += nwarps * rpw) {
-        const int e = base + slot;
-        const bool valid = slot < rpw && e < n_rec;
-        float2 part = make_float2(0.f, 0.f);
-        int j = 0;
-        if (valid) {
-          if (e < n_st) {
-            const Rec rr = read_rec(recs + e * recw, W);
-            part = row_part(rr);
-            j = rr.j;
-          } else {
-            const Rec rr = read_rec(grecs + e * recw, W);
-            part = row_part(rr);
-            j = rr.j;
-          }
-        }
-        float2 sum = part;
-        if (!MRF_DBG_ON(8)) {
-          for (int o = 1; o < W; ++o) {
-            sum.x += __shfl_down_sync(0xffffffffu, part.x, o);
-            sum.y += __shfl_down_sync(0xffffffffu, part.y, o);
-          }
-        }
-        if (valid && ty == 0) {
-          if (MRF_DBG_ON(4)) {
-            if (sum.x == 12345.f) yf[j] = sum;
-          } else {
-            atomicAdd(&yf[j].x, sum.x);
-            atomicAdd(&yf[j].y, sum.y);
-          }
+      for (int e = tid; e < n_rec; e += blockDim.x) {
+        if (W == 6) {
+          if (e < n_st) gather_rec<G, 6, false>(recs + e * recw, strip, yf);
+          else gather_rec<G, 6, true>(grecs + e * recw, strip, yf);
+        } else if (W == 8) {
+          if (e < n_st) gather_rec<G, 8, false>(recs + e * recw, strip, yf);
+          else gather_rec<G, 8, true>(grecs + e * recw, strip, yf);
+        } else {
+          gather_rec_any<G>((e < n_st ? recs : grecs) + e * recw, W, strip, yf);
         }
       }
     }
@@ -527,6 +502,52 @@ k_fwd_cols(DevPlan p, const float2* __restrict__ H, float2* __restrict__ y, int 
     }
   }
   pt.report(p.dbgbuf, nit);
+}
+
+// a4 inner loop, the strip's SELL-32 spread matrix (lane = strip cell).  On a spiral most slices
+// have width 1 (MRF: 87 %), so the chunk stores their entries first as one flat run: a thread per
+// cell, no slice table.  The n_multi wider slices follow, one warp per slice, entry k of lane l at
+// first + 32k + l.  Every cell is written exactly once.  YS: y[fc] staged in shared memory.
+template <bool YS>
+__device__ __forceinline__ void spread_cells(const int2* sl_tab, const unsigned short* cells, const int2* ents,
+                                             const int2* __restrict__ gents, int n_staged, int nsl, int n_multi,
+                                             const float2* ys, const float2* __restrict__ yf, float2* strip, int tid,
+                                             int nthreads, int warp, int nwarps, int lane) {
+  const int n1 = (nsl - n_multi) * 32;
+  const unsigned short* cells1 = cells + n_multi * 32;
+  for (int i = tid; i < n1; i += nthreads) {
+    const int cell = cells1[i];
+    const int2 e = i < n_staged ? ents[i] : __ldg(gents + i);
+    const float wgt = __int_as_float(e.y);
+    const float2 v = YS ? ys[e.x] : __ldg(yf + e.x);
+    if (cell != 0xFFFF) strip[cell] = make_float2(wgt * v.x, wgt * v.y);
+  }
+  for (int sl = warp; sl < n_multi; sl += nwarps) {
+    const int2 si = sl_tab[sl];
+    const int cell = cells[sl * 32 + lane];
+    float2 acc = make_float2(0.f, 0.f);
+    if (si.x + 32 * si.y <= n_staged) {
+      const int2* ep = ents + si.x + lane;
+      for (int kk = 0; kk < si.y; ++kk) {
+        const int2 e = ep[kk * 32];
+        const float wgt = __int_as_float(e.y);
+        const float2 v = YS ? ys[e.x] : __ldg(yf + e.x);
+        acc.x = fmaf(wgt, v.x, acc.x);
+        acc.y = fmaf(wgt, v.y, acc.y);
+      }
+    } else {
+      const int2* ep = gents + si.x + lane;
+#pragma unroll 4
+      for (int kk = 0; kk < si.y; ++kk) {
+        const int2 e = __ldg(ep + kk * 32);
+        const float wgt = __int_as_float(e.y);
+        const float2 v = YS ? ys[e.x] : __ldg(yf + e.x);
+        acc.x = fmaf(wgt, v.x, acc.x);
+        acc.y = fmaf(wgt, v.y, acc.y);
+      }
+    }
+    if (cell != 0xFFFF) strip[cell] = acc;
+  }
 }
 
 // ============================================================================ adjoint columns
@@ -543,7 +564,7 @@ k_adj_cols(DevPlan p, const float2* __restrict__ y, float2* __restrict__ H, int 
   float2* stw = reinterpret_cast<float2*>(smraw);
   float2* strip = stw + G;
   float2* ys = strip + G * SW;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<unsigned char*>(ys) + (ystage ? kYBytes : 0));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<unsigned char*>(ys) + ystage);
   int* stage = reinterpret_cast<int*>(bars + 2);
   __shared__ int copied;
   __shared__ int chunk_off;   // word offset of the staged chunk (for its unstaged tail)
@@ -551,7 +572,6 @@ k_adj_cols(DevPlan p, const float2* __restrict__ y, float2* __restrict__ H, int 
   const int n_items = nb * C * S;
   const int tid = threadIdx.x, c = tid % SW, t = tid / SW;
   const int warp = tid >> 5, lane = tid & 31, nwarps = blockDim.x >> 5;
-  const uint32_t ybytes = (uint32_t)M * sizeof(float2);
   if (tid == 0) {
     mbar_init(&bars[0], 1);
     fence_mbar_init();
@@ -569,9 +589,9 @@ k_adj_cols(DevPlan p, const float2* __restrict__ y, float2* __restrict__ H, int 
     const uint32_t bytes = (uint32_t)min(ow.y * 4, stage_cap) & ~15u;
     copied = (int)bytes;
     chunk_off = ow.x;
-    mbar_expect_tx(&bars[0], bytes + (ystage ? ybytes : 0));
+    mbar_expect_tx(&bars[0], bytes + (uint32_t)ystage);
     bulk_g2s(stage, p.achunks + ow.x, bytes, &bars[0]);
-    if (ystage) bulk_g2s(ys, y + (size_t)(item / S) * M, ybytes, &bars[0]);
+    if (ystage) bulk_g2s(ys, y + (size_t)(item / S) * M, (uint32_t)ystage, &bars[0]);
   };
   int item = blockIdx.x;
   int2 off_next = make_int2(0, 0);
@@ -592,39 +612,19 @@ k_adj_cols(DevPlan p, const float2* __restrict__ y, float2* __restrict__ H, int 
       // Staged prefix of the chunk: header, slice table and cells always fit (checked at plan
       // time); a slice whose entries lie past the staged prefix reads them from L2.
       const int nsl = MRF_DBG_ON(1) ? 0 : stage[0], cells_off = stage[1], ent_off = stage[2];
+      const int n_multi = MRF_DBG_ON(1) ? 0 : stage[3];
       const float2* yf = y + (size_t)fc * M;
       const int2* sl_tab = reinterpret_cast<const int2*>(stage + kChunkHdr);
       const unsigned short* cells = reinterpret_cast<const unsigned short*>(stage + cells_off);
       const int2* ents = reinterpret_cast<const int2*>(stage + ent_off);
       const int n_staged = (copied / 4 - ent_off) / 2;          // entries in shared memory
       const int2* gents = reinterpret_cast<const int2*>(p.achunks + chunk_off + ent_off);
-      for (int sl = warp; sl < nsl; sl += nwarps) {
-        const int2 si = sl_tab[sl];
-        const int cell = cells[sl * 32 + lane];
-        float2 acc = make_float2(0.f, 0.f);
-        if (si.x + 32 * si.y <= n_staged) {
-          const int2* ep = ents + si.x + lane;
-#pragma unroll 8
-          for (int kk = 0; kk < si.y; ++kk) {
-            const int2 e = ep[kk * 32];
-            const float wgt = __int_as_float(e.y);
-            const float2 v = ystage ? ys[e.x] : __ldg(yf + e.x);
-            acc.x = fmaf(wgt, v.x, acc.x);
-            acc.y = fmaf(wgt, v.y, acc.y);
-          }
-        } else {
-          const int2* ep = gents + si.x + lane;
-#pragma unroll 16
-          for (int kk = 0; kk < si.y; ++kk) {
-            const int2 e = __ldg(ep + kk * 32);
-            const float wgt = __int_as_float(e.y);
-            const float2 v = ystage ? ys[e.x] : __ldg(yf + e.x);
-            acc.x = fmaf(wgt, v.x, acc.x);
-            acc.y = fmaf(wgt, v.y, acc.y);
-          }
-        }
-        if (cell != 0xFFFF) strip[cell] = acc;
-      }
+      if (ystage)
+        spread_cells<true>(sl_tab, cells, ents, gents, n_staged, nsl, n_multi, ys, yf, strip, tid, blockDim.x, warp,
+                           nwarps, lane);
+      else
+        spread_cells<false>(sl_tab, cells, ents, gents, n_staged, nsl, n_multi, ys, yf, strip, tid, blockDim.x, warp,
+                            nwarps, lane);
     }
     pt.mark(1);
     __syncthreads();
@@ -658,10 +658,12 @@ k_adj_cols(DevPlan p, const float2* __restrict__ y, float2* __restrict__ H, int 
     for (int b = 0; b < B; ++b) {
       const int k1 = t + T * b;
 #pragma unroll
-      for (int n2 = 0; n2 < Q; ++n2) w[b][n2] = strip[(n2 * P + k1) * SW + c];
+      for (int n2 = 0; n2 < Q; ++n2) {   // each cell is read by its one owner, who clears it for the next spread
+        float2& cell = strip[(n2 * P + k1) * SW + c];
+        w[b][n2] = cell;
+        cell = make_float2(0.f, 0.f);
+      }
     }
-    __syncthreads();
-    for (int i = tid; i < G * SW; i += blockDim.x) strip[i] = make_float2(0.f, 0.f);   // for the next spread
     pt.mark(5);
     float2* Hc = H + (size_t)fc * N * G + (size_t)(item % S) * SW + c;    // row-major [fc][iy][G]
 #pragma unroll

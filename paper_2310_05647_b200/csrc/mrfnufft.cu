@@ -79,7 +79,7 @@ struct mrf_plan_s {
   int device = 0;
   int bf = 1;               // frames per batch
   int nsm = 148;            // SMs of the device
-  int ystage = 0;           // k_adj_cols stages y[fc] in shared memory (M even, M*8 <= kYBytes)
+  int ystage = 0;           // bytes of y[fc] k_adj_cols stages in shared memory (M*8 if M even, M*8 <= kYBytes)
   int occ_fr0 = 1, occ_fr1 = 1, occ_fc = 1, occ_ac = 1, occ_ar = 1;   // resident CTAs per SM
   int fc_stage = 0, ac_stage = 0;   // chunk staging bytes of the column kernels
   int occ_tc = 1;
@@ -303,7 +303,7 @@ static mrf_status setup_kernels(mrf_plan_s* pl) {
   pl->col_smem = (int)s_col;
   pl->acol_smem = (int)s_acol;
   pl->fc_stage = (int)((s_col - fwd_cols_fixed<G>()) & ~size_t(15));
-  pl->ac_stage = (int)((s_acol - adj_cols_fixed<G>(pl->ystage != 0)) & ~size_t(15));
+  pl->ac_stage = (int)((s_acol - adj_cols_fixed<G>((size_t)pl->ystage)) & ~size_t(15));
   CUDA_TRY(cudaFuncSetAttribute(k_fwd_rows<G, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s_fr0));
   CUDA_TRY(cudaFuncSetAttribute(k_fwd_rows<G, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s_fr1));
   CUDA_TRY(cudaFuncSetAttribute(k_adj_rows<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s_ar));
@@ -383,8 +383,8 @@ static mrf_status launch_fwd_cols(mrf_plan_s* pl, const float2* H, float2* y, in
 template <int G>
 static mrf_status launch_adj_cols(mrf_plan_s* pl, const float2* y, float2* H, int l0, int nb, cudaStream_t st) {
   const long long items = (long long)nb * pl->C * pl->S;
-  const int ys = pl->ystage && ((uintptr_t)y % 16 == 0);
-  const int stage = ys ? pl->ac_stage : (int)(((size_t)pl->acol_smem - adj_cols_fixed<G>(false)) & ~size_t(15));
+  const int ys = ((uintptr_t)y % 16 == 0) ? pl->ystage : 0;
+  const int stage = ys ? pl->ac_stage : (int)(((size_t)pl->acol_smem - adj_cols_fixed<G>(0)) & ~size_t(15));
   ProfScope ps(pl, MRF_K_ADJ_COLS, st);
   CUDA_TRY(launch_pdl(k_adj_cols<G>, pgrid(pl, pl->occ_ac, items), cols_threads<G>(), pl->acol_smem, st, pl->dp(), y, H,
                       l0, nb, ys, stage));
@@ -806,7 +806,7 @@ mrf_status mrf_plan_create(const mrf_plan_desc* d, mrf_plan* out) {
     if (cudaMalloc((void**)&pl->dbgbuf, 32 * sizeof(long long)) != cudaSuccess) return fail(MRF_ENOMEM, "dbgbuf");
     cudaMemset(pl->dbgbuf, 0, 32 * sizeof(long long));
   }
-  pl->ystage = (M % 2 == 0 && (size_t)M * sizeof(float2) <= (size_t)kYBytes) ? 1 : 0;
+  pl->ystage = (M % 2 == 0 && (size_t)M * sizeof(float2) <= (size_t)kYBytes) ? (int)(M * sizeof(float2)) : 0;
   {
     int nsm = 0;
     if (cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, d->device) == cudaSuccess && nsm > 0) pl->nsm = nsm;
@@ -885,9 +885,13 @@ mrf_status mrf_plan_create(const mrf_plan_desc* d, mrf_plan* out) {
         fch[base] = n_rec;
         for (int ri = 0; ri < n_rec; ++ri) {
           int* rp = &fch[base + kChunkHdr + (size_t)ri * recw];
+          const int pk = rb[ri].y, tx0 = (pk >> 11) & 31, ntx = (pk >> 16) & 31;
+          const float* wp = &wts[((size_t)r * M + rb[ri].x) * 2 * W];
           rp[0] = rb[ri].x;
-          rp[1] = rb[ri].y;
-          std::memcpy(rp + 2, &wts[((size_t)r * M + rb[ri].x) * 2 * W], sizeof(float) * 2 * W);
+          rp[1] = (pk & 2047) | (((pk >> 21) & 31) << 11);   // first grid row | first strip column
+          float* wx = reinterpret_cast<float*>(rp + 2);
+          for (int i = 0; i < W; ++i) wx[i] = i < ntx ? wp[tx0 + i] : 0.f;   // x-weights aligned to the strip
+          std::memcpy(rp + 2 + W, wp + W, sizeof(float) * W);
         }
         ftab[(size_t)r * S + s] = make_int2((int)base, (int)words);
       }
@@ -911,19 +915,25 @@ mrf_status mrf_plan_create(const mrf_plan_desc* d, mrf_plan* out) {
       std::stable_sort(rows.begin(), rows.end(), [](const int2& a, const int2& b) { return a.y > b.y; });
       const int nsl = (int)((rows.size() + 31) / 32);
       long long nent = 0;
-      for (int sl = 0; sl < nsl; ++sl) nent += 32LL * rows[(size_t)sl * 32].y;
+      int n_multi = 0;   // slices are sorted by width: slices [0, n_multi) have width > 1
+      for (int sl = 0; sl < nsl; ++sl) {
+        nent += 32LL * rows[(size_t)sl * 32].y;
+        if (rows[(size_t)sl * 32].y > 1) n_multi = sl + 1;
+      }
       const size_t cells_off = (size_t)kChunkHdr + 2 * (size_t)nsl;
       const size_t ent_off = (cells_off + 16 * (size_t)nsl + 1) & ~(size_t)1;
       const size_t words = (ent_off + 2 * (size_t)nent + 3) & ~(size_t)3;
       const size_t base = ach.size();
       ach.resize(base + words, 0);
       int* ch = &ach[base];
-      ch[0] = nsl; ch[1] = (int)cells_off; ch[2] = (int)ent_off;
+      ch[0] = nsl; ch[1] = (int)cells_off; ch[2] = (int)ent_off; ch[3] = n_multi;
       unsigned short* cells = reinterpret_cast<unsigned short*>(ch + cells_off);
       int2* ents = reinterpret_cast<int2*>(ch + ent_off);
-      long long first = 0;
+      // entries of the width-1 slices first (one flat run, always staged first), then the others
+      long long first = 32LL * (nsl - n_multi);
       for (int sl = 0; sl < nsl; ++sl) {
         const int width = rows[(size_t)sl * 32].y;
+        if (sl == n_multi) first = 0;
         ch[kChunkHdr + 2 * sl] = (int)first;
         ch[kChunkHdr + 2 * sl + 1] = width;
         for (int lane = 0; lane < 32; ++lane) {
