@@ -26,6 +26,7 @@ namespace mrf {
 constexpr int SW = 16;             // columns per strip (>= W: a point's x-taps touch <= 2 strips)
 constexpr int kYBytes = 32768;     // largest y[fc] staged in shared memory by k_adj_cols (M <= 4096)
 constexpr int kChunkHdr = 8;       // header words of a strip chunk
+constexpr int SWG = SW + 1;        // row stride of the forward strip during the gather (bank skew)
 constexpr int kRowThreads = 128;
 
 struct CGScalars;
@@ -46,7 +47,7 @@ struct DevPlan {
   int N, G, M, R, C, W, S, recw;      // S = G / SW strips; recw = 32-bit words per point record
   const float2* __restrict__ coils;   // [C][N][N] or nullptr (C == 1)
   const float* __restrict__ dap;      // [N]  1 / (psi(n) sqrt(N))
-  const float2* __restrict__ tw;      // [G]  tw[k1*Q + n2] = exp(-i 2 pi n2 k1 / G)
+  const float2* __restrict__ tw;      // [G]  tw[n2*P + k1] = exp(-i 2 pi n2 k1 / G)
   const int* __restrict__ fchunks;    // forward chunks
   const int2* __restrict__ ftab;      // [R*S] {offset, words}
   const int* __restrict__ achunks;    // adjoint chunks
@@ -112,6 +113,12 @@ __device__ __forceinline__ void smem_add2(float2* a, float2 v) {
 // record's W tap rows then fall in different banks, and a row is still 16 contiguous slots.
 __host__ __device__ __forceinline__ int sidx(int row, int col) { return row * SW + (col ^ (row & (SW - 1))); }
 
+// Stage-1 twiddles W_G^{n2 k1} of the two-stage FFT (fft.cuh).  Global table layout [n2][k1]:
+// in the column kernels a warp spans 2 values of n2, and the pair (k1, k1 + 1), k1 even, is one
+// 16-byte shared-memory load; the row kernels (a warp spans 16 values of n2) transpose it to
+// [k1][n2] in shared memory.
+__device__ __forceinline__ float4 tw_pair(const float2* stw, int i) { return *reinterpret_cast<const float4*>(stw + i); }
+
 // image index <-> wrapped grid index (centred n = i - N/2, grid position n mod G)
 template <int G>
 __device__ __forceinline__ int grid_to_img(int pos) {   // pos in the kept set
@@ -145,7 +152,7 @@ constexpr size_t adj_rows_smem() {              // tw | H block | x blocks[2] | 
 template <int G>
 constexpr int cols_ctas_per_sm() { return G >= 1024 ? 1 : 2; }
 template <int G>
-constexpr size_t fwd_cols_fixed() { return (size_t(G) + size_t(G / 2) * SW + size_t(G + 1) * SW) * 8 + 16; }
+constexpr size_t fwd_cols_fixed() { return (size_t(G) + size_t(G / 2) * SW + size_t(G) * SWG + SW) * 8 + 16; }
 template <int G>
 constexpr size_t toep_cols_smem() { return (size_t(G) + size_t(G / 2) * SW + size_t(G) * SW) * 8 + 16; }
 template <int G>
@@ -190,8 +197,9 @@ struct PhaseTimer {
 #endif
 
 // a3 for one point record (thread = record): y_j += sum_ty wy[ty] sum_i wx[i] strip(gy0 + ty, cx0 + i).
-// The forward strip is stored [row][16] (unswizzled) and followed by a zero pad row, so the taps
-// past the strip's last column (weight 0 by construction) read finite values.  Each y_j receives
+// The forward strip is stored [row][SWG] (16 cells + 1 skew slot per row, so the same column of
+// neighbouring rows falls in different banks) and followed by a pad, so the taps past the strip's
+// last column (weight 0 by construction) read finite values.  Each y_j receives
 // at most two strip partials, added with fp32 atomics onto 0 (order independent).
 template <int G, int W, bool GL>
 __device__ __forceinline__ void gather_rec(const int* rp, const float2* strip, float2* __restrict__ yf) {
@@ -209,7 +217,7 @@ __device__ __forceinline__ void gather_rec(const int* rp, const float2* strip, f
   float2 acc = make_float2(0.f, 0.f);
 #pragma unroll
   for (int ty = 0; ty < W; ++ty) {
-    const float2* row = strip + ((gy0 + ty) & (G - 1)) * SW + cx0;
+    const float2* row = strip + ((gy0 + ty) & (G - 1)) * SWG + cx0;
     float2 racc = make_float2(0.f, 0.f);
 #pragma unroll
     for (int i = 0; i < W; ++i) {
@@ -232,7 +240,7 @@ __device__ __forceinline__ void gather_rec_any(const int* rp, int W, const float
   const float* wx = reinterpret_cast<const float*>(rp + 2);
   float2 acc = make_float2(0.f, 0.f);
   for (int ty = 0; ty < W; ++ty) {
-    const float2* row = strip + ((gy0 + ty) & (G - 1)) * SW + cx0;
+    const float2* row = strip + ((gy0 + ty) & (G - 1)) * SWG + cx0;
     float2 racc = make_float2(0.f, 0.f);
     for (int i = 0; i < W; ++i) {
       const float2 g = row[i];
@@ -272,7 +280,7 @@ k_fwd_rows(DevPlan p, const float2* __restrict__ x, float2* __restrict__ H, int 
     mbar_init(bar, 1);
     fence_mbar_init();
   }
-  for (int i = tid; i < G; i += kRowThreads) stw[i] = p.tw[i];
+  for (int i = tid; i < G; i += kRowThreads) stw[i] = p.tw[(i % Q) * P + i / Q];   // [k1][n2]: a warp spans n2
   for (int i = tid; i < N; i += kRowThreads) sdap[i] = p.dap[i];
   __syncthreads();
   pdl_launch_dependents();
@@ -380,7 +388,7 @@ k_fwd_cols(DevPlan p, const float2* __restrict__ H, float2* __restrict__ y, int 
   float2* stw = reinterpret_cast<float2*>(smraw);
   float2* inb = stw + G;
   float2* strip = inb + N * SW;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(strip + (G + 1) * SW);   // H, chunk (after the pad row)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(strip + G * SWG + SW);   // H, chunk (after the pad)
   int* stage = reinterpret_cast<int*>(bars + 2);
   __shared__ int copied;                                             // bytes of the staged chunk
   __shared__ int fchunk_off;                                         // word offset of the staged chunk
@@ -393,7 +401,7 @@ k_fwd_cols(DevPlan p, const float2* __restrict__ H, float2* __restrict__ y, int 
     fence_mbar_init();
   }
   for (int i = tid; i < G; i += blockDim.x) stw[i] = p.tw[i];
-  for (int i = tid; i < SW; i += blockDim.x) strip[G * SW + i] = make_float2(0.f, 0.f);   // pad row
+  for (int i = tid; i < G * SWG + SW; i += blockDim.x) strip[i] = make_float2(0.f, 0.f);   // skew slots and pad
   __syncthreads();
   pdl_launch_dependents();
   pdl_wait();
@@ -448,7 +456,11 @@ k_fwd_cols(DevPlan p, const float2* __restrict__ H, float2* __restrict__ y, int 
       const int n2 = t + T * a;
       dft_halfzero<P, -1>(v[a]);
 #pragma unroll
-      for (int k1 = 0; k1 < P; ++k1) strip[(n2 * P + k1) * SW + c] = cmul(v[a][k1], stw[k1 * Q + n2]);
+      for (int k1 = 0; k1 < P; k1 += 2) {
+        const float4 tt = tw_pair(stw, n2 * P + k1);
+        strip[(n2 * P + k1) * SW + c] = cmul(v[a][k1], make_float2(tt.x, tt.y));
+        strip[(n2 * P + k1 + 1) * SW + c] = cmul(v[a][k1 + 1], make_float2(tt.z, tt.w));
+      }
     }
     __syncthreads();
     pt.mark(2);
@@ -466,7 +478,7 @@ k_fwd_cols(DevPlan p, const float2* __restrict__ H, float2* __restrict__ y, int 
       const int k1 = t + T * b;
       dft<Q, -1>(w[b]);
 #pragma unroll
-      for (int k2 = 0; k2 < Q; ++k2) strip[(k1 + P * k2) * SW + c] = w[b][k2];   // strip [gy][c]
+      for (int k2 = 0; k2 < Q; ++k2) strip[(k1 + P * k2) * SWG + c] = w[b][k2];   // strip [gy][c]
     }
     __syncthreads();
     pt.mark(4);
@@ -649,7 +661,11 @@ k_adj_cols(DevPlan p, const float2* __restrict__ y, float2* __restrict__ H, int 
       const int n2 = t + T * a;
       dft<P, +1>(v[a]);
 #pragma unroll
-      for (int k1 = 0; k1 < P; ++k1) strip[(n2 * P + k1) * SW + c] = cmulc(v[a][k1], stw[k1 * Q + n2]);
+      for (int k1 = 0; k1 < P; k1 += 2) {
+        const float4 tt = tw_pair(stw, n2 * P + k1);
+        strip[(n2 * P + k1) * SW + c] = cmulc(v[a][k1], make_float2(tt.x, tt.y));
+        strip[(n2 * P + k1 + 1) * SW + c] = cmulc(v[a][k1 + 1], make_float2(tt.z, tt.w));
+      }
     }
     __syncthreads();
     pt.mark(4);
@@ -751,7 +767,11 @@ k_toep_cols(DevPlan p, const float2* __restrict__ Hf, float2* __restrict__ Ha, c
       const int n2 = t + T * a;
       dft_halfzero<P, -1>(v[a]);
 #pragma unroll
-      for (int k1 = 0; k1 < P; ++k1) ex[(n2 * P + k1) * SW + c] = cmul(v[a][k1], stw[k1 * Q + n2]);
+      for (int k1 = 0; k1 < P; k1 += 2) {
+        const float4 tt = tw_pair(stw, n2 * P + k1);
+        ex[(n2 * P + k1) * SW + c] = cmul(v[a][k1], make_float2(tt.x, tt.y));
+        ex[(n2 * P + k1 + 1) * SW + c] = cmul(v[a][k1 + 1], make_float2(tt.z, tt.w));
+      }
     }
     __syncthreads();
     float2 w[B][Q];
@@ -770,7 +790,7 @@ k_toep_cols(DevPlan p, const float2* __restrict__ Hf, float2* __restrict__ Ha, c
       for (int k2 = 0; k2 < Q; ++k2) w[b][k2] = cscale(w[b][k2], tp[b][k2]);
       dft<Q, +1>(w[b]);                          // stage A of the inverse: index n2
 #pragma unroll
-      for (int n2 = 0; n2 < Q; ++n2) ex[(n2 * P + k1) * SW + c] = cmulc(w[b][n2], stw[k1 * Q + n2]);
+      for (int n2 = 0; n2 < Q; ++n2) ex[(n2 * P + k1) * SW + c] = cmulc(w[b][n2], stw[n2 * P + k1]);
     }
     __syncthreads();
     float2* Hc = Ha + (size_t)fc * N * G + (size_t)s * SW + c;    // row-major [fc][iy][G]
@@ -879,7 +899,7 @@ k_adj_rows(DevPlan p, const float2* __restrict__ H, float2* __restrict__ out, co
     mbar_init(&bars[2], 1);
     fence_mbar_init();
   }
-  for (int i = tid; i < G; i += kRowThreads) stw[i] = p.tw[i];
+  for (int i = tid; i < G; i += kRowThreads) stw[i] = p.tw[(i % Q) * P + i / Q];   // [k1][n2]: a warp spans n2
   for (int i = tid; i < N; i += kRowThreads) sdap[i] = p.dap[i];
   __syncthreads();
   pdl_launch_dependents();

@@ -831,7 +831,7 @@ mrf_status mrf_plan_create(const mrf_plan_desc* d, mrf_plan* out) {
   for (int k1 = 0; k1 < P; ++k1)
     for (int n2 = 0; n2 < Q; ++n2) {
       const double a = -2.0 * M_PI * (double)((long long)n2 * k1 % G) / G;
-      tw[k1 * Q + n2] = make_float2((float)std::cos(a), (float)std::sin(a));
+      tw[n2 * P + k1] = make_float2((float)std::cos(a), (float)std::sin(a));
     }
   // ---- taps, weights, strip bins (a0) ---------------------------------------------------------
   // Every point of every interleaf is binned into the 16-column strips its W x-taps touch (one

@@ -1,4 +1,4 @@
-python -m pytest tests/test_gpu_parity.py -x -q -m gpu 2>&1 | tail -3
-for op in normal forward adjoint cg; do python tools/op_breakdown.py --op $op --reps 10 2>&1 | tail -1; done
-MRF_LANES=1 python tools/op_breakdown.py --op forward --reps 10 2>&1 | tail -1
-MRF_LANES=1 python tools/op_breakdown.py --op adjoint --reps 10 2>&1 | tail -1
+python -m pytest tests/test_gpu_parity.py -x -q -m gpu 2>&1 | tail -2
+for op in normal forward adjoint; do python tools/op_breakdown.py --op $op --reps 10 2>&1 | tail -1; done
+python tools/op_breakdown.py --op normal --normal toeplitz --reps 10 2>&1 | tail -1
+MRF_LANES=1 python tools/op_breakdown.py --op normal --reps 10 2>&1 | tail -1
