@@ -176,6 +176,60 @@ __device__ __forceinline__ void dft_halfzero(float2 (&v)[P]) {
   }
 }
 
+namespace detail {
+// radix-4 DIT combine producing only X[K] and X[K + 3R/4]
+template <int R, int SIGN, int K>
+__device__ __forceinline__ void r4_combine_halfout(float2 (&v)[R], const float2 (&d0)[R / 4], const float2 (&d1)[R / 4],
+                                                   const float2 (&d2)[R / 4], const float2 (&d3)[R / 4]) {
+  if constexpr (K < R / 4) {
+    const float2 a0 = d0[K];
+    const float2 a1 = twmul<R, K, SIGN>(d1[K]);
+    const float2 a2 = twmul<R, 2 * K, SIGN>(d2[K]);
+    const float2 a3 = twmul<R, 3 * K, SIGN>(d3[K]);
+    const float2 s02 = cadd(a0, a2), d02 = csub(a0, a2);
+    const float2 s13 = cadd(a1, a3), d13 = mul_i<SIGN>(csub(a1, a3));
+    v[K] = cadd(s02, s13);
+    v[K + 3 * R / 4] = csub(d02, d13);
+    r4_combine_halfout<R, SIGN, K + 1>(v, d0, d1, d2, d3);
+  }
+}
+}  // namespace detail
+
+// R-point DFT (natural order) that produces only the outputs k < R/4 and k >= 3R/4 -- the kept
+// (cropped) half of the oversampled grid in the adjoint.  The other
+// entries of v are left unspecified.  The last butterfly stage skips the two dropped outputs.
+template <int R, int SIGN>
+__device__ __forceinline__ void dft_halfout(float2 (&v)[R]) {
+  if constexpr (R == 8) {
+    float2 e[4], o[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) { e[i] = v[2 * i]; o[i] = v[2 * i + 1]; }
+    dft<4, SIGN>(e);
+    dft<4, SIGN>(o);
+    v[0] = cadd(e[0], o[0]);
+    v[1] = cadd(e[1], twmul<8, 1, SIGN>(o[1]));
+    v[6] = csub(e[2], twmul<8, 2, SIGN>(o[2]));
+    v[7] = csub(e[3], twmul<8, 3, SIGN>(o[3]));
+  } else if constexpr (R >= 16) {
+    static_assert(R % 4 == 0, "R must be a power of two");
+    float2 d0[R / 4], d1[R / 4], d2[R / 4], d3[R / 4];
+#pragma unroll
+    for (int i = 0; i < R / 4; ++i) {
+      d0[i] = v[4 * i];
+      d1[i] = v[4 * i + 1];
+      d2[i] = v[4 * i + 2];
+      d3[i] = v[4 * i + 3];
+    }
+    dft<R / 4, SIGN>(d0);
+    dft<R / 4, SIGN>(d1);
+    dft<R / 4, SIGN>(d2);
+    dft<R / 4, SIGN>(d3);
+    detail::r4_combine_halfout<R, SIGN, 0>(v, d0, d1, d2, d3);
+  } else {
+    dft<R, SIGN>(v);
+  }
+}
+
 // Two-stage split of the supported grid sizes.  T threads (within one warp) per length-G DFT.
 template <int G> struct FFTShape;
 template <> struct FFTShape<64>   { static constexpr int P = 8,  Q = 8,  T = 8;  };

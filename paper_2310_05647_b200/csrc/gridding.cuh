@@ -685,7 +685,7 @@ k_adj_cols(DevPlan p, const float2* __restrict__ y, float2* __restrict__ H, int 
 #pragma unroll
     for (int b = 0; b < B; ++b) {
       const int k1 = t + T * b;
-      dft<Q, +1>(w[b]);
+      dft_halfout<Q, +1>(w[b]);
 #pragma unroll
       for (int k2 = 0; k2 < Q; ++k2) {
         if (k2 < Q / 4 || k2 >= 3 * Q / 4) Hc[(size_t)grid_to_img<G>(k1 + P * k2) * G] = w[b][k2];
@@ -800,7 +800,7 @@ k_toep_cols(DevPlan p, const float2* __restrict__ Hf, float2* __restrict__ Ha, c
       float2 u[P];
 #pragma unroll
       for (int k1 = 0; k1 < P; ++k1) u[k1] = ex[(n2 * P + k1) * SW + c];
-      dft<P, +1>(u);                             // stage B: index n1, row n2 + Q n1
+      dft_halfout<P, +1>(u);                             // stage B: index n1, row n2 + Q n1
 #pragma unroll
       for (int n1 = 0; n1 < P; ++n1) {
         if (n1 < P / 4 || n1 >= 3 * P / 4) Hc[(size_t)grid_to_img<G>(n2 + Q * n1) * G] = u[n1];
@@ -980,7 +980,7 @@ k_adj_rows(DevPlan p, const float2* __restrict__ H, float2* __restrict__ out, co
         float2 w[Q];
 #pragma unroll
         for (int n2 = 0; n2 < Q; ++n2) w[n2] = myex[n2 * (P + 1) + k1];
-        dft<Q, +1>(w);
+        dft_halfout<Q, +1>(w);
 #pragma unroll
         for (int kk = 0; kk < Q / 2; ++kk) {
           const int k2 = kk < Q / 4 ? kk : kk + Q / 2;
