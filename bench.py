@@ -115,6 +115,16 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------------------------ helpers
+def ncu_traffic(kernel_class):
+    """DRAM bytes per launch of one kernel class from the committed `ncu --set full` capture
+    (profiles/ncu_traffic.json, written by tools/ncu_traffic.py), or None."""
+    try:
+        t = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
+        return t["kernels"][kernel_class]
+    except (OSError, KeyError, ValueError):
+        return None
+
+
 def peaks():
     try:
         return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
@@ -391,8 +401,16 @@ def run_ours(args):
     frames_per_call = {"fwd_rows": n_iter + 1, "fwd_cols": n_iter + 1, "adj_cols": n_iter + 2, "adj_rows": n_iter + 2}
     dom_flops_total = kernel_flops(cfg, dom, L) * frames_per_call[dom] * args.steps
     achieved = dom_flops_total / (dom_ms * 1e-3) / 1e12 if dom_ms > 0 else None
+    # traffic: ncu dram bytes per launch, scaled from the capture's frames per launch to this run's
+    tr = ncu_traffic(dom)
+    traffic = None
+    if tr and dom_n:
+        frames_per_launch = L * frames_per_call[dom] * args.steps / dom_n
+        traffic = tr["dram_bytes_per_launch"] * frames_per_launch / tr["frames_per_launch"]
     roofline = {"bound": "alu", "kernel": dom, "achieved": achieved, "peak": peak_alu, "unit": "TFLOP/s",
-                "frac": (achieved / peak_alu) if achieved else None, "traffic": None,
+                "frac": (achieved / peak_alu) if achieved else None, "traffic": traffic,
+                "traffic_note": ("ncu dram__bytes_read.sum + dram__bytes_write.sum per launch "
+                                 f"({tr['source']}), scaled to this run's frames per launch") if tr else None,
                 "note": "per-launch CUDA events on the launch lane; the two batch lanes overlap, so the "
                         "durations include time-sharing with the other lane (conservative)",
                 "avg_launch_ms": dom_ms / max(dom_n, 1), "launches": dom_n,
@@ -407,6 +425,10 @@ def run_ours(args):
                     "hbm_literal_frac": aha_bytes / (ms_normal * 1e-3) / 1e9 / hbm_peak,
                     "t_roof_ms": max(aha_flops / (peak_alu * 1e12), aha_bytes / (hbm_peak * 1e9)) * 1e3}
     share = {k: (v / ms_total if ms_total > 0 else None) for k, v in cls_ms.items()}
+    # the two batch lanes overlap, so the shares above sum to > 1; normalised to the summed kernel
+    # time they compare with the serialised ncu launch list (profiles/)
+    ksum = sum(cls_ms.values())
+    share_k = {k: (v / ksum if ksum > 0 else None) for k, v in cls_ms.items()}
     hbm_bytes = step_bytes(cfg, cfg.L, n_iter)
     hbm_achieved = hbm_bytes / (ms_step * 1e-3) / 1e9
     gpu_launches = int(sum(prof[k][1] for k in ("fwd_rows", "fwd_cols", "adj_cols", "adj_rows", "cg_vec")))
@@ -432,7 +454,7 @@ def run_ours(args):
         "hbm": {"algorithmic_bytes_per_step": hbm_bytes, "achieved_GBs": hbm_achieved, "peak_GBs": hbm_peak,
                 "frac": hbm_achieved / hbm_peak},
         "cufft_ref_ms_fft2_LC": cufft_ms,
-        "roofline": roofline, "roofline_AHA": roofline_aha, "toeplitz": toep, "kernel_share": share, "gpu_launches": gpu_launches,
+        "roofline": roofline, "roofline_AHA": roofline_aha, "toeplitz": toep, "kernel_share": share, "kernel_share_of_kernel_time": share_k, "gpu_launches": gpu_launches,
         "clocks": clk, "e2e": e2e, "cpu_baseline": cpu,
     }
     if rank == 0:
