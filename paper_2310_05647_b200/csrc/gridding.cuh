@@ -25,7 +25,8 @@ namespace mrf {
 
 constexpr int SW = 16;             // columns per strip (>= W: a point's x-taps touch <= 2 strips)
 constexpr int kYBytes = 32768;     // largest y[fc] staged in shared memory by k_adj_cols (M <= 4096)
-constexpr int kChunkHdr = 8;       // header words of a strip chunk
+constexpr int kChunkHdr = 8;       // header words of a forward strip chunk (and offset of the adjoint row masks)
+constexpr int kAdjHdr = 24;        // header words of an adjoint strip chunk (8 + 16 row-mask words)
 constexpr int SWG = SW + 1;        // row stride of the forward strip during the gather (bank skew)
 constexpr int kRowThreads = 128;
 
@@ -38,6 +39,8 @@ struct CGScalars;
 // Adjoint chunk (spread), the strip's KB spread matrix in SELL-32 form (rows = strip cells
 // sorted by non-zero count, slices of 32 lanes):
 //     [0] n_slices [1] cells offset [2] entries offset [3] n_multi (slices of width > 1) [4..7] 0
+//     [8 + w], w < 16: row-pair mask of warp w's stage-1 loads in k_adj_cols (bit a*P + n1 set if
+//     row Q n1 + T a + 2w or the next row holds a spread value)
 //     slices : n_slices x {first entry, width}, widths non-increasing
 //     cells  : n_slices x 32 uint16 strip cells (swizzled slot), 0xFFFF = empty lane
 //     entries: {j, w = wx*wy (fp32 bits, from float64)}; entry k of lane l at first + 32k + l;
@@ -156,7 +159,13 @@ constexpr size_t fwd_cols_fixed() { return (size_t(G) + size_t(G / 2) * SW + siz
 template <int G>
 constexpr size_t toep_cols_smem() { return (size_t(G) + size_t(G / 2) * SW + size_t(G) * SW) * 8 + 16; }
 template <int G>
-constexpr size_t adj_cols_fixed(size_t ybytes) { return (size_t(G) + size_t(G) * SW) * 8 + ybytes + 16; }
+struct AdjCols {   // k_adj_cols layout: separate exchange buffer + register twiddles when it fits
+  static constexpr bool SEP = G <= 512;
+};
+template <int G>
+constexpr size_t adj_cols_fixed(size_t ybytes) {
+  return (AdjCols<G>::SEP ? 2 * size_t(G) * SW : size_t(G) + size_t(G) * SW) * 8 + ybytes + 16;
+}
 
 // Phase timer (experiment bit 2; only compiled with -DMRF_EXPERIMENTS): thread 0 of every CTA
 // accumulates clock64 deltas per phase into p.dbgbuf.
@@ -568,14 +577,20 @@ __device__ __forceinline__ void spread_cells(const int2* sl_tab, const unsigned 
 // a5: column iFFT, then the N kept rows are stored strip-major H[fc][strip][iy][16].
 // Pipeline: y[fc] and the chunk of the next item are fetched right after this item's spread.
 template <int G>
-__global__ void __launch_bounds__(SW * FFTShape<G>::T, (G >= 1024 ? 1 : 2))
+__global__ void __launch_bounds__(SW * FFTShape<G>::T, 1)
 k_adj_cols(DevPlan p, const float2* __restrict__ y, float2* __restrict__ H, int l0, int nb, int ystage, int stage_cap) {
   using F = FFTShape<G>;
   constexpr int P = F::P, Q = F::Q, T = F::T, N = G / 2, A = Q / T, B = P / T, S = G / SW;
+  // SEP (G <= 512): the spread strip S and the FFT exchange buffer E are separate, so S only ever
+  // holds spread values and zeros: the stage-1 loads skip the row pairs the chunk's row mask marks
+  // untouched and re-zero only the touched ones, and the stage-1 twiddles live in registers.
+  // G = 1024 (two 128 KB buffers do not fit) exchanges through S and re-zeroes it in full.
+  constexpr bool SEP = AdjCols<G>::SEP;
   extern __shared__ __align__(128) unsigned char smraw[];
-  float2* stw = reinterpret_cast<float2*>(smraw);
-  float2* strip = stw + G;
-  float2* ys = strip + G * SW;
+  float2* stw = reinterpret_cast<float2*>(smraw);                 // twiddles (!SEP only)
+  float2* strip = stw + (SEP ? 0 : G);
+  float2* ex = SEP ? strip + G * SW : strip;
+  float2* ys = strip + (SEP ? 2 : 1) * G * SW;
   uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<unsigned char*>(ys) + ystage);
   int* stage = reinterpret_cast<int*>(bars + 2);
   __shared__ int copied;
@@ -588,7 +603,15 @@ k_adj_cols(DevPlan p, const float2* __restrict__ y, float2* __restrict__ H, int 
     mbar_init(&bars[0], 1);
     fence_mbar_init();
   }
-  for (int i = tid; i < G; i += blockDim.x) stw[i] = p.tw[i];
+  float2 twr[SEP ? A : 1][SEP ? P : 1];   // stage-1 twiddles W_G^{n2 k1} of this thread (SEP)
+  if constexpr (SEP) {
+#pragma unroll
+    for (int a = 0; a < A; ++a)
+#pragma unroll
+      for (int k1 = 0; k1 < P; ++k1) twr[a][k1] = __ldg(p.tw + (t + T * a) * P + k1);
+  } else {
+    for (int i = tid; i < G; i += blockDim.x) stw[i] = p.tw[i];
+  }
   for (int i = tid; i < G * SW; i += blockDim.x) strip[i] = make_float2(0.f, 0.f);
   __syncthreads();
   pdl_launch_dependents();
@@ -620,13 +643,16 @@ k_adj_cols(DevPlan p, const float2* __restrict__ y, float2* __restrict__ H, int 
     mbar_wait(&bars[0], k & 1);
     pt.mark(0);
     ++nit;
+    // row-pair mask of this warp's stage-1 loads: bit a*P + n1 <=> rows Q n1 + T a + 2 warp + {0,1}
+    // received spread values (read before the staging buffer is refilled)
+    const uint32_t rmask = SEP ? (uint32_t)stage[kChunkHdr + warp] : ~0u;
     {
       // Staged prefix of the chunk: header, slice table and cells always fit (checked at plan
       // time); a slice whose entries lie past the staged prefix reads them from L2.
       const int nsl = MRF_DBG_ON(1) ? 0 : stage[0], cells_off = stage[1], ent_off = stage[2];
       const int n_multi = MRF_DBG_ON(1) ? 0 : stage[3];
       const float2* yf = y + (size_t)fc * M;
-      const int2* sl_tab = reinterpret_cast<const int2*>(stage + kChunkHdr);
+      const int2* sl_tab = reinterpret_cast<const int2*>(stage + kAdjHdr);
       const unsigned short* cells = reinterpret_cast<const unsigned short*>(stage + cells_off);
       const int2* ents = reinterpret_cast<const int2*>(stage + ent_off);
       const int n_staged = (copied / 4 - ent_off) / 2;          // entries in shared memory
@@ -652,9 +678,21 @@ k_adj_cols(DevPlan p, const float2* __restrict__ y, float2* __restrict__ H, int 
     for (int a = 0; a < A; ++a) {
       const int n2 = t + T * a;
 #pragma unroll
-      for (int n1 = 0; n1 < P; ++n1) v[a][n1] = strip[sidx(Q * n1 + n2, c)];
+      for (int n1 = 0; n1 < P; ++n1) {
+        if constexpr (SEP) {   // each cell is read by its one owner, who re-zeroes it for the next spread
+          if ((rmask >> (a * P + n1)) & 1u) {
+            float2& cell = strip[sidx(Q * n1 + n2, c)];
+            v[a][n1] = cell;
+            cell = make_float2(0.f, 0.f);
+          } else {
+            v[a][n1] = make_float2(0.f, 0.f);
+          }
+        } else {
+          v[a][n1] = strip[sidx(Q * n1 + n2, c)];
+        }
+      }
     }
-    __syncthreads();
+    if constexpr (!SEP) __syncthreads();   // the exchange below overwrites the strip
     pt.mark(3);
 #pragma unroll
     for (int a = 0; a < A; ++a) {
@@ -662,9 +700,17 @@ k_adj_cols(DevPlan p, const float2* __restrict__ y, float2* __restrict__ H, int 
       dft<P, +1>(v[a]);
 #pragma unroll
       for (int k1 = 0; k1 < P; k1 += 2) {
-        const float4 tt = tw_pair(stw, n2 * P + k1);
-        strip[(n2 * P + k1) * SW + c] = cmulc(v[a][k1], make_float2(tt.x, tt.y));
-        strip[(n2 * P + k1 + 1) * SW + c] = cmulc(v[a][k1 + 1], make_float2(tt.z, tt.w));
+        float2 t0, t1;
+        if constexpr (SEP) {
+          t0 = twr[a][k1];
+          t1 = twr[a][k1 + 1];
+        } else {
+          const float4 tt = tw_pair(stw, n2 * P + k1);
+          t0 = make_float2(tt.x, tt.y);
+          t1 = make_float2(tt.z, tt.w);
+        }
+        ex[(n2 * P + k1) * SW + c] = cmulc(v[a][k1], t0);
+        ex[(n2 * P + k1 + 1) * SW + c] = cmulc(v[a][k1 + 1], t1);
       }
     }
     __syncthreads();
@@ -674,10 +720,10 @@ k_adj_cols(DevPlan p, const float2* __restrict__ y, float2* __restrict__ H, int 
     for (int b = 0; b < B; ++b) {
       const int k1 = t + T * b;
 #pragma unroll
-      for (int n2 = 0; n2 < Q; ++n2) {   // each cell is read by its one owner, who clears it for the next spread
-        float2& cell = strip[(n2 * P + k1) * SW + c];
+      for (int n2 = 0; n2 < Q; ++n2) {
+        float2& cell = ex[(n2 * P + k1) * SW + c];
         w[b][n2] = cell;
-        cell = make_float2(0.f, 0.f);
+        if constexpr (!SEP) cell = make_float2(0.f, 0.f);   // owner re-zeroes for the next spread
       }
     }
     pt.mark(5);
@@ -692,7 +738,9 @@ k_adj_cols(DevPlan p, const float2* __restrict__ y, float2* __restrict__ H, int 
       }
     }
     pt.mark(6);
-    __syncthreads();   // zero-fill visible before the next spread
+    // !SEP: zero-fill visible before the next spread.  SEP: the next item's spread and exchange are
+    // ordered by its own first barrier (every thread is past its stage-2 loads by then).
+    if constexpr (!SEP) __syncthreads();
     pt.mark(7);
   }
   pt.report(p.dbgbuf ? p.dbgbuf + 16 : nullptr, nit);

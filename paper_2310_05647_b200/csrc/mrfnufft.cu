@@ -194,13 +194,19 @@ static void kb_taps(const KB& kb, int G, int W, float kx, float ky, double* out)
   }
 }
 
-static void fft_shape(int G, int* P, int* Q) {
+template <int G>
+static void fft_shape_t(int* P, int* Q, int* T) {
+  *P = FFTShape<G>::P;
+  *Q = FFTShape<G>::Q;
+  *T = FFTShape<G>::T;
+}
+static void fft_shape(int G, int* P, int* Q, int* T) {
   switch (G) {
-    case 64: *P = FFTShape<64>::P; *Q = FFTShape<64>::Q; break;
-    case 128: *P = FFTShape<128>::P; *Q = FFTShape<128>::Q; break;
-    case 256: *P = FFTShape<256>::P; *Q = FFTShape<256>::Q; break;
-    case 512: *P = FFTShape<512>::P; *Q = FFTShape<512>::Q; break;
-    default: *P = FFTShape<1024>::P; *Q = FFTShape<1024>::Q; break;
+    case 64: fft_shape_t<64>(P, Q, T); break;
+    case 128: fft_shape_t<128>(P, Q, T); break;
+    case 256: fft_shape_t<256>(P, Q, T); break;
+    case 512: fft_shape_t<512>(P, Q, T); break;
+    default: fft_shape_t<1024>(P, Q, T); break;
   }
 }
 
@@ -825,8 +831,8 @@ mrf_status mrf_plan_create(const mrf_plan_desc* d, mrf_plan* out) {
     const double psi = (d->flags & MRF_DEAPOD_DISCRETE) ? kb.psi_discrete(n, G) : kb.psi_analytic(n, G);
     dap[i] = (float)(1.0 / (psi * std::sqrt((double)N)));
   }
-  int P = 0, Q = 0;
-  fft_shape(G, &P, &Q);
+  int P = 0, Q = 0, T = 0;
+  fft_shape(G, &P, &Q, &T);
   std::vector<float2> tw(G);
   for (int k1 = 0; k1 < P; ++k1)
     for (int n2 = 0; n2 < Q; ++n2) {
@@ -920,13 +926,27 @@ mrf_status mrf_plan_create(const mrf_plan_desc* d, mrf_plan* out) {
         nent += 32LL * rows[(size_t)sl * 32].y;
         if (rows[(size_t)sl * 32].y > 1) n_multi = sl + 1;
       }
-      const size_t cells_off = (size_t)kChunkHdr + 2 * (size_t)nsl;
+      const size_t cells_off = (size_t)kAdjHdr + 2 * (size_t)nsl;
       const size_t ent_off = (cells_off + 16 * (size_t)nsl + 1) & ~(size_t)1;
       const size_t words = (ent_off + 2 * (size_t)nent + 3) & ~(size_t)3;
       const size_t base = ach.size();
       ach.resize(base + words, 0);
       int* ch = &ach[base];
       ch[0] = nsl; ch[1] = (int)cells_off; ch[2] = (int)ent_off; ch[3] = n_multi;
+      {   // row-pair masks of k_adj_cols' stage-1 loads: warp w, bit a*P + n1 <-> rows Q n1 + T a + 2w + {0,1}
+        std::vector<char> touched(G, 0);
+        for (const Nz& q : nz) touched[q.cell / SW] = 1;
+        const int nwarps = SW * T / 32, A = Q / T;
+        for (int w = 0; w < nwarps && w < 16; ++w) {
+          uint32_t m = 0;
+          for (int a = 0; a < A; ++a)
+            for (int n1 = 0; n1 < P; ++n1) {
+              const int row = Q * n1 + T * a + 2 * w;
+              if (touched[row] || touched[row + 1]) m |= 1u << (a * P + n1);
+            }
+          ch[kChunkHdr + w] = (int)m;
+        }
+      }
       unsigned short* cells = reinterpret_cast<unsigned short*>(ch + cells_off);
       int2* ents = reinterpret_cast<int2*>(ch + ent_off);
       // entries of the width-1 slices first (one flat run, always staged first), then the others
@@ -934,8 +954,8 @@ mrf_status mrf_plan_create(const mrf_plan_desc* d, mrf_plan* out) {
       for (int sl = 0; sl < nsl; ++sl) {
         const int width = rows[(size_t)sl * 32].y;
         if (sl == n_multi) first = 0;
-        ch[kChunkHdr + 2 * sl] = (int)first;
-        ch[kChunkHdr + 2 * sl + 1] = width;
+        ch[kAdjHdr + 2 * sl] = (int)first;
+        ch[kAdjHdr + 2 * sl + 1] = width;
         for (int lane = 0; lane < 32; ++lane) {
           const size_t ri = (size_t)sl * 32 + lane;
           cells[sl * 32 + lane] = ri < rows.size()
