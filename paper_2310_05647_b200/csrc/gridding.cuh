@@ -529,26 +529,33 @@ k_fwd_cols(DevPlan p, const float2* __restrict__ H, float2* __restrict__ y, int 
 // have width 1 (MRF: 87 %), so the chunk stores their entries first as one flat run: a thread per
 // cell, no slice table.  The n_multi wider slices follow, one warp per slice, entry k of lane l at
 // first + 32k + l.  Every cell is written exactly once.  YS: y[fc] staged in shared memory.
-template <bool YS>
+// PASS 0: the flat run and the wide slices whose entries are staged (entries at ents[e]);
+// PASS 1: the wide slices past the staged prefix, whose entries were brought in by a second bulk
+// copy to ents[e - e0] (up to entry e1; beyond that they are read from L2).
+template <bool YS, int PASS>
 __device__ __forceinline__ void spread_cells(const int2* sl_tab, const unsigned short* cells, const int2* ents,
-                                             const int2* __restrict__ gents, int n_staged, int nsl, int n_multi,
-                                             const float2* ys, const float2* __restrict__ yf, float2* strip, int tid,
-                                             int nthreads, int warp, int nwarps, int lane) {
-  const int n1 = (nsl - n_multi) * 32;
-  const unsigned short* cells1 = cells + n_multi * 32;
-  for (int i = tid; i < n1; i += nthreads) {
-    const int cell = cells1[i];
-    const int2 e = i < n_staged ? ents[i] : __ldg(gents + i);
-    const float wgt = __int_as_float(e.y);
-    const float2 v = YS ? ys[e.x] : __ldg(yf + e.x);
-    if (cell != 0xFFFF) strip[cell] = make_float2(wgt * v.x, wgt * v.y);
+                                             const int2* __restrict__ gents, int n_staged, int e0, int e1, int nsl,
+                                             int n_multi, const float2* ys, const float2* __restrict__ yf,
+                                             float2* strip, int tid, int nthreads, int warp, int nwarps, int lane) {
+  if (PASS == 0) {
+    const int n1 = (nsl - n_multi) * 32;
+    const unsigned short* cells1 = cells + n_multi * 32;
+    for (int i = tid; i < n1; i += nthreads) {
+      const int cell = cells1[i];
+      const int2 e = i < n_staged ? ents[i] : __ldg(gents + i);
+      const float wgt = __int_as_float(e.y);
+      const float2 v = YS ? ys[e.x] : __ldg(yf + e.x);
+      if (cell != 0xFFFF) strip[cell] = make_float2(wgt * v.x, wgt * v.y);
+    }
   }
   for (int sl = warp; sl < n_multi; sl += nwarps) {
     const int2 si = sl_tab[sl];
+    const bool staged = si.x + 32 * si.y <= n_staged;
+    if (staged != (PASS == 0)) continue;
     const int cell = cells[sl * 32 + lane];
     float2 acc = make_float2(0.f, 0.f);
-    if (si.x + 32 * si.y <= n_staged) {
-      const int2* ep = ents + si.x + lane;
+    if (PASS == 0 || si.x + 32 * si.y <= e1) {
+      const int2* ep = ents + (PASS == 0 ? si.x : si.x - e0) + lane;
       for (int kk = 0; kk < si.y; ++kk) {
         const int2 e = ep[kk * 32];
         const float wgt = __int_as_float(e.y);
@@ -594,15 +601,19 @@ k_adj_cols(DevPlan p, const float2* __restrict__ y, float2* __restrict__ H, int 
   uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<unsigned char*>(ys) + ystage);
   int* stage = reinterpret_cast<int*>(bars + 2);
   __shared__ int copied;
-  __shared__ int chunk_off;   // word offset of the staged chunk (for its unstaged tail)
+  __shared__ int chunk_off;    // word offset of the staged chunk (for its unstaged tail)
+  __shared__ int chunk_words;  // its size
+  __shared__ int2 tail;        // {e0, e1}: entries [e0, e1) brought in by the second copy
   const int C = p.C, M = p.M;
   const int n_items = nb * C * S;
   const int tid = threadIdx.x, c = tid % SW, t = tid / SW;
   const int warp = tid >> 5, lane = tid & 31, nwarps = blockDim.x >> 5;
   if (tid == 0) {
     mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
     fence_mbar_init();
   }
+  int n_tail = 0;   // second copies issued by this CTA (mbarrier parity)
   float2 twr[SEP ? A : 1][SEP ? P : 1];   // stage-1 twiddles W_G^{n2 k1} of this thread (SEP)
   if constexpr (SEP) {
 #pragma unroll
@@ -624,6 +635,7 @@ k_adj_cols(DevPlan p, const float2* __restrict__ y, float2* __restrict__ H, int 
     const uint32_t bytes = (uint32_t)min(ow.y * 4, stage_cap) & ~15u;
     copied = (int)bytes;
     chunk_off = ow.x;
+    chunk_words = ow.y;
     mbar_expect_tx(&bars[0], bytes + (uint32_t)ystage);
     bulk_g2s(stage, p.achunks + ow.x, bytes, &bars[0]);
     if (ystage) bulk_g2s(ys, y + (size_t)(item / S) * M, (uint32_t)ystage, &bars[0]);
@@ -658,11 +670,39 @@ k_adj_cols(DevPlan p, const float2* __restrict__ y, float2* __restrict__ H, int 
       const int n_staged = (copied / 4 - ent_off) / 2;          // entries in shared memory
       const int2* gents = reinterpret_cast<const int2*>(p.achunks + chunk_off + ent_off);
       if (ystage)
-        spread_cells<true>(sl_tab, cells, ents, gents, n_staged, nsl, n_multi, ys, yf, strip, tid, blockDim.x, warp,
-                           nwarps, lane);
+        spread_cells<true, 0>(sl_tab, cells, ents, gents, n_staged, 0, 0, nsl, n_multi, ys, yf, strip, tid,
+                              blockDim.x, warp, nwarps, lane);
       else
-        spread_cells<false>(sl_tab, cells, ents, gents, n_staged, nsl, n_multi, ys, yf, strip, tid, blockDim.x, warp,
-                            nwarps, lane);
+        spread_cells<false, 0>(sl_tab, cells, ents, gents, n_staged, 0, 0, nsl, n_multi, ys, yf, strip, tid,
+                               blockDim.x, warp, nwarps, lane);
+      if (copied < chunk_words * 4) {   // chunk larger than the staging buffer (block-uniform)
+        // Second bulk copy: the entries of the wide slices past the staged prefix, from the first
+        // such slice on, over the (now consumed) entry region of the staging buffer.
+        __syncthreads();
+        if (tid == 0) {
+          int sl0 = 0;
+          while (sl0 < n_multi && sl_tab[sl0].x + 32 * sl_tab[sl0].y <= n_staged) ++sl0;
+          const int e0 = sl0 < n_multi ? sl_tab[sl0].x : 0;
+          const int cap = (copied / 4 - ent_off) / 2;          // entries that fit
+          const int nent = (chunk_words - ent_off) / 2;
+          const int e1 = min(nent, e0 + cap);
+          tail = make_int2(e0, e1);
+          const uint32_t bytes = (uint32_t)(e1 - e0) * 8u;
+          fence_proxy_async();
+          mbar_expect_tx(&bars[1], bytes);   // (arrives; completes at once when bytes == 0)
+          if (bytes) bulk_g2s(stage + ent_off, p.achunks + chunk_off + ent_off + 2 * e0, bytes, &bars[1]);
+        }
+        __syncthreads();
+        mbar_wait(&bars[1], n_tail & 1);
+        ++n_tail;
+        const int2 tl = tail;
+        if (ystage)
+          spread_cells<true, 1>(sl_tab, cells, ents, gents, n_staged, tl.x, tl.y, nsl, n_multi, ys, yf, strip, tid,
+                                blockDim.x, warp, nwarps, lane);
+        else
+          spread_cells<false, 1>(sl_tab, cells, ents, gents, n_staged, tl.x, tl.y, nsl, n_multi, ys, yf, strip, tid,
+                                 blockDim.x, warp, nwarps, lane);
+      }
     }
     pt.mark(1);
     __syncthreads();

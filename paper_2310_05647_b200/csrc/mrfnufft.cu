@@ -927,7 +927,7 @@ mrf_status mrf_plan_create(const mrf_plan_desc* d, mrf_plan* out) {
         if (rows[(size_t)sl * 32].y > 1) n_multi = sl + 1;
       }
       const size_t cells_off = (size_t)kAdjHdr + 2 * (size_t)nsl;
-      const size_t ent_off = (cells_off + 16 * (size_t)nsl + 1) & ~(size_t)1;
+      const size_t ent_off = (cells_off + 16 * (size_t)nsl + 3) & ~(size_t)3;   // 16-byte aligned entries
       const size_t words = (ent_off + 2 * (size_t)nent + 3) & ~(size_t)3;
       const size_t base = ach.size();
       ach.resize(base + words, 0);
