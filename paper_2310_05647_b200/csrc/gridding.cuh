@@ -41,7 +41,8 @@ struct CGScalars;
 //     [0] n_slices [1] cells offset [2] entries offset [3] n_multi (slices of width > 1) [4..7] 0
 //     [8 + w], w < 16: row-pair mask of warp w's stage-1 loads in k_adj_cols (bit a*P + n1 set if
 //     row Q n1 + T a + 2w or the next row holds a spread value)
-//     slices : n_slices x {first entry, width}, widths non-increasing
+//     slices : n_slices x {first entry, width}; width < 0: a reduction slice (one cell, its entries
+//              spread over the 32 lanes, summed by a warp reduction), then widths non-increasing
 //     cells  : n_slices x 32 uint16 strip cells (swizzled slot), 0xFFFF = empty lane
 //     entries: {j, w = wx*wy (fp32 bits, from float64)}; entry k of lane l at first + 32k + l;
 //              the width-1 slices' entries come first (one flat run), then the wider slices'.
@@ -530,13 +531,14 @@ k_fwd_cols(DevPlan p, const float2* __restrict__ H, float2* __restrict__ y, int 
 // cell, no slice table.  The n_multi wider slices follow, one warp per slice, entry k of lane l at
 // first + 32k + l.  Every cell is written exactly once.  YS: y[fc] staged in shared memory.
 // PASS 0: the flat run and the wide slices whose entries are staged (entries at ents[e]);
-// PASS 1: the wide slices past the staged prefix, whose entries were brought in by a second bulk
-// copy to ents[e - e0] (up to entry e1; beyond that they are read from L2).
+// PASS 1: wide slices [sl_lo, sl_hi) past the staged prefix, whose entries a further bulk copy
+// brought to ents[e - e0] (from_l2: one slice too wide for the buffer, read from L2).
 template <bool YS, int PASS>
 __device__ __forceinline__ void spread_cells(const int2* sl_tab, const unsigned short* cells, const int2* ents,
-                                             const int2* __restrict__ gents, int n_staged, int e0, int e1, int nsl,
-                                             int n_multi, const float2* ys, const float2* __restrict__ yf,
-                                             float2* strip, int tid, int nthreads, int warp, int nwarps, int lane) {
+                                             const int2* __restrict__ gents, int n_staged, int e0, int sl_lo,
+                                             int sl_hi, bool from_l2, int nsl, int n_multi, const float2* ys,
+                                             const float2* __restrict__ yf, float2* strip, int tid, int nthreads,
+                                             int warp, int nwarps, int lane) {
   if (PASS == 0) {
     const int n1 = (nsl - n_multi) * 32;
     const unsigned short* cells1 = cells + n_multi * 32;
@@ -547,16 +549,18 @@ __device__ __forceinline__ void spread_cells(const int2* sl_tab, const unsigned 
       const float2 v = YS ? ys[e.x] : __ldg(yf + e.x);
       if (cell != 0xFFFF) strip[cell] = make_float2(wgt * v.x, wgt * v.y);
     }
+    sl_lo = 0;
+    sl_hi = n_multi;
   }
-  for (int sl = warp; sl < n_multi; sl += nwarps) {
+  for (int sl = sl_lo + warp; sl < sl_hi; sl += nwarps) {
     const int2 si = sl_tab[sl];
-    const bool staged = si.x + 32 * si.y <= n_staged;
-    if (staged != (PASS == 0)) continue;
+    const int width = abs(si.y);   // si.y < 0: the 32 lanes share one cell (warp reduction)
+    if (PASS == 0 && si.x + 32 * width > n_staged) break;   // firsts increase with sl
     const int cell = cells[sl * 32 + lane];
     float2 acc = make_float2(0.f, 0.f);
-    if (PASS == 0 || si.x + 32 * si.y <= e1) {
-      const int2* ep = ents + (PASS == 0 ? si.x : si.x - e0) + lane;
-      for (int kk = 0; kk < si.y; ++kk) {
+    if (!from_l2) {
+      const int2* ep = ents + (si.x - e0) + lane;
+      for (int kk = 0; kk < width; ++kk) {
         const int2 e = ep[kk * 32];
         const float wgt = __int_as_float(e.y);
         const float2 v = YS ? ys[e.x] : __ldg(yf + e.x);
@@ -566,7 +570,7 @@ __device__ __forceinline__ void spread_cells(const int2* sl_tab, const unsigned 
     } else {
       const int2* ep = gents + si.x + lane;
 #pragma unroll 4
-      for (int kk = 0; kk < si.y; ++kk) {
+      for (int kk = 0; kk < width; ++kk) {
         const int2 e = __ldg(ep + kk * 32);
         const float wgt = __int_as_float(e.y);
         const float2 v = YS ? ys[e.x] : __ldg(yf + e.x);
@@ -574,7 +578,16 @@ __device__ __forceinline__ void spread_cells(const int2* sl_tab, const unsigned 
         acc.y = fmaf(wgt, v.y, acc.y);
       }
     }
-    if (cell != 0xFFFF) strip[cell] = acc;
+    if (si.y < 0) {   // warp-uniform
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
+        acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
+      }
+      if (lane == 0) strip[cell] = acc;
+    } else if (cell != 0xFFFF) {
+      strip[cell] = acc;
+    }
   }
 }
 
@@ -603,7 +616,7 @@ k_adj_cols(DevPlan p, const float2* __restrict__ y, float2* __restrict__ H, int 
   __shared__ int copied;
   __shared__ int chunk_off;    // word offset of the staged chunk (for its unstaged tail)
   __shared__ int chunk_words;  // its size
-  __shared__ int2 tail;        // {e0, e1}: entries [e0, e1) brought in by the second copy
+  __shared__ int4 win;         // {e0, slice end, from-L2 flag}: the current window of wide slices
   const int C = p.C, M = p.M;
   const int n_items = nb * C * S;
   const int tid = threadIdx.x, c = tid % SW, t = tid / SW;
@@ -670,38 +683,47 @@ k_adj_cols(DevPlan p, const float2* __restrict__ y, float2* __restrict__ H, int 
       const int n_staged = (copied / 4 - ent_off) / 2;          // entries in shared memory
       const int2* gents = reinterpret_cast<const int2*>(p.achunks + chunk_off + ent_off);
       if (ystage)
-        spread_cells<true, 0>(sl_tab, cells, ents, gents, n_staged, 0, 0, nsl, n_multi, ys, yf, strip, tid,
+        spread_cells<true, 0>(sl_tab, cells, ents, gents, n_staged, 0, 0, 0, false, nsl, n_multi, ys, yf, strip, tid,
                               blockDim.x, warp, nwarps, lane);
       else
-        spread_cells<false, 0>(sl_tab, cells, ents, gents, n_staged, 0, 0, nsl, n_multi, ys, yf, strip, tid,
-                               blockDim.x, warp, nwarps, lane);
+        spread_cells<false, 0>(sl_tab, cells, ents, gents, n_staged, 0, 0, 0, false, nsl, n_multi, ys, yf, strip,
+                               tid, blockDim.x, warp, nwarps, lane);
       if (copied < chunk_words * 4) {   // chunk larger than the staging buffer (block-uniform)
-        // Second bulk copy: the entries of the wide slices past the staged prefix, from the first
-        // such slice on, over the (now consumed) entry region of the staging buffer.
-        __syncthreads();
-        if (tid == 0) {
-          int sl0 = 0;
-          while (sl0 < n_multi && sl_tab[sl0].x + 32 * sl_tab[sl0].y <= n_staged) ++sl0;
-          const int e0 = sl0 < n_multi ? sl_tab[sl0].x : 0;
-          const int cap = (copied / 4 - ent_off) / 2;          // entries that fit
-          const int nent = (chunk_words - ent_off) / 2;
-          const int e1 = min(nent, e0 + cap);
-          tail = make_int2(e0, e1);
-          const uint32_t bytes = (uint32_t)(e1 - e0) * 8u;
-          fence_proxy_async();
-          mbar_expect_tx(&bars[1], bytes);   // (arrives; completes at once when bytes == 0)
-          if (bytes) bulk_g2s(stage + ent_off, p.achunks + chunk_off + ent_off + 2 * e0, bytes, &bars[1]);
+        // The wide slices past the staged prefix: windows of whole slices brought in by further
+        // bulk copies over the (consumed) entry region; a slice wider than the region reads L2.
+        const int cap = (copied / 4 - ent_off) / 2;          // entries that fit
+        const int nent = (chunk_words - ent_off) / 2;
+        int sl0 = 0;
+        while (sl0 < n_multi && sl_tab[sl0].x + 32 * abs(sl_tab[sl0].y) <= n_staged) ++sl0;
+        while (sl0 < n_multi) {   // sl0 is block-uniform
+          __syncthreads();        // the previous window's entries are consumed
+          if (tid == 0) {
+            const int e0 = sl_tab[sl0].x, e1 = min(nent, e0 + cap);
+            int hi = sl0;
+            while (hi < n_multi && sl_tab[hi].x + 32 * abs(sl_tab[hi].y) <= e1) ++hi;
+            const bool big = hi == sl0;
+            win = make_int4(e0, hi == sl0 ? sl0 + 1 : hi, big ? 1 : 0, 0);
+            if (!big) {
+              const uint32_t bytes = (uint32_t)(sl_tab[hi - 1].x + 32 * abs(sl_tab[hi - 1].y) - e0) * 8u;
+              fence_proxy_async();
+              mbar_expect_tx(&bars[1], bytes);
+              bulk_g2s(stage + ent_off, p.achunks + chunk_off + ent_off + 2 * e0, bytes, &bars[1]);
+            }
+          }
+          __syncthreads();
+          const int4 wv = win;
+          if (!wv.z) {
+            mbar_wait(&bars[1], n_tail & 1);
+            ++n_tail;
+          }
+          if (ystage)
+            spread_cells<true, 1>(sl_tab, cells, ents, gents, n_staged, wv.x, sl0, wv.y, wv.z != 0, nsl, n_multi, ys,
+                                  yf, strip, tid, blockDim.x, warp, nwarps, lane);
+          else
+            spread_cells<false, 1>(sl_tab, cells, ents, gents, n_staged, wv.x, sl0, wv.y, wv.z != 0, nsl, n_multi, ys,
+                                   yf, strip, tid, blockDim.x, warp, nwarps, lane);
+          sl0 = wv.y;
         }
-        __syncthreads();
-        mbar_wait(&bars[1], n_tail & 1);
-        ++n_tail;
-        const int2 tl = tail;
-        if (ystage)
-          spread_cells<true, 1>(sl_tab, cells, ents, gents, n_staged, tl.x, tl.y, nsl, n_multi, ys, yf, strip, tid,
-                                blockDim.x, warp, nwarps, lane);
-        else
-          spread_cells<false, 1>(sl_tab, cells, ents, gents, n_staged, tl.x, tl.y, nsl, n_multi, ys, yf, strip, tid,
-                                 blockDim.x, warp, nwarps, lane);
       }
     }
     pt.mark(1);

@@ -919,12 +919,26 @@ mrf_status mrf_plan_create(const mrf_plan_desc* d, mrf_plan* out) {
         i = k;
       }
       std::stable_sort(rows.begin(), rows.end(), [](const int2& a, const int2& b) { return a.y > b.y; });
-      const int nsl = (int)((rows.size() + 31) / 32);
+      // Slices: a cell with more than kSplitEntries entries gets a slice of its own whose 32 lanes
+      // share its entries (entry i -> lane i % 32, step i / 32) and are summed by a warp reduction
+      // (width stored negated); then the other cells in groups of 32, widest first; the width-1
+      // slices last.  Slices [0, n_multi) are the ones wider than 1.
+      // measured: 128 (stress normal 254 -> 83 ms); a lower threshold costs more in per-slice
+      // reductions than it saves (MRF, where no cell exceeds 120 entries, is unaffected)
+      constexpr int kSplitEntries = 128;
+      std::vector<int2> slices;   // {first row index, width (< 0: reduction slice of one row)}
+      size_t r0 = 0;
+      while (r0 < rows.size() && rows[r0].y > kSplitEntries) {
+        slices.push_back(make_int2((int)r0, -((rows[r0].y + 31) / 32)));
+        ++r0;
+      }
+      for (size_t i = r0; i < rows.size(); i += 32) slices.push_back(make_int2((int)i, rows[i].y));
+      const int nsl = (int)slices.size();
       long long nent = 0;
-      int n_multi = 0;   // slices are sorted by width: slices [0, n_multi) have width > 1
+      int n_multi = 0;
       for (int sl = 0; sl < nsl; ++sl) {
-        nent += 32LL * rows[(size_t)sl * 32].y;
-        if (rows[(size_t)sl * 32].y > 1) n_multi = sl + 1;
+        nent += 32LL * std::abs(slices[sl].y);
+        if (slices[sl].y != 1) n_multi = sl + 1;
       }
       const size_t cells_off = (size_t)kAdjHdr + 2 * (size_t)nsl;
       const size_t ent_off = (cells_off + 16 * (size_t)nsl + 3) & ~(size_t)3;   // 16-byte aligned entries
@@ -951,26 +965,32 @@ mrf_status mrf_plan_create(const mrf_plan_desc* d, mrf_plan* out) {
       int2* ents = reinterpret_cast<int2*>(ch + ent_off);
       // entries of the width-1 slices first (one flat run, always staged first), then the others
       long long first = 32LL * (nsl - n_multi);
+      auto put = [&](long long pos, const Nz& q) {
+        const float wf = (float)q.w;
+        int2 e = make_int2(q.j, 0);
+        std::memcpy(&e.y, &wf, 4);
+        ents[pos] = e;
+      };
+      auto slot = [&](const int2& row) {
+        return (unsigned short)sidx(nz[row.x].cell / SW, nz[row.x].cell % SW);   // swizzled strip slot
+      };
       for (int sl = 0; sl < nsl; ++sl) {
-        const int width = rows[(size_t)sl * 32].y;
+        const int width = slices[sl].y;
         if (sl == n_multi) first = 0;
         ch[kAdjHdr + 2 * sl] = (int)first;
         ch[kAdjHdr + 2 * sl + 1] = width;
+        if (width < 0) {   // reduction slice: entries of one cell in order, lanes interleaved
+          const int2& row = rows[(size_t)slices[sl].x];
+          for (int lane = 0; lane < 32; ++lane) cells[sl * 32 + lane] = slot(row);
+          for (int i = 0; i < row.y; ++i) put(first + i, nz[row.x + i]);
+          first += 32LL * -width;
+          continue;
+        }
         for (int lane = 0; lane < 32; ++lane) {
-          const size_t ri = (size_t)sl * 32 + lane;
-          cells[sl * 32 + lane] = ri < rows.size()
-                                      ? (unsigned short)sidx(nz[rows[ri].x].cell / SW, nz[rows[ri].x].cell % SW)
-                                      : (unsigned short)0xFFFF;   // swizzled strip slot
-          for (int k = 0; k < width; ++k) {
-            int2 e = make_int2(0, 0);
-            if (ri < rows.size() && k < rows[ri].y) {
-              const Nz& q = nz[rows[ri].x + k];
-              const float wf = (float)q.w;
-              e.x = q.j;
-              std::memcpy(&e.y, &wf, 4);
-            }
-            ents[first + 32LL * k + lane] = e;
-          }
+          const size_t ri = (size_t)slices[sl].x + lane;
+          cells[sl * 32 + lane] = ri < rows.size() ? slot(rows[ri]) : (unsigned short)0xFFFF;
+          for (int k = 0; k < width; ++k)
+            if (ri < rows.size() && k < rows[ri].y) put(first + 32LL * k + lane, nz[rows[ri].x + k]);
         }
         first += 32LL * width;
       }
