@@ -999,12 +999,14 @@ mrf_status mrf_plan_create(const mrf_plan_desc* d, mrf_plan* out) {
   }
   if (fch.size() > (size_t)INT32_MAX || ach.size() > (size_t)INT32_MAX)
     return bail(fail(MRF_EUNSUPPORTED, "plan tables too large"));
-  // ---- batch size: keep the [bf*C][N][G] half grid well inside L2 -------------------------------
+  // ---- batch size: frames per launch (per lane) ---------------------------------------------------
   const size_t per_frame = (size_t)C * N * G * sizeof(float2);
   int bf = d->batch_frames;
   if (bf == 0) {
     const size_t target = 128ull << 20;   // per lane; measured: launch-tail amortisation beats L2 residency
     bf = (int)std::max<size_t>(1, target / per_frame);
+    // at least one batch per lane (frame shards of 8 GPUs: 125 MRF frames -> 2 x 63, 3 % faster)
+    bf = std::min(bf, std::max(1, (L + kDefaultLanes - 1) / kDefaultLanes));
   }
   bf = std::min(bf, L);
   pl->bf = bf;

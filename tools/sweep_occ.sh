@@ -1,5 +1,6 @@
 python -m pytest tests/test_gpu_parity.py -x -q -m gpu 2>&1 | tail -2
-python tools/op_breakdown.py --workload stress --op normal --reps 2 2>&1 | tail -1
-python tools/op_breakdown.py --workload stress --op normal --normal toeplitz --reps 2 2>&1 | tail -1
 python tools/op_breakdown.py --op normal --reps 10 2>&1 | tail -1
-python tools/op_breakdown.py --op cg --reps 3 2>&1 | tail -1
+python tools/op_breakdown.py --op forward --reps 10 2>&1 | tail -1
+MRF_LANES=1 python tools/op_breakdown.py --op forward --reps 10 2>&1 | tail -1
+python tools/op_breakdown.py --workload stress --op forward --reps 2 2>&1 | tail -1
+python tools/op_breakdown.py --op normal --frames 125 --reps 10 2>&1 | tail -1
