@@ -147,6 +147,31 @@ mrf_status mrf_nccl_get_unique_id(void* id_out128);
 mrf_status mrf_nccl_comm_init(void** comm_out, int nranks, const void* id128, int rank, int device);
 mrf_status mrf_nccl_comm_destroy(void* comm);
 
+/* ---- dictionary matching Phi_D (Eqs. (4)-(5)) -------------
+ *
+ *   k_v   = argmax_k |<d_k, x_v>| / ||d_k||_2        ties -> lowest k   (reading 21)
+ *   pd_v  = max(Re<d_k, x_v> / ||d_k||_2^2, 0)       eta_v = LUT[k_v]
+ *
+ * with <d, x> = sum_l conj(d_l) x_l over the L frames.  The correlations run on the tensor cores
+ * (tcgen05, fp16 operands scaled per voxel and per atom into [-1, 1], fp32 accumulation), so
+ * near-ties (atoms whose normalised correlations with x_v differ by less than ~1e-4 of the
+ * maximum) may resolve to either atom; pd is then recomputed exactly in fp32 for the chosen atom. */
+typedef struct mrf_dict_s* mrf_dict;
+
+/* atoms: HOST [K][L] complex64 (interleaved re, im), copied; lut: HOST [K][P] float (P >= 0
+ * parameters per atom, e.g. T1, T2; NULL if P == 0), copied.  K >= 1, 1 <= L <= 65536.
+ * Errors: MRF_EINVAL (sizes / NULL), MRF_ENOMEM, MRF_ECUDA.  An all-zero atom is never matched. */
+mrf_status mrf_dict_create(const void* atoms, const float* lut, int K, int L, int P, int device, mrf_dict* out);
+
+/* x: DEVICE [L][V] complex64, frame-major (the layout of the image stack, voxel fastest).
+ * index: DEVICE int32 [V]; pd: DEVICE float [V]; params: DEVICE float [V][P] or NULL.  All
+ * 16-byte aligned.  Asynchronous on `stream`; workspace (V x 2L fp16) is allocated on first use
+ * and grown as needed (that call synchronises).  Errors: MRF_EINVAL, MRF_ENOMEM, MRF_ECUDA. */
+mrf_status mrf_dict_match(mrf_dict dict, const void* x, long long V, int* index, float* pd, float* params,
+                          void* stream);
+
+mrf_status mrf_dict_destroy(mrf_dict dict);
+
 #ifdef __cplusplus
 }
 #endif

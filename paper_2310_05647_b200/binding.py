@@ -30,6 +30,7 @@ EXPORTED = [
     "mrf_plan_create", "mrf_forward", "mrf_adjoint", "mrf_normal", "mrf_dc_cg", "mrf_plan_destroy",
     "mrf_status_string", "mrf_last_error", "mrf_plan_device_bytes", "mrf_profile_enable",
     "mrf_profile_query", "mrf_nccl_get_unique_id", "mrf_nccl_comm_init", "mrf_nccl_comm_destroy",
+    "mrf_dict_create", "mrf_dict_match", "mrf_dict_destroy",
 ]
 
 
@@ -77,6 +78,9 @@ def _load() -> ctypes.CDLL:
         "mrf_nccl_get_unique_id": ([vp], ci),
         "mrf_nccl_comm_init": ([ctypes.POINTER(vp), ci, vp, ci, ci], ci),
         "mrf_nccl_comm_destroy": ([vp], ci),
+        "mrf_dict_create": ([vp, vp, ci, ci, ci, ci, ctypes.POINTER(vp)], ci),
+        "mrf_dict_match": ([vp, vp, ctypes.c_longlong, vp, vp, vp, vp], ci),
+        "mrf_dict_destroy": ([vp], ci),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)
@@ -269,3 +273,51 @@ def nccl_comm_create(rank: int, world: int, device: int):
 def nccl_comm_destroy(comm):
     if comm:
         _check(lib.mrf_nccl_comm_destroy(ctypes.c_void_p(comm)))
+
+
+class Dictionary:
+    """Dictionary matching Phi_D (Eq. (5); include/mrfnufft.h mrf_dict_*).
+
+    atoms: [K][L] complex64 (host); lut: [K][P] float32 parameters (e.g. T1, T2) or None.
+    match(x) takes the frame-major image stack x [L][...voxels] (CUDA complex64) and returns
+    (index int32 [V], pd float32 [V], params float32 [V][P] or None) on x's device.
+    """
+
+    def __init__(self, atoms, lut=None, device: Optional[int] = None):
+        a = np.ascontiguousarray(np.asarray(atoms, dtype=np.complex64))
+        if a.ndim != 2:
+            raise ValueError("atoms must be [K][L]")
+        self.K, self.L = a.shape
+        lt = None if lut is None else np.ascontiguousarray(np.asarray(lut, dtype=np.float32))
+        self.P = 0 if lt is None else lt.reshape(self.K, -1).shape[1]
+        self.device = torch.cuda.current_device() if device is None else device
+        h = ctypes.c_void_p()
+        _check(lib.mrf_dict_create(a.ctypes.data_as(ctypes.c_void_p),
+                                   None if lt is None else lt.ctypes.data_as(ctypes.c_void_p),
+                                   self.K, self.L, self.P, self.device, ctypes.byref(h)))
+        self._h = h
+
+    def match(self, x: torch.Tensor):
+        if not (isinstance(x, torch.Tensor) and x.is_cuda and x.dtype == torch.complex64 and x.is_contiguous()):
+            raise TypeError("x must be a contiguous CUDA complex64 tensor [L][...]")
+        if x.shape[0] != self.L:
+            raise ValueError(f"x must have {self.L} frames, got {x.shape[0]}")
+        V = x.numel() // self.L
+        index = torch.empty(V, dtype=torch.int32, device=x.device)
+        pd = torch.empty(V, dtype=torch.float32, device=x.device)
+        params = torch.empty((V, self.P), dtype=torch.float32, device=x.device) if self.P else None
+        st = torch.cuda.current_stream(x.device).cuda_stream
+        _check(lib.mrf_dict_match(self._h, _ptr(x), V, _ptr(index), _ptr(pd), _ptr(params), ctypes.c_void_p(st)))
+        return index, pd, params
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib.mrf_dict_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+

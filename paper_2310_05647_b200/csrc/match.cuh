@@ -1,0 +1,281 @@
+// match.cuh -- dictionary matching Phi_D (Eq. (5)) on the
+// sm_100a tensor cores.
+//
+//   k_v = argmax_k |<d_k, x_v>| / ||d_k||          (reading 21; ties -> lowest k)
+//   rho_v = max(Re<d_k, x_v> / ||d_k||^2, 0),  eta_v = LUT[k_v]
+//
+// The correlations of all voxels with all atoms are one complex GEMM, done as a real fp16 GEMM
+// with fp32 accumulation: voxel row v = (xr_0, xi_0, xr_1, xi_1, ...) / s_v, atom rows
+// 2k = (dr_l, di_l) / m_k and 2k+1 = (-di_l, dr_l) / m_k, so output columns (2k, 2k+1) are
+// (Re, Im) <d_k, x_v> / (s_v m_k).  s_v (per voxel) and m_k (per atom) are max-abs scales that
+// keep the fp16 operands in [-1, 1]; the argmax uses |c~|^2 * (m_k / ||d_k||)^2 (s_v is common
+// to a voxel's row).  rho is recomputed exactly in fp32 for the chosen atom (k_dict_fix).
+//
+// k_dict_gemm: one CTA per 128 voxels, 256 threads in roles: warp 0 = TMA producer (128-byte
+// swizzled tiles, 4-stage mbarrier ring), warp 1 = TMEM allocator + single-thread tcgen05.mma
+// issuer (M = 128, N = 256, K = 16 per instruction, fp32 accumulators in TMEM, two 256-column
+// accumulator buffers so the epilogue of one atom tile overlaps the MMAs of the next), warps
+// 4..7 = epilogue (tcgen05.ld, one voxel per thread = TMEM lane, running argmax in registers).
+#pragma once
+#include <cuda.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace mrf {
+namespace dm {
+
+constexpr int BM = 128;          // voxels per CTA (UMMA M)
+constexpr int BN = 256;          // GEMM columns per atom tile (UMMA N) = 128 atoms
+constexpr int BK = 64;           // fp16 per 128-byte swizzled row
+constexpr int UK = 16;           // UMMA K for kind::f16
+constexpr int STAGES = 4;
+constexpr int A_BYTES = BM * BK * 2;   // 16 KB
+constexpr int B_BYTES = BN * BK * 2;   // 32 KB
+constexpr int THREADS = 256;
+constexpr size_t SMEM = 1024 + (size_t)STAGES * (A_BYTES + B_BYTES) + 256;
+
+__device__ __forceinline__ uint32_t saddr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void bar_init(uint64_t* b, uint32_t n) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(saddr(b)), "r"(n) : "memory");
+}
+__device__ __forceinline__ void bar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(saddr(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(saddr(b)) : "memory");
+}
+__device__ __forceinline__ void bar_wait(uint64_t* b, uint32_t parity) {
+  uint32_t ok = 0;
+  while (!ok) {
+    asm volatile(
+        "{\n .reg .pred P;\n mbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2;\n selp.u32 %0, 1, 0, P;\n}\n"
+        : "=r"(ok)
+        : "r"(saddr(b)), "r"(parity)
+        : "memory");
+  }
+}
+// 2D tiled TMA load (box from the tensor map) into shared memory, completion on an mbarrier
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* b) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          saddr(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(saddr(b))
+      : "memory");
+}
+// UMMA shared-memory descriptor, K-major operand in 128-byte swizzled rows (8-row atoms 1 KB apart)
+__device__ __forceinline__ uint64_t sdesc(uint32_t saddr_bytes) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr_bytes >> 4) & 0x3FFF);   // start address
+  d |= (uint64_t)1 << 16;                         // leading byte offset (unused for swizzled K-major)
+  d |= (uint64_t)(1024 >> 4) << 32;               // stride byte offset: 8 rows x 128 B
+  d |= (uint64_t)1 << 46;                         // descriptor version (sm_100)
+  d |= (uint64_t)2 << 61;                         // SWIZZLE_128B
+  return d;
+}
+// instruction descriptor: kind::f16, fp16 A/B, fp32 D, both K-major, M = 128, N = 256
+constexpr uint32_t kIdesc = (1u << 4) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+
+__device__ __forceinline__ void mma_f16(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t acc) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(
+          tmem_d),
+      "l"(a), "l"(b), "r"(kIdesc), "r"(acc)
+      : "memory");
+}
+__device__ __forceinline__ void mma_commit(uint64_t* b) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(saddr(b))
+               : "memory");
+}
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+
+// 32 consecutive fp32 TMEM columns of this thread's lane
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+        "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// best[v] = argmax_k over the atom tiles.  w2[k] = (m_k / ||d_k||)^2 (0 for padding atoms).
+// X~ [Vpad][KD] and D~ [NP][KD] fp16 are read through the tensor maps; n_tiles = NP / BN;
+// kblocks = KD / BK.
+__global__ void __launch_bounds__(THREADS, 1)
+k_dict_gemm(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmd,
+            const float* __restrict__ w2, int n_tiles, int kblocks, int V, int* __restrict__ best) {
+  extern __shared__ __align__(1024) unsigned char dm_raw[];
+  unsigned char* base = (unsigned char*)(((uintptr_t)dm_raw + 1023) & ~(uintptr_t)1023);
+  unsigned char* sA = base;
+  unsigned char* sB = base + STAGES * A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * B_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tbase = reinterpret_cast<uint32_t*>(tempty + 2);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m0 = blockIdx.x * BM;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      bar_init(&full[s], 1);
+      bar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      bar_init(&tfull[a], 1);
+      bar_init(&tempty[a], 4 * 32);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {   // 512 TMEM columns = two 256-column fp32 accumulators
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(saddr(tbase)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tbase;
+
+  if (warp == 0 && lane == 0) {
+    // ---- TMA producer
+    int it = 0;
+    for (int nt = 0; nt < n_tiles; ++nt)
+      for (int kb = 0; kb < kblocks; ++kb, ++it) {
+        const int s = it % STAGES;
+        bar_wait(&empty[s], ((it / STAGES) & 1) ^ 1);
+        bar_expect_tx(&full[s], A_BYTES + B_BYTES);
+        tma_load_2d(sA + s * A_BYTES, &tmx, kb * BK, m0, &full[s]);
+        tma_load_2d(sB + s * B_BYTES, &tmd, kb * BK, nt * BN, &full[s]);
+      }
+  } else if (warp == 1 && lane == 0) {
+    // ---- MMA issuer
+    int it = 0;
+    for (int nt = 0; nt < n_tiles; ++nt) {
+      const int acc = nt & 1, use = nt >> 1;
+      bar_wait(&tempty[acc], (use & 1) ^ 1);
+      tc_fence_after();
+      const uint32_t td = tmem + (uint32_t)(acc * BN);
+      for (int kb = 0; kb < kblocks; ++kb, ++it) {
+        const int s = it % STAGES;
+        bar_wait(&full[s], (it / STAGES) & 1);
+        tc_fence_after();
+        const uint32_t a0 = saddr(sA + s * A_BYTES), b0 = saddr(sB + s * B_BYTES);
+#pragma unroll
+        for (int k = 0; k < BK / UK; ++k)
+          mma_f16(td, sdesc(a0 + k * UK * 2), sdesc(b0 + k * UK * 2), (kb | k) != 0);
+        mma_commit(&empty[s]);   // frees the stage once these MMAs have read it
+      }
+      mma_commit(&tfull[acc]);   // accumulator complete
+    }
+  } else if (warp >= 4) {
+    // ---- epilogue: thread = TMEM lane = voxel m0 + row
+    const int row = (warp - 4) * 32 + lane;
+    const uint32_t lane_addr = (uint32_t)((warp - 4) * 32) << 16;
+    float bsc = -1.f;
+    int bk = 0;
+    for (int nt = 0; nt < n_tiles; ++nt) {
+      const int acc = nt & 1, use = nt >> 1;
+      bar_wait(&tfull[acc], use & 1);
+      __syncwarp();   // tcgen05.ld is .sync.aligned
+      tc_fence_after();
+#pragma unroll 1
+      for (int ch = 0; ch < BN / 32; ++ch) {
+        float v[32];
+        tmem_ld32(tmem + lane_addr + (uint32_t)(acc * BN + ch * 32), v);
+        const int k0 = nt * (BN / 2) + ch * 16;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const float sc = (v[2 * j] * v[2 * j] + v[2 * j + 1] * v[2 * j + 1]) * __ldg(w2 + k0 + j);
+          if (sc > bsc) {   // strict: equal scores keep the lowest atom index
+            bsc = sc;
+            bk = k0 + j;
+          }
+        }
+      }
+      tc_fence_before();
+      bar_arrive(&tempty[acc]);
+    }
+    if (m0 + row < V) best[m0 + row] = bk;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    __syncwarp();
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  }
+}
+
+// X [L][V] complex64 (frame-major image stack) -> X~ [Vpad][KD] fp16, row v = interleaved
+// (Re, Im) x_v / s_v, zero-padded to KD; s[v] = max_l max(|Re|, |Im|) (1 if the voxel is zero).
+// Block = 32 voxels x 8 row-groups; two passes over the voxels' time series.
+__global__ void __launch_bounds__(256) k_dict_pack_x(const float2* __restrict__ x, int L, int V, int KD,
+                                                     __half* __restrict__ xp, float* __restrict__ s) {
+  __shared__ float red[8][33];
+  __shared__ __half2 tile[32][33];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int v = blockIdx.x * 32 + tx;
+  float m = 0.f;
+  if (v < V)
+    for (int l = ty; l < L; l += 8) {
+      const float2 a = __ldg(x + (size_t)l * V + v);
+      m = fmaxf(m, fmaxf(fabsf(a.x), fabsf(a.y)));
+    }
+  red[ty][tx] = m;
+  __syncthreads();
+  if (ty == 0) {
+    float mm = 0.f;
+    for (int i = 0; i < 8; ++i) mm = fmaxf(mm, red[i][tx]);
+    red[0][tx] = mm > 0.f ? mm : 1.f;
+    if (v < V) s[v] = red[0][tx];
+  }
+  __syncthreads();
+  const float inv = 1.f / red[0][tx];
+  const int L2 = KD / 2;   // complex slots per padded row
+  for (int l0 = 0; l0 < L2; l0 += 32) {
+    // load 32 frames x 32 voxels (coalesced over voxels), transpose through shared memory
+    for (int i = ty; i < 32; i += 8) {
+      const int l = l0 + i;
+      float2 a = make_float2(0.f, 0.f);
+      if (v < V && l < L) a = __ldg(x + (size_t)l * V + v);
+      tile[tx][i] = __floats2half2_rn(a.x * inv, a.y * inv);
+    }
+    __syncthreads();
+    for (int i = ty; i < 32; i += 8) {   // voxel blockIdx*32 + i, frames l0 + tx
+      const int vv = blockIdx.x * 32 + i;
+      reinterpret_cast<__half2*>(xp + (size_t)vv * KD)[l0 + tx] = tile[i][tx];
+    }
+    __syncthreads();
+  }
+}
+
+// rho and LUT lookup for the chosen atoms: c = <d_k, x_v> in fp32 from the complex64 data.
+__global__ void k_dict_fix(const float2* __restrict__ x, const float2* __restrict__ atoms, const float* __restrict__ n2inv,
+                           const float* __restrict__ lut, int P, int L, int V, const int* __restrict__ best,
+                           int* __restrict__ index, float* __restrict__ pd, float* __restrict__ params) {
+  const int v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= V) return;
+  const int k = best[v];
+  const float2* d = atoms + (size_t)k * L;
+  float re = 0.f;
+  for (int l = 0; l < L; ++l) {   // Re(conj(d) x) = dr xr + di xi
+    const float2 a = __ldg(d + l), b = __ldg(x + (size_t)l * V + v);
+    re = fmaf(a.x, b.x, fmaf(a.y, b.y, re));
+  }
+  index[v] = k;
+  pd[v] = fmaxf(re * __ldg(n2inv + k), 0.f);
+  if (params)
+    for (int q = 0; q < P; ++q) params[(size_t)v * P + q] = __ldg(lut + (size_t)k * P + q);
+}
+
+}  // namespace dm
+}  // namespace mrf
