@@ -46,6 +46,7 @@ def parse():
     ap.add_argument("--cg-iters", type=int, default=None)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-toeplitz", action="store_true")
+    ap.add_argument("--no-match", action="store_true", help="skip the dictionary-matching (Phi_D) measurement")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target CPU work of the oracle sample")
     ap.add_argument("--batch-frames", type=int, default=0)
@@ -369,6 +370,36 @@ def run_ours(args):
         plan_t.close()
         del xbuf_t
 
+    # ---------------------------------------------------------------- dictionary matching Phi_D
+    match = None
+    if not args.no_match and world == 1 and cfg.C == 1:
+        import synth.dictionary as sdict
+        grid = sdict.t1t2_grid()
+        atoms = sdict.surrogate_dictionary(cfg.L, grid)
+        dic = binding.Dictionary(atoms, grid, device=local)
+        xm = xbuf.view(cfg.L, -1)                       # the CG solution, frame-major [L][V]
+        ms_match = time_op(lambda: dic.match(xm), 5)
+        dic.profile(True)
+        for _ in range(5):
+            dic.match(xm)
+        gemm_ms, gemm_n = dic.profile_query()
+        dic.profile(False)
+        gemm_ms /= max(gemm_n, 1)
+        Vm, Km = xm.shape[1], atoms.shape[0]
+        vpad, np_, kd = -(-Vm // 128) * 128, -(-2 * Km // 256) * 256, -(-2 * cfg.L // 64) * 64
+        gemm_fl = 2.0 * vpad * np_ * kd
+        peak_tc = float(peaks().get("bf16_tflops", 2250.0))
+        match = {"ms": ms_match, "voxels": Vm, "atoms": Km, "frames": cfg.L,
+                 "useful_tflops": 8.0 * Vm * Km * cfg.L / (ms_match * 1e-3) / 1e12,
+                 "roofline": {"bound": "tensor", "kernel": "k_dict_gemm", "achieved": gemm_fl / (gemm_ms * 1e-3) / 1e12,
+                              "peak": peak_tc, "unit": "TFLOP/s",
+                              "frac": gemm_fl / (gemm_ms * 1e-3) / 1e12 / peak_tc, "avg_launch_ms": gemm_ms,
+                              "peak_note": "measured bf16 dense burst (MEASURED_PEAKS.json); fp16 runs at the same rate"},
+                 "note": "mrf_dict_match on the CG solution: fp16 tcgen05 GEMM (pads to 128 voxels, 128 atoms, "
+                         "32 frames) + fused argmax, then exact fp32 PD; synthetic 3336-atom dictionary "
+                         "(PAPER.md:319 grid, surrogate fingerprints)"}
+        dic.close()
+
     # ---------------------------------------------------------------- e2e through the C-ABI, host buffers
     e2e = None
     if not args.no_e2e:
@@ -454,7 +485,7 @@ def run_ours(args):
         "hbm": {"algorithmic_bytes_per_step": hbm_bytes, "achieved_GBs": hbm_achieved, "peak_GBs": hbm_peak,
                 "frac": hbm_achieved / hbm_peak},
         "cufft_ref_ms_fft2_LC": cufft_ms,
-        "roofline": roofline, "roofline_AHA": roofline_aha, "toeplitz": toep, "kernel_share": share, "kernel_share_of_kernel_time": share_k, "gpu_launches": gpu_launches,
+        "roofline": roofline, "roofline_AHA": roofline_aha, "toeplitz": toep, "match": match, "kernel_share": share, "kernel_share_of_kernel_time": share_k, "gpu_launches": gpu_launches,
         "clocks": clk, "e2e": e2e, "cpu_baseline": cpu,
     }
     if rank == 0:

@@ -172,6 +172,12 @@ mrf_status mrf_dict_match(mrf_dict dict, const void* x, long long V, int* index,
 
 mrf_status mrf_dict_destroy(mrf_dict dict);
 
+/* enable != 0 brackets every subsequent tensor-core GEMM launch (k_dict_gemm) of mrf_dict_match
+ * with CUDA events on its stream (and resets); the query synchronises them and returns the
+ * summed milliseconds and the launch count. */
+mrf_status mrf_dict_profile(mrf_dict dict, int enable);
+mrf_status mrf_dict_profile_query(mrf_dict dict, double* gemm_ms, long long* launches);
+
 #ifdef __cplusplus
 }
 #endif

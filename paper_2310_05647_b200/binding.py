@@ -30,7 +30,7 @@ EXPORTED = [
     "mrf_plan_create", "mrf_forward", "mrf_adjoint", "mrf_normal", "mrf_dc_cg", "mrf_plan_destroy",
     "mrf_status_string", "mrf_last_error", "mrf_plan_device_bytes", "mrf_profile_enable",
     "mrf_profile_query", "mrf_nccl_get_unique_id", "mrf_nccl_comm_init", "mrf_nccl_comm_destroy",
-    "mrf_dict_create", "mrf_dict_match", "mrf_dict_destroy",
+    "mrf_dict_create", "mrf_dict_match", "mrf_dict_destroy", "mrf_dict_profile", "mrf_dict_profile_query",
 ]
 
 
@@ -81,6 +81,8 @@ def _load() -> ctypes.CDLL:
         "mrf_dict_create": ([vp, vp, ci, ci, ci, ci, ctypes.POINTER(vp)], ci),
         "mrf_dict_match": ([vp, vp, ctypes.c_longlong, vp, vp, vp, vp], ci),
         "mrf_dict_destroy": ([vp], ci),
+        "mrf_dict_profile": ([vp, ci], ci),
+        "mrf_dict_profile_query": ([vp, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_longlong)], ci),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)
@@ -309,6 +311,15 @@ class Dictionary:
         st = torch.cuda.current_stream(x.device).cuda_stream
         _check(lib.mrf_dict_match(self._h, _ptr(x), V, _ptr(index), _ptr(pd), _ptr(params), ctypes.c_void_p(st)))
         return index, pd, params
+
+    def profile(self, enable: bool = True):
+        _check(lib.mrf_dict_profile(self._h, int(enable)))
+
+    def profile_query(self):
+        """(milliseconds, launches) of the tensor-core GEMM since profile(True)."""
+        ms, n = ctypes.c_double(), ctypes.c_longlong()
+        _check(lib.mrf_dict_profile_query(self._h, ctypes.byref(ms), ctypes.byref(n)))
+        return ms.value, n.value
 
     def close(self):
         if getattr(self, "_h", None):

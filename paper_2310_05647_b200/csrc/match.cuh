@@ -258,23 +258,52 @@ __global__ void __launch_bounds__(256) k_dict_pack_x(const float2* __restrict__ 
   }
 }
 
-// rho and LUT lookup for the chosen atoms: c = <d_k, x_v> in fp32 from the complex64 data.
-__global__ void k_dict_fix(const float2* __restrict__ x, const float2* __restrict__ atoms, const float* __restrict__ n2inv,
-                           const float* __restrict__ lut, int P, int L, int V, const int* __restrict__ best,
-                           int* __restrict__ index, float* __restrict__ pd, float* __restrict__ params) {
-  const int v = blockIdx.x * blockDim.x + threadIdx.x;
-  if (v >= V) return;
-  const int k = best[v];
-  const float2* d = atoms + (size_t)k * L;
-  float re = 0.f;
-  for (int l = 0; l < L; ++l) {   // Re(conj(d) x) = dr xr + di xi
-    const float2 a = __ldg(d + l), b = __ldg(x + (size_t)l * V + v);
-    re = fmaf(a.x, b.x, fmaf(a.y, b.y, re));
+// rho and LUT lookup for the chosen atoms: Re<d_k, x_v> in fp32 from the complex64 data.  A
+// CTA takes 32 voxels; 32-frame tiles of x ([l][v], coalesced over v) and of the 32 chosen atoms
+// ([v][l], coalesced over l) are staged in shared memory; warp w sums voxels 4w..4w+3 with one
+// frame per lane and a final shuffle reduction.
+__global__ void __launch_bounds__(256) k_dict_fix(const float2* __restrict__ x, const float2* __restrict__ atoms,
+                                                  const float* __restrict__ n2inv, const float* __restrict__ lut, int P,
+                                                  int L, int V, const int* __restrict__ best, int* __restrict__ index,
+                                                  float* __restrict__ pd, float* __restrict__ params) {
+  __shared__ float2 xt[32][33];   // [l][v]
+  __shared__ float2 dt[32][33];   // [v][l]
+  __shared__ int ks[32];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int v0 = blockIdx.x * 32;
+  if (threadIdx.x < 32) ks[tx] = v0 + tx < V ? best[v0 + tx] : 0;
+  __syncthreads();
+  float acc[4] = {0.f, 0.f, 0.f, 0.f};
+  for (int l0 = 0; l0 < L; l0 += 32) {
+#pragma unroll
+    for (int i = ty; i < 32; i += 8) {
+      const int l = l0 + i, v = v0 + tx;
+      xt[i][tx] = (l < L && v < V) ? __ldg(x + (size_t)l * V + v) : make_float2(0.f, 0.f);
+      dt[i][tx] = (l0 + tx < L) ? __ldg(atoms + (size_t)ks[i] * L + l0 + tx) : make_float2(0.f, 0.f);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {   // Re(conj(d) x) = dr xr + di xi, frame l0 + tx
+      const int j = ty * 4 + q;
+      const float2 d = dt[j][tx], xv = xt[tx][j];
+      acc[q] = fmaf(d.x, xv.x, fmaf(d.y, xv.y, acc[q]));
+    }
+    __syncthreads();
   }
-  index[v] = k;
-  pd[v] = fmaxf(re * __ldg(n2inv + k), 0.f);
-  if (params)
-    for (int q = 0; q < P; ++q) params[(size_t)v * P + q] = __ldg(lut + (size_t)k * P + q);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    float r = acc[q];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
+    const int v = v0 + ty * 4 + q;
+    if (tx == 0 && v < V) {
+      const int k = ks[ty * 4 + q];
+      index[v] = k;
+      pd[v] = fmaxf(r * __ldg(n2inv + k), 0.f);
+    }
+    if (params && v < V)
+      for (int c = tx; c < P; c += 32) params[(size_t)v * P + c] = __ldg(lut + (size_t)ks[ty * 4 + q] * P + c);
+  }
 }
 
 }  // namespace dm

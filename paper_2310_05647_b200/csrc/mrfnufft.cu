@@ -1234,6 +1234,9 @@ struct mrf_dict_s {
   int* best = nullptr;           // [vcap]
   long long vcap = 0;
   CUtensorMap tmd;
+  bool prof = false;             // CUDA events around the tensor-core GEMM (mrf_dict_profile)
+  std::vector<cudaEvent_t> ev;   // pairs
+  size_t ev_used = 0;
 };
 
 static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
@@ -1363,16 +1366,51 @@ mrf_status mrf_dict_match(mrf_dict d, const void* x, long long V, int* index, fl
   const float2* xf = reinterpret_cast<const float2*>(x);
   dm::k_dict_pack_x<<<(unsigned)(vpad / 32), 256, 0, st>>>(xf, d->L, (int)V, d->KD, d->xp, d->xs);
   MRF_TRY(check_launch("k_dict_pack_x"));
+  if (d->prof) {
+    while (d->ev.size() < d->ev_used + 2) {
+      cudaEvent_t e;
+      CUDA_TRY(cudaEventCreate(&e));
+      d->ev.push_back(e);
+    }
+    CUDA_TRY(cudaEventRecord(d->ev[d->ev_used], st));
+  }
   dm::k_dict_gemm<<<(unsigned)(vpad / dm::BM), dm::THREADS, dm::SMEM, st>>>(tmx, d->tmd, d->w2, d->NP / dm::BN,
                                                                             d->KD / dm::BK, (int)V, d->best);
   MRF_TRY(check_launch("k_dict_gemm"));
-  dm::k_dict_fix<<<(unsigned)((V + 255) / 256), 256, 0, st>>>(xf, d->atoms, d->n2inv, d->lut, d->P, d->L, (int)V,
+  if (d->prof) {
+    CUDA_TRY(cudaEventRecord(d->ev[d->ev_used + 1], st));
+    d->ev_used += 2;
+  }
+  dm::k_dict_fix<<<(unsigned)((V + 31) / 32), 256, 0, st>>>(xf, d->atoms, d->n2inv, d->lut, d->P, d->L, (int)V,
                                                                d->best, index, pd, params);
   MRF_TRY(check_launch("k_dict_fix"));
   return MRF_OK;
 }
 
+mrf_status mrf_dict_profile(mrf_dict d, int enable) {
+  if (!d) return fail(MRF_EINVAL, "mrf_dict_profile: null dictionary");
+  d->prof = enable != 0;
+  d->ev_used = 0;
+  return MRF_OK;
+}
+
+mrf_status mrf_dict_profile_query(mrf_dict d, double* gemm_ms, long long* launches) {
+  if (!d || !gemm_ms || !launches) return fail(MRF_EINVAL, "mrf_dict_profile_query: invalid arguments");
+  double t = 0.0;
+  for (size_t i = 0; i + 1 < d->ev_used; i += 2) {
+    float ms = 0.f;
+    CUDA_TRY(cudaEventSynchronize(d->ev[i + 1]));
+    CUDA_TRY(cudaEventElapsedTime(&ms, d->ev[i], d->ev[i + 1]));
+    t += ms;
+  }
+  *gemm_ms = t;
+  *launches = (long long)(d->ev_used / 2);
+  return MRF_OK;
+}
+
 mrf_status mrf_dict_destroy(mrf_dict d) {
+  if (d)
+    for (cudaEvent_t e : d->ev) cudaEventDestroy(e);
   dict_free(d);
   return MRF_OK;
 }
