@@ -121,7 +121,7 @@ def ncu_traffic(kernel_class):
     (profiles/ncu_traffic.json, written by tools/ncu_traffic.py), or None."""
     try:
         t = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
-        return t["kernels"][kernel_class]
+        return dict(t["kernels"][kernel_class], source=t.get("source", "profiles/ncu_traffic.json"))
     except (OSError, KeyError, ValueError):
         return None
 

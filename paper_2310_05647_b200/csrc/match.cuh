@@ -113,7 +113,7 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
 __global__ void __launch_bounds__(THREADS, 1)
 k_dict_gemm(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmd,
             const float* __restrict__ w2, int n_tiles, int kblocks, int V, int* __restrict__ best) {
-  extern __shared__ __align__(1024) unsigned char dm_raw[];
+  extern __shared__ __align__(128) unsigned char dm_raw[];   // aligned to 1024 below (SMEM has the slack)
   unsigned char* base = (unsigned char*)(((uintptr_t)dm_raw + 1023) & ~(uintptr_t)1023);
   unsigned char* sA = base;
   unsigned char* sB = base + STAGES * A_BYTES;
