@@ -66,6 +66,11 @@ typedef enum {
  * the exact (NUDFT) normal operator up to fp32 rounding -- it differs from the gridding A^H(A x) by
  * the NUFFT approximation error (~1e-5).  forward/adjoint are unchanged.  Costs R*(2N)^2*4 bytes. */
 #define MRF_NORMAL_TOEPLITZ 2u
+/* Density compensation (reading 23): the plan
+ * computes per-sample weights w[r][j] by 20 Pipe-Menon iterations w <- w / (Phi Phi^T w) on the
+ * sigma*N grid with the gridding taps (float64, at plan creation) for mrf_adjoint_dcf, the
+ * density-compensated initialisation X^0 = A^H (w . b) ("X^0 = A* b"). */
+#define MRF_DCF 4u
 
 typedef struct {
   int N;                        /* square image side, even; G = sigma*N must be a supported size */
@@ -100,6 +105,12 @@ mrf_status mrf_adjoint(mrf_plan plan, const void* y, void* x, void* stream);
 /* out = A^H A x + mu x  (the normal operator inside A*(A X^n - b), Eq. (15)).
  * out must not alias x; mu >= 0. */
 mrf_status mrf_normal(mrf_plan plan, const void* x, void* out, float mu, void* stream);
+
+/* x = A^H (w . y): the adjoint of the density-compensated k-space (plan created with MRF_DCF;
+ * else MRF_EINVAL).  Layouts, pointers and errors as mrf_adjoint. */
+mrf_status mrf_adjoint_dcf(mrf_plan plan, const void* y, void* x, void* stream);
+/* Copies the plan's weights, HOST float [R][M], into w (MRF_DCF plans; else MRF_EINVAL). */
+mrf_status mrf_dcf_weights(mrf_plan plan, float* w);
 
 typedef struct {
   int iters;               /* CG iterations performed                                           */

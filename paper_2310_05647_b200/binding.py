@@ -22,6 +22,7 @@ LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libmrfnufft
 MRF_DEAPOD_ANALYTIC = 0
 MRF_DEAPOD_DISCRETE = 1
 MRF_NORMAL_TOEPLITZ = 2
+MRF_DCF = 4
 KERNEL_CLASSES = {"fwd_rows": 0, "fwd_cols": 1, "adj_cols": 2, "adj_rows": 3, "cg_vec": 4, "other": 5}
 STATUS = {0: "MRF_OK", 1: "MRF_EINVAL", 2: "MRF_ENOMEM", 3: "MRF_ECUDA", 4: "MRF_ENCCL",
           5: "MRF_EUNSUPPORTED", 6: "MRF_ENUMERIC"}
@@ -30,7 +31,7 @@ EXPORTED = [
     "mrf_plan_create", "mrf_forward", "mrf_adjoint", "mrf_normal", "mrf_dc_cg", "mrf_plan_destroy",
     "mrf_status_string", "mrf_last_error", "mrf_plan_device_bytes", "mrf_profile_enable",
     "mrf_profile_query", "mrf_nccl_get_unique_id", "mrf_nccl_comm_init", "mrf_nccl_comm_destroy",
-    "mrf_dict_create", "mrf_dict_match", "mrf_dict_destroy", "mrf_dict_profile", "mrf_dict_profile_query",
+    "mrf_adjoint_dcf", "mrf_dcf_weights", "mrf_dict_create", "mrf_dict_match", "mrf_dict_destroy", "mrf_dict_profile", "mrf_dict_profile_query",
 ]
 
 
@@ -67,6 +68,8 @@ def _load() -> ctypes.CDLL:
         "mrf_plan_create": ([ctypes.POINTER(PlanDesc), ctypes.POINTER(vp)], ci),
         "mrf_forward": ([vp, vp, vp, vp], ci),
         "mrf_adjoint": ([vp, vp, vp, vp], ci),
+        "mrf_adjoint_dcf": ([vp, vp, vp, vp], ci),
+        "mrf_dcf_weights": ([vp, vp], ci),
         "mrf_normal": ([vp, vp, vp, cf, vp], ci),
         "mrf_dc_cg": ([vp, vp, vp, cf, ci, cf, vp, ctypes.POINTER(CGInfo), vp], ci),
         "mrf_plan_destroy": ([vp], ci),
@@ -120,7 +123,8 @@ class Plan:
 
     def __init__(self, N: int, traj, L: int, *, coils=None, W: int = 6, sigma: float = 2.0,
                  frame_interleaf=None, frame_offset: int = 0, deapod: str = "analytic", normal: str = "gridding",
-                 device: Optional[int] = None, nccl_comm: Optional[int] = None, batch_frames: int = 0):
+                 device: Optional[int] = None, nccl_comm: Optional[int] = None, batch_frames: int = 0,
+                 dcf: bool = False):
         traj_np = np.ascontiguousarray(np.asarray(traj, dtype=np.float32))
         if traj_np.ndim != 3 or traj_np.shape[2] != 2:
             raise ValueError("traj must be [R][M][2] float32")
@@ -148,7 +152,7 @@ class Plan:
         d.coils = None if coils_np is None else coils_np.ctypes.data
         d.W, d.sigma = self.W, self.sigma
         d.flags = {"analytic": MRF_DEAPOD_ANALYTIC, "discrete": MRF_DEAPOD_DISCRETE}[deapod] | \
-            {"gridding": 0, "toeplitz": MRF_NORMAL_TOEPLITZ}[normal]
+            {"gridding": 0, "toeplitz": MRF_NORMAL_TOEPLITZ}[normal] | (MRF_DCF if dcf else 0)
         d.device = self.device
         d.stream = None
         d.nccl_comm = nccl_comm
@@ -194,6 +198,19 @@ class Plan:
         x = self._like(y, self.x_shape) if x is None else _as_c64(x, self.x_shape, "x")
         _check(lib.mrf_adjoint(self._h, _ptr(y), _ptr(x), self._stream(x, y)))
         return x
+
+    def adjoint_dcf(self, y, x=None):
+        """x = A^H (w . y), w the plan's Pipe-Menon density compensation (plan made with dcf=True)."""
+        y = _as_c64(y, self.y_shape, "y")
+        x = self._like(y, self.x_shape) if x is None else _as_c64(x, self.x_shape, "x")
+        _check(lib.mrf_adjoint_dcf(self._h, _ptr(y), _ptr(x), self._stream(x, y)))
+        return x
+
+    def dcf_weights(self) -> np.ndarray:
+        """The plan's density compensation weights, float32 [R][M]."""
+        w = np.empty((self.R, self.M), dtype=np.float32)
+        _check(lib.mrf_dcf_weights(self._h, w.ctypes.data_as(ctypes.c_void_p)))
+        return w
 
     def normal(self, x, mu: float = 0.0, out=None):
         """out = A^H A x + mu x  (A*(A X))."""

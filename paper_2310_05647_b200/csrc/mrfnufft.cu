@@ -109,6 +109,9 @@ struct mrf_plan_s {
   float2* Hs[kMaxLanes] = {};      // [bf*C][N][G] half grid per lane
   float2* Has[kMaxLanes] = {};     // Toeplitz plans: the adjoint-side half grid per lane
   float* psf = nullptr;            // Toeplitz plans: [R][S][G][16] real PSF spectra
+  float* dcf = nullptr;            // MRF_DCF plans: [R][M] Pipe-Menon density compensation weights
+  std::vector<float> dcf_host;     // the same, host copy (mrf_dcf_weights)
+  float2* ydcf = nullptr;          // [L][C][M] weighted k-space (allocated on first mrf_adjoint_dcf)
   float* ones = nullptr;           // [N] of 1.0 (the Toeplitz path has no deapodisation)
   float2* ybufs[kMaxLanes] = {};   // [bf*C][M] per lane
   float2* r = nullptr;       // CG vectors [L][N][N]
@@ -240,6 +243,8 @@ static void free_plan(mrf_plan_s* pl) {
     cudaFree(pl->dbgbuf);
   }
   if (pl->psf) cudaFree(pl->psf);
+  if (pl->dcf) cudaFree(pl->dcf);
+  if (pl->ydcf) cudaFree(pl->ydcf);
   if (pl->ones) cudaFree(pl->ones);
   for (int i = 0; i < kMaxLanes; ++i) {
     if (pl->Has[i]) cudaFree(pl->Has[i]);
@@ -296,6 +301,54 @@ static mrf_status check_launch(const char* what) {
 }
 
 // Opt-in shared memory sizes and occupancy of the persistent kernels (once per plan).
+// Density compensation (reading 23): Pipe-Menon fixed-point
+// iteration w <- w / (Phi Phi^T w) on the sigma*N grid with the gridding taps, float64, per
+// interleaf at plan time (a dense G x G accumulator: spread, then interpolate back).
+static constexpr int kDcfIters = 20;
+static void pipe_menon(const KB& kb, int G, int W, const float* traj, int M, double* w) {
+  std::vector<double> tp((size_t)M * 2 * W), grid((size_t)G * G);
+  std::vector<int> m0((size_t)M * 2);
+  for (int j = 0; j < M; ++j) {
+    kb_taps(kb, G, W, traj[2 * j], traj[2 * j + 1], &tp[(size_t)j * 2 * W]);
+    for (int ax = 0; ax < 2; ++ax) {
+      const long long m = (long long)std::floor((double)G * (double)traj[2 * j + ax] - 0.5 * W) + 1;
+      m0[2 * j + ax] = (int)(((m % G) + G) % G);
+    }
+  }
+  for (int j = 0; j < M; ++j) w[j] = 1.0;
+  for (int it = 0; it < kDcfIters; ++it) {
+    std::fill(grid.begin(), grid.end(), 0.0);
+    for (int j = 0; j < M; ++j) {
+      const double* t = &tp[(size_t)j * 2 * W];
+      for (int ty = 0; ty < W; ++ty) {
+        double* row = &grid[(size_t)((m0[2 * j + 1] + ty) % G) * G];
+        for (int tx = 0; tx < W; ++tx) row[(m0[2 * j] + tx) % G] += t[W + ty] * t[tx] * w[j];
+      }
+    }
+    for (int j = 0; j < M; ++j) {
+      const double* t = &tp[(size_t)j * 2 * W];
+      double acc = 0.0;
+      for (int ty = 0; ty < W; ++ty) {
+        const double* row = &grid[(size_t)((m0[2 * j + 1] + ty) % G) * G];
+        for (int tx = 0; tx < W; ++tx) acc += t[W + ty] * t[tx] * row[(m0[2 * j] + tx) % G];
+      }
+      w[j] = acc > 0.0 ? w[j] / acc : 0.0;
+    }
+  }
+}
+
+// y_w[l][c][j] = dcf[interleaf(l)][j] * y[l][c][j]
+__global__ void k_dcf_scale(float2* __restrict__ yw, const float2* __restrict__ y, const float* __restrict__ dcf,
+                            const int* __restrict__ fil, int L, int C, int M) {
+  const size_t n = (size_t)L * C * M;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    const int l = (int)(i / ((size_t)C * M)), j = (int)(i % M);
+    const float w = __ldg(dcf + (size_t)__ldg(fil + l) * M + j);
+    const float2 v = y[i];
+    yw[i] = make_float2(w * v.x, w * v.y);
+  }
+}
+
 template <int G>
 static mrf_status setup_kernels(mrf_plan_s* pl) {
   const int ncol = cols_threads<G>();
@@ -784,7 +837,7 @@ mrf_status mrf_plan_create(const mrf_plan_desc* d, mrf_plan* out) {
   if (d->W < 2 || d->W > 16) return fail(MRF_EINVAL, "W must be in [2, 16]");
   if (!(d->sigma > 0.f) || !std::isfinite(d->sigma)) return fail(MRF_EINVAL, "sigma must be positive");
   if (d->batch_frames < 0) return fail(MRF_EINVAL, "batch_frames < 0");
-  if (d->flags & ~3u) return fail(MRF_EINVAL, "unknown flags");
+  if (d->flags & ~7u) return fail(MRF_EINVAL, "unknown flags");
   if ((double)d->sigma != 2.0) return fail(MRF_EUNSUPPORTED, "only sigma = 2 is supported");
   const double Gd = (double)d->sigma * d->N;
   const int G = (int)std::lround(Gd);
@@ -1063,6 +1116,16 @@ mrf_status mrf_plan_create(const mrf_plan_desc* d, mrf_plan* out) {
   if (!ce) ce = up(pl->atab, atab.data(), atab.size() * sizeof(int2));
   if (!ce) ce = up(pl->fil, fil.data(), fil.size() * sizeof(int));
   if (!ce && pl->coils) ce = up(pl->coils, d->coils, (size_t)C * N * N * sizeof(float2));
+  if (!ce && (pl->flags & MRF_DCF)) {
+    std::vector<double> wr((size_t)M);
+    pl->dcf_host.resize((size_t)R * M);
+    for (int r = 0; r < R; ++r) {
+      pipe_menon(kb, G, W, d->traj + (size_t)r * M * 2, M, wr.data());
+      for (int j = 0; j < M; ++j) pl->dcf_host[(size_t)r * M + j] = (float)wr[j];
+    }
+    if ((s = dev_alloc(pl, &pl->dcf, (size_t)R * M))) return bail(s);
+    ce = up(pl->dcf, pl->dcf_host.data(), pl->dcf_host.size() * sizeof(float));
+  }
   if (!ce) ce = cudaMemsetAsync(pl->sc, 0, sizeof(CGScalars), st);
   if (!ce) ce = cudaStreamSynchronize(st);
   if (ce) {
@@ -1112,6 +1175,41 @@ mrf_status mrf_adjoint(mrf_plan pl, const void* y, void* x, void* stream) {
   MRF_TRY(do_adjoint(pl, pl->stg_y, pl->stg_x, st));
   CUDA_TRY(cudaMemcpyAsync(x, pl->stg_x, bx, cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaStreamSynchronize(st));
+  return MRF_OK;
+}
+
+mrf_status mrf_adjoint_dcf(mrf_plan pl, const void* y, void* x, void* stream) {
+  if (!pl || !x || !y) return fail(MRF_EINVAL, "null plan/x/y");
+  if (!pl->dcf) return fail(MRF_EINVAL, "the plan was created without MRF_DCF");
+  DeviceGuard guard(pl->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  bool host = false;
+  MRF_TRY(classify(pl, {x, y}, &host));
+  const size_t ny = (size_t)pl->L * pl->C * pl->M;
+  if (!pl->ydcf) MRF_TRY(dev_alloc(pl, &pl->ydcf, ny));
+  const float2* src = (const float2*)y;
+  if (host) {
+    MRF_TRY(ensure_staging(pl, false));
+    CUDA_TRY(cudaMemcpyAsync(pl->stg_y, y, ny * sizeof(float2), cudaMemcpyHostToDevice, st));
+    src = pl->stg_y;
+  }
+  {
+    ProfScope ps(pl, MRF_K_OTHER, st);
+    k_dcf_scale<<<(unsigned)std::min<size_t>((ny + 255) / 256, 4096), 256, 0, st>>>(pl->ydcf, src, pl->dcf, pl->fil,
+                                                                                     pl->L, pl->C, pl->M);
+    MRF_TRY(check_launch("k_dcf_scale"));
+  }
+  if (!host) return do_adjoint(pl, pl->ydcf, (float2*)x, st);
+  MRF_TRY(do_adjoint(pl, pl->ydcf, pl->stg_x, st));
+  CUDA_TRY(cudaMemcpyAsync(x, pl->stg_x, (size_t)pl->L * pl->N * pl->N * sizeof(float2), cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  return MRF_OK;
+}
+
+mrf_status mrf_dcf_weights(mrf_plan pl, float* w) {
+  if (!pl || !w) return fail(MRF_EINVAL, "null plan/w");
+  if (pl->dcf_host.empty()) return fail(MRF_EINVAL, "the plan was created without MRF_DCF");
+  std::memcpy(w, pl->dcf_host.data(), pl->dcf_host.size() * sizeof(float));
   return MRF_OK;
 }
 

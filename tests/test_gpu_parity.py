@@ -423,3 +423,29 @@ def test_toeplitz_sizes_and_batches(mrf, N, M, L, bf):
     got = host(pl.normal(dev(x), mu=0.02))
     ref = _nudft_normal(x, traj, None, fil, 0.02)
     assert rel(got, ref) <= OP_TOL
+
+
+# ------------------------------------------------------------------ density compensation (f4)
+def test_dcf_weights_and_weighted_adjoint(mrf):
+    from oracle import dcf as odcf
+    binding = mrf
+    for name, over in (("pr1", {}), ("cfg2", {"L": 6})):
+        cfg = synth.get_config(name, **over)
+        traj = synth.spiral_trajectory(cfg.M, cfg.R, cfg.turns, cfg.p)
+        pl = binding.Plan(cfg.N, traj, cfg.L, W=cfg.W, dcf=True)
+        w = pl.dcf_weights()
+        w_ref = odcf.dcf(traj.astype(np.float64), cfg.N, cfg.W, n_iter=20)
+        assert np.max(np.abs(w - w_ref) / w_ref) < 1e-5
+        y = synth.random_kspace(1, cfg.M, range(cfg.L), cfg.seed)
+        il = np.arange(cfg.L) % cfg.R
+        yw = y.astype(np.complex128) * w_ref[il][:, None, :]
+        x_ref = on.adjoint(yw, traj, None, cfg.N, cfg.W)
+        x = pl.adjoint_dcf(torch.from_numpy(y.astype(np.complex64)).cuda())
+        assert rel(x.cpu().numpy(), x_ref) <= OP_TOL
+        xh = pl.adjoint_dcf(torch.from_numpy(y.astype(np.complex64)))          # host-pointer path
+        assert rel(xh.numpy(), x_ref) <= OP_TOL
+        pl.close()
+    pl = binding.Plan(32, synth.spiral_trajectory(256, 8, 4, 1.5), 2)
+    with pytest.raises(binding.MrfError):
+        pl.adjoint_dcf(torch.zeros(pl.y_shape, dtype=torch.complex64, device="cuda"))
+    pl.close()
