@@ -116,6 +116,8 @@ typedef struct {
   int iters;               /* CG iterations performed                                           */
   double rel_resid;        /* sqrt(rho_last / rho_0), rho = <r, r> global over all ranks        */
   double* history;         /* nullable HOST array of length n_iter+1: history[k] = sqrt(rho_k)  */
+  double* alpha;           /* nullable HOST array of length n_iter: the step lengths alpha_k    */
+  double* beta;            /* nullable HOST array of length n_iter: beta_k = rho_{k+1} / rho_k  */
 } mrf_cg_info;
 
 /* Solves (A^H A + mu I) x = A^H y + mu z by CG from x (in: x0, out: solution), inner products

@@ -55,7 +55,8 @@ class PlanDesc(ctypes.Structure):
 
 class CGInfo(ctypes.Structure):
     _fields_ = [("iters", ctypes.c_int), ("rel_resid", ctypes.c_double),
-                ("history", ctypes.POINTER(ctypes.c_double))]
+                ("history", ctypes.POINTER(ctypes.c_double)), ("alpha", ctypes.POINTER(ctypes.c_double)),
+                ("beta", ctypes.POINTER(ctypes.c_double))]
 
 
 def _load() -> ctypes.CDLL:
@@ -235,10 +236,15 @@ class Plan:
         if z is not None:
             z = _as_c64(z, self.x_shape, "z")
         hist = (ctypes.c_double * (n_iter + 1))()
-        info = CGInfo(0, 0.0, ctypes.cast(hist, ctypes.POINTER(ctypes.c_double)))
+        ha = (ctypes.c_double * max(n_iter, 1))()
+        hb = (ctypes.c_double * max(n_iter, 1))()
+        dp = lambda a: ctypes.cast(a, ctypes.POINTER(ctypes.c_double))
+        info = CGInfo(0, 0.0, dp(hist), dp(ha), dp(hb))
         _check(lib.mrf_dc_cg(self._h, _ptr(y), _ptr(z), ctypes.c_float(mu), int(n_iter), ctypes.c_float(tol),
                              _ptr(x), ctypes.byref(info), self._stream(x, y, z)))
-        return x, {"iters": info.iters, "rel_resid": info.rel_resid, "history": list(hist)[: info.iters + 1]}
+        it = info.iters
+        return x, {"iters": it, "rel_resid": info.rel_resid, "history": list(hist)[: it + 1],
+                   "alpha": list(ha)[:it], "beta": list(hb)[:it]}
 
     # ------------------------------------------------------------------ profiling
     def profile(self, enable: bool = True):

@@ -117,8 +117,8 @@ __global__ void k_cg_start(CGScalars* sc, double* hist) {
   hist[0] = sqrt(sc->rr.x);
 }
 
-// alpha = rho / Re<p,q>  (breakdown => alpha = 0, flagged)
-__global__ void k_cg_alpha(CGScalars* sc) {
+// alpha = rho / Re<p,q>  (breakdown => alpha = 0, flagged); ha[k] = alpha
+__global__ void k_cg_alpha(CGScalars* sc, double* ha, int k) {
   const double pq = sc->pq.x;
   if (sc->rho0 == 0.0) {
     sc->alpha = 0.0;
@@ -128,6 +128,7 @@ __global__ void k_cg_alpha(CGScalars* sc) {
   } else {
     sc->alpha = sc->rho / pq;
   }
+  ha[k] = sc->alpha;
 }
 
 // r -= alpha q ; partial <r,r>   (x is advanced lazily: x += alpha p in the next row pass)
@@ -188,10 +189,11 @@ __global__ void __launch_bounds__(kVecThreads) k_cg_px(float2* __restrict__ x, f
   })
 }
 
-// beta = rho' / rho ; rho = rho' ; hist[k+1]
-__global__ void k_cg_beta(CGScalars* sc, double* hist, int k) {
+// beta = rho' / rho ; rho = rho' ; hist[k+1], hb[k] = beta
+__global__ void k_cg_beta(CGScalars* sc, double* hist, double* hb, int k) {
   const double rn = sc->rr.x;
   sc->beta = sc->rho > 0.0 ? rn / sc->rho : 0.0;
+  hb[k] = sc->beta;
   sc->rho = rn;
   sc->iters = k + 1;
   hist[k + 1] = sqrt(rn);

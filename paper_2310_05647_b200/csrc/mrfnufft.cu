@@ -642,13 +642,15 @@ static mrf_status run_cg(mrf_plan_s* pl, const float2* y, const float2* z, float
                          float2* x, mrf_cg_info* info, cudaStream_t st) {
   const size_t n = (size_t)pl->L * pl->N * pl->N;
   const int nblk = vec_blocks(n);
-  if (n_iter + 1 > pl->hist_cap) {
+  if (n_iter + 1 > pl->hist_cap) {   // [sqrt(rho_k), k <= n][alpha_k][beta_k]
     if (pl->hist) cudaFree(pl->hist);
     pl->hist = nullptr;
     pl->hist_cap = 0;
-    MRF_TRY(dev_alloc(pl, &pl->hist, (size_t)n_iter + 1));
+    MRF_TRY(dev_alloc(pl, &pl->hist, 3 * ((size_t)n_iter + 1)));
     pl->hist_cap = n_iter + 1;
   }
+  double* hist_a = pl->hist + pl->hist_cap;
+  double* hist_b = pl->hist + 2 * pl->hist_cap;
   // rhs = A^H y + mu z  -> r
   MRF_TRY(do_adjoint(pl, y, pl->r, st));
   if (z && mu != 0.f) {
@@ -688,7 +690,7 @@ static mrf_status run_cg(mrf_plan_s* pl, const float2* y, const float2* z, float
     MRF_TRY(allreduce2(pl, &pl->sc->pq, st));
     {
       ProfScope ps(pl, MRF_K_CG_VEC, st);
-      k_cg_alpha<<<1, 1, 0, st>>>(pl->sc);
+      k_cg_alpha<<<1, 1, 0, st>>>(pl->sc, hist_a, k);
       MRF_TRY(vec_launch_check("k_cg_alpha"));
     }
     {
@@ -700,7 +702,7 @@ static mrf_status run_cg(mrf_plan_s* pl, const float2* y, const float2* z, float
     MRF_TRY(allreduce2(pl, &pl->sc->rr, st));
     {
       ProfScope ps(pl, MRF_K_CG_VEC, st);
-      k_cg_beta<<<1, 1, 0, st>>>(pl->sc, pl->hist, k);
+      k_cg_beta<<<1, 1, 0, st>>>(pl->sc, pl->hist, hist_b, k);
       MRF_TRY(vec_launch_check("k_cg_beta"));
     }
     if (tol > 0.f) {
@@ -717,8 +719,8 @@ static mrf_status run_cg(mrf_plan_s* pl, const float2* y, const float2* z, float
   }
   CGScalars hs;
   CUDA_TRY(cudaMemcpyAsync(&hs, pl->sc, sizeof(CGScalars), cudaMemcpyDeviceToHost, st));
-  std::vector<double> hh((size_t)n_iter + 1, 0.0);
-  CUDA_TRY(cudaMemcpyAsync(hh.data(), pl->hist, sizeof(double) * (n_iter + 1), cudaMemcpyDeviceToHost, st));
+  std::vector<double> hh(3 * (size_t)pl->hist_cap, 0.0);
+  CUDA_TRY(cudaMemcpyAsync(hh.data(), pl->hist, sizeof(double) * hh.size(), cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaStreamSynchronize(st));
   if (hs.rho0 == 0.0) iters_done = 0;
   if (info) {
@@ -726,6 +728,10 @@ static mrf_status run_cg(mrf_plan_s* pl, const float2* y, const float2* z, float
     info->rel_resid = hs.rho0 > 0.0 ? std::sqrt(hs.rho / hs.rho0) : 0.0;
     if (info->history) {
       for (int i = 0; i <= n_iter; ++i) info->history[i] = i <= iters_done ? hh[i] : 0.0;
+    }
+    for (int i = 0; i < n_iter; ++i) {
+      if (info->alpha) info->alpha[i] = i < iters_done ? hh[pl->hist_cap + i] : 0.0;
+      if (info->beta) info->beta[i] = i < iters_done ? hh[2 * pl->hist_cap + i] : 0.0;
     }
   }
   if (hs.breakdown) return fail(MRF_ENUMERIC, "CG breakdown: Re<p, (A^H A + mu I) p> <= 0 or non-finite");
