@@ -11,7 +11,7 @@
 // keep the fp16 operands in [-1, 1]; the argmax uses |c~|^2 * (m_k / ||d_k||)^2 (s_v is common
 // to a voxel's row).  rho is recomputed exactly in fp32 for the chosen atom (k_dict_fix).
 //
-// k_dict_gemm: one CTA per 128 voxels, 256 threads in roles: warp 0 = TMA producer (128-byte
+// k_dict_gemm: persistent CTAs over (128-voxel, 128-atom) units, 256 threads in roles: warp 0 = TMA producer (128-byte
 // swizzled tiles, 4-stage mbarrier ring), warp 1 = TMEM allocator + single-thread tcgen05.mma
 // issuer (M = 128, N = 256, K = 16 per instruction, fp32 accumulators in TMEM, two 256-column
 // accumulator buffers so the epilogue of one atom tile overlaps the MMAs of the next), warps
@@ -107,12 +107,14 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
-// best[v] = argmax_k over the atom tiles.  w2[k] = (m_k / ||d_k||)^2 (0 for padding atoms).
-// X~ [Vpad][KD] and D~ [NP][KD] fp16 are read through the tensor maps; n_tiles = NP / BN;
-// kblocks = KD / BK.
+// best[v] = max over the atom tiles of (score bits << 32 | ~atom), zeroed by the caller;
+// w2[k] = (m_k / ||d_k||)^2 (0 for padding atoms).  X~ [Vpad][KD] and D~ [NP][KD] fp16 are read
+// through the tensor maps; m_tiles = Vpad / BM, n_tiles = NP / BN, kblocks = KD / BK.  The
+// grid is persistent (one CTA per SM), so the m_tiles x n_tiles units quantise to < 1 %.
 __global__ void __launch_bounds__(THREADS, 1)
 k_dict_gemm(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmd,
-            const float* __restrict__ w2, int n_tiles, int kblocks, int V, int* __restrict__ best) {
+            const float* __restrict__ w2, int m_tiles, int n_tiles, int kblocks, int V,
+            unsigned long long* __restrict__ best) {
   extern __shared__ __align__(128) unsigned char dm_raw[];   // aligned to 1024 below (SMEM has the slack)
   unsigned char* base = (unsigned char*)(((uintptr_t)dm_raw + 1023) & ~(uintptr_t)1023);
   unsigned char* sA = base;
@@ -123,7 +125,8 @@ k_dict_gemm(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUt
   uint64_t* tempty = tfull + 2;
   uint32_t* tbase = reinterpret_cast<uint32_t*>(tempty + 2);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int m0 = blockIdx.x * BM;
+  // persistent: work unit u = (m tile u / n_tiles, atom tile u % n_tiles), strided over the grid
+  const int units = m_tiles * n_tiles;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -148,7 +151,8 @@ k_dict_gemm(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUt
   if (warp == 0 && lane == 0) {
     // ---- TMA producer
     int it = 0;
-    for (int nt = 0; nt < n_tiles; ++nt)
+    for (int u = blockIdx.x; u < units; u += gridDim.x) {
+      const int m0 = (u / n_tiles) * BM, nt = u % n_tiles;
       for (int kb = 0; kb < kblocks; ++kb, ++it) {
         const int s = it % STAGES;
         bar_wait(&empty[s], ((it / STAGES) & 1) ^ 1);
@@ -156,11 +160,12 @@ k_dict_gemm(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUt
         tma_load_2d(sA + s * A_BYTES, &tmx, kb * BK, m0, &full[s]);
         tma_load_2d(sB + s * B_BYTES, &tmd, kb * BK, nt * BN, &full[s]);
       }
+    }
   } else if (warp == 1 && lane == 0) {
     // ---- MMA issuer
-    int it = 0;
-    for (int nt = 0; nt < n_tiles; ++nt) {
-      const int acc = nt & 1, use = nt >> 1;
+    int it = 0, j = 0;
+    for (int u = blockIdx.x; u < units; u += gridDim.x, ++j) {
+      const int acc = j & 1, use = j >> 1;
       bar_wait(&tempty[acc], (use & 1) ^ 1);
       tc_fence_after();
       const uint32_t td = tmem + (uint32_t)(acc * BN);
@@ -177,34 +182,41 @@ k_dict_gemm(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUt
       mma_commit(&tfull[acc]);   // accumulator complete
     }
   } else if (warp >= 4) {
-    // ---- epilogue: thread = TMEM lane = voxel m0 + row
+    // ---- epilogue: thread = TMEM lane = voxel row of the unit's m tile.  The best atom of the
+    // unit's 128 is merged across units with one 64-bit atomicMax per voxel on
+    // (score bits << 32 | ~atom): scores are >= 0, so their bits order as the values, and on
+    // equal scores the lower atom index wins (order independent, deterministic).
     const int row = (warp - 4) * 32 + lane;
     const uint32_t lane_addr = (uint32_t)((warp - 4) * 32) << 16;
-    float bsc = -1.f;
-    int bk = 0;
-    for (int nt = 0; nt < n_tiles; ++nt) {
-      const int acc = nt & 1, use = nt >> 1;
+    int j = 0;
+    for (int u = blockIdx.x; u < units; u += gridDim.x, ++j) {
+      const int m0 = (u / n_tiles) * BM, nt = u % n_tiles;
+      const int acc = j & 1, use = j >> 1;
       bar_wait(&tfull[acc], use & 1);
       __syncwarp();   // tcgen05.ld is .sync.aligned
       tc_fence_after();
+      float bsc = -1.f;
+      int bk = 0;
 #pragma unroll 1
       for (int ch = 0; ch < BN / 32; ++ch) {
         float v[32];
         tmem_ld32(tmem + lane_addr + (uint32_t)(acc * BN + ch * 32), v);
         const int k0 = nt * (BN / 2) + ch * 16;
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          const float sc = (v[2 * j] * v[2 * j] + v[2 * j + 1] * v[2 * j + 1]) * __ldg(w2 + k0 + j);
+        for (int q = 0; q < 16; ++q) {
+          const float sc = (v[2 * q] * v[2 * q] + v[2 * q + 1] * v[2 * q + 1]) * __ldg(w2 + k0 + q);
           if (sc > bsc) {   // strict: equal scores keep the lowest atom index
             bsc = sc;
-            bk = k0 + j;
+            bk = k0 + q;
           }
         }
       }
       tc_fence_before();
       bar_arrive(&tempty[acc]);
+      if (m0 + row < V)
+        atomicMax(best + m0 + row,
+                  ((unsigned long long)__float_as_uint(fmaxf(bsc, 0.f)) << 32) | (0xFFFFFFFFu - (uint32_t)bk));
     }
-    if (m0 + row < V) best[m0 + row] = bk;
   }
   tc_fence_before();
   __syncthreads();
@@ -264,14 +276,15 @@ __global__ void __launch_bounds__(256) k_dict_pack_x(const float2* __restrict__ 
 // frame per lane and a final shuffle reduction.
 __global__ void __launch_bounds__(256) k_dict_fix(const float2* __restrict__ x, const float2* __restrict__ atoms,
                                                   const float* __restrict__ n2inv, const float* __restrict__ lut, int P,
-                                                  int L, int V, const int* __restrict__ best, int* __restrict__ index,
+                                                  int L, int V, const unsigned long long* __restrict__ best,
+                                                  int* __restrict__ index,
                                                   float* __restrict__ pd, float* __restrict__ params) {
   __shared__ float2 xt[32][33];   // [l][v]
   __shared__ float2 dt[32][33];   // [v][l]
   __shared__ int ks[32];
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   const int v0 = blockIdx.x * 32;
-  if (threadIdx.x < 32) ks[tx] = v0 + tx < V ? best[v0 + tx] : 0;
+  if (threadIdx.x < 32) ks[tx] = v0 + tx < V ? (int)(0xFFFFFFFFu - (uint32_t)(best[v0 + tx] & 0xFFFFFFFFull)) : 0;
   __syncthreads();
   float acc[4] = {0.f, 0.f, 0.f, 0.f};
   for (int l0 = 0; l0 < L; l0 += 32) {

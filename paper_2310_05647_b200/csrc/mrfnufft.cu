@@ -1335,7 +1335,7 @@ struct mrf_dict_s {
   float* lut = nullptr;          // [K][P]
   __half* xp = nullptr;          // workspace [vcap][KD]
   float* xs = nullptr;           // [vcap] per-voxel scale
-  int* best = nullptr;           // [vcap]
+  unsigned long long* best = nullptr;   // [vcap] packed (score, ~atom) running maxima
   long long vcap = 0;
   CUtensorMap tmd;
   bool prof = false;             // CUDA events around the tensor-core GEMM (mrf_dict_profile)
@@ -1461,7 +1461,7 @@ mrf_status mrf_dict_match(mrf_dict d, const void* x, long long V, int* index, fl
     d->xp = nullptr; d->xs = nullptr; d->best = nullptr; d->vcap = 0;
     if (cudaMalloc((void**)&d->xp, (size_t)vpad * d->KD * sizeof(__half)) != cudaSuccess ||
         cudaMalloc((void**)&d->xs, (size_t)vpad * sizeof(float)) != cudaSuccess ||
-        cudaMalloc((void**)&d->best, (size_t)vpad * sizeof(int)) != cudaSuccess)
+        cudaMalloc((void**)&d->best, (size_t)vpad * sizeof(unsigned long long)) != cudaSuccess)
       return fail(MRF_ENOMEM, "mrf_dict_match: workspace allocation failed");
     d->vcap = vpad;
   }
@@ -1478,8 +1478,12 @@ mrf_status mrf_dict_match(mrf_dict d, const void* x, long long V, int* index, fl
     }
     CUDA_TRY(cudaEventRecord(d->ev[d->ev_used], st));
   }
-  dm::k_dict_gemm<<<(unsigned)(vpad / dm::BM), dm::THREADS, dm::SMEM, st>>>(tmx, d->tmd, d->w2, d->NP / dm::BN,
-                                                                            d->KD / dm::BK, (int)V, d->best);
+  const int m_tiles = (int)(vpad / dm::BM), n_tiles = d->NP / dm::BN;
+  int n_sm = 148;
+  CUDA_TRY(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, d->device));
+  CUDA_TRY(cudaMemsetAsync(d->best, 0, (size_t)V * sizeof(unsigned long long), st));
+  dm::k_dict_gemm<<<(unsigned)std::min(n_sm, m_tiles * n_tiles), dm::THREADS, dm::SMEM, st>>>(
+      tmx, d->tmd, d->w2, m_tiles, n_tiles, d->KD / dm::BK, (int)V, d->best);
   MRF_TRY(check_launch("k_dict_gemm"));
   if (d->prof) {
     CUDA_TRY(cudaEventRecord(d->ev[d->ev_used + 1], st));
