@@ -233,15 +233,17 @@ k_dict_gemm(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUt
 __global__ void __launch_bounds__(256) k_dict_pack_x(const float2* __restrict__ x, int L, int V, int KD,
                                                      __half* __restrict__ xp, float* __restrict__ s) {
   __shared__ float red[8][33];
-  __shared__ __half2 tile[32][33];
+  __shared__ __half2 tile[32][65];
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   const int v = blockIdx.x * 32 + tx;
   float m = 0.f;
-  if (v < V)
+  if (v < V) {
+#pragma unroll 8
     for (int l = ty; l < L; l += 8) {
       const float2 a = __ldg(x + (size_t)l * V + v);
       m = fmaxf(m, fmaxf(fabsf(a.x), fabsf(a.y)));
     }
+  }
   red[ty][tx] = m;
   __syncthreads();
   if (ty == 0) {
@@ -253,18 +255,24 @@ __global__ void __launch_bounds__(256) k_dict_pack_x(const float2* __restrict__ 
   __syncthreads();
   const float inv = 1.f / red[0][tx];
   const int L2 = KD / 2;   // complex slots per padded row
-  for (int l0 = 0; l0 < L2; l0 += 32) {
-    // load 32 frames x 32 voxels (coalesced over voxels), transpose through shared memory
-    for (int i = ty; i < 32; i += 8) {
-      const int l = l0 + i;
-      float2 a = make_float2(0.f, 0.f);
-      if (v < V && l < L) a = __ldg(x + (size_t)l * V + v);
-      tile[tx][i] = __floats2half2_rn(a.x * inv, a.y * inv);
+  for (int l0 = 0; l0 < L2; l0 += 64) {
+    // load 64 frames x 32 voxels (coalesced over voxels, 8 loads in flight per thread),
+    // transpose through shared memory
+    float2 a[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int l = l0 + ty + 8 * q;
+      a[q] = (v < V && l < L) ? __ldg(x + (size_t)l * V + v) : make_float2(0.f, 0.f);
     }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) tile[tx][ty + 8 * q] = __floats2half2_rn(a[q].x * inv, a[q].y * inv);
     __syncthreads();
-    for (int i = ty; i < 32; i += 8) {   // voxel blockIdx*32 + i, frames l0 + tx
+#pragma unroll
+    for (int i = ty; i < 32; i += 8) {   // voxel blockIdx*32 + i, frames l0 + tx and l0 + 32 + tx
       const int vv = blockIdx.x * 32 + i;
-      reinterpret_cast<__half2*>(xp + (size_t)vv * KD)[l0 + tx] = tile[i][tx];
+      __half2* row = reinterpret_cast<__half2*>(xp + (size_t)vv * KD);
+      if (l0 + tx < L2) row[l0 + tx] = tile[i][tx];
+      if (l0 + 32 + tx < L2) row[l0 + 32 + tx] = tile[i][32 + tx];
     }
     __syncthreads();
   }
@@ -279,27 +287,33 @@ __global__ void __launch_bounds__(256) k_dict_fix(const float2* __restrict__ x, 
                                                   int L, int V, const unsigned long long* __restrict__ best,
                                                   int* __restrict__ index,
                                                   float* __restrict__ pd, float* __restrict__ params) {
-  __shared__ float2 xt[32][33];   // [l][v]
-  __shared__ float2 dt[32][33];   // [v][l]
+  __shared__ float2 xt[64][33];   // [l][v]
+  __shared__ float2 dt[32][65];   // [v][l]
   __shared__ int ks[32];
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   const int v0 = blockIdx.x * 32;
   if (threadIdx.x < 32) ks[tx] = v0 + tx < V ? (int)(0xFFFFFFFFu - (uint32_t)(best[v0 + tx] & 0xFFFFFFFFull)) : 0;
   __syncthreads();
   float acc[4] = {0.f, 0.f, 0.f, 0.f};
-  for (int l0 = 0; l0 < L; l0 += 32) {
+  for (int l0 = 0; l0 < L; l0 += 64) {   // 64 frames per step, 16 loads in flight per thread
 #pragma unroll
-    for (int i = ty; i < 32; i += 8) {
+    for (int i = ty; i < 64; i += 8) {
       const int l = l0 + i, v = v0 + tx;
       xt[i][tx] = (l < L && v < V) ? __ldg(x + (size_t)l * V + v) : make_float2(0.f, 0.f);
-      dt[i][tx] = (l0 + tx < L) ? __ldg(atoms + (size_t)ks[i] * L + l0 + tx) : make_float2(0.f, 0.f);
+    }
+#pragma unroll
+    for (int i = ty; i < 32; i += 8) {
+      const float2* dr = atoms + (size_t)ks[i] * L + l0;
+      dt[i][tx] = (l0 + tx < L) ? __ldg(dr + tx) : make_float2(0.f, 0.f);
+      dt[i][32 + tx] = (l0 + 32 + tx < L) ? __ldg(dr + 32 + tx) : make_float2(0.f, 0.f);
     }
     __syncthreads();
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {   // Re(conj(d) x) = dr xr + di xi, frame l0 + tx
+    for (int q = 0; q < 4; ++q) {   // Re(conj(d) x) = dr xr + di xi, frames l0 + tx and l0 + 32 + tx
       const int j = ty * 4 + q;
-      const float2 d = dt[j][tx], xv = xt[tx][j];
-      acc[q] = fmaf(d.x, xv.x, fmaf(d.y, xv.y, acc[q]));
+      const float2 d0 = dt[j][tx], x0 = xt[tx][j], d1 = dt[j][32 + tx], x1 = xt[32 + tx][j];
+      acc[q] = fmaf(d0.x, x0.x, fmaf(d0.y, x0.y, acc[q]));
+      acc[q] = fmaf(d1.x, x1.x, fmaf(d1.y, x1.y, acc[q]));
     }
     __syncthreads();
   }
