@@ -216,8 +216,8 @@ __device__ __forceinline__ void gather_rec(const int* rp, const float2* strip, f
   constexpr int RW = (2 + 2 * W + 3) & ~3;
   int wd[RW];
 #pragma unroll
-  for (int k = 0; k < RW / 4; ++k) {
-    const int4 q = GL ? __ldg(reinterpret_cast<const int4*>(rp) + k) : reinterpret_cast<const int4*>(rp)[k];
+  for (int k = 0; k < RW / 4; ++k) {   // 16-byte piece k of the record: 32 records apart
+    const int4 q = GL ? __ldg(reinterpret_cast<const int4*>(rp) + 32 * k) : reinterpret_cast<const int4*>(rp)[32 * k];
     wd[4 * k] = q.x;
     wd[4 * k + 1] = q.y;
     wd[4 * k + 2] = q.z;
@@ -246,22 +246,23 @@ __device__ __forceinline__ void gather_rec(const int* rp, const float2* strip, f
 // The same for any W in [2, 16] (run-time loops; rp may point to shared or global memory).
 template <int G>
 __device__ __forceinline__ void gather_rec_any(const int* rp, int W, const float2* strip, float2* __restrict__ yf) {
-  const int gy0 = rp[1] & 2047, cx0 = (rp[1] >> 11) & 31;
-  const float* wx = reinterpret_cast<const float*>(rp + 2);
+  auto word = [&](int w) { return rp[(w >> 2) * 128 + (w & 3)]; };   // record word w (interleaved layout)
+  auto wt = [&](int w) { return __int_as_float(word(w)); };
+  const int gy0 = word(1) & 2047, cx0 = (word(1) >> 11) & 31;
   float2 acc = make_float2(0.f, 0.f);
   for (int ty = 0; ty < W; ++ty) {
     const float2* row = strip + ((gy0 + ty) & (G - 1)) * SWG + cx0;
     float2 racc = make_float2(0.f, 0.f);
     for (int i = 0; i < W; ++i) {
       const float2 g = row[i];
-      racc.x = fmaf(wx[i], g.x, racc.x);
-      racc.y = fmaf(wx[i], g.y, racc.y);
+      racc.x = fmaf(wt(2 + i), g.x, racc.x);
+      racc.y = fmaf(wt(2 + i), g.y, racc.y);
     }
-    acc.x = fmaf(wx[W + ty], racc.x, acc.x);
-    acc.y = fmaf(wx[W + ty], racc.y, acc.y);
+    acc.x = fmaf(wt(2 + W + ty), racc.x, acc.x);
+    acc.y = fmaf(wt(2 + W + ty), racc.y, acc.y);
   }
-  atomicAdd(&yf[rp[0]].x, acc.x);
-  atomicAdd(&yf[rp[0]].y, acc.y);
+  atomicAdd(&yf[word(0)].x, acc.x);
+  atomicAdd(&yf[word(0)].y, acc.y);
 }
 
 // ============================================================================ forward rows
@@ -498,19 +499,22 @@ k_fwd_cols(DevPlan p, const float2* __restrict__ H, float2* __restrict__ y, int 
     pt.mark(5);
     if (!MRF_DBG_ON(1)) {
       const int n_rec = stage[0];
-      const int n_st = (copied / 4 - kChunkHdr) / recw;     // records staged in shared memory
+      // records in groups of 32, each group's records interleaved by 16-byte pieces (a warp's
+      // piece-k loads are one contiguous 512-byte span); whole groups are staged
+      const int n_st = ((copied / 4 - kChunkHdr) / (32 * recw)) * 32;
       const int* recs = stage + kChunkHdr;
       const int* grecs = p.fchunks + fchunk_off + kChunkHdr;
       float2* yf = y + (size_t)fc * p.M;
       for (int e = tid; e < n_rec; e += blockDim.x) {
+        const int ro = (e >> 5) * recw * 32 + (e & 31) * 4;   // word offset of the record's piece 0
         if (W == 6) {
-          if (e < n_st) gather_rec<G, 6, false>(recs + e * recw, strip, yf);
-          else gather_rec<G, 6, true>(grecs + e * recw, strip, yf);
+          if (e < n_st) gather_rec<G, 6, false>(recs + ro, strip, yf);
+          else gather_rec<G, 6, true>(grecs + ro, strip, yf);
         } else if (W == 8) {
-          if (e < n_st) gather_rec<G, 8, false>(recs + e * recw, strip, yf);
-          else gather_rec<G, 8, true>(grecs + e * recw, strip, yf);
+          if (e < n_st) gather_rec<G, 8, false>(recs + ro, strip, yf);
+          else gather_rec<G, 8, true>(grecs + ro, strip, yf);
         } else {
-          gather_rec_any<G>((e < n_st ? recs : grecs) + e * recw, W, strip, yf);
+          gather_rec_any<G>((e < n_st ? recs : grecs) + ro, W, strip, yf);
         }
       }
     }

@@ -943,23 +943,44 @@ mrf_status mrf_plan_create(const mrf_plan_desc* d, mrf_plan* out) {
       }
     }
     for (int s = 0; s < S; ++s) {
+      {   // deal the strip's records so that each run of 32 (one warp of the thread-per-record
+          // gather) covers the 16 residues (gy0 + cx0) mod 16 evenly: with the 17-slot strip rows
+          // every tap of a record sits in bank pair (gy0 + cx0 + ty + tx) mod 16, so a warp's tap
+          // loads then hit each bank pair at most twice (conflict-free 64-bit accesses)
+        std::vector<std::vector<int2>> res(16);
+        for (const int2& rr : bins[s]) res[((rr.y & 2047) + ((rr.y >> 21) & 31)) & 15].push_back(rr);
+        std::vector<size_t> nx(16, 0);
+        for (size_t o = 0; o < bins[s].size(); ++o) {
+          int b = (int)(o & 15);
+          if (nx[b] == res[b].size()) {
+            size_t best = 0;
+            for (int q = 0; q < 16; ++q)
+              if (res[q].size() - nx[q] > best) { best = res[q].size() - nx[q]; b = q; }
+          }
+          bins[s][o] = res[b][nx[b]++];
+        }
+      }
       const std::vector<int2>& rb = bins[s];
       const int n_rec = (int)rb.size();
       // forward chunk: header + records
       {
         const size_t base = fch.size();
-        const size_t words = ((size_t)kChunkHdr + (size_t)n_rec * recw + 3) & ~(size_t)3;
+        const size_t words = (size_t)kChunkHdr + (size_t)((n_rec + 31) / 32) * 32 * recw;
         fch.resize(base + words, 0);
         fch[base] = n_rec;
         for (int ri = 0; ri < n_rec; ++ri) {
-          int* rp = &fch[base + kChunkHdr + (size_t)ri * recw];
+          std::vector<int> rec((size_t)recw, 0);
           const int pk = rb[ri].y, tx0 = (pk >> 11) & 31, ntx = (pk >> 16) & 31;
           const float* wp = &wts[((size_t)r * M + rb[ri].x) * 2 * W];
-          rp[0] = rb[ri].x;
-          rp[1] = (pk & 2047) | (((pk >> 21) & 31) << 11);   // first grid row | first strip column
-          float* wx = reinterpret_cast<float*>(rp + 2);
+          rec[0] = rb[ri].x;
+          rec[1] = (pk & 2047) | (((pk >> 21) & 31) << 11);   // first grid row | first strip column
+          float* wx = reinterpret_cast<float*>(&rec[2]);
           for (int i = 0; i < W; ++i) wx[i] = i < ntx ? wp[tx0 + i] : 0.f;   // x-weights aligned to the strip
-          std::memcpy(rp + 2 + W, wp + W, sizeof(float) * W);
+          std::memcpy(&rec[2 + W], wp + W, sizeof(float) * W);
+          // interleaved store: piece k (words 4k..4k+3) of record 32g + l at (g recw + 4k) 32 + 4l
+          const size_t g = (size_t)ri / 32, l = (size_t)ri % 32;
+          for (int w = 0; w < recw; ++w)
+            fch[base + kChunkHdr + (g * recw + (size_t)(w & ~3)) * 32 + 4 * l + (w & 3)] = rec[(size_t)w];
         }
         ftab[(size_t)r * S + s] = make_int2((int)base, (int)words);
       }
