@@ -53,8 +53,11 @@ def parse():
     return ap.parse_args()
 
 
-def passes_per_step(n_iter: int) -> int:
-    return 2 * n_iter + 3          # 1 adjoint + (n_iter + 1) normals, each normal = fwd + adj
+def passes_per_step(n_iter: int, zero_init: bool = True) -> int:
+    """NUFFT point-passes of one CG step: 1 adjoint (rhs) + the normals (fwd + adj each).  From
+    x0 = 0 with mrf_dc_cg_ex(MRF_CG_ZERO_INIT) the library applies n_iter normals; the oracle's
+    textbook CG also applies one to x0 (n_iter + 1), and its reference line counts that work."""
+    return 2 * n_iter + (1 if zero_init else 3)
 
 
 # ------------------------------------------------------------------------------------ clocks
@@ -152,12 +155,12 @@ def kernel_flops(cfg, cls: str, frames: int) -> float:
 
 
 def step_bytes(cfg, L: int, n_iter: int) -> float:
-    """Compulsory HBM bytes of one dc_cg step (SURVEY.md §8(d) "Algorithmic bytes"): adjoint
-    L(8N^2 + 8CM); each normal L 16 N^2; CG init (r = rhs - q, p = r) 4 image passes; each CG
-    iteration 10 image passes (normal 2 + <p,q> 2 + x,r update 6) -- the minimum is 8."""
+    """Compulsory HBM bytes of one dc_cg step from x0 = 0 (SURVEY.md §8(d) "Algorithmic bytes"):
+    adjoint L(8N^2 + 8CM); each of the n_iter normals L 16 N^2; CG init (x = 0, r = rhs, p = r)
+    3 image passes; each CG iteration 8 image passes beyond its normal (the minimum)."""
     N, C, M = cfg.N, cfg.C, cfg.M
     img = 8.0 * N * N * L
-    return L * (8.0 * N * N + 8.0 * C * M) + (n_iter + 1) * 2 * img + 4 * img + n_iter * 8 * img
+    return L * (8.0 * N * N + 8.0 * C * M) + n_iter * 2 * img + 3 * img + n_iter * 8 * img
 
 
 def cpu_count():
@@ -199,9 +202,9 @@ def oracle_sample(cfg, n_iter: int, target_s: float, nf=None):
     rhs = ocg.dc_rhs(on.adjoint(y, traj, coils, cfg.N, cfg.W, frame_interleaf=fil, workers=workers), None, cfg.mu)
     ocg.cg(H, rhs, np.zeros_like(rhs), n_iter)
     dt = time.perf_counter() - t0
-    pts = nf * cfg.C * cfg.M * passes_per_step(n_iter)
+    pts = nf * cfg.C * cfg.M * passes_per_step(n_iter, zero_init=False)
     desc = (f"oracle dc_cg (float64 numpy/scipy, {n_iter} CG iterations) on frames 0..{nf - 1} of {cfg.L} of the "
-            f"'{cfg.name}' workload ({nf * cfg.C * cfg.M * passes_per_step(n_iter)} point-passes), "
+            f"'{cfg.name}' workload ({nf * cfg.C * cfg.M * passes_per_step(n_iter, zero_init=False)} point-passes), "
             f"{workers} ThreadPool workers over frames")
     return {"value": pts / dt, "frames": nf, "cores": workers, "seconds": dt, "sample": desc}
 
@@ -220,7 +223,7 @@ def run_reference(args):
         if i >= args.warmup:
             vals.append(last["value"])
     value = float(np.median(vals))
-    steps_ms = 1e3 * cfg.L * cfg.C * cfg.M * passes_per_step(n_iter) / value
+    steps_ms = 1e3 * cfg.L * cfg.C * cfg.M * passes_per_step(n_iter, zero_init=False) / value
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": steps_ms, "higher_is_better": True,
@@ -273,9 +276,8 @@ def run_ours(args):
     xbuf = torch.zeros(plan.x_shape, dtype=torch.complex64, device=dev)
     stream = torch.cuda.current_stream(dev)
 
-    def step():
-        xbuf.zero_()
-        plan.dc_cg(y, mu=cfg.mu, n_iter=n_iter, x=xbuf)
+    def step():   # CG from x0 = 0 (Algorithm 1's data-consistency solve); x is output only
+        plan.dc_cg(y, mu=cfg.mu, n_iter=n_iter, x=xbuf, zero_init=True)
 
     def barrier():
         if world > 1:
@@ -358,8 +360,7 @@ def run_ours(args):
         xbuf_t = torch.zeros_like(xbuf)
 
         def step_t():
-            xbuf_t.zero_()
-            plan_t.dc_cg(y, mu=cfg.mu, n_iter=n_iter, x=xbuf_t)
+            plan_t.dc_cg(y, mu=cfg.mu, n_iter=n_iter, x=xbuf_t, zero_init=True)
         ms_step_t = time_op(step_t, max(2, min(args.steps, 5)))
         fl = sum(kernel_flops(cfg, k, cfg.L) for k in ("fwd_rows", "adj_rows")) + \
             cfg.L * cfg.C * 2 * cfg.G * 5.0 * cfg.G * math.log2(cfg.G)
@@ -405,19 +406,19 @@ def run_ours(args):
     if not args.no_e2e:
         y_h = y.cpu().pin_memory()
         x_h = torch.zeros(plan.x_shape, dtype=torch.complex64).pin_memory()
-        plan.dc_cg(y_h, mu=cfg.mu, n_iter=n_iter, x=x_h)          # warm-up (allocates staging)
+        plan.dc_cg(y_h, mu=cfg.mu, n_iter=n_iter, x=x_h, zero_init=True)   # warm-up (allocates staging)
         barrier()
         t0 = time.perf_counter()
         for _ in range(max(1, min(args.steps, 3))):
-            x_h.zero_()
-            plan.dc_cg(y_h, mu=cfg.mu, n_iter=n_iter, x=x_h)
+            plan.dc_cg(y_h, mu=cfg.mu, n_iter=n_iter, x=x_h, zero_init=True)
         torch.cuda.synchronize()
         n_e2e = max(1, min(args.steps, 3))
         ms_e2e = max_over_ranks((time.perf_counter() - t0) * 1e3 / n_e2e)
         e2e = {"value": pts_step / (ms_e2e * 1e-3), "unit": UNIT, "ms_per_step": ms_e2e,
-               "h2d_bytes_per_step": int(y_h.numel() * 8 + x_h.numel() * 8) * world,
+               "h2d_bytes_per_step": int(y_h.numel() * 8) * world,
                "d2h_bytes_per_step": int(x_h.numel() * 8) * world,
-               "note": "host pinned y and x0 copied in, solution x copied out, inside each mrf_dc_cg call"}
+               "note": "host pinned k-space y copied in, solution x copied out, inside each "
+                       "mrf_dc_cg_ex(MRF_CG_ZERO_INIT) call (x0 = 0 is not transferred)"}
 
     # ---------------------------------------------------------------- roofline of the dominant kernel
     sm_count = torch.cuda.get_device_properties(dev).multi_processor_count
@@ -429,7 +430,7 @@ def run_ours(args):
     dom = max(("fwd_rows", "fwd_cols", "adj_cols", "adj_rows"), key=lambda k: cls_ms[k])
     dom_ms, dom_n = prof[dom]
     # frames processed by the dominant class in the timed region: each launch covers a batch
-    frames_per_call = {"fwd_rows": n_iter + 1, "fwd_cols": n_iter + 1, "adj_cols": n_iter + 2, "adj_rows": n_iter + 2}
+    frames_per_call = {"fwd_rows": n_iter, "fwd_cols": n_iter, "adj_cols": n_iter + 1, "adj_rows": n_iter + 1}
     dom_flops_total = kernel_flops(cfg, dom, L) * frames_per_call[dom] * args.steps
     achieved = dom_flops_total / (dom_ms * 1e-3) / 1e12 if dom_ms > 0 else None
     # traffic: ncu dram bytes per launch, scaled from the capture's frames per launch to this run's
@@ -476,7 +477,7 @@ def run_ours(args):
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": cfg.name, "N": cfg.N, "L": cfg.L, "M": cfg.M, "C": cfg.C, "R": cfg.R, "W": cfg.W,
                    "sigma": cfg.sigma, "cg_iters": n_iter, "mu": cfg.mu, "parallelism": f"frames/{world}",
-                   "step": "mrf_dc_cg: 1 adjoint + (n_iter+1) normals + CG vector ops",
+                   "step": "mrf_dc_cg_ex(MRF_CG_ZERO_INIT), x0 = 0: 1 adjoint + n_iter normals + CG vector ops",
                    "l2": "working set > L2 (x, r, p, q each %.0f MB); no flush" % (cfg.L * cfg.N ** 2 * 8 / 1e6),
                    "batch_frames": args.batch_frames or "auto"},
         "ms_per_AHA": ms_normal, "ms_per_forward": ms_fwd, "ms_per_adjoint": ms_adj,

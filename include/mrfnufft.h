@@ -130,6 +130,14 @@ typedef struct {
 mrf_status mrf_dc_cg(mrf_plan plan, const void* y, const void* z, float mu, int n_iter, float tol,
                      void* x, mrf_cg_info* info, void* stream);
 
+/* mrf_dc_cg with flags.  MRF_CG_ZERO_INIT: the initial guess is x0 = 0 (Algorithm 1's CG from
+ * rest) and x is output only: neither read nor (on the host path) copied in, and the initial
+ * residual is r = rhs without an application of the normal operator.  Same iterates as
+ * mrf_dc_cg on a zeroed x.  Unknown flags: MRF_EINVAL. */
+#define MRF_CG_ZERO_INIT 1u
+mrf_status mrf_dc_cg_ex(mrf_plan plan, const void* y, const void* z, float mu, int n_iter, float tol,
+                        unsigned flags, void* x, mrf_cg_info* info, void* stream);
+
 mrf_status mrf_plan_destroy(mrf_plan plan);
 
 const char* mrf_status_string(mrf_status status);

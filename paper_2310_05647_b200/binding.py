@@ -28,7 +28,7 @@ STATUS = {0: "MRF_OK", 1: "MRF_EINVAL", 2: "MRF_ENOMEM", 3: "MRF_ECUDA", 4: "MRF
           5: "MRF_EUNSUPPORTED", 6: "MRF_ENUMERIC"}
 
 EXPORTED = [
-    "mrf_plan_create", "mrf_forward", "mrf_adjoint", "mrf_normal", "mrf_dc_cg", "mrf_plan_destroy",
+    "mrf_plan_create", "mrf_forward", "mrf_adjoint", "mrf_normal", "mrf_dc_cg", "mrf_dc_cg_ex", "mrf_plan_destroy",
     "mrf_status_string", "mrf_last_error", "mrf_plan_device_bytes", "mrf_profile_enable",
     "mrf_profile_query", "mrf_nccl_get_unique_id", "mrf_nccl_comm_init", "mrf_nccl_comm_destroy",
     "mrf_adjoint_dcf", "mrf_dcf_weights", "mrf_dict_create", "mrf_dict_match", "mrf_dict_destroy", "mrf_dict_profile", "mrf_dict_profile_query",
@@ -73,6 +73,7 @@ def _load() -> ctypes.CDLL:
         "mrf_dcf_weights": ([vp, vp], ci),
         "mrf_normal": ([vp, vp, vp, cf, vp], ci),
         "mrf_dc_cg": ([vp, vp, vp, cf, ci, cf, vp, ctypes.POINTER(CGInfo), vp], ci),
+        "mrf_dc_cg_ex": ([vp, vp, vp, cf, ci, cf, ctypes.c_uint, vp, ctypes.POINTER(CGInfo), vp], ci),
         "mrf_plan_destroy": ([vp], ci),
         "mrf_status_string": ([ci], ctypes.c_char_p),
         "mrf_last_error": ([], ctypes.c_char_p),
@@ -220,19 +221,25 @@ class Plan:
         _check(lib.mrf_normal(self._h, _ptr(x), _ptr(out), ctypes.c_float(mu), self._stream(x, out)))
         return out
 
-    def dc_cg(self, y, x0=None, z=None, mu: float = 0.01, n_iter: int = 10, tol: float = 0.0, x=None):
-        """CG solve of (A^H A + mu I) x = A^H y + mu z from x0; returns (x, info dict)."""
+    def dc_cg(self, y, x0=None, z=None, mu: float = 0.01, n_iter: int = 10, tol: float = 0.0, x=None,
+              zero_init: bool = False):
+        """CG solve of (A^H A + mu I) x = A^H y + mu z from x0; returns (x, info dict).
+
+        zero_init=True: x0 = 0 and x is output only (mrf_dc_cg_ex with MRF_CG_ZERO_INIT: no normal
+        operator for the initial residual, and no host-to-device copy of x0 on the host path)."""
         y = _as_c64(y, self.y_shape, "y")
         if x is None:
             x = self._like(y, self.x_shape)
-            if x0 is None:
+            if x0 is None and not zero_init:
                 x.zero_()
-            else:
+            elif x0 is not None:
                 x.copy_(_as_c64(x0, self.x_shape, "x0"))
         else:
             x = _as_c64(x, self.x_shape, "x")
             if x0 is not None:
                 x.copy_(_as_c64(x0, self.x_shape, "x0"))
+        if zero_init and x0 is not None:
+            raise ValueError("zero_init excludes x0")
         if z is not None:
             z = _as_c64(z, self.x_shape, "z")
         hist = (ctypes.c_double * (n_iter + 1))()
@@ -240,8 +247,8 @@ class Plan:
         hb = (ctypes.c_double * max(n_iter, 1))()
         dp = lambda a: ctypes.cast(a, ctypes.POINTER(ctypes.c_double))
         info = CGInfo(0, 0.0, dp(hist), dp(ha), dp(hb))
-        _check(lib.mrf_dc_cg(self._h, _ptr(y), _ptr(z), ctypes.c_float(mu), int(n_iter), ctypes.c_float(tol),
-                             _ptr(x), ctypes.byref(info), self._stream(x, y, z)))
+        _check(lib.mrf_dc_cg_ex(self._h, _ptr(y), _ptr(z), ctypes.c_float(mu), int(n_iter), ctypes.c_float(tol),
+                                1 if zero_init else 0, _ptr(x), ctypes.byref(info), self._stream(x, y, z)))
         it = info.iters
         return x, {"iters": it, "rel_resid": info.rel_resid, "history": list(hist)[: it + 1],
                    "alpha": list(ha)[:it], "beta": list(hb)[:it]}

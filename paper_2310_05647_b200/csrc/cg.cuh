@@ -86,7 +86,7 @@ struct CGScalars {
   int breakdown, iters;
 };
 
-// r = rhs - q ; p = r  (initial residual); partial <r,r>
+// r = rhs - q ; p = r  (initial residual; q == nullptr: x0 = 0, r = rhs); partial <r,r>
 __global__ void __launch_bounds__(kVecThreads) k_cg_init(const float2* __restrict__ rhs, const float2* __restrict__ q,
                                                          float2* __restrict__ r, float2* __restrict__ pv, size_t n,
                                                          double2* __restrict__ part) {
@@ -96,7 +96,7 @@ __global__ void __launch_bounds__(kVecThreads) k_cg_init(const float2* __restric
   float4* p4 = reinterpret_cast<float4*>(pv);
   double2 s = make_double2(0.0, 0.0);
   MRF_VEC4_LOOP(n / 2, {
-    const float4 a = rh4[i], b = q4[i];
+    const float4 a = rh4[i], b = q4 ? q4[i] : make_float4(0.f, 0.f, 0.f, 0.f);
     const float4 v = make_float4(a.x - b.x, a.y - b.y, a.z - b.z, a.w - b.w);
     r4[i] = v;
     p4[i] = v;

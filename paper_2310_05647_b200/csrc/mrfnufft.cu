@@ -639,7 +639,7 @@ static mrf_status vec_launch_check(const char* what) { return check_launch(what)
 // x_k = x_{k-1} + alpha_{k-1} p_{k-1} (same iterates as the textbook order), the normal operator
 // whose last pass also emits <p_k, q_k> partials, and one r-update pass that emits <r, r>.
 static mrf_status run_cg(mrf_plan_s* pl, const float2* y, const float2* z, float mu, int n_iter, float tol,
-                         float2* x, mrf_cg_info* info, cudaStream_t st) {
+                         float2* x, mrf_cg_info* info, cudaStream_t st, bool zero_init = false) {
   const size_t n = (size_t)pl->L * pl->N * pl->N;
   const int nblk = vec_blocks(n);
   if (n_iter + 1 > pl->hist_cap) {   // [sqrt(rho_k), k <= n][alpha_k][beta_k]
@@ -658,11 +658,15 @@ static mrf_status run_cg(mrf_plan_s* pl, const float2* y, const float2* z, float
     k_axpy<<<nblk, kVecThreads, 0, st>>>(pl->r, z, mu, n);
     MRF_TRY(vec_launch_check("k_axpy"));
   }
-  // r = rhs - H x0 ; p = r ; rho0
-  MRF_TRY(do_normal(pl, x, pl->q, mu, st));
+  // r = rhs - H x0 ; p = r ; rho0   (x0 = 0: no normal operator, x = 0)
+  if (zero_init) {
+    CUDA_TRY(cudaMemsetAsync(x, 0, n * sizeof(float2), st));
+  } else {
+    MRF_TRY(do_normal(pl, x, pl->q, mu, st));
+  }
   {
     ProfScope ps(pl, MRF_K_CG_VEC, st);
-    k_cg_init<<<nblk, kVecThreads, 0, st>>>(pl->r, pl->q, pl->r, pl->p, n, pl->part);
+    k_cg_init<<<nblk, kVecThreads, 0, st>>>(pl->r, zero_init ? nullptr : pl->q, pl->r, pl->p, n, pl->part);
     MRF_TRY(vec_launch_check("k_cg_init"));
   }
   MRF_TRY(reduce_to(pl, pl->part, nblk, &pl->sc->rr, st));
@@ -1260,7 +1264,14 @@ mrf_status mrf_normal(mrf_plan pl, const void* x, void* out, float mu, void* str
 
 mrf_status mrf_dc_cg(mrf_plan pl, const void* y, const void* z, float mu, int n_iter, float tol, void* x,
                      mrf_cg_info* info, void* stream) {
+  return mrf_dc_cg_ex(pl, y, z, mu, n_iter, tol, 0u, x, info, stream);
+}
+
+mrf_status mrf_dc_cg_ex(mrf_plan pl, const void* y, const void* z, float mu, int n_iter, float tol, unsigned flags,
+                        void* x, mrf_cg_info* info, void* stream) {
   if (!pl || !y || !x) return fail(MRF_EINVAL, "null plan/y/x");
+  if (flags & ~MRF_CG_ZERO_INIT) return fail(MRF_EINVAL, "unknown CG flags");
+  const bool zero_init = (flags & MRF_CG_ZERO_INIT) != 0;
   if (!(mu >= 0.f) || !std::isfinite(mu)) return fail(MRF_EINVAL, "mu must be finite and >= 0");
   if (n_iter < 0) return fail(MRF_EINVAL, "n_iter < 0");
   if (!(tol >= 0.f) || !std::isfinite(tol)) return fail(MRF_EINVAL, "tol must be finite and >= 0");
@@ -1268,13 +1279,13 @@ mrf_status mrf_dc_cg(mrf_plan pl, const void* y, const void* z, float mu, int n_
   cudaStream_t st = (cudaStream_t)stream;
   bool host = false;
   MRF_TRY(classify(pl, {y, z, x}, &host));
-  if (!host) return run_cg(pl, (const float2*)y, (const float2*)z, mu, n_iter, tol, (float2*)x, info, st);
+  if (!host) return run_cg(pl, (const float2*)y, (const float2*)z, mu, n_iter, tol, (float2*)x, info, st, zero_init);
   MRF_TRY(ensure_staging(pl, z != nullptr));
   const size_t bx = (size_t)pl->L * pl->N * pl->N * sizeof(float2), by = (size_t)pl->L * pl->C * pl->M * sizeof(float2);
   CUDA_TRY(cudaMemcpyAsync(pl->stg_y, y, by, cudaMemcpyHostToDevice, st));
-  CUDA_TRY(cudaMemcpyAsync(pl->stg_x, x, bx, cudaMemcpyHostToDevice, st));
+  if (!zero_init) CUDA_TRY(cudaMemcpyAsync(pl->stg_x, x, bx, cudaMemcpyHostToDevice, st));
   if (z) CUDA_TRY(cudaMemcpyAsync(pl->stg_z, z, bx, cudaMemcpyHostToDevice, st));
-  mrf_status s = run_cg(pl, pl->stg_y, z ? pl->stg_z : nullptr, mu, n_iter, tol, pl->stg_x, info, st);
+  mrf_status s = run_cg(pl, pl->stg_y, z ? pl->stg_z : nullptr, mu, n_iter, tol, pl->stg_x, info, st, zero_init);
   if (s != MRF_OK && s != MRF_ENUMERIC) return s;
   CUDA_TRY(cudaMemcpyAsync(x, pl->stg_x, bx, cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaStreamSynchronize(st));

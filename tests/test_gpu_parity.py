@@ -481,3 +481,18 @@ def test_dcf_weights_and_weighted_adjoint(mrf):
     with pytest.raises(binding.MrfError):
         pl.adjoint_dcf(torch.zeros(pl.y_shape, dtype=torch.complex64, device="cuda"))
     pl.close()
+
+
+def test_cg_zero_init_matches_zeroed_x0(mrf):
+    """mrf_dc_cg_ex(MRF_CG_ZERO_INIT): no normal operator for r0 = rhs, x output only; the same
+    iterates as mrf_dc_cg from a zeroed x (H 0 = 0 exactly), on the device and the host path."""
+    cfg, traj, coils, frames, x = setup("pr1")
+    y = on.forward(x, traj, None, cfg.W).astype(np.complex64)
+    pl = mrf.Plan(cfg.N, traj, cfg.L, W=cfg.W)
+    xa, ia = pl.dc_cg(dev(y), mu=cfg.mu, n_iter=cfg.cg_iters)
+    xb, ib = pl.dc_cg(dev(y), mu=cfg.mu, n_iter=cfg.cg_iters, zero_init=True)
+    xh, ih = pl.dc_cg(torch.from_numpy(y), mu=cfg.mu, n_iter=cfg.cg_iters, zero_init=True)
+    pl.close()
+    a, b = host(xa), host(xb)
+    assert np.array_equal(a, b) and np.array_equal(a, xh.numpy())
+    assert ia["history"] == ib["history"] == ih["history"]
