@@ -159,13 +159,10 @@ template <int G>
 constexpr size_t fwd_cols_fixed() { return (size_t(G) + size_t(G / 2) * SW + size_t(G) * SWG + SW) * 8 + 16; }
 template <int G>
 constexpr size_t toep_cols_smem() { return (size_t(G) + size_t(G / 2) * SW + size_t(G) * SW) * 8 + 16; }
+// k_adj_cols layout: SEP = separate exchange buffer + register twiddles (G <= 512, one CTA per SM)
 template <int G>
-struct AdjCols {   // k_adj_cols layout: separate exchange buffer + register twiddles when it fits
-  static constexpr bool SEP = G <= 512;
-};
-template <int G>
-constexpr size_t adj_cols_fixed(size_t ybytes) {
-  return (AdjCols<G>::SEP ? 2 * size_t(G) * SW : size_t(G) + size_t(G) * SW) * 8 + ybytes + 16;
+constexpr size_t adj_cols_fixed(size_t ybytes, bool sep) {
+  return (sep ? 2 * size_t(G) * SW : size_t(G) + size_t(G) * SW) * 8 + ybytes + 16;
 }
 
 // Phase timer (experiment bit 2; only compiled with -DMRF_EXPERIMENTS): thread 0 of every CTA
@@ -600,8 +597,8 @@ __device__ __forceinline__ void spread_cells(const int2* sl_tab, const unsigned 
 // summing w * y_j over its (j, w) list (SELL-32 slices, no atomics, deterministic);
 // a5: column iFFT, then the N kept rows are stored strip-major H[fc][strip][iy][16].
 // Pipeline: y[fc] and the chunk of the next item are fetched right after this item's spread.
-template <int G>
-__global__ void __launch_bounds__(SW * FFTShape<G>::T, 1)
+template <int G, bool SEP>
+__global__ void __launch_bounds__(SW * FFTShape<G>::T, (SEP || G >= 1024) ? 1 : 2)
 k_adj_cols(DevPlan p, const float2* __restrict__ y, float2* __restrict__ H, int l0, int nb, int ystage, int stage_cap) {
   using F = FFTShape<G>;
   constexpr int P = F::P, Q = F::Q, T = F::T, N = G / 2, A = Q / T, B = P / T, S = G / SW;
@@ -609,7 +606,7 @@ k_adj_cols(DevPlan p, const float2* __restrict__ y, float2* __restrict__ H, int 
   // holds spread values and zeros: the stage-1 loads skip the row pairs the chunk's row mask marks
   // untouched and re-zero only the touched ones, and the stage-1 twiddles live in registers.
   // G = 1024 (two 128 KB buffers do not fit) exchanges through S and re-zeroes it in full.
-  constexpr bool SEP = AdjCols<G>::SEP;
+  static_assert(!SEP || G <= 512, "two 128 KB strips do not fit");
   extern __shared__ __align__(128) unsigned char smraw[];
   float2* stw = reinterpret_cast<float2*>(smraw);                 // twiddles (!SEP only)
   float2* strip = stw + (SEP ? 0 : G);

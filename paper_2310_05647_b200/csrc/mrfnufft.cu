@@ -73,6 +73,7 @@ struct mrf_plan_s {
   int device = 0;
   int bf = 1;               // frames per batch
   int nsm = 148;            // SMs of the device
+  bool adj_sep = false;      // k_adj_cols variant with the separate exchange buffer (one CTA per SM)
   int ystage = 0;           // bytes of y[fc] k_adj_cols stages in shared memory (M*8 if M even, M*8 <= kYBytes)
   int occ_fr0 = 1, occ_fr1 = 1, occ_fc = 1, occ_ac = 1, occ_ar = 1;   // resident CTAs per SM
   int fc_stage = 0, ac_stage = 0;   // chunk staging bytes of the column kernels
@@ -351,19 +352,21 @@ static mrf_status setup_kernels(mrf_plan_s* pl) {
   pl->col_smem = (int)s_col;
   pl->acol_smem = (int)s_acol;
   pl->fc_stage = (int)((s_col - fwd_cols_fixed<G>()) & ~size_t(15));
-  pl->ac_stage = (int)((s_acol - adj_cols_fixed<G>((size_t)pl->ystage)) & ~size_t(15));
+  pl->adj_sep = G <= 512 && actas == 1;
+  pl->ac_stage = (int)((s_acol - adj_cols_fixed<G>((size_t)pl->ystage, pl->adj_sep)) & ~size_t(15));
   CUDA_TRY(cudaFuncSetAttribute(k_fwd_rows<G, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s_fr0));
   CUDA_TRY(cudaFuncSetAttribute(k_fwd_rows<G, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s_fr1));
   CUDA_TRY(cudaFuncSetAttribute(k_adj_rows<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s_ar));
   CUDA_TRY(cudaFuncSetAttribute(k_fwd_cols<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s_col));
-  CUDA_TRY(cudaFuncSetAttribute(k_adj_cols<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s_acol));
+  auto adj_kernel = pl->adj_sep ? k_adj_cols<G, (G <= 512)> : k_adj_cols<G, false>;
+  CUDA_TRY(cudaFuncSetAttribute(adj_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s_acol));
   CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pl->occ_fr0, k_fwd_rows<G, 0>, kRowThreads, s_fr0));
   CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pl->occ_fr1, k_fwd_rows<G, 1>, kRowThreads, s_fr1));
   CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pl->occ_ar, k_adj_rows<G>, kRowThreads, s_ar));
   CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pl->occ_fc, k_fwd_cols<G>, ncol, s_col));
   CUDA_TRY(cudaFuncSetAttribute(k_toep_cols<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)toep_cols_smem<G>()));
   CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pl->occ_tc, k_toep_cols<G>, ncol, toep_cols_smem<G>()));
-  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pl->occ_ac, k_adj_cols<G>, ncol, s_acol));
+  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pl->occ_ac, adj_kernel, ncol, s_acol));
   if (pl->occ_fr0 < 1 || pl->occ_fr1 < 1 || pl->occ_ar < 1 || pl->occ_fc < 1 || pl->occ_ac < 1)
     return fail(MRF_EUNSUPPORTED, "a kernel does not fit on an SM");
   if (const char* cap = std::getenv("MRF_OCC_CAP")) {   // experiment knob: resident CTAs per SM
@@ -432,9 +435,10 @@ template <int G>
 static mrf_status launch_adj_cols(mrf_plan_s* pl, const float2* y, float2* H, int l0, int nb, cudaStream_t st) {
   const long long items = (long long)nb * pl->C * pl->S;
   const int ys = ((uintptr_t)y % 16 == 0) ? pl->ystage : 0;
-  const int stage = ys ? pl->ac_stage : (int)(((size_t)pl->acol_smem - adj_cols_fixed<G>(0)) & ~size_t(15));
+  const int stage = ys ? pl->ac_stage : (int)(((size_t)pl->acol_smem - adj_cols_fixed<G>(0, pl->adj_sep)) & ~size_t(15));
   ProfScope ps(pl, MRF_K_ADJ_COLS, st);
-  CUDA_TRY(launch_pdl(k_adj_cols<G>, pgrid(pl, pl->occ_ac, items), cols_threads<G>(), pl->acol_smem, st, pl->dp(), y, H,
+  auto adj_kernel = pl->adj_sep ? k_adj_cols<G, (G <= 512)> : k_adj_cols<G, false>;
+  CUDA_TRY(launch_pdl(adj_kernel, pgrid(pl, pl->occ_ac, items), cols_threads<G>(), pl->acol_smem, st, pl->dp(), y, H,
                       l0, nb, ys, stage));
   return MRF_OK;
 }

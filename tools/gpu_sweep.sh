@@ -1,6 +1,7 @@
-# Scratch GPU check used between kernel changes (run through gpurun): GPU parity, then
-# per-kernel-class timings of the MRF normal / forward and the stress forward (tools/op_breakdown.py).
+# Scratch GPU check used between kernel changes (run through gpurun).
 python -m pytest tests/test_gpu_parity.py -x -q -m gpu 2>&1 | tail -2
-python tools/op_breakdown.py --op normal --reps 10 2>&1 | tail -1
-MRF_LANES=1 python tools/op_breakdown.py --op forward --reps 10 2>&1 | tail -1
-python tools/op_breakdown.py --workload stress --op forward --reps 2 2>&1 | tail -1
+for A in 1 2; do
+MRF_ADJ_CTAS=$A python tools/op_breakdown.py --op normal --reps 10 2>&1 | tail -1
+MRF_ADJ_CTAS=$A MRF_LANES=1 python tools/op_breakdown.py --op adjoint --reps 10 2>&1 | tail -1
+MRF_ADJ_CTAS=$A python tools/op_breakdown.py --workload stress --op adjoint --reps 2 2>&1 | tail -1
+done
