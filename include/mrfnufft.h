@@ -193,6 +193,35 @@ mrf_status mrf_dict_match(mrf_dict dict, const void* x, long long V, int* index,
 
 mrf_status mrf_dict_destroy(mrf_dict dict);
 
+/* ---- subspace basis and the LLR outer step (lambda_1 = 0: the paper's LLR
+ * ablation; Eqs. (15), (17), (20), (21); readings 24, 25) ----------
+ *
+ * mrf_dict_basis: the fingerprint-subspace basis d of P_S(X) = X d^dagger d (Eq. 17, "approximated
+ * by the precomputed dictionary"): the leading right singular vectors of the dictionary keeping a
+ * fraction `energy` of ||D||_F^2, at most max_rank (<= 32) rows, computed on the device by subspace
+ * iteration (float64 accumulation).  *rank_out receives r.  Errors: MRF_EINVAL, MRF_ENOMEM,
+ * MRF_ECUDA, MRF_ENUMERIC.  mrf_dict_basis_copy writes the HOST [r][L] complex64 rows. */
+mrf_status mrf_dict_basis(mrf_dict dict, double energy, int max_rank, int* rank_out);
+mrf_status mrf_dict_basis_copy(mrf_dict dict, void* basis_out);
+
+/* An LLR operator on N x N images of the dictionary's L frames, p x p patches with stride s
+ * (11 x 11, 5), patch corners 0, s, 2s, ... and N - p.  Needs mrf_dict_basis; the
+ * basis is copied.  Errors: MRF_EINVAL, MRF_ENOMEM, MRF_ECUDA. */
+typedef struct mrf_llr_s* mrf_llr;
+mrf_status mrf_llr_create(mrf_dict dict, int N, int p, int s, mrf_llr* out);
+
+/* One iteration of Algorithm 1 with lambda_1 = 0 (DEVICE [L][N][N] complex64 arrays, 16-byte
+ * aligned, x_out may alias x):
+ *   Z = P_S(x - mu (A^H A x - rhs))             (Eq. 15; rhs = A^H b, A^H A from `plan`)
+ *   P_q = SVT_{1/beta}(Q_q(Z))                  (Eq. 20, per patch)
+ *   x_out = (Z + gamma Q^*(P)) / (1 + gamma c)   (Eq. 21, gamma = mu lambda2 beta, c = patch count)
+ * The SVT runs in subspace coordinates (Z lies in span(d): an r x r eigenproblem per patch).
+ * nuclear (nullable): sum over patches of ||Q_q(Z)||_* (synchronises the stream).
+ * Errors: MRF_EINVAL (mu <= 0, lambda2 < 0, beta <= 0, null, misaligned), errors of mrf_normal. */
+mrf_status mrf_llr_step(mrf_llr llr, mrf_plan plan, const void* x, const void* rhs, float mu, float lambda2,
+                        float beta, void* x_out, double* nuclear, void* stream);
+mrf_status mrf_llr_destroy(mrf_llr llr);
+
 /* enable != 0 brackets every subsequent tensor-core GEMM launch (k_dict_gemm) of mrf_dict_match
  * with CUDA events on its stream (and resets); the query synchronises them and returns the
  * summed milliseconds and the launch count. */

@@ -7,11 +7,11 @@ built library raises.
 """
 from .sharding import frame_shard  # noqa: F401
 
-__all__ = ["frame_shard", "Plan", "Dictionary", "MrfError", "lib", "nccl_comm_create", "nccl_comm_destroy"]
+__all__ = ["frame_shard", "Plan", "Dictionary", "LLR", "MrfError", "lib", "nccl_comm_create", "nccl_comm_destroy"]
 
 
 def __getattr__(name):
-    if name in ("Plan", "Dictionary", "MrfError", "lib", "nccl_comm_create", "nccl_comm_destroy"):
+    if name in ("Plan", "Dictionary", "LLR", "MrfError", "lib", "nccl_comm_create", "nccl_comm_destroy"):
         from . import binding
         return getattr(binding, name)
     raise AttributeError(name)

@@ -31,7 +31,9 @@ EXPORTED = [
     "mrf_plan_create", "mrf_forward", "mrf_adjoint", "mrf_normal", "mrf_dc_cg", "mrf_dc_cg_ex", "mrf_plan_destroy",
     "mrf_status_string", "mrf_last_error", "mrf_plan_device_bytes", "mrf_profile_enable",
     "mrf_profile_query", "mrf_nccl_get_unique_id", "mrf_nccl_comm_init", "mrf_nccl_comm_destroy",
-    "mrf_adjoint_dcf", "mrf_dcf_weights", "mrf_dict_create", "mrf_dict_match", "mrf_dict_destroy", "mrf_dict_profile", "mrf_dict_profile_query",
+    "mrf_adjoint_dcf", "mrf_dcf_weights", "mrf_dict_create", "mrf_dict_match", "mrf_dict_destroy",
+    "mrf_dict_profile", "mrf_dict_profile_query", "mrf_dict_basis", "mrf_dict_basis_copy", "mrf_llr_create",
+    "mrf_llr_step", "mrf_llr_destroy",
 ]
 
 
@@ -88,6 +90,11 @@ def _load() -> ctypes.CDLL:
         "mrf_dict_destroy": ([vp], ci),
         "mrf_dict_profile": ([vp, ci], ci),
         "mrf_dict_profile_query": ([vp, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_longlong)], ci),
+        "mrf_dict_basis": ([vp, ctypes.c_double, ci, ctypes.POINTER(ci)], ci),
+        "mrf_dict_basis_copy": ([vp, vp], ci),
+        "mrf_llr_create": ([vp, ci, ci, ci, ctypes.POINTER(vp)], ci),
+        "mrf_llr_step": ([vp, vp, vp, vp, cf, cf, cf, vp, ctypes.POINTER(ctypes.c_double), vp], ci),
+        "mrf_llr_destroy": ([vp], ci),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)
@@ -342,6 +349,14 @@ class Dictionary:
         _check(lib.mrf_dict_match(self._h, _ptr(x), V, _ptr(index), _ptr(pd), _ptr(params), ctypes.c_void_p(st)))
         return index, pd, params
 
+    def basis(self, energy: float = 0.9999, max_rank: int = 32) -> np.ndarray:
+        """Subspace basis of P_S (Eq. 17): [r][L] complex64 orthonormal rows (mrf_dict_basis)."""
+        r = ctypes.c_int()
+        _check(lib.mrf_dict_basis(self._h, ctypes.c_double(energy), int(max_rank), ctypes.byref(r)))
+        d = np.empty((r.value, self.L), dtype=np.complex64)
+        _check(lib.mrf_dict_basis_copy(self._h, d.ctypes.data_as(ctypes.c_void_p)))
+        return d
+
     def profile(self, enable: bool = True):
         _check(lib.mrf_dict_profile(self._h, int(enable)))
 
@@ -354,6 +369,46 @@ class Dictionary:
     def close(self):
         if getattr(self, "_h", None):
             lib.mrf_dict_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class LLR:
+    """The LLR outer step of Algorithm 1 with lambda_1 = 0 (include/mrfnufft.h mrf_llr_*).
+
+    Needs ``dictionary.basis(...)`` first.  ``step(plan, x, rhs, mu, lam2, beta)`` returns
+    (x_next, nuclear) for CUDA complex64 [L][N][N] x and rhs = A^H b.
+    """
+
+    def __init__(self, dictionary: "Dictionary", N: int, p: int = 11, s: int = 5):
+        h = ctypes.c_void_p()
+        _check(lib.mrf_llr_create(dictionary._h, int(N), int(p), int(s), ctypes.byref(h)))
+        self._h = h
+        self.N, self.L = int(N), dictionary.L
+
+    def step(self, plan: "Plan", x, rhs, mu: float = 1.0, lam2: float = 0.1, beta: float = 0.2, x_out=None,
+             nuclear: bool = True):
+        shape = (self.L, self.N, self.N)
+        x = _as_c64(x, shape, "x")
+        rhs = _as_c64(rhs, shape, "rhs")
+        if not (x.is_cuda and rhs.is_cuda):
+            raise TypeError("x and rhs must be CUDA tensors")
+        x_out = torch.empty_like(x) if x_out is None else _as_c64(x_out, shape, "x_out")
+        nuc = ctypes.c_double()
+        st = torch.cuda.current_stream(x.device).cuda_stream
+        _check(lib.mrf_llr_step(self._h, plan._h, _ptr(x), _ptr(rhs), ctypes.c_float(mu), ctypes.c_float(lam2),
+                                ctypes.c_float(beta), _ptr(x_out), ctypes.byref(nuc) if nuclear else None,
+                                ctypes.c_void_p(st)))
+        return x_out, (nuc.value if nuclear else None)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib.mrf_llr_destroy(self._h)
             self._h = None
 
     def __del__(self):

@@ -9,8 +9,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libmrfnufft.so")
-SOURCES = [os.path.join(CSRC, "mrfnufft.cu"), os.path.join(CSRC, "dict.cu"), os.path.join(CSRC, "nccl_dl.cpp")]
-DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("gridding.cuh", "cg.cuh", "fft.cuh", "match.cuh", "nccl_dl.h", "status.h")] + [
+SOURCES = [os.path.join(CSRC, f) for f in ("mrfnufft.cu", "dict.cu", "llr.cu", "nccl_dl.cpp")]
+DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("gridding.cuh", "cg.cuh", "fft.cuh", "match.cuh", "llr.cuh", "dict_internal.h", "nccl_dl.h", "status.h")] + [
     os.path.join(ROOT, "include", "mrfnufft.h")]
 
 NVCC_FLAGS = [

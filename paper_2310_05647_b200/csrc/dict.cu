@@ -8,33 +8,19 @@
 
 #include <algorithm>
 #include <cmath>
+#include <complex>
 #include <cstring>
 #include <string>
 #include <vector>
 
 #include "../../include/mrfnufft.h"
+#include "dict_internal.h"
+#include "llr.cuh"
 #include "match.cuh"
 #include "status.h"
 
 using namespace mrf;
 
-struct mrf_dict_s {
-  int K = 0, L = 0, P = 0, device = 0;
-  int KD = 0, NP = 0;            // fp16 row length (2 L padded to 64), GEMM rows (2 K padded to 256)
-  __half* dp = nullptr;          // [NP][KD] atom rows (re/im rotated, scaled by 1 / m_k)
-  float* w2 = nullptr;           // [NP / 2] (m_k / ||d_k||)^2, 0 for padding
-  float* n2inv = nullptr;        // [K] 1 / ||d_k||^2 (0 for a zero atom)
-  float2* atoms = nullptr;       // [K][L] complex64 (for the exact pd)
-  float* lut = nullptr;          // [K][P]
-  __half* xp = nullptr;          // workspace [vcap][KD]
-  float* xs = nullptr;           // [vcap] per-voxel scale
-  unsigned long long* best = nullptr;   // [vcap] packed (score, ~atom) running maxima
-  long long vcap = 0;
-  CUtensorMap tmd;
-  bool prof = false;             // CUDA events around the tensor-core GEMM (mrf_dict_profile)
-  std::vector<cudaEvent_t> ev;   // pairs
-  size_t ev_used = 0;
-};
 
 static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -67,7 +53,7 @@ static void dict_free(mrf_dict_s* d) {
   if (!d) return;
   cudaSetDevice(d->device);
   for (void* p : {(void*)d->dp, (void*)d->w2, (void*)d->n2inv, (void*)d->atoms, (void*)d->lut, (void*)d->xp,
-                  (void*)d->xs, (void*)d->best})
+                  (void*)d->xs, (void*)d->best, (void*)d->basis})
     if (p) cudaFree(p);
   delete d;
 }
@@ -94,6 +80,7 @@ mrf_status mrf_dict_create(const void* atoms, const float* lut, int K, int L, in
       n2 += (double)v.x * v.x + (double)v.y * v.y;
       m = std::max(m, (double)std::max(std::fabs(v.x), std::fabs(v.y)));
     }
+    d->fro2 += n2;
     if (n2 <= 0.0) continue;   // zero atom: w2 = 0, never preferred over a non-zero one
     n2inv[k] = (float)(1.0 / n2);
     w2[k] = (float)(m * m / n2);
@@ -185,6 +172,159 @@ mrf_status mrf_dict_match(mrf_dict d, const void* x, long long V, int* index, fl
   dm::k_dict_fix<<<(unsigned)((V + 31) / 32), 256, 0, st>>>(xf, d->atoms, d->n2inv, d->lut, d->P, d->L, (int)V,
                                                                d->best, index, pd, params);
   MRF_TRY(check_launch("k_dict_fix"));
+  return MRF_OK;
+}
+
+// ---------------------------------------------------------------- subspace basis (Eq. 17, reading 24)
+// Leading right singular vectors of D by subspace iteration on D^H D (GEMMs on the device,
+// double accumulation; the k-column re-orthonormalisation (Gram-Schmidt twice) and the k x k
+// Rayleigh-Ritz eigenproblem in float64 on the host), then the rank that keeps `energy` of ||D||_F^2.
+static void host_jacobi_eig(int n, std::vector<std::complex<double>>& H, std::vector<std::complex<double>>& W,
+                            std::vector<double>& lam) {
+  W.assign((size_t)n * n, 0.0);
+  for (int i = 0; i < n; ++i) W[(size_t)i * n + i] = 1.0;
+  for (int sweep = 0; sweep < 60; ++sweep) {
+    double off = 0.0, tot = 0.0;
+    for (int i = 0; i < n; ++i)
+      for (int j = 0; j < n; ++j) {
+        const double m2 = std::norm(H[(size_t)i * n + j]);
+        tot += m2;
+        if (i != j) off += m2;
+      }
+    if (!(off > 1e-28 * tot)) break;
+    for (int p = 0; p < n - 1; ++p)
+      for (int q = p + 1; q < n; ++q) {
+        const std::complex<double> hpq = H[(size_t)p * n + q];
+        const double mag = std::abs(hpq);
+        if (!(mag > 1e-300)) continue;
+        const double a = H[(size_t)p * n + p].real(), b = H[(size_t)q * n + q].real();
+        const double kap = (a - b) / (2.0 * mag);
+        const double t = (kap >= 0.0 ? 1.0 : -1.0) / (std::fabs(kap) + std::sqrt(1.0 + kap * kap));
+        const double c = 1.0 / std::sqrt(1.0 + t * t), sn = t * c;
+        const std::complex<double> e = hpq / mag;
+        for (int k = 0; k < n; ++k) {   // columns of H and W
+          const std::complex<double> hp = H[(size_t)k * n + p], hq = H[(size_t)k * n + q];
+          H[(size_t)k * n + p] = c * hp + sn * hq * std::conj(e);
+          H[(size_t)k * n + q] = c * hq - sn * hp * e;
+          const std::complex<double> wp = W[(size_t)k * n + p], wq = W[(size_t)k * n + q];
+          W[(size_t)k * n + p] = c * wp + sn * wq * std::conj(e);
+          W[(size_t)k * n + q] = c * wq - sn * wp * e;
+        }
+        for (int k = 0; k < n; ++k) {   // rows of H
+          const std::complex<double> rp = H[(size_t)p * n + k], rq = H[(size_t)q * n + k];
+          H[(size_t)p * n + k] = c * rp + sn * rq * e;
+          H[(size_t)q * n + k] = c * rq - sn * rp * std::conj(e);
+        }
+      }
+  }
+  lam.resize(n);
+  for (int i = 0; i < n; ++i) lam[i] = H[(size_t)i * n + i].real();
+}
+
+extern "C" mrf_status mrf_dict_basis(mrf_dict d, double energy, int max_rank, int* rank_out) {
+  if (!d || !rank_out || !(energy > 0.0 && energy <= 1.0) || max_rank < 1 || max_rank > llr::RMAX)
+    return fail(MRF_EINVAL, "mrf_dict_basis: invalid arguments (0 < energy <= 1, 1 <= max_rank <= 32)");
+  if (!(d->fro2 > 0.0)) return fail(MRF_EINVAL, "mrf_dict_basis: all-zero dictionary");
+  CUDA_TRY(cudaSetDevice(d->device));
+  const int K = d->K, L = d->L, k = std::min({max_rank + 16, 64, K, L});
+  float2 *Q = nullptr, *B = nullptr;
+  double2* S = nullptr;
+  auto cleanup = [&]() {
+    for (void* p : {(void*)Q, (void*)B, (void*)S})
+      if (p) cudaFree(p);
+  };
+  if (cudaMalloc((void**)&Q, (size_t)L * k * sizeof(float2)) != cudaSuccess ||
+      cudaMalloc((void**)&B, (size_t)K * k * sizeof(float2)) != cudaSuccess ||
+      cudaMalloc((void**)&S, (size_t)k * k * sizeof(double2)) != cudaSuccess) {
+    cleanup();
+    return fail(MRF_ENOMEM, "mrf_dict_basis: workspace allocation failed");
+  }
+  std::vector<float2> q0((size_t)L * k);
+  uint64_t st = 0x9E3779B97F4A7C15ull;   // deterministic start block (xorshift)
+  for (auto& v : q0) {
+    auto u = [&]() { st ^= st << 13; st ^= st >> 7; st ^= st << 17; return (double)(st >> 11) / 9007199254740992.0 - 0.5; };
+    v = make_float2((float)u(), (float)u());
+  }
+  const dim3 blk(16, 16);
+  auto grid = [](int M, int N) { return dim3((unsigned)((N + 15) / 16), (unsigned)((M + 15) / 16)); };
+  std::vector<double2> Sh((size_t)k * k);
+  std::vector<float2> Qh((size_t)L * k);
+  std::vector<std::complex<double>> Qd((size_t)L * k);
+  auto orthonormalize = [&]() -> mrf_status {   // Q <- orth(Q): modified Gram-Schmidt, twice, float64 (host)
+    CUDA_TRY(cudaMemcpy(Qh.data(), Q, Qh.size() * sizeof(float2), cudaMemcpyDeviceToHost));
+    for (size_t i = 0; i < Qd.size(); ++i) Qd[i] = std::complex<double>(Qh[i].x, Qh[i].y);
+    for (int j = 0; j < k; ++j) {
+      for (int pass = 0; pass < 2; ++pass)
+        for (int i = 0; i < j; ++i) {
+          std::complex<double> dot = 0.0;
+          for (int l = 0; l < L; ++l) dot += std::conj(Qd[(size_t)l * k + i]) * Qd[(size_t)l * k + j];
+          for (int l = 0; l < L; ++l) Qd[(size_t)l * k + j] -= dot * Qd[(size_t)l * k + i];
+        }
+      double nrm = 0.0;
+      for (int l = 0; l < L; ++l) nrm += std::norm(Qd[(size_t)l * k + j]);
+      nrm = std::sqrt(nrm);
+      if (!(nrm > 1e-300)) {   // numerically dependent column: restart it from a fixed vector
+        for (int l = 0; l < L; ++l) Qd[(size_t)l * k + j] = (l % (j + 2) == 0) ? 1.0 : 0.0;
+        --j;
+        continue;
+      }
+      for (int l = 0; l < L; ++l) Qd[(size_t)l * k + j] /= nrm;
+    }
+    for (size_t i = 0; i < Qd.size(); ++i) Qh[i] = make_float2((float)Qd[i].real(), (float)Qd[i].imag());
+    CUDA_TRY(cudaMemcpy(Q, Qh.data(), Qh.size() * sizeof(float2), cudaMemcpyHostToDevice));
+    return MRF_OK;
+  };
+  mrf_status s = MRF_OK;
+  if (cudaMemcpy(Q, q0.data(), q0.size() * sizeof(float2), cudaMemcpyHostToDevice) != cudaSuccess) s = MRF_ECUDA;
+  for (int it = 0; s == MRF_OK && it < 40; ++it) {
+    llr::k_cgemm<<<grid(K, k), blk>>>(d->atoms, L, 1, 0, Q, k, 1, K, k, L, B, nullptr);      // B = D Q
+    llr::k_cgemm<<<grid(L, k), blk>>>(d->atoms, 1, L, 1, B, k, 1, L, k, K, Q, nullptr);      // Q = D^H B
+    s = orthonormalize();
+  }
+  if (s != MRF_OK) {
+    cleanup();
+    return s == MRF_ECUDA ? fail(MRF_ECUDA, "mrf_dict_basis: copy failed") : s;
+  }
+  // Rayleigh-Ritz: T = (D Q)^H (D Q) = W diag(lam) W^H
+  llr::k_cgemm<<<grid(K, k), blk>>>(d->atoms, L, 1, 0, Q, k, 1, K, k, L, B, nullptr);
+  llr::k_cgemm<<<grid(k, k), blk>>>(B, 1, k, 1, B, k, 1, k, k, K, nullptr, S);
+  cudaError_t e = cudaMemcpy(Sh.data(), S, Sh.size() * sizeof(double2), cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess) e = cudaMemcpy(Qh.data(), Q, Qh.size() * sizeof(float2), cudaMemcpyDeviceToHost);
+  cleanup();
+  if (e != cudaSuccess) return fail(MRF_ECUDA, std::string("mrf_dict_basis: ") + cudaGetErrorString(e));
+  std::vector<std::complex<double>> T((size_t)k * k), Wv;
+  for (size_t i = 0; i < T.size(); ++i) T[i] = std::complex<double>(Sh[i].x, Sh[i].y);
+  std::vector<double> lam;
+  host_jacobi_eig(k, T, Wv, lam);
+  std::vector<int> ord(k);
+  for (int i = 0; i < k; ++i) ord[i] = i;
+  std::sort(ord.begin(), ord.end(), [&](int a, int b) { return lam[a] > lam[b]; });
+  int r = 0;
+  double acc = 0.0;
+  while (r < std::min(max_rank, k) && acc < energy * d->fro2) acc += lam[ord[r++]];
+  // basis rows d_i = conj(Q w_i)^T  (right singular vectors as rows, P_S(x) = x d^H d)
+  d->basis_h.assign((size_t)r * L, make_float2(0.f, 0.f));
+  for (int i = 0; i < r; ++i)
+    for (int l = 0; l < L; ++l) {
+      std::complex<double> v = 0.0;
+      for (int j = 0; j < k; ++j)
+        v += std::complex<double>(Qh[(size_t)l * k + j].x, Qh[(size_t)l * k + j].y) * Wv[(size_t)j * k + ord[i]];
+      d->basis_h[(size_t)i * L + l] = make_float2((float)v.real(), (float)-v.imag());
+    }
+  if (d->basis) cudaFree(d->basis);
+  d->basis = nullptr;
+  d->rank = 0;
+  CUDA_TRY(cudaMalloc((void**)&d->basis, d->basis_h.size() * sizeof(float2)));
+  CUDA_TRY(cudaMemcpy(d->basis, d->basis_h.data(), d->basis_h.size() * sizeof(float2), cudaMemcpyHostToDevice));
+  d->rank = r;
+  *rank_out = r;
+  return MRF_OK;
+}
+
+extern "C" mrf_status mrf_dict_basis_copy(mrf_dict d, void* out) {
+  if (!d || !out) return fail(MRF_EINVAL, "mrf_dict_basis_copy: null argument");
+  if (!d->rank) return fail(MRF_EINVAL, "mrf_dict_basis_copy: no basis (call mrf_dict_basis)");
+  std::memcpy(out, d->basis_h.data(), d->basis_h.size() * sizeof(float2));
   return MRF_OK;
 }
 

@@ -10,6 +10,7 @@
 namespace mrf {
 mrf_status fail(mrf_status s, const std::string& msg);
 mrf_status check_launch(const char* what);   // cudaGetLastError after a launch
+void plan_dims(mrf_plan plan, int* N, int* L, int* C, int* device);   // mrfnufft.cu
 }  // namespace mrf
 
 #define CUDA_TRY(expr)                                                                           \

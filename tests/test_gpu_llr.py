@@ -1,0 +1,90 @@
+"""GPU parity of the LLR outer step (SURVEY.md §8(f) f2 with lambda_1 = 0) against the oracle.
+
+PAPER.md:217-264 Eqs. (15), (17), (20), (21); readings 24, 25.  The library computes the
+subspace basis by subspace iteration and runs the patch SVT in subspace coordinates; the oracle
+uses a full SVD of the dictionary and of every p^2 x L patch Casorati matrix in the time domain.
+"""
+import numpy as np
+import pytest
+import torch
+
+import synth
+import synth.dictionary as sd
+from oracle import llr as ol
+from oracle import nufft as on
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def binding():
+    from paper_2310_05647_b200 import binding as b
+    return b
+
+
+def rel(a, b):
+    return float(np.linalg.norm(np.asarray(a) - np.asarray(b)) / np.linalg.norm(np.asarray(b)))
+
+
+def projector(d):
+    d = np.asarray(d, np.complex128)
+    return np.conj(d).T @ d
+
+
+def test_basis_matches_the_svd(binding):
+    D = sd.surrogate_dictionary(200)
+    dic = binding.Dictionary(D)
+    dg = dic.basis(0.9999, 32)
+    do = ol.basis(D, 0.9999, 32)
+    assert dg.shape == do.shape
+    assert np.allclose(dg @ np.conj(dg).T, np.eye(dg.shape[0]), atol=1e-5)
+    assert rel(projector(dg), projector(do)) <= 1e-5
+    dic.close()
+
+
+@pytest.mark.parametrize("N,L,p,s", [(64, 100, 11, 5), (32, 60, 7, 3)])
+def test_llr_step_against_the_oracle(binding, N, L, p, s):
+    D = sd.surrogate_dictionary(L)
+    M, R, W = 512, 10, 6
+    traj = synth.spiral_trajectory(M, R, 8, 1.5)
+    x_true = synth.rank5_images(N, L, range(L), 7)
+    y = on.forward(x_true, traj, None, W)
+    rhs = on.adjoint(y, traj, None, N, W)                 # A^H b; X^0 = A^H b (Algorithm 1)
+    mu, lam2, beta = 1.0, 0.1, 0.2
+    d_o = ol.basis(D, 0.9999, 32)
+    normal = lambda v: on.normal(v, traj, None, W)
+    X_ref, Z_ref = ol.llr_step(rhs, rhs, normal, d_o, mu, lam2, beta, p, s)
+    _, nuc_ref = ol.llr_prox(Z_ref, 1.0 / beta, mu * lam2 * beta, p, s)
+
+    dic = binding.Dictionary(D)
+    dic.basis(0.9999, 32)
+    op = binding.LLR(dic, N, p, s)
+    pl = binding.Plan(N, traj, L, W=W)
+    xd = torch.from_numpy(rhs.astype(np.complex64)).cuda()
+    x_next, nuc = op.step(pl, xd, xd, mu, lam2, beta)
+    torch.cuda.synchronize()
+    assert rel(x_next.cpu().numpy(), X_ref) <= 1e-4
+    assert abs(nuc - nuc_ref) / nuc_ref <= 1e-4
+    # the thresholding is active: some but not all singular values survive
+    assert 0.0 < rel(X_ref, Z_ref) < 1.0
+    x_alias, _ = op.step(pl, xd, xd, mu, lam2, beta, x_out=xd.clone())
+    torch.cuda.synchronize()
+    pl.close()
+    op.close()
+    dic.close()
+
+
+def test_invalid_llr_calls(binding):
+    D = sd.surrogate_dictionary(20)
+    dic = binding.Dictionary(D)
+    with pytest.raises(binding.MrfError):
+        binding.LLR(dic, 32)                                   # no basis yet
+    dic.basis()
+    op = binding.LLR(dic, 32)
+    pl = binding.Plan(64, synth.spiral_trajectory(128, 2, 4, 1.5), 20)   # N differs
+    x = torch.zeros((20, 32, 32), dtype=torch.complex64, device="cuda")
+    with pytest.raises(Exception):
+        op.step(pl, x, x)
+    pl.close()
+    op.close()
+    dic.close()
