@@ -47,6 +47,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-toeplitz", action="store_true")
     ap.add_argument("--no-match", action="store_true", help="skip the dictionary-matching (Phi_D) measurement")
+    ap.add_argument("--no-llr", action="store_true", help="skip the LLR outer-step measurement")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target CPU work of the oracle sample")
     ap.add_argument("--batch-frames", type=int, default=0)
@@ -401,6 +402,29 @@ def run_ours(args):
                          "(PAPER.md:319 grid, surrogate fingerprints)"}
         dic.close()
 
+    # ---------------------------------------------------------------- LLR outer step (lambda_1 = 0)
+    llr_res = None
+    if not args.no_llr and world == 1 and cfg.C == 1:
+        import synth.dictionary as sdict
+        grid = sdict.t1t2_grid()
+        dic = binding.Dictionary(sdict.surrogate_dictionary(cfg.L, grid), grid, device=local)
+        t0 = time.perf_counter()
+        d_basis = dic.basis(0.9999, 32)
+        basis_ms = (time.perf_counter() - t0) * 1e3
+        op = binding.LLR(dic, cfg.N, 11, 5)
+        rhs_l = plan.adjoint(y)
+        xl = torch.empty_like(xbuf)
+        ms_llr = time_op(lambda: op.step(plan, xbuf, rhs_l, 1.0, 0.1, 0.2, x_out=xl, nuclear=False), 5)
+        nc = len(range(0, cfg.N - 11 + 1, 5)) + (0 if (cfg.N - 11) % 5 == 0 else 1)
+        llr_res = {"ms_per_step": ms_llr, "ms_normal_inside": ms_normal, "rank": int(d_basis.shape[0]),
+                   "patches": nc * nc, "basis_ms": basis_ms,
+                   "note": "mrf_llr_step: Z = P_S(X - mu(A^H A X - A^H b)), per-patch SVT (11x11, stride 5, "
+                           "tau = 1/beta = 5) in subspace coordinates, overlap-exact X update; mu = 1, "
+                           "lambda_2 = 0.1, beta = 1/5 (PAPER.md:304); basis from the synthetic dictionary"}
+        op.close()
+        dic.close()
+        del xl, rhs_l
+
     # ---------------------------------------------------------------- e2e through the C-ABI, host buffers
     e2e = None
     if not args.no_e2e:
@@ -486,7 +510,7 @@ def run_ours(args):
         "hbm": {"algorithmic_bytes_per_step": hbm_bytes, "achieved_GBs": hbm_achieved, "peak_GBs": hbm_peak,
                 "frac": hbm_achieved / hbm_peak},
         "cufft_ref_ms_fft2_LC": cufft_ms,
-        "roofline": roofline, "roofline_AHA": roofline_aha, "toeplitz": toep, "match": match, "kernel_share": share, "kernel_share_of_kernel_time": share_k, "gpu_launches": gpu_launches,
+        "roofline": roofline, "roofline_AHA": roofline_aha, "toeplitz": toep, "match": match, "llr": llr_res, "kernel_share": share, "kernel_share_of_kernel_time": share_k, "gpu_launches": gpu_launches,
         "clocks": clk, "e2e": e2e, "cpu_baseline": cpu,
     }
     if rank == 0:

@@ -18,7 +18,7 @@ using namespace mrf;
 
 struct mrf_llr_s {
   int N = 0, L = 0, p = 0, s = 0, r = 0, nc = 0, device = 0;
-  float2* d = nullptr;        // [r][L] basis rows (copy of the dictionary's)
+  float2* dT = nullptr;       // [L][R] transposed basis, rows zero-padded to R = 16 or 32
   int* corners = nullptr;     // [nc]
   float2* Y = nullptr;        // [N*N][r] coefficients of Z
   float2* P = nullptr;        // [nc*nc][p*p][r] thresholded patch coefficients
@@ -30,14 +30,12 @@ struct mrf_llr_s {
 static void llr_free(mrf_llr_s* h) {
   if (!h) return;
   cudaSetDevice(h->device);
-  for (void* v : {(void*)h->d, (void*)h->corners, (void*)h->Y, (void*)h->P, (void*)h->nx, (void*)h->nuc})
+  for (void* v : {(void*)h->dT, (void*)h->corners, (void*)h->Y, (void*)h->P, (void*)h->nx, (void*)h->nuc})
     if (v) cudaFree(v);
   delete h;
 }
 
-static size_t svt_smem(int p, int r) {   // H, W (double2), M (float2), Yq (float2)
-  return 2 * (size_t)llr::RMAX * llr::RMAX * sizeof(double2) + ((size_t)llr::RMAX * llr::RMAX + (size_t)p * p * r) * sizeof(float2);
-}
+static size_t svt_smem(int p, int r) { return (llr::kSvtThreads / 32) * llr::svt_warp_bytes(p, r); }
 
 extern "C" {
 
@@ -55,7 +53,8 @@ mrf_status mrf_llr_create(mrf_dict dict, int N, int p, int s, mrf_llr* out) {
   h->nc = (int)c.size();
   const size_t V = (size_t)N * N, nq = (size_t)h->nc * h->nc;
   h->nuc_h.resize(nq);
-  bool ok = cudaMalloc((void**)&h->d, (size_t)h->r * h->L * sizeof(float2)) == cudaSuccess &&
+  const int R = h->r <= 16 ? 16 : 32;
+  bool ok = cudaMalloc((void**)&h->dT, (size_t)R * h->L * sizeof(float2)) == cudaSuccess &&
             cudaMalloc((void**)&h->corners, c.size() * sizeof(int)) == cudaSuccess &&
             cudaMalloc((void**)&h->Y, V * h->r * sizeof(float2)) == cudaSuccess &&
             cudaMalloc((void**)&h->P, nq * p * p * h->r * sizeof(float2)) == cudaSuccess &&
@@ -65,10 +64,13 @@ mrf_status mrf_llr_create(mrf_dict dict, int N, int p, int s, mrf_llr* out) {
     llr_free(h);
     return fail(MRF_ENOMEM, "mrf_llr_create: device allocation failed");
   }
-  cudaError_t e = cudaMemcpy(h->d, dict->basis, (size_t)h->r * h->L * sizeof(float2), cudaMemcpyDeviceToDevice);
+  std::vector<float2> dT((size_t)R * h->L, make_float2(0.f, 0.f));   // [L][R] from the [r][L] rows
+  for (int i = 0; i < h->r; ++i)
+    for (int l = 0; l < h->L; ++l) dT[(size_t)l * R + i] = dict->basis_h[(size_t)i * h->L + l];
+  cudaError_t e = cudaMemcpy(h->dT, dT.data(), dT.size() * sizeof(float2), cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMemcpy(h->corners, c.data(), c.size() * sizeof(int), cudaMemcpyHostToDevice);
   if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(llr::k_llr_svt, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)svt_smem(p, llr::RMAX));
+    e = cudaFuncSetAttribute(llr::k_llr_svt, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)svt_smem(p, h->r));
   if (e != cudaSuccess) {
     llr_free(h);
     return fail(MRF_ECUDA, std::string("mrf_llr_create: ") + cudaGetErrorString(e));
@@ -94,21 +96,24 @@ mrf_status mrf_llr_step(mrf_llr h, mrf_plan plan, const void* x, const void* rhs
   // A^H A x (the plan checks that x has its shape: [L][N][N] device memory)
   MRF_TRY(mrf_normal(plan, x, h->nx, 0.f, stream));
   const float2* xf = reinterpret_cast<const float2*>(x);
-  const unsigned gv = (unsigned)((V + 255) / 256);
+  const unsigned gv = (unsigned)((V + 31) / 32);   // 32 voxels x 8 frame groups per block
   if (h->r <= 16)
-    llr::k_llr_coef<16><<<gv, 256, 0, st>>>(xf, h->nx, (const float2*)rhs, h->d, h->r, h->L, V, mu, h->Y);
+    llr::k_llr_coef<16><<<gv, 32 * llr::coef_groups<16>(), 0, st>>>(xf, h->nx, (const float2*)rhs, h->dT, h->r,
+                                                                       h->L, V, mu, h->Y);
   else
-    llr::k_llr_coef<32><<<gv, 256, 0, st>>>(xf, h->nx, (const float2*)rhs, h->d, h->r, h->L, V, mu, h->Y);
+    llr::k_llr_coef<32><<<gv, 32 * llr::coef_groups<32>(), 0, st>>>(xf, h->nx, (const float2*)rhs, h->dT, h->r,
+                                                                       h->L, V, mu, h->Y);
   MRF_TRY(check_launch("k_llr_coef"));
-  llr::k_llr_svt<<<(unsigned)nq, llr::kSvtThreads, svt_smem(h->p, h->r), st>>>(h->Y, h->corners, h->nc, h->N, h->p,
-                                                                              h->r, 1.f / beta, h->P, h->nuc);
+  const int ppb = llr::kSvtThreads / 32;
+  llr::k_llr_svt<<<(unsigned)((nq + ppb - 1) / ppb), llr::kSvtThreads, svt_smem(h->p, h->r), st>>>(
+      h->Y, h->corners, h->nc, h->N, h->p, h->r, 1.f / beta, nq, h->P, h->nuc);
   MRF_TRY(check_launch("k_llr_svt"));
   const float gamma = mu * lambda2 * beta;
   if (h->r <= 16)
-    llr::k_llr_update<16><<<gv, 256, 0, st>>>(h->Y, h->P, h->corners, h->nc, h->N, h->p, h->r, h->d, h->L, gamma,
+    llr::k_llr_update<16><<<gv, 256, 0, st>>>(h->Y, h->P, h->corners, h->nc, h->N, h->p, h->r, h->dT, h->L, gamma,
                                               (float2*)x_out);
   else
-    llr::k_llr_update<32><<<gv, 256, 0, st>>>(h->Y, h->P, h->corners, h->nc, h->N, h->p, h->r, h->d, h->L, gamma,
+    llr::k_llr_update<32><<<gv, 256, 0, st>>>(h->Y, h->P, h->corners, h->nc, h->N, h->p, h->r, h->dT, h->L, gamma,
                                               (float2*)x_out);
   MRF_TRY(check_launch("k_llr_update"));
   if (nuclear) {   // sum over patches in a fixed order (synchronises the stream)

@@ -9,7 +9,7 @@
 // coefficients Y = Z d^dagger (V x r) a patch Casorati matrix is Q_q(Z) = Y_q d and
 // SVT(Q_q(Z)) = SVT(Y_q) d = Y_q W diag(max(1 - tau / sigma, 0)) W^H d with Y_q^H Y_q = W S^2 W^H:
 // the p^2 x L SVD becomes an r x r Hermitian eigenproblem per patch (r = 13 for the MRF
-// dictionary at 0.9999 energy), solved by cyclic complex Jacobi (float64) in one warp.
+// dictionary at 0.9999 energy), solved by one-sided (Hestenes) Jacobi on Y_q in one warp.
 //
 //   k_llr_coef   : Y[v][i] = sum_l conj(d[i][l]) (x - mu (n - rhs))[l][v]   (reads 3 image arrays)
 //   k_llr_svt    : per patch: Gram, Jacobi, M = W f W^H, P_q = Y_q M, sum sigma (nuclear norm)
@@ -24,209 +24,229 @@ namespace mrf {
 namespace llr {
 
 constexpr int RMAX = 32;      // largest supported subspace rank
-constexpr int kSvtThreads = 128;
+constexpr int kSvtThreads = 128;   // 4 patches (warps) per block
 
 __device__ __forceinline__ float2 cconjmul(float2 a, float2 b) {   // conj(a) * b
   return make_float2(fmaf(a.x, b.x, a.y * b.y), fmaf(a.x, b.y, -a.y * b.x));
 }
 
-// Y[v][i] for i < r, v < V.  d: [r][L] complex (orthonormal rows).  One thread per voxel;
-// R = compile-time bound on r (16 or 32).
+// Y[v][i] for i < r, v < V.  dT: [L][R] complex transpose of d (rows padded to R with zeros), so
+// one frame's R coefficients are R/2 16-byte loads, broadcast across a warp.  Block = 32 voxels
+// (lanes) x NG warps; warp w sums the frames l = w (mod NG), the NG partial sums are added in a
+// fixed order through shared memory.
 template <int R>
-__global__ void __launch_bounds__(256) k_llr_coef(const float2* __restrict__ x, const float2* __restrict__ nx,
-                                                  const float2* __restrict__ rhs, const float2* __restrict__ d,
+__host__ __device__ constexpr int coef_groups() { return R <= 16 ? 8 : 4; }   // frame groups (warps) per block
+template <int R>
+__global__ void __launch_bounds__(32 * coef_groups<R>()) k_llr_coef(const float2* __restrict__ x, const float2* __restrict__ nx,
+                                                  const float2* __restrict__ rhs, const float2* __restrict__ dT,
                                                   int r, int L, int V, float mu, float2* __restrict__ Y) {
-  const int v = blockIdx.x * blockDim.x + threadIdx.x;
-  if (v >= V) return;
+  constexpr int NG = coef_groups<R>();
+  __shared__ float2 part[NG][R][33];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int v = blockIdx.x * 32 + lane;
   float2 acc[R];
 #pragma unroll
   for (int i = 0; i < R; ++i) acc[i] = make_float2(0.f, 0.f);
-  for (int l = 0; l < L; ++l) {
-    const size_t o = (size_t)l * V + v;
-    const float2 a = __ldg(x + o), n = __ldg(nx + o), b = __ldg(rhs + o);
-    const float2 w = make_float2(a.x - mu * (n.x - b.x), a.y - mu * (n.y - b.y));
+  const float4* d4 = reinterpret_cast<const float4*>(dT);
+  if (v < V)
+    for (int l = w; l < L; l += NG) {
+      const size_t o = (size_t)l * V + v;
+      const float2 a = __ldg(x + o), n = __ldg(nx + o), b = __ldg(rhs + o);
+      const float2 wv = make_float2(a.x - mu * (n.x - b.x), a.y - mu * (n.y - b.y));
 #pragma unroll
-    for (int i = 0; i < R; ++i)
-      if (i < r) {
-        const float2 di = __ldg(d + (size_t)i * L + l);   // same address across the warp: broadcast
-        const float2 t = cconjmul(di, w);
-        acc[i].x += t.x;
-        acc[i].y += t.y;
+      for (int i2 = 0; i2 < R / 2; ++i2) {
+        const float4 dd = __ldg(d4 + (size_t)l * (R / 2) + i2);
+        const float2 t0 = cconjmul(make_float2(dd.x, dd.y), wv), t1 = cconjmul(make_float2(dd.z, dd.w), wv);
+        acc[2 * i2].x += t0.x; acc[2 * i2].y += t0.y;
+        acc[2 * i2 + 1].x += t1.x; acc[2 * i2 + 1].y += t1.y;
       }
-  }
+    }
 #pragma unroll
-  for (int i = 0; i < R; ++i)
-    if (i < r) Y[(size_t)v * r + i] = acc[i];
+  for (int i = 0; i < R; ++i) part[w][i][lane] = acc[i];
+  __syncthreads();
+  for (int e = threadIdx.x; e < 32 * r; e += blockDim.x) {
+    const int i = e / 32, ln = e % 32;
+    const int vv = blockIdx.x * 32 + ln;
+    float2 t = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int g = 0; g < NG; ++g) { t.x += part[g][i][ln].x; t.y += part[g][i][ln].y; }
+    if (vv < V) Y[(size_t)vv * r + i] = t;
+  }
 }
 
-// One patch per block.  corners: [nc] top-left coordinates (same list for rows and columns);
-// patch q = (qy, qx) with qy, qx < nc.  P: [nq][p*p][r] output coefficients; nuc: [nq] sum sigma.
+// One patch per warp, kSvtThreads / 32 patches per block.  corners: [nc] top-left coordinates
+// (same list for rows and columns); patch q = (qy, qx).  P: [nq][p*p][r] output coefficients;
+// nuc: [nq] sum sigma.  The SVD of the p^2 x r coefficient block Y_q is one-sided (Hestenes)
+// Jacobi: column pairs of Y_q are rotated until mutually orthogonal, accumulating V, so that
+// Y_q V = Yhat has orthogonal columns of norms sigma_j (float32 keeps the small sigma to relative
+// accuracy: no squared Gram); SVT(Y_q) = Yhat diag(max(1 - tau / sigma, 0)) V^H.
+// Shared memory per warp: svt_warp_bytes(p, r).
+__host__ __device__ constexpr size_t svt_warp_bytes(int p, int r) { return ((size_t)p * p * r + (size_t)r * r) * 8; }
+
 static __global__ void __launch_bounds__(kSvtThreads) k_llr_svt(const float2* __restrict__ Y, const int* __restrict__ corners,
-                                                          int nc, int N, int p, int r, float tau,
+                                                          int nc, int N, int p, int r, float tau, int nq,
                                                           float2* __restrict__ P, double* __restrict__ nuc) {
   extern __shared__ __align__(16) unsigned char llr_raw[];
-  double2* H = reinterpret_cast<double2*>(llr_raw);     // [r][r] Gram, then Jacobi working copy (float64)
-  double2* Wm = H + RMAX * RMAX;                        // [r][r] eigenvectors (columns)
-  float2* Mm = reinterpret_cast<float2*>(Wm + RMAX * RMAX);   // [r][r] W f W^H
-  float2* Yq = Mm + RMAX * RMAX;                        // [p*p][r]
-  __shared__ double fw[RMAX];
-  const int q = blockIdx.x, qy = q / nc, qx = q % nc;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int q = blockIdx.x * (kSvtThreads / 32) + warp;
+  if (q >= nq) return;   // warp-uniform
+  float2* Yq = reinterpret_cast<float2*>(llr_raw + (size_t)warp * svt_warp_bytes(p, r));   // [p*p][r]
+  float2* Vm = Yq + p * p * r;                                                            // [r][r]
+  const int qy = q / nc, qx = q % nc;
   const int y0 = corners[qy], x0 = corners[qx];
-  const int np = p * p, tid = threadIdx.x;
-  for (int e = tid; e < np * r; e += blockDim.x) {
-    const int k = e / r, i = e % r;
-    const int vy = y0 + k / p, vx = x0 + k % p;
-    Yq[e] = Y[((size_t)vy * N + vx) * r + i];
+  const int np = p * p;
+  for (int e = lane; e < np * r; e += 32) {
+    const int kk = e / r, i = e % r;
+    Yq[e] = Y[((size_t)(y0 + kk / p) * N + (x0 + kk % p)) * r + i];
   }
-  __syncthreads();
-  // Gram H = Yq^H Yq (r x r), float64 (the eigenvalues are squared singular values: float32
-  // would put an absolute error ~1e-7 lambda_max on them, i.e. ~3e-4 sigma_max on the small sigma)
-  for (int e = tid; e < r * r; e += blockDim.x) {
-    const int i = e / r, j = e % r;
-    double sx = 0.0, sy = 0.0;
-    for (int k = 0; k < np; ++k) {
-      const float2 a = Yq[k * r + i], b = Yq[k * r + j];
-      sx += (double)a.x * b.x + (double)a.y * b.y;
-      sy += (double)a.x * b.y - (double)a.y * b.x;
-    }
-    H[i * RMAX + j] = make_double2(sx, sy);
-    Wm[i * RMAX + j] = make_double2(i == j ? 1.0 : 0.0, 0.0);
-  }
-  __syncthreads();
-  // cyclic complex Jacobi in warp 0 (lane k owns index k): H <- U^H H U, W <- W U with
-  // U = [[c, -s e^{i phi}], [s e^{-i phi}, c]] on (p, q), phi = arg H[p][q], cot 2theta = (a - b) / 2|H_pq|
-  if (tid < 32) {
-    const int k = tid;
-    auto mul = [](double2 a, double2 b) { return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x); };
-    for (int sweep = 0; sweep < 30; ++sweep) {
-      double off = 0.0, tot = 0.0;
-      for (int e = k; e < r * r; e += 32) {
-        const double2 h = H[(e / r) * RMAX + e % r];
-        const double m2 = h.x * h.x + h.y * h.y;
-        tot += m2;
-        if (e / r != e % r) off += m2;
-      }
-      for (int o = 16; o > 0; o >>= 1) {
-        off += __shfl_xor_sync(0xffffffffu, off, o);
-        tot += __shfl_xor_sync(0xffffffffu, tot, o);
-      }
-      if (!(off > 1e-26 * tot)) break;
-      for (int pp = 0; pp < r - 1; ++pp)
-        for (int qq = pp + 1; qq < r; ++qq) {
-          const double2 hpq = H[pp * RMAX + qq];
-          const double mag = sqrt(hpq.x * hpq.x + hpq.y * hpq.y);
-          if (!(mag > 1e-300)) continue;
-          const double a = H[pp * RMAX + pp].x, b = H[qq * RMAX + qq].x;
-          const double kap = (a - b) / (2.0 * mag);
-          const double t = (kap >= 0.0 ? 1.0 : -1.0) / (fabs(kap) + sqrt(1.0 + kap * kap));
-          const double c = 1.0 / sqrt(1.0 + t * t), s = t * c;
-          const double2 e = make_double2(hpq.x / mag, hpq.y / mag);   // e^{i phi}
-          const double2 ec = make_double2(e.x, -e.y);
-          __syncwarp();
-          if (k < r) {   // columns: H[:,p]' = H[:,p] c + H[:,q] s e^{-i phi};  H[:,q]' = -H[:,p] s e^{i phi} + H[:,q] c
-            const double2 hp = H[k * RMAX + pp], hq = H[k * RMAX + qq];
-            const double2 a1 = mul(hq, ec), a2 = mul(hp, e);
-            H[k * RMAX + pp] = make_double2(c * hp.x + s * a1.x, c * hp.y + s * a1.y);
-            H[k * RMAX + qq] = make_double2(c * hq.x - s * a2.x, c * hq.y - s * a2.y);
-            const double2 wp = Wm[k * RMAX + pp], wq = Wm[k * RMAX + qq];
-            const double2 b1 = mul(wq, ec), b2 = mul(wp, e);
-            Wm[k * RMAX + pp] = make_double2(c * wp.x + s * b1.x, c * wp.y + s * b1.y);
-            Wm[k * RMAX + qq] = make_double2(c * wq.x - s * b2.x, c * wq.y - s * b2.y);
-          }
-          __syncwarp();
-          if (k < r) {   // rows: H[p,:]'' = c H[p,:]' + s e^{i phi} H[q,:]';  H[q,:]'' = -s e^{-i phi} H[p,:]' + c H[q,:]'
-            const double2 rp = H[pp * RMAX + k], rq = H[qq * RMAX + k];
-            const double2 a1 = mul(rq, e), a2 = mul(rp, ec);
-            H[pp * RMAX + k] = make_double2(c * rp.x + s * a1.x, c * rp.y + s * a1.y);
-            H[qq * RMAX + k] = make_double2(c * rq.x - s * a2.x, c * rq.y - s * a2.y);
-          }
-          __syncwarp();
+  for (int e = lane; e < r * r; e += 32) Vm[e] = make_float2(e / r == e % r ? 1.f : 0.f, 0.f);
+  __syncwarp();
+  // ||Y_q||_F^2 (invariant under the rotations): pairs whose inner product is below 1e-13 of it
+  // are numerically orthogonal however small the columns (rounding noise would otherwise keep
+  // rotating the negligible columns of a low-rank patch)
+  float fro = 0.f;
+  for (int e = lane; e < np * r; e += 32) fro = fmaf(Yq[e].x, Yq[e].x, fmaf(Yq[e].y, Yq[e].y, fro));
+  for (int o = 16; o > 0; o >>= 1) fro += __shfl_xor_sync(0xffffffffu, fro, o);
+  const float floor_g = 1e-13f * fro;
+  for (int sweep = 0; sweep < 40; ++sweep) {
+    bool rotated = false;
+    for (int pp = 0; pp < r - 1; ++pp)
+      for (int qq = pp + 1; qq < r; ++qq) {
+        // alpha = |y_p|^2, beta = |y_q|^2, g = <y_p, y_q> over the p^2 rows (lanes stride the rows)
+        float al = 0.f, be = 0.f, gx = 0.f, gy = 0.f;
+        for (int kk = lane; kk < np; kk += 32) {
+          const float2 a = Yq[kk * r + pp], b = Yq[kk * r + qq];
+          al = fmaf(a.x, a.x, fmaf(a.y, a.y, al));
+          be = fmaf(b.x, b.x, fmaf(b.y, b.y, be));
+          gx = fmaf(a.x, b.x, fmaf(a.y, b.y, gx));
+          gy = fmaf(a.x, b.y, fmaf(-a.y, b.x, gy));
         }
-    }
-    // f(lambda) = max(1 - tau / sqrt(lambda), 0); nuclear norm = sum sqrt(lambda)
-    double sig = 0.0;
-    if (k < r) {
-      sig = sqrt(fmax(H[k * RMAX + k].x, 0.0));
-      fw[k] = sig > (double)tau ? 1.0 - (double)tau / sig : 0.0;
-    }
-    for (int o = 16; o > 0; o >>= 1) sig += __shfl_xor_sync(0xffffffffu, sig, o);
-    if (k == 0) nuc[q] = sig;
+        for (int o = 16; o > 0; o >>= 1) {
+          al += __shfl_xor_sync(0xffffffffu, al, o);
+          be += __shfl_xor_sync(0xffffffffu, be, o);
+          gx += __shfl_xor_sync(0xffffffffu, gx, o);
+          gy += __shfl_xor_sync(0xffffffffu, gy, o);
+        }
+        const float mag = sqrtf(gx * gx + gy * gy);
+        if (!(mag > 4e-6f * sqrtf(al * be)) || !(mag > floor_g)) continue;   // orthogonal to float32 accuracy
+        rotated = true;
+        // 2x2 Hermitian [[al, g], [conj g, be]]: U = [[c, -s e^{i phi}], [s e^{-i phi}, c]],
+        // cot 2theta = (al - be) / 2|g|; columns: y_p' = c y_p + s e^{-i phi} y_q, y_q' = c y_q - s e^{i phi} y_p
+        const float kap = (al - be) / (2.f * mag);
+        const float t = (kap >= 0.f ? 1.f : -1.f) / (fabsf(kap) + sqrtf(1.f + kap * kap));
+        const float c = rsqrtf(1.f + t * t), sn = t * c;
+        const float2 e = make_float2(gx / mag, gy / mag), ec = make_float2(e.x, -e.y);
+        for (int kk = lane; kk < np; kk += 32) {
+          const float2 a = Yq[kk * r + pp], b = Yq[kk * r + qq];
+          const float2 b_ec = cmul(b, ec), a_e = cmul(a, e);
+          Yq[kk * r + pp] = make_float2(c * a.x + sn * b_ec.x, c * a.y + sn * b_ec.y);
+          Yq[kk * r + qq] = make_float2(c * b.x - sn * a_e.x, c * b.y - sn * a_e.y);
+        }
+        if (lane < r) {
+          const float2 a = Vm[lane * r + pp], b = Vm[lane * r + qq];
+          const float2 b_ec = cmul(b, ec), a_e = cmul(a, e);
+          Vm[lane * r + pp] = make_float2(c * a.x + sn * b_ec.x, c * a.y + sn * b_ec.y);
+          Vm[lane * r + qq] = make_float2(c * b.x - sn * a_e.x, c * b.y - sn * a_e.y);
+        }
+        __syncwarp();
+      }
+    if (!rotated) break;
   }
-  __syncthreads();
-  // M = W diag(f) W^H
-  for (int e = tid; e < r * r; e += blockDim.x) {
-    const int i = e / r, j = e % r;
-    double mx = 0.0, my = 0.0;
-    for (int t = 0; t < r; ++t) {
-      const double2 wi = Wm[i * RMAX + t], wj = Wm[j * RMAX + t];   // W[i][t] conj(W[j][t])
-      mx += fw[t] * (wi.x * wj.x + wi.y * wj.y);
-      my += fw[t] * (wi.y * wj.x - wi.x * wj.y);
+  // sigma_j = |yhat_j|; f_j = max(1 - tau / sigma_j, 0) held by lane j; nuclear norm = sum sigma
+  float fj = 0.f;
+  double sig = 0.0;
+  for (int j = 0; j < r; ++j) {
+    float n2 = 0.f;
+    for (int kk = lane; kk < np; kk += 32) {
+      const float2 a = Yq[kk * r + j];
+      n2 = fmaf(a.x, a.x, fmaf(a.y, a.y, n2));
     }
-    Mm[i * RMAX + j] = make_float2((float)mx, (float)my);
+    for (int o = 16; o > 0; o >>= 1) n2 += __shfl_xor_sync(0xffffffffu, n2, o);
+    const float sj = sqrtf(n2);
+    sig += sj;
+    if (lane == j) fj = sj > tau ? 1.f - tau / sj : 0.f;
   }
-  __syncthreads();
-  // P_q = Yq M
+  if (lane == 0) nuc[q] = sig;
+  // P_q = Yhat diag(f) V^H:  P[k][j'] = sum_j Yhat[k][j] f_j conj(V[j'][j])
   float2* Pq = P + (size_t)q * np * r;
-  for (int e = tid; e < np * r; e += blockDim.x) {
-    const int k = e / r, j = e % r;
+  for (int e0 = 0; e0 < np * r; e0 += 32) {   // all lanes stay in the loop (shuffles)
+    const int e = e0 + lane;
+    const bool ok = e < np * r;
+    const int kk = ok ? e / r : 0, jp = ok ? e % r : 0;
     float2 acc = make_float2(0.f, 0.f);
-    for (int t = 0; t < r; ++t) {
-      const float2 pr = cmul(Yq[k * r + t], Mm[t * RMAX + j]);
-      acc.x += pr.x;
-      acc.y += pr.y;
+    for (int j = 0; j < r; ++j) {
+      const float f = __shfl_sync(0xffffffffu, fj, j);
+      const float2 v = Vm[jp * r + j];
+      const float2 t = cmul(Yq[kk * r + j], make_float2(v.x, -v.y));
+      acc.x = fmaf(f, t.x, acc.x);
+      acc.y = fmaf(f, t.y, acc.y);
     }
-    Pq[e] = acc;
+    if (ok) Pq[e] = acc;
   }
 }
 
 // Per voxel: Xc = (Y + gamma sum_{q covering v} P_q[v]) / (1 + gamma c(v)), then
-// x+[l][v] = sum_i Xc[i] d[i][l].  Covering patches are visited in increasing (qy, qx) order.
+// x+[l][v] = sum_i Xc[i] d[i][l] (dT [L][R] as for k_llr_coef).  Covering patches are visited
+// in increasing (qy, qx) order.
 template <int R>
 __global__ void __launch_bounds__(256) k_llr_update(const float2* __restrict__ Y, const float2* __restrict__ P,
                                                     const int* __restrict__ corners, int nc, int N, int p, int r,
-                                                    const float2* __restrict__ d, int L, float gamma,
+                                                    const float2* __restrict__ dT, int L, float gamma,
                                                     float2* __restrict__ xout) {
+  __shared__ float2 xcs[R][33];
   const int V = N * N;
-  const int v = blockIdx.x * blockDim.x + threadIdx.x;
-  if (v >= V) return;
-  const int vy = v / N, vx = v % N;
-  float2 xc[R];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int v = blockIdx.x * 32 + lane;
+  if (w == 0) {   // Xc of the block's 32 voxels
+    float2 xc[R];
 #pragma unroll
-  for (int i = 0; i < R; ++i) xc[i] = make_float2(0.f, 0.f);
-  int cnt = 0;
-  for (int qy = 0; qy < nc; ++qy) {
-    const int cy = __ldg(corners + qy);
-    if (vy < cy || vy >= cy + p) continue;
-    for (int qx = 0; qx < nc; ++qx) {
-      const int cx = __ldg(corners + qx);
-      if (vx < cx || vx >= cx + p) continue;
-      const float2* pv = P + (((size_t)(qy * nc + qx) * p + (vy - cy)) * p + (vx - cx)) * r;
+    for (int i = 0; i < R; ++i) xc[i] = make_float2(0.f, 0.f);
+    if (v < V) {
+      const int vy = v / N, vx = v % N;
+      int cnt = 0;
+      for (int qy = 0; qy < nc; ++qy) {
+        const int cy = __ldg(corners + qy);
+        if (vy < cy || vy >= cy + p) continue;
+        for (int qx = 0; qx < nc; ++qx) {
+          const int cx = __ldg(corners + qx);
+          if (vx < cx || vx >= cx + p) continue;
+          const float2* pv = P + (((size_t)(qy * nc + qx) * p + (vy - cy)) * p + (vx - cx)) * r;
+#pragma unroll
+          for (int i = 0; i < R; ++i)
+            if (i < r) {
+              const float2 t = __ldg(pv + i);
+              xc[i].x += t.x;
+              xc[i].y += t.y;
+            }
+          ++cnt;
+        }
+      }
+      const float inv = 1.f / (1.f + gamma * (float)cnt);
 #pragma unroll
       for (int i = 0; i < R; ++i)
         if (i < r) {
-          const float2 t = __ldg(pv + i);
-          xc[i].x += t.x;
-          xc[i].y += t.y;
+          const float2 y = __ldg(Y + (size_t)v * r + i);
+          xc[i] = make_float2((y.x + gamma * xc[i].x) * inv, (y.y + gamma * xc[i].y) * inv);
         }
-      ++cnt;
     }
-  }
-  const float inv = 1.f / (1.f + gamma * (float)cnt);
 #pragma unroll
-  for (int i = 0; i < R; ++i)
-    if (i < r) {
-      const float2 y = __ldg(Y + (size_t)v * r + i);
-      xc[i] = make_float2((y.x + gamma * xc[i].x) * inv, (y.y + gamma * xc[i].y) * inv);
-    }
-  for (int l = 0; l < L; ++l) {
+    for (int i = 0; i < R; ++i) xcs[i][lane] = xc[i];
+  }
+  __syncthreads();
+  if (v >= V) return;
+  float2 xc[R];
+#pragma unroll
+  for (int i = 0; i < R; ++i) xc[i] = xcs[i][lane];
+  const float4* d4 = reinterpret_cast<const float4*>(dT);
+  for (int l = w; l < L; l += 8) {
     float2 acc = make_float2(0.f, 0.f);
 #pragma unroll
-    for (int i = 0; i < R; ++i)
-      if (i < r) {
-        const float2 t = cmul(xc[i], __ldg(d + (size_t)i * L + l));
-        acc.x += t.x;
-        acc.y += t.y;
-      }
+    for (int i2 = 0; i2 < R / 2; ++i2) {   // padded entries of dT are zero
+      const float4 dd = __ldg(d4 + (size_t)l * (R / 2) + i2);
+      const float2 t0 = cmul(xc[2 * i2], make_float2(dd.x, dd.y)), t1 = cmul(xc[2 * i2 + 1], make_float2(dd.z, dd.w));
+      acc.x += t0.x + t1.x;
+      acc.y += t0.y + t1.y;
+    }
     xout[(size_t)l * V + v] = acc;
   }
 }
