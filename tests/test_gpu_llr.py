@@ -88,3 +88,47 @@ def test_invalid_llr_calls(binding):
     pl.close()
     op.close()
     dic.close()
+
+
+def test_llr_step_full_mrf_size_window(binding):
+    """The MRF size (256 x 256 x 1000 frames, 2500 patches, the 3336-atom dictionary): the oracle
+    computes Z for all frames (A^H A is per frame but global in space) and the exact patch SVTs of
+    the 49 patches that cover a 21 x 21 window; the library's X+ must match there."""
+    import os
+    cfg = synth.get_config("mrf")
+    traj = synth.spiral_trajectory(cfg.M, cfg.R, cfg.turns, cfg.p)
+    D = sd.surrogate_dictionary(cfg.L)
+    x0 = synth.images(cfg)
+    workers = max(1, len(os.sched_getaffinity(0)))
+    y = on.forward(x0, traj, None, cfg.W, workers=workers)
+    rhs = on.adjoint(y, traj, None, cfg.N, cfg.W, workers=workers)
+    mu, lam2, beta, p, s = 1.0, 0.1, 0.2, 11, 5
+    # library
+    dic = binding.Dictionary(D)
+    dic.basis(0.9999, 32)
+    op = binding.LLR(dic, cfg.N, p, s)
+    pl = binding.Plan(cfg.N, traj, cfg.L, W=cfg.W)
+    xd = torch.from_numpy(rhs.astype(np.complex64)).cuda()
+    xg, _ = op.step(pl, xd, xd, mu, lam2, beta)
+    lo, hi = 120, 141
+    xg_w = xg[:, lo:hi, lo:hi].cpu().numpy()
+    pl.close()
+    op.close()
+    dic.close()
+    # oracle: Z everywhere, then the covering patches' SVTs and the update on the window
+    d_o = ol.basis(D, 0.9999, 32)
+    Z = ol.project(rhs - mu * (on.normal(rhs, traj, None, cfg.W, workers=workers) - rhs), d_o)
+    gamma = mu * lam2 * beta
+    acc = np.zeros((cfg.L, hi - lo, hi - lo), np.complex128)
+    cnt = np.zeros((hi - lo, hi - lo))
+    cs = ol.patch_corners(cfg.N, p, s)
+    near = [c for c in cs if c + p > lo and c < hi]
+    for y0 in near:
+        for x0_ in near:
+            P = ol.svt(ol.casorati(Z, y0, x0_, p), 1.0 / beta).T.reshape(cfg.L, p, p)
+            ys, xs = slice(max(y0, lo), min(y0 + p, hi)), slice(max(x0_, lo), min(x0_ + p, hi))
+            acc[:, ys.start - lo:ys.stop - lo, xs.start - lo:xs.stop - lo] += \
+                P[:, ys.start - y0:ys.stop - y0, xs.start - x0_:xs.stop - x0_]
+            cnt[ys.start - lo:ys.stop - lo, xs.start - lo:xs.stop - lo] += 1
+    X_ref = (Z[:, lo:hi, lo:hi] + gamma * acc) / (1.0 + gamma * cnt)[None]
+    assert rel(xg_w, X_ref) <= 1e-4
