@@ -75,9 +75,15 @@ def llr_prox(Z: np.ndarray, tau: float, gamma: float, p: int = 11, s: int = 5):
     return (np.asarray(Z, np.complex128) + gamma * acc) / (1.0 + gamma * cnt)[None], nuc
 
 
-def llr_step(X, rhs, normal, d, mu: float, lam2: float, beta: float, p: int = 11, s: int = 5):
-    """One LLR iteration of Algorithm 1 with lambda_1 = 0: Eq. (15) -> Eq. (20) -> Eq. (21).
-    normal(v) = A^H A v; rhs = A^H b.  Returns (X+, Z)."""
-    Z = project(np.asarray(X, np.complex128) - mu * (normal(X) - rhs), d)
+def llr_step(X, rhs, normal, d, mu: float, lam2: float, beta: float, p: int = 11, s: int = 5,
+             lam1: float = 0.0, lap=None):
+    """One iteration of Algorithm 1: Eq. (15) -> Eq. (20) -> Eq. (21).  normal(v) = A^H A v;
+    rhs = A^H b; lam1, lap: the manifold term lam1 Q^*(Q(X) L) of Eq. (15) (``oracle.manifold``),
+    omitted when lam1 = 0 (the LLR ablation).  Returns (X+, Z)."""
+    G = normal(X) - rhs
+    if lam1:
+        from .manifold import gradient
+        G = G + lam1 * gradient(np.asarray(X, np.complex128), lap, X.shape[1], p, s)
+    Z = project(np.asarray(X, np.complex128) - mu * G, d)
     Xn, _ = llr_prox(Z, 1.0 / beta, mu * lam2 * beta, p, s)
     return Xn, Z
