@@ -210,16 +210,29 @@ mrf_status mrf_dict_basis_copy(mrf_dict dict, void* basis_out);
 typedef struct mrf_llr_s* mrf_llr;
 mrf_status mrf_llr_create(mrf_dict dict, int N, int p, int s, mrf_llr* out);
 
-/* One iteration of Algorithm 1 with lambda_1 = 0 (DEVICE [L][N][N] complex64 arrays, 16-byte
- * aligned, x_out may alias x):
- *   Z = P_S(x - mu (A^H A x - rhs))             (Eq. 15; rhs = A^H b, A^H A from `plan`)
- *   P_q = SVT_{1/beta}(Q_q(Z))                  (Eq. 20, per patch)
- *   x_out = (Z + gamma Q^*(P)) / (1 + gamma c)   (Eq. 21, gamma = mu lambda2 beta, c = patch count)
- * The SVT runs in subspace coordinates (Z lies in span(d): an r x r eigenproblem per patch).
- * nuclear (nullable): sum over patches of ||Q_q(Z)||_* (synchronises the stream).
- * Errors: MRF_EINVAL (mu <= 0, lambda2 < 0, beta <= 0, null, misaligned), errors of mrf_normal. */
-mrf_status mrf_llr_step(mrf_llr llr, mrf_plan plan, const void* x, const void* rhs, float mu, float lambda2,
-                        float beta, void* x_out, double* nuclear, void* stream);
+/* The graph Laplacian of the manifold term (Eqs. 7-11; reading 26) from Phi_D's maps:
+ * params DEVICE [V][2] float (T1, T2) and pd DEVICE [V] float (mrf_dict_match outputs, V = N*N).
+ * The three channels are standardised over the foreground PD > 0.1 max PD; w_ij =
+ * exp(-||Q_i(M) - Q_j(M)||_F^2 / sigma2) over all patch pairs (dense), L = D - W.  sigma2 <= 0:
+ * the median of the nonzero pairwise squared distances.  Outputs (nullable, HOST): the sigma^2
+ * used and max_i D_ii (= max(L), for lambda_1^n = lambda_1^0 max(L)).
+ * Synchronises the stream.  Errors: MRF_EINVAL (null, no foreground), MRF_ENOMEM, MRF_ECUDA. */
+mrf_status mrf_llr_laplacian(mrf_llr llr, const float* params, const float* pd, double sigma2, double* sigma2_out,
+                             double* max_degree, void* stream);
+
+/* One iteration of Algorithm 1 (DEVICE [L][N][N] complex64 arrays, 16-byte aligned):
+ *   Z = P_S(x - mu [A^H A x - rhs + lambda1 Q^*(Q(x) L)])   (Eq. 15; rhs = A^H b, A^H A from `plan`)
+ *   P_q = SVT_{1/beta}(Q_q(Z))                              (Eq. 20, per patch)
+ *   x_out = (Z + gamma Q^*(P)) / (1 + gamma c)              (Eq. 21, gamma = mu lambda2 beta, c = patch count)
+ * lambda1 = 0 is the paper's LLR ablation; lambda1 > 0 needs mrf_llr_laplacian (the manifold term
+ * is evaluated on P_S x: P_S commutes with the patch operators).  The SVT runs in subspace
+ * coordinates (Z lies in span(d): a p^2 x r one-sided Jacobi SVD per patch).  x_out may alias x
+ * when lambda1 = 0 and penalty is NULL.  nuclear (nullable): sum_q ||Q_q(Z)||_*; penalty
+ * (nullable, needs the Laplacian): Tr(Q(P_S x) L Q(P_S x)^H) -- the cost terms of Algorithm 1;
+ * either synchronises the stream.  Errors: MRF_EINVAL (mu <= 0, lambda1 < 0, lambda2 < 0,
+ * beta <= 0, null, misaligned, plan shape), errors of mrf_normal. */
+mrf_status mrf_llr_step(mrf_llr llr, mrf_plan plan, const void* x, const void* rhs, float mu, float lambda1,
+                        float lambda2, float beta, void* x_out, double* nuclear, double* penalty, void* stream);
 mrf_status mrf_llr_destroy(mrf_llr llr);
 
 /* enable != 0 brackets every subsequent tensor-core GEMM launch (k_dict_gemm) of mrf_dict_match

@@ -33,7 +33,7 @@ EXPORTED = [
     "mrf_profile_query", "mrf_nccl_get_unique_id", "mrf_nccl_comm_init", "mrf_nccl_comm_destroy",
     "mrf_adjoint_dcf", "mrf_dcf_weights", "mrf_dict_create", "mrf_dict_match", "mrf_dict_destroy",
     "mrf_dict_profile", "mrf_dict_profile_query", "mrf_dict_basis", "mrf_dict_basis_copy", "mrf_llr_create",
-    "mrf_llr_step", "mrf_llr_destroy",
+    "mrf_llr_step", "mrf_llr_destroy", "mrf_llr_laplacian",
 ]
 
 
@@ -93,7 +93,10 @@ def _load() -> ctypes.CDLL:
         "mrf_dict_basis": ([vp, ctypes.c_double, ci, ctypes.POINTER(ci)], ci),
         "mrf_dict_basis_copy": ([vp, vp], ci),
         "mrf_llr_create": ([vp, ci, ci, ci, ctypes.POINTER(vp)], ci),
-        "mrf_llr_step": ([vp, vp, vp, vp, cf, cf, cf, vp, ctypes.POINTER(ctypes.c_double), vp], ci),
+        "mrf_llr_step": ([vp, vp, vp, vp, cf, cf, cf, cf, vp, ctypes.POINTER(ctypes.c_double),
+                          ctypes.POINTER(ctypes.c_double), vp], ci),
+        "mrf_llr_laplacian": ([vp, vp, vp, ctypes.c_double, ctypes.POINTER(ctypes.c_double),
+                               ctypes.POINTER(ctypes.c_double), vp], ci),
         "mrf_llr_destroy": ([vp], ci),
     }
     for name, (args, res) in sig.items():
@@ -391,20 +394,33 @@ class LLR:
         self._h = h
         self.N, self.L = int(N), dictionary.L
 
+    def laplacian(self, params: torch.Tensor, pd: torch.Tensor, sigma2: float = 0.0):
+        """Graph Laplacian from Phi_D's maps (params [V][2] T1/T2, pd [V]; CUDA float32).
+        Returns (sigma2, max_degree)."""
+        params = params.contiguous().float()
+        pd = pd.contiguous().float()
+        s2, md = ctypes.c_double(), ctypes.c_double()
+        st = torch.cuda.current_stream(params.device).cuda_stream
+        _check(lib.mrf_llr_laplacian(self._h, _ptr(params), _ptr(pd), ctypes.c_double(sigma2), ctypes.byref(s2),
+                                     ctypes.byref(md), ctypes.c_void_p(st)))
+        return s2.value, md.value
+
     def step(self, plan: "Plan", x, rhs, mu: float = 1.0, lam2: float = 0.1, beta: float = 0.2, x_out=None,
-             nuclear: bool = True):
+             nuclear: bool = True, lam1: float = 0.0, penalty: bool = False):
+        """One iteration of Algorithm 1; returns (x_next, nuclear or None, penalty or None)."""
         shape = (self.L, self.N, self.N)
         x = _as_c64(x, shape, "x")
         rhs = _as_c64(rhs, shape, "rhs")
         if not (x.is_cuda and rhs.is_cuda):
             raise TypeError("x and rhs must be CUDA tensors")
         x_out = torch.empty_like(x) if x_out is None else _as_c64(x_out, shape, "x_out")
-        nuc = ctypes.c_double()
+        nuc, pen = ctypes.c_double(), ctypes.c_double()
         st = torch.cuda.current_stream(x.device).cuda_stream
-        _check(lib.mrf_llr_step(self._h, plan._h, _ptr(x), _ptr(rhs), ctypes.c_float(mu), ctypes.c_float(lam2),
-                                ctypes.c_float(beta), _ptr(x_out), ctypes.byref(nuc) if nuclear else None,
+        _check(lib.mrf_llr_step(self._h, plan._h, _ptr(x), _ptr(rhs), ctypes.c_float(mu), ctypes.c_float(lam1),
+                                ctypes.c_float(lam2), ctypes.c_float(beta), _ptr(x_out),
+                                ctypes.byref(nuc) if nuclear else None, ctypes.byref(pen) if penalty else None,
                                 ctypes.c_void_p(st)))
-        return x_out, (nuc.value if nuclear else None)
+        return x_out, (nuc.value if nuclear else None), (pen.value if penalty else None)
 
     def close(self):
         if getattr(self, "_h", None):

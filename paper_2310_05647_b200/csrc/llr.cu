@@ -6,6 +6,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstring>
 #include <string>
 #include <vector>
 
@@ -25,12 +26,25 @@ struct mrf_llr_s {
   float2* nx = nullptr;       // [L][N][N] A^H A x
   double* nuc = nullptr;      // [nc*nc] per-patch nuclear norms
   std::vector<double> nuc_h;
+  // manifold term (mrf_llr_laplacian)
+  bool has_lap = false;
+  float* W = nullptr;         // [n][n] similarity weights (Eq. 8), first the squared distances
+  float* deg = nullptr;       // [n] degrees D_ii
+  float* pv = nullptr;        // [n][3 p^2] standardised patch vectors of the maps
+  unsigned* hist = nullptr;   // [65536] radix-select histogram (+1 word: max PD bits)
+  double* stats = nullptr;    // [blocks][7] foreground sums, then [6] mean/std
+  float2* YX = nullptr;       // [V][r] coefficients of x
+  float2* Qm = nullptr;       // [n][p^2 r] patch blocks of YX
+  float2* Gm = nullptr;       // [n][p^2 r] W Qm
+  double* pen = nullptr;      // [n] trace-penalty terms
 };
 
 static void llr_free(mrf_llr_s* h) {
   if (!h) return;
   cudaSetDevice(h->device);
-  for (void* v : {(void*)h->dT, (void*)h->corners, (void*)h->Y, (void*)h->P, (void*)h->nx, (void*)h->nuc})
+  for (void* v : {(void*)h->dT, (void*)h->corners, (void*)h->Y, (void*)h->P, (void*)h->nx, (void*)h->nuc, (void*)h->W,
+                  (void*)h->deg, (void*)h->pv, (void*)h->hist, (void*)h->stats, (void*)h->YX, (void*)h->Qm,
+                  (void*)h->Gm, (void*)h->pen})
     if (v) cudaFree(v);
   delete h;
 }
@@ -79,11 +93,95 @@ mrf_status mrf_llr_create(mrf_dict dict, int N, int p, int s, mrf_llr* out) {
   return MRF_OK;
 }
 
-mrf_status mrf_llr_step(mrf_llr h, mrf_plan plan, const void* x, const void* rhs, float mu, float lambda2, float beta,
-                        void* x_out, double* nuclear, void* stream) {
+static constexpr int kStatBlocks = 4 * 148;
+
+mrf_status mrf_llr_laplacian(mrf_llr h, const float* params, const float* pd, double sigma2, double* sigma2_out,
+                             double* max_degree, void* stream) {
+  if (!h || !params || !pd) return fail(MRF_EINVAL, "mrf_llr_laplacian: null argument");
+  CUDA_TRY(cudaSetDevice(h->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  const int n = h->nc * h->nc, np = h->p * h->p, V = h->N * h->N;
+  if (!h->W) {
+    bool ok = cudaMalloc((void**)&h->W, (size_t)n * n * sizeof(float)) == cudaSuccess &&
+              cudaMalloc((void**)&h->deg, (size_t)n * sizeof(float)) == cudaSuccess &&
+              cudaMalloc((void**)&h->pv, (size_t)n * 3 * np * sizeof(float)) == cudaSuccess &&
+              cudaMalloc((void**)&h->hist, (65536 + 1) * sizeof(unsigned)) == cudaSuccess &&
+              cudaMalloc((void**)&h->stats, (size_t)kStatBlocks * 7 * sizeof(double)) == cudaSuccess;
+    if (!ok) return fail(MRF_ENOMEM, "mrf_llr_laplacian: device allocation failed");
+  }
+  // foreground statistics of (T1, T2, PD) over PD > 0.1 max PD (reading 26)
+  unsigned* pdmax = h->hist + 65536;
+  CUDA_TRY(cudaMemsetAsync(pdmax, 0, sizeof(unsigned), st));
+  mfd::k_mfd_max<<<kStatBlocks, 256, 0, st>>>(pd, V, pdmax);
+  mfd::k_mfd_stats<<<kStatBlocks, 256, 0, st>>>(params, pd, V, pdmax, h->stats);
+  MRF_TRY(check_launch("k_mfd_stats"));
+  std::vector<double> part((size_t)kStatBlocks * 7);
+  CUDA_TRY(cudaMemcpyAsync(part.data(), h->stats, part.size() * sizeof(double), cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  double a[7] = {0, 0, 0, 0, 0, 0, 0};
+  for (int b = 0; b < kStatBlocks; ++b)
+    for (int i = 0; i < 7; ++i) a[i] += part[(size_t)b * 7 + i];
+  if (!(a[6] > 0.0)) return fail(MRF_EINVAL, "mrf_llr_laplacian: no foreground voxel");
+  double ms[6];
+  for (int c = 0; c < 3; ++c) {
+    const double mean = a[2 * c] / a[6], var = std::max(a[2 * c + 1] / a[6] - mean * mean, 0.0);
+    ms[2 * c] = mean;
+    ms[2 * c + 1] = var > 0.0 ? std::sqrt(var) : 1.0;
+  }
+  CUDA_TRY(cudaMemcpyAsync(h->stats, ms, sizeof(ms), cudaMemcpyHostToDevice, st));
+  mfd::k_mfd_patchvec<<<n, 128, 0, st>>>(params, pd, h->stats, h->corners, h->nc, h->N, h->p, h->pv);
+  const dim3 gd((unsigned)((n + 31) / 32), (unsigned)((n + 31) / 32));
+  mfd::k_mfd_dist<<<gd, 256, 0, st>>>(h->pv, n, 3 * np, h->W);
+  MRF_TRY(check_launch("k_mfd_dist"));
+  if (!(sigma2 > 0.0)) {   // sigma^2 = median of the nonzero upper-triangle distances (exact radix select)
+    std::vector<unsigned> hh(65536);
+    CUDA_TRY(cudaMemsetAsync(h->hist, 0, 65536 * sizeof(unsigned), st));
+    mfd::k_mfd_hist<<<1024, 256, 0, st>>>(h->W, n, 0, 0u, h->hist);
+    CUDA_TRY(cudaMemcpyAsync(hh.data(), h->hist, 65536 * sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    unsigned long long m = 0;
+    for (unsigned c : hh) m += c;
+    if (m == 0) {
+      sigma2 = 1.0;
+    } else {
+      const unsigned long long ks[2] = {(m - 1) / 2, m / 2};   // numpy's median: mean of the two middle
+      float vals[2];
+      for (int t = 0; t < 2; ++t) {
+        unsigned long long c = 0;
+        unsigned hi = 0;
+        while (c + hh[hi] <= ks[t]) c += hh[hi++];
+        std::vector<unsigned> lo(65536);
+        CUDA_TRY(cudaMemsetAsync(h->hist, 0, 65536 * sizeof(unsigned), st));
+        mfd::k_mfd_hist<<<1024, 256, 0, st>>>(h->W, n, 1, hi, h->hist);
+        CUDA_TRY(cudaMemcpyAsync(lo.data(), h->hist, 65536 * sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(cudaStreamSynchronize(st));
+        unsigned lw = 0;
+        while (c + lo[lw] <= ks[t]) c += lo[lw++];
+        const unsigned bits = (hi << 16) | lw;
+        std::memcpy(&vals[t], &bits, 4);
+      }
+      sigma2 = 0.5 * ((double)vals[0] + (double)vals[1]);
+    }
+  }
+  mfd::k_mfd_weights<<<n, 256, 0, st>>>(h->W, n, (float)(1.0 / sigma2), h->deg);
+  MRF_TRY(check_launch("k_mfd_weights"));
+  std::vector<float> dg(n);
+  CUDA_TRY(cudaMemcpyAsync(dg.data(), h->deg, (size_t)n * sizeof(float), cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  if (sigma2_out) *sigma2_out = sigma2;
+  if (max_degree) *max_degree = *std::max_element(dg.begin(), dg.end());
+  h->has_lap = true;
+  return MRF_OK;
+}
+
+mrf_status mrf_llr_step(mrf_llr h, mrf_plan plan, const void* x, const void* rhs, float mu, float lambda1,
+                        float lambda2, float beta, void* x_out, double* nuclear, double* penalty, void* stream) {
   if (!h || !plan || !x || !rhs || !x_out) return fail(MRF_EINVAL, "mrf_llr_step: null argument");
-  if (!(mu > 0.f) || !(lambda2 >= 0.f) || !(beta > 0.f) || !std::isfinite(mu * lambda2 * beta))
-    return fail(MRF_EINVAL, "mrf_llr_step: need mu > 0, lambda2 >= 0, beta > 0");
+  if (!(mu > 0.f) || !(lambda1 >= 0.f) || !(lambda2 >= 0.f) || !(beta > 0.f) || !std::isfinite(mu * lambda2 * beta))
+    return fail(MRF_EINVAL, "mrf_llr_step: need mu > 0, lambda1 >= 0, lambda2 >= 0, beta > 0");
+  const bool manifold = lambda1 > 0.f || penalty != nullptr;
+  if (manifold && !h->has_lap) return fail(MRF_EINVAL, "mrf_llr_step: lambda1 > 0 needs mrf_llr_laplacian first");
+  if (x_out == x && manifold) return fail(MRF_EINVAL, "mrf_llr_step: x_out may not alias x with the manifold term");
   for (const void* v : {x, rhs, (const void*)x_out})
     if ((uintptr_t)v % 16) return fail(MRF_EINVAL, "mrf_llr_step: arrays must be 16-byte aligned");
   int pN = 0, pL = 0, pC = 0, pdev = 0;
@@ -96,14 +194,45 @@ mrf_status mrf_llr_step(mrf_llr h, mrf_plan plan, const void* x, const void* rhs
   // A^H A x (the plan checks that x has its shape: [L][N][N] device memory)
   MRF_TRY(mrf_normal(plan, x, h->nx, 0.f, stream));
   const float2* xf = reinterpret_cast<const float2*>(x);
-  const unsigned gv = (unsigned)((V + 31) / 32);   // 32 voxels x 8 frame groups per block
-  if (h->r <= 16)
-    llr::k_llr_coef<16><<<gv, 32 * llr::coef_groups<16>(), 0, st>>>(xf, h->nx, (const float2*)rhs, h->dT, h->r,
-                                                                       h->L, V, mu, h->Y);
-  else
-    llr::k_llr_coef<32><<<gv, 32 * llr::coef_groups<32>(), 0, st>>>(xf, h->nx, (const float2*)rhs, h->dT, h->r,
-                                                                       h->L, V, mu, h->Y);
+  const unsigned gv = (unsigned)((V + 31) / 32);   // 32 voxels x NG frame groups per block
+  const int n = nq, np = h->p * h->p, blk = np * h->r;
+  if (manifold && !h->YX) {
+    bool ok = cudaMalloc((void**)&h->YX, (size_t)V * h->r * sizeof(float2)) == cudaSuccess &&
+              cudaMalloc((void**)&h->Qm, (size_t)n * blk * sizeof(float2)) == cudaSuccess &&
+              cudaMalloc((void**)&h->Gm, (size_t)n * blk * sizeof(float2)) == cudaSuccess &&
+              cudaMalloc((void**)&h->pen, (size_t)n * sizeof(double)) == cudaSuccess;
+    if (!ok) return fail(MRF_ENOMEM, "mrf_llr_step: manifold workspace allocation failed");
+  }
+  const float2* rh = (const float2*)rhs;
+  if (h->r <= 16) {
+    if (manifold) llr::k_llr_coef<16, true><<<gv, 32 * llr::coef_groups<16>(), 0, st>>>(xf, h->nx, rh, h->dT, h->r, h->L, V, mu, h->Y, h->YX);
+    else llr::k_llr_coef<16, false><<<gv, 32 * llr::coef_groups<16>(), 0, st>>>(xf, h->nx, rh, h->dT, h->r, h->L, V, mu, h->Y, nullptr);
+  } else {
+    if (manifold) llr::k_llr_coef<32, true><<<gv, 32 * llr::coef_groups<32>(), 0, st>>>(xf, h->nx, rh, h->dT, h->r, h->L, V, mu, h->Y, h->YX);
+    else llr::k_llr_coef<32, false><<<gv, 32 * llr::coef_groups<32>(), 0, st>>>(xf, h->nx, rh, h->dT, h->r, h->L, V, mu, h->Y, nullptr);
+  }
   MRF_TRY(check_launch("k_llr_coef"));
+  if (manifold) {   // Y -= mu lambda1 coef(Q^*(Q(P_S x) L)),  L = D - W (Eq. 15's manifold term)
+    mfd::k_mfd_gather<<<n, 128, 0, st>>>(h->YX, h->corners, h->nc, h->N, h->p, h->r, h->Qm);
+    const int M2 = 2 * blk;
+    const dim3 gg((unsigned)((M2 + 63) / 64), (unsigned)((n + 63) / 64));
+    mfd::k_mfd_sgemm<<<gg, 256, 0, st>>>(h->W, reinterpret_cast<const float*>(h->Qm), n, M2,
+                                         reinterpret_cast<float*>(h->Gm));
+    MRF_TRY(check_launch("k_mfd_sgemm"));
+    if (lambda1 > 0.f) {
+      if (h->r <= 16)
+        mfd::k_mfd_apply<16><<<(unsigned)((V + 255) / 256), 256, 0, st>>>(h->Y, h->Qm, h->Gm, h->deg, h->corners, h->nc,
+                                                                           h->N, h->p, h->r, mu * lambda1);
+      else
+        mfd::k_mfd_apply<32><<<(unsigned)((V + 255) / 256), 256, 0, st>>>(h->Y, h->Qm, h->Gm, h->deg, h->corners, h->nc,
+                                                                           h->N, h->p, h->r, mu * lambda1);
+      MRF_TRY(check_launch("k_mfd_apply"));
+    }
+    if (penalty) {
+      mfd::k_mfd_penalty<<<n, 256, 0, st>>>(h->Qm, h->Gm, h->deg, blk, h->pen);
+      MRF_TRY(check_launch("k_mfd_penalty"));
+    }
+  }
   const int ppb = llr::kSvtThreads / 32;
   llr::k_llr_svt<<<(unsigned)((nq + ppb - 1) / ppb), llr::kSvtThreads, svt_smem(h->p, h->r), st>>>(
       h->Y, h->corners, h->nc, h->N, h->p, h->r, 1.f / beta, nq, h->P, h->nuc);
@@ -116,6 +245,14 @@ mrf_status mrf_llr_step(mrf_llr h, mrf_plan plan, const void* x, const void* rhs
     llr::k_llr_update<32><<<gv, 256, 0, st>>>(h->Y, h->P, h->corners, h->nc, h->N, h->p, h->r, h->dT, h->L, gamma,
                                               (float2*)x_out);
   MRF_TRY(check_launch("k_llr_update"));
+  if (penalty) {   // Tr(Q(P_S x) L Q(P_S x)^H), patches summed in a fixed order (synchronises)
+    std::vector<double> pp(nq);
+    CUDA_TRY(cudaMemcpyAsync(pp.data(), h->pen, (size_t)nq * sizeof(double), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    double t = 0.0;
+    for (double v : pp) t += v;
+    *penalty = t;
+  }
   if (nuclear) {   // sum over patches in a fixed order (synchronises the stream)
     CUDA_TRY(cudaMemcpyAsync(h->nuc_h.data(), h->nuc, (size_t)nq * sizeof(double), cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaStreamSynchronize(st));

@@ -66,3 +66,23 @@ def voxel_fingerprints(D: np.ndarray, V: int, seed: int = 12, noise: float = 0.0
         sc = noise * np.sqrt(np.mean(np.abs(X) ** 2))
         X = X + sc * (rng.standard_normal(X.shape) + 1j * rng.standard_normal(X.shape)) / np.sqrt(2)
     return X, k, rho
+
+
+def parameter_maps(N: int, seed: int = 3) -> np.ndarray:
+    """(T1 [ms], T2 [ms], PD) maps [3][N][N]: seeded ellipses of tissue values on a zero background
+    (the input of the manifold weights, Eq. 8, in place of Phi_D's estimates)."""
+    rng = np.random.default_rng([seed, 2])
+    yy, xx = np.mgrid[0:N, 0:N] / N - 0.5
+    maps = np.zeros((3, N, N))
+    for _ in range(7):
+        cy, cx = rng.uniform(-0.3, 0.3, 2)
+        ay, ax = rng.uniform(0.05, 0.3, 2)
+        th = rng.uniform(0, np.pi)
+        u = ((xx - cx) * np.cos(th) + (yy - cy) * np.sin(th)) / ax
+        v = (-(xx - cx) * np.sin(th) + (yy - cy) * np.cos(th)) / ay
+        m = u * u + v * v <= 1.0
+        t2 = rng.uniform(20, 300)
+        maps[0][m] = rng.uniform(max(300.0, t2), 3000)
+        maps[1][m] = t2
+        maps[2][m] = rng.uniform(0.3, 1.0)
+    return maps

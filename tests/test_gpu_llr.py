@@ -61,13 +61,13 @@ def test_llr_step_against_the_oracle(binding, N, L, p, s):
     op = binding.LLR(dic, N, p, s)
     pl = binding.Plan(N, traj, L, W=W)
     xd = torch.from_numpy(rhs.astype(np.complex64)).cuda()
-    x_next, nuc = op.step(pl, xd, xd, mu, lam2, beta)
+    x_next, nuc, _ = op.step(pl, xd, xd, mu, lam2, beta)
     torch.cuda.synchronize()
     assert rel(x_next.cpu().numpy(), X_ref) <= 1e-4
     assert abs(nuc - nuc_ref) / nuc_ref <= 1e-4
     # the thresholding is active: some but not all singular values survive
     assert 0.0 < rel(X_ref, Z_ref) < 1.0
-    x_alias, _ = op.step(pl, xd, xd, mu, lam2, beta, x_out=xd.clone())
+    x_alias, _, _ = op.step(pl, xd, xd, mu, lam2, beta, x_out=xd.clone())
     torch.cuda.synchronize()
     pl.close()
     op.close()
@@ -109,7 +109,7 @@ def test_llr_step_full_mrf_size_window(binding):
     op = binding.LLR(dic, cfg.N, p, s)
     pl = binding.Plan(cfg.N, traj, cfg.L, W=cfg.W)
     xd = torch.from_numpy(rhs.astype(np.complex64)).cuda()
-    xg, _ = op.step(pl, xd, xd, mu, lam2, beta)
+    xg, _, _ = op.step(pl, xd, xd, mu, lam2, beta)
     lo, hi = 120, 141
     xg_w = xg[:, lo:hi, lo:hi].cpu().numpy()
     pl.close()
@@ -132,3 +132,44 @@ def test_llr_step_full_mrf_size_window(binding):
             cnt[ys.start - lo:ys.stop - lo, xs.start - lo:xs.stop - lo] += 1
     X_ref = (Z[:, lo:hi, lo:hi] + gamma * acc) / (1.0 + gamma * cnt)[None]
     assert rel(xg_w, X_ref) <= 1e-4
+
+
+def test_manifold_term_against_the_oracle(binding):
+    """MS-LLR step with the manifold term (lambda_1 > 0): the Laplacian from parameter maps
+    (sigma^2 by the median rule, degrees), the step and the trace penalty vs the oracle."""
+    from oracle import manifold as omf
+    N, L, p, s = 64, 100, 11, 5
+    D = sd.surrogate_dictionary(L)
+    traj = synth.spiral_trajectory(512, 10, 8, 1.5)
+    x_true = synth.rank5_images(N, L, range(L), 7)
+    rhs = on.adjoint(on.forward(x_true, traj, None, 6), traj, None, N, 6)
+    maps = sd.parameter_maps(N, 3)                             # (T1, T2, PD) [3][N][N]
+    W, s2 = omf.weights(maps, N, p, s)
+    Lap = omf.laplacian(W)
+    lam1 = 0.1 * float(Lap.max()) / 50.0
+    mu, lam2, beta = 1.0, 0.1, 0.2
+    d_o = ol.basis(D, 0.9999, 32)
+    X_ref, _ = ol.llr_step(rhs, rhs, lambda v: on.normal(v, traj, None, 6), d_o, mu, lam2, beta, p, s,
+                           lam1=lam1, lap=Lap)
+    pen_ref = omf.penalty(ol.project(rhs, d_o), Lap, N, p, s)
+
+    dic = binding.Dictionary(D)
+    dic.basis(0.9999, 32)
+    op = binding.LLR(dic, N, p, s)
+    params = torch.from_numpy(np.ascontiguousarray(np.stack([maps[0].ravel(), maps[1].ravel()], 1))).float().cuda()
+    pd = torch.from_numpy(np.ascontiguousarray(maps[2].ravel())).float().cuda()
+    s2g, mdeg = op.laplacian(params, pd)
+    assert abs(s2g - s2) / s2 <= 1e-5
+    assert abs(mdeg - Lap.max()) / Lap.max() <= 1e-4
+    pl = binding.Plan(N, traj, L, W=6)
+    xd = torch.from_numpy(rhs.astype(np.complex64)).cuda()
+    xg, _, pen = op.step(pl, xd, xd, mu, lam2, beta, lam1=lam1, penalty=True)
+    torch.cuda.synchronize()
+    assert rel(xg.cpu().numpy(), X_ref) <= 1e-4
+    assert abs(pen - pen_ref) / abs(pen_ref) <= 1e-4
+    # the manifold term matters here: the lambda_1 = 0 step differs
+    x0, _, _ = op.step(pl, xd, xd, mu, lam2, beta)
+    assert rel(x0.cpu().numpy(), X_ref) > 1e-3
+    pl.close()
+    op.close()
+    dic.close()
