@@ -10,7 +10,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libmrfnufft.so")
 SOURCES = [os.path.join(CSRC, f) for f in ("mrfnufft.cu", "dict.cu", "llr.cu", "nccl_dl.cpp")]
-DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("gridding.cuh", "cg.cuh", "fft.cuh", "match.cuh", "llr.cuh", "dict_internal.h", "nccl_dl.h", "status.h")] + [
+DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("gridding.cuh", "cg.cuh", "fft.cuh", "match.cuh", "umma.cuh", "gemm3.cuh", "llr.cuh", "dict_internal.h", "nccl_dl.h", "status.h")] + [
     os.path.join(ROOT, "include", "mrfnufft.h")]
 
 NVCC_FLAGS = [

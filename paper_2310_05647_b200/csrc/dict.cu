@@ -34,19 +34,25 @@ static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
   return fn;
 }
 
-// 2D fp16 tensor map over a row-major [rows][cols] array with a (64 x box_rows) 128-byte swizzled box
-static mrf_status make_tmap(CUtensorMap* m, const __half* base, uint64_t cols, uint64_t rows, uint32_t box_rows) {
+mrf_status mrf::tmap_2d(CUtensorMap* m, CUtensorMapDataType type, const void* base, uint64_t cols, uint64_t rows,
+                       uint64_t row_bytes, uint32_t box_cols, uint32_t box_rows) {
   auto enc = tensor_map_encoder();
   if (!enc) return fail(MRF_ECUDA, "cuTensorMapEncodeTiled is not available");
   const cuuint64_t dims[2] = {cols, rows};
-  const cuuint64_t strides[1] = {cols * sizeof(__half)};
-  const cuuint32_t box[2] = {(cuuint32_t)dm::BK, box_rows};
+  const cuuint64_t strides[1] = {row_bytes};
+  const cuuint32_t box[2] = {box_cols, box_rows};
   const cuuint32_t estr[2] = {1, 1};
-  const CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<__half*>(base), dims, strides, box, estr,
-                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+  const CUresult r = enc(m, type, 2, const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                         CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(MRF_ECUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
   return MRF_OK;
+}
+
+// 2D fp16 tensor map over a row-major [rows][cols] array with a (64 x box_rows) 128-byte swizzled box
+static mrf_status make_tmap(CUtensorMap* m, const __half* base, uint64_t cols, uint64_t rows, uint32_t box_rows) {
+  return tmap_2d(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, base, cols, rows, cols * sizeof(__half), (uint32_t)dm::BK,
+                 box_rows);
 }
 
 static void dict_free(mrf_dict_s* d) {

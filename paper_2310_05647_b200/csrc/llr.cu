@@ -12,6 +12,7 @@
 
 #include "../../include/mrfnufft.h"
 #include "dict_internal.h"
+#include "gemm3.cuh"
 #include "llr.cuh"
 #include "status.h"
 
@@ -37,6 +38,11 @@ struct mrf_llr_s {
   float2* Qm = nullptr;       // [n][p^2 r] patch blocks of YX
   float2* Gm = nullptr;       // [n][p^2 r] W Qm
   double* pen = nullptr;      // [n] trace-penalty terms
+  // G = W Qm on the tensor cores (gemm3.cuh): tf32 hi / lo copies, K-major, row pitch nK
+  int nK = 0, sms = 0;
+  float *Wh = nullptr, *Wl = nullptr;   // [n][nK]
+  float *Qh = nullptr, *Ql = nullptr;   // [2 p^2 r][nK] (Qm transposed)
+  CUtensorMap tWh, tWl, tQh, tQl;
 };
 
 static void llr_free(mrf_llr_s* h) {
@@ -44,12 +50,12 @@ static void llr_free(mrf_llr_s* h) {
   cudaSetDevice(h->device);
   for (void* v : {(void*)h->dT, (void*)h->corners, (void*)h->Y, (void*)h->P, (void*)h->nx, (void*)h->nuc, (void*)h->W,
                   (void*)h->deg, (void*)h->pv, (void*)h->hist, (void*)h->stats, (void*)h->YX, (void*)h->Qm,
-                  (void*)h->Gm, (void*)h->pen})
+                  (void*)h->Gm, (void*)h->pen, (void*)h->Wh, (void*)h->Wl, (void*)h->Qh, (void*)h->Ql})
     if (v) cudaFree(v);
   delete h;
 }
 
-static size_t svt_smem(int p, int r) { return (llr::kSvtThreads / 32) * llr::svt_warp_bytes(p, r); }
+static size_t svt_smem(int r) { return (llr::kSvtThreads / 32) * llr::svt_warp_bytes(r); }
 
 extern "C" {
 
@@ -84,7 +90,10 @@ mrf_status mrf_llr_create(mrf_dict dict, int N, int p, int s, mrf_llr* out) {
   cudaError_t e = cudaMemcpy(h->dT, dT.data(), dT.size() * sizeof(float2), cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMemcpy(h->corners, c.data(), c.size() * sizeof(int), cudaMemcpyHostToDevice);
   if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(llr::k_llr_svt, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)svt_smem(p, h->r));
+    e = cudaFuncSetAttribute(llr::k_llr_svt, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)svt_smem(h->r));
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(g3::k_g3_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g3::SMEM);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&h->sms, cudaDevAttrMultiProcessorCount, h->device);
   if (e != cudaSuccess) {
     llr_free(h);
     return fail(MRF_ECUDA, std::string("mrf_llr_create: ") + cudaGetErrorString(e));
@@ -107,7 +116,12 @@ mrf_status mrf_llr_laplacian(mrf_llr h, const float* params, const float* pd, do
               cudaMalloc((void**)&h->pv, (size_t)n * 3 * np * sizeof(float)) == cudaSuccess &&
               cudaMalloc((void**)&h->hist, (65536 + 1) * sizeof(unsigned)) == cudaSuccess &&
               cudaMalloc((void**)&h->stats, (size_t)kStatBlocks * 7 * sizeof(double)) == cudaSuccess;
+    h->nK = (n + 3) / 4 * 4;   // 16-byte TMA row pitch
+    ok = ok && cudaMalloc((void**)&h->Wh, (size_t)n * h->nK * sizeof(float)) == cudaSuccess &&
+         cudaMalloc((void**)&h->Wl, (size_t)n * h->nK * sizeof(float)) == cudaSuccess;
     if (!ok) return fail(MRF_ENOMEM, "mrf_llr_laplacian: device allocation failed");
+    MRF_TRY(tmap_2d(&h->tWh, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, h->Wh, n, n, (uint64_t)h->nK * 4, g3::BK, g3::BM));
+    MRF_TRY(tmap_2d(&h->tWl, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, h->Wl, n, n, (uint64_t)h->nK * 4, g3::BK, g3::BM));
   }
   // foreground statistics of (T1, T2, PD) over PD > 0.1 max PD (reading 26)
   unsigned* pdmax = h->hist + 65536;
@@ -165,6 +179,9 @@ mrf_status mrf_llr_laplacian(mrf_llr h, const float* params, const float* pd, do
   }
   mfd::k_mfd_weights<<<n, 256, 0, st>>>(h->W, n, (float)(1.0 / sigma2), h->deg);
   MRF_TRY(check_launch("k_mfd_weights"));
+  const dim3 gs((unsigned)((n + 31) / 32), (unsigned)((n + 31) / 32));
+  g3::k_g3_split<false><<<gs, 256, 0, st>>>(h->W, n, n, n, h->Wh, h->Wl, h->nK);
+  MRF_TRY(check_launch("k_g3_split"));
   std::vector<float> dg(n);
   CUDA_TRY(cudaMemcpyAsync(dg.data(), h->deg, (size_t)n * sizeof(float), cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaStreamSynchronize(st));
@@ -200,8 +217,12 @@ mrf_status mrf_llr_step(mrf_llr h, mrf_plan plan, const void* x, const void* rhs
     bool ok = cudaMalloc((void**)&h->YX, (size_t)V * h->r * sizeof(float2)) == cudaSuccess &&
               cudaMalloc((void**)&h->Qm, (size_t)n * blk * sizeof(float2)) == cudaSuccess &&
               cudaMalloc((void**)&h->Gm, (size_t)n * blk * sizeof(float2)) == cudaSuccess &&
-              cudaMalloc((void**)&h->pen, (size_t)n * sizeof(double)) == cudaSuccess;
+              cudaMalloc((void**)&h->pen, (size_t)n * sizeof(double)) == cudaSuccess &&
+              cudaMalloc((void**)&h->Qh, (size_t)2 * blk * h->nK * sizeof(float)) == cudaSuccess &&
+              cudaMalloc((void**)&h->Ql, (size_t)2 * blk * h->nK * sizeof(float)) == cudaSuccess;
     if (!ok) return fail(MRF_ENOMEM, "mrf_llr_step: manifold workspace allocation failed");
+    MRF_TRY(tmap_2d(&h->tQh, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, h->Qh, n, 2 * blk, (uint64_t)h->nK * 4, g3::BK, g3::BN));
+    MRF_TRY(tmap_2d(&h->tQl, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, h->Ql, n, 2 * blk, (uint64_t)h->nK * 4, g3::BK, g3::BN));
   }
   const float2* rh = (const float2*)rhs;
   if (h->r <= 16) {
@@ -214,11 +235,13 @@ mrf_status mrf_llr_step(mrf_llr h, mrf_plan plan, const void* x, const void* rhs
   MRF_TRY(check_launch("k_llr_coef"));
   if (manifold) {   // Y -= mu lambda1 coef(Q^*(Q(P_S x) L)),  L = D - W (Eq. 15's manifold term)
     mfd::k_mfd_gather<<<n, 128, 0, st>>>(h->YX, h->corners, h->nc, h->N, h->p, h->r, h->Qm);
-    const int M2 = 2 * blk;
-    const dim3 gg((unsigned)((M2 + 63) / 64), (unsigned)((n + 63) / 64));
-    mfd::k_mfd_sgemm<<<gg, 256, 0, st>>>(h->W, reinterpret_cast<const float*>(h->Qm), n, M2,
-                                         reinterpret_cast<float*>(h->Gm));
-    MRF_TRY(check_launch("k_mfd_sgemm"));
+    const int M2 = 2 * blk;   // G [n][M2] = W [n][n] Qm [n][M2]: A = W (K-major), B = Qm^T [M2][n]
+    const dim3 gs((unsigned)((M2 + 31) / 32), (unsigned)((n + 31) / 32));
+    g3::k_g3_split<true><<<gs, 256, 0, st>>>(reinterpret_cast<const float*>(h->Qm), n, M2, M2, h->Qh, h->Ql, h->nK);
+    const int mt = (n + g3::BM - 1) / g3::BM, nt = (M2 + g3::BN - 1) / g3::BN;
+    g3::k_g3_gemm<<<std::min(mt * nt, h->sms), g3::THREADS, g3::SMEM, st>>>(
+        h->tWh, h->tWl, h->tQh, h->tQl, mt, nt, (n + g3::BK - 1) / g3::BK, n, M2, reinterpret_cast<float*>(h->Gm), M2);
+    MRF_TRY(check_launch("k_g3_gemm"));
     if (lambda1 > 0.f) {
       if (h->r <= 16)
         mfd::k_mfd_apply<16><<<(unsigned)((V + 255) / 256), 256, 0, st>>>(h->Y, h->Qm, h->Gm, h->deg, h->corners, h->nc,
@@ -234,7 +257,7 @@ mrf_status mrf_llr_step(mrf_llr h, mrf_plan plan, const void* x, const void* rhs
     }
   }
   const int ppb = llr::kSvtThreads / 32;
-  llr::k_llr_svt<<<(unsigned)((nq + ppb - 1) / ppb), llr::kSvtThreads, svt_smem(h->p, h->r), st>>>(
+  llr::k_llr_svt<<<(unsigned)((nq + ppb - 1) / ppb), llr::kSvtThreads, svt_smem(h->r), st>>>(
       h->Y, h->corners, h->nc, h->N, h->p, h->r, 1.f / beta, nq, h->P, h->nuc);
   MRF_TRY(check_launch("k_llr_svt"));
   const float gamma = mu * lambda2 * beta;

@@ -9,7 +9,7 @@
 // coefficients Y = Z d^dagger (V x r) a patch Casorati matrix is Q_q(Z) = Y_q d and
 // SVT(Q_q(Z)) = SVT(Y_q) d = Y_q W diag(max(1 - tau / sigma, 0)) W^H d with Y_q^H Y_q = W S^2 W^H:
 // the p^2 x L SVD becomes an r x r Hermitian eigenproblem per patch (r = 13 for the MRF
-// dictionary at 0.9999 energy), solved by one-sided (Hestenes) Jacobi on Y_q in one warp.
+// dictionary at 0.9999 energy), solved by a float64 Jacobi on the Gram matrix in one warp.
 //
 //   k_llr_coef   : Y[v][i] = sum_l conj(d[i][l]) (x - mu (n - rhs))[l][v]   (reads 3 image arrays)
 //   k_llr_svt    : per patch: Gram, Jacobi, M = W f W^H, P_q = Y_q M, sum sigma (nuclear norm)
@@ -90,12 +90,22 @@ __global__ void __launch_bounds__(32 * coef_groups<R>()) k_llr_coef(const float2
 
 // One patch per warp, kSvtThreads / 32 patches per block.  corners: [nc] top-left coordinates
 // (same list for rows and columns); patch q = (qy, qx).  P: [nq][p*p][r] output coefficients;
-// nuc: [nq] sum sigma.  The SVD of the p^2 x r coefficient block Y_q is one-sided (Hestenes)
-// Jacobi: column pairs of Y_q are rotated until mutually orthogonal, accumulating V, so that
-// Y_q V = Yhat has orthogonal columns of norms sigma_j (float32 keeps the small sigma to relative
-// accuracy: no squared Gram); SVT(Y_q) = Yhat diag(max(1 - tau / sigma, 0)) V^H.
-// Shared memory per warp: svt_warp_bytes(p, r).
-__host__ __device__ constexpr size_t svt_warp_bytes(int p, int r) { return ((size_t)p * p * r + (size_t)r * r) * 8; }
+// nuc: [nq] sum sigma.  SVT(Y_q) = Y_q W diag(max(1 - tau / sigma, 0)) W^H with the Hermitian
+// eigendecomposition Y_q^H Y_q = W S^2 W^H:
+//   1. the r x r Gram matrix in float64 (products of float32 are exact in float64, so the small
+//      eigenvalues keep an absolute error ~1e-16 ||Y_q||_F^2 -- far below tau^2);
+//   2. cyclic parallel Jacobi in float64: each round applies rp / 2 disjoint rotations (round-robin
+//      pairing, rp = r rounded up to even), all rows then all columns, lanes striding the entries;
+//   3. M = W F W^H (float64 -> float32), P_q = Y_q M.
+// Shared memory per warp: svt_warp_bytes(r).
+__host__ __device__ constexpr int svt_rp(int r) { return (r + 1) & ~1; }
+__host__ __device__ constexpr size_t svt_warp_bytes(int r) {
+  return (size_t)2 * svt_rp(r) * svt_rp(r) * 16 + (size_t)svt_rp(r) / 2 * 32 + ((size_t)r * r * 8 + 15) / 16 * 16;
+}
+
+__device__ __forceinline__ double2 zmul(double2 a, double2 b) {
+  return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
+}
 
 static __global__ void __launch_bounds__(kSvtThreads) k_llr_svt(const float2* __restrict__ Y, const int* __restrict__ corners,
                                                           int nc, int N, int p, int r, float tau, int nq,
@@ -104,98 +114,137 @@ static __global__ void __launch_bounds__(kSvtThreads) k_llr_svt(const float2* __
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int q = blockIdx.x * (kSvtThreads / 32) + warp;
   if (q >= nq) return;   // warp-uniform
-  float2* Yq = reinterpret_cast<float2*>(llr_raw + (size_t)warp * svt_warp_bytes(p, r));   // [p*p][r]
-  float2* Vm = Yq + p * p * r;                                                            // [r][r]
+  const int rp = svt_rp(r), half = rp / 2;
+  double2* A = reinterpret_cast<double2*>(llr_raw + (size_t)warp * svt_warp_bytes(r));   // [rp][rp]
+  double2* Wm = A + rp * rp;                                                             // [rp][rp]
+  double4* rot = reinterpret_cast<double4*>(Wm + rp * rp);                               // [half] (c, s, e)
+  float2* M = reinterpret_cast<float2*>(rot + half);                                     // [r][r]
   const int qy = q / nc, qx = q % nc;
   const int y0 = corners[qy], x0 = corners[qx];
   const int np = p * p;
-  for (int e = lane; e < np * r; e += 32) {
-    const int kk = e / r, i = e % r;
-    Yq[e] = Y[((size_t)(y0 + kk / p) * N + (x0 + kk % p)) * r + i];
-  }
-  for (int e = lane; e < r * r; e += 32) Vm[e] = make_float2(e / r == e % r ? 1.f : 0.f, 0.f);
-  __syncwarp();
-  // ||Y_q||_F^2 (invariant under the rotations): pairs whose inner product is below 1e-13 of it
-  // are numerically orthogonal however small the columns (rounding noise would otherwise keep
-  // rotating the negligible columns of a low-rank patch)
-  float fro = 0.f;
-  for (int e = lane; e < np * r; e += 32) fro = fmaf(Yq[e].x, Yq[e].x, fmaf(Yq[e].y, Yq[e].y, fro));
-  for (int o = 16; o > 0; o >>= 1) fro += __shfl_xor_sync(0xffffffffu, fro, o);
-  const float floor_g = 1e-13f * fro;
-  for (int sweep = 0; sweep < 40; ++sweep) {
-    bool rotated = false;
-    for (int pp = 0; pp < r - 1; ++pp)
-      for (int qq = pp + 1; qq < r; ++qq) {
-        // alpha = |y_p|^2, beta = |y_q|^2, g = <y_p, y_q> over the p^2 rows (lanes stride the rows)
-        float al = 0.f, be = 0.f, gx = 0.f, gy = 0.f;
-        for (int kk = lane; kk < np; kk += 32) {
-          const float2 a = Yq[kk * r + pp], b = Yq[kk * r + qq];
-          al = fmaf(a.x, a.x, fmaf(a.y, a.y, al));
-          be = fmaf(b.x, b.x, fmaf(b.y, b.y, be));
-          gx = fmaf(a.x, b.x, fmaf(a.y, b.y, gx));
-          gy = fmaf(a.x, b.y, fmaf(-a.y, b.x, gy));
-        }
-        for (int o = 16; o > 0; o >>= 1) {
-          al += __shfl_xor_sync(0xffffffffu, al, o);
-          be += __shfl_xor_sync(0xffffffffu, be, o);
-          gx += __shfl_xor_sync(0xffffffffu, gx, o);
-          gy += __shfl_xor_sync(0xffffffffu, gy, o);
-        }
-        const float mag = sqrtf(gx * gx + gy * gy);
-        if (!(mag > 4e-6f * sqrtf(al * be)) || !(mag > floor_g)) continue;   // orthogonal to float32 accuracy
-        rotated = true;
-        // 2x2 Hermitian [[al, g], [conj g, be]]: U = [[c, -s e^{i phi}], [s e^{-i phi}, c]],
-        // cot 2theta = (al - be) / 2|g|; columns: y_p' = c y_p + s e^{-i phi} y_q, y_q' = c y_q - s e^{i phi} y_p
-        const float kap = (al - be) / (2.f * mag);
-        const float t = (kap >= 0.f ? 1.f : -1.f) / (fabsf(kap) + sqrtf(1.f + kap * kap));
-        const float c = rsqrtf(1.f + t * t), sn = t * c;
-        const float2 e = make_float2(gx / mag, gy / mag), ec = make_float2(e.x, -e.y);
-        for (int kk = lane; kk < np; kk += 32) {
-          const float2 a = Yq[kk * r + pp], b = Yq[kk * r + qq];
-          const float2 b_ec = cmul(b, ec), a_e = cmul(a, e);
-          Yq[kk * r + pp] = make_float2(c * a.x + sn * b_ec.x, c * a.y + sn * b_ec.y);
-          Yq[kk * r + qq] = make_float2(c * b.x - sn * a_e.x, c * b.y - sn * a_e.y);
-        }
-        if (lane < r) {
-          const float2 a = Vm[lane * r + pp], b = Vm[lane * r + qq];
-          const float2 b_ec = cmul(b, ec), a_e = cmul(a, e);
-          Vm[lane * r + pp] = make_float2(c * a.x + sn * b_ec.x, c * a.y + sn * b_ec.y);
-          Vm[lane * r + qq] = make_float2(c * b.x - sn * a_e.x, c * b.y - sn * a_e.y);
-        }
-        __syncwarp();
+  const float2* Yb = Y + ((size_t)y0 * N + x0) * r;   // row k of Y_q: Yb + ((k / p) * N + k % p) * r
+  // 1. Gram G[i][j] = sum_k conj(Y[k][i]) Y[k][j], upper triangle entries strided over the lanes
+  double tr = 0.0;
+  for (int e = lane; e < r * (r + 1) / 2; e += 32) {
+    int i = 0, rem = e;
+    while (rem >= r - i) { rem -= r - i; ++i; }
+    const int j = i + rem;
+    double gx = 0.0, gy = 0.0;
+    for (int yy = 0; yy < p; ++yy) {
+      const float2* row = Yb + (size_t)yy * N * r;
+      for (int xx = 0; xx < p; ++xx, row += r) {
+        const float2 a = __ldg(row + i), b = __ldg(row + j);
+        gx = fma((double)a.x, (double)b.x, fma((double)a.y, (double)b.y, gx));
+        gy = fma((double)a.x, (double)b.y, fma(-(double)a.y, (double)b.x, gy));
       }
+    }
+    A[i * rp + j] = make_double2(gx, gy);
+    A[j * rp + i] = make_double2(gx, -gy);
+    if (i == j) tr += gx;
+  }
+  for (int e = lane; e < rp * rp; e += 32) {
+    const int i = e / rp, j = e % rp;
+    if (i >= r || j >= r) A[e] = make_double2(0.0, 0.0);   // padding row / column of odd r
+    Wm[e] = make_double2(i == j ? 1.0 : 0.0, 0.0);
+  }
+  for (int o = 16; o > 0; o >>= 1) tr += __shfl_xor_sync(0xffffffffu, tr, o);
+  // |g| <= 1e-14 tr is zero at the scale of ||Y_q||_F^2: the eigenvalues then carry an absolute
+  // error <= ~1e-14 ||Y_q||_F^2, and M = W F W^H an error ~1e-14 ||Y_q||_F^2 / tau^2
+  const double floor_g = 1e-14 * tr;
+  // lane = (group g, index c): groups of w = 16 lanes (rp <= 16) or one group of 32
+  const int w = rp <= 16 ? 16 : 32, G = 32 / w, g = lane / w, c = lane % w;
+  int2* pr = reinterpret_cast<int2*>(M);   // round's pairs (M is free until step 3)
+  __syncwarp();
+  // 2. cyclic Jacobi, round-robin pairs: round t, slot k: (t, rp-1) for k = 0, else
+  //    ((t + k) mod (rp-1), (t - k) mod (rp-1))
+  for (int sweep = 0; sweep < 30; ++sweep) {
+    bool rotated = false;
+    for (int t = 0; t < rp - 1; ++t) {
+      if (lane < half) {
+        int a = lane ? (t + lane) % (rp - 1) : t, b = lane ? (t - lane + rp - 1) % (rp - 1) : rp - 1;
+        if (a > b) { const int u = a; a = b; b = u; }
+        double4 R = make_double4(1.0, 0.0, 1.0, 0.0);
+        if (b < r) {
+          const double al = A[a * rp + a].x, be = A[b * rp + b].x;
+          const double2 gg = A[a * rp + b];
+          const double mag = sqrt(gg.x * gg.x + gg.y * gg.y);
+          if (mag > floor_g) {
+            // A <- J^H A J with J = [[c, -s e], [s conj(e), c]] on (a, b), e = g / |g|:
+            // cot 2theta = (al - be) / 2|g| zeroes the (a, b) entry
+            const double kap = (al - be) / (2.0 * mag);
+            const double tt = (kap >= 0.0 ? 1.0 : -1.0) / (fabs(kap) + sqrt(1.0 + kap * kap));
+            const double cs = 1.0 / sqrt(1.0 + tt * tt);
+            R = make_double4(cs, tt * cs, gg.x / mag, gg.y / mag);
+          }
+        }
+        rot[lane] = R;
+        pr[lane] = make_int2(a, b);
+        rotated |= R.y != 0.0;
+      }
+      rotated = __any_sync(0xffffffffu, rotated);
+      __syncwarp();
+      // rows a, b: A[a][k] <- c A[a][k] + s e A[b][k],  A[b][k] <- c A[b][k] - s conj(e) A[a][k]
+      for (int k = g; k < half; k += G) {
+        const double4 R = rot[k];
+        if (R.y == 0.0 || c >= r) continue;
+        const int2 ab = pr[k];
+        const double2 x = A[ab.x * rp + c], y = A[ab.y * rp + c];
+        const double2 ey = zmul(make_double2(R.z, R.w), y), ecx = zmul(make_double2(R.z, -R.w), x);
+        A[ab.x * rp + c] = make_double2(R.x * x.x + R.y * ey.x, R.x * x.y + R.y * ey.y);
+        A[ab.y * rp + c] = make_double2(R.x * y.x - R.y * ecx.x, R.x * y.y - R.y * ecx.y);
+      }
+      __syncwarp();
+      // columns a, b of A and of W: X[k][a] <- c X[k][a] + s conj(e) X[k][b],
+      // X[k][b] <- c X[k][b] - s e X[k][a]
+      for (int mk = g; mk < 2 * half; mk += G) {
+        const double4 R = rot[mk >> 1];
+        if (R.y == 0.0 || c >= r) continue;
+        const int2 ab = pr[mk >> 1];
+        double2* X = (mk & 1) ? Wm : A;
+        const double2 x = X[c * rp + ab.x], y = X[c * rp + ab.y];
+        const double2 ecy = zmul(make_double2(R.z, -R.w), y), ex = zmul(make_double2(R.z, R.w), x);
+        X[c * rp + ab.x] = make_double2(R.x * x.x + R.y * ecy.x, R.x * x.y + R.y * ecy.y);
+        X[c * rp + ab.y] = make_double2(R.x * y.x - R.y * ex.x, R.x * y.y - R.y * ex.y);
+      }
+      __syncwarp();
+    }
     if (!rotated) break;
   }
-  // sigma_j = |yhat_j|; f_j = max(1 - tau / sigma_j, 0) held by lane j; nuclear norm = sum sigma
-  float fj = 0.f;
+  // sigma_j = sqrt(lambda_j); f_j = max(1 - tau / sigma_j, 0) (kept in the rot scratch)
+  double* f = reinterpret_cast<double*>(rot);
   double sig = 0.0;
   for (int j = 0; j < r; ++j) {
-    float n2 = 0.f;
-    for (int kk = lane; kk < np; kk += 32) {
-      const float2 a = Yq[kk * r + j];
-      n2 = fmaf(a.x, a.x, fmaf(a.y, a.y, n2));
-    }
-    for (int o = 16; o > 0; o >>= 1) n2 += __shfl_xor_sync(0xffffffffu, n2, o);
-    const float sj = sqrtf(n2);
+    const double sj = sqrt(fmax(A[j * rp + j].x, 0.0));
     sig += sj;
-    if (lane == j) fj = sj > tau ? 1.f - tau / sj : 0.f;
+    if (lane == 0) f[j] = sj > (double)tau ? 1.0 - (double)tau / sj : 0.0;
   }
   if (lane == 0) nuc[q] = sig;
-  // P_q = Yhat diag(f) V^H:  P[k][j'] = sum_j Yhat[k][j] f_j conj(V[j'][j])
+  __syncwarp();
+  // 3. M = W F W^H
+  for (int e = lane; e < r * r; e += 32) {
+    const int a = e / r, b = e % r;
+    double2 acc = make_double2(0.0, 0.0);
+    for (int j = 0; j < r; ++j) {
+      const double2 wa = Wm[a * rp + j], wb = Wm[b * rp + j];
+      const double2 t = zmul(wa, make_double2(wb.x, -wb.y));
+      acc.x = fma(f[j], t.x, acc.x);
+      acc.y = fma(f[j], t.y, acc.y);
+    }
+    M[e] = make_float2((float)acc.x, (float)acc.y);
+  }
+  __syncwarp();
+  // P_q = Y_q M:  P[k][j'] = sum_j Y[k][j] M[j][j'];  lane = (row group g, column c)
   float2* Pq = P + (size_t)q * np * r;
-  for (int e0 = 0; e0 < np * r; e0 += 32) {   // all lanes stay in the loop (shuffles)
-    const int e = e0 + lane;
-    const bool ok = e < np * r;
-    const int kk = ok ? e / r : 0, jp = ok ? e % r : 0;
+  for (int kk = g; kk < np; kk += G) {
+    if (c >= r) continue;
+    const float2* row = Yb + ((size_t)(kk / p) * N + kk % p) * r;
     float2 acc = make_float2(0.f, 0.f);
     for (int j = 0; j < r; ++j) {
-      const float f = __shfl_sync(0xffffffffu, fj, j);
-      const float2 v = Vm[jp * r + j];
-      const float2 t = cmul(Yq[kk * r + j], make_float2(v.x, -v.y));
-      acc.x = fmaf(f, t.x, acc.x);
-      acc.y = fmaf(f, t.y, acc.y);
+      const float2 t = cmul(__ldg(row + j), M[j * r + c]);
+      acc.x += t.x;
+      acc.y += t.y;
     }
-    if (ok) Pq[e] = acc;
+    Pq[kk * r + c] = acc;
   }
 }
 
@@ -423,46 +472,6 @@ static __global__ void k_mfd_gather(const float2* __restrict__ YX, const int* __
     const int k = e / r, i = e % r;
     Qm[(size_t)q * np * r + e] = YX[((size_t)(y0 + k / p) * N + x0 + k % p) * r + i];
   }
-}
-
-// C[n][M] = W[n][n] B[n][M] (fp32, W symmetric real; B, C real views of complex blocks).
-// 64 x 64 output tile per 256-thread block, 4 x 4 outputs per thread, K chunks of 16 via smem.
-static __global__ void __launch_bounds__(256) k_mfd_sgemm(const float* __restrict__ W, const float* __restrict__ B, int n,
-                                                          int M, float* __restrict__ C) {
-  __shared__ float As[16][65], Bs[16][65];
-  const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
-  const int row0 = blockIdx.y * 64, col0 = blockIdx.x * 64;
-  float acc[4][4] = {};
-  for (int k0 = 0; k0 < n; k0 += 16) {
-    for (int e = threadIdx.x; e < 16 * 64; e += 256) {
-      const int kk = e / 64, c = e % 64;
-      // A tile: W[row0 + c][k0 + kk] read as W[k0 + kk][row0 + c] (symmetric) -> coalesced over c
-      As[kk][c] = (row0 + c < n && k0 + kk < n) ? W[(size_t)(k0 + kk) * n + row0 + c] : 0.f;
-      Bs[kk][c] = (k0 + kk < n && col0 + c < M) ? B[(size_t)(k0 + kk) * M + col0 + c] : 0.f;
-    }
-    __syncthreads();
-#pragma unroll
-    for (int kk = 0; kk < 16; ++kk) {
-      float a[4], b[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        a[u] = As[kk][ty + 16 * u];
-        b[u] = Bs[kk][tx + 16 * u];
-      }
-#pragma unroll
-      for (int u = 0; u < 4; ++u)
-#pragma unroll
-        for (int v = 0; v < 4; ++v) acc[u][v] = fmaf(a[u], b[v], acc[u][v]);
-    }
-    __syncthreads();
-  }
-#pragma unroll
-  for (int u = 0; u < 4; ++u)
-#pragma unroll
-    for (int v = 0; v < 4; ++v) {
-      const int rr = row0 + ty + 16 * u, cc = col0 + tx + 16 * v;
-      if (rr < n && cc < M) C[(size_t)rr * M + cc] = acc[u][v];
-    }
 }
 
 // Y[v] -= scale * sum_{q covering v} (deg_q Qm_q[v] - G_q[v])   (Q^*(Q(X) L) in coefficients);

@@ -1,6 +1,7 @@
 // status.h -- internal error helpers shared by the library's translation units (not public API).
 // fail() records the message returned by mrf_last_error(); CUDA_TRY / MRF_TRY propagate errors.
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <string>
@@ -11,6 +12,11 @@ namespace mrf {
 mrf_status fail(mrf_status s, const std::string& msg);
 mrf_status check_launch(const char* what);   // cudaGetLastError after a launch
 void plan_dims(mrf_plan plan, int* N, int* L, int* C, int* device);   // mrfnufft.cu
+// 2D tiled TMA map over a row-major [rows][cols] array (row pitch row_bytes, a multiple of 16):
+// (box_cols x box_rows) boxes, 128-byte swizzle (box_cols x element size = 128), out-of-bounds
+// elements read as zero.  dict.cu.
+mrf_status tmap_2d(CUtensorMap* m, CUtensorMapDataType type, const void* base, uint64_t cols, uint64_t rows,
+                   uint64_t row_bytes, uint32_t box_cols, uint32_t box_rows);
 }  // namespace mrf
 
 #define CUDA_TRY(expr)                                                                           \

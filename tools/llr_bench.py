@@ -1,8 +1,11 @@
-"""Time the LLR outer step (mrf_llr_step) at the MRF size: 256 x 256 x 1000 frames, 2500 patches."""
+"""Time the MS-LLR outer step (mrf_llr_step) at the MRF size: 256 x 256 x 1000 frames, 2500
+patches, with lambda_1 = 0 (LLR ablation) and with the manifold term (Laplacian from maps)."""
 import os
 import sys
+import time
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
 import synth  # noqa: E402
@@ -18,13 +21,29 @@ op = binding.LLR(dic, cfg.N)
 x = torch.from_numpy(synth.images(cfg)).cuda()
 rhs = pl.adjoint(pl.forward(x))
 xo = torch.empty_like(x)
-for _ in range(3):
-    op.step(pl, rhs, rhs, x_out=xo, nuclear=False)
+maps = sd.parameter_maps(cfg.N, 3)
+params = torch.from_numpy(np.ascontiguousarray(np.stack([maps[0].ravel(), maps[1].ravel()], 1))).float().cuda()
+pdm = torch.from_numpy(np.ascontiguousarray(maps[2].ravel())).float().cuda()
+op.laplacian(params, pdm)
 torch.cuda.synchronize()
-s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-s.record()
-for _ in range(5):
-    op.step(pl, rhs, rhs, x_out=xo, nuclear=False)
-e.record()
+t0 = time.perf_counter()
+s2, mdeg = op.laplacian(params, pdm)
 torch.cuda.synchronize()
-print(f"llr step: {s.elapsed_time(e) / 5:.3f} ms (rank {d.shape[0]})")
+print(f"laplacian: {1e3 * (time.perf_counter() - t0):.1f} ms (sigma2 {s2:.3f}, max degree {mdeg:.1f})")
+
+
+def timed(lam1):
+    for _ in range(3):
+        op.step(pl, rhs, rhs, x_out=xo, nuclear=False, lam1=lam1)
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(5):
+        op.step(pl, rhs, rhs, x_out=xo, nuclear=False, lam1=lam1)
+    e.record()
+    torch.cuda.synchronize()
+    return s.elapsed_time(e) / 5
+
+
+print(f"llr step (lambda1 = 0): {timed(0.0):.3f} ms; ms-llr step (lambda1 > 0): {timed(0.1 * mdeg / 100):.3f} ms "
+      f"(rank {d.shape[0]})")
