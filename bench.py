@@ -402,7 +402,7 @@ def run_ours(args):
                          "(PAPER.md:319 grid, surrogate fingerprints)"}
         dic.close()
 
-    # ---------------------------------------------------------------- LLR outer step (lambda_1 = 0)
+    # ---------------------------------------------------------------- (MS-)LLR outer step and Algorithm 1
     llr_res = None
     if not args.no_llr and world == 1 and cfg.C == 1:
         import synth.dictionary as sdict
@@ -416,11 +416,35 @@ def run_ours(args):
         xl = torch.empty_like(xbuf)
         ms_llr = time_op(lambda: op.step(plan, xbuf, rhs_l, 1.0, 0.1, 0.2, x_out=xl, nuclear=False), 5)
         nc = len(range(0, cfg.N - 11 + 1, 5)) + (0 if (cfg.N - 11) % 5 == 0 else 1)
+        # the manifold term (lambda_1 > 0): maps by Phi_D, the Laplacian, the MS-LLR step, the cost
+        _, pd_m, par_m = dic.match(xbuf)
+        ms_lap = time_op(lambda: op.laplacian(par_m, pd_m), 3)
+        _, maxdeg = op.laplacian(par_m, pd_m)
+        lam1 = 1e-7 * maxdeg                      # lambda_1^0 max(L) with lambda_1^0 = 1e-7
+        ms_ms = time_op(lambda: op.step(plan, xbuf, rhs_l, 1.0, 0.1, 0.2, x_out=xl, nuclear=False, lam1=lam1), 5)
+        ms_cost = time_op(lambda: op.cost(plan, xl, y, lam1=lam1, lam2=0.1), 3)
+
+        def solve_s(n, l1):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            op.solve(dic, plan, y, mu=0.018, lam1=l1, lam2=0.1, beta=0.2, max_iter=n, tol=0.0)
+            torch.cuda.synchronize()
+            return (time.perf_counter() - t0) * 1e3
+
+        solve_s(1, 1e-7)
+        it_llr = (solve_s(5, 0.0) - solve_s(1, 0.0)) / 4
+        it_ms = (solve_s(5, 1e-7) - solve_s(1, 1e-7)) / 4
         llr_res = {"ms_per_step": ms_llr, "ms_normal_inside": ms_normal, "rank": int(d_basis.shape[0]),
                    "patches": nc * nc, "basis_ms": basis_ms,
-                   "note": "mrf_llr_step: Z = P_S(X - mu(A^H A X - A^H b)), per-patch SVT (11x11, stride 5, "
-                           "tau = 1/beta = 5) in subspace coordinates, overlap-exact X update; mu = 1, "
-                           "lambda_2 = 0.1, beta = 1/5 (PAPER.md:304); basis from the synthetic dictionary"}
+                   "ms_per_step_manifold": ms_ms, "ms_laplacian": ms_lap, "ms_cost": ms_cost,
+                   "ms_per_algorithm1_iteration": {"llr": it_llr, "ms_llr": it_ms,
+                                                   "note": "mrf_msllr_solve wall clock (T(5) - T(1)) / 4: step + "
+                                                           "cost (+ Phi_D + Laplacian update for MS-LLR); "
+                                                           "mu = 0.018 (< 1/lambda_max), lambda_1^0 = 1e-7"},
+                   "note": "mrf_llr_step: Z = P_S(X - mu(A^H A X - A^H b) [+ mu lambda_1 Q*(Q(X) L)]), per-patch "
+                           "SVT (11x11, stride 5, tau = 1/beta = 5) in subspace coordinates, overlap-exact X "
+                           "update; mu = 1, lambda_2 = 0.1, beta = 1/5 (PAPER.md:304); basis from the synthetic "
+                           "dictionary; manifold GEMM on tcgen05 (tf32 x3)"}
         op.close()
         dic.close()
         del xl, rhs_l

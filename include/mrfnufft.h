@@ -226,13 +226,48 @@ mrf_status mrf_llr_laplacian(mrf_llr llr, const float* params, const float* pd, 
  *   x_out = (Z + gamma Q^*(P)) / (1 + gamma c)              (Eq. 21, gamma = mu lambda2 beta, c = patch count)
  * lambda1 = 0 is the paper's LLR ablation; lambda1 > 0 needs mrf_llr_laplacian (the manifold term
  * is evaluated on P_S x: P_S commutes with the patch operators).  The SVT runs in subspace
- * coordinates (Z lies in span(d): a p^2 x r one-sided Jacobi SVD per patch).  x_out may alias x
+ * coordinates (Z lies in span(d): a float64 r x r Gram eigendecomposition per patch).  x_out may alias x
  * when lambda1 = 0 and penalty is NULL.  nuclear (nullable): sum_q ||Q_q(Z)||_*; penalty
  * (nullable, needs the Laplacian): Tr(Q(P_S x) L Q(P_S x)^H) -- the cost terms of Algorithm 1;
  * either synchronises the stream.  Errors: MRF_EINVAL (mu <= 0, lambda1 < 0, lambda2 < 0,
  * beta <= 0, null, misaligned, plan shape), errors of mrf_normal. */
 mrf_status mrf_llr_step(mrf_llr llr, mrf_plan plan, const void* x, const void* rhs, float mu, float lambda1,
                         float lambda2, float beta, void* x_out, double* nuclear, double* penalty, void* stream);
+/* Cost of Algorithm 1 at x, DEVICE x [L][N][N] and b [L][C][M] (16-byte aligned):
+ *   terms[0] = 1/2 ||A x - b||_F^2,  terms[1] = Tr(Q(P_S x) L Q(P_S x)^H) (0 without a Laplacian),
+ *   terms[2] = sum_q ||Q_q(P_S x)||_*,  *cost = terms[0] + lambda1 terms[1] + lambda2 terms[2].
+ * The regularisers are evaluated on P_S x (equal to x for the iterates of mrf_llr_step).  Both
+ * outputs HOST, nullable; float64 reductions in a fixed order; synchronises the stream.  Uses the
+ * operator's workspaces (not concurrently with mrf_llr_step on another stream).  Errors:
+ * MRF_EINVAL (null, lambda < 0, lambda1 > 0 without a Laplacian, plan shape), errors of mrf_forward. */
+mrf_status mrf_llr_cost(mrf_llr llr, mrf_plan plan, const void* x, const void* b, float lambda1, float lambda2,
+                        double* cost, double* terms, void* stream);
+
+/* Algorithm 1 of the paper, MS-LLR reconstruction and parameter maps:
+ *   X^0 = A^* b;  M^0 = Phi_D(X^0);  L^0 and lambda_1 = lambda1 max(L^0)     (lambda1 > 0 only)
+ *   for n = 1 .. max_iter:  X^n = mrf_llr_step(X^{n-1});  cost(n) = mrf_llr_cost(X^n)
+ *                           stop if n >= 2 and cost(n-1)/cost(n) - 1 < tol     (reading 27)
+ *                           M^{n+1} = Phi_D(X^n);  L^{n+1};  lambda_1 = lambda1 max(L^{n+1})
+ *   outputs X^ (in x) and M^ = Phi_D(X^) (index, pd, params).
+ * lambda1 = 0 is the LLR-only reconstruction (no maps inside the loop).  lambda1 > 0 needs a
+ * dictionary LUT of (T1, T2) (P = 2) and params.  b: DEVICE [L][C][M]; x: DEVICE [L][N][N] (out);
+ * index int32 [V], pd float [V], params float [V][P] (nullable when lambda1 = 0): DEVICE.
+ * info (nullable): iterations run, cost(1..iters) into info->cost (HOST, max_iter entries, nullable)
+ * and the last lambda_1.  Allocates two image stacks on first use; synchronises.  Errors: MRF_EINVAL,
+ * and the errors of the calls above. */
+typedef struct {
+  float mu, lambda1, lambda2, beta;   /* Eq. 15 step, lambda_1^0, lambda_2, beta (SVT threshold 1/beta) */
+  int max_iter;                       /* N_max */
+  double tol;                         /* stop-rule tolerance (1e-5); <= 0: run max_iter */
+  double sigma2;                      /* Laplacian bandwidth; <= 0: the median rule at every update */
+} mrf_msllr_params;
+typedef struct {
+  int iters;
+  double* cost;                       /* HOST [max_iter] or NULL */
+  double lambda1;                     /* lambda_1 of the last step */
+} mrf_msllr_info;
+mrf_status mrf_msllr_solve(mrf_llr llr, mrf_dict dict, mrf_plan plan, const void* b, const mrf_msllr_params* prm,
+                           void* x, int* index, float* pd, float* params, mrf_msllr_info* info, void* stream);
 mrf_status mrf_llr_destroy(mrf_llr llr);
 
 /* enable != 0 brackets every subsequent tensor-core GEMM launch (k_dict_gemm) of mrf_dict_match

@@ -33,7 +33,7 @@ EXPORTED = [
     "mrf_profile_query", "mrf_nccl_get_unique_id", "mrf_nccl_comm_init", "mrf_nccl_comm_destroy",
     "mrf_adjoint_dcf", "mrf_dcf_weights", "mrf_dict_create", "mrf_dict_match", "mrf_dict_destroy",
     "mrf_dict_profile", "mrf_dict_profile_query", "mrf_dict_basis", "mrf_dict_basis_copy", "mrf_llr_create",
-    "mrf_llr_step", "mrf_llr_destroy", "mrf_llr_laplacian",
+    "mrf_llr_step", "mrf_llr_destroy", "mrf_llr_laplacian", "mrf_llr_cost", "mrf_msllr_solve",
 ]
 
 
@@ -53,6 +53,16 @@ class PlanDesc(ctypes.Structure):
         ("device", ctypes.c_int), ("stream", ctypes.c_void_p), ("nccl_comm", ctypes.c_void_p),
         ("batch_frames", ctypes.c_int),
     ]
+
+
+class MsllrParams(ctypes.Structure):
+    _fields_ = [("mu", ctypes.c_float), ("lambda1", ctypes.c_float), ("lambda2", ctypes.c_float),
+                ("beta", ctypes.c_float), ("max_iter", ctypes.c_int), ("tol", ctypes.c_double),
+                ("sigma2", ctypes.c_double)]
+
+
+class MsllrInfo(ctypes.Structure):
+    _fields_ = [("iters", ctypes.c_int), ("cost", ctypes.POINTER(ctypes.c_double)), ("lambda1", ctypes.c_double)]
 
 
 class CGInfo(ctypes.Structure):
@@ -98,6 +108,10 @@ def _load() -> ctypes.CDLL:
         "mrf_llr_laplacian": ([vp, vp, vp, ctypes.c_double, ctypes.POINTER(ctypes.c_double),
                                ctypes.POINTER(ctypes.c_double), vp], ci),
         "mrf_llr_destroy": ([vp], ci),
+        "mrf_llr_cost": ([vp, vp, vp, vp, cf, cf, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double),
+                          vp], ci),
+        "mrf_msllr_solve": ([vp, vp, vp, vp, ctypes.POINTER(MsllrParams), vp, vp, vp, vp, ctypes.POINTER(MsllrInfo),
+                             vp], ci),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)
@@ -382,10 +396,12 @@ class Dictionary:
 
 
 class LLR:
-    """The LLR outer step of Algorithm 1 with lambda_1 = 0 (include/mrfnufft.h mrf_llr_*).
+    """The (MS-)LLR outer step of Algorithm 1 (include/mrfnufft.h mrf_llr_*, mrf_msllr_solve).
 
     Needs ``dictionary.basis(...)`` first.  ``step(plan, x, rhs, mu, lam2, beta)`` returns
-    (x_next, nuclear) for CUDA complex64 [L][N][N] x and rhs = A^H b.
+    (x_next, nuclear, penalty) for CUDA complex64 [L][N][N] x and rhs = A^H b; ``laplacian``
+    builds the manifold term's graph Laplacian from Phi_D's maps; ``cost`` evaluates Algorithm 1's
+    cost; ``solve`` runs Algorithm 1 end to end.
     """
 
     def __init__(self, dictionary: "Dictionary", N: int, p: int = 11, s: int = 5):
@@ -421,6 +437,38 @@ class LLR:
                                 ctypes.byref(nuc) if nuclear else None, ctypes.byref(pen) if penalty else None,
                                 ctypes.c_void_p(st)))
         return x_out, (nuc.value if nuclear else None), (pen.value if penalty else None)
+
+    def cost(self, plan: "Plan", x, b, lam1: float = 0.0, lam2: float = 0.1):
+        """Algorithm 1's cost at x (b = k-space [L][C][M]): (cost, (data, manifold, nuclear))."""
+        x = _as_c64(x, (self.L, self.N, self.N), "x")
+        if not (x.is_cuda and b.is_cuda and b.dtype == torch.complex64 and b.is_contiguous()):
+            raise TypeError("x and b must be contiguous CUDA complex64 tensors")
+        c = ctypes.c_double()
+        t = (ctypes.c_double * 3)()
+        st = torch.cuda.current_stream(x.device).cuda_stream
+        _check(lib.mrf_llr_cost(self._h, plan._h, _ptr(x), _ptr(b), ctypes.c_float(lam1), ctypes.c_float(lam2),
+                                ctypes.byref(c), t, ctypes.c_void_p(st)))
+        return c.value, (t[0], t[1], t[2])
+
+    def solve(self, dictionary: "Dictionary", plan: "Plan", b, mu: float = 1.0, lam1: float = 0.0,
+              lam2: float = 0.1, beta: float = 0.2, max_iter: int = 10, tol: float = 1e-5, sigma2: float = 0.0):
+        """Algorithm 1 (mrf_msllr_solve).  Returns dict(x, index, pd, params, iters, cost, lambda1)."""
+        if not (isinstance(b, torch.Tensor) and b.is_cuda and b.dtype == torch.complex64 and b.is_contiguous()):
+            raise TypeError("b must be a contiguous CUDA complex64 tensor [L][C][M]")
+        dev = b.device
+        V = self.N * self.N
+        x = torch.empty((self.L, self.N, self.N), dtype=torch.complex64, device=dev)
+        index = torch.empty(V, dtype=torch.int32, device=dev)
+        pd = torch.empty(V, dtype=torch.float32, device=dev)
+        params = torch.empty((V, dictionary.P), dtype=torch.float32, device=dev) if dictionary.P else None
+        prm = MsllrParams(mu, lam1, lam2, beta, int(max_iter), tol, sigma2)
+        cost = (ctypes.c_double * max(int(max_iter), 1))()
+        info = MsllrInfo(0, ctypes.cast(cost, ctypes.POINTER(ctypes.c_double)), 0.0)
+        st = torch.cuda.current_stream(dev).cuda_stream
+        _check(lib.mrf_msllr_solve(self._h, dictionary._h, plan._h, _ptr(b), ctypes.byref(prm), _ptr(x), _ptr(index),
+                                   _ptr(pd), _ptr(params), ctypes.byref(info), ctypes.c_void_p(st)))
+        return {"x": x, "index": index, "pd": pd, "params": params, "iters": info.iters,
+                "cost": [cost[i] for i in range(info.iters)], "lambda1": info.lambda1}
 
     def close(self):
         if getattr(self, "_h", None):

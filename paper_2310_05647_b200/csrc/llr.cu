@@ -27,6 +27,10 @@ struct mrf_llr_s {
   float2* nx = nullptr;       // [L][N][N] A^H A x
   double* nuc = nullptr;      // [nc*nc] per-patch nuclear norms
   std::vector<double> nuc_h;
+  float2* yb = nullptr;       // [L][C][M] A x of mrf_llr_cost
+  size_t ny = 0;
+  double* part = nullptr;     // [kStatBlocks] partial sums
+  float2 *rhs = nullptr, *x2 = nullptr;   // mrf_msllr_solve: A^H b and the second iterate buffer
   // manifold term (mrf_llr_laplacian)
   bool has_lap = false;
   float* W = nullptr;         // [n][n] similarity weights (Eq. 8), first the squared distances
@@ -50,12 +54,84 @@ static void llr_free(mrf_llr_s* h) {
   cudaSetDevice(h->device);
   for (void* v : {(void*)h->dT, (void*)h->corners, (void*)h->Y, (void*)h->P, (void*)h->nx, (void*)h->nuc, (void*)h->W,
                   (void*)h->deg, (void*)h->pv, (void*)h->hist, (void*)h->stats, (void*)h->YX, (void*)h->Qm,
-                  (void*)h->Gm, (void*)h->pen, (void*)h->Wh, (void*)h->Wl, (void*)h->Qh, (void*)h->Ql})
+                  (void*)h->Gm, (void*)h->pen, (void*)h->Wh, (void*)h->Wl, (void*)h->Qh, (void*)h->Ql, (void*)h->yb, (void*)h->part, (void*)h->rhs, (void*)h->x2})
     if (v) cudaFree(v);
   delete h;
 }
 
 static size_t svt_smem(int r) { return (llr::kSvtThreads / 32) * llr::svt_warp_bytes(r); }
+
+
+// manifold-term workspaces (first use): YX, Qm, Gm, per-patch penalties, Qm^T hi / lo + tensor maps
+static mrf_status manifold_ws(mrf_llr_s* h) {
+  if (h->YX) return MRF_OK;
+  const int V = h->N * h->N, n = h->nc * h->nc, blk = h->p * h->p * h->r;
+  bool ok = cudaMalloc((void**)&h->YX, (size_t)V * h->r * sizeof(float2)) == cudaSuccess &&
+            cudaMalloc((void**)&h->Qm, (size_t)n * blk * sizeof(float2)) == cudaSuccess &&
+            cudaMalloc((void**)&h->Gm, (size_t)n * blk * sizeof(float2)) == cudaSuccess &&
+            cudaMalloc((void**)&h->pen, (size_t)n * sizeof(double)) == cudaSuccess &&
+            cudaMalloc((void**)&h->Qh, (size_t)2 * blk * h->nK * sizeof(float)) == cudaSuccess &&
+            cudaMalloc((void**)&h->Ql, (size_t)2 * blk * h->nK * sizeof(float)) == cudaSuccess;
+  if (!ok) return fail(MRF_ENOMEM, "manifold workspace allocation failed");
+  MRF_TRY(tmap_2d(&h->tQh, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, h->Qh, n, 2 * blk, (uint64_t)h->nK * 4, g3::BK, g3::BN));
+  MRF_TRY(tmap_2d(&h->tQl, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, h->Ql, n, 2 * blk, (uint64_t)h->nK * 4, g3::BK, g3::BN));
+  return MRF_OK;
+}
+
+// Qm = Q(coef) (patch blocks of the [V][r] coefficients), Gm = W Qm on the tensor cores
+static mrf_status manifold_G(mrf_llr_s* h, const float2* coef, cudaStream_t st) {
+  const int n = h->nc * h->nc, blk = h->p * h->p * h->r;
+  mfd::k_mfd_gather<<<n, 128, 0, st>>>(coef, h->corners, h->nc, h->N, h->p, h->r, h->Qm);
+  const int M2 = 2 * blk;   // G [n][M2] = W [n][n] Qm [n][M2]: A = W (K-major), B = Qm^T [M2][n]
+  const dim3 gs((unsigned)((M2 + 31) / 32), (unsigned)((n + 31) / 32));
+  g3::k_g3_split<true><<<gs, 256, 0, st>>>(reinterpret_cast<const float*>(h->Qm), n, M2, M2, h->Qh, h->Ql, h->nK);
+  const int mt = (n + g3::BM - 1) / g3::BM, nt = (M2 + g3::BN - 1) / g3::BN;
+  g3::k_g3_gemm<<<std::min(mt * nt, h->sms), g3::THREADS, g3::SMEM, st>>>(
+      h->tWh, h->tWl, h->tQh, h->tQl, mt, nt, (n + g3::BK - 1) / g3::BK, n, M2, reinterpret_cast<float*>(h->Gm), M2);
+  return check_launch("k_g3_gemm");
+}
+
+// coefficients Y = (x - mu (nx - rhs)) d^dagger and, with yx, also x d^dagger
+static mrf_status coefs(mrf_llr_s* h, const float2* x, const float2* nx, const float2* rhs, float mu, float2* y,
+                        float2* yx, cudaStream_t st) {
+  const int V = h->N * h->N;
+  const unsigned gv = (unsigned)((V + 31) / 32);   // 32 voxels x NG frame groups per block
+  if (h->r <= 16) {
+    if (yx) llr::k_llr_coef<16, true><<<gv, 32 * llr::coef_groups<16>(), 0, st>>>(x, nx, rhs, h->dT, h->r, h->L, V, mu, y, yx);
+    else llr::k_llr_coef<16, false><<<gv, 32 * llr::coef_groups<16>(), 0, st>>>(x, nx, rhs, h->dT, h->r, h->L, V, mu, y, nullptr);
+  } else {
+    if (yx) llr::k_llr_coef<32, true><<<gv, 32 * llr::coef_groups<32>(), 0, st>>>(x, nx, rhs, h->dT, h->r, h->L, V, mu, y, yx);
+    else llr::k_llr_coef<32, false><<<gv, 32 * llr::coef_groups<32>(), 0, st>>>(x, nx, rhs, h->dT, h->r, h->L, V, mu, y, nullptr);
+  }
+  return check_launch("k_llr_coef");
+}
+
+// per-patch SVT of the coefficient blocks of Y (nuclear norms into h->nuc, thresholded blocks into h->P)
+static mrf_status svt(mrf_llr_s* h, float tau, cudaStream_t st) {
+  const int nq = h->nc * h->nc, ppb = llr::kSvtThreads / 32;
+  llr::k_llr_svt<<<(unsigned)((nq + ppb - 1) / ppb), llr::kSvtThreads, svt_smem(h->r), st>>>(
+      h->Y, h->corners, h->nc, h->N, h->p, h->r, tau, nq, h->P, h->nuc);
+  return check_launch("k_llr_svt");
+}
+
+// sum of n doubles copied from the device, in index order (synchronises)
+static mrf_status host_sum(const double* dev, int n, cudaStream_t st, double* out) {
+  std::vector<double> v(n);
+  CUDA_TRY(cudaMemcpyAsync(v.data(), dev, (size_t)n * sizeof(double), cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  double t = 0.0;
+  for (double a : v) t += a;
+  *out = t;
+  return MRF_OK;
+}
+
+static mrf_status check_plan(mrf_llr_s* h, mrf_plan plan, const char* who) {
+  int pN = 0, pL = 0, pC = 0, pdev = 0;
+  plan_dims(plan, &pN, &pL, &pC, &pdev);
+  if (pN != h->N || pL != h->L || pdev != h->device)
+    return fail(MRF_EINVAL, std::string(who) + ": the plan's N, L or device differ from the LLR operator's");
+  return MRF_OK;
+}
 
 extern "C" {
 
@@ -201,47 +277,16 @@ mrf_status mrf_llr_step(mrf_llr h, mrf_plan plan, const void* x, const void* rhs
   if (x_out == x && manifold) return fail(MRF_EINVAL, "mrf_llr_step: x_out may not alias x with the manifold term");
   for (const void* v : {x, rhs, (const void*)x_out})
     if ((uintptr_t)v % 16) return fail(MRF_EINVAL, "mrf_llr_step: arrays must be 16-byte aligned");
-  int pN = 0, pL = 0, pC = 0, pdev = 0;
-  plan_dims(plan, &pN, &pL, &pC, &pdev);
-  if (pN != h->N || pL != h->L || pdev != h->device)
-    return fail(MRF_EINVAL, "mrf_llr_step: the plan's N, L or device differ from the LLR operator's");
+  MRF_TRY(check_plan(h, plan, "mrf_llr_step"));
   CUDA_TRY(cudaSetDevice(h->device));
   cudaStream_t st = (cudaStream_t)stream;
   const int V = h->N * h->N, nq = h->nc * h->nc;
   // A^H A x (the plan checks that x has its shape: [L][N][N] device memory)
   MRF_TRY(mrf_normal(plan, x, h->nx, 0.f, stream));
-  const float2* xf = reinterpret_cast<const float2*>(x);
-  const unsigned gv = (unsigned)((V + 31) / 32);   // 32 voxels x NG frame groups per block
-  const int n = nq, np = h->p * h->p, blk = np * h->r;
-  if (manifold && !h->YX) {
-    bool ok = cudaMalloc((void**)&h->YX, (size_t)V * h->r * sizeof(float2)) == cudaSuccess &&
-              cudaMalloc((void**)&h->Qm, (size_t)n * blk * sizeof(float2)) == cudaSuccess &&
-              cudaMalloc((void**)&h->Gm, (size_t)n * blk * sizeof(float2)) == cudaSuccess &&
-              cudaMalloc((void**)&h->pen, (size_t)n * sizeof(double)) == cudaSuccess &&
-              cudaMalloc((void**)&h->Qh, (size_t)2 * blk * h->nK * sizeof(float)) == cudaSuccess &&
-              cudaMalloc((void**)&h->Ql, (size_t)2 * blk * h->nK * sizeof(float)) == cudaSuccess;
-    if (!ok) return fail(MRF_ENOMEM, "mrf_llr_step: manifold workspace allocation failed");
-    MRF_TRY(tmap_2d(&h->tQh, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, h->Qh, n, 2 * blk, (uint64_t)h->nK * 4, g3::BK, g3::BN));
-    MRF_TRY(tmap_2d(&h->tQl, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, h->Ql, n, 2 * blk, (uint64_t)h->nK * 4, g3::BK, g3::BN));
-  }
-  const float2* rh = (const float2*)rhs;
-  if (h->r <= 16) {
-    if (manifold) llr::k_llr_coef<16, true><<<gv, 32 * llr::coef_groups<16>(), 0, st>>>(xf, h->nx, rh, h->dT, h->r, h->L, V, mu, h->Y, h->YX);
-    else llr::k_llr_coef<16, false><<<gv, 32 * llr::coef_groups<16>(), 0, st>>>(xf, h->nx, rh, h->dT, h->r, h->L, V, mu, h->Y, nullptr);
-  } else {
-    if (manifold) llr::k_llr_coef<32, true><<<gv, 32 * llr::coef_groups<32>(), 0, st>>>(xf, h->nx, rh, h->dT, h->r, h->L, V, mu, h->Y, h->YX);
-    else llr::k_llr_coef<32, false><<<gv, 32 * llr::coef_groups<32>(), 0, st>>>(xf, h->nx, rh, h->dT, h->r, h->L, V, mu, h->Y, nullptr);
-  }
-  MRF_TRY(check_launch("k_llr_coef"));
+  if (manifold) MRF_TRY(manifold_ws(h));
+  MRF_TRY(coefs(h, (const float2*)x, h->nx, (const float2*)rhs, mu, h->Y, manifold ? h->YX : nullptr, st));
   if (manifold) {   // Y -= mu lambda1 coef(Q^*(Q(P_S x) L)),  L = D - W (Eq. 15's manifold term)
-    mfd::k_mfd_gather<<<n, 128, 0, st>>>(h->YX, h->corners, h->nc, h->N, h->p, h->r, h->Qm);
-    const int M2 = 2 * blk;   // G [n][M2] = W [n][n] Qm [n][M2]: A = W (K-major), B = Qm^T [M2][n]
-    const dim3 gs((unsigned)((M2 + 31) / 32), (unsigned)((n + 31) / 32));
-    g3::k_g3_split<true><<<gs, 256, 0, st>>>(reinterpret_cast<const float*>(h->Qm), n, M2, M2, h->Qh, h->Ql, h->nK);
-    const int mt = (n + g3::BM - 1) / g3::BM, nt = (M2 + g3::BN - 1) / g3::BN;
-    g3::k_g3_gemm<<<std::min(mt * nt, h->sms), g3::THREADS, g3::SMEM, st>>>(
-        h->tWh, h->tWl, h->tQh, h->tQl, mt, nt, (n + g3::BK - 1) / g3::BK, n, M2, reinterpret_cast<float*>(h->Gm), M2);
-    MRF_TRY(check_launch("k_g3_gemm"));
+    MRF_TRY(manifold_G(h, h->YX, st));
     if (lambda1 > 0.f) {
       if (h->r <= 16)
         mfd::k_mfd_apply<16><<<(unsigned)((V + 255) / 256), 256, 0, st>>>(h->Y, h->Qm, h->Gm, h->deg, h->corners, h->nc,
@@ -252,15 +297,13 @@ mrf_status mrf_llr_step(mrf_llr h, mrf_plan plan, const void* x, const void* rhs
       MRF_TRY(check_launch("k_mfd_apply"));
     }
     if (penalty) {
-      mfd::k_mfd_penalty<<<n, 256, 0, st>>>(h->Qm, h->Gm, h->deg, blk, h->pen);
+      mfd::k_mfd_penalty<<<nq, 256, 0, st>>>(h->Qm, h->Gm, h->deg, h->p * h->p * h->r, h->pen);
       MRF_TRY(check_launch("k_mfd_penalty"));
     }
   }
-  const int ppb = llr::kSvtThreads / 32;
-  llr::k_llr_svt<<<(unsigned)((nq + ppb - 1) / ppb), llr::kSvtThreads, svt_smem(h->r), st>>>(
-      h->Y, h->corners, h->nc, h->N, h->p, h->r, 1.f / beta, nq, h->P, h->nuc);
-  MRF_TRY(check_launch("k_llr_svt"));
+  MRF_TRY(svt(h, 1.f / beta, st));
   const float gamma = mu * lambda2 * beta;
+  const unsigned gv = (unsigned)((V + 31) / 32);
   if (h->r <= 16)
     llr::k_llr_update<16><<<gv, 256, 0, st>>>(h->Y, h->P, h->corners, h->nc, h->N, h->p, h->r, h->dT, h->L, gamma,
                                               (float2*)x_out);
@@ -268,20 +311,121 @@ mrf_status mrf_llr_step(mrf_llr h, mrf_plan plan, const void* x, const void* rhs
     llr::k_llr_update<32><<<gv, 256, 0, st>>>(h->Y, h->P, h->corners, h->nc, h->N, h->p, h->r, h->dT, h->L, gamma,
                                               (float2*)x_out);
   MRF_TRY(check_launch("k_llr_update"));
-  if (penalty) {   // Tr(Q(P_S x) L Q(P_S x)^H), patches summed in a fixed order (synchronises)
-    std::vector<double> pp(nq);
-    CUDA_TRY(cudaMemcpyAsync(pp.data(), h->pen, (size_t)nq * sizeof(double), cudaMemcpyDeviceToHost, st));
-    CUDA_TRY(cudaStreamSynchronize(st));
-    double t = 0.0;
-    for (double v : pp) t += v;
-    *penalty = t;
+  // Tr(Q(P_S x) L Q(P_S x)^H) and sum_q ||Q_q(Z)||_*: patches summed in a fixed order (synchronise)
+  if (penalty) MRF_TRY(host_sum(h->pen, nq, st, penalty));
+  if (nuclear) MRF_TRY(host_sum(h->nuc, nq, st, nuclear));
+  return MRF_OK;
+}
+
+mrf_status mrf_llr_cost(mrf_llr h, mrf_plan plan, const void* x, const void* b, float lambda1, float lambda2,
+                        double* cost, double* terms, void* stream) {
+  if (!h || !plan || !x || !b) return fail(MRF_EINVAL, "mrf_llr_cost: null argument");
+  if (!(lambda1 >= 0.f) || !(lambda2 >= 0.f)) return fail(MRF_EINVAL, "mrf_llr_cost: need lambda1, lambda2 >= 0");
+  if (lambda1 > 0.f && !h->has_lap) return fail(MRF_EINVAL, "mrf_llr_cost: lambda1 > 0 needs mrf_llr_laplacian first");
+  for (const void* v : {x, b})
+    if ((uintptr_t)v % 16) return fail(MRF_EINVAL, "mrf_llr_cost: arrays must be 16-byte aligned");
+  MRF_TRY(check_plan(h, plan, "mrf_llr_cost"));
+  CUDA_TRY(cudaSetDevice(h->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  int pN = 0, pL = 0, pC = 0, pdev = 0, pM = 0;
+  plan_dims(plan, &pN, &pL, &pC, &pdev, &pM);
+  const size_t ny = (size_t)pL * pC * pM;
+  if (!h->yb || h->ny < ny) {
+    if (h->yb) cudaFree(h->yb);
+    h->yb = nullptr;
+    if (cudaMalloc((void**)&h->yb, ny * sizeof(float2)) != cudaSuccess) return fail(MRF_ENOMEM, "mrf_llr_cost: allocation failed");
+    h->ny = ny;
   }
-  if (nuclear) {   // sum over patches in a fixed order (synchronises the stream)
-    CUDA_TRY(cudaMemcpyAsync(h->nuc_h.data(), h->nuc, (size_t)nq * sizeof(double), cudaMemcpyDeviceToHost, st));
-    CUDA_TRY(cudaStreamSynchronize(st));
-    double t = 0.0;
-    for (double v : h->nuc_h) t += v;
-    *nuclear = t;
+  if (!h->part && cudaMalloc((void**)&h->part, (size_t)kStatBlocks * sizeof(double)) != cudaSuccess)
+    return fail(MRF_ENOMEM, "mrf_llr_cost: allocation failed");
+  // 1/2 ||A x - b||^2
+  MRF_TRY(mrf_forward(plan, x, h->yb, stream));
+  llr::k_llr_resid<<<kStatBlocks, 256, 0, st>>>(h->yb, (const float2*)b, ny, h->part);
+  MRF_TRY(check_launch("k_llr_resid"));
+  double t[3] = {0.0, 0.0, 0.0};
+  MRF_TRY(host_sum(h->part, kStatBlocks, st, &t[0]));
+  t[0] *= 0.5;
+  // coefficients of P_S x (k_llr_coef with mu = 0 reads x three times: x - 0 (x - x) = x)
+  const float2* xf = (const float2*)x;
+  MRF_TRY(coefs(h, xf, xf, xf, 0.f, h->Y, nullptr, st));
+  const int nq = h->nc * h->nc;
+  if (h->has_lap && (lambda1 > 0.f || terms)) {   // Tr(Q(P_S x) L Q(P_S x)^H)
+    MRF_TRY(manifold_ws(h));
+    MRF_TRY(manifold_G(h, h->Y, st));
+    mfd::k_mfd_penalty<<<nq, 256, 0, st>>>(h->Qm, h->Gm, h->deg, h->p * h->p * h->r, h->pen);
+    MRF_TRY(check_launch("k_mfd_penalty"));
+    MRF_TRY(host_sum(h->pen, nq, st, &t[1]));
+  }
+  // sum_q ||Q_q(P_S x)||_* (threshold +inf: only the singular values are used)
+  MRF_TRY(svt(h, INFINITY, st));
+  MRF_TRY(host_sum(h->nuc, nq, st, &t[2]));
+  if (terms)
+    for (int i = 0; i < 3; ++i) terms[i] = t[i];
+  if (cost) *cost = t[0] + (double)lambda1 * t[1] + (double)lambda2 * t[2];
+  return MRF_OK;
+}
+
+mrf_status mrf_msllr_solve(mrf_llr h, mrf_dict dict, mrf_plan plan, const void* b, const mrf_msllr_params* prm,
+                           void* x, int* index, float* pd, float* params, mrf_msllr_info* info, void* stream) {
+  if (!h || !dict || !plan || !b || !prm || !x || !index || !pd) return fail(MRF_EINVAL, "mrf_msllr_solve: null argument");
+  if (!(prm->mu > 0.f) || !(prm->lambda1 >= 0.f) || !(prm->lambda2 >= 0.f) || !(prm->beta > 0.f) || prm->max_iter < 0)
+    return fail(MRF_EINVAL, "mrf_msllr_solve: need mu > 0, lambda1 >= 0, lambda2 >= 0, beta > 0, max_iter >= 0");
+  if (dict->L != h->L || dict->device != h->device)
+    return fail(MRF_EINVAL, "mrf_msllr_solve: the dictionary's L or device differ from the LLR operator's");
+  const bool manifold = prm->lambda1 > 0.f;
+  if (manifold && (dict->P != 2 || !params))
+    return fail(MRF_EINVAL, "mrf_msllr_solve: lambda1 > 0 needs a (T1, T2) look-up table (P = 2) and params");
+  if (params && dict->P < 1) return fail(MRF_EINVAL, "mrf_msllr_solve: params given but the dictionary has no LUT");
+  MRF_TRY(check_plan(h, plan, "mrf_msllr_solve"));
+  CUDA_TRY(cudaSetDevice(h->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  const long long V = (long long)h->N * h->N;
+  const size_t xbytes = (size_t)h->L * V * sizeof(float2);
+  if (!h->rhs) {
+    if (cudaMalloc((void**)&h->rhs, xbytes) != cudaSuccess || cudaMalloc((void**)&h->x2, xbytes) != cudaSuccess)
+      return fail(MRF_ENOMEM, "mrf_msllr_solve: allocation failed");
+  }
+  // X^0 = A^* b, M^0 = Phi_D(X^0), L^0, lambda_1^0 max(L^0)   (Algorithm 1)
+  MRF_TRY(mrf_adjoint(plan, b, h->rhs, stream));
+  CUDA_TRY(cudaMemcpyAsync(x, h->rhs, xbytes, cudaMemcpyDeviceToDevice, st));
+  float lam1 = 0.f;
+  auto update_maps = [&](const void* cur) -> mrf_status {
+    MRF_TRY(mrf_dict_match(dict, cur, V, index, pd, params, stream));
+    if (manifold) {
+      double maxdeg = 0.0;
+      MRF_TRY(mrf_llr_laplacian(h, params, pd, prm->sigma2, nullptr, &maxdeg, stream));
+      lam1 = (float)((double)prm->lambda1 * maxdeg);   // lambda_1^n = lambda_1^0 max(L^n)
+    }
+    return MRF_OK;
+  };
+  if (manifold) MRF_TRY(update_maps(x));
+  void* cur = x;
+  void* nxt = h->x2;
+  double prev = 0.0;
+  int it = 0;
+  bool maps_current = manifold;
+  for (int n = 1; n <= prm->max_iter; ++n) {
+    // Z^n, P^n, X^n (Eqs. 15, 20, 21), then cost(n)
+    MRF_TRY(mrf_llr_step(h, plan, cur, h->rhs, prm->mu, lam1, prm->lambda2, prm->beta, nxt, nullptr, nullptr, stream));
+    double c = 0.0;
+    MRF_TRY(mrf_llr_cost(h, plan, nxt, b, lam1, prm->lambda2, &c, nullptr, stream));
+    if (info && info->cost) info->cost[n - 1] = c;
+    std::swap(cur, nxt);
+    it = n;
+    maps_current = false;
+    // stop rule cost(n-1) / cost(n) - 1 < tol, from n = 2 (reading 27: cost(0) is not defined)
+    if (n >= 2 && prm->tol > 0.0 && prev / c - 1.0 < prm->tol) break;
+    prev = c;
+    if (manifold && n < prm->max_iter) {   // M^{n+1} = Phi_D(X^n), L^{n+1}, lambda_1^{n+1}
+      MRF_TRY(update_maps(cur));
+      maps_current = true;
+    }
+  }
+  if (!maps_current) MRF_TRY(mrf_dict_match(dict, cur, V, index, pd, params, stream));   // M^ = Phi_D(X^)
+  if (cur != x) CUDA_TRY(cudaMemcpyAsync(x, cur, xbytes, cudaMemcpyDeviceToDevice, st));
+  if (info) {
+    info->iters = it;
+    info->lambda1 = lam1;
   }
   return MRF_OK;
 }

@@ -314,6 +314,27 @@ __global__ void __launch_bounds__(256) k_llr_update(const float2* __restrict__ Y
   }
 }
 
+// part[block] = sum |a - b|^2 over a grid-stride slice (float64; fixed grid, so the partials and
+// their host sum are deterministic)
+static __global__ void __launch_bounds__(256) k_llr_resid(const float2* __restrict__ a, const float2* __restrict__ b,
+                                                          size_t n, double* __restrict__ part) {
+  double s = 0.0;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    const float2 u = __ldg(a + i), v = __ldg(b + i);
+    const double dx = (double)u.x - (double)v.x, dy = (double)u.y - (double)v.y;
+    s = fma(dx, dx, fma(dy, dy, s));
+  }
+  __shared__ double red[8];
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < 8; ++w) t += red[w];
+    part[blockIdx.x] = t;
+  }
+}
+
 // ---- basis of the dictionary subspace (creation time): complex GEMM with double accumulation,
 // C(m, n) = sum_t A(m, t) B(t, n), A(m, t) = [conj] a[m*sam + t*sat], B(t, n) = b[t*sbt + n*sbn].
 static __global__ void k_cgemm(const float2* __restrict__ a, long long sam, long long sat, int conj_a,

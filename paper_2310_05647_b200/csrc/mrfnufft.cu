@@ -808,7 +808,8 @@ static mrf_status build_psf(mrf_plan_s* pl, const float* traj_host, cudaStream_t
   return MRF_OK;
 }
 
-void mrf::plan_dims(mrf_plan pl, int* N, int* L, int* C, int* device) {
+void mrf::plan_dims(mrf_plan pl, int* N, int* L, int* C, int* device, int* M) {
+  if (M) *M = pl->M;
   *N = pl->N;
   *L = pl->L;
   *C = pl->C;

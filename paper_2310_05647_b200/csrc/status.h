@@ -11,7 +11,7 @@
 namespace mrf {
 mrf_status fail(mrf_status s, const std::string& msg);
 mrf_status check_launch(const char* what);   // cudaGetLastError after a launch
-void plan_dims(mrf_plan plan, int* N, int* L, int* C, int* device);   // mrfnufft.cu
+void plan_dims(mrf_plan plan, int* N, int* L, int* C, int* device, int* M = nullptr);   // mrfnufft.cu
 // 2D tiled TMA map over a row-major [rows][cols] array (row pitch row_bytes, a multiple of 16):
 // (box_cols x box_rows) boxes, 128-byte swizzle (box_cols x element size = 128), out-of-bounds
 // elements read as zero.  dict.cu.

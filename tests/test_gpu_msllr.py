@@ -1,0 +1,154 @@
+"""GPU parity of Algorithm 1 (mrf_msllr_solve, mrf_llr_cost) against the float64 oracle
+(oracle/msllr.py).
+
+Inputs are synthetic and seeded: a coarse (T1, T2) grid of surrogate atoms (synth.dictionary),
+tissue maps with every voxel in some tissue (so Phi_D has no noise-driven background voxels),
+x_true[l, v] = pd_v d_{k_v}[l] and b = A x_true from the oracle's gridding NUFFT.  The GPU and the
+oracle each run the whole loop from b (basis, X^0, maps, Laplacian, steps, costs, stop rule).
+The loop's maps feed back into the iteration when lambda_1 > 0 (through the Laplacian), so that
+case uses one tissue with piecewise-constant PD, where Phi_D's atom is unambiguous; the final maps
+must equal the oracle's except valid near-ties (within TIE_REL of the best score).
+"""
+import numpy as np
+import pytest
+import torch
+
+import synth
+import synth.dictionary as sd
+from oracle import llr as ol
+from oracle import msllr as oms
+from oracle import nufft as on
+
+pytestmark = pytest.mark.gpu
+
+N, L, P, S, W = 32, 60, 7, 3, 6
+
+
+@pytest.fixture(scope="module")
+def binding():
+    from paper_2310_05647_b200 import binding as b
+    return b
+
+
+def make_problem(tissues: int):
+    grid = sd.t1t2_grid()[::80]                                   # coarse: well-separated atoms
+    D = sd.surrogate_dictionary(L, grid)
+    lut = grid.astype(np.float32)
+    rng = np.random.default_rng([27, tissues])
+    yy, xx = np.mgrid[0:N, 0:N] / N - 0.5
+    kmap = np.full((N, N), rng.integers(len(grid)))
+    pdm = np.full((N, N), 0.4)
+    for _ in range(4):                                            # ellipses on a tissue background
+        cy, cx = rng.uniform(-0.25, 0.25, 2)
+        a, c = rng.uniform(0.1, 0.3, 2)
+        m = ((yy - cy) / a) ** 2 + ((xx - cx) / c) ** 2 <= 1.0
+        if tissues > 1:
+            kmap[m] = rng.integers(len(grid))
+        pdm[m] = rng.uniform(0.5, 1.0)
+    x_true = (pdm.reshape(-1)[:, None] * D[kmap.reshape(-1)]).T.reshape(L, N, N)
+    traj = synth.spiral_trajectory(512, 10, 8, 1.5)
+    b = on.forward(x_true, traj, None, W)
+    # mu below 1 / lambda_max(A^H A) (power iteration on one frame of the oracle's normal operator)
+    v = rng.standard_normal((1, N, N)) + 0j
+    for _ in range(30):
+        v = on.normal(v, traj, None, W)
+        lam = np.linalg.norm(v)
+        v /= lam
+    d = ol.basis(D, 0.9999, 32)
+    return {"D": D, "lut": lut, "traj": traj, "b": b, "mu": 0.9 / lam, "d": d}
+
+
+@pytest.fixture(scope="module")
+def problem():
+    """Four tissues: boundary voxels are mixtures, so Phi_D may resolve near-ties either way."""
+    return make_problem(4)
+
+
+@pytest.fixture(scope="module")
+def problem1():
+    """One tissue with piecewise-constant PD: the maps that feed the Laplacian back into the loop
+    carry no tissue-boundary mixtures."""
+    return make_problem(1)
+
+
+def _gpu(binding, pr):
+    dic = binding.Dictionary(pr["D"], pr["lut"])
+    dic.basis(0.9999, 32)
+    op = binding.LLR(dic, N, P, S)
+    pl = binding.Plan(N, pr["traj"], L, W=W)
+    b = torch.from_numpy(pr["b"].astype(np.complex64)).cuda()
+    return dic, op, pl, b
+
+
+def _rel(a, b):
+    return float(np.linalg.norm(np.asarray(a) - np.asarray(b)) / np.linalg.norm(np.asarray(b)))
+
+
+TIE_REL = 2e-4   # as tests/test_gpu_match.py
+
+
+@pytest.mark.parametrize("lam1,iters,which", [(0.0, 3, "problem"), (2e-3, 2, "problem1")])
+def test_solve_against_the_oracle(binding, request, lam1, iters, which):
+    pr = request.getfixturevalue(which)
+    lam2, beta = 0.05, 0.5
+    ref = oms.solve(pr["b"], pr["traj"], pr["D"], pr["lut"], pr["d"], pr["mu"], lam1, lam2, beta, iters, tol=0.0,
+                    W=W, N=N, p=P, s=S)
+    dic, op, pl, b = _gpu(binding, pr)
+    out = op.solve(dic, pl, b, mu=pr["mu"], lam1=lam1, lam2=lam2, beta=beta, max_iter=iters, tol=0.0)
+    torch.cuda.synchronize()
+    assert out["iters"] == ref["iters"] == iters
+    assert _rel(out["x"].cpu().numpy(), ref["x"]) <= 1e-4
+    assert np.allclose(out["cost"], ref["cost"], rtol=1e-4, atol=0)
+    # final maps M^ = Phi_D(X^): the oracle's atom wherever its best score is clear of the second
+    # by TIE_REL, else a valid near-tie (within TIE_REL of the best)
+    k = out["index"].cpu().numpy()
+    _, _, _, score = __import__("oracle").match.match(ref["x"].reshape(L, -1).T, pr["D"], pr["lut"])
+    srt = np.sort(score, axis=1)
+    clear = (srt[:, -1] - srt[:, -2]) > TIE_REL * srt[:, -1]
+    assert np.array_equal(k[clear], ref["k"][clear])
+    assert np.all(score[np.arange(k.size), k] >= (1 - TIE_REL) * srt[:, -1])
+    same = k == ref["k"]
+    # pd follows x, which is compared in the global relative norm: tolerance relative to max pd
+    assert np.max(np.abs(out["pd"].cpu().numpy()[same] - ref["rho"][same])) <= 1e-4 * ref["rho"].max()
+    assert np.array_equal(out["params"].cpu().numpy()[same], ref["eta"][same])
+    if lam1:
+        assert abs(out["lambda1"] - ref["lambda1"]) <= 1e-4 * ref["lambda1"]
+    pl.close(), op.close(), dic.close()
+
+
+def test_cost_terms_against_the_oracle(binding, problem1):
+    """mrf_llr_cost at a step iterate (in the subspace, where it equals the paper's cost)."""
+    pr = problem1
+    dic, op, pl, b = _gpu(binding, pr)
+    out = op.solve(dic, pl, b, mu=pr["mu"], lam1=0.0, lam2=0.05, beta=0.5, max_iter=1, tol=0.0)
+    x = out["x"]
+    params = out["params"][:, :2].contiguous()
+    op.laplacian(params, out["pd"])
+    c, terms = op.cost(pl, x, b, lam1=0.3, lam2=0.7)
+    torch.cuda.synchronize()
+    # oracle at the GPU iterate is not allowed (no oracle input from the CUDA path): run the
+    # oracle's own one-step solve and its own maps, then compare the cost of its iterate
+    ref = oms.solve(pr["b"], pr["traj"], pr["D"], pr["lut"], pr["d"], pr["mu"], 0.0, 0.05, 0.5, 1, tol=0.0,
+                    W=W, N=N, p=P, s=S)
+    from oracle import manifold as omf
+    _, m = oms.maps_of(ref["x"], pr["D"], pr["lut"])
+    lap = omf.laplacian(omf.weights(m, N, P, S)[0])
+    A = lambda X: on.forward(X, pr["traj"], None, W)
+    c_ref, t_ref = oms.cost(ref["x"], pr["b"], A, 0.3, 0.7, lap, P, S)
+    for g, o in zip(terms, t_ref):
+        assert abs(g - o) <= 1e-4 * abs(o), (terms, t_ref)
+    assert abs(c - c_ref) <= 1e-4 * c_ref
+    pl.close(), op.close(), dic.close()
+
+
+def test_stop_rule(binding, problem):
+    pr = problem
+    dic, op, pl, b = _gpu(binding, pr)
+    out = op.solve(dic, pl, b, mu=pr["mu"], lam1=0.0, lam2=0.05, beta=0.5, max_iter=6, tol=1e9)
+    assert out["iters"] == 2 and len(out["cost"]) == 2
+    with pytest.raises(binding.MrfError):        # lambda1 > 0 needs a (T1, T2) LUT
+        dnl = binding.Dictionary(pr["D"])
+        dnl.basis()
+        op2 = binding.LLR(dnl, N, P, S)
+        op2.solve(dnl, pl, b, mu=pr["mu"], lam1=1e-3, max_iter=1)
+    pl.close(), op.close(), dic.close()

@@ -47,3 +47,34 @@ def timed(lam1):
 
 print(f"llr step (lambda1 = 0): {timed(0.0):.3f} ms; ms-llr step (lambda1 > 0): {timed(0.1 * mdeg / 100):.3f} ms "
       f"(rank {d.shape[0]})")
+
+# Algorithm 1 end to end (mrf_msllr_solve): per-iteration time = (T(5) - T(1)) / 4, where one
+# iteration = step + cost + Phi_D + Laplacian update (lambda1 > 0)
+lut = sd.t1t2_grid().astype(np.float32)
+dic2 = binding.Dictionary(sd.surrogate_dictionary(cfg.L), lut)
+dic2.basis(0.9999, 32)
+op2 = binding.LLR(dic2, cfg.N)
+b = pl.forward(x)
+c, terms = op.cost(pl, xo, b, lam1=0.1, lam2=0.1)
+torch.cuda.synchronize()
+t0 = time.perf_counter()
+for _ in range(5):
+    op.cost(pl, xo, b, lam1=0.1, lam2=0.1)
+torch.cuda.synchronize()
+print(f"cost: {1e3 * (time.perf_counter() - t0) / 5:.3f} ms (terms {terms})")
+
+
+def solve_ms(n, lam1):
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    out = op2.solve(dic2, pl, b, mu=0.02, lam1=lam1, lam2=0.05, beta=0.5, max_iter=n, tol=0.0)
+    torch.cuda.synchronize()
+    return time.perf_counter() - t0, out
+
+
+solve_ms(1, 1e-3)
+for lam1 in (0.0, 1e-3):
+    t1, _ = solve_ms(1, lam1)
+    t5, out = solve_ms(5, lam1)
+    print(f"msllr solve lambda1_0={lam1}: {1e3 * (t5 - t1) / 4:.2f} ms per Algorithm-1 iteration "
+          f"(T(1) = {1e3 * t1:.1f} ms, cost {['%.4g' % c for c in out['cost']]})")
