@@ -453,20 +453,27 @@ def run_ours(args):
     e2e = None
     if not args.no_e2e:
         y_h = y.cpu().pin_memory()
-        x_h = torch.zeros(plan.x_shape, dtype=torch.complex64).pin_memory()
-        plan.dc_cg(y_h, mu=cfg.mu, n_iter=n_iter, x=x_h, zero_init=True)   # warm-up (allocates staging)
+        x_h = [torch.zeros(plan.x_shape, dtype=torch.complex64).pin_memory() for _ in range(2)]
+        # warm-up (allocates the slots), then a pipelined stream of solves through the C-ABI with
+        # host buffers (MRF_CG_ASYNC_HOST: each result copy overlaps the next solve; the timed
+        # region ends when the last result is on the host)
+        plan.dc_cg(y_h, mu=cfg.mu, n_iter=n_iter, x=x_h[0], zero_init=True, async_host=True)
+        plan.wait()
+        n_e2e = max(1, min(args.steps, 10))
         barrier()
         t0 = time.perf_counter()
-        for _ in range(max(1, min(args.steps, 3))):
-            plan.dc_cg(y_h, mu=cfg.mu, n_iter=n_iter, x=x_h, zero_init=True)
+        for k in range(n_e2e):
+            plan.dc_cg(y_h, mu=cfg.mu, n_iter=n_iter, x=x_h[k % 2], zero_init=True, async_host=True)
+        plan.wait()
         torch.cuda.synchronize()
-        n_e2e = max(1, min(args.steps, 3))
         ms_e2e = max_over_ranks((time.perf_counter() - t0) * 1e3 / n_e2e)
-        e2e = {"value": pts_step / (ms_e2e * 1e-3), "unit": UNIT, "ms_per_step": ms_e2e,
+        e2e = {"value": pts_step / (ms_e2e * 1e-3), "unit": UNIT, "ms_per_step": ms_e2e, "steps": n_e2e,
                "h2d_bytes_per_step": int(y_h.numel() * 8) * world,
-               "d2h_bytes_per_step": int(x_h.numel() * 8) * world,
+               "d2h_bytes_per_step": int(x_h[0].numel() * 8) * world,
                "note": "host pinned k-space y copied in, solution x copied out, inside each "
-                       "mrf_dc_cg_ex(MRF_CG_ZERO_INIT) call (x0 = 0 is not transferred)"}
+                       "mrf_dc_cg_ex(MRF_CG_ZERO_INIT | MRF_CG_ASYNC_HOST) call (x0 = 0 is not transferred); "
+                       "the result copy of step k overlaps the solve of step k+1; wall clock from the first "
+                       "call to the last result on the host"}
 
     # ---------------------------------------------------------------- roofline of the dominant kernel
     sm_count = torch.cuda.get_device_properties(dev).multi_processor_count

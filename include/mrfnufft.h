@@ -135,8 +135,18 @@ mrf_status mrf_dc_cg(mrf_plan plan, const void* y, const void* z, float mu, int 
  * residual is r = rhs without an application of the normal operator.  Same iterates as
  * mrf_dc_cg on a zeroed x.  Unknown flags: MRF_EINVAL. */
 #define MRF_CG_ZERO_INIT 1u
+/* MRF_CG_ASYNC_HOST (host buffers only, else MRF_EINVAL): pipelined host path for a stream of
+ * solves.  The call copies y (and x0 / z) into one of two device slots on `stream`, solves there,
+ * and copies the result to the host x on the plan's own copy stream, then returns without waiting
+ * for that copy: the result copy of call k overlaps the solve of call k+1 (PCIe is full duplex;
+ * call k+2 reuses the slot after call k's copy).  The host buffers of a call stay in use until
+ * mrf_plan_wait returns; pinned host memory is needed for the overlap.  `info`, if given, is
+ * filled as usual (that synchronises `stream`, not the copy stream). */
+#define MRF_CG_ASYNC_HOST 2u
 mrf_status mrf_dc_cg_ex(mrf_plan plan, const void* y, const void* z, float mu, int n_iter, float tol,
                         unsigned flags, void* x, mrf_cg_info* info, void* stream);
+/* Waits for every result copy of MRF_CG_ASYNC_HOST calls on the plan.  Errors: MRF_EINVAL, MRF_ECUDA. */
+mrf_status mrf_plan_wait(mrf_plan plan);
 
 mrf_status mrf_plan_destroy(mrf_plan plan);
 

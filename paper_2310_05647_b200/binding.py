@@ -33,7 +33,7 @@ EXPORTED = [
     "mrf_profile_query", "mrf_nccl_get_unique_id", "mrf_nccl_comm_init", "mrf_nccl_comm_destroy",
     "mrf_adjoint_dcf", "mrf_dcf_weights", "mrf_dict_create", "mrf_dict_match", "mrf_dict_destroy",
     "mrf_dict_profile", "mrf_dict_profile_query", "mrf_dict_basis", "mrf_dict_basis_copy", "mrf_llr_create",
-    "mrf_llr_step", "mrf_llr_destroy", "mrf_llr_laplacian", "mrf_llr_cost", "mrf_msllr_solve",
+    "mrf_llr_step", "mrf_llr_destroy", "mrf_llr_laplacian", "mrf_llr_cost", "mrf_msllr_solve", "mrf_plan_wait",
 ]
 
 
@@ -87,6 +87,7 @@ def _load() -> ctypes.CDLL:
         "mrf_dc_cg": ([vp, vp, vp, cf, ci, cf, vp, ctypes.POINTER(CGInfo), vp], ci),
         "mrf_dc_cg_ex": ([vp, vp, vp, cf, ci, cf, ctypes.c_uint, vp, ctypes.POINTER(CGInfo), vp], ci),
         "mrf_plan_destroy": ([vp], ci),
+        "mrf_plan_wait": ([vp], ci),
         "mrf_status_string": ([ci], ctypes.c_char_p),
         "mrf_last_error": ([], ctypes.c_char_p),
         "mrf_plan_device_bytes": ([vp], ctypes.c_size_t),
@@ -246,11 +247,13 @@ class Plan:
         return out
 
     def dc_cg(self, y, x0=None, z=None, mu: float = 0.01, n_iter: int = 10, tol: float = 0.0, x=None,
-              zero_init: bool = False):
+              zero_init: bool = False, async_host: bool = False):
         """CG solve of (A^H A + mu I) x = A^H y + mu z from x0; returns (x, info dict).
 
         zero_init=True: x0 = 0 and x is output only (mrf_dc_cg_ex with MRF_CG_ZERO_INIT: no normal
-        operator for the initial residual, and no host-to-device copy of x0 on the host path)."""
+        operator for the initial residual, and no host-to-device copy of x0 on the host path).
+        async_host=True (pinned host tensors): MRF_CG_ASYNC_HOST -- the result copy overlaps the
+        next call's solve; call ``wait()`` before reading x."""
         y = _as_c64(y, self.y_shape, "y")
         if x is None:
             x = self._like(y, self.x_shape)
@@ -272,10 +275,15 @@ class Plan:
         dp = lambda a: ctypes.cast(a, ctypes.POINTER(ctypes.c_double))
         info = CGInfo(0, 0.0, dp(hist), dp(ha), dp(hb))
         _check(lib.mrf_dc_cg_ex(self._h, _ptr(y), _ptr(z), ctypes.c_float(mu), int(n_iter), ctypes.c_float(tol),
-                                1 if zero_init else 0, _ptr(x), ctypes.byref(info), self._stream(x, y, z)))
+                                (1 if zero_init else 0) | (2 if async_host else 0), _ptr(x), ctypes.byref(info),
+                                self._stream(x, y, z)))
         it = info.iters
         return x, {"iters": it, "rel_resid": info.rel_resid, "history": list(hist)[: it + 1],
                    "alpha": list(ha)[:it], "beta": list(hb)[:it]}
+
+    def wait(self):
+        """Waits for the result copies of async_host solves (mrf_plan_wait)."""
+        _check(lib.mrf_plan_wait(self._h))
 
     # ------------------------------------------------------------------ profiling
     def profile(self, enable: bool = True):

@@ -119,6 +119,13 @@ struct mrf_plan_s {
   float2* stg_x = nullptr;
   float2* stg_y = nullptr;
   float2* stg_z = nullptr;
+  // MRF_CG_ASYNC_HOST: two device slots (x, y) per call parity, a copy stream for the
+  // device-to-host result copies, and events ordering slot reuse
+  float2* ax[2] = {nullptr, nullptr};
+  float2* ay[2] = {nullptr, nullptr};
+  cudaStream_t cstream = nullptr;
+  cudaEvent_t ev_solved[2] = {}, ev_copied[2] = {};
+  unsigned long long acalls = 0;
   size_t bytes = 0;
   Prof prof;
   DevPlan dp() const {
@@ -244,7 +251,13 @@ static void free_plan(mrf_plan_s* pl) {
     if (pl->ybufs[i]) cudaFree(pl->ybufs[i]);
   }
   void* ptrs[] = {pl->coils, pl->dap, pl->tw, pl->fchunks, pl->ftab, pl->achunks, pl->atab, pl->fil, pl->r, pl->p, pl->q,
-                  pl->part, pl->dotp, pl->sc, pl->hist, pl->stg_x, pl->stg_y, pl->stg_z};
+                  pl->part, pl->dotp, pl->sc, pl->hist, pl->stg_x, pl->stg_y, pl->stg_z, pl->ax[0], pl->ax[1],
+                  pl->ay[0], pl->ay[1]};
+  for (int i = 0; i < 2; ++i) {
+    if (pl->ev_solved[i]) cudaEventDestroy(pl->ev_solved[i]);
+    if (pl->ev_copied[i]) cudaEventDestroy(pl->ev_copied[i]);
+  }
+  if (pl->cstream) cudaStreamDestroy(pl->cstream);
   for (void* v : ptrs)
     if (v) cudaFree(v);
   for (int k = 0; k < MRF_K_COUNT; ++k)
@@ -767,6 +780,18 @@ static mrf_status ensure_staging(mrf_plan_s* pl, bool need_z) {
   return MRF_OK;
 }
 
+static mrf_status ensure_async(mrf_plan_s* pl, bool need_z) {
+  const size_t nx = (size_t)pl->L * pl->N * pl->N, ny = (size_t)pl->L * pl->C * pl->M;
+  for (int i = 0; i < 2; ++i) {
+    if (!pl->ax[i]) MRF_TRY(dev_alloc(pl, &pl->ax[i], nx));
+    if (!pl->ay[i]) MRF_TRY(dev_alloc(pl, &pl->ay[i], ny));
+    if (!pl->ev_solved[i]) CUDA_TRY(cudaEventCreateWithFlags(&pl->ev_solved[i], cudaEventDisableTiming));
+    if (!pl->ev_copied[i]) CUDA_TRY(cudaEventCreateWithFlags(&pl->ev_copied[i], cudaEventDisableTiming));
+  }
+  if (!pl->cstream) CUDA_TRY(cudaStreamCreateWithFlags(&pl->cstream, cudaStreamNonBlocking));
+  if (need_z && !pl->stg_z) MRF_TRY(dev_alloc(pl, &pl->stg_z, nx));
+  return MRF_OK;
+}
 
 // Toeplitz PSF spectra (MRF_NORMAL_TOEPLITZ), float64 on the device, one interleaf at a time:
 // Dirichlet factors D_x, D_y [M][G], T_r = D_y^T D_x / (G^2 N^2) (gridding.cuh k_psf_*), stored fp32.
@@ -1268,8 +1293,8 @@ mrf_status mrf_dc_cg(mrf_plan pl, const void* y, const void* z, float mu, int n_
 mrf_status mrf_dc_cg_ex(mrf_plan pl, const void* y, const void* z, float mu, int n_iter, float tol, unsigned flags,
                         void* x, mrf_cg_info* info, void* stream) {
   if (!pl || !y || !x) return fail(MRF_EINVAL, "null plan/y/x");
-  if (flags & ~MRF_CG_ZERO_INIT) return fail(MRF_EINVAL, "unknown CG flags");
-  const bool zero_init = (flags & MRF_CG_ZERO_INIT) != 0;
+  if (flags & ~(MRF_CG_ZERO_INIT | MRF_CG_ASYNC_HOST)) return fail(MRF_EINVAL, "unknown CG flags");
+  const bool zero_init = (flags & MRF_CG_ZERO_INIT) != 0, async = (flags & MRF_CG_ASYNC_HOST) != 0;
   if (!(mu >= 0.f) || !std::isfinite(mu)) return fail(MRF_EINVAL, "mu must be finite and >= 0");
   if (n_iter < 0) return fail(MRF_EINVAL, "n_iter < 0");
   if (!(tol >= 0.f) || !std::isfinite(tol)) return fail(MRF_EINVAL, "tol must be finite and >= 0");
@@ -1277,9 +1302,31 @@ mrf_status mrf_dc_cg_ex(mrf_plan pl, const void* y, const void* z, float mu, int
   cudaStream_t st = (cudaStream_t)stream;
   bool host = false;
   MRF_TRY(classify(pl, {y, z, x}, &host));
-  if (!host) return run_cg(pl, (const float2*)y, (const float2*)z, mu, n_iter, tol, (float2*)x, info, st, zero_init);
-  MRF_TRY(ensure_staging(pl, z != nullptr));
+  if (!host) {
+    if (async) return fail(MRF_EINVAL, "MRF_CG_ASYNC_HOST needs host buffers");
+    return run_cg(pl, (const float2*)y, (const float2*)z, mu, n_iter, tol, (float2*)x, info, st, zero_init);
+  }
   const size_t bx = (size_t)pl->L * pl->N * pl->N * sizeof(float2), by = (size_t)pl->L * pl->C * pl->M * sizeof(float2);
+  if (async) {
+    // slot s = call parity: wait until the result copy of the call before last (same slot) has
+    // left the device buffer, copy the inputs in and solve on `stream`, then copy the result out
+    // on the plan's copy stream -- overlapping the next call's solve.  No host synchronisation
+    // except the one that fills `info`.
+    MRF_TRY(ensure_async(pl, z != nullptr));
+    const int s = (int)(pl->acalls++ & 1);
+    CUDA_TRY(cudaStreamWaitEvent(st, pl->ev_copied[s], 0));
+    CUDA_TRY(cudaMemcpyAsync(pl->ay[s], y, by, cudaMemcpyHostToDevice, st));
+    if (!zero_init) CUDA_TRY(cudaMemcpyAsync(pl->ax[s], x, bx, cudaMemcpyHostToDevice, st));
+    if (z) CUDA_TRY(cudaMemcpyAsync(pl->stg_z, z, bx, cudaMemcpyHostToDevice, st));
+    mrf_status r = run_cg(pl, pl->ay[s], z ? pl->stg_z : nullptr, mu, n_iter, tol, pl->ax[s], info, st, zero_init);
+    if (r != MRF_OK && r != MRF_ENUMERIC) return r;
+    CUDA_TRY(cudaEventRecord(pl->ev_solved[s], st));
+    CUDA_TRY(cudaStreamWaitEvent(pl->cstream, pl->ev_solved[s], 0));
+    CUDA_TRY(cudaMemcpyAsync(x, pl->ax[s], bx, cudaMemcpyDeviceToHost, pl->cstream));
+    CUDA_TRY(cudaEventRecord(pl->ev_copied[s], pl->cstream));
+    return r;
+  }
+  MRF_TRY(ensure_staging(pl, z != nullptr));
   CUDA_TRY(cudaMemcpyAsync(pl->stg_y, y, by, cudaMemcpyHostToDevice, st));
   if (!zero_init) CUDA_TRY(cudaMemcpyAsync(pl->stg_x, x, bx, cudaMemcpyHostToDevice, st));
   if (z) CUDA_TRY(cudaMemcpyAsync(pl->stg_z, z, bx, cudaMemcpyHostToDevice, st));
@@ -1288,6 +1335,13 @@ mrf_status mrf_dc_cg_ex(mrf_plan pl, const void* y, const void* z, float mu, int
   CUDA_TRY(cudaMemcpyAsync(x, pl->stg_x, bx, cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaStreamSynchronize(st));
   return s;
+}
+
+mrf_status mrf_plan_wait(mrf_plan pl) {
+  if (!pl) return fail(MRF_EINVAL, "null plan");
+  DeviceGuard guard(pl->device);
+  if (pl->cstream) CUDA_TRY(cudaStreamSynchronize(pl->cstream));
+  return MRF_OK;
 }
 
 mrf_status mrf_profile_enable(mrf_plan pl, int enable) {

@@ -487,3 +487,24 @@ def test_cg_zero_init_matches_zeroed_x0(mrf):
     a, b = host(xa), host(xb)
     assert np.array_equal(a, b) and np.array_equal(a, xh.numpy())
     assert ia["history"] == ib["history"] == ih["history"]
+
+
+def test_cg_async_host_pipeline(mrf):
+    """MRF_CG_ASYNC_HOST: a pipelined stream of host-buffer solves (result copies on the plan's
+    copy stream, two device slots) gives exactly the synchronous host path's results, and a
+    device-pointer call with the flag is rejected."""
+    cfg, traj, coils, frames, x = setup("pr1")
+    rng = np.random.default_rng(5)
+    ys = [on.forward(x * (1.0 + 0.5 * k), traj, None, cfg.W).astype(np.complex64) for k in range(3)]
+    pl = mrf.Plan(cfg.N, traj, cfg.L, W=cfg.W)
+    ref = [pl.dc_cg(torch.from_numpy(y), mu=cfg.mu, n_iter=cfg.cg_iters, zero_init=True)[0].numpy() for y in ys]
+    yh = [torch.from_numpy(y).pin_memory() for y in ys]
+    xh = [torch.full(pl.x_shape, complex(rng.standard_normal()), dtype=torch.complex64).pin_memory() for _ in ys]
+    for k in range(3):
+        pl.dc_cg(yh[k], mu=cfg.mu, n_iter=cfg.cg_iters, x=xh[k], zero_init=True, async_host=True)
+    pl.wait()
+    for k in range(3):
+        assert np.array_equal(xh[k].numpy(), ref[k])
+    with pytest.raises(mrf.MrfError):
+        pl.dc_cg(dev(ys[0]), mu=cfg.mu, n_iter=2, zero_init=True, async_host=True)
+    pl.close()
