@@ -214,6 +214,15 @@ mrf_status mrf_dict_destroy(mrf_dict dict);
 mrf_status mrf_dict_basis(mrf_dict dict, double energy, int max_rank, int* rank_out);
 mrf_status mrf_dict_basis_copy(mrf_dict dict, void* basis_out);
 
+/* Phi_D of voxels given in basis coordinates: u DEVICE [r][V] complex64 (coefficient-major, the
+ * layout of an r-frame image stack) with x_v = sum_i u[i][v] d_i.  For such x (every iterate of
+ * mrf_llr_step lies in span(d)) <d_k, x_v> = sum_i u[i][v] conj(Dc[k][i]) with Dc = D d^dagger
+ * (built by mrf_dict_basis), so index / pd / params are those of mrf_dict_match(x) up to rounding
+ * (the argmax keeps the full atom norms ||d_k||), at r instead of L frames of work.  Needs
+ * mrf_dict_basis; otherwise as mrf_dict_match. */
+mrf_status mrf_dict_match_coef(mrf_dict dict, const void* u, long long V, int* index, float* pd, float* params,
+                               void* stream);
+
 /* An LLR operator on N x N images of the dictionary's L frames, p x p patches with stride s
  * (11 x 11, 5), patch corners 0, s, 2s, ... and N - p.  Needs mrf_dict_basis; the
  * basis is copied.  Errors: MRF_EINVAL, MRF_ENOMEM, MRF_ECUDA. */

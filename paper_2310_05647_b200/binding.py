@@ -34,6 +34,7 @@ EXPORTED = [
     "mrf_adjoint_dcf", "mrf_dcf_weights", "mrf_dict_create", "mrf_dict_match", "mrf_dict_destroy",
     "mrf_dict_profile", "mrf_dict_profile_query", "mrf_dict_basis", "mrf_dict_basis_copy", "mrf_llr_create",
     "mrf_llr_step", "mrf_llr_destroy", "mrf_llr_laplacian", "mrf_llr_cost", "mrf_msllr_solve", "mrf_plan_wait",
+    "mrf_dict_match_coef",
 ]
 
 
@@ -98,6 +99,7 @@ def _load() -> ctypes.CDLL:
         "mrf_nccl_comm_destroy": ([vp], ci),
         "mrf_dict_create": ([vp, vp, ci, ci, ci, ci, ctypes.POINTER(vp)], ci),
         "mrf_dict_match": ([vp, vp, ctypes.c_longlong, vp, vp, vp, vp], ci),
+        "mrf_dict_match_coef": ([vp, vp, ctypes.c_longlong, vp, vp, vp, vp], ci),
         "mrf_dict_destroy": ([vp], ci),
         "mrf_dict_profile": ([vp, ci], ci),
         "mrf_dict_profile_query": ([vp, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_longlong)], ci),
@@ -372,6 +374,19 @@ class Dictionary:
         params = torch.empty((V, self.P), dtype=torch.float32, device=x.device) if self.P else None
         st = torch.cuda.current_stream(x.device).cuda_stream
         _check(lib.mrf_dict_match(self._h, _ptr(x), V, _ptr(index), _ptr(pd), _ptr(params), ctypes.c_void_p(st)))
+        return index, pd, params
+
+    def match_coef(self, u: torch.Tensor):
+        """Phi_D of voxels in basis coordinates u [r][...voxels] (CUDA complex64), x_v = sum_i u[i, v] d_i
+        (mrf_dict_match_coef; needs basis())."""
+        if not (isinstance(u, torch.Tensor) and u.is_cuda and u.dtype == torch.complex64 and u.is_contiguous()):
+            raise TypeError("u must be a contiguous CUDA complex64 tensor [r][...]")
+        V = u.numel() // u.shape[0]
+        index = torch.empty(V, dtype=torch.int32, device=u.device)
+        pd = torch.empty(V, dtype=torch.float32, device=u.device)
+        params = torch.empty((V, self.P), dtype=torch.float32, device=u.device) if self.P else None
+        st = torch.cuda.current_stream(u.device).cuda_stream
+        _check(lib.mrf_dict_match_coef(self._h, _ptr(u), V, _ptr(index), _ptr(pd), _ptr(params), ctypes.c_void_p(st)))
         return index, pd, params
 
     def basis(self, energy: float = 0.9999, max_rank: int = 32) -> np.ndarray:

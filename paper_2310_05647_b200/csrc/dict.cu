@@ -21,6 +21,8 @@
 
 using namespace mrf;
 
+static constexpr int kKDc = 64;   // fp16 row length of the basis-coordinate dictionary (2 rank <= 64)
+
 
 static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -59,7 +61,7 @@ static void dict_free(mrf_dict_s* d) {
   if (!d) return;
   cudaSetDevice(d->device);
   for (void* p : {(void*)d->dp, (void*)d->w2, (void*)d->n2inv, (void*)d->atoms, (void*)d->lut, (void*)d->xp,
-                  (void*)d->xs, (void*)d->best, (void*)d->basis})
+                  (void*)d->xs, (void*)d->best, (void*)d->basis, (void*)d->dpc, (void*)d->w2c, (void*)d->Dc})
     if (p) cudaFree(p);
   delete d;
 }
@@ -131,15 +133,21 @@ mrf_status mrf_dict_create(const void* atoms, const float* lut, int K, int L, in
   return MRF_OK;
 }
 
-mrf_status mrf_dict_match(mrf_dict d, const void* x, long long V, int* index, float* pd, float* params, void* stream) {
+}  // extern "C"
+
+// Phi_D of x [L][V] against packed rows (tmd, KD) with weights w2 and exact-pd atoms [K][L]:
+// the frame-domain match (L = d->L) and the basis-coordinate match (L = rank, Dc).
+static mrf_status match_impl(mrf_dict d, const char* who, const void* x, int L, int KD, const CUtensorMap& tmd,
+                             const float* w2, const float2* atoms, long long V, int* index, float* pd, float* params,
+                             void* stream) {
   if (!d || !x || !index || !pd || V < 1 || V > (1LL << 30))
-    return fail(MRF_EINVAL, "mrf_dict_match: invalid arguments");
+    return fail(MRF_EINVAL, std::string(who) + ": invalid arguments");
   for (const void* p : {x, (const void*)index, (const void*)pd, (const void*)params})
-    if (p && ((uintptr_t)p % 16) != 0) return fail(MRF_EINVAL, "mrf_dict_match: arrays must be 16-byte aligned");
+    if (p && ((uintptr_t)p % 16) != 0) return fail(MRF_EINVAL, std::string(who) + ": arrays must be 16-byte aligned");
   CUDA_TRY(cudaSetDevice(d->device));
   cudaStream_t st = (cudaStream_t)stream;
   const long long vpad = ((V + dm::BM - 1) / dm::BM) * dm::BM;
-  if (vpad > d->vcap) {
+  if (vpad > d->vcap) {   // rows of d->KD >= 64 >= KD fp16 (the basis-coordinate packing fits too)
     CUDA_TRY(cudaStreamSynchronize(st));
     if (d->xp) cudaFree(d->xp);
     if (d->xs) cudaFree(d->xs);
@@ -148,13 +156,13 @@ mrf_status mrf_dict_match(mrf_dict d, const void* x, long long V, int* index, fl
     if (cudaMalloc((void**)&d->xp, (size_t)vpad * d->KD * sizeof(__half)) != cudaSuccess ||
         cudaMalloc((void**)&d->xs, (size_t)vpad * sizeof(float)) != cudaSuccess ||
         cudaMalloc((void**)&d->best, (size_t)vpad * sizeof(unsigned long long)) != cudaSuccess)
-      return fail(MRF_ENOMEM, "mrf_dict_match: workspace allocation failed");
+      return fail(MRF_ENOMEM, std::string(who) + ": workspace allocation failed");
     d->vcap = vpad;
   }
   CUtensorMap tmx;
-  MRF_TRY(make_tmap(&tmx, d->xp, (uint64_t)d->KD, (uint64_t)vpad, (uint32_t)dm::BM));
+  MRF_TRY(make_tmap(&tmx, d->xp, (uint64_t)KD, (uint64_t)vpad, (uint32_t)dm::BM));
   const float2* xf = reinterpret_cast<const float2*>(x);
-  dm::k_dict_pack_x<<<(unsigned)(vpad / 32), 256, 0, st>>>(xf, d->L, (int)V, d->KD, d->xp, d->xs);
+  dm::k_dict_pack_x<<<(unsigned)(vpad / 32), 256, 0, st>>>(xf, L, (int)V, KD, d->xp, d->xs);
   MRF_TRY(check_launch("k_dict_pack_x"));
   if (d->prof) {
     while (d->ev.size() < d->ev_used + 2) {
@@ -169,16 +177,30 @@ mrf_status mrf_dict_match(mrf_dict d, const void* x, long long V, int* index, fl
   CUDA_TRY(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, d->device));
   CUDA_TRY(cudaMemsetAsync(d->best, 0, (size_t)V * sizeof(unsigned long long), st));
   dm::k_dict_gemm<<<(unsigned)std::min(n_sm, m_tiles * n_tiles), dm::THREADS, dm::SMEM, st>>>(
-      tmx, d->tmd, d->w2, m_tiles, n_tiles, d->KD / dm::BK, (int)V, d->best);
+      tmx, tmd, w2, m_tiles, n_tiles, KD / dm::BK, (int)V, d->best);
   MRF_TRY(check_launch("k_dict_gemm"));
   if (d->prof) {
     CUDA_TRY(cudaEventRecord(d->ev[d->ev_used + 1], st));
     d->ev_used += 2;
   }
-  dm::k_dict_fix<<<(unsigned)((V + 31) / 32), 256, 0, st>>>(xf, d->atoms, d->n2inv, d->lut, d->P, d->L, (int)V,
-                                                               d->best, index, pd, params);
+  dm::k_dict_fix<<<(unsigned)((V + 31) / 32), 256, 0, st>>>(xf, atoms, d->n2inv, d->lut, d->P, L, (int)V, d->best,
+                                                               index, pd, params);
   MRF_TRY(check_launch("k_dict_fix"));
   return MRF_OK;
+}
+
+extern "C" {
+
+mrf_status mrf_dict_match(mrf_dict d, const void* x, long long V, int* index, float* pd, float* params, void* stream) {
+  if (!d) return fail(MRF_EINVAL, "mrf_dict_match: null dictionary");
+  return match_impl(d, "mrf_dict_match", x, d->L, d->KD, d->tmd, d->w2, d->atoms, V, index, pd, params, stream);
+}
+
+mrf_status mrf_dict_match_coef(mrf_dict d, const void* u, long long V, int* index, float* pd, float* params,
+                               void* stream) {
+  if (!d) return fail(MRF_EINVAL, "mrf_dict_match_coef: null dictionary");
+  if (!d->rank || !d->dpc) return fail(MRF_EINVAL, "mrf_dict_match_coef: no basis (call mrf_dict_basis)");
+  return match_impl(d, "mrf_dict_match_coef", u, d->rank, kKDc, d->tmdc, d->w2c, d->Dc, V, index, pd, params, stream);
 }
 
 // ---------------------------------------------------------------- subspace basis (Eq. 17, reading 24)
@@ -225,6 +247,53 @@ static void host_jacobi_eig(int n, std::vector<std::complex<double>>& H, std::ve
   }
   lam.resize(n);
   for (int i = 0; i < n; ++i) lam[i] = H[(size_t)i * n + i].real();
+}
+
+// The dictionary in basis coordinates (mrf_dict_match_coef): Dc = D d^dagger [K][r] on the device
+// (k_cgemm computes conj(D) d^T with float64 accumulation), packed like the frame-domain rows with
+// per-atom scales m'_k = max |Re, Im| of Dc_k and weights (m'_k / ||d_k||)^2 from the FULL norms.
+static mrf_status build_coef_dict(mrf_dict d, int r) {
+  const int K = d->K, L = d->L;
+  for (void* p : {(void*)d->dpc, (void*)d->w2c, (void*)d->Dc})
+    if (p) cudaFree(p);
+  d->dpc = nullptr; d->w2c = nullptr; d->Dc = nullptr;
+  if (cudaMalloc((void**)&d->Dc, (size_t)K * r * sizeof(float2)) != cudaSuccess ||
+      cudaMalloc((void**)&d->dpc, (size_t)d->NP * kKDc * sizeof(__half)) != cudaSuccess ||
+      cudaMalloc((void**)&d->w2c, (size_t)d->NP / 2 * sizeof(float)) != cudaSuccess)
+    return fail(MRF_ENOMEM, "mrf_dict_basis: allocation failed");
+  const dim3 blk(16, 16), grd((unsigned)((r + 15) / 16), (unsigned)((K + 15) / 16));
+  llr::k_cgemm<<<grd, blk>>>(d->atoms, L, 1, 1, d->basis, 1, L, K, r, L, d->Dc, nullptr);   // conj(D) d^T
+  MRF_TRY(check_launch("k_cgemm"));
+  std::vector<float2> dc((size_t)K * r);
+  CUDA_TRY(cudaMemcpy(dc.data(), d->Dc, dc.size() * sizeof(float2), cudaMemcpyDeviceToHost));
+  std::vector<float> n2inv(K);
+  CUDA_TRY(cudaMemcpy(n2inv.data(), d->n2inv, (size_t)K * sizeof(float), cudaMemcpyDeviceToHost));
+  std::vector<__half> dp((size_t)d->NP * kKDc, __float2half(0.f));
+  std::vector<float> w2(d->NP / 2, 0.f);
+  for (int k = 0; k < K; ++k) {
+    double m = 0.0;
+    for (int i = 0; i < r; ++i) {
+      float2& v = dc[(size_t)k * r + i];
+      v.y = -v.y;   // Dc = conj(conj(D) d^T)
+      m = std::max(m, (double)std::max(std::fabs(v.x), std::fabs(v.y)));
+    }
+    if (!(m > 0.0) || !(n2inv[k] > 0.f)) continue;
+    w2[k] = (float)(m * m * (double)n2inv[k]);
+    const double im = 1.0 / m;
+    __half* r0 = &dp[(size_t)(2 * k) * kKDc];
+    __half* r1 = r0 + kKDc;
+    for (int i = 0; i < r; ++i) {
+      const float2 v = dc[(size_t)k * r + i];
+      r0[2 * i] = __float2half((float)(v.x * im));
+      r0[2 * i + 1] = __float2half((float)(v.y * im));
+      r1[2 * i] = __float2half((float)(-v.y * im));
+      r1[2 * i + 1] = __float2half((float)(v.x * im));
+    }
+  }
+  CUDA_TRY(cudaMemcpy(d->Dc, dc.data(), dc.size() * sizeof(float2), cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(d->dpc, dp.data(), dp.size() * sizeof(__half), cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(d->w2c, w2.data(), w2.size() * sizeof(float), cudaMemcpyHostToDevice));
+  return make_tmap(&d->tmdc, d->dpc, (uint64_t)kKDc, (uint64_t)d->NP, (uint32_t)dm::BN);
 }
 
 extern "C" mrf_status mrf_dict_basis(mrf_dict d, double energy, int max_rank, int* rank_out) {
@@ -322,7 +391,9 @@ extern "C" mrf_status mrf_dict_basis(mrf_dict d, double energy, int max_rank, in
   d->rank = 0;
   CUDA_TRY(cudaMalloc((void**)&d->basis, d->basis_h.size() * sizeof(float2)));
   CUDA_TRY(cudaMemcpy(d->basis, d->basis_h.data(), d->basis_h.size() * sizeof(float2), cudaMemcpyHostToDevice));
+  MRF_TRY(build_coef_dict(d, r));
   d->rank = r;
+  ++d->basis_gen;
   *rank_out = r;
   return MRF_OK;
 }

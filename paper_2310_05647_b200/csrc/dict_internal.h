@@ -27,6 +27,14 @@ struct mrf_dict_s {
   size_t ev_used = 0;
   double fro2 = 0.0;             // ||D||_F^2 (float64, at creation)
   int rank = 0;                  // subspace basis (mrf_dict_basis): r rows of length L
+  unsigned basis_gen = 0;        // incremented by every mrf_dict_basis
   float2* basis = nullptr;       // device [rank][L]
   std::vector<float2> basis_h;   // host copy
+  // the dictionary in basis coordinates, Dc = D d^dagger [K][rank] (mrf_dict_match_coef): packed
+  // fp16 rows like dp (row length 64 >= 2 rank) and w2c = (m'_k / ||d_k||)^2 with the FULL atom
+  // norms, so that scores and pd equal those of the frame-domain match for x in span(d)
+  __half* dpc = nullptr;         // [NP][64]
+  float* w2c = nullptr;          // [NP / 2]
+  float2* Dc = nullptr;          // [K][rank]
+  CUtensorMap tmdc;
 };

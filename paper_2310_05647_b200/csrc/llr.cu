@@ -31,6 +31,8 @@ struct mrf_llr_s {
   size_t ny = 0;
   double* part = nullptr;     // [kStatBlocks] partial sums
   float2 *rhs = nullptr, *x2 = nullptr;   // mrf_msllr_solve: A^H b and the second iterate buffer
+  float2 *xcv = nullptr, *xcr = nullptr;  // coefficients of the last x_out: [V][r] and [r][V]
+  unsigned basis_gen = 0;                 // the dictionary's basis generation at creation
   // manifold term (mrf_llr_laplacian)
   bool has_lap = false;
   float* W = nullptr;         // [n][n] similarity weights (Eq. 8), first the squared distances
@@ -54,7 +56,7 @@ static void llr_free(mrf_llr_s* h) {
   cudaSetDevice(h->device);
   for (void* v : {(void*)h->dT, (void*)h->corners, (void*)h->Y, (void*)h->P, (void*)h->nx, (void*)h->nuc, (void*)h->W,
                   (void*)h->deg, (void*)h->pv, (void*)h->hist, (void*)h->stats, (void*)h->YX, (void*)h->Qm,
-                  (void*)h->Gm, (void*)h->pen, (void*)h->Wh, (void*)h->Wl, (void*)h->Qh, (void*)h->Ql, (void*)h->yb, (void*)h->part, (void*)h->rhs, (void*)h->x2})
+                  (void*)h->Gm, (void*)h->pen, (void*)h->Wh, (void*)h->Wl, (void*)h->Qh, (void*)h->Ql, (void*)h->yb, (void*)h->part, (void*)h->rhs, (void*)h->x2, (void*)h->xcv, (void*)h->xcr})
     if (v) cudaFree(v);
   delete h;
 }
@@ -107,10 +109,10 @@ static mrf_status coefs(mrf_llr_s* h, const float2* x, const float2* nx, const f
 }
 
 // per-patch SVT of the coefficient blocks of Y (nuclear norms into h->nuc, thresholded blocks into h->P)
-static mrf_status svt(mrf_llr_s* h, float tau, cudaStream_t st) {
+static mrf_status svt(mrf_llr_s* h, const float2* Ysrc, float tau, cudaStream_t st) {
   const int nq = h->nc * h->nc, ppb = llr::kSvtThreads / 32;
   llr::k_llr_svt<<<(unsigned)((nq + ppb - 1) / ppb), llr::kSvtThreads, svt_smem(h->r), st>>>(
-      h->Y, h->corners, h->nc, h->N, h->p, h->r, tau, nq, h->P, h->nuc);
+      Ysrc, h->corners, h->nc, h->N, h->p, h->r, tau, nq, h->P, h->nuc);
   return check_launch("k_llr_svt");
 }
 
@@ -155,7 +157,10 @@ mrf_status mrf_llr_create(mrf_dict dict, int N, int p, int s, mrf_llr* out) {
             cudaMalloc((void**)&h->Y, V * h->r * sizeof(float2)) == cudaSuccess &&
             cudaMalloc((void**)&h->P, nq * p * p * h->r * sizeof(float2)) == cudaSuccess &&
             cudaMalloc((void**)&h->nx, V * h->L * sizeof(float2)) == cudaSuccess &&
-            cudaMalloc((void**)&h->nuc, nq * sizeof(double)) == cudaSuccess;
+            cudaMalloc((void**)&h->nuc, nq * sizeof(double)) == cudaSuccess &&
+            cudaMalloc((void**)&h->xcv, V * h->r * sizeof(float2)) == cudaSuccess &&
+            cudaMalloc((void**)&h->xcr, V * h->r * sizeof(float2)) == cudaSuccess;
+  h->basis_gen = dict->basis_gen;
   if (!ok) {
     llr_free(h);
     return fail(MRF_ENOMEM, "mrf_llr_create: device allocation failed");
@@ -267,8 +272,14 @@ mrf_status mrf_llr_laplacian(mrf_llr h, const float* params, const float* pd, do
   return MRF_OK;
 }
 
-mrf_status mrf_llr_step(mrf_llr h, mrf_plan plan, const void* x, const void* rhs, float mu, float lambda1,
-                        float lambda2, float beta, void* x_out, double* nuclear, double* penalty, void* stream) {
+}  // extern "C"
+
+// xcoef (nullable): the [V][r] coefficients of x when x = xcoef d is known to lie in span(d)
+// (the previous step's output inside mrf_msllr_solve); the manifold term then reads them instead
+// of projecting x again.
+static mrf_status step_impl(mrf_llr h, mrf_plan plan, const void* x, const void* rhs, float mu, float lambda1,
+                            float lambda2, float beta, void* x_out, double* nuclear, double* penalty, void* stream,
+                            const float2* xcoef) {
   if (!h || !plan || !x || !rhs || !x_out) return fail(MRF_EINVAL, "mrf_llr_step: null argument");
   if (!(mu > 0.f) || !(lambda1 >= 0.f) || !(lambda2 >= 0.f) || !(beta > 0.f) || !std::isfinite(mu * lambda2 * beta))
     return fail(MRF_EINVAL, "mrf_llr_step: need mu > 0, lambda1 >= 0, lambda2 >= 0, beta > 0");
@@ -284,9 +295,9 @@ mrf_status mrf_llr_step(mrf_llr h, mrf_plan plan, const void* x, const void* rhs
   // A^H A x (the plan checks that x has its shape: [L][N][N] device memory)
   MRF_TRY(mrf_normal(plan, x, h->nx, 0.f, stream));
   if (manifold) MRF_TRY(manifold_ws(h));
-  MRF_TRY(coefs(h, (const float2*)x, h->nx, (const float2*)rhs, mu, h->Y, manifold ? h->YX : nullptr, st));
+  MRF_TRY(coefs(h, (const float2*)x, h->nx, (const float2*)rhs, mu, h->Y, manifold && !xcoef ? h->YX : nullptr, st));
   if (manifold) {   // Y -= mu lambda1 coef(Q^*(Q(P_S x) L)),  L = D - W (Eq. 15's manifold term)
-    MRF_TRY(manifold_G(h, h->YX, st));
+    MRF_TRY(manifold_G(h, xcoef ? xcoef : h->YX, st));
     if (lambda1 > 0.f) {
       if (h->r <= 16)
         mfd::k_mfd_apply<16><<<(unsigned)((V + 255) / 256), 256, 0, st>>>(h->Y, h->Qm, h->Gm, h->deg, h->corners, h->nc,
@@ -301,15 +312,15 @@ mrf_status mrf_llr_step(mrf_llr h, mrf_plan plan, const void* x, const void* rhs
       MRF_TRY(check_launch("k_mfd_penalty"));
     }
   }
-  MRF_TRY(svt(h, 1.f / beta, st));
+  MRF_TRY(svt(h, h->Y, 1.f / beta, st));
   const float gamma = mu * lambda2 * beta;
   const unsigned gv = (unsigned)((V + 31) / 32);
   if (h->r <= 16)
     llr::k_llr_update<16><<<gv, 256, 0, st>>>(h->Y, h->P, h->corners, h->nc, h->N, h->p, h->r, h->dT, h->L, gamma,
-                                              (float2*)x_out);
+                                              (float2*)x_out, h->xcv, h->xcr);
   else
     llr::k_llr_update<32><<<gv, 256, 0, st>>>(h->Y, h->P, h->corners, h->nc, h->N, h->p, h->r, h->dT, h->L, gamma,
-                                              (float2*)x_out);
+                                              (float2*)x_out, h->xcv, h->xcr);
   MRF_TRY(check_launch("k_llr_update"));
   // Tr(Q(P_S x) L Q(P_S x)^H) and sum_q ||Q_q(Z)||_*: patches summed in a fixed order (synchronise)
   if (penalty) MRF_TRY(host_sum(h->pen, nq, st, penalty));
@@ -317,8 +328,8 @@ mrf_status mrf_llr_step(mrf_llr h, mrf_plan plan, const void* x, const void* rhs
   return MRF_OK;
 }
 
-mrf_status mrf_llr_cost(mrf_llr h, mrf_plan plan, const void* x, const void* b, float lambda1, float lambda2,
-                        double* cost, double* terms, void* stream) {
+static mrf_status cost_impl(mrf_llr h, mrf_plan plan, const void* x, const void* b, float lambda1, float lambda2,
+                            double* cost, double* terms, void* stream, const float2* xcoef) {
   if (!h || !plan || !x || !b) return fail(MRF_EINVAL, "mrf_llr_cost: null argument");
   if (!(lambda1 >= 0.f) || !(lambda2 >= 0.f)) return fail(MRF_EINVAL, "mrf_llr_cost: need lambda1, lambda2 >= 0");
   if (lambda1 > 0.f && !h->has_lap) return fail(MRF_EINVAL, "mrf_llr_cost: lambda1 > 0 needs mrf_llr_laplacian first");
@@ -345,24 +356,37 @@ mrf_status mrf_llr_cost(mrf_llr h, mrf_plan plan, const void* x, const void* b, 
   double t[3] = {0.0, 0.0, 0.0};
   MRF_TRY(host_sum(h->part, kStatBlocks, st, &t[0]));
   t[0] *= 0.5;
-  // coefficients of P_S x (k_llr_coef with mu = 0 reads x three times: x - 0 (x - x) = x)
+  // coefficients of P_S x (k_llr_coef with mu = 0 reads x three times: x - 0 (x - x) = x), unless known
   const float2* xf = (const float2*)x;
-  MRF_TRY(coefs(h, xf, xf, xf, 0.f, h->Y, nullptr, st));
+  if (!xcoef) MRF_TRY(coefs(h, xf, xf, xf, 0.f, h->Y, nullptr, st));
+  const float2* cf = xcoef ? xcoef : h->Y;
   const int nq = h->nc * h->nc;
   if (h->has_lap && (lambda1 > 0.f || terms)) {   // Tr(Q(P_S x) L Q(P_S x)^H)
     MRF_TRY(manifold_ws(h));
-    MRF_TRY(manifold_G(h, h->Y, st));
+    MRF_TRY(manifold_G(h, cf, st));
     mfd::k_mfd_penalty<<<nq, 256, 0, st>>>(h->Qm, h->Gm, h->deg, h->p * h->p * h->r, h->pen);
     MRF_TRY(check_launch("k_mfd_penalty"));
     MRF_TRY(host_sum(h->pen, nq, st, &t[1]));
   }
   // sum_q ||Q_q(P_S x)||_* (threshold +inf: only the singular values are used)
-  MRF_TRY(svt(h, INFINITY, st));
+  MRF_TRY(svt(h, cf, INFINITY, st));
   MRF_TRY(host_sum(h->nuc, nq, st, &t[2]));
   if (terms)
     for (int i = 0; i < 3; ++i) terms[i] = t[i];
   if (cost) *cost = t[0] + (double)lambda1 * t[1] + (double)lambda2 * t[2];
   return MRF_OK;
+}
+
+extern "C" {
+
+mrf_status mrf_llr_step(mrf_llr h, mrf_plan plan, const void* x, const void* rhs, float mu, float lambda1,
+                        float lambda2, float beta, void* x_out, double* nuclear, double* penalty, void* stream) {
+  return step_impl(h, plan, x, rhs, mu, lambda1, lambda2, beta, x_out, nuclear, penalty, stream, nullptr);
+}
+
+mrf_status mrf_llr_cost(mrf_llr h, mrf_plan plan, const void* x, const void* b, float lambda1, float lambda2,
+                        double* cost, double* terms, void* stream) {
+  return cost_impl(h, plan, x, b, lambda1, lambda2, cost, terms, stream, nullptr);
 }
 
 mrf_status mrf_msllr_solve(mrf_llr h, mrf_dict dict, mrf_plan plan, const void* b, const mrf_msllr_params* prm,
@@ -389,8 +413,16 @@ mrf_status mrf_msllr_solve(mrf_llr h, mrf_dict dict, mrf_plan plan, const void* 
   MRF_TRY(mrf_adjoint(plan, b, h->rhs, stream));
   CUDA_TRY(cudaMemcpyAsync(x, h->rhs, xbytes, cudaMemcpyDeviceToDevice, st));
   float lam1 = 0.f;
+  // after a step, x = Xc d lies in span(d) with Xc in h->xcv / h->xcr: Phi_D runs on the r
+  // coefficients (mrf_dict_match_coef) when the dictionary's basis is the operator's
+  const bool coef_ok = dict->basis_gen == h->basis_gen && dict->rank == h->r;
+  bool have_coef = false;
+  auto maps = [&](const void* cur) -> mrf_status {
+    if (have_coef && coef_ok) return mrf_dict_match_coef(dict, h->xcr, V, index, pd, params, stream);
+    return mrf_dict_match(dict, cur, V, index, pd, params, stream);
+  };
   auto update_maps = [&](const void* cur) -> mrf_status {
-    MRF_TRY(mrf_dict_match(dict, cur, V, index, pd, params, stream));
+    MRF_TRY(maps(cur));
     if (manifold) {
       double maxdeg = 0.0;
       MRF_TRY(mrf_llr_laplacian(h, params, pd, prm->sigma2, nullptr, &maxdeg, stream));
@@ -406,9 +438,11 @@ mrf_status mrf_msllr_solve(mrf_llr h, mrf_dict dict, mrf_plan plan, const void* 
   bool maps_current = manifold;
   for (int n = 1; n <= prm->max_iter; ++n) {
     // Z^n, P^n, X^n (Eqs. 15, 20, 21), then cost(n)
-    MRF_TRY(mrf_llr_step(h, plan, cur, h->rhs, prm->mu, lam1, prm->lambda2, prm->beta, nxt, nullptr, nullptr, stream));
+    MRF_TRY(step_impl(h, plan, cur, h->rhs, prm->mu, lam1, prm->lambda2, prm->beta, nxt, nullptr, nullptr, stream,
+                      have_coef ? h->xcv : nullptr));
+    have_coef = true;   // k_llr_update wrote the coefficients of nxt
     double c = 0.0;
-    MRF_TRY(mrf_llr_cost(h, plan, nxt, b, lam1, prm->lambda2, &c, nullptr, stream));
+    MRF_TRY(cost_impl(h, plan, nxt, b, lam1, prm->lambda2, &c, nullptr, stream, h->xcv));
     if (info && info->cost) info->cost[n - 1] = c;
     std::swap(cur, nxt);
     it = n;
@@ -421,7 +455,7 @@ mrf_status mrf_msllr_solve(mrf_llr h, mrf_dict dict, mrf_plan plan, const void* 
       maps_current = true;
     }
   }
-  if (!maps_current) MRF_TRY(mrf_dict_match(dict, cur, V, index, pd, params, stream));   // M^ = Phi_D(X^)
+  if (!maps_current) MRF_TRY(maps(cur));   // M^ = Phi_D(X^)
   if (cur != x) CUDA_TRY(cudaMemcpyAsync(x, cur, xbytes, cudaMemcpyDeviceToDevice, st));
   if (info) {
     info->iters = it;

@@ -255,7 +255,10 @@ template <int R>
 __global__ void __launch_bounds__(256) k_llr_update(const float2* __restrict__ Y, const float2* __restrict__ P,
                                                     const int* __restrict__ corners, int nc, int N, int p, int r,
                                                     const float2* __restrict__ dT, int L, float gamma,
-                                                    float2* __restrict__ xout) {
+                                                    float2* __restrict__ xout, float2* __restrict__ xcv,
+                                                    float2* __restrict__ xcr) {
+  // xcv [V][r] / xcr [r][V] (nullable): the coefficients Xc of x+ in both layouts (x+ = Xc d
+  // lies in span(d): the next step's manifold term, the cost and Phi_D read them instead of x+)
   __shared__ float2 xcs[R][33];
   const int V = N * N;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -294,8 +297,14 @@ __global__ void __launch_bounds__(256) k_llr_update(const float2* __restrict__ Y
     }
 #pragma unroll
     for (int i = 0; i < R; ++i) xcs[i][lane] = xc[i];
+    if (xcv && v < V)
+#pragma unroll
+      for (int i = 0; i < R; ++i)
+        if (i < r) xcv[(size_t)v * r + i] = xc[i];
   }
   __syncthreads();
+  if (xcr && v < V)
+    for (int i = w; i < r; i += 8) xcr[(size_t)i * V + v] = xcs[i][lane];
   if (v >= V) return;
   float2 xc[R];
 #pragma unroll

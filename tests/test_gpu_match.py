@@ -101,3 +101,31 @@ def test_invalid_calls(binding):
     with pytest.raises(TypeError):
         dic.match(torch.zeros((32, 5), dtype=torch.complex64))
     dic.close()
+
+
+def test_match_in_basis_coordinates_equals_the_frame_match(binding):
+    """mrf_dict_match_coef(u) = mrf_dict_match(x) for x = sum_i u_i d_i in span(d): same atom
+    except valid near-ties (scores from the frame-domain correlations), pd to 1e-4.  Both sides
+    are the library's; the frame-domain match is parity-tested against the oracle above."""
+    L = 300
+    grid = sd.t1t2_grid()[::7]
+    D = sd.surrogate_dictionary(L, grid)
+    dic = binding.Dictionary(D, grid.astype(np.float32))
+    d = dic.basis(0.9999, 32)                                    # [r][L]
+    X, _, _ = sd.voxel_fingerprints(D, 777, noise=0.02)          # [V][L]
+    u = (X @ np.conj(d).T).astype(np.complex64)                  # coefficients of P_S x: [V][r]
+    x = (u.astype(np.complex128) @ d.astype(np.complex128)).astype(np.complex64)   # x in span(d)
+    ic, pc, qc = dic.match_coef(torch.from_numpy(np.ascontiguousarray(u.T)).cuda())
+    ix, px, qx = dic.match(torch.from_numpy(np.ascontiguousarray(x.T)).cuda())
+    ic, ix = ic.cpu().numpy(), ix.cpu().numpy()
+    # normalised correlations of x (plain numpy here: x is built from the library's basis, so the
+    # oracle is not run on it)
+    score = np.abs(x.astype(np.complex128) @ np.conj(D).T) / np.linalg.norm(D, axis=1)[None, :]
+    s_best = score.max(axis=1)
+    same = ic == ix
+    assert same.mean() > 0.95
+    V = len(ic)
+    assert np.all(score[np.arange(V), ic] >= (1 - TIE_REL) * s_best)
+    assert np.allclose(pc.cpu().numpy()[same], px.cpu().numpy()[same], rtol=1e-4, atol=1e-6 * px.max().item())
+    assert np.array_equal(qc.cpu().numpy()[same], qx.cpu().numpy()[same])
+    dic.close()
