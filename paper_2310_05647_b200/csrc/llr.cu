@@ -112,7 +112,7 @@ static mrf_status coefs(mrf_llr_s* h, const float2* x, const float2* nx, const f
 static mrf_status svt(mrf_llr_s* h, const float2* Ysrc, float tau, cudaStream_t st) {
   const int nq = h->nc * h->nc, ppb = llr::kSvtThreads / 32;
   llr::k_llr_svt<<<(unsigned)((nq + ppb - 1) / ppb), llr::kSvtThreads, svt_smem(h->r), st>>>(
-      Ysrc, h->corners, h->nc, h->N, h->p, h->r, tau, nq, h->P, h->nuc);
+      Ysrc, h->corners, h->nc, h->N, h->p, h->r, tau, nq, std::isinf(tau) ? nullptr : h->P, h->nuc);
   return check_launch("k_llr_svt");
 }
 
@@ -225,34 +225,45 @@ mrf_status mrf_llr_laplacian(mrf_llr h, const float* params, const float* pd, do
   }
   CUDA_TRY(cudaMemcpyAsync(h->stats, ms, sizeof(ms), cudaMemcpyHostToDevice, st));
   mfd::k_mfd_patchvec<<<n, 128, 0, st>>>(params, pd, h->stats, h->corners, h->nc, h->N, h->p, h->pv);
-  const dim3 gd((unsigned)((n + 31) / 32), (unsigned)((n + 31) / 32));
+  const dim3 gd((unsigned)((n + 63) / 64), (unsigned)((n + 63) / 64));
   mfd::k_mfd_dist<<<gd, 256, 0, st>>>(h->pv, n, 3 * np, h->W);
   MRF_TRY(check_launch("k_mfd_dist"));
   if (!(sigma2 > 0.0)) {   // sigma^2 = median of the nonzero upper-triangle distances (exact radix select)
-    std::vector<unsigned> hh(65536);
-    CUDA_TRY(cudaMemsetAsync(h->hist, 0, 65536 * sizeof(unsigned), st));
-    mfd::k_mfd_hist<<<1024, 256, 0, st>>>(h->W, n, 0, 0u, h->hist);
-    CUDA_TRY(cudaMemcpyAsync(hh.data(), h->hist, 65536 * sizeof(unsigned), cudaMemcpyDeviceToHost, st));
-    CUDA_TRY(cudaStreamSynchronize(st));
+    // the k-th smallest nonzero value bit pattern by three histogram passes (11 + 11 + 10 bits);
+    // positive floats order as their bits
+    std::vector<unsigned> hh(2048);
+    auto pass = [&](int ps, unsigned pre) -> mrf_status {
+      CUDA_TRY(cudaMemsetAsync(h->hist, 0, 2048 * sizeof(unsigned), st));
+      mfd::k_mfd_hist<<<2 * 148, 256, 0, st>>>(h->W, n, ps, pre, h->hist);
+      MRF_TRY(check_launch("k_mfd_hist"));
+      CUDA_TRY(cudaMemcpyAsync(hh.data(), h->hist, 2048 * sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+      CUDA_TRY(cudaStreamSynchronize(st));
+      return MRF_OK;
+    };
+    MRF_TRY(pass(0, 0u));
+    const std::vector<unsigned> h0 = hh;
     unsigned long long m = 0;
-    for (unsigned c : hh) m += c;
+    for (unsigned c : h0) m += c;
     if (m == 0) {
       sigma2 = 1.0;
     } else {
       const unsigned long long ks[2] = {(m - 1) / 2, m / 2};   // numpy's median: mean of the two middle
       float vals[2];
       for (int t = 0; t < 2; ++t) {
+        if (t == 1 && ks[1] == ks[0]) {
+          vals[1] = vals[0];
+          break;
+        }
         unsigned long long c = 0;
-        unsigned hi = 0;
-        while (c + hh[hi] <= ks[t]) c += hh[hi++];
-        std::vector<unsigned> lo(65536);
-        CUDA_TRY(cudaMemsetAsync(h->hist, 0, 65536 * sizeof(unsigned), st));
-        mfd::k_mfd_hist<<<1024, 256, 0, st>>>(h->W, n, 1, hi, h->hist);
-        CUDA_TRY(cudaMemcpyAsync(lo.data(), h->hist, 65536 * sizeof(unsigned), cudaMemcpyDeviceToHost, st));
-        CUDA_TRY(cudaStreamSynchronize(st));
-        unsigned lw = 0;
-        while (c + lo[lw] <= ks[t]) c += lo[lw++];
-        const unsigned bits = (hi << 16) | lw;
+        unsigned b0 = 0;
+        while (c + h0[b0] <= ks[t]) c += h0[b0++];
+        MRF_TRY(pass(1, b0));
+        unsigned b1 = 0;
+        while (c + hh[b1] <= ks[t]) c += hh[b1++];
+        MRF_TRY(pass(2, (b0 << 11) | b1));
+        unsigned b2 = 0;
+        while (c + hh[b2] <= ks[t]) c += hh[b2++];
+        const unsigned bits = (b0 << 21) | (b1 << 10) | b2;
         std::memcpy(&vals[t], &bits, 4);
       }
       sigma2 = 0.5 * ((double)vals[0] + (double)vals[1]);
@@ -277,9 +288,11 @@ mrf_status mrf_llr_laplacian(mrf_llr h, const float* params, const float* pd, do
 // xcoef (nullable): the [V][r] coefficients of x when x = xcoef d is known to lie in span(d)
 // (the previous step's output inside mrf_msllr_solve); the manifold term then reads them instead
 // of projecting x again.
+// ax (nullable): A x already computed (the previous cost's forward inside mrf_msllr_solve), so
+// A^H A x = A^H (A x) is one adjoint instead of a normal application.
 static mrf_status step_impl(mrf_llr h, mrf_plan plan, const void* x, const void* rhs, float mu, float lambda1,
                             float lambda2, float beta, void* x_out, double* nuclear, double* penalty, void* stream,
-                            const float2* xcoef) {
+                            const float2* xcoef, const float2* ax = nullptr) {
   if (!h || !plan || !x || !rhs || !x_out) return fail(MRF_EINVAL, "mrf_llr_step: null argument");
   if (!(mu > 0.f) || !(lambda1 >= 0.f) || !(lambda2 >= 0.f) || !(beta > 0.f) || !std::isfinite(mu * lambda2 * beta))
     return fail(MRF_EINVAL, "mrf_llr_step: need mu > 0, lambda1 >= 0, lambda2 >= 0, beta > 0");
@@ -293,7 +306,8 @@ static mrf_status step_impl(mrf_llr h, mrf_plan plan, const void* x, const void*
   cudaStream_t st = (cudaStream_t)stream;
   const int V = h->N * h->N, nq = h->nc * h->nc;
   // A^H A x (the plan checks that x has its shape: [L][N][N] device memory)
-  MRF_TRY(mrf_normal(plan, x, h->nx, 0.f, stream));
+  if (ax) MRF_TRY(mrf_adjoint(plan, ax, h->nx, stream));
+  else MRF_TRY(mrf_normal(plan, x, h->nx, 0.f, stream));
   if (manifold) MRF_TRY(manifold_ws(h));
   MRF_TRY(coefs(h, (const float2*)x, h->nx, (const float2*)rhs, mu, h->Y, manifold && !xcoef ? h->YX : nullptr, st));
   if (manifold) {   // Y -= mu lambda1 coef(Q^*(Q(P_S x) L)),  L = D - W (Eq. 15's manifold term)
@@ -368,7 +382,7 @@ static mrf_status cost_impl(mrf_llr h, mrf_plan plan, const void* x, const void*
     MRF_TRY(check_launch("k_mfd_penalty"));
     MRF_TRY(host_sum(h->pen, nq, st, &t[1]));
   }
-  // sum_q ||Q_q(P_S x)||_* (threshold +inf: only the singular values are used)
+  // sum_q ||Q_q(P_S x)||_* (threshold +inf: only the singular values, no thresholded blocks)
   MRF_TRY(svt(h, cf, INFINITY, st));
   MRF_TRY(host_sum(h->nuc, nq, st, &t[2]));
   if (terms)
@@ -438,8 +452,9 @@ mrf_status mrf_msllr_solve(mrf_llr h, mrf_dict dict, mrf_plan plan, const void* 
   bool maps_current = manifold;
   for (int n = 1; n <= prm->max_iter; ++n) {
     // Z^n, P^n, X^n (Eqs. 15, 20, 21), then cost(n)
+    // from n = 2 on, A X^{n-1} is the previous cost's forward (h->yb): A^H A X^{n-1} = A^H (h->yb)
     MRF_TRY(step_impl(h, plan, cur, h->rhs, prm->mu, lam1, prm->lambda2, prm->beta, nxt, nullptr, nullptr, stream,
-                      have_coef ? h->xcv : nullptr));
+                      have_coef ? h->xcv : nullptr, have_coef ? h->yb : nullptr));
     have_coef = true;   // k_llr_update wrote the coefficients of nxt
     double c = 0.0;
     MRF_TRY(cost_impl(h, plan, nxt, b, lam1, prm->lambda2, &c, nullptr, stream, h->xcv));

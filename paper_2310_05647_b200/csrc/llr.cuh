@@ -219,6 +219,7 @@ static __global__ void __launch_bounds__(kSvtThreads) k_llr_svt(const float2* __
     if (lane == 0) f[j] = sj > (double)tau ? 1.0 - (double)tau / sj : 0.0;
   }
   if (lane == 0) nuc[q] = sig;
+  if (!P) return;   // singular values only (the cost's nuclear norms)
   __syncwarp();
   // 3. M = W F W^H
   for (int e = lane; e < r * r; e += 32) {
@@ -431,47 +432,74 @@ static __global__ void k_mfd_patchvec(const float* __restrict__ params, const fl
 }
 
 // d2[i][j] = ||pv_i - pv_j||^2, 32 x 32 tiles of patch pairs
-static __global__ void k_mfd_dist(const float* __restrict__ pv, int n, int dim, float* __restrict__ d2) {
-  __shared__ float A[32][33], B[32][33];
-  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;   // 32 x 8 threads
-  const int i0 = blockIdx.y * 32, j0 = blockIdx.x * 32;
-  float acc[4] = {0.f, 0.f, 0.f, 0.f};
-  for (int k0 = 0; k0 < dim; k0 += 32) {
-    for (int r = ty; r < 32; r += 8) {
-      A[r][tx] = (i0 + r < n && k0 + tx < dim) ? pv[(size_t)(i0 + r) * dim + k0 + tx] : 0.f;
-      B[r][tx] = (j0 + r < n && k0 + tx < dim) ? pv[(size_t)(j0 + r) * dim + k0 + tx] : 0.f;
+// d2[i][j] = ||pv_i - pv_j||^2 over dim components: 64 x 64 tiles of the upper triangle (the
+// lower one is the mirror), 16 x 16 threads with 4 x 4 outputs each, 16-component chunks in smem.
+static __global__ void __launch_bounds__(256) k_mfd_dist(const float* __restrict__ pv, int n, int dim,
+                                                         float* __restrict__ d2) {
+  if (blockIdx.y > blockIdx.x) return;   // lower-triangle tile: written by its mirror
+  __shared__ float A[16][65], B[16][65];   // [component][row]
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const int i0 = blockIdx.y * 64, j0 = blockIdx.x * 64;
+  float acc[4][4] = {};
+  for (int k0 = 0; k0 < dim; k0 += 16) {
+    for (int e = threadIdx.x; e < 16 * 64; e += 256) {   // coalesced over the components
+      const int rr = e / 16, kk = e % 16;
+      A[kk][rr] = (i0 + rr < n && k0 + kk < dim) ? pv[(size_t)(i0 + rr) * dim + k0 + kk] : 0.f;
+      B[kk][rr] = (j0 + rr < n && k0 + kk < dim) ? pv[(size_t)(j0 + rr) * dim + k0 + kk] : 0.f;
     }
     __syncthreads();
-#pragma unroll 8
-    for (int k = 0; k < 32; ++k) {
-      const float b = B[tx][k];
+#pragma unroll
+    for (int kk = 0; kk < 16; ++kk) {
+      float a[4], bb[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
-        const float dd = A[ty + 8 * u][k] - b;
-        acc[u] = fmaf(dd, dd, acc[u]);
+        a[u] = A[kk][ty + 16 * u];
+        bb[u] = B[kk][tx + 16 * u];
       }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          const float dd = a[u] - bb[v];
+          acc[u][v] = fmaf(dd, dd, acc[u][v]);
+        }
     }
     __syncthreads();
   }
 #pragma unroll
-  for (int u = 0; u < 4; ++u) {
-    const int i = i0 + ty + 8 * u, j = j0 + tx;
-    if (i < n && j < n) d2[(size_t)i * n + j] = acc[u];
-  }
+  for (int u = 0; u < 4; ++u)
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      const int i = i0 + ty + 16 * u, j = j0 + tx + 16 * v;
+      if (i < n && j < n) {
+        d2[(size_t)i * n + j] = acc[u][v];
+        d2[(size_t)j * n + i] = acc[u][v];
+      }
+    }
 }
 
-// histogram of the strict upper triangle's nonzero d2 bits: pass 0 on the high 16 bits, pass 1
-// on the low 16 bits of the values whose high bits equal `hi`
-static __global__ void k_mfd_hist(const float* __restrict__ d2, int n, int pass, unsigned hi, unsigned* __restrict__ hist) {
-  const long long total = (long long)n * n;
-  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total; e += (long long)gridDim.x * blockDim.x) {
-    const int i = (int)(e / n), j = (int)(e % n);
-    if (j <= i) continue;
-    const unsigned b = __float_as_uint(d2[e]);
-    if (b == 0u) continue;
-    if (pass == 0) atomicAdd(&hist[b >> 16], 1u);
-    else if ((b >> 16) == hi) atomicAdd(&hist[b & 0xFFFFu], 1u);
-  }
+// Radix select of the nonzero strict-upper-triangle d2 bits, 11 + 11 + 10 bits: pass 0 counts
+// bits [31:21], pass 1 bits [20:10] of the values whose bits [31:21] equal `pre`, pass 2 bits
+// [9:0] of those whose bits [31:10] equal `pre`.  Block-private shared-memory histograms (2048
+// bins), merged with one global atomic per non-empty bin.
+static __global__ void __launch_bounds__(256) k_mfd_hist(const float* __restrict__ d2, int n, int pass, unsigned pre,
+                                                         unsigned* __restrict__ hist) {
+  __shared__ unsigned sh[2048];
+  for (int i = threadIdx.x; i < 2048; i += blockDim.x) sh[i] = 0u;
+  __syncthreads();
+  const int shift = pass == 0 ? 21 : pass == 1 ? 10 : 0;
+  const unsigned mask = pass == 2 ? 0x3FFu : 0x7FFu;
+  const int pshift = pass == 0 ? 32 : pass == 1 ? 21 : 10;
+  for (int i = blockIdx.x; i < n; i += gridDim.x)   // row i, columns j > i (coalesced)
+    for (int j = i + 1 + (int)threadIdx.x; j < n; j += blockDim.x) {
+      const unsigned b = __float_as_uint(d2[(size_t)i * n + j]);
+      if (b == 0u) continue;
+      if (pass > 0 && (b >> pshift) != pre) continue;
+      atomicAdd(&sh[(b >> shift) & mask], 1u);
+    }
+  __syncthreads();
+  for (int i = threadIdx.x; i < 2048; i += blockDim.x)
+    if (sh[i]) atomicAdd(&hist[i], sh[i]);
 }
 
 // W[i][j] = exp(-d2 / sigma2) (i != j), 0 on the diagonal; deg[i] = sum_j W[i][j] in a fixed order
