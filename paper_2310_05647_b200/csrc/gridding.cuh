@@ -921,6 +921,152 @@ k_toep_cols(DevPlan p, const float2* __restrict__ Hf, float2* __restrict__ Ha, c
   }
 }
 
+// ============================================================================ subspace normal
+// P_S A^H A in basis coordinates (SURVEY.md §8(f) f2 on a Toeplitz plan): for
+// x = sum_i u_i d_i (d: r x L orthonormal rows) the coefficients of P_S(A^H A x) are
+//   z_j = sum_i crop F^-1 [K_ji ⊙ F pad(u_i)],   K_ji = sum_rho c^rho_ji T_rho,
+//   c^rho_ji = sum_{l : interleaf(l) = rho} conj(d_jl) d_il,
+// with T_rho the real PSF spectra of the Toeplitz plan: r row/column FFT pairs and an r x r
+// mixing per frequency instead of L frames of A^H A.  The spectra of one (frame, coil) are kept in
+// the PSF layout [strip][row][16] (E = G * G elements).
+template <int G>
+constexpr size_t sn_cols_smem() { return (size_t(G) + size_t(G) * SW) * 8; }
+
+// forward column FFT of the strip-major half grid (pruned input rows), spectrum out
+template <int G>
+__global__ void __launch_bounds__(SW * FFTShape<G>::T) k_sn_fcols(const float2* __restrict__ tw,
+                                                                   const float2* __restrict__ Hf,
+                                                                   float2* __restrict__ spec, int nfc) {
+  using F = FFTShape<G>;
+  constexpr int P = F::P, Q = F::Q, T = F::T, N = G / 2, A = Q / T, B = P / T, S = G / SW;
+  extern __shared__ __align__(128) unsigned char smraw[];
+  float2* stw = reinterpret_cast<float2*>(smraw);
+  float2* ex = stw + G;
+  const int tid = threadIdx.x, c = tid % SW, t = tid / SW;
+  for (int i = tid; i < G; i += blockDim.x) stw[i] = tw[i];
+  __syncthreads();
+  for (int item = blockIdx.x; item < nfc * S; item += gridDim.x) {
+    const float2* in = Hf + (size_t)item * N * SW;   // [fc][s] strip: N rows x 16
+    float2 v[A][P];
+#pragma unroll
+    for (int a = 0; a < A; ++a) {
+      const int n2 = t + T * a;
+#pragma unroll
+      for (int n1 = 0; n1 < P; ++n1)
+        v[a][n1] = (n1 < P / 4 || n1 >= 3 * P / 4) ? in[grid_to_img<G>(Q * n1 + n2) * SW + c] : make_float2(0.f, 0.f);
+    }
+#pragma unroll
+    for (int a = 0; a < A; ++a) {
+      const int n2 = t + T * a;
+      dft_halfzero<P, -1>(v[a]);
+#pragma unroll
+      for (int k1 = 0; k1 < P; k1 += 2) {
+        const float4 tt = tw_pair(stw, n2 * P + k1);
+        ex[(n2 * P + k1) * SW + c] = cmul(v[a][k1], make_float2(tt.x, tt.y));
+        ex[(n2 * P + k1 + 1) * SW + c] = cmul(v[a][k1 + 1], make_float2(tt.z, tt.w));
+      }
+    }
+    __syncthreads();
+    float2* out = spec + (size_t)item * G * SW;
+#pragma unroll
+    for (int b = 0; b < B; ++b) {
+      const int k1 = t + T * b;
+      float2 w[Q];
+#pragma unroll
+      for (int n2 = 0; n2 < Q; ++n2) w[n2] = ex[(n2 * P + k1) * SW + c];
+      dft<Q, -1>(w);                                   // w[k2] = X[k1 + P k2]
+#pragma unroll
+      for (int k2 = 0; k2 < Q; ++k2) out[(size_t)(k1 + P * k2) * SW + c] = w[k2];
+    }
+    __syncthreads();
+  }
+}
+
+// inverse column FFT of a spectrum (the transposed split of k_toep_cols), the N kept rows stored
+// row-major [fc][iy][G] for k_adj_rows
+template <int G>
+__global__ void __launch_bounds__(SW * FFTShape<G>::T) k_sn_icols(const float2* __restrict__ tw,
+                                                                   const float2* __restrict__ spec,
+                                                                   float2* __restrict__ Ha, int nfc) {
+  using F = FFTShape<G>;
+  constexpr int P = F::P, Q = F::Q, T = F::T, N = G / 2, A = Q / T, B = P / T, S = G / SW;
+  extern __shared__ __align__(128) unsigned char smraw[];
+  float2* stw = reinterpret_cast<float2*>(smraw);
+  float2* ex = stw + G;
+  const int tid = threadIdx.x, c = tid % SW, t = tid / SW;
+  for (int i = tid; i < G; i += blockDim.x) stw[i] = tw[i];
+  __syncthreads();
+  for (int item = blockIdx.x; item < nfc * S; item += gridDim.x) {
+    const int fc = item / S, s = item % S;
+    const float2* in = spec + (size_t)item * G * SW;
+#pragma unroll
+    for (int b = 0; b < B; ++b) {
+      const int k1 = t + T * b;
+      float2 w[Q];
+#pragma unroll
+      for (int k2 = 0; k2 < Q; ++k2) w[k2] = in[(size_t)(k1 + P * k2) * SW + c];
+      dft<Q, +1>(w);                                   // stage A of the inverse: index n2
+#pragma unroll
+      for (int n2 = 0; n2 < Q; ++n2) ex[(n2 * P + k1) * SW + c] = cmulc(w[n2], stw[n2 * P + k1]);
+    }
+    __syncthreads();
+    float2* Hc = Ha + (size_t)fc * N * G + (size_t)s * SW + c;
+#pragma unroll
+    for (int a = 0; a < A; ++a) {
+      const int n2 = t + T * a;
+      float2 u[P];
+#pragma unroll
+      for (int k1 = 0; k1 < P; ++k1) u[k1] = ex[(n2 * P + k1) * SW + c];
+      dft_halfout<P, +1>(u);                           // stage B: index n1, row n2 + Q n1
+#pragma unroll
+      for (int n1 = 0; n1 < P; ++n1)
+        if (n1 < P / 4 || n1 >= 3 * P / 4) Hc[(size_t)grid_to_img<G>(n2 + Q * n1) * G] = u[n1];
+    }
+    __syncthreads();
+  }
+}
+
+// spec_out[j][c][e] = sum_i K[j][i][e] spec_in[i][c][e]   (r x r mixing per frequency; R >= r)
+template <int R>
+__global__ void __launch_bounds__(256) k_sn_mix(const float2* __restrict__ spec_in, const float2* __restrict__ K,
+                                                float2* __restrict__ spec_out, int r, int C, long long E) {
+  const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (idx >= (long long)C * E) return;
+  const int c = (int)(idx / E);
+  const long long e = idx % E;
+  float2 u[R];
+#pragma unroll
+  for (int i = 0; i < R; ++i) u[i] = i < r ? __ldg(spec_in + ((size_t)i * C + c) * E + e) : make_float2(0.f, 0.f);
+  for (int j = 0; j < r; ++j) {
+    float2 acc = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int i = 0; i < R; ++i)
+      if (i < r) {
+        const float2 k = __ldg(K + ((size_t)j * r + i) * E + e);
+        acc.x = fmaf(k.x, u[i].x, fmaf(-k.y, u[i].y, acc.x));
+        acc.y = fmaf(k.x, u[i].y, fmaf(k.y, u[i].x, acc.y));
+      }
+    spec_out[((size_t)j * C + c) * E + e] = acc;
+  }
+}
+
+// K[pair][e] = sum_rho cc[pair][rho] T_rho[e]  (plan time; pairs = r * r, T real)
+__global__ void __launch_bounds__(256) k_sn_kbuild(const float* __restrict__ psf, const float2* __restrict__ cc,
+                                                   int pairs, int R, long long E, float2* __restrict__ K) {
+  const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (idx >= (long long)pairs * E) return;
+  const int pr = (int)(idx / E);
+  const long long e = idx % E;
+  float ax = 0.f, ay = 0.f;
+  for (int rho = 0; rho < R; ++rho) {
+    const float tv = __ldg(psf + (size_t)rho * E + e);
+    const float2 cv = __ldg(cc + (size_t)pr * R + rho);
+    ax = fmaf(cv.x, tv, ax);
+    ay = fmaf(cv.y, tv, ay);
+  }
+  K[idx] = make_float2(ax, ay);
+}
+
 // ---------------------------------------------------------------------------- PSF (plan time)
 // T[my][mx] = 1/(G^2 N^2) sum_j D(ky_j - my/G) D(kx_j - mx/G),
 // D(theta) = sum_{d=-(N-1)}^{N-1} e^{i 2 pi d theta} = sin((2N-1) pi theta) / sin(pi theta):

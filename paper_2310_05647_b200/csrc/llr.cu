@@ -33,6 +33,11 @@ struct mrf_llr_s {
   float2 *rhs = nullptr, *x2 = nullptr;   // mrf_msllr_solve: A^H b and the second iterate buffer
   float2 *xcv = nullptr, *xcr = nullptr;  // coefficients of the last x_out: [V][r] and [r][V]
   unsigned basis_gen = 0;                 // the dictionary's basis generation at creation
+  std::vector<float2> basis_h;            // host [r][L] copy of the basis
+  // basis-coordinate loop on Toeplitz plans (mrf_msllr_solve): mixing kernels [r][r][G*G], the
+  // spectra workspaces [r][C][G*G], zs = P_S A^H A x and bv = P_S A^H b coefficients
+  float2 *Ksn = nullptr, *spa = nullptr, *spb = nullptr, *zs = nullptr, *bv = nullptr;
+  size_t sn_bytes = 0;
   // manifold term (mrf_llr_laplacian)
   bool has_lap = false;
   float* W = nullptr;         // [n][n] similarity weights (Eq. 8), first the squared distances
@@ -56,7 +61,8 @@ static void llr_free(mrf_llr_s* h) {
   cudaSetDevice(h->device);
   for (void* v : {(void*)h->dT, (void*)h->corners, (void*)h->Y, (void*)h->P, (void*)h->nx, (void*)h->nuc, (void*)h->W,
                   (void*)h->deg, (void*)h->pv, (void*)h->hist, (void*)h->stats, (void*)h->YX, (void*)h->Qm,
-                  (void*)h->Gm, (void*)h->pen, (void*)h->Wh, (void*)h->Wl, (void*)h->Qh, (void*)h->Ql, (void*)h->yb, (void*)h->part, (void*)h->rhs, (void*)h->x2, (void*)h->xcv, (void*)h->xcr})
+                  (void*)h->Gm, (void*)h->pen, (void*)h->Wh, (void*)h->Wl, (void*)h->Qh, (void*)h->Ql, (void*)h->yb, (void*)h->part, (void*)h->rhs, (void*)h->x2, (void*)h->xcv, (void*)h->xcr, (void*)h->Ksn,
+                  (void*)h->spa, (void*)h->spb, (void*)h->zs, (void*)h->bv})
     if (v) cudaFree(v);
   delete h;
 }
@@ -161,6 +167,7 @@ mrf_status mrf_llr_create(mrf_dict dict, int N, int p, int s, mrf_llr* out) {
             cudaMalloc((void**)&h->xcv, V * h->r * sizeof(float2)) == cudaSuccess &&
             cudaMalloc((void**)&h->xcr, V * h->r * sizeof(float2)) == cudaSuccess;
   h->basis_gen = dict->basis_gen;
+  h->basis_h = dict->basis_h;
   if (!ok) {
     llr_free(h);
     return fail(MRF_ENOMEM, "mrf_llr_create: device allocation failed");
@@ -391,6 +398,67 @@ static mrf_status cost_impl(mrf_llr h, mrf_plan plan, const void* x, const void*
   return MRF_OK;
 }
 
+// float64 sum over a grid-stride kernel's kStatBlocks partials (fixed order; synchronises)
+static mrf_status dot_re(mrf_llr_s* h, const float2* a, const float2* b, size_t n, cudaStream_t st, double* out) {
+  llr::k_llr_dotre<<<kStatBlocks, 256, 0, st>>>(a, b, n, h->part);
+  MRF_TRY(check_launch("k_llr_dotre"));
+  return host_sum(h->part, kStatBlocks, st, out);
+}
+
+// One step of Algorithm 1 in basis coordinates (x = xcv d; zs = P_S A^H A x from the previous
+// cost): Y = xcv - mu (zs - bv) [- mu lambda1 coef(Q^*(Q(x) L))], SVT, the Eq. 21 update of the
+// coefficients (no frame-domain image).
+static mrf_status sub_step(mrf_llr_s* h, float mu, float lambda1, float lambda2, float beta, cudaStream_t st) {
+  const int V = h->N * h->N;
+  llr::k_sn_grad<<<(unsigned)((V + 255) / 256), 256, 0, st>>>(h->xcv, h->zs, h->bv, mu, h->r, V, h->Y);
+  MRF_TRY(check_launch("k_sn_grad"));
+  if (lambda1 > 0.f) {
+    MRF_TRY(manifold_ws(h));
+    MRF_TRY(manifold_G(h, h->xcv, st));
+    if (h->r <= 16)
+      mfd::k_mfd_apply<16><<<(unsigned)((V + 255) / 256), 256, 0, st>>>(h->Y, h->Qm, h->Gm, h->deg, h->corners, h->nc,
+                                                                         h->N, h->p, h->r, mu * lambda1);
+    else
+      mfd::k_mfd_apply<32><<<(unsigned)((V + 255) / 256), 256, 0, st>>>(h->Y, h->Qm, h->Gm, h->deg, h->corners, h->nc,
+                                                                         h->N, h->p, h->r, mu * lambda1);
+    MRF_TRY(check_launch("k_mfd_apply"));
+  }
+  MRF_TRY(svt(h, h->Y, 1.f / beta, st));
+  const float gamma = mu * lambda2 * beta;
+  const unsigned gv = (unsigned)((V + 31) / 32);
+  if (h->r <= 16)
+    llr::k_llr_update<16><<<gv, 256, 0, st>>>(h->Y, h->P, h->corners, h->nc, h->N, h->p, h->r, h->dT, h->L, gamma,
+                                              nullptr, h->xcv, h->xcr);
+  else
+    llr::k_llr_update<32><<<gv, 256, 0, st>>>(h->Y, h->P, h->corners, h->nc, h->N, h->p, h->r, h->dT, h->L, gamma,
+                                              nullptr, h->xcv, h->xcr);
+  return check_launch("k_llr_update");
+}
+
+// cost(n) in basis coordinates: zs = P_S A^H A x (kept for the next step),
+// 1/2 ||A x - b||^2 = 1/2 <x, A^H A x> - Re <x, A^H b> + 1/2 ||b||^2 = 1/2 <u, zs> - Re <u, bv> + b2 / 2,
+// the trace term and the nuclear norms from the coefficients
+static mrf_status sub_cost(mrf_llr_s* h, mrf_plan plan, double b2, float lambda1, float lambda2, double* cost,
+                           cudaStream_t st) {
+  const size_t n = (size_t)h->N * h->N * h->r;
+  MRF_TRY(sn_apply(plan, h->Ksn, h->r, h->xcr, h->zs, h->spa, h->spb, st));
+  double uz = 0.0, ub = 0.0, tr = 0.0, nuc = 0.0;
+  MRF_TRY(dot_re(h, h->xcr, h->zs, n, st, &uz));
+  MRF_TRY(dot_re(h, h->xcv, h->bv, n, st, &ub));
+  const int nq = h->nc * h->nc;
+  if (h->has_lap && lambda1 > 0.f) {
+    MRF_TRY(manifold_ws(h));
+    MRF_TRY(manifold_G(h, h->xcv, st));
+    mfd::k_mfd_penalty<<<nq, 256, 0, st>>>(h->Qm, h->Gm, h->deg, h->p * h->p * h->r, h->pen);
+    MRF_TRY(check_launch("k_mfd_penalty"));
+    MRF_TRY(host_sum(h->pen, nq, st, &tr));
+  }
+  MRF_TRY(svt(h, h->xcv, INFINITY, st));
+  MRF_TRY(host_sum(h->nuc, nq, st, &nuc));
+  *cost = (0.5 * uz - ub + 0.5 * b2) + (double)lambda1 * tr + (double)lambda2 * nuc;
+  return MRF_OK;
+}
+
 extern "C" {
 
 mrf_status mrf_llr_step(mrf_llr h, mrf_plan plan, const void* x, const void* rhs, float mu, float lambda1,
@@ -430,6 +498,37 @@ mrf_status mrf_msllr_solve(mrf_llr h, mrf_dict dict, mrf_plan plan, const void* 
   // after a step, x = Xc d lies in span(d) with Xc in h->xcv / h->xcr: Phi_D runs on the r
   // coefficients (mrf_dict_match_coef) when the dictionary's basis is the operator's
   const bool coef_ok = dict->basis_gen == h->basis_gen && dict->rank == h->r;
+  // Toeplitz plans: from n = 2 on the loop runs in basis coordinates (the subspace normal, the
+  // cost by the inner-product identity; frames only for X^0, the first step and the output)
+  const bool sub = plan_toeplitz(plan) && coef_ok;
+  double b2 = 0.0;
+  if (sub) {
+    int pN = 0, pL = 0, pC = 0, pdev = 0, pM = 0;
+    plan_dims(plan, &pN, &pL, &pC, &pdev, &pM);
+    const size_t E = (size_t)sn_elems(plan), r = (size_t)h->r;
+    const size_t need = (r * r * E + 2 * r * pC * E + 2 * r * V) * sizeof(float2);
+    if (h->sn_bytes < need) {
+      for (float2** p : {&h->Ksn, &h->spa, &h->spb, &h->zs, &h->bv}) {
+        if (*p) cudaFree(*p);
+        *p = nullptr;
+      }
+      h->sn_bytes = 0;
+      if (cudaMalloc((void**)&h->Ksn, r * r * E * sizeof(float2)) != cudaSuccess ||
+          cudaMalloc((void**)&h->spa, r * pC * E * sizeof(float2)) != cudaSuccess ||
+          cudaMalloc((void**)&h->spb, r * pC * E * sizeof(float2)) != cudaSuccess ||
+          cudaMalloc((void**)&h->zs, r * V * sizeof(float2)) != cudaSuccess ||
+          cudaMalloc((void**)&h->bv, r * V * sizeof(float2)) != cudaSuccess)
+        return fail(MRF_ENOMEM, "mrf_msllr_solve: subspace workspace allocation failed");
+      h->sn_bytes = need;
+    }
+    MRF_TRY(sn_build(plan, h->basis_h.data(), h->r, h->Ksn, st));
+    const float2* rh = h->rhs;
+    MRF_TRY(coefs(h, rh, rh, rh, 0.f, h->bv, nullptr, st));   // P_S A^H b coefficients
+    const size_t ny = (size_t)pL * pC * pM;
+    if (!h->part && cudaMalloc((void**)&h->part, (size_t)kStatBlocks * sizeof(double)) != cudaSuccess)
+      return fail(MRF_ENOMEM, "mrf_msllr_solve: allocation failed");
+    MRF_TRY(dot_re(h, (const float2*)b, (const float2*)b, ny, st, &b2));   // ||b||^2
+  }
   bool have_coef = false;
   auto maps = [&](const void* cur) -> mrf_status {
     if (have_coef && coef_ok) return mrf_dict_match_coef(dict, h->xcr, V, index, pd, params, stream);
@@ -453,13 +552,18 @@ mrf_status mrf_msllr_solve(mrf_llr h, mrf_dict dict, mrf_plan plan, const void* 
   for (int n = 1; n <= prm->max_iter; ++n) {
     // Z^n, P^n, X^n (Eqs. 15, 20, 21), then cost(n)
     // from n = 2 on, A X^{n-1} is the previous cost's forward (h->yb): A^H A X^{n-1} = A^H (h->yb)
-    MRF_TRY(step_impl(h, plan, cur, h->rhs, prm->mu, lam1, prm->lambda2, prm->beta, nxt, nullptr, nullptr, stream,
-                      have_coef ? h->xcv : nullptr, have_coef ? h->yb : nullptr));
-    have_coef = true;   // k_llr_update wrote the coefficients of nxt
+    if (sub && have_coef) {
+      MRF_TRY(sub_step(h, prm->mu, lam1, prm->lambda2, prm->beta, st));
+    } else {
+      MRF_TRY(step_impl(h, plan, cur, h->rhs, prm->mu, lam1, prm->lambda2, prm->beta, nxt, nullptr, nullptr, stream,
+                        have_coef ? h->xcv : nullptr, have_coef ? h->yb : nullptr));
+      std::swap(cur, nxt);
+    }
+    have_coef = true;   // k_llr_update wrote the coefficients of X^n
     double c = 0.0;
-    MRF_TRY(cost_impl(h, plan, nxt, b, lam1, prm->lambda2, &c, nullptr, stream, h->xcv));
+    if (sub) MRF_TRY(sub_cost(h, plan, b2, lam1, prm->lambda2, &c, st));
+    else MRF_TRY(cost_impl(h, plan, cur, b, lam1, prm->lambda2, &c, nullptr, stream, h->xcv));
     if (info && info->cost) info->cost[n - 1] = c;
-    std::swap(cur, nxt);
     it = n;
     maps_current = false;
     // stop rule cost(n-1) / cost(n) - 1 < tol, from n = 2 (reading 27: cost(0) is not defined)
@@ -471,7 +575,18 @@ mrf_status mrf_msllr_solve(mrf_llr h, mrf_dict dict, mrf_plan plan, const void* 
     }
   }
   if (!maps_current) MRF_TRY(maps(cur));   // M^ = Phi_D(X^)
-  if (cur != x) CUDA_TRY(cudaMemcpyAsync(x, cur, xbytes, cudaMemcpyDeviceToDevice, st));
+  if (sub && it > 1) {   // X^ = Xc d into x (k_llr_update with gamma = 0 expands its Y)
+    const unsigned gv = (unsigned)((V + 31) / 32);
+    if (h->r <= 16)
+      llr::k_llr_update<16><<<gv, 256, 0, st>>>(h->xcv, h->P, h->corners, h->nc, h->N, h->p, h->r, h->dT, h->L, 0.f,
+                                                (float2*)x, nullptr, nullptr);
+    else
+      llr::k_llr_update<32><<<gv, 256, 0, st>>>(h->xcv, h->P, h->corners, h->nc, h->N, h->p, h->r, h->dT, h->L, 0.f,
+                                                (float2*)x, nullptr, nullptr);
+    MRF_TRY(check_launch("k_llr_update"));
+  } else if (cur != x) {
+    CUDA_TRY(cudaMemcpyAsync(x, cur, xbytes, cudaMemcpyDeviceToDevice, st));
+  }
   if (info) {
     info->iters = it;
     info->lambda1 = lam1;

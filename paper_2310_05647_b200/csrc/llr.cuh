@@ -306,7 +306,7 @@ __global__ void __launch_bounds__(256) k_llr_update(const float2* __restrict__ Y
   __syncthreads();
   if (xcr && v < V)
     for (int i = w; i < r; i += 8) xcr[(size_t)i * V + v] = xcs[i][lane];
-  if (v >= V) return;
+  if (v >= V || !xout) return;   // xout == nullptr: coefficients only (basis-coordinate loop)
   float2 xc[R];
 #pragma unroll
   for (int i = 0; i < R; ++i) xc[i] = xcs[i][lane];
@@ -333,6 +333,38 @@ static __global__ void __launch_bounds__(256) k_llr_resid(const float2* __restri
     const float2 u = __ldg(a + i), v = __ldg(b + i);
     const double dx = (double)u.x - (double)v.x, dy = (double)u.y - (double)v.y;
     s = fma(dx, dx, fma(dy, dy, s));
+  }
+  __shared__ double red[8];
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < 8; ++w) t += red[w];
+    part[blockIdx.x] = t;
+  }
+}
+
+// Y[v][i] = xcv[v][i] - mu (zs[i][v] - bv[v][i]): Eq. 15's gradient step in basis coordinates
+// (zs = P_S A^H A x, bv = P_S A^H b coefficients; thread per voxel, coefficient-major zs reads)
+static __global__ void __launch_bounds__(256) k_sn_grad(const float2* __restrict__ xcv, const float2* __restrict__ zs,
+                                                        const float2* __restrict__ bv, float mu, int r, int V,
+                                                        float2* __restrict__ Y) {
+  const int v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= V) return;
+  for (int i = 0; i < r; ++i) {
+    const float2 a = xcv[(size_t)v * r + i], z = __ldg(zs + (size_t)i * V + v), b = bv[(size_t)v * r + i];
+    Y[(size_t)v * r + i] = make_float2(a.x - mu * (z.x - b.x), a.y - mu * (z.y - b.y));
+  }
+}
+
+// part[block] = sum Re(conj(a) b) over a grid-stride slice (float64; fixed grid)
+static __global__ void __launch_bounds__(256) k_llr_dotre(const float2* __restrict__ a, const float2* __restrict__ b,
+                                                          size_t n, double* __restrict__ part) {
+  double s = 0.0;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    const float2 u = __ldg(a + i), w = __ldg(b + i);
+    s = fma((double)u.x, (double)w.x, fma((double)u.y, (double)w.y, s));
   }
   __shared__ double red[8];
   for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);

@@ -9,6 +9,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <complex>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -380,6 +381,8 @@ static mrf_status setup_kernels(mrf_plan_s* pl) {
   CUDA_TRY(cudaFuncSetAttribute(k_toep_cols<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)toep_cols_smem<G>()));
   CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pl->occ_tc, k_toep_cols<G>, ncol, toep_cols_smem<G>()));
   CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pl->occ_ac, adj_kernel, ncol, s_acol));
+  CUDA_TRY(cudaFuncSetAttribute(k_sn_fcols<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sn_cols_smem<G>()));
+  CUDA_TRY(cudaFuncSetAttribute(k_sn_icols<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sn_cols_smem<G>()));
   if (pl->occ_fr0 < 1 || pl->occ_fr1 < 1 || pl->occ_ar < 1 || pl->occ_fc < 1 || pl->occ_ac < 1)
     return fail(MRF_EUNSUPPORTED, "a kernel does not fit on an SM");
   if (const char* cap = std::getenv("MRF_OCC_CAP")) {   // experiment knob: resident CTAs per SM
@@ -839,6 +842,88 @@ void mrf::plan_dims(mrf_plan pl, int* N, int* L, int* C, int* device, int* M) {
   *L = pl->L;
   *C = pl->C;
   *device = pl->device;
+}
+
+// ---------------------------------------------------------------------------- subspace normal
+// (gridding.cuh k_sn_*; used by mrf_msllr_solve on Toeplitz plans, llr.cu)
+bool mrf::plan_toeplitz(mrf_plan pl) { return (pl->flags & MRF_NORMAL_TOEPLITZ) != 0 && pl->psf; }
+long long mrf::sn_elems(mrf_plan pl) { return (long long)pl->G * pl->G; }
+
+mrf_status mrf::sn_build(mrf_plan pl, const float2* basis_h, int r, float2* K, cudaStream_t st) {
+  if (!plan_toeplitz(pl)) return fail(MRF_EINVAL, "the subspace normal needs a plan with MRF_NORMAL_TOEPLITZ");
+  DeviceGuard guard(pl->device);
+  const int L = pl->L, R = pl->R;
+  std::vector<int> fil(L);
+  CUDA_TRY(cudaMemcpy(fil.data(), pl->fil, (size_t)L * sizeof(int), cudaMemcpyDeviceToHost));
+  // c^rho_ji = sum_{l in rho} conj(d_jl) d_il  (float64)
+  std::vector<std::complex<double>> cd((size_t)r * r * R, 0.0);
+  for (int l = 0; l < L; ++l) {
+    const int rho = fil[l];
+    for (int j = 0; j < r; ++j) {
+      const std::complex<double> dj(basis_h[(size_t)j * L + l].x, -basis_h[(size_t)j * L + l].y);
+      for (int i = 0; i < r; ++i) {
+        const std::complex<double> di(basis_h[(size_t)i * L + l].x, basis_h[(size_t)i * L + l].y);
+        cd[((size_t)j * r + i) * R + rho] += dj * di;
+      }
+    }
+  }
+  std::vector<float2> cc(cd.size());
+  for (size_t i = 0; i < cd.size(); ++i) cc[i] = make_float2((float)cd[i].real(), (float)cd[i].imag());
+  float2* ccd = nullptr;
+  CUDA_TRY(cudaMalloc((void**)&ccd, cc.size() * sizeof(float2)));
+  cudaError_t e = cudaMemcpyAsync(ccd, cc.data(), cc.size() * sizeof(float2), cudaMemcpyHostToDevice, st);
+  const long long E = sn_elems(pl), tot = (long long)r * r * E;
+  if (e == cudaSuccess) {
+    k_sn_kbuild<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(pl->psf, ccd, r * r, R, E, K);
+    e = cudaGetLastError();
+  }
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  cudaFree(ccd);
+  if (e != cudaSuccess) return fail(MRF_ECUDA, std::string("sn_build: ") + cudaGetErrorString(e));
+  return MRF_OK;
+}
+
+template <int G>
+static mrf_status run_sn(mrf_plan_s* pl, const float2* K, int r, const float2* U, float2* Z, float2* spec_a,
+                         float2* spec_b, cudaStream_t st) {
+  const int C = pl->C, ncol = cols_threads<G>();
+  const long long E = (long long)G * G;
+  float* dap = pl->dap;
+  pl->dap = pl->ones;   // Toeplitz form: no deapodisation (dp() copies it into the launches)
+  mrf_status rc = MRF_OK;
+  for (int l0 = 0; l0 < r && rc == MRF_OK; l0 += pl->bf) {   // r frames: row FFTs, column FFTs -> spectra
+    const int nb = std::min(pl->bf, r - l0);
+    rc = launch_fwd_rows<G>(pl, U, pl->Hs[0], l0, nb, st);
+    if (rc == MRF_OK) {
+      const int items = nb * C * pl->S;
+      k_sn_fcols<G><<<std::min(items, pl->nsm * 2), ncol, sn_cols_smem<G>(), st>>>(pl->tw, pl->Hs[0],
+                                                                                   spec_a + (size_t)l0 * C * E, nb * C);
+      if (cudaGetLastError() != cudaSuccess) rc = fail(MRF_ECUDA, "k_sn_fcols launch failed");
+    }
+  }
+  if (rc == MRF_OK) {
+    const long long n = (long long)C * E;
+    if (r <= 16) k_sn_mix<16><<<(unsigned)((n + 255) / 256), 256, 0, st>>>(spec_a, K, spec_b, r, C, E);
+    else k_sn_mix<32><<<(unsigned)((n + 255) / 256), 256, 0, st>>>(spec_a, K, spec_b, r, C, E);
+    if (cudaGetLastError() != cudaSuccess) rc = fail(MRF_ECUDA, "k_sn_mix launch failed");
+  }
+  for (int l0 = 0; l0 < r && rc == MRF_OK; l0 += pl->bf) {   // inverse column FFTs, row iFFTs + crop
+    const int nb = std::min(pl->bf, r - l0);
+    const int items = nb * C * pl->S;
+    k_sn_icols<G><<<std::min(items, pl->nsm * 2), ncol, sn_cols_smem<G>(), st>>>(pl->tw, spec_b + (size_t)l0 * C * E,
+                                                                                 pl->Has[0], nb * C);
+    if (cudaGetLastError() != cudaSuccess) rc = fail(MRF_ECUDA, "k_sn_icols launch failed");
+    if (rc == MRF_OK) rc = launch_adj_rows<G>(pl, pl->Has[0], Z, nullptr, 0.f, l0, nb, nullptr, st);
+  }
+  pl->dap = dap;
+  return rc;
+}
+
+mrf_status mrf::sn_apply(mrf_plan pl, const float2* K, int r, const float2* U, float2* Z, float2* spec_a,
+                         float2* spec_b, cudaStream_t st) {
+  if (!plan_toeplitz(pl)) return fail(MRF_EINVAL, "the subspace normal needs a plan with MRF_NORMAL_TOEPLITZ");
+  DeviceGuard guard(pl->device);
+  DISPATCH_G(pl, run_sn, pl, K, r, U, Z, spec_a, spec_b, st);
 }
 
 // ================================================================================== C-ABI

@@ -15,6 +15,14 @@ void plan_dims(mrf_plan plan, int* N, int* L, int* C, int* device, int* M = null
 // 2D tiled TMA map over a row-major [rows][cols] array (row pitch row_bytes, a multiple of 16):
 // (box_cols x box_rows) boxes, 128-byte swizzle (box_cols x element size = 128), out-of-bounds
 // elements read as zero.  dict.cu.
+// subspace normal operator on Toeplitz plans (mrfnufft.cu): K = [r][r][G*G] complex mixing
+// kernels from the basis rows (host [r][L]); apply: Z = P_S A^H A (U d) in coefficients, U and Z
+// DEVICE [r][N][N], spectra workspaces [r][C][G*G] each.
+bool plan_toeplitz(mrf_plan plan);
+long long sn_elems(mrf_plan plan);
+mrf_status sn_build(mrf_plan plan, const float2* basis_h, int r, float2* K, cudaStream_t st);
+mrf_status sn_apply(mrf_plan plan, const float2* K, int r, const float2* U, float2* Z, float2* spec_a, float2* spec_b,
+                    cudaStream_t st);
 mrf_status tmap_2d(CUtensorMap* m, CUtensorMapDataType type, const void* base, uint64_t cols, uint64_t rows,
                    uint64_t row_bytes, uint32_t box_cols, uint32_t box_rows);
 }  // namespace mrf

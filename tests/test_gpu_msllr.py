@@ -152,3 +152,27 @@ def test_stop_rule(binding, problem):
         op2 = binding.LLR(dnl, N, P, S)
         op2.solve(dnl, pl, b, mu=pr["mu"], lam1=1e-3, max_iter=1)
     pl.close(), op.close(), dic.close()
+
+
+@pytest.mark.parametrize("lam1,iters,which", [(0.0, 4, "problem"), (2e-3, 2, "problem1")])
+def test_basis_coordinate_loop_on_a_toeplitz_plan(binding, request, lam1, iters, which):
+    """On a MRF_NORMAL_TOEPLITZ plan mrf_msllr_solve runs iterations n >= 2 in basis coordinates
+    (subspace normal P_S A^H A from the PSF spectra, the cost by the inner-product identity): the
+    operator is the exact NUDFT normal, so the oracle runs its loop with op="nudft"."""
+    pr = request.getfixturevalue(which)
+    lam2, beta = 0.05, 0.5
+    ref = oms.solve(pr["b"], pr["traj"], pr["D"], pr["lut"], pr["d"], pr["mu"], lam1, lam2, beta, iters, tol=0.0,
+                    W=W, N=N, p=P, s=S, op="nudft")
+    dic = binding.Dictionary(pr["D"], pr["lut"])
+    dic.basis(0.9999, 32)
+    op = binding.LLR(dic, N, P, S)
+    pl = binding.Plan(N, pr["traj"], L, W=W, normal="toeplitz")
+    b = torch.from_numpy(pr["b"].astype(np.complex64)).cuda()
+    out = op.solve(dic, pl, b, mu=pr["mu"], lam1=lam1, lam2=lam2, beta=beta, max_iter=iters, tol=0.0)
+    torch.cuda.synchronize()
+    assert out["iters"] == iters
+    assert _rel(out["x"].cpu().numpy(), ref["x"]) <= 1e-4
+    assert np.allclose(out["cost"], ref["cost"], rtol=1e-4, atol=0)
+    if lam1:
+        assert abs(out["lambda1"] - ref["lambda1"]) <= 1e-4 * ref["lambda1"]
+    pl.close(), op.close(), dic.close()

@@ -64,20 +64,25 @@ torch.cuda.synchronize()
 print(f"cost: {1e3 * (time.perf_counter() - t0) / 5:.3f} ms (terms {terms})")
 
 
-def solve_ms(n, lam1):
+plt = binding.Plan(cfg.N, traj, cfg.L, W=cfg.W, normal="toeplitz")
+
+
+def solve_ms(n, lam1, plan=None):
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    out = op2.solve(dic2, pl, b, mu=0.018, lam1=lam1, lam2=0.05, beta=0.5, max_iter=n, tol=0.0)
+    out = op2.solve(dic2, plan or pl, b, mu=0.018, lam1=lam1, lam2=0.05, beta=0.5, max_iter=n, tol=0.0)
     torch.cuda.synchronize()
     return time.perf_counter() - t0, out
 
 
 solve_ms(1, 1e-3)
-for lam1 in (0.0, 1e-7):
-    per = []
-    for _ in range(2):
-        t1, _ = solve_ms(1, lam1)
-        t11, out = solve_ms(11, lam1)
-        per.append((t11 - t1) / 10)
-    print(f"msllr solve lambda1_0={lam1}: {1e3 * min(per):.2f} ms per Algorithm-1 iteration "
-          f"(T(1) = {1e3 * t1:.1f} ms, cost {['%.4g' % c for c in out['cost'][:4]]} ...)")
+solve_ms(2, 1e-3, plt)
+for plan, name in ((pl, "gridding plan"), (plt, "toeplitz plan (basis coordinates)")):
+    for lam1 in (0.0, 1e-7):
+        per = []
+        for _ in range(2):
+            t1, _ = solve_ms(1, lam1, plan)
+            t11, out = solve_ms(11, lam1, plan)
+            per.append((t11 - t1) / 10)
+        print(f"msllr solve {name} lambda1_0={lam1}: {1e3 * min(per):.2f} ms per Algorithm-1 iteration "
+              f"(T(1) = {1e3 * t1:.1f} ms, cost {['%.4g' % c for c in out['cost'][:4]]} ...)")
