@@ -268,6 +268,12 @@ mrf_status mrf_llr_cost(mrf_llr llr, mrf_plan plan, const void* x, const void* b
  *                           stop if n >= 2 and cost(n-1)/cost(n) - 1 < tol     (reading 27)
  *                           M^{n+1} = Phi_D(X^n);  L^{n+1};  lambda_1 = lambda1 max(L^{n+1})
  *   outputs X^ (in x) and M^ = Phi_D(X^) (index, pd, params).
+ * On a plan created with MRF_NORMAL_TOEPLITZ the iterations n >= 2 run in basis coordinates: x = u d
+ * with u [V][r], P_S A^H A x from the plan's PSF spectra (r forward / inverse 2D FFT pairs and an
+ * r x r mixing per frequency, K_ji = sum_rho c^rho_ji T_rho, c^rho_ji = sum_{l in rho} conj(d_jl) d_il),
+ * the data term by 1/2 ||A x - b||^2 = 1/2 <u, P_S A^H A x> - Re <u, P_S A^H b> + 1/2 ||b||^2, and
+ * Phi_D on the coefficients; the operator is then the exact (NUDFT) normal of the Toeplitz plan
+ * (A^H b stays the gridding adjoint), and x is expanded to the L frames once at the end.
  * lambda1 = 0 is the LLR-only reconstruction (no maps inside the loop).  lambda1 > 0 needs a
  * dictionary LUT of (T1, T2) (P = 2) and params.  b: DEVICE [L][C][M]; x: DEVICE [L][N][N] (out);
  * index int32 [V], pd float [V], params float [V][P] (nullable when lambda1 = 0): DEVICE.
