@@ -140,12 +140,12 @@ k_dict_gemm(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUt
       float bsc = -1.f;
       int bk = 0;
 #pragma unroll 1
-      for (int ch = 0; ch < BN / 32; ++ch) {
-        float v[32];
-        tmem_ld32(tmem + lane_addr + (uint32_t)(acc * BN + ch * 32), v);
-        const int k0 = nt * (BN / 2) + ch * 16;
+      for (int ch = 0; ch < BN / 128; ++ch) {   // 128 columns (64 atoms) per TMEM load and wait
+        float v[128];
+        tmem_ld128(tmem + lane_addr + (uint32_t)(acc * BN + ch * 128), v);
+        const int k0 = nt * (BN / 2) + ch * 64;
 #pragma unroll
-        for (int q = 0; q < 16; ++q) {
+        for (int q = 0; q < 64; ++q) {
           const float sc = (v[2 * q] * v[2 * q] + v[2 * q + 1] * v[2 * q + 1]) * __ldg(w2 + k0 + q);
           if (sc > bsc) {   // strict: equal scores keep the lowest atom index
             bsc = sc;
