@@ -18,6 +18,8 @@
 
 using namespace mrf;
 
+static constexpr int kStatBlocks = 4 * 148;   // blocks of the grid-stride reductions
+
 struct mrf_llr_s {
   int N = 0, L = 0, p = 0, s = 0, r = 0, nc = 0, device = 0;
   float2* dT = nullptr;       // [L][R] transposed basis, rows zero-padded to R = 16 or 32
@@ -29,7 +31,9 @@ struct mrf_llr_s {
   std::vector<double> nuc_h;
   float2* yb = nullptr;       // [L][C][M] A x of mrf_llr_cost
   size_t ny = 0;
-  double* part = nullptr;     // [kStatBlocks] partial sums
+  double* part = nullptr;     // [4][kStatBlocks] partial sums
+  double* hsum = nullptr;     // pinned host staging of deferred sums (Sums)
+  size_t hsum_cap = 0;
   float2 *rhs = nullptr, *x2 = nullptr;   // mrf_msllr_solve: A^H b and the second iterate buffer
   float2 *xcv = nullptr, *xcr = nullptr;  // coefficients of the last x_out: [V][r] and [r][V]
   unsigned basis_gen = 0;                 // the dictionary's basis generation at creation
@@ -46,7 +50,9 @@ struct mrf_llr_s {
   float* W = nullptr;         // [n][n] similarity weights (Eq. 8), first the squared distances
   float* deg = nullptr;       // [n] degrees D_ii
   float* pv = nullptr;        // [n][3 p^2] standardised patch vectors of the maps
-  unsigned* hist = nullptr;   // [65536] radix-select histogram (+1 word: max PD bits)
+  unsigned* hist = nullptr;   // [2][2048] radix-select histograms (+1 word: max PD bits)
+  mfd::LapSel* sel = nullptr;   // device state of the Laplacian build
+  mfd::LapSel* sel_h = nullptr; // pinned host copy
   double* stats = nullptr;    // [blocks][7] foreground sums, then [6] mean/std
   float2* YX = nullptr;       // [V][r] coefficients of x
   float2* Qm = nullptr;       // [n][p^2 r] patch blocks of YX
@@ -62,7 +68,9 @@ struct mrf_llr_s {
 static void llr_free(mrf_llr_s* h) {
   if (!h) return;
   cudaSetDevice(h->device);
-  for (void* v : {(void*)h->dT, (void*)h->corners, (void*)h->Y, (void*)h->P, (void*)h->nx, (void*)h->nuc, (void*)h->W,
+  if (h->sel_h) cudaFreeHost(h->sel_h);
+  if (h->hsum) cudaFreeHost(h->hsum);
+  for (void* v : {(void*)h->sel, (void*)h->dT, (void*)h->corners, (void*)h->Y, (void*)h->P, (void*)h->nx, (void*)h->nuc, (void*)h->W,
                   (void*)h->deg, (void*)h->pv, (void*)h->hist, (void*)h->stats, (void*)h->YX, (void*)h->Qm,
                   (void*)h->Gm, (void*)h->pen, (void*)h->Wh, (void*)h->Wl, (void*)h->Qh, (void*)h->Ql, (void*)h->yb, (void*)h->part, (void*)h->rhs, (void*)h->x2, (void*)h->xcv, (void*)h->xcr, (void*)h->Ksn,
                   (void*)h->spa, (void*)h->spb, (void*)h->zs, (void*)h->bv, (void*)h->wc_step, (void*)h->wc_cost})
@@ -140,6 +148,33 @@ static mrf_status host_sum(const double* dev, int n, cudaStream_t st, double* ou
   return MRF_OK;
 }
 
+// Deferred float64 sums: the partial arrays are copied into a pinned host buffer and summed in a
+// fixed order after ONE stream synchronisation for all of them.
+struct Sums {
+  mrf_llr_s* h;
+  cudaStream_t st;
+  size_t used = 0;
+  std::vector<std::pair<size_t, int>> seg;
+  std::vector<double*> out;
+  mrf_status add(const double* dev, int n, double* dst) {
+    if (used + (size_t)n > h->hsum_cap) return fail(MRF_EINVAL, "internal: sum staging overflow");
+    CUDA_TRY(cudaMemcpyAsync(h->hsum + used, dev, (size_t)n * sizeof(double), cudaMemcpyDeviceToHost, st));
+    seg.emplace_back(used, n);
+    out.push_back(dst);
+    used += (size_t)n;
+    return MRF_OK;
+  }
+  mrf_status finish() {
+    CUDA_TRY(cudaStreamSynchronize(st));
+    for (size_t i = 0; i < seg.size(); ++i) {
+      double t = 0.0;
+      for (int k = 0; k < seg[i].second; ++k) t += h->hsum[seg[i].first + k];
+      *out[i] = t;
+    }
+    return MRF_OK;
+  }
+};
+
 static mrf_status check_plan(mrf_llr_s* h, mrf_plan plan, const char* who) {
   int pN = 0, pL = 0, pC = 0, pdev = 0;
   plan_dims(plan, &pN, &pL, &pC, &pdev);
@@ -174,7 +209,10 @@ mrf_status mrf_llr_create(mrf_dict dict, int N, int p, int s, mrf_llr* out) {
             cudaMalloc((void**)&h->xcv, V * h->r * sizeof(float2)) == cudaSuccess &&
             cudaMalloc((void**)&h->xcr, V * h->r * sizeof(float2)) == cudaSuccess &&
             cudaMalloc((void**)&h->wc_step, nq * h->r * h->r * sizeof(double2)) == cudaSuccess &&
-            cudaMalloc((void**)&h->wc_cost, nq * h->r * h->r * sizeof(double2)) == cudaSuccess;
+            cudaMalloc((void**)&h->wc_cost, nq * h->r * h->r * sizeof(double2)) == cudaSuccess &&
+            cudaMalloc((void**)&h->part, 4 * (size_t)kStatBlocks * sizeof(double)) == cudaSuccess &&
+            cudaMallocHost((void**)&h->hsum, (4 * (size_t)kStatBlocks + 4 * nq) * sizeof(double)) == cudaSuccess;
+  h->hsum_cap = 4 * (size_t)kStatBlocks + 4 * nq;
   h->basis_gen = dict->basis_gen;
   h->basis_h = dict->basis_h;
   if (!ok) {
@@ -199,7 +237,6 @@ mrf_status mrf_llr_create(mrf_dict dict, int N, int p, int s, mrf_llr* out) {
   return MRF_OK;
 }
 
-static constexpr int kStatBlocks = 4 * 148;
 
 mrf_status mrf_llr_laplacian(mrf_llr h, const float* params, const float* pd, double sigma2, double* sigma2_out,
                              double* max_degree, void* stream) {
@@ -211,7 +248,9 @@ mrf_status mrf_llr_laplacian(mrf_llr h, const float* params, const float* pd, do
     bool ok = cudaMalloc((void**)&h->W, (size_t)n * n * sizeof(float)) == cudaSuccess &&
               cudaMalloc((void**)&h->deg, (size_t)n * sizeof(float)) == cudaSuccess &&
               cudaMalloc((void**)&h->pv, (size_t)n * 3 * np * sizeof(float)) == cudaSuccess &&
-              cudaMalloc((void**)&h->hist, (65536 + 1) * sizeof(unsigned)) == cudaSuccess &&
+              cudaMalloc((void**)&h->hist, (3 * 2048 + 1) * sizeof(unsigned)) == cudaSuccess &&
+              cudaMalloc((void**)&h->sel, sizeof(mfd::LapSel)) == cudaSuccess &&
+              cudaMallocHost((void**)&h->sel_h, sizeof(mfd::LapSel)) == cudaSuccess &&
               cudaMalloc((void**)&h->stats, (size_t)kStatBlocks * 7 * sizeof(double)) == cudaSuccess;
     h->nK = (n + 3) / 4 * 4;   // 16-byte TMA row pitch
     ok = ok && cudaMalloc((void**)&h->Wh, (size_t)n * h->nK * sizeof(float)) == cudaSuccess &&
@@ -220,81 +259,56 @@ mrf_status mrf_llr_laplacian(mrf_llr h, const float* params, const float* pd, do
     MRF_TRY(tmap_2d(&h->tWh, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, h->Wh, n, n, (uint64_t)h->nK * 4, g3::BK, g3::BM));
     MRF_TRY(tmap_2d(&h->tWl, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, h->Wl, n, n, (uint64_t)h->nK * 4, g3::BK, g3::BM));
   }
+  // Everything stays on the device until the final copy of the LapSel state (one synchronisation):
   // foreground statistics of (T1, T2, PD) over PD > 0.1 max PD (reading 26)
-  unsigned* pdmax = h->hist + 65536;
+  unsigned* pdmax = h->hist + 3 * 2048;
+  mfd::LapSel* sel = h->sel;
   CUDA_TRY(cudaMemsetAsync(pdmax, 0, sizeof(unsigned), st));
   mfd::k_mfd_max<<<kStatBlocks, 256, 0, st>>>(pd, V, pdmax);
   mfd::k_mfd_stats<<<kStatBlocks, 256, 0, st>>>(params, pd, V, pdmax, h->stats);
+  mfd::k_mfd_stats_final<<<1, 32, 0, st>>>(h->stats, kStatBlocks, sel);
   MRF_TRY(check_launch("k_mfd_stats"));
-  std::vector<double> part((size_t)kStatBlocks * 7);
-  CUDA_TRY(cudaMemcpyAsync(part.data(), h->stats, part.size() * sizeof(double), cudaMemcpyDeviceToHost, st));
-  CUDA_TRY(cudaStreamSynchronize(st));
-  double a[7] = {0, 0, 0, 0, 0, 0, 0};
-  for (int b = 0; b < kStatBlocks; ++b)
-    for (int i = 0; i < 7; ++i) a[i] += part[(size_t)b * 7 + i];
-  if (!(a[6] > 0.0)) return fail(MRF_EINVAL, "mrf_llr_laplacian: no foreground voxel");
-  double ms[6];
-  for (int c = 0; c < 3; ++c) {
-    const double mean = a[2 * c] / a[6], var = std::max(a[2 * c + 1] / a[6] - mean * mean, 0.0);
-    ms[2 * c] = mean;
-    ms[2 * c + 1] = var > 0.0 ? std::sqrt(var) : 1.0;
-  }
-  CUDA_TRY(cudaMemcpyAsync(h->stats, ms, sizeof(ms), cudaMemcpyHostToDevice, st));
-  mfd::k_mfd_patchvec<<<n, 128, 0, st>>>(params, pd, h->stats, h->corners, h->nc, h->N, h->p, h->pv);
+  mfd::k_mfd_patchvec<<<n, 128, 0, st>>>(params, pd, sel, h->corners, h->nc, h->N, h->p, h->pv);
   const dim3 gd((unsigned)((n + 63) / 64), (unsigned)((n + 63) / 64));
   mfd::k_mfd_dist<<<gd, 256, 0, st>>>(h->pv, n, 3 * np, h->W);
   MRF_TRY(check_launch("k_mfd_dist"));
-  if (!(sigma2 > 0.0)) {   // sigma^2 = median of the nonzero upper-triangle distances (exact radix select)
-    // the k-th smallest nonzero value bit pattern by three histogram passes (11 + 11 + 10 bits);
-    // positive floats order as their bits
-    std::vector<unsigned> hh(2048);
-    auto pass = [&](int ps, unsigned pre) -> mrf_status {
-      CUDA_TRY(cudaMemsetAsync(h->hist, 0, 2048 * sizeof(unsigned), st));
-      mfd::k_mfd_hist<<<2 * 148, 256, 0, st>>>(h->W, n, ps, pre, h->hist);
-      MRF_TRY(check_launch("k_mfd_hist"));
-      CUDA_TRY(cudaMemcpyAsync(hh.data(), h->hist, 2048 * sizeof(unsigned), cudaMemcpyDeviceToHost, st));
-      CUDA_TRY(cudaStreamSynchronize(st));
-      return MRF_OK;
-    };
-    MRF_TRY(pass(0, 0u));
-    const std::vector<unsigned> h0 = hh;
-    unsigned long long m = 0;
-    for (unsigned c : h0) m += c;
-    if (m == 0) {
-      sigma2 = 1.0;
-    } else {
-      const unsigned long long ks[2] = {(m - 1) / 2, m / 2};   // numpy's median: mean of the two middle
-      float vals[2];
-      for (int t = 0; t < 2; ++t) {
-        if (t == 1 && ks[1] == ks[0]) {
-          vals[1] = vals[0];
-          break;
-        }
-        unsigned long long c = 0;
-        unsigned b0 = 0;
-        while (c + h0[b0] <= ks[t]) c += h0[b0++];
-        MRF_TRY(pass(1, b0));
-        unsigned b1 = 0;
-        while (c + hh[b1] <= ks[t]) c += hh[b1++];
-        MRF_TRY(pass(2, (b0 << 11) | b1));
-        unsigned b2 = 0;
-        while (c + hh[b2] <= ks[t]) c += hh[b2++];
-        const unsigned bits = (b0 << 21) | (b1 << 10) | b2;
-        std::memcpy(&vals[t], &bits, 4);
-      }
-      sigma2 = 0.5 * ((double)vals[0] + (double)vals[1]);
+  // sigma^2: given, or the median of the nonzero upper-triangle distances by an exact radix select
+  // (11 + 11 + 10 bits; positive floats order as their bits), the bookkeeping on the device
+  const unsigned given = sigma2 > 0.0 ? 1u : 0u;
+  CUDA_TRY(cudaMemcpyAsync(&sel->given, &given, sizeof(unsigned), cudaMemcpyHostToDevice, st));
+  if (given) {
+    CUDA_TRY(cudaMemcpyAsync(&sel->sigma2, &sigma2, sizeof(double), cudaMemcpyHostToDevice, st));
+  } else {
+    unsigned* h0 = h->hist;
+    unsigned* h1 = h->hist + 2048;
+    const unsigned hb = 2 * 148;
+    CUDA_TRY(cudaMemsetAsync(h0, 0, 2048 * sizeof(unsigned), st));
+    mfd::k_mfd_hist<<<hb, 256, 0, st>>>(h->W, n, 0, nullptr, h0);
+    mfd::k_mfd_select<<<1, 256, 0, st>>>(0, h0, h0, sel);
+    for (int ps = 1; ps <= 2; ++ps) {
+      CUDA_TRY(cudaMemsetAsync(h0, 0, 2 * 2048 * sizeof(unsigned), st));
+      mfd::k_mfd_hist<<<hb, 256, 0, st>>>(h->W, n, ps, &sel->pre[0], h0);
+      mfd::k_mfd_hist<<<hb, 256, 0, st>>>(h->W, n, ps, &sel->pre[1], h1);
+      mfd::k_mfd_select<<<1, 256, 0, st>>>(ps, h0, h1, sel);
     }
+    MRF_TRY(check_launch("k_mfd_select"));
   }
-  mfd::k_mfd_weights<<<n, 256, 0, st>>>(h->W, n, (float)(1.0 / sigma2), h->deg);
+  mfd::k_mfd_weights<<<n, 256, 0, st>>>(h->W, n, &sel->sigma2, h->deg);
   MRF_TRY(check_launch("k_mfd_weights"));
+  mfd::k_mfd_degmax<<<(unsigned)std::min((n + 255) / 256, 148), 256, 0, st>>>(h->deg, n, sel);
+  MRF_TRY(check_launch("k_mfd_degmax"));
   const dim3 gs((unsigned)((n + 31) / 32), (unsigned)((n + 31) / 32));
   g3::k_g3_split<false><<<gs, 256, 0, st>>>(h->W, n, n, n, h->Wh, h->Wl, h->nK);
   MRF_TRY(check_launch("k_g3_split"));
-  std::vector<float> dg(n);
-  CUDA_TRY(cudaMemcpyAsync(dg.data(), h->deg, (size_t)n * sizeof(float), cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaMemcpyAsync(h->sel_h, sel, sizeof(mfd::LapSel), cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaStreamSynchronize(st));
-  if (sigma2_out) *sigma2_out = sigma2;
-  if (max_degree) *max_degree = *std::max_element(dg.begin(), dg.end());
+  if (!(h->sel_h->count > 0.0)) return fail(MRF_EINVAL, "mrf_llr_laplacian: no foreground voxel");
+  if (sigma2_out) *sigma2_out = h->sel_h->sigma2;
+  if (max_degree) {
+    float md;
+    std::memcpy(&md, &h->sel_h->maxdeg, 4);
+    *max_degree = md;
+  }
   h->has_lap = true;
   return MRF_OK;
 }
@@ -353,8 +367,12 @@ static mrf_status step_impl(mrf_llr h, mrf_plan plan, const void* x, const void*
                                               (float2*)x_out, h->xcv, h->xcr);
   MRF_TRY(check_launch("k_llr_update"));
   // Tr(Q(P_S x) L Q(P_S x)^H) and sum_q ||Q_q(Z)||_*: patches summed in a fixed order (synchronise)
-  if (penalty) MRF_TRY(host_sum(h->pen, nq, st, penalty));
-  if (nuclear) MRF_TRY(host_sum(h->nuc, nq, st, nuclear));
+  if (penalty || nuclear) {
+    Sums sums{h, st};
+    if (penalty) MRF_TRY(sums.add(h->pen, nq, penalty));
+    if (nuclear) MRF_TRY(sums.add(h->nuc, nq, nuclear));
+    MRF_TRY(sums.finish());
+  }
   return MRF_OK;
 }
 
@@ -377,15 +395,13 @@ static mrf_status cost_impl(mrf_llr h, mrf_plan plan, const void* x, const void*
     if (cudaMalloc((void**)&h->yb, ny * sizeof(float2)) != cudaSuccess) return fail(MRF_ENOMEM, "mrf_llr_cost: allocation failed");
     h->ny = ny;
   }
-  if (!h->part && cudaMalloc((void**)&h->part, (size_t)kStatBlocks * sizeof(double)) != cudaSuccess)
-    return fail(MRF_ENOMEM, "mrf_llr_cost: allocation failed");
   // 1/2 ||A x - b||^2
   MRF_TRY(mrf_forward(plan, x, h->yb, stream));
   llr::k_llr_resid<<<kStatBlocks, 256, 0, st>>>(h->yb, (const float2*)b, ny, h->part);
   MRF_TRY(check_launch("k_llr_resid"));
   double t[3] = {0.0, 0.0, 0.0};
-  MRF_TRY(host_sum(h->part, kStatBlocks, st, &t[0]));
-  t[0] *= 0.5;
+  Sums sums{h, st};
+  MRF_TRY(sums.add(h->part, kStatBlocks, &t[0]));
   // coefficients of P_S x (k_llr_coef with mu = 0 reads x three times: x - 0 (x - x) = x), unless known
   const float2* xf = (const float2*)x;
   if (!xcoef) MRF_TRY(coefs(h, xf, xf, xf, 0.f, h->Y, nullptr, st));
@@ -396,11 +412,13 @@ static mrf_status cost_impl(mrf_llr h, mrf_plan plan, const void* x, const void*
     MRF_TRY(manifold_G(h, cf, st));
     mfd::k_mfd_penalty<<<nq, 256, 0, st>>>(h->Qm, h->Gm, h->deg, h->p * h->p * h->r, h->pen);
     MRF_TRY(check_launch("k_mfd_penalty"));
-    MRF_TRY(host_sum(h->pen, nq, st, &t[1]));
+    MRF_TRY(sums.add(h->pen, nq, &t[1]));
   }
   // sum_q ||Q_q(P_S x)||_* (threshold +inf: only the singular values, no thresholded blocks)
   MRF_TRY(svt(h, cf, INFINITY, st));
-  MRF_TRY(host_sum(h->nuc, nq, st, &t[2]));
+  MRF_TRY(sums.add(h->nuc, nq, &t[2]));
+  MRF_TRY(sums.finish());
+  t[0] *= 0.5;
   if (terms)
     for (int i = 0; i < 3; ++i) terms[i] = t[i];
   if (cost) *cost = t[0] + (double)lambda1 * t[1] + (double)lambda2 * t[2];
@@ -452,18 +470,23 @@ static mrf_status sub_cost(mrf_llr_s* h, mrf_plan plan, double b2, float lambda1
   const size_t n = (size_t)h->N * h->N * h->r;
   MRF_TRY(sn_apply(plan, h->Ksn, h->r, h->xcr, h->zs, h->spa, h->spb, st));
   double uz = 0.0, ub = 0.0, tr = 0.0, nuc = 0.0;
-  MRF_TRY(dot_re(h, h->xcr, h->zs, n, st, &uz));
-  MRF_TRY(dot_re(h, h->xcv, h->bv, n, st, &ub));
+  Sums sums{h, st};
+  llr::k_llr_dotre<<<kStatBlocks, 256, 0, st>>>(h->xcr, h->zs, n, h->part);
+  llr::k_llr_dotre<<<kStatBlocks, 256, 0, st>>>(h->xcv, h->bv, n, h->part + kStatBlocks);
+  MRF_TRY(check_launch("k_llr_dotre"));
+  MRF_TRY(sums.add(h->part, kStatBlocks, &uz));
+  MRF_TRY(sums.add(h->part + kStatBlocks, kStatBlocks, &ub));
   const int nq = h->nc * h->nc;
   if (h->has_lap && lambda1 > 0.f) {
     MRF_TRY(manifold_ws(h));
     MRF_TRY(manifold_G(h, h->xcv, st));
     mfd::k_mfd_penalty<<<nq, 256, 0, st>>>(h->Qm, h->Gm, h->deg, h->p * h->p * h->r, h->pen);
     MRF_TRY(check_launch("k_mfd_penalty"));
-    MRF_TRY(host_sum(h->pen, nq, st, &tr));
+    MRF_TRY(sums.add(h->pen, nq, &tr));
   }
   MRF_TRY(svt(h, h->xcv, INFINITY, st));
-  MRF_TRY(host_sum(h->nuc, nq, st, &nuc));
+  MRF_TRY(sums.add(h->nuc, nq, &nuc));
+  MRF_TRY(sums.finish());
   *cost = (0.5 * uz - ub + 0.5 * b2) + (double)lambda1 * tr + (double)lambda2 * nuc;
   return MRF_OK;
 }
@@ -534,8 +557,6 @@ mrf_status mrf_msllr_solve(mrf_llr h, mrf_dict dict, mrf_plan plan, const void* 
     const float2* rh = h->rhs;
     MRF_TRY(coefs(h, rh, rh, rh, 0.f, h->bv, nullptr, st));   // P_S A^H b coefficients
     const size_t ny = (size_t)pL * pC * pM;
-    if (!h->part && cudaMalloc((void**)&h->part, (size_t)kStatBlocks * sizeof(double)) != cudaSuccess)
-      return fail(MRF_ENOMEM, "mrf_msllr_solve: allocation failed");
     MRF_TRY(dot_re(h, (const float2*)b, (const float2*)b, ny, st, &b2));   // ||b||^2
   }
   bool have_coef = false;

@@ -486,11 +486,119 @@ static __global__ void __launch_bounds__(256) k_mfd_stats(const float* __restric
   }
 }
 
+// Device-resident state of the Laplacian build (no host round trip until the end)
+struct LapSel {
+  double ms[6];                  // foreground mean / std of T1, T2, PD
+  double count;                  // foreground voxels
+  double sigma2;                 // bandwidth (median or given)
+  unsigned long long m, k[2], c[2];
+  unsigned pre[2];               // radix-select prefixes of the two middle order statistics
+  unsigned maxdeg;               // float bits of max_i D_ii
+  unsigned given;                // sigma2 given by the caller
+};
+
+// ms from the per-block partials of k_mfd_stats, summed in block order (one thread per sum)
+static __global__ void k_mfd_stats_final(const double* __restrict__ part, int nblk, LapSel* __restrict__ sel) {
+  __shared__ double a[7];
+  if (threadIdx.x < 7) {
+    double t = 0.0;
+    for (int b = 0; b < nblk; ++b) t += part[(size_t)b * 7 + threadIdx.x];
+    a[threadIdx.x] = t;
+  }
+  __syncthreads();
+  if (threadIdx.x < 3) {
+    const int c = threadIdx.x;
+    const double cnt = a[6] > 0.0 ? a[6] : 1.0;
+    const double mean = a[2 * c] / cnt, var = fmax(a[2 * c + 1] / cnt - mean * mean, 0.0);
+    sel->ms[2 * c] = mean;
+    sel->ms[2 * c + 1] = var > 0.0 ? sqrt(var) : 1.0;
+  }
+  if (threadIdx.x == 0) {
+    sel->count = a[6];
+    sel->maxdeg = 0u;
+  }
+}
+
+// Radix-select bookkeeping after histogram pass `pass` (one block of 256 threads, 8 bins each,
+// a block-wide exclusive scan of the bin counts): pass 0 sets the ranks of the two middle values
+// (numpy's median) and the 11-bit prefixes; passes 1, 2 extend them; after pass 2 sigma2 = the
+// mean of the two middle values (1 if there is none).
+__device__ __forceinline__ void sel_find(const unsigned* __restrict__ h, unsigned long long base,
+                                         unsigned long long k, unsigned long long* c_out, unsigned* b_out,
+                                         unsigned long long* scan) {
+  // scan[256]: shared; returns (through the owning thread) the bin b with base + cum(<b) <= k < base + cum(<=b)
+  const int t = threadIdx.x;
+  unsigned long long loc = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) loc += h[t * 8 + i];
+  scan[t] = loc;
+  __syncthreads();
+  for (int off = 1; off < 256; off <<= 1) {   // inclusive Hillis-Steele scan
+    const unsigned long long v = t >= off ? scan[t - off] : 0ull;
+    __syncthreads();
+    scan[t] += v;
+    __syncthreads();
+  }
+  unsigned long long c = base + scan[t] - loc;   // exclusive prefix of this thread's first bin
+  if (c <= k && k < c + loc) {
+    unsigned b = t * 8;
+    while (c + h[b] <= k) c += h[b++];
+    *c_out = c;
+    *b_out = b;
+  }
+  __syncthreads();
+}
+
+static __global__ void __launch_bounds__(256) k_mfd_select(int pass, const unsigned* __restrict__ h0,
+                                                           const unsigned* __restrict__ h1, LapSel* __restrict__ sel) {
+  __shared__ unsigned long long scan[256];
+  if (sel->given) return;   // block-uniform
+  if (pass == 0) {
+    unsigned long long loc = 0;
+    for (int i = threadIdx.x; i < 2048; i += 256) loc += h0[i];
+    scan[threadIdx.x] = loc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      unsigned long long m = 0;
+      for (int i = 0; i < 256; ++i) m += scan[i];
+      sel->m = m;
+      if (m == 0) sel->sigma2 = 1.0;
+      sel->k[0] = m ? (m - 1) / 2 : 0;
+      sel->k[1] = m / 2;
+    }
+    __syncthreads();
+    if (sel->m == 0) return;
+    for (int t = 0; t < 2; ++t) sel_find(h0, 0ull, sel->k[t], &sel->c[t], &sel->pre[t], scan);
+    return;
+  }
+  if (sel->m == 0) return;
+  __shared__ unsigned bsel[2];
+  for (int t = 0; t < 2; ++t) sel_find(t ? h1 : h0, sel->c[t], sel->k[t], &sel->c[t], &bsel[t], scan);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (pass == 1) {
+      for (int t = 0; t < 2; ++t) sel->pre[t] = (sel->pre[t] << 11) | bsel[t];
+    } else {
+      const float v0 = __uint_as_float((sel->pre[0] << 10) | bsel[0]);
+      const float v1 = __uint_as_float((sel->pre[1] << 10) | bsel[1]);
+      sel->sigma2 = 0.5 * ((double)v0 + (double)v1);
+    }
+  }
+}
+
+static __global__ void k_mfd_degmax(const float* __restrict__ deg, int n, LapSel* __restrict__ sel) {
+  float m = 0.f;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) m = fmaxf(m, deg[i]);
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(&sel->maxdeg, __float_as_uint(m));
+}
+
 // standardised patch vectors [n][3 p^2] (channel-major, row-major inside the patch); ms = mean, std x3
 static __global__ void k_mfd_patchvec(const float* __restrict__ params, const float* __restrict__ pd,
-                                      const double* __restrict__ ms, const int* __restrict__ corners, int nc, int N,
+                                      const LapSel* __restrict__ sel, const int* __restrict__ corners, int nc, int N,
                                       int p, float* __restrict__ pv) {
   const int q = blockIdx.x, y0 = corners[q / nc], x0 = corners[q % nc], np = p * p;
+  const double* ms = sel->ms;
   for (int e = threadIdx.x; e < 3 * np; e += blockDim.x) {
     const int ch = e / np, k = e % np, v = (y0 + k / p) * N + x0 + k % p;
     const float raw = ch == 2 ? pd[v] : params[2 * v + ch];
@@ -549,9 +657,11 @@ static __global__ void __launch_bounds__(256) k_mfd_dist(const float* __restrict
 // bits [31:21], pass 1 bits [20:10] of the values whose bits [31:21] equal `pre`, pass 2 bits
 // [9:0] of those whose bits [31:10] equal `pre`.  Block-private shared-memory histograms (2048
 // bins), merged with one global atomic per non-empty bin.
-static __global__ void __launch_bounds__(256) k_mfd_hist(const float* __restrict__ d2, int n, int pass, unsigned pre,
+static __global__ void __launch_bounds__(256) k_mfd_hist(const float* __restrict__ d2, int n, int pass,
+                                                         const unsigned* __restrict__ pre_dev,
                                                          unsigned* __restrict__ hist) {
   __shared__ unsigned sh[2048];
+  const unsigned pre = pass > 0 ? *pre_dev : 0u;
   for (int i = threadIdx.x; i < 2048; i += blockDim.x) sh[i] = 0u;
   __syncthreads();
   const int shift = pass == 0 ? 21 : pass == 1 ? 10 : 0;
@@ -570,8 +680,10 @@ static __global__ void __launch_bounds__(256) k_mfd_hist(const float* __restrict
 }
 
 // W[i][j] = exp(-d2 / sigma2) (i != j), 0 on the diagonal; deg[i] = sum_j W[i][j] in a fixed order
-static __global__ void k_mfd_weights(float* __restrict__ d2w, int n, float inv_s2, float* __restrict__ deg) {
+static __global__ void k_mfd_weights(float* __restrict__ d2w, int n, const double* __restrict__ sigma2,
+                                     float* __restrict__ deg) {
   const int i = blockIdx.x;
+  const float inv_s2 = (float)(1.0 / *sigma2);
   double s = 0.0;
   for (int j = threadIdx.x; j < n; j += blockDim.x) {
     float w = j == i ? 0.f : expf(-d2w[(size_t)i * n + j] * inv_s2);
