@@ -1026,7 +1026,11 @@ __global__ void __launch_bounds__(SW * FFTShape<G>::T) k_sn_icols(const float2* 
   }
 }
 
-// spec_out[j][c][e] = sum_i K[j][i][e] spec_in[i][c][e]   (r x r mixing per frequency; R >= r)
+// spec_out[j][c][e] = sum_i K[j][i][e] spec_in[i][c][e]   (r x r mixing per frequency; R >= r).
+// K is Hermitian in (j, i) (T real, c^rho Hermitian): only j <= i is stored, pair index
+// sn_pair(j, i, r) = j r - j (j - 1) / 2 + (i - j), and K_ij = conj(K_ji).
+__host__ __device__ __forceinline__ int sn_pair(int j, int i, int r) { return j * r - j * (j - 1) / 2 + (i - j); }
+
 template <int R>
 __global__ void __launch_bounds__(256) k_sn_mix(const float2* __restrict__ spec_in, const float2* __restrict__ K,
                                                 float2* __restrict__ spec_out, int r, int C, long long E) {
@@ -1042,7 +1046,8 @@ __global__ void __launch_bounds__(256) k_sn_mix(const float2* __restrict__ spec_
 #pragma unroll
     for (int i = 0; i < R; ++i)
       if (i < r) {
-        const float2 k = __ldg(K + ((size_t)j * r + i) * E + e);
+        float2 k = __ldg(K + (size_t)(i >= j ? sn_pair(j, i, r) : sn_pair(i, j, r)) * E + e);
+        if (i < j) k.y = -k.y;
         acc.x = fmaf(k.x, u[i].x, fmaf(-k.y, u[i].y, acc.x));
         acc.y = fmaf(k.x, u[i].y, fmaf(k.y, u[i].x, acc.y));
       }
@@ -1050,7 +1055,7 @@ __global__ void __launch_bounds__(256) k_sn_mix(const float2* __restrict__ spec_
   }
 }
 
-// K[pair][e] = sum_rho cc[pair][rho] T_rho[e]  (plan time; pairs = r * r, T real)
+// K[pair][e] = sum_rho cc[pair][rho] T_rho[e]  (plan time; pairs j <= i, sn_pair order; T real)
 __global__ void __launch_bounds__(256) k_sn_kbuild(const float* __restrict__ psf, const float2* __restrict__ cc,
                                                    int pairs, int R, long long E, float2* __restrict__ K) {
   const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;

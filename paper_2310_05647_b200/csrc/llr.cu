@@ -538,14 +538,14 @@ mrf_status mrf_msllr_solve(mrf_llr h, mrf_dict dict, mrf_plan plan, const void* 
     int pN = 0, pL = 0, pC = 0, pdev = 0, pM = 0;
     plan_dims(plan, &pN, &pL, &pC, &pdev, &pM);
     const size_t E = (size_t)sn_elems(plan), r = (size_t)h->r;
-    const size_t need = (r * r * E + 2 * r * pC * E + 2 * r * V) * sizeof(float2);
+    const size_t need = (r * (r + 1) / 2 * E + 2 * r * pC * E + 2 * r * V) * sizeof(float2);
     if (h->sn_bytes < need) {
       for (float2** p : {&h->Ksn, &h->spa, &h->spb, &h->zs, &h->bv}) {
         if (*p) cudaFree(*p);
         *p = nullptr;
       }
       h->sn_bytes = 0;
-      if (cudaMalloc((void**)&h->Ksn, r * r * E * sizeof(float2)) != cudaSuccess ||
+      if (cudaMalloc((void**)&h->Ksn, r * (r + 1) / 2 * E * sizeof(float2)) != cudaSuccess ||
           cudaMalloc((void**)&h->spa, r * pC * E * sizeof(float2)) != cudaSuccess ||
           cudaMalloc((void**)&h->spb, r * pC * E * sizeof(float2)) != cudaSuccess ||
           cudaMalloc((void**)&h->zs, r * V * sizeof(float2)) != cudaSuccess ||

@@ -867,14 +867,20 @@ mrf_status mrf::sn_build(mrf_plan pl, const float2* basis_h, int r, float2* K, c
       }
     }
   }
-  std::vector<float2> cc(cd.size());
-  for (size_t i = 0; i < cd.size(); ++i) cc[i] = make_float2((float)cd[i].real(), (float)cd[i].imag());
+  const int pairs = r * (r + 1) / 2;   // j <= i (K is Hermitian in (j, i))
+  std::vector<float2> cc((size_t)pairs * R);
+  for (int j = 0; j < r; ++j)
+    for (int i = j; i < r; ++i)
+      for (int rho = 0; rho < R; ++rho) {
+        const std::complex<double> v = cd[((size_t)j * r + i) * R + rho];
+        cc[(size_t)sn_pair(j, i, r) * R + rho] = make_float2((float)v.real(), (float)v.imag());
+      }
   float2* ccd = nullptr;
   CUDA_TRY(cudaMalloc((void**)&ccd, cc.size() * sizeof(float2)));
   cudaError_t e = cudaMemcpyAsync(ccd, cc.data(), cc.size() * sizeof(float2), cudaMemcpyHostToDevice, st);
-  const long long E = sn_elems(pl), tot = (long long)r * r * E;
+  const long long E = sn_elems(pl), tot = (long long)pairs * E;
   if (e == cudaSuccess) {
-    k_sn_kbuild<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(pl->psf, ccd, r * r, R, E, K);
+    k_sn_kbuild<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(pl->psf, ccd, pairs, R, E, K);
     e = cudaGetLastError();
   }
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);

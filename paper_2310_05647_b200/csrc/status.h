@@ -15,7 +15,7 @@ void plan_dims(mrf_plan plan, int* N, int* L, int* C, int* device, int* M = null
 // 2D tiled TMA map over a row-major [rows][cols] array (row pitch row_bytes, a multiple of 16):
 // (box_cols x box_rows) boxes, 128-byte swizzle (box_cols x element size = 128), out-of-bounds
 // elements read as zero.  dict.cu.
-// subspace normal operator on Toeplitz plans (mrfnufft.cu): K = [r][r][G*G] complex mixing
+// subspace normal operator on Toeplitz plans (mrfnufft.cu): K = [r (r + 1) / 2][G*G] complex mixing
 // kernels from the basis rows (host [r][L]); apply: Z = P_S A^H A (U d) in coefficients, U and Z
 // DEVICE [r][N][N], spectra workspaces [r][C][G*G] each.
 bool plan_toeplitz(mrf_plan plan);
