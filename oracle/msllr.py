@@ -54,20 +54,21 @@ def maps_of(X, D, lut):
 
 def solve(b, traj, D, lut, d, mu: float, lam1_0: float, lam2: float, beta: float, max_iter: int,
           tol: float = 1e-5, W: int = 6, N: int | None = None, p: int = 11, s: int = 5,
-          sigma2: float | None = None, workers: int = 1, op: str = "grid"):
-    """Algorithm 1.  b [L][1][M] k-space (single coil), traj [R][M][2], D [K][L] atoms, lut [K][2]
-    (T1, T2), d [r][L] the basis of P_S.  op = "grid": A is the KB gridding NUFFT; op = "nudft":
-    A is the plain definition (the direct non-uniform DFT).
+          sigma2: float | None = None, workers: int = 1, op: str = "grid", coils=None):
+    """Algorithm 1.  b [L][C][M] k-space, traj [R][M][2], D [K][L] atoms, lut [K][2] (T1, T2),
+    d [r][L] the basis of P_S, coils [C][N][N] or None (A = F_u C).  op = "grid":
+    A is the KB gridding NUFFT; op = "nudft": A is the plain definition (the direct non-uniform DFT).
     Returns dict(x, k, eta, rho, iters, cost, lambda1)."""
     b = np.asarray(b, np.complex128)
+    S = coils
     if op == "nudft":
-        A = lambda X: on.nudft_forward(X, traj, None)
-        normal = lambda X: on.nudft_adjoint(on.nudft_forward(X, traj, None), traj, None, N)
-        rhs = on.nudft_adjoint(b, traj, None, N)
+        A = lambda X: on.nudft_forward(X, traj, S)
+        normal = lambda X: on.nudft_adjoint(on.nudft_forward(X, traj, S), traj, S, N)
+        rhs = on.nudft_adjoint(b, traj, S, N)
     else:
-        A = lambda X: on.forward(X, traj, None, W, workers=workers)
-        normal = lambda X: on.normal(X, traj, None, W, workers=workers)
-        rhs = on.adjoint(b, traj, None, N, W, workers=workers)        # A^* b
+        A = lambda X: on.forward(X, traj, S, W, workers=workers)
+        normal = lambda X: on.normal(X, traj, S, W, workers=workers)
+        rhs = on.adjoint(b, traj, S, N, W, workers=workers)           # A^* b
     X = rhs.copy()                                                     # X^0
     lam1, lap = 0.0, None
 

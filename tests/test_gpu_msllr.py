@@ -176,3 +176,28 @@ def test_basis_coordinate_loop_on_a_toeplitz_plan(binding, request, lam1, iters,
     if lam1:
         assert abs(out["lambda1"] - ref["lambda1"]) <= 1e-4 * ref["lambda1"]
     pl.close(), op.close(), dic.close()
+
+
+@pytest.mark.parametrize("normal,opn", [("gridding", "grid"), ("toeplitz", "nudft")])
+def test_multicoil_loop(binding, problem, normal, opn):
+    """Algorithm 1 with C = 3 coil sensitivities (A = F_u C, SENSE-like; SURVEY.md §8(c) #13 maps):
+    LLR-only, 3 iterations, on a gridding and on a Toeplitz (basis-coordinate) plan."""
+    pr = problem
+    coils = synth.coil_maps(N, 3, 5)
+    D = pr["D"]                                   # the fixture's dictionary; data re-simulated with coils
+    rng = np.random.default_rng([27, 9])
+    k = rng.integers(D.shape[0], size=N * N)
+    x_true = (rng.uniform(0.4, 1.0, N * N)[:, None] * D[k]).T.reshape(L, N, N)
+    b = on.forward(x_true, pr["traj"], coils, W)
+    ref = oms.solve(b, pr["traj"], D, pr["lut"], pr["d"], pr["mu"], 0.0, 0.05, 0.5, 3, tol=0.0, W=W, N=N, p=P, s=S,
+                    op=opn, coils=coils)
+    dic = binding.Dictionary(D, pr["lut"])
+    dic.basis(0.9999, 32)
+    op = binding.LLR(dic, N, P, S)
+    pl = binding.Plan(N, pr["traj"], L, W=W, coils=coils, normal=normal)
+    bd = torch.from_numpy(b.astype(np.complex64)).cuda()
+    out = op.solve(dic, pl, bd, mu=pr["mu"], lam1=0.0, lam2=0.05, beta=0.5, max_iter=3, tol=0.0)
+    torch.cuda.synchronize()
+    assert _rel(out["x"].cpu().numpy(), ref["x"]) <= 1e-4
+    assert np.allclose(out["cost"], ref["cost"], rtol=1e-4, atol=0)
+    pl.close(), op.close(), dic.close()
