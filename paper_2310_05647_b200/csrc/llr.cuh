@@ -200,14 +200,17 @@ static __global__ void __launch_bounds__(kSvtThreads) k_llr_svt(const float2* __
         if (b < r) {
           const double al = A[a * rp + a].x, be = A[b * rp + b].x;
           const double2 gg = A[a * rp + b];
-          const double mag = sqrt(gg.x * gg.x + gg.y * gg.y);
-          if (mag > floor_g) {
+          const double g2 = gg.x * gg.x + gg.y * gg.y;
+          if (g2 > floor_g * floor_g) {
             // A <- J^H A J with J = [[c, -s e], [s conj(e), c]] on (a, b), e = g / |g|:
-            // cot 2theta = (al - be) / 2|g| zeroes the (a, b) entry
-            const double kap = (al - be) / (2.0 * mag);
+            // cot 2theta = (al - be) / 2|g| zeroes the (a, b) entry.  rsqrt (1 ulp) instead of
+            // sqrt + divisions: |e| and c^2 (1 + t^2) equal 1 to float64 rounding either way,
+            // so J stays unitary; t only sets the angle.
+            const double inv = rsqrt(g2);
+            const double kap = (al - be) * (0.5 * inv);
             const double tt = (kap >= 0.0 ? 1.0 : -1.0) / (fabs(kap) + sqrt(1.0 + kap * kap));
-            const double cs = 1.0 / sqrt(1.0 + tt * tt);
-            R = make_double4(cs, tt * cs, gg.x / mag, gg.y / mag);
+            const double cs = rsqrt(1.0 + tt * tt);
+            R = make_double4(cs, tt * cs, gg.x * inv, gg.y * inv);
           }
         }
         rot[lane] = R;
