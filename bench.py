@@ -402,6 +402,21 @@ def run_ours(args):
                          "(PAPER.md:319 grid, surrogate fingerprints)"}
         dic.close()
 
+    # ---------------------------------------------------------------- density compensation
+    dcf_res = None
+    if world == 1:
+        t0 = time.perf_counter()
+        plan_d = binding.Plan(cfg.N, traj, L, coils=coils, W=cfg.W, device=local, dcf=True)
+        plan_ms = (time.perf_counter() - t0) * 1e3
+        xd = torch.empty_like(xbuf)
+        ms_adj_dcf = time_op(lambda: plan_d.adjoint_dcf(y, x=xd), 5)
+        ms_adj = time_op(lambda: plan_d.adjoint(y, x=xd), 5)
+        dcf_res = {"ms_adjoint_dcf": ms_adj_dcf, "ms_adjoint": ms_adj, "plan_ms_with_dcf": plan_ms,
+                   "note": "mrf_adjoint_dcf = A^H (w . y) with the plan's Pipe-Menon weights (20 iterations, "
+                           "float64 at plan time): one scaling kernel + the adjoint pipeline"}
+        plan_d.close()
+        del xd
+
     # ---------------------------------------------------------------- (MS-)LLR outer step and Algorithm 1
     llr_res = None
     if not args.no_llr and world == 1 and cfg.C == 1:
@@ -550,7 +565,7 @@ def run_ours(args):
         "hbm": {"algorithmic_bytes_per_step": hbm_bytes, "achieved_GBs": hbm_achieved, "peak_GBs": hbm_peak,
                 "frac": hbm_achieved / hbm_peak},
         "cufft_ref_ms_fft2_LC": cufft_ms,
-        "roofline": roofline, "roofline_AHA": roofline_aha, "toeplitz": toep, "match": match, "llr": llr_res, "kernel_share": share, "kernel_share_of_kernel_time": share_k, "gpu_launches": gpu_launches,
+        "roofline": roofline, "roofline_AHA": roofline_aha, "toeplitz": toep, "match": match, "dcf": dcf_res, "llr": llr_res, "kernel_share": share, "kernel_share_of_kernel_time": share_k, "gpu_launches": gpu_launches,
         "clocks": clk, "e2e": e2e, "cpu_baseline": cpu,
     }
     if rank == 0:
