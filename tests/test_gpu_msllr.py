@@ -201,3 +201,52 @@ def test_multicoil_loop(binding, problem, normal, opn):
     assert _rel(out["x"].cpu().numpy(), ref["x"]) <= 1e-4
     assert np.allclose(out["cost"], ref["cost"], rtol=1e-4, atol=0)
     pl.close(), op.close(), dic.close()
+
+
+def test_solve_edge_cases(binding, problem):
+    """max_iter = 0 returns X^0 = A^H b and Phi_D(X^0); a dictionary whose basis changed after the
+    LLR operator was created falls back to frame-domain matching and stays correct; match_coef
+    without a basis is rejected."""
+    pr = problem
+    dic, op, pl, b = _gpu(binding, pr)
+    out0 = op.solve(dic, pl, b, mu=pr["mu"], lam1=0.0, max_iter=0)
+    assert out0["iters"] == 0 and out0["cost"] == []
+    x0 = pl.adjoint(b)
+    torch.cuda.synchronize()
+    assert torch.equal(out0["x"], x0)
+    i0, _, _ = dic.match(x0.view(L, -1))
+    assert torch.equal(out0["index"], i0)
+    # basis recomputed with another rank after the operator was created: the operator keeps its
+    # own basis; Phi_D inside the loop then runs on frames (same answer as the coefficient path)
+    ref = op.solve(dic, pl, b, mu=pr["mu"], lam1=0.0, lam2=0.05, beta=0.5, max_iter=2, tol=0.0)
+    dic.basis(0.99, 4)
+    alt = op.solve(dic, pl, b, mu=pr["mu"], lam1=0.0, lam2=0.05, beta=0.5, max_iter=2, tol=0.0)
+    torch.cuda.synchronize()
+    assert _rel(alt["x"].cpu().numpy(), ref["x"].cpu().numpy()) <= 1e-6
+    assert np.allclose(alt["cost"], ref["cost"], rtol=1e-6)
+    assert (alt["index"] == ref["index"]).float().mean().item() > 0.99
+    pl.close(), op.close(), dic.close()
+    d2 = binding.Dictionary(pr["D"], pr["lut"])
+    with pytest.raises(binding.MrfError):
+        d2.match_coef(torch.zeros((4, 16), dtype=torch.complex64, device="cuda"))
+    d2.close()
+
+
+def test_stop_rule_in_basis_coordinates(binding, problem):
+    pr = problem
+    dic = binding.Dictionary(pr["D"], pr["lut"])
+    dic.basis(0.9999, 32)
+    op = binding.LLR(dic, N, P, S)
+    pl = binding.Plan(N, pr["traj"], L, W=W, normal="toeplitz")
+    b = torch.from_numpy(pr["b"].astype(np.complex64)).cuda()
+    full = op.solve(dic, pl, b, mu=pr["mu"], lam1=0.0, lam2=0.05, beta=0.5, max_iter=8, tol=0.0)
+    c = full["cost"]
+    # a tolerance between two successive relative decreases stops exactly after the first of them
+    rel = [c[n - 1] / c[n] - 1.0 for n in range(1, len(c))]
+    n_stop = next(n for n in range(1, len(rel)) if rel[n] < rel[n - 1])   # first n where the decrease slows
+    tol = 0.5 * (rel[n_stop] + rel[n_stop - 1])
+    early = [n for n in range(1, len(c)) if rel[n - 1] < tol]
+    out = op.solve(dic, pl, b, mu=pr["mu"], lam1=0.0, lam2=0.05, beta=0.5, max_iter=8, tol=tol)
+    assert out["iters"] == early[0] + 1
+    assert np.allclose(out["cost"], c[:out["iters"]], rtol=1e-6)
+    pl.close(), op.close(), dic.close()
