@@ -250,3 +250,27 @@ def test_stop_rule_in_basis_coordinates(binding, problem):
     assert out["iters"] == early[0] + 1
     assert np.allclose(out["cost"], c[:out["iters"]], rtol=1e-6)
     pl.close(), op.close(), dic.close()
+
+
+def test_basis_coordinate_loop_at_the_mrf_size(binding):
+    """Full MRF size (256^2, 1000 frames, the 3336-atom dictionary, 2500 patches): three MS-LLR
+    iterations in basis coordinates (Toeplitz plan) against the frame-domain loop on a gridding plan
+    (both parity-tested against the oracle at small sizes above).  They differ by the gridding
+    error of the gridding plan's A^H A (~1e-5), not by the reformulation."""
+    cfg = synth.get_config("mrf")
+    traj = synth.spiral_trajectory(cfg.M, cfg.R, cfg.turns, cfg.p)
+    grid = sd.t1t2_grid()
+    dic = binding.Dictionary(sd.surrogate_dictionary(cfg.L, grid), grid.astype(np.float32))
+    dic.basis(0.9999, 32)
+    op = binding.LLR(dic, cfg.N)
+    pg = binding.Plan(cfg.N, traj, cfg.L, W=cfg.W)
+    pt = binding.Plan(cfg.N, traj, cfg.L, W=cfg.W, normal="toeplitz")
+    b = pg.forward(torch.from_numpy(synth.images(cfg)).cuda())
+    kw = dict(mu=0.018, lam1=1e-7, lam2=0.1, beta=0.2, max_iter=3, tol=0.0)
+    og = op.solve(dic, pg, b, **kw)
+    ot = op.solve(dic, pt, b, **kw)
+    torch.cuda.synchronize()
+    assert _rel(ot["x"].cpu().numpy(), og["x"].cpu().numpy()) <= 1e-4
+    assert np.allclose(ot["cost"], og["cost"], rtol=1e-4)
+    assert (ot["index"] == og["index"]).float().mean().item() > 0.999
+    pg.close(), pt.close(), op.close(), dic.close()
