@@ -1,7 +1,9 @@
-// llr.cu -- host side of the LLR outer step (lambda_1 = 0; PAPER.md:217-264,
-// Eqs. (15), (17), (20), (21)): mrf_llr_create / mrf_llr_step / mrf_llr_destroy of
-// include/mrfnufft.h.  Kernels in llr.cuh; the subspace basis comes from the dictionary
-// (mrf_dict_basis, dict.cu).
+// llr.cu -- host side of the MS-LLR outer step and of Algorithm 1 (
+// PAPER.md:130-180 Eqs. (7)-(11), 217-264 Eqs. (15), (17), (20), (21), 266-298 Algorithm 1):
+// mrf_llr_create / _laplacian / _step / _cost / _destroy and mrf_msllr_solve of include/mrfnufft.h.
+// Kernels in llr.cuh (coefficients, SVT, update, manifold term), gemm3.cuh (the tf32 x 3
+// tensor-core GEMM G = W Q) and gridding.cuh (the subspace normal k_sn_*); the subspace basis and
+// the basis-coordinate dictionary come from dict.cu (mrf_dict_basis).
 #include <cuda_runtime.h>
 
 #include <algorithm>

@@ -1,7 +1,7 @@
-// llr.cuh -- the locally-low-rank outer step of Algorithm 1 in subspace coordinates (SURVEY.md
-// §8(f) f2, the paper's LLR ablation: lambda_1 = 0).  PAPER.md:217-264:
+// llr.cuh -- the (MS-)LLR outer step of Algorithm 1 in subspace coordinates.
+// PAPER.md:217-264:
 //
-//   Z   = P_S(X - mu A^*(A X - b)),  P_S(X) = X d^dagger d               (Eqs. 15, 17)
+//   Z   = P_S(X - mu [A^*(A X - b) + lambda_1 Q^*(Q(X) L)]),  P_S(X) = X d^dagger d   (Eqs. 15, 17)
 //   P_q = SVT_{1/beta}(Q_q(Z))                                            (Eq. 20)
 //   X+  = (Z + gamma Q^*(P)) / (1 + gamma c),  gamma = mu lambda_2 beta    (Eq. 21, reading 25)
 //
@@ -14,7 +14,11 @@
 //   k_llr_coef   : Y[v][i] = sum_l conj(d[i][l]) (x - mu (n - rhs))[l][v]   (reads 3 image arrays)
 //   k_llr_svt    : per patch: Gram, Jacobi, M = W f W^H, P_q = Y_q M, sum sigma (nuclear norm)
 //   k_llr_update : per voxel: sum of its covering patches' P (fixed order), the Eq. 21 division,
-//                  x+[l][v] = sum_i Xc[i] d[i][l]
+//                  the coefficients Xc of x+ and (optionally) x+[l][v] = sum_i Xc[i] d[i][l]
+//   k_sn_grad, k_llr_resid, k_llr_dotre : the basis-coordinate gradient and float64 reductions
+//   mfd::*       : the manifold term (Eqs. 7-11): foreground statistics, patch distances, the
+//                  radix-select median bandwidth, weights and degrees, Q(x) blocks, the update
+//                  with deg Q - W Q, the trace penalty (W Q itself: gemm3.cuh)
 #pragma once
 #include <cuda_runtime.h>
 
@@ -24,7 +28,7 @@ namespace mrf {
 namespace llr {
 
 constexpr int RMAX = 32;      // largest supported subspace rank
-constexpr int kSvtThreads = 128;   // 4 patches (warps) per block
+constexpr int kSvtThreads = 128;   // 4 patches (one warp each) per block
 
 __device__ __forceinline__ float2 cconjmul(float2 a, float2 b) {   // conj(a) * b
   return make_float2(fmaf(a.x, b.x, a.y * b.y), fmaf(a.x, b.y, -a.y * b.x));
