@@ -439,10 +439,10 @@ def run_ours(args):
         ms_ms = time_op(lambda: op.step(plan, xbuf, rhs_l, 1.0, 0.1, 0.2, x_out=xl, nuclear=False, lam1=lam1), 5)
         ms_cost = time_op(lambda: op.cost(plan, xl, y, lam1=lam1, lam2=0.1), 3)
 
-        def solve_s(n, l1, pln=None):
+        def solve_s(n, l1, pln=None, costs=True):
             torch.cuda.synchronize()
             t0 = time.perf_counter()
-            op.solve(dic, pln or plan, y, mu=0.018, lam1=l1, lam2=0.1, beta=0.2, max_iter=n, tol=0.0)
+            op.solve(dic, pln or plan, y, mu=0.018, lam1=l1, lam2=0.1, beta=0.2, max_iter=n, tol=0.0, costs=costs)
             torch.cuda.synchronize()
             return (time.perf_counter() - t0) * 1e3
 
@@ -454,17 +454,20 @@ def run_ours(args):
         solve_s(2, 1e-7, plan_t)
         it_llr_t = min((solve_s(11, 0.0, plan_t) - solve_s(1, 0.0, plan_t)) / 10 for _ in range(2))
         it_ms_t = min((solve_s(11, 1e-7, plan_t) - solve_s(1, 1e-7, plan_t)) / 10 for _ in range(2))
+        it_ms_t_nc = min((solve_s(11, 1e-7, plan_t, False) - solve_s(1, 1e-7, plan_t, False)) / 10 for _ in range(2))
         plan_t.close()
         llr_res = {"ms_per_step": ms_llr, "ms_normal_inside": ms_normal, "rank": int(d_basis.shape[0]),
                    "patches": nc * nc, "basis_ms": basis_ms,
                    "ms_per_step_manifold": ms_ms, "ms_laplacian": ms_lap, "ms_cost": ms_cost,
                    "ms_per_algorithm1_iteration": {"llr": it_llr, "ms_llr": it_ms,
                                                    "llr_basis_coordinates": it_llr_t, "ms_llr_basis_coordinates": it_ms_t,
+                                                   "ms_llr_basis_coordinates_no_cost": it_ms_t_nc,
                                                    "note": "mrf_msllr_solve wall clock (T(11) - T(1)) / 10, best of 2: step + "
                                                            "cost (+ Phi_D + Laplacian update for MS-LLR); "
                                                            "mu = 0.018 (< 1/lambda_max), lambda_1^0 = 1e-7; "
                                                            "*_basis_coordinates: on a MRF_NORMAL_TOEPLITZ plan (subspace "
-                                                           "normal, exact NUDFT normal operator)"},
+                                                           "normal, exact NUDFT normal operator); *_no_cost: fixed iteration count without "
+                                                           "cost(n) (tol = 0, no cost output)"},
                    "note": "mrf_llr_step: Z = P_S(X - mu(A^H A X - A^H b) [+ mu lambda_1 Q*(Q(X) L)]), per-patch "
                            "SVT (11x11, stride 5, tau = 1/beta = 5) in subspace coordinates, overlap-exact X "
                            "update; mu = 1, lambda_2 = 0.1, beta = 1/5 (PAPER.md:304); basis from the synthetic "

@@ -278,7 +278,8 @@ mrf_status mrf_llr_cost(mrf_llr llr, mrf_plan plan, const void* x, const void* b
  * dictionary LUT of (T1, T2) (P = 2) and params.  b: DEVICE [L][C][M]; x: DEVICE [L][N][N] (out);
  * index int32 [V], pd float [V], params float [V][P] (nullable when lambda1 = 0): DEVICE.
  * info (nullable): iterations run, cost(1..iters) into info->cost (HOST, max_iter entries, nullable)
- * and the last lambda_1.  Allocates two image stacks on first use; synchronises.  Errors: MRF_EINVAL,
+ * and the last lambda_1.  With tol <= 0 and no info->cost the cost is not evaluated (nothing
+ * depends on it).  Allocates two image stacks on first use; synchronises.  Errors: MRF_EINVAL,
  * and the errors of the calls above. */
 typedef struct {
   float mu, lambda1, lambda2, beta;   /* Eq. 15 step, lambda_1^0, lambda_2, beta (SVT threshold 1/beta) */

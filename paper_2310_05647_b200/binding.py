@@ -474,8 +474,10 @@ class LLR:
         return c.value, (t[0], t[1], t[2])
 
     def solve(self, dictionary: "Dictionary", plan: "Plan", b, mu: float = 1.0, lam1: float = 0.0,
-              lam2: float = 0.1, beta: float = 0.2, max_iter: int = 10, tol: float = 1e-5, sigma2: float = 0.0):
-        """Algorithm 1 (mrf_msllr_solve).  Returns dict(x, index, pd, params, iters, cost, lambda1)."""
+              lam2: float = 0.1, beta: float = 0.2, max_iter: int = 10, tol: float = 1e-5, sigma2: float = 0.0,
+              costs: bool = True):
+        """Algorithm 1 (mrf_msllr_solve).  Returns dict(x, index, pd, params, iters, cost, lambda1).
+        costs=False with tol <= 0: cost(n) is not evaluated (cost = [])."""
         if not (isinstance(b, torch.Tensor) and b.is_cuda and b.dtype == torch.complex64 and b.is_contiguous()):
             raise TypeError("b must be a contiguous CUDA complex64 tensor [L][C][M]")
         dev = b.device
@@ -486,12 +488,12 @@ class LLR:
         params = torch.empty((V, dictionary.P), dtype=torch.float32, device=dev) if dictionary.P else None
         prm = MsllrParams(mu, lam1, lam2, beta, int(max_iter), tol, sigma2)
         cost = (ctypes.c_double * max(int(max_iter), 1))()
-        info = MsllrInfo(0, ctypes.cast(cost, ctypes.POINTER(ctypes.c_double)), 0.0)
+        info = MsllrInfo(0, ctypes.cast(cost, ctypes.POINTER(ctypes.c_double)) if costs else None, 0.0)
         st = torch.cuda.current_stream(dev).cuda_stream
         _check(lib.mrf_msllr_solve(self._h, dictionary._h, plan._h, _ptr(b), ctypes.byref(prm), _ptr(x), _ptr(index),
                                    _ptr(pd), _ptr(params), ctypes.byref(info), ctypes.c_void_p(st)))
         return {"x": x, "index": index, "pd": pd, "params": params, "iters": info.iters,
-                "cost": [cost[i] for i in range(info.iters)], "lambda1": info.lambda1}
+                "cost": [cost[i] for i in range(info.iters)] if costs else [], "lambda1": info.lambda1}
 
     def close(self):
         if getattr(self, "_h", None):

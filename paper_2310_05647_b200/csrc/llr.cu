@@ -581,6 +581,9 @@ mrf_status mrf_msllr_solve(mrf_llr h, mrf_dict dict, mrf_plan plan, const void* 
   double prev = 0.0;
   int it = 0;
   bool maps_current = manifold;
+  // cost(n) only feeds the stop rule and info->cost: without either it is not evaluated (the
+  // iterates do not depend on it)
+  const bool monitor = prm->tol > 0.0 || (info && info->cost);
   for (int n = 1; n <= prm->max_iter; ++n) {
     // Z^n, P^n, X^n (Eqs. 15, 20, 21), then cost(n)
     // from n = 2 on, A X^{n-1} is the previous cost's forward (h->yb): A^H A X^{n-1} = A^H (h->yb)
@@ -588,14 +591,18 @@ mrf_status mrf_msllr_solve(mrf_llr h, mrf_dict dict, mrf_plan plan, const void* 
       MRF_TRY(sub_step(h, prm->mu, lam1, prm->lambda2, prm->beta, st));
     } else {
       MRF_TRY(step_impl(h, plan, cur, h->rhs, prm->mu, lam1, prm->lambda2, prm->beta, nxt, nullptr, nullptr, stream,
-                        have_coef ? h->xcv : nullptr, have_coef ? h->yb : nullptr));
+                        have_coef ? h->xcv : nullptr, have_coef && monitor ? h->yb : nullptr));
       std::swap(cur, nxt);
     }
     have_coef = true;   // k_llr_update wrote the coefficients of X^n
     double c = 0.0;
-    if (sub) MRF_TRY(sub_cost(h, plan, b2, lam1, prm->lambda2, &c, st));
-    else MRF_TRY(cost_impl(h, plan, cur, b, lam1, prm->lambda2, &c, nullptr, stream, h->xcv));
-    if (info && info->cost) info->cost[n - 1] = c;
+    if (monitor) {
+      if (sub) MRF_TRY(sub_cost(h, plan, b2, lam1, prm->lambda2, &c, st));
+      else MRF_TRY(cost_impl(h, plan, cur, b, lam1, prm->lambda2, &c, nullptr, stream, h->xcv));
+      if (info && info->cost) info->cost[n - 1] = c;
+    } else if (sub) {   // no cost wanted: only the subspace normal the next step needs
+      MRF_TRY(sn_apply(plan, h->Ksn, h->r, h->xcr, h->zs, h->spa, h->spb, st));
+    }
     it = n;
     maps_current = false;
     // stop rule cost(n-1) / cost(n) - 1 < tol, from n = 2 (reading 27: cost(0) is not defined)

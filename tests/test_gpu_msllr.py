@@ -274,3 +274,22 @@ def test_basis_coordinate_loop_at_the_mrf_size(binding):
     assert np.allclose(ot["cost"], og["cost"], rtol=1e-4)
     assert (ot["index"] == og["index"]).float().mean().item() > 0.999
     pg.close(), pt.close(), op.close(), dic.close()
+
+
+@pytest.mark.parametrize("normal", ["gridding", "toeplitz"])
+def test_solve_without_cost_monitoring(binding, problem1, normal):
+    """tol <= 0 and no cost output: cost(n) is skipped, the iterates are unchanged."""
+    pr = problem1
+    dic = binding.Dictionary(pr["D"], pr["lut"])
+    dic.basis(0.9999, 32)
+    op = binding.LLR(dic, N, P, S)
+    pl = binding.Plan(N, pr["traj"], L, W=W, normal=normal)
+    b = torch.from_numpy(pr["b"].astype(np.complex64)).cuda()
+    kw = dict(mu=pr["mu"], lam1=2e-3, lam2=0.05, beta=0.5, max_iter=3, tol=0.0)
+    a = op.solve(dic, pl, b, **kw)
+    c = op.solve(dic, pl, b, costs=False, **kw)
+    torch.cuda.synchronize()
+    assert c["cost"] == [] and c["iters"] == 3
+    assert _rel(c["x"].cpu().numpy(), a["x"].cpu().numpy()) <= 1e-6
+    assert torch.equal(c["index"], a["index"])
+    pl.close(), op.close(), dic.close()
