@@ -249,6 +249,17 @@ static __global__ void __launch_bounds__(kSvtThreads) k_llr_svt(const float2* __
       __syncwarp();
     }
     if (!rotated) break;
+    // converged if no off-diagonal entry is above the floor: the next sweep would rotate nothing
+    // (one parallel scan instead of a sweep of no-op rounds)
+    bool big = false;
+    for (int e = lane; e < r * r; e += 32) {
+      const int i = e / r, j = e % r;
+      if (i < j) {
+        const double2 v = A[i * rp + j];
+        big |= v.x * v.x + v.y * v.y > floor_g * floor_g;
+      }
+    }
+    if (!__any_sync(0xffffffffu, big)) break;
   }
   if (Wq)
     for (int e = lane; e < r * r; e += 32) Wq[e] = Wm[(e / r) * rp + e % r];
