@@ -1034,25 +1034,33 @@ __host__ __device__ __forceinline__ int sn_pair(int j, int i, int r) { return j 
 template <int R>
 __global__ void __launch_bounds__(256) k_sn_mix(const float2* __restrict__ spec_in, const float2* __restrict__ K,
                                                 float2* __restrict__ spec_out, int r, int C, long long E) {
+  // each stored pair (j <= i) is loaded once and used twice: out_j += K u_i, out_i += conj(K) u_j
   const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (idx >= (long long)C * E) return;
   const int c = (int)(idx / E);
   const long long e = idx % E;
-  float2 u[R];
+  float2 u[R], acc[R];
 #pragma unroll
-  for (int i = 0; i < R; ++i) u[i] = i < r ? __ldg(spec_in + ((size_t)i * C + c) * E + e) : make_float2(0.f, 0.f);
-  for (int j = 0; j < r; ++j) {
-    float2 acc = make_float2(0.f, 0.f);
-#pragma unroll
-    for (int i = 0; i < R; ++i)
-      if (i < r) {
-        float2 k = __ldg(K + (size_t)(i >= j ? sn_pair(j, i, r) : sn_pair(i, j, r)) * E + e);
-        if (i < j) k.y = -k.y;
-        acc.x = fmaf(k.x, u[i].x, fmaf(-k.y, u[i].y, acc.x));
-        acc.y = fmaf(k.x, u[i].y, fmaf(k.y, u[i].x, acc.y));
-      }
-    spec_out[((size_t)j * C + c) * E + e] = acc;
+  for (int i = 0; i < R; ++i) {
+    u[i] = i < r ? __ldg(spec_in + ((size_t)i * C + c) * E + e) : make_float2(0.f, 0.f);
+    acc[i] = make_float2(0.f, 0.f);
   }
+#pragma unroll
+  for (int j = 0; j < R; ++j)
+#pragma unroll
+    for (int i = j; i < R; ++i)
+      if (i < r) {
+        const float2 k = __ldg(K + (size_t)sn_pair(j, i, r) * E + e);
+        acc[j].x = fmaf(k.x, u[i].x, fmaf(-k.y, u[i].y, acc[j].x));
+        acc[j].y = fmaf(k.x, u[i].y, fmaf(k.y, u[i].x, acc[j].y));
+        if (i != j) {   // conj(K_ji) u_j
+          acc[i].x = fmaf(k.x, u[j].x, fmaf(k.y, u[j].y, acc[i].x));
+          acc[i].y = fmaf(k.x, u[j].y, fmaf(-k.y, u[j].x, acc[i].y));
+        }
+      }
+#pragma unroll
+  for (int j = 0; j < R; ++j)
+    if (j < r) spec_out[((size_t)j * C + c) * E + e] = acc[j];
 }
 
 // K[pair][e] = sum_rho cc[pair][rho] T_rho[e]  (plan time; pairs j <= i, sn_pair order; T real)
