@@ -268,10 +268,10 @@ mrf_status mrf_llr_laplacian(mrf_llr h, const float* params, const float* pd, do
   CUDA_TRY(cudaMemsetAsync(pdmax, 0, sizeof(unsigned), st));
   mfd::k_mfd_max<<<kStatBlocks, 256, 0, st>>>(pd, V, pdmax);
   mfd::k_mfd_stats<<<kStatBlocks, 256, 0, st>>>(params, pd, V, pdmax, h->stats);
-  mfd::k_mfd_stats_final<<<1, 32, 0, st>>>(h->stats, kStatBlocks, sel);
+  mfd::k_mfd_stats_final<<<1, 256, 0, st>>>(h->stats, kStatBlocks, sel);
   MRF_TRY(check_launch("k_mfd_stats"));
   mfd::k_mfd_patchvec<<<n, 128, 0, st>>>(params, pd, sel, h->corners, h->nc, h->N, h->p, h->pv);
-  const dim3 gd((unsigned)((n + 63) / 64), (unsigned)((n + 63) / 64));
+  const dim3 gd((unsigned)((n + 127) / 128), (unsigned)((n + 127) / 128));
   mfd::k_mfd_dist<<<gd, 256, 0, st>>>(h->pv, n, 3 * np, h->W);
   MRF_TRY(check_launch("k_mfd_dist"));
   // sigma^2: given, or the median of the nonzero upper-triangle distances by an exact radix select
@@ -285,12 +285,11 @@ mrf_status mrf_llr_laplacian(mrf_llr h, const float* params, const float* pd, do
     unsigned* h1 = h->hist + 2048;
     const unsigned hb = 2 * 148;
     CUDA_TRY(cudaMemsetAsync(h0, 0, 2048 * sizeof(unsigned), st));
-    mfd::k_mfd_hist<<<hb, 256, 0, st>>>(h->W, n, 0, nullptr, h0);
+    mfd::k_mfd_hist<<<hb, 256, 0, st>>>(h->W, n, 0, nullptr, h0, h1);
     mfd::k_mfd_select<<<1, 256, 0, st>>>(0, h0, h0, sel);
     for (int ps = 1; ps <= 2; ++ps) {
       CUDA_TRY(cudaMemsetAsync(h0, 0, 2 * 2048 * sizeof(unsigned), st));
-      mfd::k_mfd_hist<<<hb, 256, 0, st>>>(h->W, n, ps, &sel->pre[0], h0);
-      mfd::k_mfd_hist<<<hb, 256, 0, st>>>(h->W, n, ps, &sel->pre[1], h1);
+      mfd::k_mfd_hist<<<hb, 256, 0, st>>>(h->W, n, ps, sel->pre, h0, h1);
       mfd::k_mfd_select<<<1, 256, 0, st>>>(ps, h0, h1, sel);
     }
     MRF_TRY(check_launch("k_mfd_select"));

@@ -515,13 +515,16 @@ struct LapSel {
   unsigned given;                // sigma2 given by the caller
 };
 
-// ms from the per-block partials of k_mfd_stats, summed in block order (one thread per sum)
+// ms from the per-block partials of k_mfd_stats: each of the 7 sums is reduced by 32 lanes of one
+// warp (fixed strided partial sums, then a fixed xor tree: deterministic), one warp per sum
 static __global__ void k_mfd_stats_final(const double* __restrict__ part, int nblk, LapSel* __restrict__ sel) {
-  __shared__ double a[7];
-  if (threadIdx.x < 7) {
+  __shared__ double a[8];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (w < 7) {
     double t = 0.0;
-    for (int b = 0; b < nblk; ++b) t += part[(size_t)b * 7 + threadIdx.x];
-    a[threadIdx.x] = t;
+    for (int b = lane; b < nblk; b += 32) t += part[(size_t)b * 7 + w];
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    if (lane == 0) a[w] = t;
   }
   __syncthreads();
   if (threadIdx.x < 3) {
@@ -625,34 +628,34 @@ static __global__ void k_mfd_patchvec(const float* __restrict__ params, const fl
 }
 
 // d2[i][j] = ||pv_i - pv_j||^2, 32 x 32 tiles of patch pairs
-// d2[i][j] = ||pv_i - pv_j||^2 over dim components: 64 x 64 tiles of the upper triangle (the
-// lower one is the mirror), 16 x 16 threads with 4 x 4 outputs each, 16-component chunks in smem.
+// d2[i][j] = ||pv_i - pv_j||^2 over dim components: 128 x 128 tiles of the upper triangle (the
+// lower one is the mirror), 16 x 16 threads with 8 x 8 outputs each, 16-component chunks in smem.
 static __global__ void __launch_bounds__(256) k_mfd_dist(const float* __restrict__ pv, int n, int dim,
                                                          float* __restrict__ d2) {
   if (blockIdx.y > blockIdx.x) return;   // lower-triangle tile: written by its mirror
-  __shared__ float A[16][65], B[16][65];   // [component][row]
+  __shared__ float A[16][129], B[16][129];   // [component][row]
   const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-  const int i0 = blockIdx.y * 64, j0 = blockIdx.x * 64;
-  float acc[4][4] = {};
+  const int i0 = blockIdx.y * 128, j0 = blockIdx.x * 128;
+  float acc[8][8] = {};
   for (int k0 = 0; k0 < dim; k0 += 16) {
-    for (int e = threadIdx.x; e < 16 * 64; e += 256) {   // coalesced over the components
+    for (int e = threadIdx.x; e < 16 * 128; e += 256) {   // coalesced over the components
       const int rr = e / 16, kk = e % 16;
       A[kk][rr] = (i0 + rr < n && k0 + kk < dim) ? pv[(size_t)(i0 + rr) * dim + k0 + kk] : 0.f;
       B[kk][rr] = (j0 + rr < n && k0 + kk < dim) ? pv[(size_t)(j0 + rr) * dim + k0 + kk] : 0.f;
     }
     __syncthreads();
-#pragma unroll
+#pragma unroll 4
     for (int kk = 0; kk < 16; ++kk) {
-      float a[4], bb[4];
+      float a[8], bb[8];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < 8; ++u) {
         a[u] = A[kk][ty + 16 * u];
         bb[u] = B[kk][tx + 16 * u];
       }
 #pragma unroll
-      for (int u = 0; u < 4; ++u)
+      for (int u = 0; u < 8; ++u)
 #pragma unroll
-        for (int v = 0; v < 4; ++v) {
+        for (int v = 0; v < 8; ++v) {
           const float dd = a[u] - bb[v];
           acc[u][v] = fmaf(dd, dd, acc[u][v]);
         }
@@ -660,15 +663,26 @@ static __global__ void __launch_bounds__(256) k_mfd_dist(const float* __restrict
     __syncthreads();
   }
 #pragma unroll
-  for (int u = 0; u < 4; ++u)
+  for (int u = 0; u < 8; ++u)
 #pragma unroll
-    for (int v = 0; v < 4; ++v) {
+    for (int v = 0; v < 8; ++v) {
       const int i = i0 + ty + 16 * u, j = j0 + tx + 16 * v;
-      if (i < n && j < n) {
-        d2[(size_t)i * n + j] = acc[u][v];
-        d2[(size_t)j * n + i] = acc[u][v];
-      }
+      if (i < n && j < n) d2[(size_t)i * n + j] = acc[u][v];
     }
+  if (blockIdx.x == blockIdx.y) return;   // diagonal tile: the rows above already hold it
+  // mirror d2[j][i]: 16 tile columns at a time transposed through shared memory (coalesced rows)
+#pragma unroll
+  for (int v = 0; v < 8; ++v) {
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < 8; ++u) A[tx][ty + 16 * u] = acc[u][v];   // A[col][row]
+    __syncthreads();
+    for (int e = threadIdx.x; e < 16 * 128; e += 256) {
+      const int cc = e / 128, rr = e % 128;
+      const int j = j0 + cc + 16 * v, i = i0 + rr;
+      if (i < n && j < n) d2[(size_t)j * n + i] = A[cc][rr];
+    }
+  }
 }
 
 // Radix select of the nonzero strict-upper-triangle d2 bits, 11 + 11 + 10 bits: pass 0 counts
@@ -677,10 +691,12 @@ static __global__ void __launch_bounds__(256) k_mfd_dist(const float* __restrict
 // bins), merged with one global atomic per non-empty bin.
 static __global__ void __launch_bounds__(256) k_mfd_hist(const float* __restrict__ d2, int n, int pass,
                                                          const unsigned* __restrict__ pre_dev,
-                                                         unsigned* __restrict__ hist) {
-  __shared__ unsigned sh[2048];
-  const unsigned pre = pass > 0 ? *pre_dev : 0u;
-  for (int i = threadIdx.x; i < 2048; i += blockDim.x) sh[i] = 0u;
+                                                         unsigned* __restrict__ hist0, unsigned* __restrict__ hist1) {
+  // pass 0: one histogram (hist0); passes 1, 2: the two middle order statistics' prefixes
+  // pre_dev[0], pre_dev[1] counted together (hist0, hist1)
+  __shared__ unsigned sh[2][2048];
+  const unsigned pre0 = pass > 0 ? pre_dev[0] : 0u, pre1 = pass > 0 ? pre_dev[1] : 0u;
+  for (int i = threadIdx.x; i < 2 * 2048; i += blockDim.x) sh[i >> 11][i & 2047] = 0u;
   __syncthreads();
   const int shift = pass == 0 ? 21 : pass == 1 ? 10 : 0;
   const unsigned mask = pass == 2 ? 0x3FFu : 0x7FFu;
@@ -689,12 +705,20 @@ static __global__ void __launch_bounds__(256) k_mfd_hist(const float* __restrict
     for (int j = i + 1 + (int)threadIdx.x; j < n; j += blockDim.x) {
       const unsigned b = __float_as_uint(d2[(size_t)i * n + j]);
       if (b == 0u) continue;
-      if (pass > 0 && (b >> pshift) != pre) continue;
-      atomicAdd(&sh[(b >> shift) & mask], 1u);
+      const unsigned bin = (b >> shift) & mask;
+      if (pass == 0) {
+        atomicAdd(&sh[0][bin], 1u);
+      } else {
+        const unsigned pb = b >> pshift;
+        if (pb == pre0) atomicAdd(&sh[0][bin], 1u);
+        if (pb == pre1) atomicAdd(&sh[1][bin], 1u);
+      }
     }
   __syncthreads();
-  for (int i = threadIdx.x; i < 2048; i += blockDim.x)
-    if (sh[i]) atomicAdd(&hist[i], sh[i]);
+  for (int i = threadIdx.x; i < 2048; i += blockDim.x) {
+    if (sh[0][i]) atomicAdd(&hist0[i], sh[0][i]);
+    if (pass > 0 && sh[1][i]) atomicAdd(&hist1[i], sh[1][i]);
+  }
 }
 
 // W[i][j] = exp(-d2 / sigma2) (i != j), 0 on the diagonal; deg[i] = sum_j W[i][j] in a fixed order
