@@ -345,10 +345,10 @@ static mrf_status step_impl(mrf_llr h, mrf_plan plan, const void* x, const void*
     MRF_TRY(manifold_G(h, xcoef ? xcoef : h->YX, st));
     if (lambda1 > 0.f) {
       if (h->r <= 16)
-        mfd::k_mfd_apply<16><<<(unsigned)((V + 255) / 256), 256, 0, st>>>(h->Y, h->Qm, h->Gm, h->deg, h->corners, h->nc,
+        mfd::k_mfd_apply<16><<<(unsigned)(((long long)V * h->r + 255) / 256), 256, 0, st>>>(h->Y, h->Qm, h->Gm, h->deg, h->corners, h->nc,
                                                                            h->N, h->p, h->r, mu * lambda1);
       else
-        mfd::k_mfd_apply<32><<<(unsigned)((V + 255) / 256), 256, 0, st>>>(h->Y, h->Qm, h->Gm, h->deg, h->corners, h->nc,
+        mfd::k_mfd_apply<32><<<(unsigned)(((long long)V * h->r + 255) / 256), 256, 0, st>>>(h->Y, h->Qm, h->Gm, h->deg, h->corners, h->nc,
                                                                            h->N, h->p, h->r, mu * lambda1);
       MRF_TRY(check_launch("k_mfd_apply"));
     }
@@ -444,10 +444,10 @@ static mrf_status sub_step(mrf_llr_s* h, float mu, float lambda1, float lambda2,
     MRF_TRY(manifold_ws(h));
     MRF_TRY(manifold_G(h, h->xcv, st));
     if (h->r <= 16)
-      mfd::k_mfd_apply<16><<<(unsigned)((V + 255) / 256), 256, 0, st>>>(h->Y, h->Qm, h->Gm, h->deg, h->corners, h->nc,
+      mfd::k_mfd_apply<16><<<(unsigned)(((long long)V * h->r + 255) / 256), 256, 0, st>>>(h->Y, h->Qm, h->Gm, h->deg, h->corners, h->nc,
                                                                          h->N, h->p, h->r, mu * lambda1);
     else
-      mfd::k_mfd_apply<32><<<(unsigned)((V + 255) / 256), 256, 0, st>>>(h->Y, h->Qm, h->Gm, h->deg, h->corners, h->nc,
+      mfd::k_mfd_apply<32><<<(unsigned)(((long long)V * h->r + 255) / 256), 256, 0, st>>>(h->Y, h->Qm, h->Gm, h->deg, h->corners, h->nc,
                                                                          h->N, h->p, h->r, mu * lambda1);
     MRF_TRY(check_launch("k_mfd_apply"));
   }

@@ -755,18 +755,20 @@ static __global__ void k_mfd_gather(const float2* __restrict__ YX, const int* __
 
 // Y[v] -= scale * sum_{q covering v} (deg_q Qm_q[v] - G_q[v])   (Q^*(Q(X) L) in coefficients);
 // pen[q-block]: per-block partial of Re sum_q <Qm_q, deg_q Qm_q - G_q> (the trace penalty) when q0 < 0
+// thread = (voxel v, coefficient i): consecutive threads read consecutive words of a patch block
+// (coalesced); the covering patches are visited in increasing (qy, qx) order (deterministic).
+// R is unused (kept for the launch sites' dispatch on r).
 template <int R>
 __global__ void __launch_bounds__(256) k_mfd_apply(float2* __restrict__ Y, const float2* __restrict__ Qm,
                                                    const float2* __restrict__ G, const float* __restrict__ deg,
                                                    const int* __restrict__ corners, int nc, int N, int p, int r,
                                                    float scale) {
   const int V = N * N;
-  const int v = blockIdx.x * blockDim.x + threadIdx.x;
-  if (v >= V) return;
+  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (t >= (long long)V * r) return;
+  const int v = (int)(t / r), i = (int)(t % r);
   const int vy = v / N, vx = v % N, np = p * p;
-  float2 acc[R];
-#pragma unroll
-  for (int i = 0; i < R; ++i) acc[i] = make_float2(0.f, 0.f);
+  float2 acc = make_float2(0.f, 0.f);
   for (int qy = 0; qy < nc; ++qy) {
     const int cy = __ldg(corners + qy);
     if (vy < cy || vy >= cy + p) continue;
@@ -775,24 +777,16 @@ __global__ void __launch_bounds__(256) k_mfd_apply(float2* __restrict__ Y, const
       if (vx < cx || vx >= cx + p) continue;
       const int q = qy * nc + qx;
       const float dq = __ldg(deg + q);
-      const size_t o = ((size_t)q * np + (size_t)(vy - cy) * p + (vx - cx)) * r;
-#pragma unroll
-      for (int i = 0; i < R; ++i)
-        if (i < r) {
-          const float2 a = __ldg(Qm + o + i), g = __ldg(G + o + i);
-          acc[i].x += dq * a.x - g.x;
-          acc[i].y += dq * a.y - g.y;
-        }
+      const size_t o = ((size_t)q * np + (size_t)(vy - cy) * p + (vx - cx)) * r + i;
+      const float2 a = __ldg(Qm + o), g = __ldg(G + o);
+      acc.x += dq * a.x - g.x;
+      acc.y += dq * a.y - g.y;
     }
   }
-#pragma unroll
-  for (int i = 0; i < R; ++i)
-    if (i < r) {
-      float2 y = Y[(size_t)v * r + i];
-      y.x -= scale * acc[i].x;
-      y.y -= scale * acc[i].y;
-      Y[(size_t)v * r + i] = y;
-    }
+  float2 y = Y[t];
+  y.x -= scale * acc.x;
+  y.y -= scale * acc.y;
+  Y[t] = y;
 }
 
 // per-patch Re <Qm_q, deg_q Qm_q - G_q> (trace penalty terms), one block per patch, fixed order
