@@ -453,14 +453,9 @@ static mrf_status sub_step(mrf_llr_s* h, float mu, float lambda1, float lambda2,
   }
   MRF_TRY(svt(h, h->Y, 1.f / beta, st));
   const float gamma = mu * lambda2 * beta;
-  const unsigned gv = (unsigned)((V + 31) / 32);
-  if (h->r <= 16)
-    llr::k_llr_update<16><<<gv, 256, 0, st>>>(h->Y, h->P, h->corners, h->nc, h->N, h->p, h->r, h->dT, h->L, gamma,
-                                              nullptr, h->xcv, h->xcr);
-  else
-    llr::k_llr_update<32><<<gv, 256, 0, st>>>(h->Y, h->P, h->corners, h->nc, h->N, h->p, h->r, h->dT, h->L, gamma,
-                                              nullptr, h->xcv, h->xcr);
-  return check_launch("k_llr_update");
+  llr::k_llr_update_coef<<<(unsigned)(((long long)V * h->r + 255) / 256), 256, 0, st>>>(
+      h->Y, h->P, h->corners, h->nc, h->N, h->p, h->r, gamma, h->xcv, h->xcr);
+  return check_launch("k_llr_update_coef");
 }
 
 // cost(n) in basis coordinates: zs = P_S A^H A x (kept for the next step),

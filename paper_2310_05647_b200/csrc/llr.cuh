@@ -377,6 +377,40 @@ __global__ void __launch_bounds__(256) k_llr_update(const float2* __restrict__ Y
   }
 }
 
+// Coefficient-only Eq. 21 update (basis-coordinate loop): thread = (voxel v, coefficient i),
+// xc = (Y + gamma sum_{q covering v} P_q[v]) / (1 + gamma c(v)) with the covering patches in
+// increasing (qy, qx) order (the same arithmetic as k_llr_update); writes xcv [V][r] and xcr [r][V].
+static __global__ void __launch_bounds__(256) k_llr_update_coef(const float2* __restrict__ Y,
+                                                                const float2* __restrict__ P,
+                                                                const int* __restrict__ corners, int nc, int N, int p,
+                                                                int r, float gamma, float2* __restrict__ xcv,
+                                                                float2* __restrict__ xcr) {
+  const int V = N * N;
+  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (t >= (long long)V * r) return;
+  const int v = (int)(t / r), i = (int)(t % r);
+  const int vy = v / N, vx = v % N;
+  float2 acc = make_float2(0.f, 0.f);
+  int cnt = 0;
+  for (int qy = 0; qy < nc; ++qy) {
+    const int cy = __ldg(corners + qy);
+    if (vy < cy || vy >= cy + p) continue;
+    for (int qx = 0; qx < nc; ++qx) {
+      const int cx = __ldg(corners + qx);
+      if (vx < cx || vx >= cx + p) continue;
+      const float2 u = __ldg(P + (((size_t)(qy * nc + qx) * p + (vy - cy)) * p + (vx - cx)) * r + i);
+      acc.x += u.x;
+      acc.y += u.y;
+      ++cnt;
+    }
+  }
+  const float inv = 1.f / (1.f + gamma * (float)cnt);
+  const float2 y = __ldg(Y + t);
+  const float2 xc = make_float2((y.x + gamma * acc.x) * inv, (y.y + gamma * acc.y) * inv);
+  xcv[t] = xc;
+  xcr[(size_t)i * V + v] = xc;
+}
+
 // part[block] = sum |a - b|^2 over a grid-stride slice (float64; fixed grid, so the partials and
 // their host sum are deterministic)
 static __global__ void __launch_bounds__(256) k_llr_resid(const float2* __restrict__ a, const float2* __restrict__ b,
