@@ -44,9 +44,6 @@ struct mrf_llr_s {
   // spectra workspaces [r][C][G*G], zs = P_S A^H A x and bv = P_S A^H b coefficients
   float2 *Ksn = nullptr, *spa = nullptr, *spb = nullptr, *zs = nullptr, *bv = nullptr;
   size_t sn_bytes = 0;
-  // per-patch eigenvector caches of the step's SVT and of the cost's singular values (warm starts)
-  double2 *wc_step = nullptr, *wc_cost = nullptr;
-  bool wc_step_ok = false, wc_cost_ok = false;
   // manifold term (mrf_llr_laplacian)
   bool has_lap = false;
   float* W = nullptr;         // [n][n] similarity weights (Eq. 8), first the squared distances
@@ -75,7 +72,7 @@ static void llr_free(mrf_llr_s* h) {
   for (void* v : {(void*)h->sel, (void*)h->dT, (void*)h->corners, (void*)h->Y, (void*)h->P, (void*)h->nx, (void*)h->nuc, (void*)h->W,
                   (void*)h->deg, (void*)h->pv, (void*)h->hist, (void*)h->stats, (void*)h->YX, (void*)h->Qm,
                   (void*)h->Gm, (void*)h->pen, (void*)h->Wh, (void*)h->Wl, (void*)h->Qh, (void*)h->Ql, (void*)h->yb, (void*)h->part, (void*)h->rhs, (void*)h->x2, (void*)h->xcv, (void*)h->xcr, (void*)h->Ksn,
-                  (void*)h->spa, (void*)h->spb, (void*)h->zs, (void*)h->bv, (void*)h->wc_step, (void*)h->wc_cost})
+                  (void*)h->spa, (void*)h->spb, (void*)h->zs, (void*)h->bv})
     if (v) cudaFree(v);
   delete h;
 }
@@ -130,12 +127,9 @@ static mrf_status coefs(mrf_llr_s* h, const float2* x, const float2* nx, const f
 // per-patch SVT of the coefficient blocks of Y (nuclear norms into h->nuc, thresholded blocks into h->P)
 static mrf_status svt(mrf_llr_s* h, const float2* Ysrc, float tau, cudaStream_t st) {
   const int nq = h->nc * h->nc, ppb = llr::kSvtThreads / 32;
-  const bool cost = std::isinf(tau);   // singular values only (the cost), with its own W cache
-  double2* wc = cost ? h->wc_cost : h->wc_step;
-  bool& ok = cost ? h->wc_cost_ok : h->wc_step_ok;
+  const bool cost = std::isinf(tau);   // singular values only (the cost): eigenvalues, no vectors
   llr::k_llr_svt<<<(unsigned)((nq + ppb - 1) / ppb), llr::kSvtThreads, svt_smem(h->r), st>>>(
-      Ysrc, h->corners, h->nc, h->N, h->p, h->r, tau, nq, cost ? nullptr : h->P, h->nuc, wc, ok ? 1 : 0);
-  ok = true;
+      Ysrc, h->corners, h->nc, h->N, h->p, h->r, tau, nq, cost ? nullptr : h->P, h->nuc);
   return check_launch("k_llr_svt");
 }
 
@@ -210,8 +204,6 @@ mrf_status mrf_llr_create(mrf_dict dict, int N, int p, int s, mrf_llr* out) {
             cudaMalloc((void**)&h->nuc, nq * sizeof(double)) == cudaSuccess &&
             cudaMalloc((void**)&h->xcv, V * h->r * sizeof(float2)) == cudaSuccess &&
             cudaMalloc((void**)&h->xcr, V * h->r * sizeof(float2)) == cudaSuccess &&
-            cudaMalloc((void**)&h->wc_step, nq * h->r * h->r * sizeof(double2)) == cudaSuccess &&
-            cudaMalloc((void**)&h->wc_cost, nq * h->r * h->r * sizeof(double2)) == cudaSuccess &&
             cudaMalloc((void**)&h->part, 4 * (size_t)kStatBlocks * sizeof(double)) == cudaSuccess &&
             cudaMallocHost((void**)&h->hsum, (4 * (size_t)kStatBlocks + 4 * nq) * sizeof(double)) == cudaSuccess;
   h->hsum_cap = 4 * (size_t)kStatBlocks + 4 * nq;

@@ -104,7 +104,7 @@ __global__ void __launch_bounds__(32 * coef_groups<R>()) k_llr_coef(const float2
 // Shared memory per warp: svt_warp_bytes(r).
 __host__ __device__ constexpr int svt_rp(int r) { return (r + 1) & ~1; }
 __host__ __device__ constexpr size_t svt_warp_bytes(int r) {
-  return (size_t)3 * svt_rp(r) * svt_rp(r) * 16 + (size_t)svt_rp(r) / 2 * 32 + ((size_t)r * r * 8 + 15) / 16 * 16;
+  return (size_t)2 * svt_rp(r) * svt_rp(r) * 16 + (size_t)svt_rp(r) / 2 * 32 + ((size_t)r * r * 8 + 15) / 16 * 16;
 }
 
 __device__ __forceinline__ double2 zmul(double2 a, double2 b) {
@@ -113,20 +113,19 @@ __device__ __forceinline__ double2 zmul(double2 a, double2 b) {
 
 static __global__ void __launch_bounds__(kSvtThreads) k_llr_svt(const float2* __restrict__ Y, const int* __restrict__ corners,
                                                           int nc, int N, int p, int r, float tau, int nq,
-                                                          float2* __restrict__ P, double* __restrict__ nuc,
-                                                          double2* __restrict__ Wc, int warm) {
-  // Wc (nullable): [nq][r][r] eigenvector cache.  warm: start the Jacobi from the cached W (the
-  // Gram matrices of successive iterations differ little, so W^H G W is nearly diagonal and a
-  // sweep or two converge it); the final W is written back.
+                                                          float2* __restrict__ P, double* __restrict__ nuc) {
+  // P == nullptr: singular values only (eigenvalues of the Gram matrix, no eigenvectors).
+  // (A warm start from cached eigenvectors of the previous iteration was measured: it does not
+  // reduce the sweeps inside the MS-LLR loop.)
   extern __shared__ __align__(16) unsigned char llr_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int q = blockIdx.x * (kSvtThreads / 32) + warp;
   if (q >= nq) return;   // warp-uniform
   const int rp = svt_rp(r), half = rp / 2;
+  const bool vecs = P != nullptr;   // eigenvectors needed
   double2* A = reinterpret_cast<double2*>(llr_raw + (size_t)warp * svt_warp_bytes(r));   // [rp][rp]
   double2* Wm = A + rp * rp;                                                             // [rp][rp]
-  double2* Tb = Wm + rp * rp;                                                            // [rp][rp] scratch
-  double4* rot = reinterpret_cast<double4*>(Tb + rp * rp);                               // [half] (c, s, e)
+  double4* rot = reinterpret_cast<double4*>(Wm + rp * rp);                               // [half] (c, s, e)
   float2* M = reinterpret_cast<float2*>(rot + half);                                     // [r][r]
   const int qy = q / nc, qx = q % nc;
   const int y0 = corners[qy], x0 = corners[qx];
@@ -157,34 +156,6 @@ static __global__ void __launch_bounds__(kSvtThreads) k_llr_svt(const float2* __
     Wm[e] = make_double2(i == j ? 1.0 : 0.0, 0.0);
   }
   for (int o = 16; o > 0; o >>= 1) tr += __shfl_xor_sync(0xffffffffu, tr, o);
-  double2* Wq = Wc ? Wc + (size_t)q * r * r : nullptr;
-  if (Wq && warm) {   // A <- Wp^H A Wp, W <- Wp
-    __syncwarp();
-    for (int e = lane; e < r * r; e += 32) Wm[(e / r) * rp + e % r] = Wq[e];
-    __syncwarp();
-    for (int e = lane; e < r * r; e += 32) {   // T = A Wp
-      const int i = e / r, j = e % r;
-      double2 acc = make_double2(0.0, 0.0);
-      for (int k = 0; k < r; ++k) {
-        const double2 t = zmul(A[i * rp + k], Wm[k * rp + j]);
-        acc.x += t.x;
-        acc.y += t.y;
-      }
-      Tb[i * rp + j] = acc;
-    }
-    __syncwarp();
-    for (int e = lane; e < r * r; e += 32) {   // A = Wp^H T
-      const int i = e / r, j = e % r;
-      double2 acc = make_double2(0.0, 0.0);
-      for (int k = 0; k < r; ++k) {
-        const double2 w = Wm[k * rp + i];
-        const double2 t = zmul(make_double2(w.x, -w.y), Tb[k * rp + j]);
-        acc.x += t.x;
-        acc.y += t.y;
-      }
-      A[i * rp + j] = acc;
-    }
-  }
   // |g| <= 1e-14 tr is zero at the scale of ||Y_q||_F^2: the eigenvalues then carry an absolute
   // error <= ~1e-14 ||Y_q||_F^2, and M = W F W^H an error ~1e-14 ||Y_q||_F^2 / tau^2
   const double floor_g = 1e-14 * tr;
@@ -236,7 +207,9 @@ static __global__ void __launch_bounds__(kSvtThreads) k_llr_svt(const float2* __
       __syncwarp();
       // columns a, b of A and of W: X[k][a] <- c X[k][a] + s conj(e) X[k][b],
       // X[k][b] <- c X[k][b] - s e X[k][a]
-      for (int mk = g; mk < 2 * half; mk += G) {
+      // (eigenvalues only -- no P -- skip W: only the A columns)
+      const int mstep = vecs ? 1 : 2;
+      for (int mk = g * mstep; mk < 2 * half; mk += G * mstep) {
         const double4 R = rot[mk >> 1];
         if (R.y == 0.0 || c >= r) continue;
         const int2 ab = pr[mk >> 1];
@@ -261,8 +234,6 @@ static __global__ void __launch_bounds__(kSvtThreads) k_llr_svt(const float2* __
     }
     if (!__any_sync(0xffffffffu, big)) break;
   }
-  if (Wq)
-    for (int e = lane; e < r * r; e += 32) Wq[e] = Wm[(e / r) * rp + e % r];
   // sigma_j = sqrt(lambda_j); f_j = max(1 - tau / sigma_j, 0) (kept in the rot scratch)
   double* f = reinterpret_cast<double*>(rot);
   double sig = 0.0;
