@@ -109,3 +109,20 @@ def test_null_arguments(binding):
     assert binding.lib.mrf_dc_cg(None, None, None, ctypes.c_float(0.0), 1, ctypes.c_float(0.0), None, None, None) == 1
     assert binding.lib.mrf_plan_destroy(None) == 1
     assert binding.lib.mrf_nccl_get_unique_id(None) == 1
+
+
+def test_binding_fails_loudly_without_the_library(tmp_path):
+    """The product path has no CPU fallback: importing the binding without libmrfnufft.so raises."""
+    import shutil
+    import subprocess
+    import sys
+    pkg = tmp_path / "paper_2310_05647_b200"
+    pkg.mkdir()
+    src = os.path.join(ROOT, "paper_2310_05647_b200")
+    for name in ("__init__.py", "binding.py", "sharding.py"):
+        if os.path.exists(os.path.join(src, name)):
+            shutil.copy(os.path.join(src, name), pkg / name)
+    code = "import paper_2310_05647_b200.binding"
+    out = subprocess.run([sys.executable, "-c", code], cwd=tmp_path, capture_output=True, text=True)
+    assert out.returncode != 0
+    assert "ImportError" in out.stderr and "not built" in out.stderr
