@@ -228,6 +228,16 @@ mrf_status mrf_dict_match_coef(mrf_dict dict, const void* u, long long V, int* i
  * basis is copied.  Errors: MRF_EINVAL, MRF_ENOMEM, MRF_ECUDA. */
 typedef struct mrf_llr_s* mrf_llr;
 mrf_status mrf_llr_create(mrf_dict dict, int N, int p, int s, mrf_llr* out);
+/* The same with a caller-supplied basis: HOST [r][L] complex64 with orthonormal rows (copied),
+ * 1 <= r <= 32.  Phi_D inside mrf_msllr_solve then always runs on the frames. */
+mrf_status mrf_llr_create_basis(const void* basis, int r, int L, int N, int p, int s, int device, mrf_llr* out);
+
+/* The subspace normal operator in basis coordinates on a MRF_NORMAL_TOEPLITZ plan: for
+ * x = sum_i u_i d_i (u DEVICE [r][N][N] complex64), z = the coefficients of P_S A^H A x, DEVICE
+ * [r][N][N] (z_j = sum_i crop F^-1 [K_ji ⊙ F pad(u_i)], K_ji = sum_rho c^rho_ji T_rho; the exact
+ * (NUDFT) normal of the Toeplitz plan).  The mixing kernels are built on first use per plan.
+ * Errors: MRF_EINVAL (null, aliasing, not a Toeplitz plan, plan shape), MRF_ENOMEM, MRF_ECUDA. */
+mrf_status mrf_llr_subspace_normal(mrf_llr llr, mrf_plan plan, const void* u, void* z, void* stream);
 
 /* The graph Laplacian of the manifold term (Eqs. 7-11; reading 26) from Phi_D's maps:
  * params DEVICE [V][2] float (T1, T2) and pd DEVICE [V] float (mrf_dict_match outputs, V = N*N).

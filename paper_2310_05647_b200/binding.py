@@ -34,7 +34,7 @@ EXPORTED = [
     "mrf_adjoint_dcf", "mrf_dcf_weights", "mrf_dict_create", "mrf_dict_match", "mrf_dict_destroy",
     "mrf_dict_profile", "mrf_dict_profile_query", "mrf_dict_basis", "mrf_dict_basis_copy", "mrf_llr_create",
     "mrf_llr_step", "mrf_llr_destroy", "mrf_llr_laplacian", "mrf_llr_cost", "mrf_msllr_solve", "mrf_plan_wait",
-    "mrf_dict_match_coef",
+    "mrf_dict_match_coef", "mrf_llr_create_basis", "mrf_llr_subspace_normal",
 ]
 
 
@@ -106,6 +106,8 @@ def _load() -> ctypes.CDLL:
         "mrf_dict_basis": ([vp, ctypes.c_double, ci, ctypes.POINTER(ci)], ci),
         "mrf_dict_basis_copy": ([vp, vp], ci),
         "mrf_llr_create": ([vp, ci, ci, ci, ctypes.POINTER(vp)], ci),
+        "mrf_llr_create_basis": ([vp, ci, ci, ci, ci, ci, ci, ctypes.POINTER(vp)], ci),
+        "mrf_llr_subspace_normal": ([vp, vp, vp, vp, vp], ci),
         "mrf_llr_step": ([vp, vp, vp, vp, cf, cf, cf, cf, vp, ctypes.POINTER(ctypes.c_double),
                           ctypes.POINTER(ctypes.c_double), vp], ci),
         "mrf_llr_laplacian": ([vp, vp, vp, ctypes.c_double, ctypes.POINTER(ctypes.c_double),
@@ -432,6 +434,31 @@ class LLR:
         _check(lib.mrf_llr_create(dictionary._h, int(N), int(p), int(s), ctypes.byref(h)))
         self._h = h
         self.N, self.L = int(N), dictionary.L
+        self.r = None
+
+    @classmethod
+    def from_basis(cls, basis, N: int, p: int = 11, s: int = 5, device: Optional[int] = None) -> "LLR":
+        """An operator with a caller-supplied basis d ([r][L] complex, orthonormal rows; mrf_llr_create_basis)."""
+        d = np.ascontiguousarray(np.asarray(basis, dtype=np.complex64))
+        if d.ndim != 2:
+            raise ValueError("basis must be [r][L]")
+        self = cls.__new__(cls)
+        h = ctypes.c_void_p()
+        dev = torch.cuda.current_device() if device is None else device
+        _check(lib.mrf_llr_create_basis(d.ctypes.data_as(ctypes.c_void_p), d.shape[0], d.shape[1], int(N), int(p),
+                                        int(s), dev, ctypes.byref(h)))
+        self._h = h
+        self.N, self.L, self.r = int(N), d.shape[1], d.shape[0]
+        return self
+
+    def subspace_normal(self, plan: "Plan", u, z=None):
+        """Coefficients of P_S A^H A (sum_i u_i d_i) for u [r][N][N] on a Toeplitz plan (mrf_llr_subspace_normal)."""
+        if not (isinstance(u, torch.Tensor) and u.is_cuda and u.dtype == torch.complex64 and u.is_contiguous()):
+            raise TypeError("u must be a contiguous CUDA complex64 tensor [r][N][N]")
+        z = torch.empty_like(u) if z is None else z
+        st = torch.cuda.current_stream(u.device).cuda_stream
+        _check(lib.mrf_llr_subspace_normal(self._h, plan._h, _ptr(u), _ptr(z), ctypes.c_void_p(st)))
+        return z
 
     def laplacian(self, params: torch.Tensor, pd: torch.Tensor, sigma2: float = 0.0):
         """Graph Laplacian from Phi_D's maps (params [V][2] T1/T2, pd [V]; CUDA float32).

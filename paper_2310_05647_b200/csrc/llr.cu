@@ -44,6 +44,7 @@ struct mrf_llr_s {
   // spectra workspaces [r][C][G*G], zs = P_S A^H A x and bv = P_S A^H b coefficients
   float2 *Ksn = nullptr, *spa = nullptr, *spb = nullptr, *zs = nullptr, *bv = nullptr;
   size_t sn_bytes = 0;
+  mrf_plan sn_plan = nullptr;             // plan the mixing kernels were built for
   // manifold term (mrf_llr_laplacian)
   bool has_lap = false;
   float* W = nullptr;         // [n][n] similarity weights (Eq. 8), first the squared distances
@@ -181,14 +182,14 @@ static mrf_status check_plan(mrf_llr_s* h, mrf_plan plan, const char* who) {
 
 extern "C" {
 
-mrf_status mrf_llr_create(mrf_dict dict, int N, int p, int s, mrf_llr* out) {
-  if (!dict || !out || N < 2 || p < 1 || p > N || s < 1 || p * p > 1024)
-    return fail(MRF_EINVAL, "mrf_llr_create: invalid arguments");
-  if (!dict->rank) return fail(MRF_EINVAL, "mrf_llr_create: the dictionary has no basis (call mrf_dict_basis)");
+}  // extern "C"
+
+static mrf_status create_impl(const float2* basis_h, int r, int L, int device, unsigned gen, int N, int p, int s,
+                              mrf_llr* out) {
   *out = nullptr;
-  CUDA_TRY(cudaSetDevice(dict->device));
+  CUDA_TRY(cudaSetDevice(device));
   auto* h = new mrf_llr_s();
-  h->N = N; h->L = dict->L; h->p = p; h->s = s; h->r = dict->rank; h->device = dict->device;
+  h->N = N; h->L = L; h->p = p; h->s = s; h->r = r; h->device = device;
   std::vector<int> c;   // patch corners 0, s, 2s, ... and N - p (reading 25)
   for (int v = 0; v + p <= N; v += s) c.push_back(v);
   if (c.back() != N - p) c.push_back(N - p);
@@ -207,15 +208,15 @@ mrf_status mrf_llr_create(mrf_dict dict, int N, int p, int s, mrf_llr* out) {
             cudaMalloc((void**)&h->part, 4 * (size_t)kStatBlocks * sizeof(double)) == cudaSuccess &&
             cudaMallocHost((void**)&h->hsum, (4 * (size_t)kStatBlocks + 4 * nq) * sizeof(double)) == cudaSuccess;
   h->hsum_cap = 4 * (size_t)kStatBlocks + 4 * nq;
-  h->basis_gen = dict->basis_gen;
-  h->basis_h = dict->basis_h;
+  h->basis_gen = gen;
+  h->basis_h.assign(basis_h, basis_h + (size_t)r * L);
   if (!ok) {
     llr_free(h);
     return fail(MRF_ENOMEM, "mrf_llr_create: device allocation failed");
   }
   std::vector<float2> dT((size_t)R * h->L, make_float2(0.f, 0.f));   // [L][R] from the [r][L] rows
   for (int i = 0; i < h->r; ++i)
-    for (int l = 0; l < h->L; ++l) dT[(size_t)l * R + i] = dict->basis_h[(size_t)i * h->L + l];
+    for (int l = 0; l < h->L; ++l) dT[(size_t)l * R + i] = basis_h[(size_t)i * h->L + l];
   cudaError_t e = cudaMemcpy(h->dT, dT.data(), dT.size() * sizeof(float2), cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMemcpy(h->corners, c.data(), c.size() * sizeof(int), cudaMemcpyHostToDevice);
   if (e == cudaSuccess)
@@ -229,6 +230,23 @@ mrf_status mrf_llr_create(mrf_dict dict, int N, int p, int s, mrf_llr* out) {
   }
   *out = h;
   return MRF_OK;
+}
+
+extern "C" {
+
+mrf_status mrf_llr_create(mrf_dict dict, int N, int p, int s, mrf_llr* out) {
+  if (!dict || !out || N < 2 || p < 1 || p > N || s < 1 || p * p > 1024)
+    return fail(MRF_EINVAL, "mrf_llr_create: invalid arguments");
+  if (!dict->rank) return fail(MRF_EINVAL, "mrf_llr_create: the dictionary has no basis (call mrf_dict_basis)");
+  return create_impl(dict->basis_h.data(), dict->rank, dict->L, dict->device, dict->basis_gen, N, p, s, out);
+}
+
+mrf_status mrf_llr_create_basis(const void* basis, int r, int L, int N, int p, int s, int device, mrf_llr* out) {
+  if (!basis || !out || r < 1 || r > llr::RMAX || L < 1 || N < 2 || p < 1 || p > N || s < 1 || p * p > 1024)
+    return fail(MRF_EINVAL, "mrf_llr_create_basis: invalid arguments");
+  // a caller-supplied basis never equals a dictionary's basis generation: Phi_D inside
+  // mrf_msllr_solve then runs on frames
+  return create_impl(reinterpret_cast<const float2*>(basis), r, L, device, ~0u, N, p, s, out);
 }
 
 
@@ -479,6 +497,36 @@ static mrf_status sub_cost(mrf_llr_s* h, mrf_plan plan, double b2, float lambda1
   return MRF_OK;
 }
 
+// Subspace-normal workspaces (mixing kernels, spectra, zs, bv) sized for `plan`, and the mixing
+// kernels K for the operator's basis on the plan's PSF spectra (rebuilt when the plan changes or
+// `force`).
+static mrf_status ensure_sn(mrf_llr_s* h, mrf_plan plan, cudaStream_t st, bool force) {
+  int pN = 0, pL = 0, pC = 0, pdev = 0, pM = 0;
+  plan_dims(plan, &pN, &pL, &pC, &pdev, &pM);
+  const size_t E = (size_t)sn_elems(plan), r = (size_t)h->r, V = (size_t)h->N * h->N;
+  const size_t need = (r * (r + 1) / 2 * E + 2 * r * pC * E + 2 * r * V) * sizeof(float2);
+  if (h->sn_bytes < need) {
+    for (float2** p : {&h->Ksn, &h->spa, &h->spb, &h->zs, &h->bv}) {
+      if (*p) cudaFree(*p);
+      *p = nullptr;
+    }
+    h->sn_bytes = 0;
+    h->sn_plan = nullptr;
+    if (cudaMalloc((void**)&h->Ksn, r * (r + 1) / 2 * E * sizeof(float2)) != cudaSuccess ||
+        cudaMalloc((void**)&h->spa, r * pC * E * sizeof(float2)) != cudaSuccess ||
+        cudaMalloc((void**)&h->spb, r * pC * E * sizeof(float2)) != cudaSuccess ||
+        cudaMalloc((void**)&h->zs, r * V * sizeof(float2)) != cudaSuccess ||
+        cudaMalloc((void**)&h->bv, r * V * sizeof(float2)) != cudaSuccess)
+      return fail(MRF_ENOMEM, "subspace normal: workspace allocation failed");
+    h->sn_bytes = need;
+  }
+  if (force || h->sn_plan != plan) {
+    MRF_TRY(sn_build(plan, h->basis_h.data(), h->r, h->Ksn, st));
+    h->sn_plan = plan;
+  }
+  return MRF_OK;
+}
+
 extern "C" {
 
 mrf_status mrf_llr_step(mrf_llr h, mrf_plan plan, const void* x, const void* rhs, float mu, float lambda1,
@@ -525,23 +573,7 @@ mrf_status mrf_msllr_solve(mrf_llr h, mrf_dict dict, mrf_plan plan, const void* 
   if (sub) {
     int pN = 0, pL = 0, pC = 0, pdev = 0, pM = 0;
     plan_dims(plan, &pN, &pL, &pC, &pdev, &pM);
-    const size_t E = (size_t)sn_elems(plan), r = (size_t)h->r;
-    const size_t need = (r * (r + 1) / 2 * E + 2 * r * pC * E + 2 * r * V) * sizeof(float2);
-    if (h->sn_bytes < need) {
-      for (float2** p : {&h->Ksn, &h->spa, &h->spb, &h->zs, &h->bv}) {
-        if (*p) cudaFree(*p);
-        *p = nullptr;
-      }
-      h->sn_bytes = 0;
-      if (cudaMalloc((void**)&h->Ksn, r * (r + 1) / 2 * E * sizeof(float2)) != cudaSuccess ||
-          cudaMalloc((void**)&h->spa, r * pC * E * sizeof(float2)) != cudaSuccess ||
-          cudaMalloc((void**)&h->spb, r * pC * E * sizeof(float2)) != cudaSuccess ||
-          cudaMalloc((void**)&h->zs, r * V * sizeof(float2)) != cudaSuccess ||
-          cudaMalloc((void**)&h->bv, r * V * sizeof(float2)) != cudaSuccess)
-        return fail(MRF_ENOMEM, "mrf_msllr_solve: subspace workspace allocation failed");
-      h->sn_bytes = need;
-    }
-    MRF_TRY(sn_build(plan, h->basis_h.data(), h->r, h->Ksn, st));
+    MRF_TRY(ensure_sn(h, plan, st, true));   // rebuilt per solve (the plan may be a new one at the same address)
     const float2* rh = h->rhs;
     MRF_TRY(coefs(h, rh, rh, rh, 0.f, h->bv, nullptr, st));   // P_S A^H b coefficients
     const size_t ny = (size_t)pL * pC * pM;
@@ -617,6 +649,17 @@ mrf_status mrf_msllr_solve(mrf_llr h, mrf_dict dict, mrf_plan plan, const void* 
     info->lambda1 = lam1;
   }
   return MRF_OK;
+}
+
+mrf_status mrf_llr_subspace_normal(mrf_llr h, mrf_plan plan, const void* u, void* z, void* stream) {
+  if (!h || !plan || !u || !z) return fail(MRF_EINVAL, "mrf_llr_subspace_normal: null argument");
+  if (u == z) return fail(MRF_EINVAL, "mrf_llr_subspace_normal: z may not alias u");
+  if (!plan_toeplitz(plan)) return fail(MRF_EINVAL, "mrf_llr_subspace_normal: needs a plan with MRF_NORMAL_TOEPLITZ");
+  MRF_TRY(check_plan(h, plan, "mrf_llr_subspace_normal"));
+  CUDA_TRY(cudaSetDevice(h->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  MRF_TRY(ensure_sn(h, plan, st, false));
+  return sn_apply(plan, h->Ksn, h->r, (const float2*)u, (float2*)z, h->spa, h->spb, st);
 }
 
 mrf_status mrf_llr_destroy(mrf_llr h) {

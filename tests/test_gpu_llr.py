@@ -173,3 +173,51 @@ def test_manifold_term_against_the_oracle(binding):
     pl.close()
     op.close()
     dic.close()
+
+
+def _oracle_basis_problem(N=32, L=60, seed=11):
+    D = sd.surrogate_dictionary(L)
+    d_o = ol.basis(D, 0.9999, 32)                               # float64 SVD basis (the oracle's)
+    traj = synth.spiral_trajectory(512, 10, 8, 1.5)
+    return D, d_o, traj
+
+
+def test_subspace_normal_against_the_nudft(binding):
+    """mrf_llr_subspace_normal on a Toeplitz plan with the ORACLE's basis (mrf_llr_create_basis):
+    the coefficients of P_S A^H A (u d) against the plain-definition operator (NUDFT) in float64."""
+    N, L = 32, 60
+    D, d_o, traj = _oracle_basis_problem(N, L)
+    r = d_o.shape[0]
+    rng = np.random.default_rng([31, 1])
+    u = (rng.standard_normal((r, N, N)) + 1j * rng.standard_normal((r, N, N))).astype(np.complex64)
+    op = binding.LLR.from_basis(d_o, N, 7, 3)
+    pl = binding.Plan(N, traj, L, W=6, normal="toeplitz")
+    z = op.subspace_normal(pl, torch.from_numpy(u).cuda())
+    torch.cuda.synchronize()
+    X = np.einsum("il,iyx->lyx", d_o.astype(np.complex64).astype(np.complex128), u.astype(np.complex128))
+    n = on.nudft_adjoint(on.nudft_forward(X, traj, None), traj, None, N)
+    z_ref = np.einsum("il,lyx->iyx", np.conj(d_o.astype(np.complex64).astype(np.complex128)), n)
+    assert rel(z.cpu().numpy(), z_ref) <= 1e-5
+    with pytest.raises(binding.MrfError):
+        op.subspace_normal(binding.Plan(N, traj, L, W=6), torch.from_numpy(u).cuda())   # gridding plan
+    pl.close(), op.close()
+
+
+def test_llr_step_with_the_oracle_basis(binding):
+    """The LLR step with the oracle's basis (no basis difference between the two sides)."""
+    N, L, p, s = 32, 60, 7, 3
+    D, d_o, traj = _oracle_basis_problem(N, L)
+    x_true = synth.rank5_images(N, L, range(L), 7)
+    rhs = on.adjoint(on.forward(x_true, traj, None, 6), traj, None, N, 6)
+    mu, lam2, beta = 0.02, 0.1, 0.2
+    X_ref, _ = ol.llr_step(rhs, rhs, lambda v: on.normal(v, traj, None, 6), d_o.astype(np.complex64).astype(np.complex128),
+                           mu, lam2, beta, p, s)
+    op = binding.LLR.from_basis(d_o, N, p, s)
+    pl = binding.Plan(N, traj, L, W=6)
+    xd = torch.from_numpy(rhs.astype(np.complex64)).cuda()
+    xg, _, _ = op.step(pl, xd, xd, mu, lam2, beta)
+    torch.cuda.synchronize()
+    assert rel(xg.cpu().numpy(), X_ref) <= 1e-5
+    with pytest.raises(binding.MrfError):
+        binding.LLR.from_basis(np.zeros((0, L), np.complex64), N)
+    pl.close(), op.close()
