@@ -44,7 +44,7 @@ struct mrf_llr_s {
   // spectra workspaces [r][C][G*G], zs = P_S A^H A x and bv = P_S A^H b coefficients
   float2 *Ksn = nullptr, *spa = nullptr, *spb = nullptr, *zs = nullptr, *bv = nullptr;
   size_t sn_bytes = 0;
-  mrf_plan sn_plan = nullptr;             // plan the mixing kernels were built for
+  unsigned long long sn_plan = 0;         // serial of the plan the mixing kernels were built for
   // manifold term (mrf_llr_laplacian)
   bool has_lap = false;
   float* W = nullptr;         // [n][n] similarity weights (Eq. 8), first the squared distances
@@ -511,7 +511,7 @@ static mrf_status ensure_sn(mrf_llr_s* h, mrf_plan plan, cudaStream_t st, bool f
       *p = nullptr;
     }
     h->sn_bytes = 0;
-    h->sn_plan = nullptr;
+    h->sn_plan = 0;
     if (cudaMalloc((void**)&h->Ksn, r * (r + 1) / 2 * E * sizeof(float2)) != cudaSuccess ||
         cudaMalloc((void**)&h->spa, r * pC * E * sizeof(float2)) != cudaSuccess ||
         cudaMalloc((void**)&h->spb, r * pC * E * sizeof(float2)) != cudaSuccess ||
@@ -520,9 +520,9 @@ static mrf_status ensure_sn(mrf_llr_s* h, mrf_plan plan, cudaStream_t st, bool f
       return fail(MRF_ENOMEM, "subspace normal: workspace allocation failed");
     h->sn_bytes = need;
   }
-  if (force || h->sn_plan != plan) {
+  if (force || h->sn_plan != plan_serial(plan)) {
     MRF_TRY(sn_build(plan, h->basis_h.data(), h->r, h->Ksn, st));
-    h->sn_plan = plan;
+    h->sn_plan = plan_serial(plan);
   }
   return MRF_OK;
 }
@@ -573,7 +573,7 @@ mrf_status mrf_msllr_solve(mrf_llr h, mrf_dict dict, mrf_plan plan, const void* 
   if (sub) {
     int pN = 0, pL = 0, pC = 0, pdev = 0, pM = 0;
     plan_dims(plan, &pN, &pL, &pC, &pdev, &pM);
-    MRF_TRY(ensure_sn(h, plan, st, true));   // rebuilt per solve (the plan may be a new one at the same address)
+    MRF_TRY(ensure_sn(h, plan, st, false));   // built once per plan (plan serial)
     const float2* rh = h->rhs;
     MRF_TRY(coefs(h, rh, rh, rh, 0.f, h->bv, nullptr, st));   // P_S A^H b coefficients
     const size_t ny = (size_t)pL * pC * pM;

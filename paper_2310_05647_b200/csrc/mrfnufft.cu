@@ -8,6 +8,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <complex>
 #include <cstdio>
@@ -72,6 +73,7 @@ struct mrf_plan_s {
   int N = 0, G = 0, L = 0, M = 0, R = 0, C = 1, W = 0, S = 0, frame_offset = 0, recw = 0;
   unsigned flags = 0;
   int device = 0;
+  unsigned long long serial = 0;   // creation number (process-wide), identifies the plan
   int bf = 1;               // frames per batch
   int nsm = 148;            // SMs of the device
   bool adj_sep = false;      // k_adj_cols variant with the separate exchange buffer (one CTA per SM)
@@ -847,6 +849,7 @@ void mrf::plan_dims(mrf_plan pl, int* N, int* L, int* C, int* device, int* M) {
 // ---------------------------------------------------------------------------- subspace normal
 // (gridding.cuh k_sn_*; used by mrf_msllr_solve on Toeplitz plans, llr.cu)
 bool mrf::plan_toeplitz(mrf_plan pl) { return (pl->flags & MRF_NORMAL_TOEPLITZ) != 0 && pl->psf; }
+unsigned long long mrf::plan_serial(mrf_plan pl) { return pl->serial; }
 long long mrf::sn_elems(mrf_plan pl) { return (long long)pl->G * pl->G; }
 
 mrf_status mrf::sn_build(mrf_plan pl, const float2* basis_h, int r, float2* K, cudaStream_t st) {
@@ -985,6 +988,8 @@ mrf_status mrf_plan_create(const mrf_plan_desc* d, mrf_plan* out) {
   cudaStream_t st = (cudaStream_t)d->stream;
 
   mrf_plan_s* pl = new mrf_plan_s();
+  static std::atomic<unsigned long long> plan_counter{0};
+  pl->serial = ++plan_counter;
   pl->N = N; pl->G = G; pl->L = L; pl->M = M; pl->R = R; pl->C = C; pl->W = W; pl->S = G / SW;
   pl->recw = (2 + 2 * W + 3) & ~3;
   if (const char* e = std::getenv("MRF_DBG")) pl->dbg = std::atoi(e);
