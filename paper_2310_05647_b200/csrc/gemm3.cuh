@@ -51,6 +51,32 @@ __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t a, uint64_t b
       : "memory");
 }
 
+// 2D TMA load multicast to the CTAs of `mask` in the cluster (same smem offset, and complete_tx on
+// the mbarrier at the same offset in each)
+__device__ __forceinline__ void tma_load_2d_mc(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* b,
+                                               uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+      " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(saddr(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(saddr(b)), "h"(mask)
+      : "memory");
+}
+// tcgen05.commit arriving on the mbarrier at this offset in every CTA of `mask`
+__device__ __forceinline__ void mma_commit_mc(uint64_t* b, uint16_t mask) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                   saddr(b)),
+               "h"(mask)
+               : "memory");
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+
 __device__ __forceinline__ float tf32_hi(float x) {
   uint32_t r;
   asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
@@ -59,6 +85,11 @@ __device__ __forceinline__ float tf32_hi(float x) {
 
 // C [m_rows][ldc] fp32 (columns < n_cols written).  Tensor maps: ta_hi / ta_lo over A [m_rows][K]
 // (box 32 x BM), tb_hi / tb_lo over B [n_cols][K] (box 32 x BN); kblocks = ceil(K / 32).
+// MC: clusters of 2 CTAs take row tiles (2p, 2p + 1) of the same column tile; each loads half of the
+// B tile's rows and multicasts it to both (tb_* boxes of BN / 2 rows), halving the B traffic from L2;
+// a stage is refilled once both CTAs' MMAs have released it (multicast commits, empty count 2).
+// m_tiles must then be even (an extra row tile reads zeros and stores nothing).
+template <bool MC>
 __global__ void __launch_bounds__(THREADS, 1)
 k_g3_gemm(const __grid_constant__ CUtensorMap ta_hi, const __grid_constant__ CUtensorMap ta_lo,
           const __grid_constant__ CUtensorMap tb_hi, const __grid_constant__ CUtensorMap tb_lo, int m_tiles,
@@ -71,13 +102,19 @@ k_g3_gemm(const __grid_constant__ CUtensorMap ta_hi, const __grid_constant__ CUt
   uint64_t* tempty = tfull + 2;
   uint32_t* tbase = reinterpret_cast<uint32_t*>(tempty + 2);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  // unit u = (row tile u % m_tiles, column tile u / m_tiles): CTAs running together share column tiles
-  const int units = m_tiles * n_tiles;
+  // unit u = (row tile u % m_tiles, column tile u / m_tiles): CTAs running together share column tiles.
+  // MC: unit index over pairs, row tile 2 (u % (m_tiles / 2)) + rank
+  const int rank = MC ? (int)cluster_rank() : 0;
+  const int grid_units = MC ? (int)gridDim.x / 2 : (int)gridDim.x;
+  const int first = MC ? (int)blockIdx.x / 2 : (int)blockIdx.x;
+  const int mt_n = MC ? m_tiles / 2 : m_tiles;
+  const int units = mt_n * n_tiles;
+  auto unit_m0 = [&](int u) { return (MC ? 2 * (u % mt_n) + rank : u % mt_n) * BM; };
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       bar_init(&full[s], 1);
-      bar_init(&empty[s], 1);
+      bar_init(&empty[s], MC ? 2 : 1);
     }
     for (int a = 0; a < 2; ++a) {
       bar_init(&tfull[a], 1);
@@ -90,15 +127,16 @@ k_g3_gemm(const __grid_constant__ CUtensorMap ta_hi, const __grid_constant__ CUt
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   tc_fence_before();
-  __syncthreads();
+  if (MC) cluster_sync_all();   // the peer's multicasts land only after our barriers exist
+  else __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tbase;
 
   if (warp == 0 && lane == 0) {
     // ---- TMA producer
     int it = 0;
-    for (int u = blockIdx.x; u < units; u += gridDim.x) {
-      const int m0 = (u % m_tiles) * BM, n0 = (u / m_tiles) * BN;
+    for (int u = first; u < units; u += grid_units) {
+      const int m0 = unit_m0(u), n0 = (u / mt_n) * BN;
       for (int kb = 0; kb < kblocks; ++kb, ++it) {
         const int s = it % STAGES;
         unsigned char* st = base + s * STAGE_BYTES;
@@ -106,14 +144,20 @@ k_g3_gemm(const __grid_constant__ CUtensorMap ta_hi, const __grid_constant__ CUt
         bar_expect_tx(&full[s], STAGE_BYTES);
         tma_load_2d(st, &ta_hi, kb * BK, m0, &full[s]);
         tma_load_2d(st + A_BYTES, &ta_lo, kb * BK, m0, &full[s]);
-        tma_load_2d(st + 2 * A_BYTES, &tb_hi, kb * BK, n0, &full[s]);
-        tma_load_2d(st + 2 * A_BYTES + B_BYTES, &tb_lo, kb * BK, n0, &full[s]);
+        if constexpr (MC) {   // this CTA's half of the B rows, to both CTAs
+          const int off = rank * (B_BYTES / 2);
+          tma_load_2d_mc(st + 2 * A_BYTES + off, &tb_hi, kb * BK, n0 + rank * (BN / 2), &full[s], 0x3);
+          tma_load_2d_mc(st + 2 * A_BYTES + B_BYTES + off, &tb_lo, kb * BK, n0 + rank * (BN / 2), &full[s], 0x3);
+        } else {
+          tma_load_2d(st + 2 * A_BYTES, &tb_hi, kb * BK, n0, &full[s]);
+          tma_load_2d(st + 2 * A_BYTES + B_BYTES, &tb_lo, kb * BK, n0, &full[s]);
+        }
       }
     }
   } else if (warp == 1 && lane == 0) {
     // ---- MMA issuer
     int it = 0, j = 0;
-    for (int u = blockIdx.x; u < units; u += gridDim.x, ++j) {
+    for (int u = first; u < units; u += grid_units, ++j) {
       const int acc = j & 1, use = j >> 1;
       bar_wait(&tempty[acc], (use & 1) ^ 1);
       tc_fence_after();
@@ -131,7 +175,8 @@ k_g3_gemm(const __grid_constant__ CUtensorMap ta_hi, const __grid_constant__ CUt
           mma_tf32(td, sdesc(ah + o), sdesc(bl + o), 1u);
           mma_tf32(td, sdesc(ah + o), sdesc(bh + o), 1u);
         }
-        mma_commit(&empty[s]);   // frees the stage once these MMAs have read it
+        if constexpr (MC) mma_commit_mc(&empty[s], 0x3);   // both CTAs' producers refill this stage
+        else mma_commit(&empty[s]);   // frees the stage once these MMAs have read it
       }
       mma_commit(&tfull[acc]);   // accumulator complete
     }
@@ -140,8 +185,8 @@ k_g3_gemm(const __grid_constant__ CUtensorMap ta_hi, const __grid_constant__ CUt
     const int row = (warp - 4) * 32 + lane;
     const uint32_t lane_addr = (uint32_t)((warp - 4) * 32) << 16;
     int j = 0;
-    for (int u = blockIdx.x; u < units; u += gridDim.x, ++j) {
-      const int m = (u % m_tiles) * BM + row, n0 = (u / m_tiles) * BN;
+    for (int u = first; u < units; u += grid_units, ++j) {
+      const int m = unit_m0(u) + row, n0 = (u / mt_n) * BN;
       const int acc = j & 1, use = j >> 1;
       bar_wait(&tfull[acc], use & 1);
       __syncwarp();   // tcgen05.ld is .sync.aligned
@@ -168,7 +213,8 @@ k_g3_gemm(const __grid_constant__ CUtensorMap ta_hi, const __grid_constant__ CUt
     }
   }
   tc_fence_before();
-  __syncthreads();
+  if (MC) cluster_sync_all();   // no CTA leaves while its peer may still multicast into it
+  else __syncthreads();
   if (warp == 1) {
     __syncwarp();
     tc_fence_after();

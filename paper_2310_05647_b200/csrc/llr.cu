@@ -8,6 +8,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -63,6 +64,8 @@ struct mrf_llr_s {
   float *Wh = nullptr, *Wl = nullptr;   // [n][nK]
   float *Qh = nullptr, *Ql = nullptr;   // [2 p^2 r][nK] (Qm transposed)
   CUtensorMap tWh, tWl, tQh, tQl;
+  CUtensorMap tQh2, tQl2;                 // the same with BN / 2-row boxes (multicast halves)
+  bool g3_mc = true;                      // clusters of 2 with multicast B tiles (MRF_G3_MC=0: off)
 };
 
 static void llr_free(mrf_llr_s* h) {
@@ -94,6 +97,8 @@ static mrf_status manifold_ws(mrf_llr_s* h) {
   if (!ok) return fail(MRF_ENOMEM, "manifold workspace allocation failed");
   MRF_TRY(tmap_2d(&h->tQh, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, h->Qh, n, 2 * blk, (uint64_t)h->nK * 4, g3::BK, g3::BN));
   MRF_TRY(tmap_2d(&h->tQl, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, h->Ql, n, 2 * blk, (uint64_t)h->nK * 4, g3::BK, g3::BN));
+  MRF_TRY(tmap_2d(&h->tQh2, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, h->Qh, n, 2 * blk, (uint64_t)h->nK * 4, g3::BK, g3::BN / 2));
+  MRF_TRY(tmap_2d(&h->tQl2, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, h->Ql, n, 2 * blk, (uint64_t)h->nK * 4, g3::BK, g3::BN / 2));
   return MRF_OK;
 }
 
@@ -104,9 +109,28 @@ static mrf_status manifold_G(mrf_llr_s* h, const float2* coef, cudaStream_t st) 
   const int M2 = 2 * blk;   // G [n][M2] = W [n][n] Qm [n][M2]: A = W (K-major), B = Qm^T [M2][n]
   const dim3 gs((unsigned)((M2 + 31) / 32), (unsigned)((n + 31) / 32));
   g3::k_g3_split<true><<<gs, 256, 0, st>>>(reinterpret_cast<const float*>(h->Qm), n, M2, M2, h->Qh, h->Ql, h->nK);
-  const int mt = (n + g3::BM - 1) / g3::BM, nt = (M2 + g3::BN - 1) / g3::BN;
-  g3::k_g3_gemm<<<std::min(mt * nt, h->sms), g3::THREADS, g3::SMEM, st>>>(
-      h->tWh, h->tWl, h->tQh, h->tQl, mt, nt, (n + g3::BK - 1) / g3::BK, n, M2, reinterpret_cast<float*>(h->Gm), M2);
+  int mt = (n + g3::BM - 1) / g3::BM;
+  const int nt = (M2 + g3::BN - 1) / g3::BN, kb = (n + g3::BK - 1) / g3::BK;
+  if (h->g3_mc && mt > 1) {   // clusters of 2 CTAs sharing the B tile by multicast
+    mt += mt & 1;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(std::min(mt / 2 * nt, h->sms / 2) * 2));
+    cfg.blockDim = dim3(g3::THREADS);
+    cfg.dynamicSmemBytes = g3::SMEM;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    CUDA_TRY(cudaLaunchKernelEx(&cfg, g3::k_g3_gemm<true>, h->tWh, h->tWl, h->tQh2, h->tQl2, mt, nt, kb, n, M2,
+                                reinterpret_cast<float*>(h->Gm), (long long)M2));
+  } else {
+    g3::k_g3_gemm<false><<<std::min(mt * nt, h->sms), g3::THREADS, g3::SMEM, st>>>(
+        h->tWh, h->tWl, h->tQh, h->tQl, mt, nt, kb, n, M2, reinterpret_cast<float*>(h->Gm), M2);
+  }
   return check_launch("k_g3_gemm");
 }
 
@@ -222,7 +246,10 @@ static mrf_status create_impl(const float2* basis_h, int r, int L, int device, u
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(llr::k_llr_svt, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)svt_smem(h->r));
   if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(g3::k_g3_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g3::SMEM);
+    e = cudaFuncSetAttribute(g3::k_g3_gemm<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g3::SMEM);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(g3::k_g3_gemm<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g3::SMEM);
+  if (const char* mc = std::getenv("MRF_G3_MC")) h->g3_mc = std::atoi(mc) != 0;
   if (e == cudaSuccess) e = cudaDeviceGetAttribute(&h->sms, cudaDevAttrMultiProcessorCount, h->device);
   if (e != cudaSuccess) {
     llr_free(h);
