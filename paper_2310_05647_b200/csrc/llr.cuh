@@ -194,30 +194,69 @@ static __global__ void __launch_bounds__(kSvtThreads) k_llr_svt(const float2* __
       }
       rotated = __any_sync(0xffffffffu, rotated);
       __syncwarp();
-      // rows a, b: A[a][k] <- c A[a][k] + s e A[b][k],  A[b][k] <- c A[b][k] - s conj(e) A[a][k]
-      for (int k = g; k < half; k += G) {
-        const double4 R = rot[k];
-        if (R.y == 0.0 || c >= r) continue;
-        const int2 ab = pr[k];
-        const double2 x = A[ab.x * rp + c], y = A[ab.y * rp + c];
-        const double2 ey = zmul(make_double2(R.z, R.w), y), ecx = zmul(make_double2(R.z, -R.w), x);
-        A[ab.x * rp + c] = make_double2(R.x * x.x + R.y * ey.x, R.x * x.y + R.y * ey.y);
-        A[ab.y * rp + c] = make_double2(R.x * y.x - R.y * ecx.x, R.x * y.y - R.y * ecx.y);
-      }
-      __syncwarp();
-      // columns a, b of A and of W: X[k][a] <- c X[k][a] + s conj(e) X[k][b],
-      // X[k][b] <- c X[k][b] - s e X[k][a]
-      // (eigenvalues only -- no P -- skip W: only the A columns)
-      const int mstep = vecs ? 1 : 2;
-      for (int mk = g * mstep; mk < 2 * half; mk += G * mstep) {
-        const double4 R = rot[mk >> 1];
-        if (R.y == 0.0 || c >= r) continue;
-        const int2 ab = pr[mk >> 1];
-        double2* X = (mk & 1) ? Wm : A;
-        const double2 x = X[c * rp + ab.x], y = X[c * rp + ab.y];
-        const double2 ecy = zmul(make_double2(R.z, -R.w), y), ex = zmul(make_double2(R.z, R.w), x);
-        X[c * rp + ab.x] = make_double2(R.x * x.x + R.y * ecy.x, R.x * x.y + R.y * ecy.y);
-        X[c * rp + ab.y] = make_double2(R.x * y.x - R.y * ex.x, R.x * y.y - R.y * ex.y);
+      if (vecs) {
+        // with eigenvectors (measured faster this way): rows a, b of A,
+        // A[a][k] <- c A[a][k] + s e A[b][k],  A[b][k] <- c A[b][k] - s conj(e) A[a][k], then columns
+        // a, b of A and of W: X[k][a] <- c X[k][a] + s conj(e) X[k][b], X[k][b] <- c X[k][b] - s e X[k][a]
+        for (int k = g; k < half; k += G) {
+          const double4 R = rot[k];
+          if (R.y == 0.0 || c >= r) continue;
+          const int2 ab = pr[k];
+          const double2 x = A[ab.x * rp + c], y = A[ab.y * rp + c];
+          const double2 ey = zmul(make_double2(R.z, R.w), y), ecx = zmul(make_double2(R.z, -R.w), x);
+          A[ab.x * rp + c] = make_double2(R.x * x.x + R.y * ey.x, R.x * x.y + R.y * ey.y);
+          A[ab.y * rp + c] = make_double2(R.x * y.x - R.y * ecx.x, R.x * y.y - R.y * ecx.y);
+        }
+        __syncwarp();
+        for (int mk = g; mk < 2 * half; mk += G) {
+          const double4 R = rot[mk >> 1];
+          if (R.y == 0.0 || c >= r) continue;
+          const int2 ab = pr[mk >> 1];
+          double2* X = (mk & 1) ? Wm : A;
+          const double2 x = X[c * rp + ab.x], y = X[c * rp + ab.y];
+          const double2 ecy = zmul(make_double2(R.z, -R.w), y), ex = zmul(make_double2(R.z, R.w), x);
+          X[c * rp + ab.x] = make_double2(R.x * x.x + R.y * ecy.x, R.x * x.y + R.y * ecy.y);
+          X[c * rp + ab.y] = make_double2(R.x * y.x - R.y * ex.x, R.x * y.y - R.y * ex.y);
+        }
+      } else {
+        // eigenvalues only: A <- J^H A J in one pass over the 2 x 2 blocks (pair k1 of rows, pair k2
+        // of columns); every entry belongs to exactly one block, whose new value depends only on its
+        // own 4 entries
+        const int nblk = half * half;
+        for (int it = lane; it < nblk; it += 32) {   // A blocks
+          {
+            const int k1 = it / half, k2 = it - k1 * half;
+            const double4 R1 = rot[k1], R2 = rot[k2];
+            if (R1.y == 0.0 && R2.y == 0.0) continue;
+            const int2 p1 = pr[k1], p2 = pr[k2];
+            double2 x00 = A[p1.x * rp + p2.x], x01 = A[p1.x * rp + p2.y];
+            double2 x10 = A[p1.y * rp + p2.x], x11 = A[p1.y * rp + p2.y];
+            if (R1.y != 0.0) {
+              const double2 e = make_double2(R1.z, R1.w), ec = make_double2(R1.z, -R1.w);
+              const double2 e10 = zmul(e, x10), e11 = zmul(e, x11), c00 = zmul(ec, x00), c01 = zmul(ec, x01);
+              const double2 n00 = make_double2(R1.x * x00.x + R1.y * e10.x, R1.x * x00.y + R1.y * e10.y);
+              const double2 n01 = make_double2(R1.x * x01.x + R1.y * e11.x, R1.x * x01.y + R1.y * e11.y);
+              x10 = make_double2(R1.x * x10.x - R1.y * c00.x, R1.x * x10.y - R1.y * c00.y);
+              x11 = make_double2(R1.x * x11.x - R1.y * c01.x, R1.x * x11.y - R1.y * c01.y);
+              x00 = n00;
+              x01 = n01;
+            }
+            if (R2.y != 0.0) {
+              const double2 e = make_double2(R2.z, R2.w), ec = make_double2(R2.z, -R2.w);
+              const double2 c01 = zmul(ec, x01), c11 = zmul(ec, x11), e00 = zmul(e, x00), e10 = zmul(e, x10);
+              const double2 n00 = make_double2(R2.x * x00.x + R2.y * c01.x, R2.x * x00.y + R2.y * c01.y);
+              const double2 n10 = make_double2(R2.x * x10.x + R2.y * c11.x, R2.x * x10.y + R2.y * c11.y);
+              x01 = make_double2(R2.x * x01.x - R2.y * e00.x, R2.x * x01.y - R2.y * e00.y);
+              x11 = make_double2(R2.x * x11.x - R2.y * e10.x, R2.x * x11.y - R2.y * e10.y);
+              x00 = n00;
+              x10 = n10;
+            }
+            A[p1.x * rp + p2.x] = x00;
+            A[p1.x * rp + p2.y] = x01;
+            A[p1.y * rp + p2.x] = x10;
+            A[p1.y * rp + p2.y] = x11;
+          }
+        }
       }
       __syncwarp();
     }
