@@ -11,11 +11,13 @@
 // keep the fp16 operands in [-1, 1]; the argmax uses |c~|^2 * (m_k / ||d_k||)^2 (s_v is common
 // to a voxel's row).  rho is recomputed exactly in fp32 for the chosen atom (k_dict_fix).
 //
-// k_dict_gemm: persistent CTAs over (128-voxel, 128-atom) units, 256 threads in roles: warp 0 = TMA producer (128-byte
+// k_dict_gemm: persistent CTAs over (128-voxel, 128-atom) units, 384 threads in roles: warp 0 = TMA producer (128-byte
 // swizzled tiles, 4-stage mbarrier ring), warp 1 = TMEM allocator + single-thread tcgen05.mma
 // issuer (M = 128, N = 256, K = 16 per instruction, fp32 accumulators in TMEM, two 256-column
 // accumulator buffers so the epilogue of one atom tile overlaps the MMAs of the next), warps
-// 4..7 = epilogue (tcgen05.ld, one voxel per thread = TMEM lane, running argmax in registers).
+// 4..11 = epilogue in two groups of 4 warps, one per half of the atom tile (tcgen05.ld, one voxel
+// per thread = TMEM lane, running argmax in registers) -- with the 13 basis coefficients (K = 64)
+// the MMAs are short and the epilogue sets the pace.
 #pragma once
 #include <cuda.h>
 #include <cuda_fp16.h>
@@ -36,7 +38,7 @@ constexpr int UK = 16;           // UMMA K for kind::f16
 constexpr int STAGES = 4;
 constexpr int A_BYTES = BM * BK * 2;   // 16 KB
 constexpr int B_BYTES = BN * BK * 2;   // 32 KB
-constexpr int THREADS = 256;
+constexpr int THREADS = 384;   // warps 0-3: TMA / MMA roles; 4-11: two epilogue groups
 constexpr size_t SMEM = 1024 + (size_t)STAGES * (A_BYTES + B_BYTES) + 256;
 
 // instruction descriptor: kind::f16, fp16 A/B, fp32 D, both K-major, M = 128, N = 256
@@ -77,7 +79,7 @@ k_dict_gemm(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUt
     }
     for (int a = 0; a < 2; ++a) {
       bar_init(&tfull[a], 1);
-      bar_init(&tempty[a], 4 * 32);
+      bar_init(&tempty[a], 8 * 32);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -124,12 +126,15 @@ k_dict_gemm(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUt
       mma_commit(&tfull[acc]);   // accumulator complete
     }
   } else if (warp >= 4) {
-    // ---- epilogue: thread = TMEM lane = voxel row of the unit's m tile.  The best atom of the
-    // unit's 128 is merged across units with one 64-bit atomicMax per voxel on
-    // (score bits << 32 | ~atom): scores are >= 0, so their bits order as the values, and on
-    // equal scores the lower atom index wins (order independent, deterministic).
-    const int row = (warp - 4) * 32 + lane;
-    const uint32_t lane_addr = (uint32_t)((warp - 4) * 32) << 16;
+    // ---- epilogue: thread = TMEM lane = voxel row of the unit's m tile; two groups of 4 warps
+    // (warp % 4 selects the TMEM lane quarter) take the accumulator's columns [0, 128) and
+    // [128, 256) (64 atoms each).  The best atom of a group's 64 is merged across groups and units
+    // with one 64-bit atomicMax per voxel on (score bits << 32 | ~atom): scores are >= 0, so their
+    // bits order as the values, and on equal scores the lower atom index wins (order independent,
+    // deterministic).
+    const int grp = (warp - 4) >> 2, quarter = warp & 3;
+    const int row = quarter * 32 + lane;
+    const uint32_t lane_addr = (uint32_t)(quarter * 32) << 16;
     int j = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x, ++j) {
       const int m0 = (u / n_tiles) * BM, nt = u % n_tiles;
@@ -140,12 +145,13 @@ k_dict_gemm(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUt
       float bsc = -1.f;
       int bk = 0;
 #pragma unroll 1
-      for (int ch = 0; ch < BN / 128; ++ch) {   // 128 columns (64 atoms) per TMEM load and wait
-        float v[128];
-        tmem_ld128(tmem + lane_addr + (uint32_t)(acc * BN + ch * 128), v);
-        const int k0 = nt * (BN / 2) + ch * 64;
+      for (int ch = 0; ch < 2; ++ch) {   // 64 columns (32 atoms) per TMEM load and wait
+        float v[64];
+        const int col = grp * 128 + ch * 64;
+        tmem_ld64(tmem + lane_addr + (uint32_t)(acc * BN + col), v);
+        const int k0 = nt * (BN / 2) + col / 2;
 #pragma unroll
-        for (int q = 0; q < 64; ++q) {
+        for (int q = 0; q < 32; ++q) {
           const float sc = (v[2 * q] * v[2 * q] + v[2 * q + 1] * v[2 * q + 1]) * __ldg(w2 + k0 + q);
           if (sc > bsc) {   // strict: equal scores keep the lowest atom index
             bsc = sc;
