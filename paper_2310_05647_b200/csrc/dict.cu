@@ -162,7 +162,10 @@ static mrf_status match_impl(mrf_dict d, const char* who, const void* x, int L, 
   CUtensorMap tmx;
   MRF_TRY(make_tmap(&tmx, d->xp, (uint64_t)KD, (uint64_t)vpad, (uint32_t)dm::BM));
   const float2* xf = reinterpret_cast<const float2*>(x);
-  dm::k_dict_pack_x<<<(unsigned)(vpad / 32), 256, 0, st>>>(xf, L, (int)V, KD, d->xp, d->xs);
+  if (L <= 32 && KD == 64)
+    dm::k_dict_pack_short<<<(unsigned)((vpad + 255) / 256), 256, 0, st>>>(xf, L, (int)V, (int)vpad, KD, d->xp, d->xs);
+  else
+    dm::k_dict_pack_x<<<(unsigned)(vpad / 32), 256, 0, st>>>(xf, L, (int)V, KD, d->xp, d->xs);
   MRF_TRY(check_launch("k_dict_pack_x"));
   if (d->prof) {
     while (d->ev.size() < d->ev_used + 2) {
@@ -183,8 +186,12 @@ static mrf_status match_impl(mrf_dict d, const char* who, const void* x, int L, 
     CUDA_TRY(cudaEventRecord(d->ev[d->ev_used + 1], st));
     d->ev_used += 2;
   }
-  dm::k_dict_fix<<<(unsigned)((V + 31) / 32), 256, 0, st>>>(xf, atoms, d->n2inv, d->lut, d->P, L, (int)V, d->best,
-                                                               index, pd, params);
+  if (L <= 32)
+    dm::k_dict_fix_short<<<(unsigned)((V + 255) / 256), 256, 0, st>>>(xf, atoms, d->n2inv, d->lut, d->P, L, (int)V,
+                                                                      d->best, index, pd, params);
+  else
+    dm::k_dict_fix<<<(unsigned)((V + 31) / 32), 256, 0, st>>>(xf, atoms, d->n2inv, d->lut, d->P, L, (int)V, d->best,
+                                                                 index, pd, params);
   MRF_TRY(check_launch("k_dict_fix"));
   return MRF_OK;
 }

@@ -281,5 +281,51 @@ __global__ void __launch_bounds__(256) k_dict_fix(const float2* __restrict__ x, 
   }
 }
 
+// Short time series (L <= 32: the basis-coordinate match, K = 64): one thread per voxel.
+// Pack: x [L][V] -> X~ [Vpad][KD] fp16 row v = (Re, Im) x_v / s_v, zero-padded; s_v = max |Re|, |Im|.
+__global__ void __launch_bounds__(256) k_dict_pack_short(const float2* __restrict__ x, int L, int V, int Vpad, int KD,
+                                                         __half* __restrict__ xp, float* __restrict__ s) {
+  const int v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= Vpad) return;
+  float2 a[32];
+  float m = 0.f;
+#pragma unroll
+  for (int l = 0; l < 32; ++l) {
+    a[l] = (l < L && v < V) ? __ldg(x + (size_t)l * V + v) : make_float2(0.f, 0.f);
+    m = fmaxf(m, fmaxf(fabsf(a[l].x), fabsf(a[l].y)));
+  }
+  const float sc = m > 0.f ? m : 1.f, inv = 1.f / sc;
+  if (v < V) s[v] = sc;
+  uint4* row = reinterpret_cast<uint4*>(xp + (size_t)v * KD);
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {   // 8 x 16 bytes = 64 halves = 32 complex slots (KD == 64)
+    __half2 h[4];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) h[t] = __floats2half2_rn(a[4 * q + t].x * inv, a[4 * q + t].y * inv);
+    row[q] = *reinterpret_cast<uint4*>(h);
+  }
+}
+
+// rho and LUT lookup for the chosen atoms, one thread per voxel (L <= 32): Re<d_k, x_v> in fp32.
+__global__ void __launch_bounds__(256) k_dict_fix_short(const float2* __restrict__ x, const float2* __restrict__ atoms,
+                                                        const float* __restrict__ n2inv, const float* __restrict__ lut,
+                                                        int P, int L, int V, const unsigned long long* __restrict__ best,
+                                                        int* __restrict__ index, float* __restrict__ pd,
+                                                        float* __restrict__ params) {
+  const int v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= V) return;
+  const int k = (int)(0xFFFFFFFFu - (uint32_t)(best[v] & 0xFFFFFFFFull));
+  const float2* d = atoms + (size_t)k * L;
+  float acc = 0.f;
+  for (int l = 0; l < L; ++l) {
+    const float2 dv = __ldg(d + l), xv = __ldg(x + (size_t)l * V + v);
+    acc = fmaf(dv.x, xv.x, fmaf(dv.y, xv.y, acc));
+  }
+  index[v] = k;
+  pd[v] = fmaxf(acc * __ldg(n2inv + k), 0.f);
+  if (params)
+    for (int c = 0; c < P; ++c) params[(size_t)v * P + c] = __ldg(lut + (size_t)k * P + c);
+}
+
 }  // namespace dm
 }  // namespace mrf
