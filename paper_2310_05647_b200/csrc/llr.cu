@@ -45,9 +45,19 @@ struct mrf_llr_s {
   // spectra workspaces [r][C][G*G], zs = P_S A^H A x and bv = P_S A^H b coefficients
   float2 *Ksn = nullptr, *spa = nullptr, *spb = nullptr, *zs = nullptr, *bv = nullptr;
   size_t sn_bytes = 0;
+  cudaStream_t side = nullptr;            // second stream: the cost's SVT overlaps its subspace normal
+  cudaStream_t side2 = nullptr;           // third stream: the next maps and Laplacian overlap the cost
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_step = nullptr;
   unsigned long long sn_plan = 0;         // serial of the plan the mixing kernels were built for
   // manifold term (mrf_llr_laplacian)
   bool has_lap = false;
+  // two Laplacian sets (W, deg, the tf32 split and its tensor maps); W, deg, Wh, Wl, tWh, tWl below
+  // alias the current one.  A build writes the other set and switches at its end, so a step or cost
+  // already enqueued on another stream keeps reading the previous Laplacian.
+  int lap_cur = 0;
+  float *Wset[2] = {nullptr, nullptr}, *degset[2] = {nullptr, nullptr};
+  float *Whset[2] = {nullptr, nullptr}, *Wlset[2] = {nullptr, nullptr};
+  CUtensorMap tWhset[2], tWlset[2];
   float* W = nullptr;         // [n][n] similarity weights (Eq. 8), first the squared distances
   float* deg = nullptr;       // [n] degrees D_ii
   float* pv = nullptr;        // [n][3 p^2] standardised patch vectors of the maps
@@ -72,10 +82,19 @@ static void llr_free(mrf_llr_s* h) {
   if (!h) return;
   cudaSetDevice(h->device);
   if (h->sel_h) cudaFreeHost(h->sel_h);
+  if (h->ev_fork) cudaEventDestroy(h->ev_fork);
+  if (h->ev_join) cudaEventDestroy(h->ev_join);
+  if (h->side) cudaStreamDestroy(h->side);
+  if (h->side2) cudaStreamDestroy(h->side2);
+  if (h->ev_step) cudaEventDestroy(h->ev_step);
   if (h->hsum) cudaFreeHost(h->hsum);
-  for (void* v : {(void*)h->sel, (void*)h->dT, (void*)h->corners, (void*)h->Y, (void*)h->P, (void*)h->nx, (void*)h->nuc, (void*)h->W,
-                  (void*)h->deg, (void*)h->pv, (void*)h->hist, (void*)h->stats, (void*)h->YX, (void*)h->Qm,
-                  (void*)h->Gm, (void*)h->pen, (void*)h->Wh, (void*)h->Wl, (void*)h->Qh, (void*)h->Ql, (void*)h->yb, (void*)h->part, (void*)h->rhs, (void*)h->x2, (void*)h->xcv, (void*)h->xcr, (void*)h->Ksn,
+  for (int i = 0; i < 2; ++i)
+    for (void* v : {(void*)h->Wset[i], (void*)h->degset[i], (void*)h->Whset[i], (void*)h->Wlset[i]})
+      if (v) cudaFree(v);
+  h->W = h->deg = h->Wh = h->Wl = nullptr;   // aliases of a set
+  for (void* v : {(void*)h->sel, (void*)h->dT, (void*)h->corners, (void*)h->Y, (void*)h->P, (void*)h->nx, (void*)h->nuc,
+                  (void*)h->pv, (void*)h->hist, (void*)h->stats, (void*)h->YX, (void*)h->Qm,
+                  (void*)h->Gm, (void*)h->pen, (void*)h->Qh, (void*)h->Ql, (void*)h->yb, (void*)h->part, (void*)h->rhs, (void*)h->x2, (void*)h->xcv, (void*)h->xcr, (void*)h->Ksn,
                   (void*)h->spa, (void*)h->spb, (void*)h->zs, (void*)h->bv})
     if (v) cudaFree(v);
   delete h;
@@ -251,6 +270,11 @@ static mrf_status create_impl(const float2* basis_h, int r, int L, int device, u
     e = cudaFuncSetAttribute(g3::k_g3_gemm<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g3::SMEM);
   if (const char* mc = std::getenv("MRF_G3_MC")) h->g3_mc = std::atoi(mc) != 0;
   if (e == cudaSuccess) e = cudaDeviceGetAttribute(&h->sms, cudaDevAttrMultiProcessorCount, h->device);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->side2, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->ev_step, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming);
   if (e != cudaSuccess) {
     llr_free(h);
     return fail(MRF_ECUDA, std::string("mrf_llr_create: ") + cudaGetErrorString(e));
@@ -283,21 +307,31 @@ mrf_status mrf_llr_laplacian(mrf_llr h, const float* params, const float* pd, do
   CUDA_TRY(cudaSetDevice(h->device));
   cudaStream_t st = (cudaStream_t)stream;
   const int n = h->nc * h->nc, np = h->p * h->p, V = h->N * h->N;
-  if (!h->W) {
-    bool ok = cudaMalloc((void**)&h->W, (size_t)n * n * sizeof(float)) == cudaSuccess &&
-              cudaMalloc((void**)&h->deg, (size_t)n * sizeof(float)) == cudaSuccess &&
-              cudaMalloc((void**)&h->pv, (size_t)n * 3 * np * sizeof(float)) == cudaSuccess &&
+  if (!h->Wset[0]) {
+    bool ok = true;
+    for (int i = 0; i < 2; ++i)
+      ok = ok && cudaMalloc((void**)&h->Wset[i], (size_t)n * n * sizeof(float)) == cudaSuccess &&
+           cudaMalloc((void**)&h->degset[i], (size_t)n * sizeof(float)) == cudaSuccess;
+    ok = ok && cudaMalloc((void**)&h->pv, (size_t)n * 3 * np * sizeof(float)) == cudaSuccess &&
               cudaMalloc((void**)&h->hist, (3 * 2048 + 1) * sizeof(unsigned)) == cudaSuccess &&
               cudaMalloc((void**)&h->sel, sizeof(mfd::LapSel)) == cudaSuccess &&
               cudaMallocHost((void**)&h->sel_h, sizeof(mfd::LapSel)) == cudaSuccess &&
               cudaMalloc((void**)&h->stats, (size_t)kStatBlocks * 7 * sizeof(double)) == cudaSuccess;
     h->nK = (n + 3) / 4 * 4;   // 16-byte TMA row pitch
-    ok = ok && cudaMalloc((void**)&h->Wh, (size_t)n * h->nK * sizeof(float)) == cudaSuccess &&
-         cudaMalloc((void**)&h->Wl, (size_t)n * h->nK * sizeof(float)) == cudaSuccess;
+    for (int i = 0; i < 2; ++i)
+      ok = ok && cudaMalloc((void**)&h->Whset[i], (size_t)n * h->nK * sizeof(float)) == cudaSuccess &&
+           cudaMalloc((void**)&h->Wlset[i], (size_t)n * h->nK * sizeof(float)) == cudaSuccess;
     if (!ok) return fail(MRF_ENOMEM, "mrf_llr_laplacian: device allocation failed");
-    MRF_TRY(tmap_2d(&h->tWh, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, h->Wh, n, n, (uint64_t)h->nK * 4, g3::BK, g3::BM));
-    MRF_TRY(tmap_2d(&h->tWl, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, h->Wl, n, n, (uint64_t)h->nK * 4, g3::BK, g3::BM));
+    for (int i = 0; i < 2; ++i) {
+      MRF_TRY(tmap_2d(&h->tWhset[i], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, h->Whset[i], n, n, (uint64_t)h->nK * 4, g3::BK,
+                      g3::BM));
+      MRF_TRY(tmap_2d(&h->tWlset[i], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, h->Wlset[i], n, n, (uint64_t)h->nK * 4, g3::BK,
+                      g3::BM));
+    }
   }
+  // build into the set not in use (the first build: set 0)
+  const int bs = h->has_lap ? h->lap_cur ^ 1 : 0;
+  float *Wb = h->Wset[bs], *degb = h->degset[bs];
   // Everything stays on the device until the final copy of the LapSel state (one synchronisation):
   // foreground statistics of (T1, T2, PD) over PD > 0.1 max PD (reading 26)
   unsigned* pdmax = h->hist + 3 * 2048;
@@ -309,7 +343,7 @@ mrf_status mrf_llr_laplacian(mrf_llr h, const float* params, const float* pd, do
   MRF_TRY(check_launch("k_mfd_stats"));
   mfd::k_mfd_patchvec<<<n, 128, 0, st>>>(params, pd, sel, h->corners, h->nc, h->N, h->p, h->pv);
   const dim3 gd((unsigned)((n + 127) / 128), (unsigned)((n + 127) / 128));
-  mfd::k_mfd_dist<<<gd, 256, 0, st>>>(h->pv, n, 3 * np, h->W);
+  mfd::k_mfd_dist<<<gd, 256, 0, st>>>(h->pv, n, 3 * np, Wb);
   MRF_TRY(check_launch("k_mfd_dist"));
   // sigma^2: given, or the median of the nonzero upper-triangle distances by an exact radix select
   // (11 + 11 + 10 bits; positive floats order as their bits), the bookkeeping on the device
@@ -322,21 +356,21 @@ mrf_status mrf_llr_laplacian(mrf_llr h, const float* params, const float* pd, do
     unsigned* h1 = h->hist + 2048;
     const unsigned hb = 2 * 148;
     CUDA_TRY(cudaMemsetAsync(h0, 0, 2048 * sizeof(unsigned), st));
-    mfd::k_mfd_hist<<<hb, 256, 0, st>>>(h->W, n, 0, nullptr, h0, h1);
+    mfd::k_mfd_hist<<<hb, 256, 0, st>>>(Wb, n, 0, nullptr, h0, h1);
     mfd::k_mfd_select<<<1, 256, 0, st>>>(0, h0, h0, sel);
     for (int ps = 1; ps <= 2; ++ps) {
       CUDA_TRY(cudaMemsetAsync(h0, 0, 2 * 2048 * sizeof(unsigned), st));
-      mfd::k_mfd_hist<<<hb, 256, 0, st>>>(h->W, n, ps, sel->pre, h0, h1);
+      mfd::k_mfd_hist<<<hb, 256, 0, st>>>(Wb, n, ps, sel->pre, h0, h1);
       mfd::k_mfd_select<<<1, 256, 0, st>>>(ps, h0, h1, sel);
     }
     MRF_TRY(check_launch("k_mfd_select"));
   }
-  mfd::k_mfd_weights<<<n, 256, 0, st>>>(h->W, n, &sel->sigma2, h->deg);
+  mfd::k_mfd_weights<<<n, 256, 0, st>>>(Wb, n, &sel->sigma2, degb);
   MRF_TRY(check_launch("k_mfd_weights"));
-  mfd::k_mfd_degmax<<<(unsigned)std::min((n + 255) / 256, 148), 256, 0, st>>>(h->deg, n, sel);
+  mfd::k_mfd_degmax<<<(unsigned)std::min((n + 255) / 256, 148), 256, 0, st>>>(degb, n, sel);
   MRF_TRY(check_launch("k_mfd_degmax"));
   const dim3 gs((unsigned)((n + 31) / 32), (unsigned)((n + 31) / 32));
-  g3::k_g3_split<false><<<gs, 256, 0, st>>>(h->W, n, n, n, h->Wh, h->Wl, h->nK);
+  g3::k_g3_split<false><<<gs, 256, 0, st>>>(Wb, n, n, n, h->Whset[bs], h->Wlset[bs], h->nK);
   MRF_TRY(check_launch("k_g3_split"));
   CUDA_TRY(cudaMemcpyAsync(h->sel_h, sel, sizeof(mfd::LapSel), cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaStreamSynchronize(st));
@@ -347,6 +381,14 @@ mrf_status mrf_llr_laplacian(mrf_llr h, const float* params, const float* pd, do
     std::memcpy(&md, &h->sel_h->maxdeg, 4);
     *max_degree = md;
   }
+  // switch to the new set (everything that reads it is enqueued after this returns)
+  h->lap_cur = bs;
+  h->W = Wb;
+  h->deg = degb;
+  h->Wh = h->Whset[bs];
+  h->Wl = h->Wlset[bs];
+  h->tWh = h->tWhset[bs];
+  h->tWl = h->tWlset[bs];
   h->has_lap = true;
   return MRF_OK;
 }
@@ -498,30 +540,34 @@ static mrf_status sub_step(mrf_llr_s* h, float mu, float lambda1, float lambda2,
 // cost(n) in basis coordinates: zs = P_S A^H A x (kept for the next step),
 // 1/2 ||A x - b||^2 = 1/2 <x, A^H A x> - Re <x, A^H b> + 1/2 ||b||^2 = 1/2 <u, zs> - Re <u, bv> + b2 / 2,
 // the trace term and the nuclear norms from the coefficients
-static mrf_status sub_cost(mrf_llr_s* h, mrf_plan plan, double b2, float lambda1, float lambda2, double* cost,
-                           cudaStream_t st) {
-  const size_t n = (size_t)h->N * h->N * h->r;
-  MRF_TRY(sn_apply(plan, h->Ksn, h->r, h->xcr, h->zs, h->spa, h->spb, st));
+struct SubCost {
   double uz = 0.0, ub = 0.0, tr = 0.0, nuc = 0.0;
-  Sums sums{h, st};
+};
+static mrf_status sub_cost_launch(mrf_llr_s* h, mrf_plan plan, float lambda1, cudaStream_t st, Sums& sums,
+                                  SubCost& t) {
+  const size_t n = (size_t)h->N * h->N * h->r;
+  // the nuclear norms (latency-bound SVT, a quarter of the warp slots) on the side stream,
+  // overlapping the subspace normal and the trace term on `st`
+  CUDA_TRY(cudaEventRecord(h->ev_fork, st));
+  CUDA_TRY(cudaStreamWaitEvent(h->side, h->ev_fork, 0));
+  MRF_TRY(svt(h, h->xcv, INFINITY, h->side));
+  CUDA_TRY(cudaEventRecord(h->ev_join, h->side));
+  MRF_TRY(sn_apply(plan, h->Ksn, h->r, h->xcr, h->zs, h->spa, h->spb, st));
   llr::k_llr_dotre<<<kStatBlocks, 256, 0, st>>>(h->xcr, h->zs, n, h->part);
   llr::k_llr_dotre<<<kStatBlocks, 256, 0, st>>>(h->xcv, h->bv, n, h->part + kStatBlocks);
   MRF_TRY(check_launch("k_llr_dotre"));
-  MRF_TRY(sums.add(h->part, kStatBlocks, &uz));
-  MRF_TRY(sums.add(h->part + kStatBlocks, kStatBlocks, &ub));
+  MRF_TRY(sums.add(h->part, kStatBlocks, &t.uz));
+  MRF_TRY(sums.add(h->part + kStatBlocks, kStatBlocks, &t.ub));
   const int nq = h->nc * h->nc;
   if (h->has_lap && lambda1 > 0.f) {
     MRF_TRY(manifold_ws(h));
     MRF_TRY(manifold_G(h, h->xcv, st));
     mfd::k_mfd_penalty<<<nq, 256, 0, st>>>(h->Qm, h->Gm, h->deg, h->p * h->p * h->r, h->pen);
     MRF_TRY(check_launch("k_mfd_penalty"));
-    MRF_TRY(sums.add(h->pen, nq, &tr));
+    MRF_TRY(sums.add(h->pen, nq, &t.tr));
   }
-  MRF_TRY(svt(h, h->xcv, INFINITY, st));
-  MRF_TRY(sums.add(h->nuc, nq, &nuc));
-  MRF_TRY(sums.finish());
-  *cost = (0.5 * uz - ub + 0.5 * b2) + (double)lambda1 * tr + (double)lambda2 * nuc;
-  return MRF_OK;
+  CUDA_TRY(cudaStreamWaitEvent(st, h->ev_join, 0));
+  return sums.add(h->nuc, nq, &t.nuc);
 }
 
 // Subspace-normal workspaces (mixing kernels, spectra, zs, bv) sized for `plan`, and the mixing
@@ -607,24 +653,25 @@ mrf_status mrf_msllr_solve(mrf_llr h, mrf_dict dict, mrf_plan plan, const void* 
     MRF_TRY(dot_re(h, (const float2*)b, (const float2*)b, ny, st, &b2));   // ||b||^2
   }
   bool have_coef = false;
-  auto maps = [&](const void* cur) -> mrf_status {
-    if (have_coef && coef_ok) return mrf_dict_match_coef(dict, h->xcr, V, index, pd, params, stream);
-    return mrf_dict_match(dict, cur, V, index, pd, params, stream);
+  auto maps = [&](const void* cur, void* ms) -> mrf_status {
+    if (have_coef && coef_ok) return mrf_dict_match_coef(dict, h->xcr, V, index, pd, params, ms);
+    return mrf_dict_match(dict, cur, V, index, pd, params, ms);
   };
-  auto update_maps = [&](const void* cur) -> mrf_status {
-    MRF_TRY(maps(cur));
+  auto update_maps = [&](const void* cur, void* ms) -> mrf_status {
+    MRF_TRY(maps(cur, ms));
     if (manifold) {
       double maxdeg = 0.0;
-      MRF_TRY(mrf_llr_laplacian(h, params, pd, prm->sigma2, nullptr, &maxdeg, stream));
+      MRF_TRY(mrf_llr_laplacian(h, params, pd, prm->sigma2, nullptr, &maxdeg, ms));
       lam1 = (float)((double)prm->lambda1 * maxdeg);   // lambda_1^n = lambda_1^0 max(L^n)
     }
     return MRF_OK;
   };
-  if (manifold) MRF_TRY(update_maps(x));
+  if (manifold) MRF_TRY(update_maps(x, stream));
   void* cur = x;
   void* nxt = h->x2;
   double prev = 0.0;
   int it = 0;
+  float lam1_last = lam1;   // lambda_1 of the last step (info)
   bool maps_current = manifold;
   // cost(n) only feeds the stop rule and info->cost: without either it is not evaluated (the
   // iterates do not depend on it)
@@ -640,25 +687,49 @@ mrf_status mrf_msllr_solve(mrf_llr h, mrf_dict dict, mrf_plan plan, const void* 
       std::swap(cur, nxt);
     }
     have_coef = true;   // k_llr_update wrote the coefficients of X^n
+    lam1_last = lam1;
+    it = n;
+    maps_current = false;
+    // basis coordinates: the next maps and Laplacian (they read X^n's coefficients, and the
+    // Laplacian builds into its other set) run on a third stream while cost(n) runs here
+    const bool overlap = sub && manifold && n < prm->max_iter;
+    if (overlap) {
+      CUDA_TRY(cudaEventRecord(h->ev_step, st));
+      CUDA_TRY(cudaStreamWaitEvent(h->side2, h->ev_step, 0));
+    }
     double c = 0.0;
     if (monitor) {
-      if (sub) MRF_TRY(sub_cost(h, plan, b2, lam1, prm->lambda2, &c, st));
-      else MRF_TRY(cost_impl(h, plan, cur, b, lam1, prm->lambda2, &c, nullptr, stream, h->xcv));
+      if (sub) {
+        Sums sums{h, st};
+        SubCost t;
+        MRF_TRY(sub_cost_launch(h, plan, lam1, st, sums, t));
+        if (overlap) {
+          MRF_TRY(update_maps(cur, h->side2));   // synchronises side2
+          maps_current = true;
+        }
+        MRF_TRY(sums.finish());
+        c = (0.5 * t.uz - t.ub + 0.5 * b2) + (double)lam1_last * t.tr + (double)prm->lambda2 * t.nuc;
+      } else {
+        MRF_TRY(cost_impl(h, plan, cur, b, lam1, prm->lambda2, &c, nullptr, stream, h->xcv));
+      }
       if (info && info->cost) info->cost[n - 1] = c;
     } else if (sub) {   // no cost wanted: only the subspace normal the next step needs
       MRF_TRY(sn_apply(plan, h->Ksn, h->r, h->xcr, h->zs, h->spa, h->spb, st));
+      if (overlap) {
+        MRF_TRY(update_maps(cur, h->side2));
+        maps_current = true;
+      }
     }
-    it = n;
-    maps_current = false;
-    // stop rule cost(n-1) / cost(n) - 1 < tol, from n = 2 (reading 27: cost(0) is not defined)
+    // stop rule cost(n-1) / cost(n) - 1 < tol, from n = 2 (reading 27: cost(0) is not defined);
+    // with the overlap the maps of X^n are already there (they are also the output maps)
     if (n >= 2 && prm->tol > 0.0 && prev / c - 1.0 < prm->tol) break;
     prev = c;
-    if (manifold && n < prm->max_iter) {   // M^{n+1} = Phi_D(X^n), L^{n+1}, lambda_1^{n+1}
-      MRF_TRY(update_maps(cur));
+    if (!overlap && manifold && n < prm->max_iter) {   // M^{n+1} = Phi_D(X^n), L^{n+1}, lambda_1^{n+1}
+      MRF_TRY(update_maps(cur, stream));
       maps_current = true;
     }
   }
-  if (!maps_current) MRF_TRY(maps(cur));   // M^ = Phi_D(X^)
+  if (!maps_current) MRF_TRY(maps(cur, stream));   // M^ = Phi_D(X^)
   if (sub && it > 1) {   // X^ = Xc d into x (k_llr_update with gamma = 0 expands its Y)
     const unsigned gv = (unsigned)((V + 31) / 32);
     if (h->r <= 16)
@@ -673,7 +744,7 @@ mrf_status mrf_msllr_solve(mrf_llr h, mrf_dict dict, mrf_plan plan, const void* 
   }
   if (info) {
     info->iters = it;
-    info->lambda1 = lam1;
+    info->lambda1 = lam1_last;
   }
   return MRF_OK;
 }
