@@ -10,6 +10,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <string>
 #include <vector>
 
@@ -456,8 +457,11 @@ static mrf_status step_impl(mrf_llr h, mrf_plan plan, const void* x, const void*
   return MRF_OK;
 }
 
+// xcoef known (inside mrf_msllr_solve): the SVT runs on the side stream beside the forward, and
+// `mid` (nullable) runs after every launch and before the host sums (the overlapped map update).
 static mrf_status cost_impl(mrf_llr h, mrf_plan plan, const void* x, const void* b, float lambda1, float lambda2,
-                            double* cost, double* terms, void* stream, const float2* xcoef) {
+                            double* cost, double* terms, void* stream, const float2* xcoef,
+                            const std::function<mrf_status()>& mid = nullptr) {
   if (!h || !plan || !x || !b) return fail(MRF_EINVAL, "mrf_llr_cost: null argument");
   if (!(lambda1 >= 0.f) || !(lambda2 >= 0.f)) return fail(MRF_EINVAL, "mrf_llr_cost: need lambda1, lambda2 >= 0");
   if (lambda1 > 0.f && !h->has_lap) return fail(MRF_EINVAL, "mrf_llr_cost: lambda1 > 0 needs mrf_llr_laplacian first");
@@ -475,6 +479,13 @@ static mrf_status cost_impl(mrf_llr h, mrf_plan plan, const void* x, const void*
     if (cudaMalloc((void**)&h->yb, ny * sizeof(float2)) != cudaSuccess) return fail(MRF_ENOMEM, "mrf_llr_cost: allocation failed");
     h->ny = ny;
   }
+  const int nq = h->nc * h->nc;
+  if (xcoef) {   // sum_q ||Q_q(P_S x)||_* on the side stream (overlapping the forward)
+    CUDA_TRY(cudaEventRecord(h->ev_fork, st));
+    CUDA_TRY(cudaStreamWaitEvent(h->side, h->ev_fork, 0));
+    MRF_TRY(svt(h, xcoef, INFINITY, h->side));
+    CUDA_TRY(cudaEventRecord(h->ev_join, h->side));
+  }
   // 1/2 ||A x - b||^2
   MRF_TRY(mrf_forward(plan, x, h->yb, stream));
   llr::k_llr_resid<<<kStatBlocks, 256, 0, st>>>(h->yb, (const float2*)b, ny, h->part);
@@ -486,7 +497,6 @@ static mrf_status cost_impl(mrf_llr h, mrf_plan plan, const void* x, const void*
   const float2* xf = (const float2*)x;
   if (!xcoef) MRF_TRY(coefs(h, xf, xf, xf, 0.f, h->Y, nullptr, st));
   const float2* cf = xcoef ? xcoef : h->Y;
-  const int nq = h->nc * h->nc;
   if (h->has_lap && (lambda1 > 0.f || terms)) {   // Tr(Q(P_S x) L Q(P_S x)^H)
     MRF_TRY(manifold_ws(h));
     MRF_TRY(manifold_G(h, cf, st));
@@ -495,8 +505,10 @@ static mrf_status cost_impl(mrf_llr h, mrf_plan plan, const void* x, const void*
     MRF_TRY(sums.add(h->pen, nq, &t[1]));
   }
   // sum_q ||Q_q(P_S x)||_* (threshold +inf: only the singular values, no thresholded blocks)
-  MRF_TRY(svt(h, cf, INFINITY, st));
+  if (xcoef) CUDA_TRY(cudaStreamWaitEvent(st, h->ev_join, 0));
+  else MRF_TRY(svt(h, cf, INFINITY, st));
   MRF_TRY(sums.add(h->nuc, nq, &t[2]));
+  if (mid) MRF_TRY(mid());
   MRF_TRY(sums.finish());
   t[0] *= 0.5;
   if (terms)
@@ -692,7 +704,7 @@ mrf_status mrf_msllr_solve(mrf_llr h, mrf_dict dict, mrf_plan plan, const void* 
     maps_current = false;
     // basis coordinates: the next maps and Laplacian (they read X^n's coefficients, and the
     // Laplacian builds into its other set) run on a third stream while cost(n) runs here
-    const bool overlap = sub && manifold && n < prm->max_iter;
+    const bool overlap = manifold && n < prm->max_iter && (sub || monitor);
     if (overlap) {
       CUDA_TRY(cudaEventRecord(h->ev_step, st));
       CUDA_TRY(cudaStreamWaitEvent(h->side2, h->ev_step, 0));
@@ -710,7 +722,14 @@ mrf_status mrf_msllr_solve(mrf_llr h, mrf_dict dict, mrf_plan plan, const void* 
         MRF_TRY(sums.finish());
         c = (0.5 * t.uz - t.ub + 0.5 * b2) + (double)lam1_last * t.tr + (double)prm->lambda2 * t.nuc;
       } else {
-        MRF_TRY(cost_impl(h, plan, cur, b, lam1, prm->lambda2, &c, nullptr, stream, h->xcv));
+        std::function<mrf_status()> mid;
+        if (overlap)
+          mid = [&]() -> mrf_status {
+            MRF_TRY(update_maps(cur, h->side2));   // synchronises side2
+            maps_current = true;
+            return MRF_OK;
+          };
+        MRF_TRY(cost_impl(h, plan, cur, b, lam1, prm->lambda2, &c, nullptr, stream, h->xcv, mid));
       }
       if (info && info->cost) info->cost[n - 1] = c;
     } else if (sub) {   // no cost wanted: only the subspace normal the next step needs
