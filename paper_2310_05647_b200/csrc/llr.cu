@@ -52,6 +52,7 @@ struct mrf_llr_s {
   unsigned long long sn_plan = 0;         // serial of the plan the mixing kernels were built for
   // manifold term (mrf_llr_laplacian)
   bool has_lap = false;
+  bool q_fresh = false;   // Qm / Qh / Ql hold Q of the current coefficients xcv (set by the solve's cost)
   // two Laplacian sets (W, deg, the tf32 split and its tensor maps); W, deg, Wh, Wl, tWh, tWl below
   // alias the current one.  A build writes the other set and switches at its end, so a step or cost
   // already enqueued on another stream keeps reading the previous Laplacian.
@@ -123,12 +124,16 @@ static mrf_status manifold_ws(mrf_llr_s* h) {
 }
 
 // Qm = Q(coef) (patch blocks of the [V][r] coefficients), Gm = W Qm on the tensor cores
-static mrf_status manifold_G(mrf_llr_s* h, const float2* coef, cudaStream_t st) {
+// reuse_q: Qm and its split already hold Q(coef) (inside mrf_msllr_solve the cost of X^n and the
+// next step both need Q(X^n); only W changes between them)
+static mrf_status manifold_G(mrf_llr_s* h, const float2* coef, cudaStream_t st, bool reuse_q = false) {
   const int n = h->nc * h->nc, blk = h->p * h->p * h->r;
-  mfd::k_mfd_gather<<<n, 128, 0, st>>>(coef, h->corners, h->nc, h->N, h->p, h->r, h->Qm);
   const int M2 = 2 * blk;   // G [n][M2] = W [n][n] Qm [n][M2]: A = W (K-major), B = Qm^T [M2][n]
-  const dim3 gs((unsigned)((M2 + 31) / 32), (unsigned)((n + 31) / 32));
-  g3::k_g3_split<true><<<gs, 256, 0, st>>>(reinterpret_cast<const float*>(h->Qm), n, M2, M2, h->Qh, h->Ql, h->nK);
+  if (!reuse_q) {
+    mfd::k_mfd_gather<<<n, 128, 0, st>>>(coef, h->corners, h->nc, h->N, h->p, h->r, h->Qm);
+    const dim3 gs((unsigned)((M2 + 31) / 32), (unsigned)((n + 31) / 32));
+    g3::k_g3_split<true><<<gs, 256, 0, st>>>(reinterpret_cast<const float*>(h->Qm), n, M2, M2, h->Qh, h->Ql, h->nK);
+  }
   int mt = (n + g3::BM - 1) / g3::BM;
   const int nt = (M2 + g3::BN - 1) / g3::BN, kb = (n + g3::BK - 1) / g3::BK;
   if (h->g3_mc && mt > 1) {   // clusters of 2 CTAs sharing the B tile by multicast
@@ -422,7 +427,7 @@ static mrf_status step_impl(mrf_llr h, mrf_plan plan, const void* x, const void*
   if (manifold) MRF_TRY(manifold_ws(h));
   MRF_TRY(coefs(h, (const float2*)x, h->nx, (const float2*)rhs, mu, h->Y, manifold && !xcoef ? h->YX : nullptr, st));
   if (manifold) {   // Y -= mu lambda1 coef(Q^*(Q(P_S x) L)),  L = D - W (Eq. 15's manifold term)
-    MRF_TRY(manifold_G(h, xcoef ? xcoef : h->YX, st));
+    MRF_TRY(manifold_G(h, xcoef ? xcoef : h->YX, st, xcoef && h->q_fresh));
     if (lambda1 > 0.f) {
       if (h->r <= 16)
         mfd::k_mfd_apply<16><<<(unsigned)(((long long)V * h->r + 255) / 256), 256, 0, st>>>(h->Y, h->Qm, h->Gm, h->deg, h->corners, h->nc,
@@ -447,6 +452,7 @@ static mrf_status step_impl(mrf_llr h, mrf_plan plan, const void* x, const void*
     llr::k_llr_update<32><<<gv, 256, 0, st>>>(h->Y, h->P, h->corners, h->nc, h->N, h->p, h->r, h->dT, h->L, gamma,
                                               (float2*)x_out, h->xcv, h->xcr);
   MRF_TRY(check_launch("k_llr_update"));
+  h->q_fresh = false;   // the coefficients moved on
   // Tr(Q(P_S x) L Q(P_S x)^H) and sum_q ||Q_q(Z)||_*: patches summed in a fixed order (synchronise)
   if (penalty || nuclear) {
     Sums sums{h, st};
@@ -500,6 +506,7 @@ static mrf_status cost_impl(mrf_llr h, mrf_plan plan, const void* x, const void*
   if (h->has_lap && (lambda1 > 0.f || terms)) {   // Tr(Q(P_S x) L Q(P_S x)^H)
     MRF_TRY(manifold_ws(h));
     MRF_TRY(manifold_G(h, cf, st));
+    h->q_fresh = xcoef != nullptr;
     mfd::k_mfd_penalty<<<nq, 256, 0, st>>>(h->Qm, h->Gm, h->deg, h->p * h->p * h->r, h->pen);
     MRF_TRY(check_launch("k_mfd_penalty"));
     MRF_TRY(sums.add(h->pen, nq, &t[1]));
@@ -533,7 +540,7 @@ static mrf_status sub_step(mrf_llr_s* h, float mu, float lambda1, float lambda2,
   MRF_TRY(check_launch("k_sn_grad"));
   if (lambda1 > 0.f) {
     MRF_TRY(manifold_ws(h));
-    MRF_TRY(manifold_G(h, h->xcv, st));
+    MRF_TRY(manifold_G(h, h->xcv, st, h->q_fresh));
     if (h->r <= 16)
       mfd::k_mfd_apply<16><<<(unsigned)(((long long)V * h->r + 255) / 256), 256, 0, st>>>(h->Y, h->Qm, h->Gm, h->deg, h->corners, h->nc,
                                                                          h->N, h->p, h->r, mu * lambda1);
@@ -546,6 +553,7 @@ static mrf_status sub_step(mrf_llr_s* h, float mu, float lambda1, float lambda2,
   const float gamma = mu * lambda2 * beta;
   llr::k_llr_update_coef<<<(unsigned)(((long long)V * h->r + 255) / 256), 256, 0, st>>>(
       h->Y, h->P, h->corners, h->nc, h->N, h->p, h->r, gamma, h->xcv, h->xcr);
+  h->q_fresh = false;   // the coefficients moved on
   return check_launch("k_llr_update_coef");
 }
 
@@ -574,6 +582,7 @@ static mrf_status sub_cost_launch(mrf_llr_s* h, mrf_plan plan, float lambda1, cu
   if (h->has_lap && lambda1 > 0.f) {
     MRF_TRY(manifold_ws(h));
     MRF_TRY(manifold_G(h, h->xcv, st));
+    h->q_fresh = true;
     mfd::k_mfd_penalty<<<nq, 256, 0, st>>>(h->Qm, h->Gm, h->deg, h->p * h->p * h->r, h->pen);
     MRF_TRY(check_launch("k_mfd_penalty"));
     MRF_TRY(sums.add(h->pen, nq, &t.tr));
