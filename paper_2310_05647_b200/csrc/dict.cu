@@ -124,7 +124,9 @@ mrf_status mrf_dict_create(const void* atoms, const float* lut, int K, int L, in
     dict_free(d);
     return s;
   }
-  e = cudaFuncSetAttribute(dm::k_dict_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dm::SMEM);
+  e = cudaFuncSetAttribute(dm::k_dict_gemm<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dm::SMEM);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(dm::k_dict_gemm<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dm::SMEM);
   if (e != cudaSuccess) {
     dict_free(d);
     return fail(MRF_ECUDA, std::string("mrf_dict_create: ") + cudaGetErrorString(e));
@@ -179,8 +181,12 @@ static mrf_status match_impl(mrf_dict d, const char* who, const void* x, int L, 
   int n_sm = 148;
   CUDA_TRY(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, d->device));
   CUDA_TRY(cudaMemsetAsync(d->best, 0, (size_t)V * sizeof(unsigned long long), st));
-  dm::k_dict_gemm<<<(unsigned)std::min(n_sm, m_tiles * n_tiles), dm::THREADS, dm::SMEM, st>>>(
-      tmx, tmd, w2, m_tiles, n_tiles, KD / dm::BK, (int)V, d->best);
+  const unsigned grid = (unsigned)std::min(n_sm, m_tiles * n_tiles);
+  if (KD / dm::BK == 1)   // short series (basis coordinates): two epilogue groups
+    dm::k_dict_gemm<2><<<grid, dm::threads<2>(), dm::SMEM, st>>>(tmx, tmd, w2, m_tiles, n_tiles, 1, (int)V, d->best);
+  else
+    dm::k_dict_gemm<1><<<grid, dm::threads<1>(), dm::SMEM, st>>>(tmx, tmd, w2, m_tiles, n_tiles, KD / dm::BK, (int)V,
+                                                                 d->best);
   MRF_TRY(check_launch("k_dict_gemm"));
   if (d->prof) {
     CUDA_TRY(cudaEventRecord(d->ev[d->ev_used + 1], st));

@@ -38,7 +38,11 @@ constexpr int UK = 16;           // UMMA K for kind::f16
 constexpr int STAGES = 4;
 constexpr int A_BYTES = BM * BK * 2;   // 16 KB
 constexpr int B_BYTES = BN * BK * 2;   // 32 KB
-constexpr int THREADS = 384;   // warps 0-3: TMA / MMA roles; 4-11: two epilogue groups
+// warps 0-3: TMA / MMA roles; then NG epilogue groups of 4 warps (NG = 1 for long series, where
+// the MMAs set the pace; NG = 2 for the 13-coefficient basis match, where the epilogue does)
+template <int NG>
+constexpr int threads() { return 128 + 128 * NG; }
+constexpr int THREADS = threads<1>();
 constexpr size_t SMEM = 1024 + (size_t)STAGES * (A_BYTES + B_BYTES) + 256;
 
 // instruction descriptor: kind::f16, fp16 A/B, fp32 D, both K-major, M = 128, N = 256
@@ -55,7 +59,8 @@ __device__ __forceinline__ void mma_f16(uint32_t tmem_d, uint64_t a, uint64_t b,
 // w2[k] = (m_k / ||d_k||)^2 (0 for padding atoms).  X~ [Vpad][KD] and D~ [NP][KD] fp16 are read
 // through the tensor maps; m_tiles = Vpad / BM, n_tiles = NP / BN, kblocks = KD / BK.  The
 // grid is persistent (one CTA per SM), so the m_tiles x n_tiles units quantise to < 1 %.
-__global__ void __launch_bounds__(THREADS, 1)
+template <int NG>
+__global__ void __launch_bounds__(threads<NG>(), 1)
 k_dict_gemm(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmd,
             const float* __restrict__ w2, int m_tiles, int n_tiles, int kblocks, int V,
             unsigned long long* __restrict__ best) {
@@ -79,7 +84,7 @@ k_dict_gemm(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUt
     }
     for (int a = 0; a < 2; ++a) {
       bar_init(&tfull[a], 1);
-      bar_init(&tempty[a], 8 * 32);
+      bar_init(&tempty[a], NG * 4 * 32);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -144,14 +149,17 @@ k_dict_gemm(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUt
       tc_fence_after();
       float bsc = -1.f;
       int bk = 0;
+      // CW columns (CW / 2 atoms) per TMEM load and wait: 128 with one group, 64 with two (registers)
+      constexpr int CW = NG == 1 ? 128 : 64;
 #pragma unroll 1
-      for (int ch = 0; ch < 2; ++ch) {   // 64 columns (32 atoms) per TMEM load and wait
-        float v[64];
-        const int col = grp * 128 + ch * 64;
-        tmem_ld64(tmem + lane_addr + (uint32_t)(acc * BN + col), v);
+      for (int ch = 0; ch < BN / NG / CW; ++ch) {
+        float v[CW];
+        const int col = grp * (BN / NG) + ch * CW;
+        if constexpr (CW == 128) tmem_ld128(tmem + lane_addr + (uint32_t)(acc * BN + col), v);
+        else tmem_ld64(tmem + lane_addr + (uint32_t)(acc * BN + col), v);
         const int k0 = nt * (BN / 2) + col / 2;
 #pragma unroll
-        for (int q = 0; q < 32; ++q) {
+        for (int q = 0; q < CW / 2; ++q) {
           const float sc = (v[2 * q] * v[2 * q] + v[2 * q + 1] * v[2 * q + 1]) * __ldg(w2 + k0 + q);
           if (sc > bsc) {   // strict: equal scores keep the lowest atom index
             bsc = sc;
