@@ -53,7 +53,7 @@ typedef enum {
   MRF_ENOMEM = 2,        /* device or host allocation failed                                    */
   MRF_ECUDA = 3,         /* CUDA runtime error (message in mrf_last_error)                      */
   MRF_ENCCL = 4,         /* NCCL unavailable or a collective failed                             */
-  MRF_EUNSUPPORTED = 5,  /* sigma != 2 or G = sigma*N not in {64,128,256,512,1024}             */
+  MRF_EUNSUPPORTED = 5,  /* sigma != 2, G = sigma*N not in {64,...,1024}, or unsupported mode  */
   MRF_ENUMERIC = 6       /* CG breakdown: Re<p, (A^H A + mu I) p> <= 0 or non-finite           */
 } mrf_status;
 
@@ -228,6 +228,19 @@ mrf_status mrf_dict_match_coef(mrf_dict dict, const void* u, long long V, int* i
  * basis is copied.  Errors: MRF_EINVAL, MRF_ENOMEM, MRF_ECUDA. */
 typedef struct mrf_llr_s* mrf_llr;
 mrf_status mrf_llr_create(mrf_dict dict, int N, int p, int s, mrf_llr* out);
+/* Frame sharding of the LLR operator (multi-GPU): the operator
+ * for frames [frame0, frame0 + L_local) of the dictionary's L, with those columns of its basis
+ * (the basis itself is the global one, so Phi_D on coefficients stays exact).  Used with a plan
+ * over the same frames (mrf_plan_desc.frame_offset = frame0) that carries the ranks' NCCL
+ * communicator: the coefficient projection Y = Z d^dagger (Eq. 17) is then a sum over ranks, done
+ * as an in-place ncclAllReduce of the [N*N][r] partials (8 N^2 r bytes) on the call's stream, so
+ * every rank holds all patches' coefficients and runs the SVT, the manifold term and the cost
+ * terms on them redundantly; the data term of mrf_llr_cost is all-reduced the same way.  Every
+ * rank must make the same calls in the same order.  mrf_msllr_solve then supports lambda1 = 0,
+ * max_iter >= 1 on gridding plans (MRF_EUNSUPPORTED otherwise: Phi_D of X^0 would need the frames
+ * of all ranks).  Errors: MRF_EINVAL (no basis, frame range outside [0, L)), MRF_ENOMEM, MRF_ECUDA. */
+mrf_status mrf_llr_create_shard(mrf_dict dict, int frame0, int L_local, int N, int p, int s, mrf_llr* out);
+
 /* The same with a caller-supplied basis: HOST [r][L] complex64 with orthonormal rows (copied),
  * 1 <= r <= 32.  Phi_D inside mrf_msllr_solve then always runs on the frames. */
 mrf_status mrf_llr_create_basis(const void* basis, int r, int L, int N, int p, int s, int device, mrf_llr* out);

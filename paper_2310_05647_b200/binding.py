@@ -34,7 +34,7 @@ EXPORTED = [
     "mrf_adjoint_dcf", "mrf_dcf_weights", "mrf_dict_create", "mrf_dict_match", "mrf_dict_destroy",
     "mrf_dict_profile", "mrf_dict_profile_query", "mrf_dict_basis", "mrf_dict_basis_copy", "mrf_llr_create",
     "mrf_llr_step", "mrf_llr_destroy", "mrf_llr_laplacian", "mrf_llr_cost", "mrf_msllr_solve", "mrf_plan_wait",
-    "mrf_dict_match_coef", "mrf_llr_create_basis", "mrf_llr_subspace_normal",
+    "mrf_dict_match_coef", "mrf_llr_create_basis", "mrf_llr_subspace_normal", "mrf_llr_create_shard",
 ]
 
 
@@ -107,6 +107,7 @@ def _load() -> ctypes.CDLL:
         "mrf_dict_basis_copy": ([vp, vp], ci),
         "mrf_llr_create": ([vp, ci, ci, ci, ctypes.POINTER(vp)], ci),
         "mrf_llr_create_basis": ([vp, ci, ci, ci, ci, ci, ci, ctypes.POINTER(vp)], ci),
+        "mrf_llr_create_shard": ([vp, ci, ci, ci, ci, ci, ctypes.POINTER(vp)], ci),
         "mrf_llr_subspace_normal": ([vp, vp, vp, vp, vp], ci),
         "mrf_llr_step": ([vp, vp, vp, vp, cf, cf, cf, cf, vp, ctypes.POINTER(ctypes.c_double),
                           ctypes.POINTER(ctypes.c_double), vp], ci),
@@ -449,6 +450,20 @@ class LLR:
                                         int(s), dev, ctypes.byref(h)))
         self._h = h
         self.N, self.L, self.r = int(N), d.shape[1], d.shape[0]
+        return self
+
+    @classmethod
+    def shard(cls, dictionary: "Dictionary", frame0: int, L_local: int, N: int, p: int = 11,
+              s: int = 5) -> "LLR":
+        """The operator for frames [frame0, frame0 + L_local) of the dictionary's basis
+        (mrf_llr_create_shard); with a plan carrying the ranks' NCCL communicator the coefficient
+        partials are all-reduced inside every call."""
+        self = cls.__new__(cls)
+        h = ctypes.c_void_p()
+        _check(lib.mrf_llr_create_shard(dictionary._h, int(frame0), int(L_local), int(N), int(p), int(s),
+                                        ctypes.byref(h)))
+        self._h = h
+        self.N, self.L, self.r = int(N), int(L_local), None
         return self
 
     def subspace_normal(self, plan: "Plan", u, z=None):

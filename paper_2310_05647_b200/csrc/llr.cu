@@ -19,6 +19,7 @@
 #include "gemm3.cuh"
 #include "llr.cuh"
 #include "status.h"
+#include "nccl_dl.h"
 
 using namespace mrf;
 
@@ -26,6 +27,10 @@ static constexpr int kStatBlocks = 4 * 148;   // blocks of the grid-stride reduc
 
 struct mrf_llr_s {
   int N = 0, L = 0, p = 0, s = 0, r = 0, nc = 0, device = 0;
+  // frame sharding (mrf_llr_create_shard): this operator owns frames [frame0, frame0 + L) of Lg;
+  // comm = the plan's ncclComm_t of the last call (coefficient partials are all-reduced)
+  int frame0 = 0, Lg = 0;
+  void* comm = nullptr;
   float2* dT = nullptr;       // [L][R] transposed basis, rows zero-padded to R = 16 or 32
   int* corners = nullptr;     // [nc]
   float2* Y = nullptr;        // [N*N][r] coefficients of Z
@@ -159,7 +164,20 @@ static mrf_status manifold_G(mrf_llr_s* h, const float2* coef, cudaStream_t st, 
   return check_launch("k_g3_gemm");
 }
 
-// coefficients Y = (x - mu (nx - rhs)) d^dagger and, with yx, also x d^dagger
+// In-place sum over the ranks of the plan's communicator (frame sharding): no-op without one.
+static mrf_status allreduce(mrf_llr_s* h, void* buf, size_t n, int dtype, cudaStream_t st) {
+  if (!h->comm) return MRF_OK;
+  const char* why = nullptr;
+  const NcclApi* api = nccl_api(&why);
+  if (!api) return fail(MRF_ENCCL, why);
+  const int rc = api->AllReduce(buf, buf, n, dtype, kNcclSum, h->comm, st);
+  if (rc != 0) return fail(MRF_ENCCL, std::string("ncclAllReduce: ") + api->GetErrorString(rc));
+  return MRF_OK;
+}
+
+// coefficients Y = (x - mu (nx - rhs)) d^dagger and, with yx, also x d^dagger.  Frame-sharded:
+// each rank's kernel sums its own frames; the [V][r] partials (6.8 MB at the MRF size, instead of
+// re-sharding the 524 MB frame stack to patches) are all-reduced, so every rank holds all of Y.
 static mrf_status coefs(mrf_llr_s* h, const float2* x, const float2* nx, const float2* rhs, float mu, float2* y,
                         float2* yx, cudaStream_t st) {
   const int V = h->N * h->N;
@@ -171,7 +189,10 @@ static mrf_status coefs(mrf_llr_s* h, const float2* x, const float2* nx, const f
     if (yx) llr::k_llr_coef<32, true><<<gv, 32 * llr::coef_groups<32>(), 0, st>>>(x, nx, rhs, h->dT, h->r, h->L, V, mu, y, yx);
     else llr::k_llr_coef<32, false><<<gv, 32 * llr::coef_groups<32>(), 0, st>>>(x, nx, rhs, h->dT, h->r, h->L, V, mu, y, nullptr);
   }
-  return check_launch("k_llr_coef");
+  MRF_TRY(check_launch("k_llr_coef"));
+  MRF_TRY(allreduce(h, y, (size_t)V * h->r * 2, kNcclFloat32, st));
+  if (yx) MRF_TRY(allreduce(h, yx, (size_t)V * h->r * 2, kNcclFloat32, st));
+  return MRF_OK;
 }
 
 // per-patch SVT of the coefficient blocks of Y (nuclear norms into h->nuc, thresholded blocks into h->P)
@@ -226,6 +247,7 @@ static mrf_status check_plan(mrf_llr_s* h, mrf_plan plan, const char* who) {
   plan_dims(plan, &pN, &pL, &pC, &pdev);
   if (pN != h->N || pL != h->L || pdev != h->device)
     return fail(MRF_EINVAL, std::string(who) + ": the plan's N, L or device differ from the LLR operator's");
+  h->comm = plan_comm(plan);
   return MRF_OK;
 }
 
@@ -238,7 +260,7 @@ static mrf_status create_impl(const float2* basis_h, int r, int L, int device, u
   *out = nullptr;
   CUDA_TRY(cudaSetDevice(device));
   auto* h = new mrf_llr_s();
-  h->N = N; h->L = L; h->p = p; h->s = s; h->r = r; h->device = device;
+  h->N = N; h->L = L; h->Lg = L; h->p = p; h->s = s; h->r = r; h->device = device;
   std::vector<int> c;   // patch corners 0, s, 2s, ... and N - p (reading 25)
   for (int v = 0; v + p <= N; v += s) c.push_back(v);
   if (c.back() != N - p) c.push_back(N - p);
@@ -296,6 +318,22 @@ mrf_status mrf_llr_create(mrf_dict dict, int N, int p, int s, mrf_llr* out) {
     return fail(MRF_EINVAL, "mrf_llr_create: invalid arguments");
   if (!dict->rank) return fail(MRF_EINVAL, "mrf_llr_create: the dictionary has no basis (call mrf_dict_basis)");
   return create_impl(dict->basis_h.data(), dict->rank, dict->L, dict->device, dict->basis_gen, N, p, s, out);
+}
+
+mrf_status mrf_llr_create_shard(mrf_dict dict, int frame0, int L_local, int N, int p, int s, mrf_llr* out) {
+  if (!dict || !out || N < 2 || p < 1 || p > N || s < 1 || p * p > 1024)
+    return fail(MRF_EINVAL, "mrf_llr_create_shard: invalid arguments");
+  if (!dict->rank) return fail(MRF_EINVAL, "mrf_llr_create_shard: the dictionary has no basis (call mrf_dict_basis)");
+  if (frame0 < 0 || L_local < 1 || frame0 + L_local > dict->L)
+    return fail(MRF_EINVAL, "mrf_llr_create_shard: frames [frame0, frame0 + L_local) must lie in [0, L)");
+  const int r = dict->rank, L = dict->L;
+  std::vector<float2> cols((size_t)r * L_local);   // the shard's columns of the global basis
+  for (int i = 0; i < r; ++i)
+    std::memcpy(&cols[(size_t)i * L_local], &dict->basis_h[(size_t)i * L + frame0], (size_t)L_local * sizeof(float2));
+  MRF_TRY(create_impl(cols.data(), r, L_local, dict->device, dict->basis_gen, N, p, s, out));
+  (*out)->frame0 = frame0;
+  (*out)->Lg = L;
+  return MRF_OK;
 }
 
 mrf_status mrf_llr_create_basis(const void* basis, int r, int L, int N, int p, int s, int device, mrf_llr* out) {
@@ -496,6 +534,7 @@ static mrf_status cost_impl(mrf_llr h, mrf_plan plan, const void* x, const void*
   MRF_TRY(mrf_forward(plan, x, h->yb, stream));
   llr::k_llr_resid<<<kStatBlocks, 256, 0, st>>>(h->yb, (const float2*)b, ny, h->part);
   MRF_TRY(check_launch("k_llr_resid"));
+  MRF_TRY(allreduce(h, h->part, kStatBlocks, kNcclFloat64, st));   // the data term over all ranks' frames
   double t[3] = {0.0, 0.0, 0.0};
   Sums sums{h, st};
   MRF_TRY(sums.add(h->part, kStatBlocks, &t[0]));
@@ -638,7 +677,7 @@ mrf_status mrf_msllr_solve(mrf_llr h, mrf_dict dict, mrf_plan plan, const void* 
   if (!h || !dict || !plan || !b || !prm || !x || !index || !pd) return fail(MRF_EINVAL, "mrf_msllr_solve: null argument");
   if (!(prm->mu > 0.f) || !(prm->lambda1 >= 0.f) || !(prm->lambda2 >= 0.f) || !(prm->beta > 0.f) || prm->max_iter < 0)
     return fail(MRF_EINVAL, "mrf_msllr_solve: need mu > 0, lambda1 >= 0, lambda2 >= 0, beta > 0, max_iter >= 0");
-  if (dict->L != h->L || dict->device != h->device)
+  if (dict->L != h->Lg || dict->device != h->device)
     return fail(MRF_EINVAL, "mrf_msllr_solve: the dictionary's L or device differ from the LLR operator's");
   const bool manifold = prm->lambda1 > 0.f;
   if (manifold && (dict->P != 2 || !params))
@@ -663,6 +702,14 @@ mrf_status mrf_msllr_solve(mrf_llr h, mrf_dict dict, mrf_plan plan, const void* 
   // Toeplitz plans: from n = 2 on the loop runs in basis coordinates (the subspace normal, the
   // cost by the inner-product identity; frames only for X^0, the first step and the output)
   const bool sub = plan_toeplitz(plan) && coef_ok;
+  // frame-sharded (a communicator, or a shard of the dictionary's frames): Phi_D can only run on
+  // the all-reduced coefficients, so X^0 = A^* b (not in span(d)) is never matched
+  if (h->comm || h->L != h->Lg) {
+    if (sub) return fail(MRF_EUNSUPPORTED, "mrf_msllr_solve: frame sharding needs a gridding plan (not MRF_NORMAL_TOEPLITZ)");
+    if (!coef_ok) return fail(MRF_EUNSUPPORTED, "mrf_msllr_solve: frame sharding needs the dictionary's own basis");
+    if (manifold || prm->max_iter < 1)
+      return fail(MRF_EUNSUPPORTED, "mrf_msllr_solve: frame sharding needs lambda1 = 0 and max_iter >= 1 (Phi_D of X^0)");
+  }
   double b2 = 0.0;
   if (sub) {
     int pN = 0, pL = 0, pC = 0, pdev = 0, pM = 0;

@@ -848,6 +848,7 @@ void mrf::plan_dims(mrf_plan pl, int* N, int* L, int* C, int* device, int* M) {
 
 // ---------------------------------------------------------------------------- subspace normal
 // (gridding.cuh k_sn_*; used by mrf_msllr_solve on Toeplitz plans, llr.cu)
+void* mrf::plan_comm(mrf_plan pl) { return pl->nccl_comm; }
 bool mrf::plan_toeplitz(mrf_plan pl) { return (pl->flags & MRF_NORMAL_TOEPLITZ) != 0 && pl->psf; }
 unsigned long long mrf::plan_serial(mrf_plan pl) { return pl->serial; }
 long long mrf::sn_elems(mrf_plan pl) { return (long long)pl->G * pl->G; }

@@ -7,7 +7,7 @@ namespace mrf {
 
 typedef struct { char internal[128]; } NcclUniqueId;
 typedef void* NcclComm;
-enum { kNcclFloat64 = 8, kNcclSum = 0 };
+enum { kNcclFloat32 = 7, kNcclFloat64 = 8, kNcclSum = 0 };
 
 struct NcclApi {
   int (*GetUniqueId)(NcclUniqueId*);

@@ -19,6 +19,7 @@ void plan_dims(mrf_plan plan, int* N, int* L, int* C, int* device, int* M = null
 // kernels from the basis rows (host [r][L]); apply: Z = P_S A^H A (U d) in coefficients, U and Z
 // DEVICE [r][N][N], spectra workspaces [r][C][G*G] each.
 bool plan_toeplitz(mrf_plan plan);
+void* plan_comm(mrf_plan plan);   // the plan's ncclComm_t or nullptr
 unsigned long long plan_serial(mrf_plan plan);   // process-wide creation number of the plan
 long long sn_elems(mrf_plan plan);
 mrf_status sn_build(mrf_plan plan, const float2* basis_h, int r, float2* K, cudaStream_t st);

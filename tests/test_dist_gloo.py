@@ -90,3 +90,73 @@ def test_sharded_cg_equals_unsharded_gloo():
     x_ref, hist_ref = ocg.cg(H, rhs, np.zeros_like(rhs), cfg.cg_iters)
     assert np.linalg.norm(x_sh - x_ref) <= 1e-12 * np.linalg.norm(x_ref)
     assert np.allclose(res[0][3], hist_ref, rtol=1e-12, atol=0)
+
+
+# ------------------------------------------------------- frame-sharded LLR step
+_LN, _LL, _LP, _LS = 16, 12, 5, 2     # N, L, patch, stride of the small LLR case
+
+
+def _llr_case():
+    from oracle import llr as ol
+    rng = np.random.default_rng(41)
+    traj = synth.spiral_trajectory(96, 4, 4, 1.5)
+    t = rng.standard_normal((3, _LL)) + 1j * rng.standard_normal((3, _LL))
+    amps = rng.standard_normal((3, _LN, _LN)) + 1j * rng.standard_normal((3, _LN, _LN))
+    X = np.einsum("kl,kyx->lyx", t, amps) + 0.1 * (rng.standard_normal((_LL, _LN, _LN)) + 0j)
+    rhs = rng.standard_normal((_LL, _LN, _LN)) + 1j * rng.standard_normal((_LL, _LN, _LN))
+    D = np.concatenate([t, rng.standard_normal((6, _LL)) + 1j * rng.standard_normal((6, _LL))])
+    d = ol.basis(D, 0.9999, 8)
+    return traj, X, rhs, d
+
+
+def _llr_worker(rank, world, port, out_q):
+    """The decomposition mrf_llr_create_shard implements: each rank forms the projected gradient
+    on its own frames, the coefficient partials Y_rank = Z_rank d_rank^dagger are all-reduced (the
+    only exchange), every rank runs the patch SVT on the full Y (SVT(Q_q(Y d)) = SVT(Y_q) d for
+    orthonormal rows of d), and expands the update on its own frames."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from oracle import llr as ol, nufft as on
+    traj, X, rhs, d = _llr_case()
+    off, cnt = frame_shard(_LL, world, rank)
+    Xl, rl, dl = X[off:off + cnt], rhs[off:off + cnt], d[:, off:off + cnt]
+    mu, lam2, beta = 0.02, 0.3, 0.5
+    Z = Xl - mu * (on.normal(Xl, traj, None, 6, frame_offset=off) - rl)
+    Yp = Z.reshape(cnt, -1).T @ np.conj(dl).T                           # [V][r] partial
+    t = torch.from_numpy(np.stack([Yp.real, Yp.imag]))
+    dist.all_reduce(t)
+    Y = t[0].numpy() + 1j * t[1].numpy()
+    Yi = Y.reshape(_LN, _LN, -1)
+    acc = np.zeros_like(Yi)
+    cnt_p = np.zeros((_LN, _LN))
+    gamma = mu * lam2 * beta
+    for y0 in ol.patch_corners(_LN, _LP, _LS):
+        for x0 in ol.patch_corners(_LN, _LP, _LS):
+            Yq = Yi[y0:y0 + _LP, x0:x0 + _LP].reshape(_LP * _LP, -1)
+            acc[y0:y0 + _LP, x0:x0 + _LP] += ol.svt(Yq, 1.0 / beta).reshape(_LP, _LP, -1)
+            cnt_p[y0:y0 + _LP, x0:x0 + _LP] += 1.0
+    Xc = (Yi + gamma * acc) / (1.0 + gamma * cnt_p)[..., None]
+    out_q.put((rank, np.einsum("yxr,rl->lyx", Xc, dl)))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_sharded_llr_step_equals_unsharded_gloo():
+    from oracle import llr as ol, nufft as on
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_llr_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    res.sort(key=lambda t: t[0])
+    x_sh = np.concatenate([r[1] for r in res])
+    traj, X, rhs, d = _llr_case()
+    ref, _ = ol.llr_step(X, rhs, lambda v: on.normal(v, traj, None, 6), d, 0.02, 0.3, 0.5, _LP, _LS)
+    assert np.linalg.norm(x_sh - ref) <= 1e-10 * np.linalg.norm(ref)

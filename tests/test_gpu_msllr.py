@@ -293,3 +293,72 @@ def test_solve_without_cost_monitoring(binding, problem1, normal):
     assert _rel(c["x"].cpu().numpy(), a["x"].cpu().numpy()) <= 1e-6
     assert torch.equal(c["index"], a["index"])
     pl.close(), op.close(), dic.close()
+
+
+# ------------------------------------------------------------------ frame sharding
+def _comm1(binding):
+    import ctypes
+    buf = (ctypes.c_ubyte * 128)()
+    assert binding.lib.mrf_nccl_get_unique_id(ctypes.cast(buf, ctypes.c_void_p)) == 0, binding.lib.mrf_last_error()
+    comm = ctypes.c_void_p()
+    assert binding.lib.mrf_nccl_comm_init(ctypes.byref(comm), 1, ctypes.cast(buf, ctypes.c_void_p), 0,
+                                          torch.cuda.current_device()) == 0, binding.lib.mrf_last_error()
+    return comm.value
+
+
+def test_shard_takes_its_columns_of_the_basis(binding, problem):
+    """mrf_llr_create_shard(dict, f0, Ll) on a plan over frames [f0, f0 + Ll) (frame_offset = f0)
+    is the operator of the basis columns [f0, f0 + Ll): bit-identical to mrf_llr_create_basis with
+    that slice (no communicator: the coefficients are this shard's partial sums)."""
+    pr = problem
+    dic = binding.Dictionary(pr["D"], pr["lut"])
+    d = dic.basis(0.9999, 32)
+    f0, Ll = 21, 25
+    sh = binding.LLR.shard(dic, f0, Ll, N, P, S)
+    ref = binding.LLR.from_basis(d[:, f0:f0 + Ll], N, P, S)
+    pl = binding.Plan(N, pr["traj"], Ll, W=W, frame_offset=f0)
+    rng = np.random.default_rng(5)
+    x = torch.from_numpy((rng.standard_normal((Ll, N, N)) + 1j * rng.standard_normal((Ll, N, N))).astype(np.complex64)).cuda()
+    rhs = torch.from_numpy((rng.standard_normal((Ll, N, N)) + 1j * rng.standard_normal((Ll, N, N))).astype(np.complex64)).cuda()
+    a, na, _ = sh.step(pl, x, rhs, mu=pr["mu"], lam2=0.05, beta=0.5)
+    b, nb, _ = ref.step(pl, x, rhs, mu=pr["mu"], lam2=0.05, beta=0.5)
+    torch.cuda.synchronize()
+    assert torch.equal(a, b) and na == nb
+    # the full range is the unsharded operator
+    full, one = binding.LLR.shard(dic, 0, L, N, P, S), binding.LLR(dic, N, P, S)
+    pl2 = binding.Plan(N, pr["traj"], L, W=W)
+    xb = torch.from_numpy(on.adjoint(pr["b"], pr["traj"], None, N, W).astype(np.complex64)).cuda()
+    assert torch.equal(full.step(pl2, xb, xb, mu=pr["mu"])[0], one.step(pl2, xb, xb, mu=pr["mu"])[0])
+    with pytest.raises(binding.MrfError):
+        binding.LLR.shard(dic, 50, 20, N, P, S)                  # frames beyond L
+    for o in (sh, ref, full, one, pl, pl2, dic):
+        o.close()
+
+
+def test_sharded_solve_through_a_single_rank_communicator(binding, problem):
+    """Algorithm 1 (lambda_1 = 0) on a frame-sharded operator whose plan carries a 1-rank NCCL
+    communicator: the coefficient and data-term all-reduces run, and with one rank the result is
+    the unsharded solve's, bit for bit.  Unsupported sharded modes fail loudly."""
+    pr = problem
+    comm = _comm1(binding)
+    try:
+        dic = binding.Dictionary(pr["D"], pr["lut"])
+        dic.basis(0.9999, 32)
+        b = torch.from_numpy(pr["b"].astype(np.complex64)).cuda()
+        kw = dict(mu=pr["mu"], lam1=0.0, lam2=0.05, beta=0.5, max_iter=3, tol=0.0)
+        sh, pl_c = binding.LLR.shard(dic, 0, L, N, P, S), binding.Plan(N, pr["traj"], L, W=W, nccl_comm=comm)
+        one, pl = binding.LLR(dic, N, P, S), binding.Plan(N, pr["traj"], L, W=W)
+        a = sh.solve(dic, pl_c, b, **kw)
+        c = one.solve(dic, pl, b, **kw)
+        torch.cuda.synchronize()
+        assert torch.equal(a["x"], c["x"]) and torch.equal(a["index"], c["index"])
+        assert a["cost"] == c["cost"] and a["iters"] == 3
+        with pytest.raises(binding.MrfError):                     # Phi_D of X^0 needs every rank's frames
+            sh.solve(dic, pl_c, b, **{**kw, "lam1": 2e-3})
+        pl_t = binding.Plan(N, pr["traj"], L, W=W, normal="toeplitz", nccl_comm=comm)
+        with pytest.raises(binding.MrfError):                     # basis coordinates are not frame-sharded
+            sh.solve(dic, pl_t, b, **kw)
+        for o in (sh, pl_c, one, pl, pl_t, dic):
+            o.close()
+    finally:
+        binding.nccl_comm_destroy(comm)
