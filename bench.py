@@ -164,6 +164,24 @@ def step_bytes(cfg, L: int, n_iter: int) -> float:
     return L * (8.0 * N * N + 8.0 * C * M) + n_iter * 2 * img + 3 * img + n_iter * 8 * img
 
 
+def cpu_model():
+    """The host CPU model (lscpu "Model name", else /proc/cpuinfo)."""
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for ln in out.splitlines():
+            if ln.lower().startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
 def cpu_count():
     try:
         return len(os.sched_getaffinity(0))
@@ -232,8 +250,8 @@ def run_reference(args):
         "config": {"workload": cfg.name, "N": cfg.N, "L": cfg.L, "M": cfg.M, "C": cfg.C, "W": cfg.W,
                    "sigma": cfg.sigma, "cg_iters": n_iter, "mu": cfg.mu,
                    "step": "oracle dc_cg on a frame sample; ms_per_step extrapolated to all L frames"},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": last["cores"], "kind": "oracle",
-                         "sample": last["sample"]},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": last["cores"], "cpu_model": cpu_model(),
+                         "kind": "oracle", "sample": last["sample"]},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -250,6 +268,10 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}: launch one rank per GPU")
+    if torch.cuda.device_count() < world:
+        raise SystemExit(f"bench.py: {world} ranks need {world} GPUs, found {torch.cuda.device_count()}")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     comm = None
@@ -337,7 +359,9 @@ def run_ours(args):
     ms_normal = time_op(lambda: plan.normal(xin, mu=cfg.mu, out=xout), reps)
     ms_fwd = time_op(lambda: plan.forward(xin, y=yout), reps)
     ms_adj = time_op(lambda: plan.adjoint(y, x=xout), reps)
-    ms_cg_iter = max(0.0, (ms_step - ms_adj - ms_normal) / max(1, n_iter))
+    # the timed step runs from x0 = 0 (MRF_CG_ZERO_INIT): 1 adjoint for the rhs, then n_iter
+    # iterations (no normal operator for the initial residual)
+    ms_cg_iter = max(0.0, (ms_step - ms_adj) / max(1, n_iter))
     # cuFFT reference (timing only, never in the product path): batched C2C G x G, L*C transforms
     cufft_ms = None
     try:
@@ -548,10 +572,11 @@ def run_ours(args):
     gpu_launches = int(sum(prof[k][1] for k in ("fwd_rows", "fwd_cols", "adj_cols", "adj_rows", "cg_vec")))
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and not args.no_cpu_baseline:   # after every timed region; the other ranks wait
         o = oracle_sample(cfg, n_iter, args.cpu_seconds)
-        cpu = {"value": o["value"], "unit": UNIT, "cores": o["cores"], "kind": "oracle", "sample": o["sample"],
-               "seconds": o["seconds"]}
+        cpu = {"value": o["value"], "unit": UNIT, "cores": o["cores"], "cpu_model": cpu_model(), "kind": "oracle",
+               "sample": o["sample"], "seconds": o["seconds"]}
+    barrier()
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -582,10 +607,38 @@ def run_ours(args):
     return 0
 
 
+def _spawned_rank(local: int, world: int, port: int, argv):
+    """Entry of a rank started by bench.py itself (``--gpus N`` without torchrun)."""
+    os.environ.update(RANK=str(local), LOCAL_RANK=str(local), WORLD_SIZE=str(world),
+                      LOCAL_WORLD_SIZE=str(world), MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    sys.argv = argv
+    rc = run_ours(parse())
+    if rc:
+        raise SystemExit(rc)
+
+
+def spawn_ranks(args) -> int:
+    """``python bench.py --gpus N`` (N > 1) outside torchrun: one process per GPU, the same
+    environment torchrun would give them (RANK / LOCAL_RANK / WORLD_SIZE / MASTER_*)."""
+    import socket
+    import torch
+    import torch.multiprocessing as mp
+    n = torch.cuda.device_count()
+    if n < args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} needs {args.gpus} GPUs, found {n}")
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    mp.spawn(_spawned_rank, args=(args.gpus, port, list(sys.argv)), nprocs=args.gpus, join=True)
+    return 0
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         return run_reference(args)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn_ranks(args)
     return run_ours(args)
 
 

@@ -178,6 +178,27 @@ mrf_status mrf_nccl_get_unique_id(void* id_out128);
 mrf_status mrf_nccl_comm_init(void** comm_out, int nranks, const void* id128, int rank, int device);
 mrf_status mrf_nccl_comm_destroy(void* comm);
 
+/* ---- host-side reduction hook (frame sharding without NCCL) -------------------------------
+ * The frame-sharded solve (the operator is block-diagonal over frames,
+ * PAPER.md:60, so the only coupling between ranks is the sum over frames inside the CG inner
+ * products and the coefficient projection of mrf_llr_step) needs one primitive: an in-place
+ * SUM of a small buffer over all ranks.  By default it is ncclAllReduce on the plan's
+ * communicator (mrf_plan_desc.nccl_comm).  mrf_plan_set_host_allreduce replaces it by a host
+ * callback, for process layouts NCCL cannot serve (several ranks on one GPU: the multi-rank
+ * tests, or a gloo/MPI job): every all-reduce the plan (and an mrf_llr operator called with it)
+ * performs then copies the device buffer into plan-owned pinned host memory on the call's
+ * stream, synchronises the stream, calls fn(buf, count, dtype, ctx) -- which must replace the
+ * `count` elements at `buf` (HOST) by their sum over all ranks and return 0 -- and copies the
+ * result back.  dtype is MRF_DTYPE_F32 or MRF_DTYPE_F64.  The calls happen on the calling
+ * thread in the same order on every rank; a non-zero return makes the operation fail with
+ * MRF_ENCCL.  This inserts host synchronisations, so such a plan's mrf_dc_cg is not CUDA-graph
+ * capturable.  fn = NULL restores the plan's NCCL communicator (or no reduction).
+ * Errors: MRF_EINVAL (null plan). */
+#define MRF_DTYPE_F32 0
+#define MRF_DTYPE_F64 1
+typedef int (*mrf_host_allreduce_fn)(void* buf, size_t count, int dtype, void* ctx);
+mrf_status mrf_plan_set_host_allreduce(mrf_plan plan, mrf_host_allreduce_fn fn, void* ctx);
+
 /* ---- dictionary matching Phi_D (Eqs. (4)-(5)) -------------
  *
  *   k_v   = argmax_k |<d_k, x_v>| / ||d_k||_2        ties -> lowest k   (reading 21)

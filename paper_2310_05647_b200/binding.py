@@ -35,7 +35,13 @@ EXPORTED = [
     "mrf_dict_profile", "mrf_dict_profile_query", "mrf_dict_basis", "mrf_dict_basis_copy", "mrf_llr_create",
     "mrf_llr_step", "mrf_llr_destroy", "mrf_llr_laplacian", "mrf_llr_cost", "mrf_msllr_solve", "mrf_plan_wait",
     "mrf_dict_match_coef", "mrf_llr_create_basis", "mrf_llr_subspace_normal", "mrf_llr_create_shard",
+    "mrf_plan_set_host_allreduce",
 ]
+
+MRF_DTYPE_F32 = 0
+MRF_DTYPE_F64 = 1
+# int (*)(void* buf, size_t count, int dtype, void* ctx)
+HOST_ALLREDUCE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int, ctypes.c_void_p)
 
 
 class MrfError(RuntimeError):
@@ -97,6 +103,7 @@ def _load() -> ctypes.CDLL:
         "mrf_nccl_get_unique_id": ([vp], ci),
         "mrf_nccl_comm_init": ([ctypes.POINTER(vp), ci, vp, ci, ci], ci),
         "mrf_nccl_comm_destroy": ([vp], ci),
+        "mrf_plan_set_host_allreduce": ([vp, HOST_ALLREDUCE_FN, vp], ci),
         "mrf_dict_create": ([vp, vp, ci, ci, ci, ci, ctypes.POINTER(vp)], ci),
         "mrf_dict_match": ([vp, vp, ctypes.c_longlong, vp, vp, vp, vp], ci),
         "mrf_dict_match_coef": ([vp, vp, ctypes.c_longlong, vp, vp, vp, vp], ci),
@@ -285,6 +292,31 @@ class Plan:
         it = info.iters
         return x, {"iters": it, "rel_resid": info.rel_resid, "history": list(hist)[: it + 1],
                    "alpha": list(ha)[:it], "beta": list(hb)[:it]}
+
+    def set_host_allreduce(self, fn):
+        """Route the plan's rank reductions through a host callable (mrf_plan_set_host_allreduce).
+
+        ``fn(buf)`` receives a numpy float32/float64 array view of the library's pinned staging
+        buffer and must replace it in place by its sum over all ranks (e.g. a gloo
+        ``torch.distributed.all_reduce`` on ``torch.from_numpy(buf)``).  ``fn=None`` restores NCCL."""
+        if fn is None:
+            self._host_ar = None
+            _check(lib.mrf_plan_set_host_allreduce(self._h, HOST_ALLREDUCE_FN(), None))
+            return
+
+        def tramp(buf, count, dtype, _ctx):
+            try:
+                ct = ctypes.c_double if dtype == MRF_DTYPE_F64 else ctypes.c_float
+                arr = np.ctypeslib.as_array(ctypes.cast(buf, ctypes.POINTER(ct)), shape=(int(count),))
+                fn(arr)
+                return 0
+            except Exception:   # reported to the library as MRF_ENCCL
+                import traceback
+                traceback.print_exc()
+                return 1
+
+        self._host_ar = HOST_ALLREDUCE_FN(tramp)   # keep the trampoline alive with the plan
+        _check(lib.mrf_plan_set_host_allreduce(self._h, self._host_ar, None))
 
     def wait(self):
         """Waits for the result copies of async_host solves (mrf_plan_wait)."""

@@ -6,6 +6,8 @@
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
+#include <atomic>
+
 #include <algorithm>
 #include <cmath>
 #include <complex>
@@ -406,7 +408,10 @@ extern "C" mrf_status mrf_dict_basis(mrf_dict d, double energy, int max_rank, in
   CUDA_TRY(cudaMemcpy(d->basis, d->basis_h.data(), d->basis_h.size() * sizeof(float2), cudaMemcpyHostToDevice));
   MRF_TRY(build_coef_dict(d, r));
   d->rank = r;
-  ++d->basis_gen;
+  // process-wide generation: two dictionaries (or two bases of one) never share a value, so an
+  // LLR operator recognises exactly the basis it was built from (mrf_msllr_solve's coef_ok)
+  static std::atomic<unsigned> basis_counter{0};
+  d->basis_gen = ++basis_counter;
   *rank_out = r;
   return MRF_OK;
 }

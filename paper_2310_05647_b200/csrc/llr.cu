@@ -19,7 +19,6 @@
 #include "gemm3.cuh"
 #include "llr.cuh"
 #include "status.h"
-#include "nccl_dl.h"
 
 using namespace mrf;
 
@@ -28,9 +27,10 @@ static constexpr int kStatBlocks = 4 * 148;   // blocks of the grid-stride reduc
 struct mrf_llr_s {
   int N = 0, L = 0, p = 0, s = 0, r = 0, nc = 0, device = 0;
   // frame sharding (mrf_llr_create_shard): this operator owns frames [frame0, frame0 + L) of Lg;
-  // comm = the plan's ncclComm_t of the last call (coefficient partials are all-reduced)
+  // comm = the plan of the last call when it reduces over ranks (NCCL communicator or host
+  // hook; the coefficient partials are all-reduced through it), else nullptr
   int frame0 = 0, Lg = 0;
-  void* comm = nullptr;
+  mrf_plan comm = nullptr;
   float2* dT = nullptr;       // [L][R] transposed basis, rows zero-padded to R = 16 or 32
   int* corners = nullptr;     // [nc]
   float2* Y = nullptr;        // [N*N][r] coefficients of Z
@@ -167,12 +167,7 @@ static mrf_status manifold_G(mrf_llr_s* h, const float2* coef, cudaStream_t st, 
 // In-place sum over the ranks of the plan's communicator (frame sharding): no-op without one.
 static mrf_status allreduce(mrf_llr_s* h, void* buf, size_t n, int dtype, cudaStream_t st) {
   if (!h->comm) return MRF_OK;
-  const char* why = nullptr;
-  const NcclApi* api = nccl_api(&why);
-  if (!api) return fail(MRF_ENCCL, why);
-  const int rc = api->AllReduce(buf, buf, n, dtype, kNcclSum, h->comm, st);
-  if (rc != 0) return fail(MRF_ENCCL, std::string("ncclAllReduce: ") + api->GetErrorString(rc));
-  return MRF_OK;
+  return plan_allreduce(h->comm, buf, n, dtype, st);
 }
 
 // coefficients Y = (x - mu (nx - rhs)) d^dagger and, with yx, also x d^dagger.  Frame-sharded:
@@ -190,8 +185,8 @@ static mrf_status coefs(mrf_llr_s* h, const float2* x, const float2* nx, const f
     else llr::k_llr_coef<32, false><<<gv, 32 * llr::coef_groups<32>(), 0, st>>>(x, nx, rhs, h->dT, h->r, h->L, V, mu, y, nullptr);
   }
   MRF_TRY(check_launch("k_llr_coef"));
-  MRF_TRY(allreduce(h, y, (size_t)V * h->r * 2, kNcclFloat32, st));
-  if (yx) MRF_TRY(allreduce(h, yx, (size_t)V * h->r * 2, kNcclFloat32, st));
+  MRF_TRY(allreduce(h, y, (size_t)V * h->r * 2, MRF_DTYPE_F32, st));
+  if (yx) MRF_TRY(allreduce(h, yx, (size_t)V * h->r * 2, MRF_DTYPE_F32, st));
   return MRF_OK;
 }
 
@@ -247,7 +242,11 @@ static mrf_status check_plan(mrf_llr_s* h, mrf_plan plan, const char* who) {
   plan_dims(plan, &pN, &pL, &pC, &pdev);
   if (pN != h->N || pL != h->L || pdev != h->device)
     return fail(MRF_EINVAL, std::string(who) + ": the plan's N, L or device differ from the LLR operator's");
-  h->comm = plan_comm(plan);
+  // a shard's basis columns are frames [frame0, frame0 + L) of the dictionary: the plan must hold
+  // the same global frames, or the coefficient all-reduce would sum misaligned projections
+  if (h->L != h->Lg && plan_frame_offset(plan) != h->frame0)
+    return fail(MRF_EINVAL, std::string(who) + ": the plan's frame_offset differs from the shard's first frame");
+  h->comm = plan_has_comm(plan) ? plan : nullptr;
   return MRF_OK;
 }
 
@@ -534,7 +533,7 @@ static mrf_status cost_impl(mrf_llr h, mrf_plan plan, const void* x, const void*
   MRF_TRY(mrf_forward(plan, x, h->yb, stream));
   llr::k_llr_resid<<<kStatBlocks, 256, 0, st>>>(h->yb, (const float2*)b, ny, h->part);
   MRF_TRY(check_launch("k_llr_resid"));
-  MRF_TRY(allreduce(h, h->part, kStatBlocks, kNcclFloat64, st));   // the data term over all ranks' frames
+  MRF_TRY(allreduce(h, h->part, kStatBlocks, MRF_DTYPE_F64, st));   // the data term over all ranks' frames
   double t[3] = {0.0, 0.0, 0.0};
   Sums sums{h, st};
   MRF_TRY(sums.add(h->part, kStatBlocks, &t[0]));
@@ -829,6 +828,10 @@ mrf_status mrf_llr_subspace_normal(mrf_llr h, mrf_plan plan, const void* u, void
   if (u == z) return fail(MRF_EINVAL, "mrf_llr_subspace_normal: z may not alias u");
   if (!plan_toeplitz(plan)) return fail(MRF_EINVAL, "mrf_llr_subspace_normal: needs a plan with MRF_NORMAL_TOEPLITZ");
   MRF_TRY(check_plan(h, plan, "mrf_llr_subspace_normal"));
+  // the mixing kernels of a shard sum over its own frames only, and z would be a rank-local
+  // partial: the subspace normal is defined for the whole frame stack
+  if (h->comm || h->L != h->Lg)
+    return fail(MRF_EUNSUPPORTED, "mrf_llr_subspace_normal: not available on a frame-sharded operator");
   CUDA_TRY(cudaSetDevice(h->device));
   cudaStream_t st = (cudaStream_t)stream;
   MRF_TRY(ensure_sn(h, plan, st, false));

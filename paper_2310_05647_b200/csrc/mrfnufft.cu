@@ -84,6 +84,10 @@ struct mrf_plan_s {
   int col_smem = 0;                 // dynamic shared memory of k_fwd_cols
   int acol_smem = 0;                // dynamic shared memory of k_adj_cols
   void* nccl_comm = nullptr;
+  mrf_host_allreduce_fn host_ar = nullptr;   // mrf_plan_set_host_allreduce (replaces nccl_comm)
+  void* host_ar_ctx = nullptr;
+  void* host_ar_buf = nullptr;               // pinned staging of the host all-reduce
+  size_t host_ar_cap = 0;
   int dbg = 0;               // MRF_DBG experiment bits (1: skip gather/spread, 2: phase timers)
   long long* dbgbuf = nullptr;
   // device tables
@@ -261,6 +265,7 @@ static void free_plan(mrf_plan_s* pl) {
     if (pl->ev_copied[i]) cudaEventDestroy(pl->ev_copied[i]);
   }
   if (pl->cstream) cudaStreamDestroy(pl->cstream);
+  if (pl->host_ar_buf) cudaFreeHost(pl->host_ar_buf);
   for (void* v : ptrs)
     if (v) cudaFree(v);
   for (int k = 0; k < MRF_K_COUNT; ++k)
@@ -622,15 +627,41 @@ static int vec_blocks(size_t n) {
   return (int)std::max<size_t>(1, std::min<size_t>(b, kPartBlocks));
 }
 
-static mrf_status allreduce2(mrf_plan_s* pl, double2* v, cudaStream_t st) {
+// In-place sum over the plan's ranks: NCCL on the plan's communicator, or the
+// host hook of mrf_plan_set_host_allreduce (D2H into pinned staging, synchronise, callback, H2D).
+mrf_status mrf::plan_allreduce(mrf_plan pl, void* buf, size_t n, int dtype, cudaStream_t st) {
+  if (n == 0) return MRF_OK;
+  if (pl->host_ar) {
+    const size_t bytes = n * (dtype == MRF_DTYPE_F64 ? 8 : 4);
+    if (pl->host_ar_cap < bytes) {
+      if (pl->host_ar_buf) cudaFreeHost(pl->host_ar_buf);
+      pl->host_ar_buf = nullptr;
+      pl->host_ar_cap = 0;
+      CUDA_TRY(cudaMallocHost(&pl->host_ar_buf, bytes));
+      pl->host_ar_cap = bytes;
+    }
+    ProfScope ps(pl, MRF_K_OTHER, st);
+    CUDA_TRY(cudaMemcpyAsync(pl->host_ar_buf, buf, bytes, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    const int rc = pl->host_ar(pl->host_ar_buf, n, dtype, pl->host_ar_ctx);
+    if (rc != 0) return fail(MRF_ENCCL, "host all-reduce callback returned " + std::to_string(rc));
+    CUDA_TRY(cudaMemcpyAsync(buf, pl->host_ar_buf, bytes, cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaStreamSynchronize(st));   // the staging buffer is reused by the next call
+    return MRF_OK;
+  }
   if (!pl->nccl_comm) return MRF_OK;
   const char* why = nullptr;
   const NcclApi* api = nccl_api(&why);
   if (!api) return fail(MRF_ENCCL, why);
   ProfScope ps(pl, MRF_K_OTHER, st);
-  int rc = api->AllReduce(v, v, 2, kNcclFloat64, kNcclSum, pl->nccl_comm, st);
+  const int rc = api->AllReduce(buf, buf, n, dtype == MRF_DTYPE_F64 ? kNcclFloat64 : kNcclFloat32, kNcclSum,
+                                pl->nccl_comm, st);
   if (rc != 0) return fail(MRF_ENCCL, std::string("ncclAllReduce: ") + api->GetErrorString(rc));
   return MRF_OK;
+}
+
+static mrf_status allreduce2(mrf_plan_s* pl, double2* v, cudaStream_t st) {
+  return plan_allreduce(pl, v, 2, MRF_DTYPE_F64, st);
 }
 
 static mrf_status reduce_to(mrf_plan_s* pl, const double2* part, int nblk, double2* dst, cudaStream_t st) {
@@ -848,7 +879,8 @@ void mrf::plan_dims(mrf_plan pl, int* N, int* L, int* C, int* device, int* M) {
 
 // ---------------------------------------------------------------------------- subspace normal
 // (gridding.cuh k_sn_*; used by mrf_msllr_solve on Toeplitz plans, llr.cu)
-void* mrf::plan_comm(mrf_plan pl) { return pl->nccl_comm; }
+bool mrf::plan_has_comm(mrf_plan pl) { return pl->nccl_comm != nullptr || pl->host_ar != nullptr; }
+int mrf::plan_frame_offset(mrf_plan pl) { return pl->frame_offset; }
 bool mrf::plan_toeplitz(mrf_plan pl) { return (pl->flags & MRF_NORMAL_TOEPLITZ) != 0 && pl->psf; }
 unsigned long long mrf::plan_serial(mrf_plan pl) { return pl->serial; }
 long long mrf::sn_elems(mrf_plan pl) { return (long long)pl->G * pl->G; }
@@ -1464,6 +1496,13 @@ mrf_status mrf_profile_query(mrf_plan pl, int cls, double* total_ms, long long* 
   }
   if (total_ms) *total_ms = tot;
   if (launches) *launches = (long long)(pr.used[cls] / 2);
+  return MRF_OK;
+}
+
+mrf_status mrf_plan_set_host_allreduce(mrf_plan pl, mrf_host_allreduce_fn fn, void* ctx) {
+  if (!pl) return fail(MRF_EINVAL, "null plan");
+  pl->host_ar = fn;
+  pl->host_ar_ctx = fn ? ctx : nullptr;
   return MRF_OK;
 }
 

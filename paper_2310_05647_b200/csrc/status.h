@@ -19,7 +19,12 @@ void plan_dims(mrf_plan plan, int* N, int* L, int* C, int* device, int* M = null
 // kernels from the basis rows (host [r][L]); apply: Z = P_S A^H A (U d) in coefficients, U and Z
 // DEVICE [r][N][N], spectra workspaces [r][C][G*G] each.
 bool plan_toeplitz(mrf_plan plan);
-void* plan_comm(mrf_plan plan);   // the plan's ncclComm_t or nullptr
+bool plan_has_comm(mrf_plan plan);   // the plan reduces over ranks (NCCL communicator or host hook)
+int plan_frame_offset(mrf_plan plan);   // global index of the plan's local frame 0
+// In-place sum of n elements (dtype MRF_DTYPE_F32 / MRF_DTYPE_F64) of a DEVICE buffer over the
+// plan's ranks, on `st`: ncclAllReduce on its communicator, or the host hook
+// (mrf_plan_set_host_allreduce); a no-op for an unsharded plan.
+mrf_status plan_allreduce(mrf_plan plan, void* buf, size_t n, int dtype, cudaStream_t st);
 unsigned long long plan_serial(mrf_plan plan);   // process-wide creation number of the plan
 long long sn_elems(mrf_plan plan);
 mrf_status sn_build(mrf_plan plan, const float2* basis_h, int r, float2* K, cudaStream_t st);
