@@ -319,7 +319,6 @@ def run_ours(args):
 
     # ---------------------------------------------------------------- timed region
     clocks = ClockSampler(local)
-    plan.profile(True)
     barrier()
     torch.cuda.synchronize()
     clocks.start()
@@ -332,6 +331,12 @@ def run_ours(args):
     barrier()
     ms_total = max_over_ranks(ev0.elapsed_time(ev1))
     clk = clocks.stop()
+    # per-kernel-class CUDA events (the library brackets every launch): the same steps again,
+    # outside the timed region -- profiling replaces the solve's CUDA graph by direct launches
+    plan.profile(True)
+    for _ in range(args.steps):
+        step()
+    torch.cuda.synchronize()
     prof = {k: plan.profile_query(k) for k in binding.KERNEL_CLASSES}
     plan.profile(False)
     ms_step = ms_total / args.steps

@@ -28,10 +28,57 @@ __device__ __forceinline__ double2 block_sum2(double2 v) {
   return s;   // valid in thread 0
 }
 
+// Device-resident CG scalars.
+struct CGScalars {
+  double2 pq;        // <p, q>          (global after allreduce)
+  double2 rr;        // <r, r>          (global after allreduce)
+  double rho, rho0, alpha, beta;
+  int breakdown, iters;
+};
+
+// The scalar steps of the iteration (single thread).
+// rho0 = rho = rr.x ; hist[0]
+__device__ __forceinline__ void cg_start(CGScalars* sc, double* hist) {
+  sc->rho = sc->rr.x;
+  sc->rho0 = sc->rr.x;
+  sc->breakdown = 0;
+  sc->iters = 0;
+  sc->alpha = 0.0;   // consumed by the first fused row pass: x += 0 * p, p = r + 0 * p
+  sc->beta = 0.0;
+  hist[0] = sqrt(sc->rr.x);
+}
+// alpha = rho / Re<p,q>  (breakdown => alpha = 0, flagged); ha[k] = alpha
+__device__ __forceinline__ void cg_alpha(CGScalars* sc, double* ha, int k) {
+  const double pq = sc->pq.x;
+  if (sc->rho0 == 0.0) {
+    sc->alpha = 0.0;
+  } else if (!(pq > 0.0) || !isfinite(pq)) {
+    sc->alpha = 0.0;
+    sc->breakdown = 1;
+  } else {
+    sc->alpha = sc->rho / pq;
+  }
+  ha[k] = sc->alpha;
+}
+// beta = rho' / rho ; rho = rho' ; hist[k+1], hb[k] = beta
+__device__ __forceinline__ void cg_beta(CGScalars* sc, double* hist, double* hb, int k) {
+  const double rn = sc->rr.x;
+  sc->beta = sc->rho > 0.0 ? rn / sc->rho : 0.0;
+  hb[k] = sc->beta;
+  sc->rho = rn;
+  sc->iters = k + 1;
+  hist[k + 1] = sqrt(rn);
+}
+enum { kRedPlain = 0, kRedStart = 1, kRedAlpha = 2, kRedBeta = 3 };
+
 // dst = sum of part[0..n) in a fixed order (one block of kReduceThreads, 4 independent loads in
 // flight per thread)
 constexpr int kReduceThreads = 1024;
-__global__ void __launch_bounds__(kReduceThreads) k_reduce(const double2* __restrict__ part, int n, double2* __restrict__ dst) {
+// OP != kRedPlain: then the scalar step that consumes dst (one launch instead of two when the
+// plan has no communicator to all-reduce dst first).
+template <int OP>
+__global__ void __launch_bounds__(kReduceThreads) k_reduce(const double2* __restrict__ part, int n, double2* __restrict__ dst,
+                                                           CGScalars* sc, double* hist, double* hx, int k) {
   __shared__ double2 red[kReduceThreads / 32];
   double2 s0 = make_double2(0.0, 0.0), s1 = s0, s2 = s0, s3 = s0;
   int i = threadIdx.x;
@@ -52,6 +99,9 @@ __global__ void __launch_bounds__(kReduceThreads) k_reduce(const double2* __rest
     double2 t = make_double2(0.0, 0.0);
     for (int w = 0; w < kReduceThreads / 32; ++w) { t.x += red[w].x; t.y += red[w].y; }
     *dst = t;
+    if (OP == kRedStart) cg_start(sc, hist);
+    if (OP == kRedAlpha) cg_alpha(sc, hx, k);
+    if (OP == kRedBeta) cg_beta(sc, hist, hx, k);
   }
 }
 
@@ -78,13 +128,6 @@ __device__ __forceinline__ double norm2d(float4 v) {
   return ((double)v.x * v.x + (double)v.y * v.y) + ((double)v.z * v.z + (double)v.w * v.w);
 }
 
-// Device-resident CG scalars.
-struct CGScalars {
-  double2 pq;        // <p, q>          (global after allreduce)
-  double2 rr;        // <r, r>          (global after allreduce)
-  double rho, rho0, alpha, beta;
-  int breakdown, iters;
-};
 
 // r = rhs - q ; p = r  (initial residual; q == nullptr: x0 = 0, r = rhs); partial <r,r>
 __global__ void __launch_bounds__(kVecThreads) k_cg_init(const float2* __restrict__ rhs, const float2* __restrict__ q,
@@ -106,30 +149,8 @@ __global__ void __launch_bounds__(kVecThreads) k_cg_init(const float2* __restric
   if (threadIdx.x == 0) part[blockIdx.x] = s;
 }
 
-// rho0 = rho = rr.x ; hist[0]
-__global__ void k_cg_start(CGScalars* sc, double* hist) {
-  sc->rho = sc->rr.x;
-  sc->rho0 = sc->rr.x;
-  sc->breakdown = 0;
-  sc->iters = 0;
-  sc->alpha = 0.0;   // consumed by the first fused row pass: x += 0 * p, p = r + 0 * p
-  sc->beta = 0.0;
-  hist[0] = sqrt(sc->rr.x);
-}
-
-// alpha = rho / Re<p,q>  (breakdown => alpha = 0, flagged); ha[k] = alpha
-__global__ void k_cg_alpha(CGScalars* sc, double* ha, int k) {
-  const double pq = sc->pq.x;
-  if (sc->rho0 == 0.0) {
-    sc->alpha = 0.0;
-  } else if (!(pq > 0.0) || !isfinite(pq)) {
-    sc->alpha = 0.0;
-    sc->breakdown = 1;
-  } else {
-    sc->alpha = sc->rho / pq;
-  }
-  ha[k] = sc->alpha;
-}
+__global__ void k_cg_start(CGScalars* sc, double* hist) { cg_start(sc, hist); }
+__global__ void k_cg_alpha(CGScalars* sc, double* ha, int k) { cg_alpha(sc, ha, k); }
 
 // r -= alpha q ; partial <r,r>   (x is advanced lazily: x += alpha p in the next row pass)
 __global__ void __launch_bounds__(kVecThreads) k_cg_r(float2* __restrict__ r, const float2* __restrict__ q, size_t n,
@@ -189,15 +210,7 @@ __global__ void __launch_bounds__(kVecThreads) k_cg_px(float2* __restrict__ x, f
   })
 }
 
-// beta = rho' / rho ; rho = rho' ; hist[k+1], hb[k] = beta
-__global__ void k_cg_beta(CGScalars* sc, double* hist, double* hb, int k) {
-  const double rn = sc->rr.x;
-  sc->beta = sc->rho > 0.0 ? rn / sc->rho : 0.0;
-  hb[k] = sc->beta;
-  sc->rho = rn;
-  sc->iters = k + 1;
-  hist[k + 1] = sqrt(rn);
-}
+__global__ void k_cg_beta(CGScalars* sc, double* hist, double* hb, int k) { cg_beta(sc, hist, hb, k); }
 
 // a += mu b   (rhs = A^H y + mu z)
 __global__ void __launch_bounds__(kVecThreads) k_axpy(float2* __restrict__ a, const float2* __restrict__ b, float mu, size_t n) {

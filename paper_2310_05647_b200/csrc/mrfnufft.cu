@@ -66,6 +66,16 @@ struct DeviceGuard {
 }  // namespace
 
 static constexpr int kMaxLanes = 4;
+
+struct CgKey {   // the arguments a captured CG graph bakes in
+  const void *x = nullptr, *y = nullptr, *z = nullptr;
+  float mu = 0.f;
+  int n_iter = -1;
+  bool zero_init = false;
+  bool operator==(const CgKey& o) const {
+    return x == o.x && y == o.y && z == o.z && mu == o.mu && n_iter == o.n_iter && zero_init == o.zero_init;
+  }
+};
 static constexpr int kDefaultLanes = 2;
 
 struct mrf_plan_s {
@@ -133,6 +143,12 @@ struct mrf_plan_s {
   cudaStream_t cstream = nullptr;
   cudaEvent_t ev_solved[2] = {}, ev_copied[2] = {};
   unsigned long long acalls = 0;
+  // CUDA graph of the last tol == 0 solve (run_cg) and the arguments it was captured with
+  cudaStream_t gstream = nullptr;
+  static constexpr int kGraphs = 4;   // e.g. the two device slots of MRF_CG_ASYNC_HOST
+  cudaGraphExec_t cg_exec[kGraphs] = {};
+  CgKey cg_key[kGraphs];
+  unsigned long long cg_use[kGraphs] = {}, cg_clock = 0;
   size_t bytes = 0;
   Prof prof;
   DevPlan dp() const {
@@ -265,6 +281,9 @@ static void free_plan(mrf_plan_s* pl) {
     if (pl->ev_copied[i]) cudaEventDestroy(pl->ev_copied[i]);
   }
   if (pl->cstream) cudaStreamDestroy(pl->cstream);
+  for (cudaGraphExec_t e : pl->cg_exec)
+    if (e) cudaGraphExecDestroy(e);
+  if (pl->gstream) cudaStreamDestroy(pl->gstream);
   if (pl->host_ar_buf) cudaFreeHost(pl->host_ar_buf);
   for (void* v : ptrs)
     if (v) cudaFree(v);
@@ -664,11 +683,25 @@ static mrf_status allreduce2(mrf_plan_s* pl, double2* v, cudaStream_t st) {
   return plan_allreduce(pl, v, 2, MRF_DTYPE_F64, st);
 }
 
-static mrf_status reduce_to(mrf_plan_s* pl, const double2* part, int nblk, double2* dst, cudaStream_t st) {
+// dst = the fixed-order sum of the partials; then the scalar step OP.  Without a communicator the
+// reduction and the scalar step are one launch; with one, dst is all-reduced in between.
+template <int OP>
+static mrf_status reduce_step(mrf_plan_s* pl, const double2* part, int nblk, double2* dst, double* hx, int k,
+                              cudaStream_t st) {
+  const bool comm = pl->nccl_comm || pl->host_ar;
+  {
+    ProfScope ps(pl, MRF_K_CG_VEC, st);
+    if (comm) k_reduce<kRedPlain><<<1, kReduceThreads, 0, st>>>(part, nblk, dst, pl->sc, pl->hist, hx, k);
+    else k_reduce<OP><<<1, kReduceThreads, 0, st>>>(part, nblk, dst, pl->sc, pl->hist, hx, k);
+    MRF_TRY(check_launch("k_reduce"));
+  }
+  if (!comm) return MRF_OK;
+  MRF_TRY(allreduce2(pl, dst, st));
   ProfScope ps(pl, MRF_K_CG_VEC, st);
-  k_reduce<<<1, kReduceThreads, 0, st>>>(part, nblk, dst);
-  MRF_TRY(check_launch("k_reduce"));
-  return MRF_OK;
+  if (OP == kRedStart) k_cg_start<<<1, 1, 0, st>>>(pl->sc, pl->hist);
+  if (OP == kRedAlpha) k_cg_alpha<<<1, 1, 0, st>>>(pl->sc, hx, k);
+  if (OP == kRedBeta) k_cg_beta<<<1, 1, 0, st>>>(pl->sc, pl->hist, hx, k);
+  return check_launch("k_cg_scalar");
 }
 
 static mrf_status vec_launch_check(const char* what) { return check_launch(what); }
@@ -677,17 +710,12 @@ static mrf_status vec_launch_check(const char* what) { return check_launch(what)
 // iteration k runs one row pass that forms p_k = r_k + beta_{k-1} p_{k-1} and advances
 // x_k = x_{k-1} + alpha_{k-1} p_{k-1} (same iterates as the textbook order), the normal operator
 // whose last pass also emits <p_k, q_k> partials, and one r-update pass that emits <r, r>.
-static mrf_status run_cg(mrf_plan_s* pl, const float2* y, const float2* z, float mu, int n_iter, float tol,
-                         float2* x, mrf_cg_info* info, cudaStream_t st, bool zero_init = false) {
+// run_cg_launch issues the whole solve on `st` (no host synchronisation when tol == 0); it is
+// what the CUDA graph of a tol == 0 solve captures.
+static mrf_status run_cg_launch(mrf_plan_s* pl, const float2* y, const float2* z, float mu, int n_iter, float tol,
+                                float2* x, cudaStream_t st, bool zero_init, int* iters_done, double* rho0_out) {
   const size_t n = (size_t)pl->L * pl->N * pl->N;
   const int nblk = vec_blocks(n);
-  if (n_iter + 1 > pl->hist_cap) {   // [sqrt(rho_k), k <= n][alpha_k][beta_k]
-    if (pl->hist) cudaFree(pl->hist);
-    pl->hist = nullptr;
-    pl->hist_cap = 0;
-    MRF_TRY(dev_alloc(pl, &pl->hist, 3 * ((size_t)n_iter + 1)));
-    pl->hist_cap = n_iter + 1;
-  }
   double* hist_a = pl->hist + pl->hist_cap;
   double* hist_b = pl->hist + 2 * pl->hist_cap;
   // rhs = A^H y + mu z  -> r
@@ -708,57 +736,108 @@ static mrf_status run_cg(mrf_plan_s* pl, const float2* y, const float2* z, float
     k_cg_init<<<nblk, kVecThreads, 0, st>>>(pl->r, zero_init ? nullptr : pl->q, pl->r, pl->p, n, pl->part);
     MRF_TRY(vec_launch_check("k_cg_init"));
   }
-  MRF_TRY(reduce_to(pl, pl->part, nblk, &pl->sc->rr, st));
-  MRF_TRY(allreduce2(pl, &pl->sc->rr, st));
-  {
-    ProfScope ps(pl, MRF_K_CG_VEC, st);
-    k_cg_start<<<1, 1, 0, st>>>(pl->sc, pl->hist);
-    MRF_TRY(vec_launch_check("k_cg_start"));
-  }
+  MRF_TRY(reduce_step<kRedStart>(pl, pl->part, nblk, &pl->sc->rr, nullptr, 0, st));
   double rho0 = -1.0;
   if (tol > 0.f) {
     CUDA_TRY(cudaMemcpyAsync(&rho0, &pl->sc->rho0, sizeof(double), cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaStreamSynchronize(st));
   }
-  int iters_done = n_iter;
+  *iters_done = n_iter;
   for (int k = 0; k < n_iter; ++k) {
-    if (tol > 0.f && rho0 == 0.0) { iters_done = 0; break; }
+    if (tol > 0.f && rho0 == 0.0) { *iters_done = 0; break; }
     if (pl->C > 1) {   // unfused p / x update (the multi-coil row pass reads the image once per coil)
       ProfScope ps(pl, MRF_K_CG_VEC, st);
       k_cg_px<<<nblk, kVecThreads, 0, st>>>(x, pl->p, pl->r, n, pl->sc);
       MRF_TRY(vec_launch_check("k_cg_px"));
     }
     MRF_TRY(do_normal(pl, pl->p, pl->q, mu, st, 1, x));
-    MRF_TRY(reduce_to(pl, pl->dotp, (int)pl->ndotp, &pl->sc->pq, st));
-    MRF_TRY(allreduce2(pl, &pl->sc->pq, st));
-    {
-      ProfScope ps(pl, MRF_K_CG_VEC, st);
-      k_cg_alpha<<<1, 1, 0, st>>>(pl->sc, hist_a, k);
-      MRF_TRY(vec_launch_check("k_cg_alpha"));
-    }
+    MRF_TRY(reduce_step<kRedAlpha>(pl, pl->dotp, (int)pl->ndotp, &pl->sc->pq, hist_a, k, st));
     {
       ProfScope ps(pl, MRF_K_CG_VEC, st);
       k_cg_r<<<nblk, kVecThreads, 0, st>>>(pl->r, pl->q, n, pl->sc, pl->part);
       MRF_TRY(vec_launch_check("k_cg_r"));
     }
-    MRF_TRY(reduce_to(pl, pl->part, nblk, &pl->sc->rr, st));
-    MRF_TRY(allreduce2(pl, &pl->sc->rr, st));
-    {
-      ProfScope ps(pl, MRF_K_CG_VEC, st);
-      k_cg_beta<<<1, 1, 0, st>>>(pl->sc, pl->hist, hist_b, k);
-      MRF_TRY(vec_launch_check("k_cg_beta"));
-    }
+    MRF_TRY(reduce_step<kRedBeta>(pl, pl->part, nblk, &pl->sc->rr, hist_b, k, st));
     if (tol > 0.f) {
       double rho = 0.0;
       CUDA_TRY(cudaMemcpyAsync(&rho, &pl->sc->rho, sizeof(double), cudaMemcpyDeviceToHost, st));
       CUDA_TRY(cudaStreamSynchronize(st));
-      if (std::sqrt(rho / rho0) < (double)tol) { iters_done = k + 1; break; }
+      if (std::sqrt(rho / rho0) < (double)tol) { *iters_done = k + 1; break; }
     }
   }
-  if (n_iter > 0 && iters_done > 0) {   // x += alpha_last p_last
+  if (n_iter > 0 && *iters_done > 0) {   // x += alpha_last p_last
     ProfScope ps(pl, MRF_K_CG_VEC, st);
     k_cg_xfin<<<nblk, kVecThreads, 0, st>>>(x, pl->p, n, pl->sc);
     MRF_TRY(vec_launch_check("k_cg_xfin"));
+  }
+  *rho0_out = rho0;
+  return MRF_OK;
+}
+
+// A tol == 0 solve is a fixed launch sequence: it is captured once into a CUDA graph (on the
+// plan's capture stream, forked from the caller's stream) and replayed while its arguments stay
+// the same -- one graph launch per solve instead of ~40 launches per iteration.  Not used when
+// tol > 0 (host-side stopping), with the host all-reduce hook (host synchronisation), while
+// per-kernel profiling is on (its events are per launch), or with MRF_CG_GRAPH=0.
+static bool g_cg_graph = [] {
+  const char* e = std::getenv("MRF_CG_GRAPH");
+  return !(e && e[0] == '0');
+}();
+
+static void drop_cg_graphs(mrf_plan_s* pl) {
+  for (int i = 0; i < mrf_plan_s::kGraphs; ++i) {
+    if (pl->cg_exec[i]) cudaGraphExecDestroy(pl->cg_exec[i]);
+    pl->cg_exec[i] = nullptr;
+    pl->cg_key[i] = CgKey();
+  }
+}
+
+static mrf_status run_cg(mrf_plan_s* pl, const float2* y, const float2* z, float mu, int n_iter, float tol,
+                         float2* x, mrf_cg_info* info, cudaStream_t st, bool zero_init = false) {
+  if (n_iter + 1 > pl->hist_cap) {   // [sqrt(rho_k), k <= n][alpha_k][beta_k]
+    drop_cg_graphs(pl);
+    if (pl->hist) cudaFree(pl->hist);
+    pl->hist = nullptr;
+    pl->hist_cap = 0;
+    MRF_TRY(dev_alloc(pl, &pl->hist, 3 * ((size_t)n_iter + 1)));
+    pl->hist_cap = n_iter + 1;
+  }
+  int iters_done = n_iter;
+  double rho0 = -1.0;
+  const bool graph = g_cg_graph && tol == 0.f && !pl->host_ar && !pl->prof.on;
+  if (graph) {
+    const CgKey key{x, y, z, mu, n_iter, zero_init};
+    int slot = -1;
+    for (int i = 0; i < mrf_plan_s::kGraphs; ++i)
+      if (pl->cg_exec[i] && pl->cg_key[i] == key) slot = i;
+    if (slot < 0) {   // capture into the least recently used slot
+      slot = 0;
+      for (int i = 1; i < mrf_plan_s::kGraphs; ++i)
+        if (pl->cg_use[i] < pl->cg_use[slot]) slot = i;
+      if (pl->cg_exec[slot]) cudaGraphExecDestroy(pl->cg_exec[slot]);
+      pl->cg_exec[slot] = nullptr;
+      if (!pl->gstream) CUDA_TRY(cudaStreamCreateWithFlags(&pl->gstream, cudaStreamNonBlocking));
+      CUDA_TRY(cudaStreamBeginCapture(pl->gstream, cudaStreamCaptureModeThreadLocal));
+      mrf_status rc = run_cg_launch(pl, y, z, mu, n_iter, tol, x, pl->gstream, zero_init, &iters_done, &rho0);
+      cudaGraph_t g = nullptr;
+      const cudaError_t ce = cudaStreamEndCapture(pl->gstream, &g);
+      if (rc != MRF_OK) {
+        if (g) cudaGraphDestroy(g);
+        return rc;
+      }
+      if (ce != cudaSuccess) return fail(MRF_ECUDA, std::string("CG graph capture: ") + cudaGetErrorString(ce));
+      const cudaError_t ie = cudaGraphInstantiate(&pl->cg_exec[slot], g, 0);
+      cudaGraphDestroy(g);
+      if (ie != cudaSuccess) {
+        pl->cg_exec[slot] = nullptr;
+        return fail(MRF_ECUDA, std::string("CG graph instantiate: ") + cudaGetErrorString(ie));
+      }
+      pl->cg_key[slot] = key;
+    }
+    pl->cg_use[slot] = ++pl->cg_clock;
+    CUDA_TRY(cudaGraphLaunch(pl->cg_exec[slot], st));
+  } else {
+    MRF_TRY(run_cg_launch(pl, y, z, mu, n_iter, tol, x, st, zero_init, &iters_done, &rho0));
   }
   CGScalars hs;
   CUDA_TRY(cudaMemcpyAsync(&hs, pl->sc, sizeof(CGScalars), cudaMemcpyDeviceToHost, st));
