@@ -21,4 +21,4 @@ Cartesian trajectory, closed forms (delta image, single DC sample, KB Fourier tr
 quadrature), the adjoint identity, Hermitian/PSD structure, A^H A = I on a full Cartesian
 trajectory, and CG = Krylov projection / dense solve.
 """
-from . import kb, nufft, cg, match, dcf, llr, manifold, msllr  # noqa: F401
+from . import kb, nufft, cg, pcg, match, dcf, llr, manifold, msllr  # noqa: F401
