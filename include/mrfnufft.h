@@ -143,8 +143,20 @@ mrf_status mrf_dc_cg(mrf_plan plan, const void* y, const void* z, float mu, int 
  * mrf_plan_wait returns; pinned host memory is needed for the overlap.  `info`, if given, is
  * filled as usual (that synchronises `stream`, not the copy stream). */
 #define MRF_CG_ASYNC_HOST 2u
+/* MRF_CG_PRECOND: preconditioned CG (reading 28) -- same system,
+ * same solution, other iterates.  Per frame M = C + gamma I, C = T. Chan's optimal circulant of the
+ * frame's exact normal operator (eigenvalues lambda_m = ||A f_m||^2 at the Fourier vectors f_m,
+ * PAPER.md:217's A^H A, computed in float64 per interleaf on the first such call and scaled by the
+ * mean coil power), gamma = mu + shift * mean(lambda) (shift: mrf_plan_set_precond_shift, default
+ * 30).  z = M^-1 r costs a 2D FFT pair over the frames (three passes).  history / rel_resid /
+ * tol report the true residual ||r||; alpha, beta are the PCG step lengths.  Costs 2 more image
+ * stacks of device memory. */
+#define MRF_CG_PRECOND 4u
 mrf_status mrf_dc_cg_ex(mrf_plan plan, const void* y, const void* z, float mu, int n_iter, float tol,
                         unsigned flags, void* x, mrf_cg_info* info, void* stream);
+/* The preconditioner's shift (MRF_CG_PRECOND): gamma = mu + shift * mean(lambda); shift >= 0,
+ * finite (else MRF_EINVAL).  Synchronises the device (cached CUDA graphs of PCG solves are dropped). */
+mrf_status mrf_plan_set_precond_shift(mrf_plan plan, double shift);
 /* Waits for every result copy of MRF_CG_ASYNC_HOST calls on the plan.  Errors: MRF_EINVAL, MRF_ECUDA. */
 mrf_status mrf_plan_wait(mrf_plan plan);
 

@@ -35,7 +35,7 @@ EXPORTED = [
     "mrf_dict_profile", "mrf_dict_profile_query", "mrf_dict_basis", "mrf_dict_basis_copy", "mrf_llr_create",
     "mrf_llr_step", "mrf_llr_destroy", "mrf_llr_laplacian", "mrf_llr_cost", "mrf_msllr_solve", "mrf_plan_wait",
     "mrf_dict_match_coef", "mrf_llr_create_basis", "mrf_llr_subspace_normal", "mrf_llr_create_shard",
-    "mrf_plan_set_host_allreduce",
+    "mrf_plan_set_host_allreduce", "mrf_plan_set_precond_shift",
 ]
 
 MRF_DTYPE_F32 = 0
@@ -104,6 +104,7 @@ def _load() -> ctypes.CDLL:
         "mrf_nccl_comm_init": ([ctypes.POINTER(vp), ci, vp, ci, ci], ci),
         "mrf_nccl_comm_destroy": ([vp], ci),
         "mrf_plan_set_host_allreduce": ([vp, HOST_ALLREDUCE_FN, vp], ci),
+        "mrf_plan_set_precond_shift": ([vp, ctypes.c_double], ci),
         "mrf_dict_create": ([vp, vp, ci, ci, ci, ci, ctypes.POINTER(vp)], ci),
         "mrf_dict_match": ([vp, vp, ctypes.c_longlong, vp, vp, vp, vp], ci),
         "mrf_dict_match_coef": ([vp, vp, ctypes.c_longlong, vp, vp, vp, vp], ci),
@@ -259,13 +260,14 @@ class Plan:
         return out
 
     def dc_cg(self, y, x0=None, z=None, mu: float = 0.01, n_iter: int = 10, tol: float = 0.0, x=None,
-              zero_init: bool = False, async_host: bool = False):
+              zero_init: bool = False, async_host: bool = False, precond: bool = False):
         """CG solve of (A^H A + mu I) x = A^H y + mu z from x0; returns (x, info dict).
 
         zero_init=True: x0 = 0 and x is output only (mrf_dc_cg_ex with MRF_CG_ZERO_INIT: no normal
         operator for the initial residual, and no host-to-device copy of x0 on the host path).
         async_host=True (pinned host tensors): MRF_CG_ASYNC_HOST -- the result copy overlaps the
-        next call's solve; call ``wait()`` before reading x."""
+        next call's solve; call ``wait()`` before reading x.
+        precond=True: MRF_CG_PRECOND -- PCG with the circulant preconditioner (same solution)."""
         y = _as_c64(y, self.y_shape, "y")
         if x is None:
             x = self._like(y, self.x_shape)
@@ -287,11 +289,16 @@ class Plan:
         dp = lambda a: ctypes.cast(a, ctypes.POINTER(ctypes.c_double))
         info = CGInfo(0, 0.0, dp(hist), dp(ha), dp(hb))
         _check(lib.mrf_dc_cg_ex(self._h, _ptr(y), _ptr(z), ctypes.c_float(mu), int(n_iter), ctypes.c_float(tol),
-                                (1 if zero_init else 0) | (2 if async_host else 0), _ptr(x), ctypes.byref(info),
+                                (1 if zero_init else 0) | (2 if async_host else 0) | (4 if precond else 0), _ptr(x),
+                                ctypes.byref(info),
                                 self._stream(x, y, z)))
         it = info.iters
         return x, {"iters": it, "rel_resid": info.rel_resid, "history": list(hist)[: it + 1],
                    "alpha": list(ha)[:it], "beta": list(hb)[:it]}
+
+    def set_precond_shift(self, shift: float):
+        """gamma = mu + shift * mean(lambda) of the PCG preconditioner (mrf_plan_set_precond_shift)."""
+        _check(lib.mrf_plan_set_precond_shift(self._h, ctypes.c_double(shift)))
 
     def set_host_allreduce(self, fn):
         """Route the plan's rank reductions through a host callable (mrf_plan_set_host_allreduce).

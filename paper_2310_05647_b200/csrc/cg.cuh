@@ -32,7 +32,9 @@ __device__ __forceinline__ double2 block_sum2(double2 v) {
 struct CGScalars {
   double2 pq;        // <p, q>          (global after allreduce)
   double2 rr;        // <r, r>          (global after allreduce)
-  double rho, rho0, alpha, beta;
+  double2 rz;        // <r, z>, z = M^-1 r (PCG; global after allreduce)
+  double rho, rho0, alpha, beta;   // rho = <r, r> (CG) or <r, z> (PCG)
+  double res, res0;                // <r, r> now and at the start (history, tol, rel_resid)
   int breakdown, iters;
 };
 
@@ -41,6 +43,7 @@ struct CGScalars {
 __device__ __forceinline__ void cg_start(CGScalars* sc, double* hist) {
   sc->rho = sc->rr.x;
   sc->rho0 = sc->rr.x;
+  sc->res = sc->res0 = sc->rr.x;
   sc->breakdown = 0;
   sc->iters = 0;
   sc->alpha = 0.0;   // consumed by the first fused row pass: x += 0 * p, p = r + 0 * p
@@ -66,10 +69,27 @@ __device__ __forceinline__ void cg_beta(CGScalars* sc, double* hist, double* hb,
   sc->beta = sc->rho > 0.0 ? rn / sc->rho : 0.0;
   hb[k] = sc->beta;
   sc->rho = rn;
+  sc->res = rn;
   sc->iters = k + 1;
   hist[k + 1] = sqrt(rn);
 }
-enum { kRedPlain = 0, kRedStart = 1, kRedAlpha = 2, kRedBeta = 3 };
+// PCG: rho0 = <r0, z0> (steps), res0 = <r0, r0> (history); rr already reduced
+__device__ __forceinline__ void cg_start_pc(CGScalars* sc, double* hist) {
+  cg_start(sc, hist);
+  sc->rho = sc->rz.x;
+  sc->rho0 = sc->rz.x;
+}
+// PCG: beta = <r', z'> / <r, z> ; rho = <r', z'> ; res = <r', r'>
+__device__ __forceinline__ void cg_beta_pc(CGScalars* sc, double* hist, double* hb, int k) {
+  const double rn = sc->rz.x;
+  sc->beta = sc->rho > 0.0 ? rn / sc->rho : 0.0;
+  hb[k] = sc->beta;
+  sc->rho = rn;
+  sc->res = sc->rr.x;
+  sc->iters = k + 1;
+  hist[k + 1] = sqrt(sc->rr.x);
+}
+enum { kRedPlain = 0, kRedStart = 1, kRedAlpha = 2, kRedBeta = 3, kRedStartPc = 4, kRedBetaPc = 5 };
 
 // dst = sum of part[0..n) in a fixed order (one block of kReduceThreads, 4 independent loads in
 // flight per thread)
@@ -102,6 +122,8 @@ __global__ void __launch_bounds__(kReduceThreads) k_reduce(const double2* __rest
     if (OP == kRedStart) cg_start(sc, hist);
     if (OP == kRedAlpha) cg_alpha(sc, hx, k);
     if (OP == kRedBeta) cg_beta(sc, hist, hx, k);
+    if (OP == kRedStartPc) cg_start_pc(sc, hist);
+    if (OP == kRedBetaPc) cg_beta_pc(sc, hist, hx, k);
   }
 }
 
@@ -211,6 +233,8 @@ __global__ void __launch_bounds__(kVecThreads) k_cg_px(float2* __restrict__ x, f
 }
 
 __global__ void k_cg_beta(CGScalars* sc, double* hist, double* hb, int k) { cg_beta(sc, hist, hb, k); }
+__global__ void k_cg_start_pc(CGScalars* sc, double* hist) { cg_start_pc(sc, hist); }
+__global__ void k_cg_beta_pc(CGScalars* sc, double* hist, double* hb, int k) { cg_beta_pc(sc, hist, hb, k); }
 
 // a += mu b   (rhs = A^H y + mu z)
 __global__ void __launch_bounds__(kVecThreads) k_axpy(float2* __restrict__ a, const float2* __restrict__ b, float mu, size_t n) {

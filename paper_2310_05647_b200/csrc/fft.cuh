@@ -232,6 +232,7 @@ __device__ __forceinline__ void dft_halfout(float2 (&v)[R]) {
 
 // Two-stage split of the supported grid sizes.  T threads (within one warp) per length-G DFT.
 template <int G> struct FFTShape;
+template <> struct FFTShape<32>   { static constexpr int P = 4,  Q = 8,  T = 4;  };   // N = 32 image transforms (precond.cuh)
 template <> struct FFTShape<64>   { static constexpr int P = 8,  Q = 8,  T = 8;  };
 template <> struct FFTShape<128>  { static constexpr int P = 8,  Q = 16, T = 8;  };
 template <> struct FFTShape<256>  { static constexpr int P = 16, Q = 16, T = 16; };

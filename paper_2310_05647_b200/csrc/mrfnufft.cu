@@ -20,6 +20,7 @@
 #include "../../include/mrfnufft.h"
 #include "cg.cuh"
 #include "gridding.cuh"
+#include "precond.cuh"
 #include "nccl_dl.h"
 #include "status.h"
 
@@ -71,9 +72,10 @@ struct CgKey {   // the arguments a captured CG graph bakes in
   const void *x = nullptr, *y = nullptr, *z = nullptr;
   float mu = 0.f;
   int n_iter = -1;
-  bool zero_init = false;
+  bool zero_init = false, pc = false;
   bool operator==(const CgKey& o) const {
-    return x == o.x && y == o.y && z == o.z && mu == o.mu && n_iter == o.n_iter && zero_init == o.zero_init;
+    return x == o.x && y == o.y && z == o.z && mu == o.mu && n_iter == o.n_iter && zero_init == o.zero_init &&
+           pc == o.pc;
   }
 };
 static constexpr int kDefaultLanes = 2;
@@ -130,6 +132,19 @@ struct mrf_plan_s {
   double2* dotp = nullptr;   // [L * rowblocks] fused <p, q> partials of k_adj_rows
   size_t ndotp = 0;
   CGScalars* sc = nullptr;
+  float2* cg_rin = nullptr;  // the vector the fused CG row pass adds to beta p: r (CG) or z (PCG)
+  // PCG (MRF_CG_PRECOND; precond.cuh, reading 28): Chan circulant eigenvalues per
+  // interleaf, z = M^-1 r, the row-pass workspace and the <r, z> partials
+  std::vector<float> traj_h;       // host copy of the trajectory [R][M][2]
+  float* pc_lam = nullptr;         // [R][N][N] float32, [my + N/2][mx + N/2]
+  double pc_lam_sum = 0.0;         // mean of lambda over R interleaves (float64)
+  double pc_gamma = -1.0;          // gamma of the current solve
+  double pc_shift = 30.0;          // gamma = mu + shift * scale * mean(lambda)
+  float pc_scale = 1.f;            // mean coil power
+  float2* z = nullptr;
+  float2* pc_tmp = nullptr;
+  double2* pc_part = nullptr;      // [kPcBlocks]
+  int pc_occ_rows = 0, pc_occ_cols = 0;
   double* hist = nullptr;    // device [hist_cap]
   int hist_cap = 0;
   // host staging (allocated on first host-pointer call)
@@ -273,7 +288,8 @@ static void free_plan(mrf_plan_s* pl) {
     if (pl->Hs[i]) cudaFree(pl->Hs[i]);
     if (pl->ybufs[i]) cudaFree(pl->ybufs[i]);
   }
-  void* ptrs[] = {pl->coils, pl->dap, pl->tw, pl->fchunks, pl->ftab, pl->achunks, pl->atab, pl->fil, pl->r, pl->p, pl->q,
+  void* ptrs[] = {pl->pc_lam, pl->z, pl->pc_tmp, pl->pc_part,
+                  pl->coils, pl->dap, pl->tw, pl->fchunks, pl->ftab, pl->achunks, pl->atab, pl->fil, pl->r, pl->p, pl->q,
                   pl->part, pl->dotp, pl->sc, pl->hist, pl->stg_x, pl->stg_y, pl->stg_z, pl->ax[0], pl->ax[1],
                   pl->ay[0], pl->ay[1]};
   for (int i = 0; i < 2; ++i) {
@@ -462,7 +478,7 @@ static mrf_status launch_fwd_rows_cg(mrf_plan_s* pl, float2* x, float2* H, int l
   const long long items = (long long)nb * (pl->N / RowCfg<G>::RPC) * pl->C;
   ProfScope ps(pl, MRF_K_FWD_ROWS, st);
   CUDA_TRY(launch_pdl(k_fwd_rows<G, 1>, pgrid(pl, pl->occ_fr1, items), kRowThreads, fwd_rows_smem<G>(3), st, pl->dp(),
-                      nullptr, H, l0, nb, pl->r, pl->p, x, &pl->sc->alpha, yzero, nyzero));
+                      nullptr, H, l0, nb, pl->cg_rin ? pl->cg_rin : pl->r, pl->p, x, &pl->sc->alpha, yzero, nyzero));
   return MRF_OK;
 }
 template <int G>
@@ -683,6 +699,129 @@ static mrf_status allreduce2(mrf_plan_s* pl, double2* v, cudaStream_t st) {
   return plan_allreduce(pl, v, 2, MRF_DTYPE_F64, st);
 }
 
+// ---------------------------------------------------------------------------- PCG preconditioner
+// (precond.cuh; reading 28)
+static constexpr int kPcBlocks = 16 * 148;
+
+template <int N>
+static mrf_status pc_setup_t(mrf_plan_s* pl) {
+  CUDA_TRY(cudaFuncSetAttribute(pc::k_pc_rows<N, -1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)pc::rows_smem<N>()));
+  CUDA_TRY(cudaFuncSetAttribute(pc::k_pc_rows<N, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)pc::rows_smem<N>()));
+  CUDA_TRY(cudaFuncSetAttribute(pc::k_pc_cols<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pc::cols_smem<N>()));
+  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pl->pc_occ_rows, pc::k_pc_rows<N, 1, true>, pc::kRowThreads,
+                                                         pc::rows_smem<N>()));
+  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pl->pc_occ_cols, pc::k_pc_cols<N>, pc::cols_threads<N>(),
+                                                         pc::cols_smem<N>()));
+  if (pl->pc_occ_rows < 1 || pl->pc_occ_cols < 1) return fail(MRF_EUNSUPPORTED, "preconditioner kernels do not fit");
+  return MRF_OK;
+}
+
+// z = M^-1 r over the plan's frames, *npart float64 partials of <r, z> in pl->pc_part
+template <int N>
+static mrf_status run_precond(mrf_plan_s* pl, const float2* r, float2* z, cudaStream_t st, int* npart) {
+  const long long nrows = (long long)pl->L * N;
+  const long long ritems = nrows / pc::Row<N>::RPC;
+  const int gr = (int)std::max<long long>(1, std::min<long long>({ritems, (long long)pl->pc_occ_rows * pl->nsm, kPcBlocks}));
+  const int gc = (int)std::max<long long>(1, std::min<long long>((long long)pl->L * (N / pc::SWc), (long long)pl->pc_occ_cols * pl->nsm));
+  const double gamma = pl->pc_gamma;   // set by ensure_precond for the call's mu
+  ProfScope ps(pl, MRF_K_CG_VEC, st);
+  pc::k_pc_rows<N, -1, false><<<gr, pc::kRowThreads, pc::rows_smem<N>(), st>>>(r, pl->pc_tmp, nullptr, nrows, 1.f, nullptr);
+  MRF_TRY(check_launch("k_pc_rows"));
+  pc::k_pc_cols<N><<<gc, pc::cols_threads<N>(), pc::cols_smem<N>(), st>>>(pl->pc_tmp, pl->pc_lam, pl->fil, pl->L,
+                                                                            pl->pc_scale, (float)gamma);
+  MRF_TRY(check_launch("k_pc_cols"));
+  pc::k_pc_rows<N, 1, true><<<gr, pc::kRowThreads, pc::rows_smem<N>(), st>>>(pl->pc_tmp, z, r, nrows,
+                                                                                1.f / ((float)N * (float)N), pl->pc_part);
+  MRF_TRY(check_launch("k_pc_rows"));
+  *npart = gr;
+  return MRF_OK;
+}
+
+#define DISPATCH_N(pl, fn, ...)                               \
+  switch ((pl)->N) {                                          \
+    case 32: return fn<32>(__VA_ARGS__);                      \
+    case 64: return fn<64>(__VA_ARGS__);                      \
+    case 128: return fn<128>(__VA_ARGS__);                    \
+    case 256: return fn<256>(__VA_ARGS__);                    \
+    case 512: return fn<512>(__VA_ARGS__);                    \
+    default: return fail(MRF_EUNSUPPORTED, "unsupported N");  \
+  }
+static mrf_status pc_setup(mrf_plan_s* pl) { DISPATCH_N(pl, pc_setup_t, pl); }
+static mrf_status do_precond(mrf_plan_s* pl, const float2* r, float2* z, cudaStream_t st, int* npart) {
+  DISPATCH_N(pl, run_precond, pl, r, z, st, npart);
+}
+
+// Plan-time (first PCG call) eigenvalues lambda_r[m] = N^-4 sum_j F(kx_j - mx/N) F(ky_j - my/N) in
+// float64 on the device (Fejer factors, then the (N x M)(M x N) product of k_psf_gemm), stored
+// fp32; the float64 mean over all interleaves and the mean coil power fix gamma.  pc_gamma
+// caches gamma for the last mu.
+static mrf_status ensure_precond(mrf_plan_s* pl, float mu, cudaStream_t st) {
+  const int N = pl->N, M = pl->M, R = pl->R;
+  const size_t nx = (size_t)pl->L * N * N;
+  if (!pl->pc_lam) {
+    MRF_TRY(pc_setup(pl));
+    MRF_TRY(dev_alloc(pl, &pl->z, nx));
+    MRF_TRY(dev_alloc(pl, &pl->pc_tmp, nx));
+    MRF_TRY(dev_alloc(pl, &pl->pc_part, kPcBlocks));
+    float* lam = nullptr;
+    MRF_TRY(dev_alloc(pl, &lam, (size_t)R * N * N));
+    float* traj = nullptr;
+    double *Fx = nullptr, *Fy = nullptr, *Tm = nullptr;
+    auto cleanup = [&]() {
+      for (void* v : {(void*)traj, (void*)Fx, (void*)Fy, (void*)Tm})
+        if (v) cudaFree(v);
+    };
+    if (cudaMalloc((void**)&traj, (size_t)R * M * 2 * sizeof(float)) != cudaSuccess ||
+        cudaMalloc((void**)&Fx, (size_t)M * N * sizeof(double)) != cudaSuccess ||
+        cudaMalloc((void**)&Fy, (size_t)M * N * sizeof(double)) != cudaSuccess ||
+        cudaMalloc((void**)&Tm, (size_t)R * N * N * sizeof(double)) != cudaSuccess) {
+      cleanup();
+      cudaFree(lam);
+      cudaGetLastError();
+      return fail(MRF_ENOMEM, "preconditioner workspace");
+    }
+    cudaError_t e = cudaMemcpyAsync(traj, pl->traj_h.data(), (size_t)R * M * 2 * sizeof(float), cudaMemcpyHostToDevice, st);
+    const double scale = 1.0 / ((double)N * N * (double)N * N);
+    for (int r = 0; r < R && e == cudaSuccess; ++r) {
+      const float* tr = traj + (size_t)r * M * 2;
+      pc::k_pc_fejer<<<592, 256, 0, st>>>(tr, M, N, 0, Fx);
+      pc::k_pc_fejer<<<592, 256, 0, st>>>(tr, M, N, 1, Fy);
+      k_psf_gemm<<<dim3((N + 63) / 64, (N + 63) / 64), 256, 0, st>>>(Fy, Fx, M, N, scale, Tm + (size_t)r * N * N);
+      e = cudaGetLastError();
+    }
+    std::vector<double> h((size_t)R * N * N);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(h.data(), Tm, h.size() * sizeof(double), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    cleanup();
+    if (e != cudaSuccess) {
+      cudaFree(lam);
+      return fail(MRF_ECUDA, std::string("preconditioner eigenvalues: ") + cudaGetErrorString(e));
+    }
+    std::vector<float> hf(h.size());
+    double sum = 0.0;
+    for (size_t i = 0; i < h.size(); ++i) {
+      sum += h[i];
+      hf[i] = (float)h[i];
+    }
+    CUDA_TRY(cudaMemcpy(lam, hf.data(), hf.size() * sizeof(float), cudaMemcpyHostToDevice));
+    pl->pc_lam = lam;
+    pl->pc_lam_sum = sum / (double)h.size();
+    double cp = 1.0;   // mean coil power (1/N^2) sum_n sum_c |S_c|^2
+    if (pl->coils) {
+      std::vector<float2> c((size_t)pl->C * N * N);
+      CUDA_TRY(cudaMemcpy(c.data(), pl->coils, c.size() * sizeof(float2), cudaMemcpyDeviceToHost));
+      cp = 0.0;
+      for (const float2& v : c) cp += (double)v.x * v.x + (double)v.y * v.y;
+      cp /= (double)N * N;
+    }
+    pl->pc_scale = (float)cp;
+  }
+  pl->pc_gamma = (double)mu + pl->pc_shift * (double)pl->pc_scale * pl->pc_lam_sum;   // gamma
+  return MRF_OK;
+}
+
 // dst = the fixed-order sum of the partials; then the scalar step OP.  Without a communicator the
 // reduction and the scalar step are one launch; with one, dst is all-reduced in between.
 template <int OP>
@@ -701,6 +840,8 @@ static mrf_status reduce_step(mrf_plan_s* pl, const double2* part, int nblk, dou
   if (OP == kRedStart) k_cg_start<<<1, 1, 0, st>>>(pl->sc, pl->hist);
   if (OP == kRedAlpha) k_cg_alpha<<<1, 1, 0, st>>>(pl->sc, hx, k);
   if (OP == kRedBeta) k_cg_beta<<<1, 1, 0, st>>>(pl->sc, pl->hist, hx, k);
+  if (OP == kRedStartPc) k_cg_start_pc<<<1, 1, 0, st>>>(pl->sc, pl->hist);
+  if (OP == kRedBetaPc) k_cg_beta_pc<<<1, 1, 0, st>>>(pl->sc, pl->hist, hx, k);
   return check_launch("k_cg_scalar");
 }
 
@@ -713,11 +854,14 @@ static mrf_status vec_launch_check(const char* what) { return check_launch(what)
 // run_cg_launch issues the whole solve on `st` (no host synchronisation when tol == 0); it is
 // what the CUDA graph of a tol == 0 solve captures.
 static mrf_status run_cg_launch(mrf_plan_s* pl, const float2* y, const float2* z, float mu, int n_iter, float tol,
-                                float2* x, cudaStream_t st, bool zero_init, int* iters_done, double* rho0_out) {
+                                float2* x, cudaStream_t st, bool zero_init, bool pc, int* iters_done, double* res0_out) {
   const size_t n = (size_t)pl->L * pl->N * pl->N;
   const int nblk = vec_blocks(n);
   double* hist_a = pl->hist + pl->hist_cap;
   double* hist_b = pl->hist + 2 * pl->hist_cap;
+  // PCG (oracle/pcg.py): the fused row pass forms p = z + beta p from z = M^-1 r
+  float2* rin = pc ? pl->z : pl->r;
+  pl->cg_rin = rin;
   // rhs = A^H y + mu z  -> r
   MRF_TRY(do_adjoint(pl, y, pl->r, st));
   if (z && mu != 0.f) {
@@ -736,18 +880,25 @@ static mrf_status run_cg_launch(mrf_plan_s* pl, const float2* y, const float2* z
     k_cg_init<<<nblk, kVecThreads, 0, st>>>(pl->r, zero_init ? nullptr : pl->q, pl->r, pl->p, n, pl->part);
     MRF_TRY(vec_launch_check("k_cg_init"));
   }
-  MRF_TRY(reduce_step<kRedStart>(pl, pl->part, nblk, &pl->sc->rr, nullptr, 0, st));
-  double rho0 = -1.0;
+  if (pc) {   // rr0, then z0 = M^-1 r0 and rho0 = <r0, z0>
+    MRF_TRY(reduce_step<kRedPlain>(pl, pl->part, nblk, &pl->sc->rr, nullptr, 0, st));
+    int npart = 0;
+    MRF_TRY(do_precond(pl, pl->r, pl->z, st, &npart));
+    MRF_TRY(reduce_step<kRedStartPc>(pl, pl->pc_part, npart, &pl->sc->rz, nullptr, 0, st));
+  } else {
+    MRF_TRY(reduce_step<kRedStart>(pl, pl->part, nblk, &pl->sc->rr, nullptr, 0, st));
+  }
+  double res0 = -1.0;
   if (tol > 0.f) {
-    CUDA_TRY(cudaMemcpyAsync(&rho0, &pl->sc->rho0, sizeof(double), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaMemcpyAsync(&res0, &pl->sc->res0, sizeof(double), cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaStreamSynchronize(st));
   }
   *iters_done = n_iter;
   for (int k = 0; k < n_iter; ++k) {
-    if (tol > 0.f && rho0 == 0.0) { *iters_done = 0; break; }
+    if (tol > 0.f && res0 == 0.0) { *iters_done = 0; break; }
     if (pl->C > 1) {   // unfused p / x update (the multi-coil row pass reads the image once per coil)
       ProfScope ps(pl, MRF_K_CG_VEC, st);
-      k_cg_px<<<nblk, kVecThreads, 0, st>>>(x, pl->p, pl->r, n, pl->sc);
+      k_cg_px<<<nblk, kVecThreads, 0, st>>>(x, pl->p, rin, n, pl->sc);
       MRF_TRY(vec_launch_check("k_cg_px"));
     }
     MRF_TRY(do_normal(pl, pl->p, pl->q, mu, st, 1, x));
@@ -757,12 +908,19 @@ static mrf_status run_cg_launch(mrf_plan_s* pl, const float2* y, const float2* z
       k_cg_r<<<nblk, kVecThreads, 0, st>>>(pl->r, pl->q, n, pl->sc, pl->part);
       MRF_TRY(vec_launch_check("k_cg_r"));
     }
-    MRF_TRY(reduce_step<kRedBeta>(pl, pl->part, nblk, &pl->sc->rr, hist_b, k, st));
+    if (pc) {
+      MRF_TRY(reduce_step<kRedPlain>(pl, pl->part, nblk, &pl->sc->rr, nullptr, 0, st));
+      int npart = 0;
+      MRF_TRY(do_precond(pl, pl->r, pl->z, st, &npart));
+      MRF_TRY(reduce_step<kRedBetaPc>(pl, pl->pc_part, npart, &pl->sc->rz, hist_b, k, st));
+    } else {
+      MRF_TRY(reduce_step<kRedBeta>(pl, pl->part, nblk, &pl->sc->rr, hist_b, k, st));
+    }
     if (tol > 0.f) {
-      double rho = 0.0;
-      CUDA_TRY(cudaMemcpyAsync(&rho, &pl->sc->rho, sizeof(double), cudaMemcpyDeviceToHost, st));
+      double res = 0.0;
+      CUDA_TRY(cudaMemcpyAsync(&res, &pl->sc->res, sizeof(double), cudaMemcpyDeviceToHost, st));
       CUDA_TRY(cudaStreamSynchronize(st));
-      if (std::sqrt(rho / rho0) < (double)tol) { *iters_done = k + 1; break; }
+      if (std::sqrt(res / res0) < (double)tol) { *iters_done = k + 1; break; }
     }
   }
   if (n_iter > 0 && *iters_done > 0) {   // x += alpha_last p_last
@@ -770,7 +928,7 @@ static mrf_status run_cg_launch(mrf_plan_s* pl, const float2* y, const float2* z
     k_cg_xfin<<<nblk, kVecThreads, 0, st>>>(x, pl->p, n, pl->sc);
     MRF_TRY(vec_launch_check("k_cg_xfin"));
   }
-  *rho0_out = rho0;
+  *res0_out = res0;
   return MRF_OK;
 }
 
@@ -793,7 +951,8 @@ static void drop_cg_graphs(mrf_plan_s* pl) {
 }
 
 static mrf_status run_cg(mrf_plan_s* pl, const float2* y, const float2* z, float mu, int n_iter, float tol,
-                         float2* x, mrf_cg_info* info, cudaStream_t st, bool zero_init = false) {
+                         float2* x, mrf_cg_info* info, cudaStream_t st, bool zero_init = false, bool pc = false) {
+  if (pc) MRF_TRY(ensure_precond(pl, mu, st));
   if (n_iter + 1 > pl->hist_cap) {   // [sqrt(rho_k), k <= n][alpha_k][beta_k]
     drop_cg_graphs(pl);
     if (pl->hist) cudaFree(pl->hist);
@@ -806,7 +965,7 @@ static mrf_status run_cg(mrf_plan_s* pl, const float2* y, const float2* z, float
   double rho0 = -1.0;
   const bool graph = g_cg_graph && tol == 0.f && !pl->host_ar && !pl->prof.on;
   if (graph) {
-    const CgKey key{x, y, z, mu, n_iter, zero_init};
+    const CgKey key{x, y, z, mu, n_iter, zero_init, pc};
     int slot = -1;
     for (int i = 0; i < mrf_plan_s::kGraphs; ++i)
       if (pl->cg_exec[i] && pl->cg_key[i] == key) slot = i;
@@ -818,7 +977,7 @@ static mrf_status run_cg(mrf_plan_s* pl, const float2* y, const float2* z, float
       pl->cg_exec[slot] = nullptr;
       if (!pl->gstream) CUDA_TRY(cudaStreamCreateWithFlags(&pl->gstream, cudaStreamNonBlocking));
       CUDA_TRY(cudaStreamBeginCapture(pl->gstream, cudaStreamCaptureModeThreadLocal));
-      mrf_status rc = run_cg_launch(pl, y, z, mu, n_iter, tol, x, pl->gstream, zero_init, &iters_done, &rho0);
+      mrf_status rc = run_cg_launch(pl, y, z, mu, n_iter, tol, x, pl->gstream, zero_init, pc, &iters_done, &rho0);
       cudaGraph_t g = nullptr;
       const cudaError_t ce = cudaStreamEndCapture(pl->gstream, &g);
       if (rc != MRF_OK) {
@@ -837,17 +996,17 @@ static mrf_status run_cg(mrf_plan_s* pl, const float2* y, const float2* z, float
     pl->cg_use[slot] = ++pl->cg_clock;
     CUDA_TRY(cudaGraphLaunch(pl->cg_exec[slot], st));
   } else {
-    MRF_TRY(run_cg_launch(pl, y, z, mu, n_iter, tol, x, st, zero_init, &iters_done, &rho0));
+    MRF_TRY(run_cg_launch(pl, y, z, mu, n_iter, tol, x, st, zero_init, pc, &iters_done, &rho0));
   }
   CGScalars hs;
   CUDA_TRY(cudaMemcpyAsync(&hs, pl->sc, sizeof(CGScalars), cudaMemcpyDeviceToHost, st));
   std::vector<double> hh(3 * (size_t)pl->hist_cap, 0.0);
   CUDA_TRY(cudaMemcpyAsync(hh.data(), pl->hist, sizeof(double) * hh.size(), cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaStreamSynchronize(st));
-  if (hs.rho0 == 0.0) iters_done = 0;
+  if (hs.res0 == 0.0) iters_done = 0;
   if (info) {
     info->iters = iters_done;
-    info->rel_resid = hs.rho0 > 0.0 ? std::sqrt(hs.rho / hs.rho0) : 0.0;
+    info->rel_resid = hs.res0 > 0.0 ? std::sqrt(hs.res / hs.res0) : 0.0;
     if (info->history) {
       for (int i = 0; i <= n_iter; ++i) info->history[i] = i <= iters_done ? hh[i] : 0.0;
     }
@@ -1116,6 +1275,7 @@ mrf_status mrf_plan_create(const mrf_plan_desc* d, mrf_plan* out) {
   }
   pl->frame_offset = d->frame_offset;
   pl->flags = d->flags;
+  pl->traj_h.assign(d->traj, d->traj + (size_t)R * M * 2);
   pl->device = d->device;
   pl->nccl_comm = d->nccl_comm;
   auto bail = [&](mrf_status s) { free_plan(pl); return s; };
@@ -1501,8 +1661,9 @@ mrf_status mrf_dc_cg(mrf_plan pl, const void* y, const void* z, float mu, int n_
 mrf_status mrf_dc_cg_ex(mrf_plan pl, const void* y, const void* z, float mu, int n_iter, float tol, unsigned flags,
                         void* x, mrf_cg_info* info, void* stream) {
   if (!pl || !y || !x) return fail(MRF_EINVAL, "null plan/y/x");
-  if (flags & ~(MRF_CG_ZERO_INIT | MRF_CG_ASYNC_HOST)) return fail(MRF_EINVAL, "unknown CG flags");
+  if (flags & ~(MRF_CG_ZERO_INIT | MRF_CG_ASYNC_HOST | MRF_CG_PRECOND)) return fail(MRF_EINVAL, "unknown CG flags");
   const bool zero_init = (flags & MRF_CG_ZERO_INIT) != 0, async = (flags & MRF_CG_ASYNC_HOST) != 0;
+  const bool pc = (flags & MRF_CG_PRECOND) != 0;
   if (!(mu >= 0.f) || !std::isfinite(mu)) return fail(MRF_EINVAL, "mu must be finite and >= 0");
   if (n_iter < 0) return fail(MRF_EINVAL, "n_iter < 0");
   if (!(tol >= 0.f) || !std::isfinite(tol)) return fail(MRF_EINVAL, "tol must be finite and >= 0");
@@ -1512,7 +1673,7 @@ mrf_status mrf_dc_cg_ex(mrf_plan pl, const void* y, const void* z, float mu, int
   MRF_TRY(classify(pl, {y, z, x}, &host));
   if (!host) {
     if (async) return fail(MRF_EINVAL, "MRF_CG_ASYNC_HOST needs host buffers");
-    return run_cg(pl, (const float2*)y, (const float2*)z, mu, n_iter, tol, (float2*)x, info, st, zero_init);
+    return run_cg(pl, (const float2*)y, (const float2*)z, mu, n_iter, tol, (float2*)x, info, st, zero_init, pc);
   }
   const size_t bx = (size_t)pl->L * pl->N * pl->N * sizeof(float2), by = (size_t)pl->L * pl->C * pl->M * sizeof(float2);
   if (async) {
@@ -1526,7 +1687,7 @@ mrf_status mrf_dc_cg_ex(mrf_plan pl, const void* y, const void* z, float mu, int
     CUDA_TRY(cudaMemcpyAsync(pl->ay[s], y, by, cudaMemcpyHostToDevice, st));
     if (!zero_init) CUDA_TRY(cudaMemcpyAsync(pl->ax[s], x, bx, cudaMemcpyHostToDevice, st));
     if (z) CUDA_TRY(cudaMemcpyAsync(pl->stg_z, z, bx, cudaMemcpyHostToDevice, st));
-    mrf_status r = run_cg(pl, pl->ay[s], z ? pl->stg_z : nullptr, mu, n_iter, tol, pl->ax[s], info, st, zero_init);
+    mrf_status r = run_cg(pl, pl->ay[s], z ? pl->stg_z : nullptr, mu, n_iter, tol, pl->ax[s], info, st, zero_init, pc);
     if (r != MRF_OK && r != MRF_ENUMERIC) return r;
     CUDA_TRY(cudaEventRecord(pl->ev_solved[s], st));
     CUDA_TRY(cudaStreamWaitEvent(pl->cstream, pl->ev_solved[s], 0));
@@ -1538,7 +1699,7 @@ mrf_status mrf_dc_cg_ex(mrf_plan pl, const void* y, const void* z, float mu, int
   CUDA_TRY(cudaMemcpyAsync(pl->stg_y, y, by, cudaMemcpyHostToDevice, st));
   if (!zero_init) CUDA_TRY(cudaMemcpyAsync(pl->stg_x, x, bx, cudaMemcpyHostToDevice, st));
   if (z) CUDA_TRY(cudaMemcpyAsync(pl->stg_z, z, bx, cudaMemcpyHostToDevice, st));
-  mrf_status s = run_cg(pl, pl->stg_y, z ? pl->stg_z : nullptr, mu, n_iter, tol, pl->stg_x, info, st, zero_init);
+  mrf_status s = run_cg(pl, pl->stg_y, z ? pl->stg_z : nullptr, mu, n_iter, tol, pl->stg_x, info, st, zero_init, pc);
   if (s != MRF_OK && s != MRF_ENUMERIC) return s;
   CUDA_TRY(cudaMemcpyAsync(x, pl->stg_x, bx, cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaStreamSynchronize(st));
@@ -1575,6 +1736,16 @@ mrf_status mrf_profile_query(mrf_plan pl, int cls, double* total_ms, long long* 
   }
   if (total_ms) *total_ms = tot;
   if (launches) *launches = (long long)(pr.used[cls] / 2);
+  return MRF_OK;
+}
+
+mrf_status mrf_plan_set_precond_shift(mrf_plan pl, double shift) {
+  if (!pl) return fail(MRF_EINVAL, "null plan");
+  if (!(shift >= 0.0) || !std::isfinite(shift)) return fail(MRF_EINVAL, "shift must be finite and >= 0");
+  DeviceGuard guard(pl->device);
+  cudaDeviceSynchronize();   // captured PCG graphs bake gamma in
+  drop_cg_graphs(pl);
+  pl->pc_shift = shift;
   return MRF_OK;
 }
 
