@@ -216,23 +216,37 @@ mrf_status mrf_plan_set_host_allreduce(mrf_plan plan, mrf_host_allreduce_fn fn, 
  *   k_v   = argmax_k |<d_k, x_v>| / ||d_k||_2        ties -> lowest k   (reading 21)
  *   pd_v  = max(Re<d_k, x_v> / ||d_k||_2^2, 0)       eta_v = LUT[k_v]
  *
- * with <d, x> = sum_l conj(d_l) x_l over the L frames.  The correlations run on the tensor cores
- * (tcgen05, fp16 operands scaled per voxel and per atom into [-1, 1], fp32 accumulation), so
- * near-ties (atoms whose normalised correlations with x_v differ by less than ~1e-4 of the
- * maximum) may resolve to either atom; pd is then recomputed exactly in fp32 for the chosen atom. */
+ * with <d, x> = sum_l conj(d_l) x_l over the L frames.  The argmax is exact: a certified filter on
+ * the tensor cores lists every atom that can be the best, and the listed atoms are rescored from the
+ * complex64 data with float64 accumulation (ties -> lowest index).  Filter: the dictionary's leading
+ * Rf <= 64 right singular vectors phi (computed at mrf_dict_create); for any x,
+ * <d_k, x> = <phi d_k, phi x> + <r_k, x> with r_k = (I - phi^H phi) d_k, so the normalised
+ * correlation rho = |<d, x>| / (||d|| ||x||) is approximated by a 3xFP16 tcgen05 GEMM of the
+ * coefficients to within a bound beta that adds max_k ||r_k|| / ||d_k|| (float64), the projection's
+ * fp32 rounding, the split-operand rounding and the worst-case fp32 accumulation; every atom within
+ * 2 beta of the filter's best is rescored.  A voxel with more than 32 such atoms is rescored
+ * against every atom (mrf_dict_overflow counts them), so the result never depends on the filter;
+ * a dictionary without a compressible spectrum is slower, never wrong.  pd uses the exact <d_k, x>. */
 typedef struct mrf_dict_s* mrf_dict;
 
 /* atoms: HOST [K][L] complex64 (interleaved re, im), copied; lut: HOST [K][P] float (P >= 0
- * parameters per atom, e.g. T1, T2; NULL if P == 0), copied.  K >= 1, 1 <= L <= 65536.
+ * parameters per atom, e.g. T1, T2; NULL if P == 0), copied.  K >= 1, 1 <= L <= 65536.  Builds the
+ * filter basis (subspace iteration on D^H D, float64 residuals; synchronous).
  * Errors: MRF_EINVAL (sizes / NULL), MRF_ENOMEM, MRF_ECUDA.  An all-zero atom is never matched. */
 mrf_status mrf_dict_create(const void* atoms, const float* lut, int K, int L, int P, int device, mrf_dict* out);
 
 /* x: DEVICE [L][V] complex64, frame-major (the layout of the image stack, voxel fastest).
  * index: DEVICE int32 [V]; pd: DEVICE float [V]; params: DEVICE float [V][P] or NULL.  All
- * 16-byte aligned.  Asynchronous on `stream`; workspace (V x 2L fp16) is allocated on first use
- * and grown as needed (that call synchronises).  Errors: MRF_EINVAL, MRF_ENOMEM, MRF_ECUDA. */
+ * 16-byte aligned.  Asynchronous on `stream`; workspaces (a voxel-major copy of x, V x 8L bytes,
+ * and V x ~1 KB) are allocated on first use and grown as needed (that call synchronises).  A zero
+ * voxel gets index 0, pd 0.  Errors: MRF_EINVAL, MRF_ENOMEM, MRF_ECUDA. */
 mrf_status mrf_dict_match(mrf_dict dict, const void* x, long long V, int* index, float* pd, float* params,
                           void* stream);
+/* Voxels of the last match that were rescored against every atom (more than 32 atoms inside the
+ * certified band); synchronises.  The filter: *rank = Rf, *beta = the bound on the normalised
+ * correlation, *residual = max_k ||r_k|| / ||d_k|| (nullable outputs). */
+mrf_status mrf_dict_overflow(mrf_dict dict, int* voxels);
+mrf_status mrf_dict_filter_info(mrf_dict dict, int* rank, double* beta, double* residual);
 
 mrf_status mrf_dict_destroy(mrf_dict dict);
 
@@ -250,9 +264,10 @@ mrf_status mrf_dict_basis_copy(mrf_dict dict, void* basis_out);
 /* Phi_D of voxels given in basis coordinates: u DEVICE [r][V] complex64 (coefficient-major, the
  * layout of an r-frame image stack) with x_v = sum_i u[i][v] d_i.  For such x (every iterate of
  * mrf_llr_step lies in span(d)) <d_k, x_v> = sum_i u[i][v] conj(Dc[k][i]) with Dc = D d^dagger
- * (built by mrf_dict_basis), so index / pd / params are those of mrf_dict_match(x) up to rounding
- * (the argmax keeps the full atom norms ||d_k||), at r instead of L frames of work.  Needs
- * mrf_dict_basis; otherwise as mrf_dict_match. */
+ * (built by mrf_dict_basis in float64), so the exact scores need r instead of L frames of work;
+ * the filter coefficients are phi x = sum_i u_i (phi d_i) and ||x||^2 = u^H (d d^H) u (float64).
+ * The argmax is exact for that x (same certified filter and rescoring as mrf_dict_match; the full
+ * atom norms ||d_k|| are kept).  Needs mrf_dict_basis; otherwise as mrf_dict_match. */
 mrf_status mrf_dict_match_coef(mrf_dict dict, const void* u, long long V, int* index, float* pd, float* params,
                                void* stream);
 

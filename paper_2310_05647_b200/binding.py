@@ -35,7 +35,7 @@ EXPORTED = [
     "mrf_dict_profile", "mrf_dict_profile_query", "mrf_dict_basis", "mrf_dict_basis_copy", "mrf_llr_create",
     "mrf_llr_step", "mrf_llr_destroy", "mrf_llr_laplacian", "mrf_llr_cost", "mrf_msllr_solve", "mrf_plan_wait",
     "mrf_dict_match_coef", "mrf_llr_create_basis", "mrf_llr_subspace_normal", "mrf_llr_create_shard",
-    "mrf_plan_set_host_allreduce", "mrf_plan_set_precond_shift",
+    "mrf_plan_set_host_allreduce", "mrf_plan_set_precond_shift", "mrf_dict_overflow", "mrf_dict_filter_info",
 ]
 
 MRF_DTYPE_F32 = 0
@@ -109,6 +109,9 @@ def _load() -> ctypes.CDLL:
         "mrf_dict_match": ([vp, vp, ctypes.c_longlong, vp, vp, vp, vp], ci),
         "mrf_dict_match_coef": ([vp, vp, ctypes.c_longlong, vp, vp, vp, vp], ci),
         "mrf_dict_destroy": ([vp], ci),
+        "mrf_dict_overflow": ([vp, ctypes.POINTER(ci)], ci),
+        "mrf_dict_filter_info": ([vp, ctypes.POINTER(ci), ctypes.POINTER(ctypes.c_double),
+                                  ctypes.POINTER(ctypes.c_double)], ci),
         "mrf_dict_profile": ([vp, ci], ci),
         "mrf_dict_profile_query": ([vp, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_longlong)], ci),
         "mrf_dict_basis": ([vp, ctypes.c_double, ci, ctypes.POINTER(ci)], ci),
@@ -430,6 +433,18 @@ class Dictionary:
         st = torch.cuda.current_stream(u.device).cuda_stream
         _check(lib.mrf_dict_match_coef(self._h, _ptr(u), V, _ptr(index), _ptr(pd), _ptr(params), ctypes.c_void_p(st)))
         return index, pd, params
+
+    def overflow(self) -> int:
+        """Voxels of the last match rescored against every atom (mrf_dict_overflow)."""
+        n = ctypes.c_int()
+        _check(lib.mrf_dict_overflow(self._h, ctypes.byref(n)))
+        return n.value
+
+    def filter_info(self):
+        """(Rf, beta, max residual) of the certified filter (mrf_dict_filter_info)."""
+        r, b, res = ctypes.c_int(), ctypes.c_double(), ctypes.c_double()
+        _check(lib.mrf_dict_filter_info(self._h, ctypes.byref(r), ctypes.byref(b), ctypes.byref(res)))
+        return r.value, b.value, res.value
 
     def basis(self, energy: float = 0.9999, max_rank: int = 32) -> np.ndarray:
         """Subspace basis of P_S (Eq. 17): [r][L] complex64 orthonormal rows (mrf_dict_basis)."""

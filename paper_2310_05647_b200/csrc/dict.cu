@@ -23,8 +23,6 @@
 
 using namespace mrf;
 
-static constexpr int kKDc = 64;   // fp16 row length of the basis-coordinate dictionary (2 rank <= 64)
-
 
 static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -62,10 +60,108 @@ static mrf_status make_tmap(CUtensorMap* m, const __half* base, uint64_t cols, u
 static void dict_free(mrf_dict_s* d) {
   if (!d) return;
   cudaSetDevice(d->device);
-  for (void* p : {(void*)d->dp, (void*)d->w2, (void*)d->n2inv, (void*)d->atoms, (void*)d->lut, (void*)d->xp,
-                  (void*)d->xs, (void*)d->best, (void*)d->basis, (void*)d->dpc, (void*)d->w2c, (void*)d->Dc})
+  for (void* p : {(void*)d->atoms, (void*)d->dn2, (void*)d->lut, (void*)d->phi, (void*)d->phiT, (void*)d->dpf,
+                  (void*)d->w2f, (void*)d->xp, (void*)d->xs, (void*)d->xnorm, (void*)d->best, (void*)d->thr,
+                  (void*)d->ncand, (void*)d->cand, (void*)d->ov, (void*)d->nov, (void*)d->xT, (void*)d->basis,
+                  (void*)d->Mf, (void*)d->Gd, (void*)d->Dc})
     if (p) cudaFree(p);
   delete d;
+}
+
+static mrf_status top_right_vectors(mrf_dict d, int k, std::vector<std::complex<double>>& rows, std::vector<double>& lam);
+
+// The certified filter of Phi_D (match.cuh header): phi = the leading Rf <= 64 right singular
+// vectors (subspace iteration, as mrf_dict_basis), a_k = phi d_k, ||r_k|| and ||a_k||_1 in float64
+// on the device (k_dict_filter_atoms), the packed fp16 rows [a_hi | a_hi | a_lo] / m_k, the weights
+// (m_k / ||d_k||)^2, and the bound beta on |rho~_k - rho_k| of the normalised correlation.
+static mrf_status build_filter(mrf_dict d) {
+  const int K = d->K, L = d->L, k = std::min({dm::RF + 16, K, L});
+  std::vector<std::complex<double>> rows;
+  std::vector<double> lam;
+  MRF_TRY(top_right_vectors(d, k, rows, lam));
+  const int Rf = std::min(dm::RF, k);
+  d->Rf = Rf;
+  std::vector<float2> ph((size_t)dm::RF * L, make_float2(0.f, 0.f)), phT((size_t)L * dm::RF, make_float2(0.f, 0.f));
+  for (int f = 0; f < Rf; ++f)
+    for (int l = 0; l < L; ++l) {
+      const std::complex<double> v = rows[(size_t)f * L + l];
+      ph[(size_t)f * L + l] = phT[(size_t)l * dm::RF + f] = make_float2((float)v.real(), (float)v.imag());
+    }
+  double2* a = nullptr;
+  double *res2 = nullptr, *a1 = nullptr;
+  auto cleanup = [&]() {
+    for (void* p : {(void*)a, (void*)res2, (void*)a1})
+      if (p) cudaFree(p);
+  };
+  if (cudaMalloc((void**)&d->phi, ph.size() * sizeof(float2)) != cudaSuccess ||
+      cudaMalloc((void**)&d->phiT, phT.size() * sizeof(float2)) != cudaSuccess ||
+      cudaMalloc((void**)&a, (size_t)K * dm::RF * sizeof(double2)) != cudaSuccess ||
+      cudaMalloc((void**)&res2, (size_t)K * sizeof(double)) != cudaSuccess ||
+      cudaMalloc((void**)&a1, (size_t)K * sizeof(double)) != cudaSuccess) {
+    cleanup();
+    return fail(MRF_ENOMEM, "mrf_dict_create: filter allocation failed");
+  }
+  cudaError_t e = cudaMemcpy(d->phi, ph.data(), ph.size() * sizeof(float2), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(d->phiT, phT.data(), phT.size() * sizeof(float2), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) {
+    dm::k_dict_filter_atoms<<<K, 256>>>(d->atoms, d->phi, L, a, res2, a1);
+    e = cudaGetLastError();
+  }
+  std::vector<double2> ah((size_t)K * dm::RF);
+  std::vector<double> r2h(K), a1h(K), dn2(K);
+  if (e == cudaSuccess) e = cudaMemcpy(ah.data(), a, ah.size() * sizeof(double2), cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess) e = cudaMemcpy(r2h.data(), res2, (size_t)K * sizeof(double), cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess) e = cudaMemcpy(a1h.data(), a1, (size_t)K * sizeof(double), cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess) e = cudaMemcpy(dn2.data(), d->dn2, (size_t)K * sizeof(double), cudaMemcpyDeviceToHost);
+  cleanup();
+  if (e != cudaSuccess) return fail(MRF_ECUDA, std::string("mrf_dict_create: filter setup: ") + cudaGetErrorString(e));
+  // packed atom rows: 2k = (ar, ai) and 2k+1 = (-ai, ar) per coefficient, scaled by 1/m_k, split
+  // into fp16 hi + lo: [hi | hi | lo] against the voxel rows [u_hi | u_lo | u_hi]
+  std::vector<__half> dp((size_t)d->NP * dm::KF, __float2half(0.f));
+  std::vector<float> w2((size_t)d->NP / 2, 0.f);
+  double bres = 0.0, ba1 = 0.0;
+  for (int kk = 0; kk < K; ++kk) {
+    if (!(dn2[kk] > 0.0)) continue;   // zero atom: w2 = 0, never listed
+    double m = 0.0;
+    for (int f = 0; f < dm::RF; ++f) m = std::max({m, std::fabs(ah[(size_t)kk * dm::RF + f].x), std::fabs(ah[(size_t)kk * dm::RF + f].y)});
+    const double nd = std::sqrt(dn2[kk]);
+    bres = std::max(bres, std::sqrt(std::max(r2h[kk], 0.0)) / nd);
+    ba1 = std::max(ba1, a1h[kk] / nd);
+    if (!(m > 0.0)) continue;         // no component in the filter space: its score is 0 (+ band)
+    w2[kk] = (float)(m * m / dn2[kk]);
+    __half* r0 = &dp[(size_t)(2 * kk) * dm::KF];
+    __half* r1 = r0 + dm::KF;
+    for (int f = 0; f < dm::RF; ++f) {
+      const double2 v = ah[(size_t)kk * dm::RF + f];
+      double comp[4] = {v.x / m, v.y / m, -v.y / m, v.x / m};   // r0: (ar, ai), r1: (-ai, ar)
+      for (int c = 0; c < 4; ++c) {
+        __half hi, lo;
+        hi = __double2half(comp[c]);
+        lo = __double2half(comp[c] - (double)__half2float(hi));
+        __half* row = c < 2 ? r0 : r1;
+        const int col = 2 * f + (c & 1);
+        row[col] = hi;
+        row[2 * dm::RF + col] = hi;
+        row[4 * dm::RF + col] = lo;
+      }
+    }
+  }
+  // beta (match.cuh): residual ||r_k|| / ||d_k|| (plus 1e-12 for its float64 evaluation) +
+  // projection rounding sqrt(2) 32 u32 ||a_k||_1 / ||d_k|| + split-operand rounding 3 u16^2 +
+  // subnormal half (2^-25 sqrt(2 RF) 2) + worst-case fp32 accumulation of the K = 384 products
+  // gamma_384, on both components (sqrt 2), + the fp32 score arithmetic (1e-6), x 1.05
+  const double u32 = std::ldexp(1.0, -24), u16 = std::ldexp(1.0, -11);
+  const double g384 = 384.0 * u32 / (1.0 - 384.0 * u32);
+  const double gemm = std::sqrt(2.0) * ((3.0 * u16 * u16 + g384) * 1.001 + std::ldexp(1.0, -25) * std::sqrt(2.0 * dm::RF) * 2.0);
+  d->beta_res = bres;
+  d->beta_a1 = ba1;
+  d->beta = 1.05 * ((bres + 1e-12) + std::sqrt(2.0) * 32.0 * u32 * ba1 + gemm + 1e-6);
+  if (cudaMalloc((void**)&d->dpf, dp.size() * sizeof(__half)) != cudaSuccess ||
+      cudaMalloc((void**)&d->w2f, w2.size() * sizeof(float)) != cudaSuccess)
+    return fail(MRF_ENOMEM, "mrf_dict_create: filter allocation failed");
+  CUDA_TRY(cudaMemcpy(d->dpf, dp.data(), dp.size() * sizeof(__half), cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(d->w2f, w2.data(), w2.size() * sizeof(float), cudaMemcpyHostToDevice));
+  return make_tmap(&d->tmdf, d->dpf, (uint64_t)dm::KF, (uint64_t)d->NP, (uint32_t)dm::BN);
 }
 
 extern "C" {
@@ -77,61 +173,43 @@ mrf_status mrf_dict_create(const void* atoms, const float* lut, int K, int L, in
   CUDA_TRY(cudaSetDevice(device));
   auto* d = new mrf_dict_s();
   d->K = K; d->L = L; d->P = P; d->device = device;
-  d->KD = ((2 * L + dm::BK - 1) / dm::BK) * dm::BK;
   d->NP = ((2 * K + dm::BN - 1) / dm::BN) * dm::BN;
   const float2* a = reinterpret_cast<const float2*>(atoms);
-  // host packing (once per dictionary): fp16 rows 2k = (dr, di)/m_k, 2k+1 = (-di, dr)/m_k
-  std::vector<__half> dp((size_t)d->NP * d->KD, __float2half(0.f));
-  std::vector<float> w2(d->NP / 2, 0.f), n2inv(K, 0.f);
+  std::vector<double> dn2(K, 0.0);
   for (int k = 0; k < K; ++k) {
-    double n2 = 0.0, m = 0.0;
+    double n2 = 0.0;
     for (int l = 0; l < L; ++l) {
       const float2 v = a[(size_t)k * L + l];
       n2 += (double)v.x * v.x + (double)v.y * v.y;
-      m = std::max(m, (double)std::max(std::fabs(v.x), std::fabs(v.y)));
     }
+    dn2[k] = n2;
     d->fro2 += n2;
-    if (n2 <= 0.0) continue;   // zero atom: w2 = 0, never preferred over a non-zero one
-    n2inv[k] = (float)(1.0 / n2);
-    w2[k] = (float)(m * m / n2);
-    const double im = 1.0 / m;
-    __half* r0 = &dp[(size_t)(2 * k) * d->KD];
-    __half* r1 = r0 + d->KD;
-    for (int l = 0; l < L; ++l) {
-      const float2 v = a[(size_t)k * L + l];
-      r0[2 * l] = __float2half((float)(v.x * im));
-      r0[2 * l + 1] = __float2half((float)(v.y * im));
-      r1[2 * l] = __float2half((float)(-v.y * im));
-      r1[2 * l + 1] = __float2half((float)(v.x * im));
-    }
   }
   auto alloc = [&](void** p, size_t bytes) { return cudaMalloc(p, bytes) == cudaSuccess; };
-  if (!alloc((void**)&d->dp, dp.size() * sizeof(__half)) || !alloc((void**)&d->w2, w2.size() * sizeof(float)) ||
-      !alloc((void**)&d->n2inv, (size_t)K * sizeof(float)) || !alloc((void**)&d->atoms, (size_t)K * L * sizeof(float2)) ||
+  if (!alloc((void**)&d->atoms, (size_t)K * L * sizeof(float2)) || !alloc((void**)&d->dn2, (size_t)K * sizeof(double)) ||
       (P > 0 && !alloc((void**)&d->lut, (size_t)K * P * sizeof(float)))) {
     dict_free(d);
     return fail(MRF_ENOMEM, "mrf_dict_create: device allocation failed");
   }
-  cudaError_t e = cudaMemcpy(d->dp, dp.data(), dp.size() * sizeof(__half), cudaMemcpyHostToDevice);
-  if (e == cudaSuccess) e = cudaMemcpy(d->w2, w2.data(), w2.size() * sizeof(float), cudaMemcpyHostToDevice);
-  if (e == cudaSuccess) e = cudaMemcpy(d->n2inv, n2inv.data(), (size_t)K * sizeof(float), cudaMemcpyHostToDevice);
-  if (e == cudaSuccess) e = cudaMemcpy(d->atoms, a, (size_t)K * L * sizeof(float2), cudaMemcpyHostToDevice);
+  cudaError_t e = cudaMemcpy(d->atoms, a, (size_t)K * L * sizeof(float2), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(d->dn2, dn2.data(), (size_t)K * sizeof(double), cudaMemcpyHostToDevice);
   if (e == cudaSuccess && P > 0) e = cudaMemcpy(d->lut, lut, (size_t)K * P * sizeof(float), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(dm::k_dict_gemm<2, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dm::SMEM);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(dm::k_dict_gemm<2, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dm::SMEM);
   if (e != cudaSuccess) {
     dict_free(d);
     return fail(MRF_ECUDA, std::string("mrf_dict_create: ") + cudaGetErrorString(e));
   }
-  mrf_status s = make_tmap(&d->tmd, d->dp, (uint64_t)d->KD, (uint64_t)d->NP, (uint32_t)dm::BN);
+  if (!(d->fro2 > 0.0)) {   // all-zero dictionary: every score is 0 (no filter needed)
+    *out = d;
+    return MRF_OK;
+  }
+  mrf_status s = build_filter(d);
   if (s != MRF_OK) {
     dict_free(d);
     return s;
-  }
-  e = cudaFuncSetAttribute(dm::k_dict_gemm<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dm::SMEM);
-  if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(dm::k_dict_gemm<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dm::SMEM);
-  if (e != cudaSuccess) {
-    dict_free(d);
-    return fail(MRF_ECUDA, std::string("mrf_dict_create: ") + cudaGetErrorString(e));
   }
   *out = d;
   return MRF_OK;
@@ -139,38 +217,48 @@ mrf_status mrf_dict_create(const void* atoms, const float* lut, int K, int L, in
 
 }  // extern "C"
 
-// Phi_D of x [L][V] against packed rows (tmd, KD) with weights w2 and exact-pd atoms [K][L]:
-// the frame-domain match (L = d->L) and the basis-coordinate match (L = rank, Dc).
-static mrf_status match_impl(mrf_dict d, const char* who, const void* x, int L, int KD, const CUtensorMap& tmd,
-                             const float* w2, const float2* atoms, long long V, int* index, float* pd, float* params,
-                             void* stream) {
-  if (!d || !x || !index || !pd || V < 1 || V > (1LL << 30))
-    return fail(MRF_EINVAL, std::string(who) + ": invalid arguments");
-  for (const void* p : {x, (const void*)index, (const void*)pd, (const void*)params})
-    if (p && ((uintptr_t)p % 16) != 0) return fail(MRF_EINVAL, std::string(who) + ": arrays must be 16-byte aligned");
-  CUDA_TRY(cudaSetDevice(d->device));
-  cudaStream_t st = (cudaStream_t)stream;
-  const long long vpad = ((V + dm::BM - 1) / dm::BM) * dm::BM;
-  if (vpad > d->vcap) {   // rows of d->KD >= 64 >= KD fp16 (the basis-coordinate packing fits too)
+static mrf_status grow(mrf_dict d, long long vpad, long long vt, int L, cudaStream_t st, const char* who) {
+  if (vpad > d->vcap) {
     CUDA_TRY(cudaStreamSynchronize(st));
-    if (d->xp) cudaFree(d->xp);
-    if (d->xs) cudaFree(d->xs);
-    if (d->best) cudaFree(d->best);
-    d->xp = nullptr; d->xs = nullptr; d->best = nullptr; d->vcap = 0;
-    if (cudaMalloc((void**)&d->xp, (size_t)vpad * d->KD * sizeof(__half)) != cudaSuccess ||
+    for (void** p : {(void**)&d->xp, (void**)&d->xs, (void**)&d->xnorm, (void**)&d->best, (void**)&d->thr,
+                     (void**)&d->ncand, (void**)&d->cand, (void**)&d->ov})
+      if (*p) { cudaFree(*p); *p = nullptr; }
+    d->vcap = 0;
+    if (cudaMalloc((void**)&d->xp, (size_t)vpad * dm::KF * sizeof(__half)) != cudaSuccess ||
         cudaMalloc((void**)&d->xs, (size_t)vpad * sizeof(float)) != cudaSuccess ||
-        cudaMalloc((void**)&d->best, (size_t)vpad * sizeof(unsigned long long)) != cudaSuccess)
+        cudaMalloc((void**)&d->xnorm, (size_t)vpad * sizeof(double)) != cudaSuccess ||
+        cudaMalloc((void**)&d->best, (size_t)vpad * sizeof(unsigned long long)) != cudaSuccess ||
+        cudaMalloc((void**)&d->thr, (size_t)vpad * sizeof(float)) != cudaSuccess ||
+        cudaMalloc((void**)&d->ncand, (size_t)vpad * sizeof(int)) != cudaSuccess ||
+        cudaMalloc((void**)&d->cand, (size_t)vpad * dm::kCand * sizeof(int)) != cudaSuccess ||
+        cudaMalloc((void**)&d->ov, (size_t)vpad * sizeof(int)) != cudaSuccess)
+      return fail(MRF_ENOMEM, std::string(who) + ": workspace allocation failed");
+    if (!d->nov && cudaMalloc((void**)&d->nov, sizeof(int)) != cudaSuccess)
       return fail(MRF_ENOMEM, std::string(who) + ": workspace allocation failed");
     d->vcap = vpad;
   }
+  if (vt > d->vtcap) {
+    CUDA_TRY(cudaStreamSynchronize(st));
+    if (d->xT) cudaFree(d->xT);
+    d->xT = nullptr;
+    d->vtcap = 0;
+    if (cudaMalloc((void**)&d->xT, (size_t)vt * L * sizeof(float2)) != cudaSuccess)
+      return fail(MRF_ENOMEM, std::string(who) + ": workspace allocation failed");
+    d->vtcap = vt;
+  }
+  return MRF_OK;
+}
+
+// The two filter GEMM passes over the packed voxel rows d->xp (match.cuh steps 3): best score,
+// certified band, candidate lists.
+static mrf_status filter_passes(mrf_dict d, long long V, long long vpad, cudaStream_t st) {
   CUtensorMap tmx;
-  MRF_TRY(make_tmap(&tmx, d->xp, (uint64_t)KD, (uint64_t)vpad, (uint32_t)dm::BM));
-  const float2* xf = reinterpret_cast<const float2*>(x);
-  if (L <= 32 && KD == 64)
-    dm::k_dict_pack_short<<<(unsigned)((vpad + 255) / 256), 256, 0, st>>>(xf, L, (int)V, (int)vpad, KD, d->xp, d->xs);
-  else
-    dm::k_dict_pack_x<<<(unsigned)(vpad / 32), 256, 0, st>>>(xf, L, (int)V, KD, d->xp, d->xs);
-  MRF_TRY(check_launch("k_dict_pack_x"));
+  MRF_TRY(make_tmap(&tmx, d->xp, (uint64_t)dm::KF, (uint64_t)vpad, (uint32_t)dm::BM));
+  const int m_tiles = (int)(vpad / dm::BM), n_tiles = d->NP / dm::BN;
+  int n_sm = 148;
+  CUDA_TRY(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, d->device));
+  const unsigned grid = (unsigned)std::min(n_sm, m_tiles * n_tiles);
+  CUDA_TRY(cudaMemsetAsync(d->best, 0, (size_t)V * sizeof(unsigned long long), st));
   if (d->prof) {
     while (d->ev.size() < d->ev_used + 2) {
       cudaEvent_t e;
@@ -179,44 +267,100 @@ static mrf_status match_impl(mrf_dict d, const char* who, const void* x, int L, 
     }
     CUDA_TRY(cudaEventRecord(d->ev[d->ev_used], st));
   }
-  const int m_tiles = (int)(vpad / dm::BM), n_tiles = d->NP / dm::BN;
-  int n_sm = 148;
-  CUDA_TRY(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, d->device));
-  CUDA_TRY(cudaMemsetAsync(d->best, 0, (size_t)V * sizeof(unsigned long long), st));
-  const unsigned grid = (unsigned)std::min(n_sm, m_tiles * n_tiles);
-  if (KD / dm::BK == 1)   // short series (basis coordinates): two epilogue groups
-    dm::k_dict_gemm<2><<<grid, dm::threads<2>(), dm::SMEM, st>>>(tmx, tmd, w2, m_tiles, n_tiles, 1, (int)V, d->best);
-  else
-    dm::k_dict_gemm<1><<<grid, dm::threads<1>(), dm::SMEM, st>>>(tmx, tmd, w2, m_tiles, n_tiles, KD / dm::BK, (int)V,
-                                                                 d->best);
+  dm::k_dict_gemm<2, 0><<<grid, dm::threads<2>(), dm::SMEM, st>>>(tmx, d->tmdf, d->w2f, m_tiles, n_tiles, dm::KF / dm::BK,
+                                                                  (int)V, d->best, nullptr, nullptr, nullptr);
+  MRF_TRY(check_launch("k_dict_gemm"));
+  dm::k_dict_thr<<<(unsigned)((V + 255) / 256), 256, 0, st>>>(d->best, d->xnorm, d->xs, d->beta, (int)V, d->thr, d->ncand);
+  MRF_TRY(check_launch("k_dict_thr"));
+  dm::k_dict_gemm<2, 1><<<grid, dm::threads<2>(), dm::SMEM, st>>>(tmx, d->tmdf, d->w2f, m_tiles, n_tiles, dm::KF / dm::BK,
+                                                                  (int)V, nullptr, d->thr, d->ncand, d->cand);
   MRF_TRY(check_launch("k_dict_gemm"));
   if (d->prof) {
     CUDA_TRY(cudaEventRecord(d->ev[d->ev_used + 1], st));
     d->ev_used += 2;
   }
-  if (L <= 32)
-    dm::k_dict_fix_short<<<(unsigned)((V + 255) / 256), 256, 0, st>>>(xf, atoms, d->n2inv, d->lut, d->P, L, (int)V,
-                                                                      d->best, index, pd, params);
-  else
-    dm::k_dict_fix<<<(unsigned)((V + 31) / 32), 256, 0, st>>>(xf, atoms, d->n2inv, d->lut, d->P, L, (int)V, d->best,
-                                                                 index, pd, params);
-  MRF_TRY(check_launch("k_dict_fix"));
+  CUDA_TRY(cudaMemsetAsync(d->nov, 0, sizeof(int), st));
+  return MRF_OK;
+}
+
+static mrf_status check_args(mrf_dict d, const char* who, const void* x, long long V, int* index, float* pd,
+                             float* params) {
+  if (!d || !x || !index || !pd || V < 1 || V > (1LL << 30)) return fail(MRF_EINVAL, std::string(who) + ": invalid arguments");
+  for (const void* p : {x, (const void*)index, (const void*)pd, (const void*)params})
+    if (p && ((uintptr_t)p % 16) != 0) return fail(MRF_EINVAL, std::string(who) + ": arrays must be 16-byte aligned");
   return MRF_OK;
 }
 
 extern "C" {
 
 mrf_status mrf_dict_match(mrf_dict d, const void* x, long long V, int* index, float* pd, float* params, void* stream) {
-  if (!d) return fail(MRF_EINVAL, "mrf_dict_match: null dictionary");
-  return match_impl(d, "mrf_dict_match", x, d->L, d->KD, d->tmd, d->w2, d->atoms, V, index, pd, params, stream);
+  MRF_TRY(check_args(d, "mrf_dict_match", x, V, index, pd, params));
+  CUDA_TRY(cudaSetDevice(d->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  const long long vpad = ((V + dm::BM - 1) / dm::BM) * dm::BM;
+  MRF_TRY(grow(d, vpad, V, d->L, st, "mrf_dict_match"));
+  const float2* xf = reinterpret_cast<const float2*>(x);
+  if (!d->phi) {   // all-zero dictionary: the lowest index, PD 0 (every score is 0)
+    CUDA_TRY(cudaMemsetAsync(index, 0, (size_t)V * sizeof(int), st));
+    CUDA_TRY(cudaMemsetAsync(pd, 0, (size_t)V * sizeof(float), st));
+    if (params) CUDA_TRY(cudaMemsetAsync(params, 0, (size_t)V * d->P * sizeof(float), st));
+    return MRF_OK;
+  }
+  CUDA_TRY(cudaMemsetAsync(d->xp + (size_t)V * dm::KF, 0, (size_t)(vpad - V) * dm::KF * sizeof(__half), st));
+  dm::k_dict_proj_frames<<<(unsigned)((V + 31) / 32), 256, 0, st>>>(xf, d->phiT, d->L, (int)V, d->xT, d->xp, d->xs, d->xnorm);
+  MRF_TRY(check_launch("k_dict_proj_frames"));
+  MRF_TRY(filter_passes(d, V, vpad, st));
+  dm::k_dict_rescore_frames<<<(unsigned)((V + 7) / 8), 256, 0, st>>>(d->xT, d->atoms, d->dn2, d->xnorm, d->ncand, d->cand,
+                                                                    d->lut, d->P, d->L, (int)V, index, pd, params, d->ov,
+                                                                    d->nov);
+  MRF_TRY(check_launch("k_dict_rescore_frames"));
+  dm::k_dict_exact_frames<<<(unsigned)std::min<long long>(V, 1184), 256, 0, st>>>(d->xT, d->atoms, d->dn2, d->K, d->lut,
+                                                                                  d->P, d->L, d->ov, d->nov, index, pd,
+                                                                                  params);
+  return check_launch("k_dict_exact_frames");
 }
 
 mrf_status mrf_dict_match_coef(mrf_dict d, const void* u, long long V, int* index, float* pd, float* params,
                                void* stream) {
-  if (!d) return fail(MRF_EINVAL, "mrf_dict_match_coef: null dictionary");
-  if (!d->rank || !d->dpc) return fail(MRF_EINVAL, "mrf_dict_match_coef: no basis (call mrf_dict_basis)");
-  return match_impl(d, "mrf_dict_match_coef", u, d->rank, kKDc, d->tmdc, d->w2c, d->Dc, V, index, pd, params, stream);
+  MRF_TRY(check_args(d, "mrf_dict_match_coef", u, V, index, pd, params));
+  if (!d->rank || !d->Dc) return fail(MRF_EINVAL, "mrf_dict_match_coef: no basis (call mrf_dict_basis)");
+  CUDA_TRY(cudaSetDevice(d->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  const long long vpad = ((V + dm::BM - 1) / dm::BM) * dm::BM;
+  MRF_TRY(grow(d, vpad, 0, d->L, st, "mrf_dict_match_coef"));
+  const float2* w = reinterpret_cast<const float2*>(u);
+  CUDA_TRY(cudaMemsetAsync(d->xp + (size_t)V * dm::KF, 0, (size_t)(vpad - V) * dm::KF * sizeof(__half), st));
+  dm::k_dict_proj_coef<<<(unsigned)((V + 127) / 128), 128, 0, st>>>(w, d->rank, (int)V, d->Mf, d->Gd, d->xp, d->xs,
+                                                                     d->xnorm);
+  MRF_TRY(check_launch("k_dict_proj_coef"));
+  MRF_TRY(filter_passes(d, V, vpad, st));
+  dm::k_dict_rescore_coef<<<(unsigned)((V + 127) / 128), 128, 0, st>>>(w, d->rank, d->Dc, d->dn2, d->xnorm, d->ncand,
+                                                                        d->cand, d->lut, d->P, (int)V, index, pd, params,
+                                                                        d->ov, d->nov);
+  MRF_TRY(check_launch("k_dict_rescore_coef"));
+  dm::k_dict_exact_coef<<<64, 128, 0, st>>>(w, d->rank, d->Dc, d->dn2, d->K, d->lut, d->P, (int)V, d->ov, d->nov, index,
+                                            pd, params);
+  return check_launch("k_dict_exact_coef");
 }
+
+mrf_status mrf_dict_overflow(mrf_dict d, int* voxels) {
+  if (!d || !voxels) return fail(MRF_EINVAL, "mrf_dict_overflow: null argument");
+  CUDA_TRY(cudaSetDevice(d->device));
+  int n = 0;
+  if (d->nov) CUDA_TRY(cudaMemcpy(&n, d->nov, sizeof(int), cudaMemcpyDeviceToHost));
+  *voxels = n;
+  return MRF_OK;
+}
+
+mrf_status mrf_dict_filter_info(mrf_dict d, int* rank, double* beta, double* residual) {
+  if (!d) return fail(MRF_EINVAL, "mrf_dict_filter_info: null dictionary");
+  if (rank) *rank = d->Rf;
+  if (beta) *beta = d->beta;
+  if (residual) *residual = d->beta_res;
+  return MRF_OK;
+}
+
+}  // extern "C"
 
 // ---------------------------------------------------------------- subspace basis (Eq. 17, reading 24)
 // Leading right singular vectors of D by subspace iteration on D^H D (GEMMs on the device,
@@ -264,59 +408,46 @@ static void host_jacobi_eig(int n, std::vector<std::complex<double>>& H, std::ve
   for (int i = 0; i < n; ++i) lam[i] = H[(size_t)i * n + i].real();
 }
 
-// The dictionary in basis coordinates (mrf_dict_match_coef): Dc = D d^dagger [K][r] on the device
-// (k_cgemm computes conj(D) d^T with float64 accumulation), packed like the frame-domain rows with
-// per-atom scales m'_k = max |Re, Im| of Dc_k and weights (m'_k / ||d_k||)^2 from the FULL norms.
+// The match in basis coordinates (mrf_dict_match_coef; x = sum_i w_i d_i for the basis rows d_i):
+// Dc[k][i] = <d_i, d_k> (exact scores <d_k, x> = sum_i w_i conj(Dc[k][i])), Mf[i][f] = <phi_f, d_i>
+// (the filter coefficients u = phi x = sum_i w_i Mf[i]) and Gd[i][j] = <d_i, d_j> (||x||^2 =
+// w^H Gd w), all float64 on the device from the fp32 basis (k_cgemm, float64 accumulation).
 static mrf_status build_coef_dict(mrf_dict d, int r) {
   const int K = d->K, L = d->L;
-  for (void* p : {(void*)d->dpc, (void*)d->w2c, (void*)d->Dc})
+  for (void* p : {(void*)d->Mf, (void*)d->Gd, (void*)d->Dc})
     if (p) cudaFree(p);
-  d->dpc = nullptr; d->w2c = nullptr; d->Dc = nullptr;
-  if (cudaMalloc((void**)&d->Dc, (size_t)K * r * sizeof(float2)) != cudaSuccess ||
-      cudaMalloc((void**)&d->dpc, (size_t)d->NP * kKDc * sizeof(__half)) != cudaSuccess ||
-      cudaMalloc((void**)&d->w2c, (size_t)d->NP / 2 * sizeof(float)) != cudaSuccess)
+  d->Mf = nullptr; d->Gd = nullptr; d->Dc = nullptr;
+  if (cudaMalloc((void**)&d->Dc, (size_t)K * r * sizeof(double2)) != cudaSuccess ||
+      cudaMalloc((void**)&d->Mf, (size_t)r * dm::RF * sizeof(double2)) != cudaSuccess ||
+      cudaMalloc((void**)&d->Gd, (size_t)r * r * sizeof(double2)) != cudaSuccess)
     return fail(MRF_ENOMEM, "mrf_dict_basis: allocation failed");
-  const dim3 blk(16, 16), grd((unsigned)((r + 15) / 16), (unsigned)((K + 15) / 16));
-  llr::k_cgemm<<<grd, blk>>>(d->atoms, L, 1, 1, d->basis, 1, L, K, r, L, d->Dc, nullptr);   // conj(D) d^T
+  const dim3 blk(16, 16);
+  auto grid = [](int M, int N) { return dim3((unsigned)((N + 15) / 16), (unsigned)((M + 15) / 16)); };
+  // Dc^* = conj(D) d^T, i.e. conj(Dc[k][i]) = sum_l conj(d_kl) d_il  (conjugated on the host below)
+  llr::k_cgemm<<<grid(K, r), blk>>>(d->atoms, L, 1, 1, d->basis, 1, L, K, r, L, nullptr, d->Dc);
   MRF_TRY(check_launch("k_cgemm"));
-  std::vector<float2> dc((size_t)K * r);
-  CUDA_TRY(cudaMemcpy(dc.data(), d->Dc, dc.size() * sizeof(float2), cudaMemcpyDeviceToHost));
-  std::vector<float> n2inv(K);
-  CUDA_TRY(cudaMemcpy(n2inv.data(), d->n2inv, (size_t)K * sizeof(float), cudaMemcpyDeviceToHost));
-  std::vector<__half> dp((size_t)d->NP * kKDc, __float2half(0.f));
-  std::vector<float> w2(d->NP / 2, 0.f);
-  for (int k = 0; k < K; ++k) {
-    double m = 0.0;
-    for (int i = 0; i < r; ++i) {
-      float2& v = dc[(size_t)k * r + i];
-      v.y = -v.y;   // Dc = conj(conj(D) d^T)
-      m = std::max(m, (double)std::max(std::fabs(v.x), std::fabs(v.y)));
-    }
-    if (!(m > 0.0) || !(n2inv[k] > 0.f)) continue;
-    w2[k] = (float)(m * m * (double)n2inv[k]);
-    const double im = 1.0 / m;
-    __half* r0 = &dp[(size_t)(2 * k) * kKDc];
-    __half* r1 = r0 + kKDc;
-    for (int i = 0; i < r; ++i) {
-      const float2 v = dc[(size_t)k * r + i];
-      r0[2 * i] = __float2half((float)(v.x * im));
-      r0[2 * i + 1] = __float2half((float)(v.y * im));
-      r1[2 * i] = __float2half((float)(-v.y * im));
-      r1[2 * i + 1] = __float2half((float)(v.x * im));
-    }
+  // Mf^* [r][RF]: conj(Mf[i][f]) = sum_l conj(d_il) phi_fl
+  llr::k_cgemm<<<grid(r, dm::RF), blk>>>(d->basis, L, 1, 1, d->phi, 1, L, r, dm::RF, L, nullptr, d->Mf);
+  MRF_TRY(check_launch("k_cgemm"));
+  // Gd [r][r]: Gd[i][j] = sum_l conj(d_il) d_jl = <d_i, d_j>
+  llr::k_cgemm<<<grid(r, r), blk>>>(d->basis, L, 1, 1, d->basis, 1, L, r, r, L, nullptr, d->Gd);
+  MRF_TRY(check_launch("k_cgemm"));
+  for (double2* p : {d->Dc, d->Mf}) {
+    const size_t n = p == d->Dc ? (size_t)K * r : (size_t)r * dm::RF;
+    std::vector<double2> h(n);
+    CUDA_TRY(cudaMemcpy(h.data(), p, n * sizeof(double2), cudaMemcpyDeviceToHost));
+    for (auto& v : h) v.y = -v.y;
+    CUDA_TRY(cudaMemcpy(p, h.data(), n * sizeof(double2), cudaMemcpyHostToDevice));
   }
-  CUDA_TRY(cudaMemcpy(d->Dc, dc.data(), dc.size() * sizeof(float2), cudaMemcpyHostToDevice));
-  CUDA_TRY(cudaMemcpy(d->dpc, dp.data(), dp.size() * sizeof(__half), cudaMemcpyHostToDevice));
-  CUDA_TRY(cudaMemcpy(d->w2c, w2.data(), w2.size() * sizeof(float), cudaMemcpyHostToDevice));
-  return make_tmap(&d->tmdc, d->dpc, (uint64_t)kKDc, (uint64_t)d->NP, (uint32_t)dm::BN);
+  return MRF_OK;
 }
 
-extern "C" mrf_status mrf_dict_basis(mrf_dict d, double energy, int max_rank, int* rank_out) {
-  if (!d || !rank_out || !(energy > 0.0 && energy <= 1.0) || max_rank < 1 || max_rank > llr::RMAX)
-    return fail(MRF_EINVAL, "mrf_dict_basis: invalid arguments (0 < energy <= 1, 1 <= max_rank <= 32)");
-  if (!(d->fro2 > 0.0)) return fail(MRF_EINVAL, "mrf_dict_basis: all-zero dictionary");
-  CUDA_TRY(cudaSetDevice(d->device));
-  const int K = d->K, L = d->L, k = std::min({max_rank + 16, 64, K, L});
+// Leading right singular vectors of D by subspace iteration on D^H D (GEMMs on the device, double
+// accumulation; the k-column re-orthonormalisation (Gram-Schmidt twice) and the k x k Rayleigh-Ritz
+// eigenproblem in float64 on the host).  rows [k][L]: the Ritz vectors as rows in the convention
+// of the basis d (P_S(x) = x d^H d), by decreasing Ritz value lam.
+static mrf_status top_right_vectors(mrf_dict d, int k, std::vector<std::complex<double>>& rows, std::vector<double>& lam_out) {
+  const int K = d->K, L = d->L;
   float2 *Q = nullptr, *B = nullptr;
   double2* S = nullptr;
   auto cleanup = [&]() {
@@ -327,7 +458,7 @@ extern "C" mrf_status mrf_dict_basis(mrf_dict d, double energy, int max_rank, in
       cudaMalloc((void**)&B, (size_t)K * k * sizeof(float2)) != cudaSuccess ||
       cudaMalloc((void**)&S, (size_t)k * k * sizeof(double2)) != cudaSuccess) {
     cleanup();
-    return fail(MRF_ENOMEM, "mrf_dict_basis: workspace allocation failed");
+    return fail(MRF_ENOMEM, "subspace basis: workspace allocation failed");
   }
   std::vector<float2> q0((size_t)L * k);
   uint64_t st = 0x9E3779B97F4A7C15ull;   // deterministic start block (xorshift)
@@ -373,7 +504,7 @@ extern "C" mrf_status mrf_dict_basis(mrf_dict d, double energy, int max_rank, in
   }
   if (s != MRF_OK) {
     cleanup();
-    return s == MRF_ECUDA ? fail(MRF_ECUDA, "mrf_dict_basis: copy failed") : s;
+    return s == MRF_ECUDA ? fail(MRF_ECUDA, "subspace basis: copy failed") : s;
   }
   // Rayleigh-Ritz: T = (D Q)^H (D Q) = W diag(lam) W^H
   llr::k_cgemm<<<grid(K, k), blk>>>(d->atoms, L, 1, 0, Q, k, 1, K, k, L, B, nullptr);
@@ -381,7 +512,7 @@ extern "C" mrf_status mrf_dict_basis(mrf_dict d, double energy, int max_rank, in
   cudaError_t e = cudaMemcpy(Sh.data(), S, Sh.size() * sizeof(double2), cudaMemcpyDeviceToHost);
   if (e == cudaSuccess) e = cudaMemcpy(Qh.data(), Q, Qh.size() * sizeof(float2), cudaMemcpyDeviceToHost);
   cleanup();
-  if (e != cudaSuccess) return fail(MRF_ECUDA, std::string("mrf_dict_basis: ") + cudaGetErrorString(e));
+  if (e != cudaSuccess) return fail(MRF_ECUDA, std::string("subspace basis: ") + cudaGetErrorString(e));
   std::vector<std::complex<double>> T((size_t)k * k), Wv;
   for (size_t i = 0; i < T.size(); ++i) T[i] = std::complex<double>(Sh[i].x, Sh[i].y);
   std::vector<double> lam;
@@ -389,17 +520,37 @@ extern "C" mrf_status mrf_dict_basis(mrf_dict d, double energy, int max_rank, in
   std::vector<int> ord(k);
   for (int i = 0; i < k; ++i) ord[i] = i;
   std::sort(ord.begin(), ord.end(), [&](int a, int b) { return lam[a] > lam[b]; });
-  int r = 0;
-  double acc = 0.0;
-  while (r < std::min(max_rank, k) && acc < energy * d->fro2) acc += lam[ord[r++]];
-  // basis rows d_i = conj(Q w_i)^T  (right singular vectors as rows, P_S(x) = x d^H d)
-  d->basis_h.assign((size_t)r * L, make_float2(0.f, 0.f));
-  for (int i = 0; i < r; ++i)
+  rows.assign((size_t)k * L, 0.0);
+  lam_out.resize(k);
+  for (int i = 0; i < k; ++i) {
+    lam_out[i] = lam[ord[i]];
     for (int l = 0; l < L; ++l) {
       std::complex<double> v = 0.0;
       for (int j = 0; j < k; ++j)
         v += std::complex<double>(Qh[(size_t)l * k + j].x, Qh[(size_t)l * k + j].y) * Wv[(size_t)j * k + ord[i]];
-      d->basis_h[(size_t)i * L + l] = make_float2((float)v.real(), (float)-v.imag());
+      rows[(size_t)i * L + l] = std::conj(v);   // basis rows d_i = conj(Q w_i)^T
+    }
+  }
+  return MRF_OK;
+}
+
+extern "C" mrf_status mrf_dict_basis(mrf_dict d, double energy, int max_rank, int* rank_out) {
+  if (!d || !rank_out || !(energy > 0.0 && energy <= 1.0) || max_rank < 1 || max_rank > llr::RMAX)
+    return fail(MRF_EINVAL, "mrf_dict_basis: invalid arguments (0 < energy <= 1, 1 <= max_rank <= 32)");
+  if (!(d->fro2 > 0.0)) return fail(MRF_EINVAL, "mrf_dict_basis: all-zero dictionary");
+  CUDA_TRY(cudaSetDevice(d->device));
+  const int K = d->K, L = d->L, k = std::min({max_rank + 16, 64, K, L});
+  std::vector<std::complex<double>> rows;
+  std::vector<double> lam;
+  MRF_TRY(top_right_vectors(d, k, rows, lam));
+  int r = 0;
+  double acc = 0.0;
+  while (r < std::min(max_rank, k) && acc < energy * d->fro2) acc += lam[r++];
+  d->basis_h.assign((size_t)r * L, make_float2(0.f, 0.f));
+  for (int i = 0; i < r; ++i)
+    for (int l = 0; l < L; ++l) {
+      const std::complex<double> v = rows[(size_t)i * L + l];
+      d->basis_h[(size_t)i * L + l] = make_float2((float)v.real(), (float)v.imag());
     }
   if (d->basis) cudaFree(d->basis);
   d->basis = nullptr;
@@ -416,7 +567,9 @@ extern "C" mrf_status mrf_dict_basis(mrf_dict d, double energy, int max_rank, in
   return MRF_OK;
 }
 
-extern "C" mrf_status mrf_dict_basis_copy(mrf_dict d, void* out) {
+extern "C" {
+
+mrf_status mrf_dict_basis_copy(mrf_dict d, void* out) {
   if (!d || !out) return fail(MRF_EINVAL, "mrf_dict_basis_copy: null argument");
   if (!d->rank) return fail(MRF_EINVAL, "mrf_dict_basis_copy: no basis (call mrf_dict_basis)");
   std::memcpy(out, d->basis_h.data(), d->basis_h.size() * sizeof(float2));

@@ -11,30 +11,47 @@
 
 struct mrf_dict_s {
   int K = 0, L = 0, P = 0, device = 0;
-  int KD = 0, NP = 0;            // fp16 row length (2 L padded to 64), GEMM rows (2 K padded to 256)
-  __half* dp = nullptr;          // [NP][KD] atom rows (re/im rotated, scaled by 1 / m_k)
-  float* w2 = nullptr;           // [NP / 2] (m_k / ||d_k||)^2, 0 for padding
-  float* n2inv = nullptr;        // [K] 1 / ||d_k||^2 (0 for a zero atom)
-  float2* atoms = nullptr;       // [K][L] complex64 (for the exact pd)
+  int NP = 0;                    // GEMM rows (2 K padded to 256)
+  float2* atoms = nullptr;       // [K][L] complex64 (the exact rescoring)
+  double* dn2 = nullptr;         // [K] ||d_k||^2 (float64)
   float* lut = nullptr;          // [K][P]
-  __half* xp = nullptr;          // workspace [vcap][KD]
+  // certified filter of Phi_D (match.cuh): Rf <= 64 orthonormal rows phi of the dictionary's
+  // leading right singular vectors, the atoms' coefficients a_k = phi d_k packed as fp16
+  // [a_hi | a_hi | a_lo] rows, the filter weights (m_k / ||d_k||)^2 and the error bound beta
+  int Rf = 0;
+  float2* phi = nullptr;         // [64][L] (rows past Rf zero)
+  float2* phiT = nullptr;        // [L][64]
+  __half* dpf = nullptr;         // [NP][KF]
+  float* w2f = nullptr;          // [NP / 2]
+  CUtensorMap tmdf;
+  double beta = 0.0;             // |rho~_k - rho_k| <= beta for every atom and voxel
+  double beta_res = 0.0, beta_a1 = 0.0;   // max ||r_k|| / ||d_k||, max ||a_k||_1 / ||d_k|| (diagnostics)
+  // per-voxel workspaces (grown on demand)
+  __half* xp = nullptr;          // [vcap][KF] packed filter coefficients
   float* xs = nullptr;           // [vcap] per-voxel scale
-  unsigned long long* best = nullptr;   // [vcap] packed (score, ~atom) running maxima
+  double* xnorm = nullptr;       // [vcap] ||x_v||
+  unsigned long long* best = nullptr;   // [vcap] packed (score, ~atom) maxima of the filter pass
+  float* thr = nullptr;          // [vcap] certified-band threshold
+  int* ncand = nullptr;          // [vcap]
+  int* cand = nullptr;           // [vcap][kCand]
+  int* ov = nullptr;             // [vcap] voxels rescored against every atom
+  int* nov = nullptr;            // [1]
   long long vcap = 0;
-  CUtensorMap tmd;
-  bool prof = false;             // CUDA events around the tensor-core GEMM (mrf_dict_profile)
+  float2* xT = nullptr;          // [vtcap][L] voxel-major frames (frame-domain match)
+  long long vtcap = 0;
+  bool prof = false;             // CUDA events around the tensor-core GEMMs (mrf_dict_profile)
   std::vector<cudaEvent_t> ev;   // pairs
   size_t ev_used = 0;
   double fro2 = 0.0;             // ||D||_F^2 (float64, at creation)
   int rank = 0;                  // subspace basis (mrf_dict_basis): r rows of length L
-  unsigned basis_gen = 0;        // incremented by every mrf_dict_basis
+  unsigned basis_gen = 0;        // process-wide generation of the basis (mrf_dict_basis)
   float2* basis = nullptr;       // device [rank][L]
   std::vector<float2> basis_h;   // host copy
-  // the dictionary in basis coordinates, Dc = D d^dagger [K][rank] (mrf_dict_match_coef): packed
-  // fp16 rows like dp (row length 64 >= 2 rank) and w2c = (m'_k / ||d_k||)^2 with the FULL atom
-  // norms, so that scores and pd equal those of the frame-domain match for x in span(d)
-  __half* dpc = nullptr;         // [NP][64]
-  float* w2c = nullptr;          // [NP / 2]
-  float2* Dc = nullptr;          // [K][rank]
-  CUtensorMap tmdc;
+  // the match in basis coordinates (mrf_dict_match_coef, x = sum_i w_i d_i): Mf = phi d_i
+  // [rank][64], Gd = d d^H [rank][rank] and Dc [K][rank] = <d_i, d_k>, all float64
+  double2* Mf = nullptr;
+  double2* Gd = nullptr;
+  double2* Dc = nullptr;
+  // last match: voxels rescored against every atom (diagnostics)
+  int last_overflow = 0;
 };

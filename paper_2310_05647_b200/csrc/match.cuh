@@ -1,23 +1,26 @@
-// match.cuh -- dictionary matching Phi_D (Eq. (5)) on the
-// sm_100a tensor cores.
+// match.cuh -- exact dictionary matching Phi_D (Eq. (5)) on
+// the sm_100a tensor cores with a certified filter and exact float64 rescoring.
 //
 //   k_v = argmax_k |<d_k, x_v>| / ||d_k||          (reading 21; ties -> lowest k)
 //   rho_v = max(Re<d_k, x_v> / ||d_k||^2, 0),  eta_v = LUT[k_v]
 //
-// The correlations of all voxels with all atoms are one complex GEMM, done as a real fp16 GEMM
-// with fp32 accumulation: voxel row v = (xr_0, xi_0, xr_1, xi_1, ...) / s_v, atom rows
-// 2k = (dr_l, di_l) / m_k and 2k+1 = (-di_l, dr_l) / m_k, so output columns (2k, 2k+1) are
-// (Re, Im) <d_k, x_v> / (s_v m_k).  s_v (per voxel) and m_k (per atom) are max-abs scales that
-// keep the fp16 operands in [-1, 1]; the argmax uses |c~|^2 * (m_k / ||d_k||)^2 (s_v is common
-// to a voxel's row).  rho is recomputed exactly in fp32 for the chosen atom (k_dict_fix).
-//
-// k_dict_gemm: persistent CTAs over (128-voxel, 128-atom) units, 384 threads in roles: warp 0 = TMA producer (128-byte
-// swizzled tiles, 4-stage mbarrier ring), warp 1 = TMEM allocator + single-thread tcgen05.mma
-// issuer (M = 128, N = 256, K = 16 per instruction, fp32 accumulators in TMEM, two 256-column
-// accumulator buffers so the epilogue of one atom tile overlaps the MMAs of the next), warps
-// 4..11 = epilogue in two groups of 4 warps, one per half of the atom tile (tcgen05.ld, one voxel
-// per thread = TMEM lane, running argmax in registers) -- with the 13 basis coefficients (K = 64)
-// the MMAs are short and the epilogue sets the pace.
+// 1. Filter basis Phi (Rf <= 64 orthonormal rows, the dictionary's leading right singular vectors,
+//    fp32): u_v = Phi x_v, a_k = Phi d_k.  For any x the identity
+//        <d_k, x> = <a_k, u> + <r_k, x>,   r_k = (I - Phi^H Phi) d_k   (Phi^H Phi Hermitian)
+//    holds exactly, and |<r_k, x>| <= ||r_k|| ||x|| (float64 residual norms per atom, plan time).
+// 2. k_dict_proj_*: u_v with fp32 FMAs in 16-frame chunks summed in float64 (error <= 32 u_32 per
+//    chunk, Sum_l |phi||x| <= ||x||), ||x_v|| in float64, and the rows [u_hi | u_lo | u_hi] / s_v
+//    (fp16 hi/lo split of u / s_v, s_v = max-abs of u): K = 3 x 128.
+// 3. k_dict_gemm: the 3xFP16 correlation GEMM [u_hi|u_lo|u_hi] . [a_hi|a_hi|a_lo]^T on tcgen05
+//    (fp32 accumulation) -- pass EPI = 0 keeps the best filter score per voxel (64-bit atomicMax),
+//    pass EPI = 1 lists every atom whose filter score lies within the certified band 2 beta of it.
+//    beta bounds |rho~_k - rho_k| of the normalised correlation rho = |<d,x>| / (||d|| ||x||):
+//    residual + projection rounding + split-operand rounding + worst-case fp32 accumulation
+//    (dict.cu filter_beta), so the true argmax is always listed.
+// 4. k_dict_rescore_*: exact scores of the listed atoms, fp32 products summed in float64 (frames:
+//    from the voxel-major copy x^T; coefficients: from the float64 Dc = <d_i, d_k>), argmax with
+//    ties to the lowest index, pd and LUT.  A voxel whose list overflows (or an all-atoms band) is
+//    rescored against every atom (k_dict_exact_*), so the result never depends on the filter.
 #pragma once
 #include <cuda.h>
 #include <cuda_fp16.h>
@@ -59,11 +62,14 @@ __device__ __forceinline__ void mma_f16(uint32_t tmem_d, uint64_t a, uint64_t b,
 // w2[k] = (m_k / ||d_k||)^2 (0 for padding atoms).  X~ [Vpad][KD] and D~ [NP][KD] fp16 are read
 // through the tensor maps; m_tiles = Vpad / BM, n_tiles = NP / BN, kblocks = KD / BK.  The
 // grid is persistent (one CTA per SM), so the m_tiles x n_tiles units quantise to < 1 %.
-template <int NG>
+constexpr int kCand = 32;   // listed candidates per voxel (more: the voxel is rescored against every atom)
+
+template <int NG, int EPI>
 __global__ void __launch_bounds__(threads<NG>(), 1)
 k_dict_gemm(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmd,
             const float* __restrict__ w2, int m_tiles, int n_tiles, int kblocks, int V,
-            unsigned long long* __restrict__ best) {
+            unsigned long long* __restrict__ best, const float* __restrict__ thr, int* __restrict__ ncand,
+            int* __restrict__ cand) {
   extern __shared__ __align__(128) unsigned char dm_raw[];   // aligned to 1024 below (SMEM has the slack)
   unsigned char* base = (unsigned char*)(((uintptr_t)dm_raw + 1023) & ~(uintptr_t)1023);
   unsigned char* sA = base;
@@ -144,6 +150,7 @@ k_dict_gemm(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUt
     for (int u = blockIdx.x; u < units; u += gridDim.x, ++j) {
       const int m0 = (u / n_tiles) * BM, nt = u % n_tiles;
       const int acc = j & 1, use = j >> 1;
+      const float th = (EPI == 1 && m0 + row < V) ? __ldg(thr + m0 + row) : INFINITY;
       bar_wait(&tfull[acc], use & 1);
       __syncwarp();   // tcgen05.ld is .sync.aligned
       tc_fence_after();
@@ -160,16 +167,22 @@ k_dict_gemm(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUt
         const int k0 = nt * (BN / 2) + col / 2;
 #pragma unroll
         for (int q = 0; q < CW / 2; ++q) {
-          const float sc = (v[2 * q] * v[2 * q] + v[2 * q + 1] * v[2 * q + 1]) * __ldg(w2 + k0 + q);
-          if (sc > bsc) {   // strict: equal scores keep the lowest atom index
-            bsc = sc;
-            bk = k0 + q;
+          const float wq = __ldg(w2 + k0 + q);
+          const float sc = (v[2 * q] * v[2 * q] + v[2 * q + 1] * v[2 * q + 1]) * wq;
+          if (EPI == 0) {
+            if (sc > bsc) {   // strict: equal scores keep the lowest atom index
+              bsc = sc;
+              bk = k0 + q;
+            }
+          } else if (sc >= th && wq > 0.f) {   // inside the certified band (zero / padding atoms never)
+            const int slot = atomicAdd(ncand + m0 + row, 1);
+            if (slot < kCand) cand[(size_t)(m0 + row) * kCand + slot] = k0 + q;
           }
         }
       }
       tc_fence_before();
       bar_arrive(&tempty[acc]);
-      if (m0 + row < V)
+      if (EPI == 0 && m0 + row < V)
         atomicMax(best + m0 + row,
                   ((unsigned long long)__float_as_uint(fmaxf(bsc, 0.f)) << 32) | (0xFFFFFFFFu - (uint32_t)bk));
     }
@@ -183,156 +196,376 @@ k_dict_gemm(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUt
   }
 }
 
-// X [L][V] complex64 (frame-major image stack) -> X~ [Vpad][KD] fp16, row v = interleaved
-// (Re, Im) x_v / s_v, zero-padded to KD; s[v] = max_l max(|Re|, |Im|) (1 if the voxel is zero).
-// Block = 32 voxels x 8 row-groups; two passes over the voxels' time series.
-__global__ void __launch_bounds__(256) k_dict_pack_x(const float2* __restrict__ x, int L, int V, int KD,
-                                                     __half* __restrict__ xp, float* __restrict__ s) {
-  __shared__ float red[8][33];
-  __shared__ __half2 tile[32][65];
-  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
-  const int v = blockIdx.x * 32 + tx;
-  float m = 0.f;
-  if (v < V) {
-#pragma unroll 8
-    for (int l = ty; l < L; l += 8) {
-      const float2 a = __ldg(x + (size_t)l * V + v);
-      m = fmaxf(m, fmaxf(fabsf(a.x), fabsf(a.y)));
-    }
-  }
-  red[ty][tx] = m;
-  __syncthreads();
-  if (ty == 0) {
-    float mm = 0.f;
-    for (int i = 0; i < 8; ++i) mm = fmaxf(mm, red[i][tx]);
-    red[0][tx] = mm > 0.f ? mm : 1.f;
-    if (v < V) s[v] = red[0][tx];
-  }
-  __syncthreads();
-  const float inv = 1.f / red[0][tx];
-  const int L2 = KD / 2;   // complex slots per padded row
-  for (int l0 = 0; l0 < L2; l0 += 64) {
-    // load 64 frames x 32 voxels (coalesced over voxels, 8 loads in flight per thread),
-    // transpose through shared memory
-    float2 a[8];
+
+// ------------------------------------------------------------------------------ projections
+constexpr int RF = 64;          // filter basis rows (padded)
+constexpr int KF = 3 * 2 * RF;  // fp16 row length [u_hi | u_lo | u_hi] = 384
+
+// split v (already divided by the scale) into fp16 hi + lo: |v - hi - lo| <= u16^2 |v| + 2^-25
+__device__ __forceinline__ void split_h(double v, __half& hi, __half& lo) {
+  hi = __double2half(v);
+  lo = __double2half(v - (double)__half2float(hi));
+}
+
+// Frame domain: x [L][V] complex64 -> u = Phi x (float64 totals of 16-frame fp32 chunks), ||x||
+// (float64), the packed row [V][KF] and scale s_v, and the voxel-major copy xT [V][L].
+// Block = 32 voxels x 8 groups; group g owns filter rows 8g .. 8g+7 (phiT [L][RF] complex, rows
+// past Rf zero); lane = voxel, so phi loads are warp-uniform broadcasts and x loads coalesce.
+__global__ void __launch_bounds__(256) k_dict_proj_frames(const float2* __restrict__ x, const float2* __restrict__ phiT,
+                                                          int L, int V, float2* __restrict__ xT,
+                                                          __half* __restrict__ xp, float* __restrict__ xs,
+                                                          double* __restrict__ xnorm) {
+  __shared__ float2 tile[32][33];   // [frame][voxel] staging of the transpose
+  __shared__ double red[8][32];
+  const int lane = threadIdx.x & 31, g = threadIdx.x >> 5;
+  const int v = blockIdx.x * 32 + lane;
+  const bool ok = v < V;
+  double ur[8], ui[8], nrm = 0.0;
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const int l = l0 + ty + 8 * q;
-      a[q] = (v < V && l < L) ? __ldg(x + (size_t)l * V + v) : make_float2(0.f, 0.f);
-    }
+  for (int i = 0; i < 8; ++i) ur[i] = ui[i] = 0.0;
+  for (int l0 = 0; l0 < L; l0 += 32) {
+    // transpose tile: warp g loads frames l0 + g + 8q for the 32 voxels (coalesced over voxels)
 #pragma unroll
-    for (int q = 0; q < 8; ++q) tile[tx][ty + 8 * q] = __floats2half2_rn(a[q].x * inv, a[q].y * inv);
-    __syncthreads();
-#pragma unroll
-    for (int i = ty; i < 32; i += 8) {   // voxel blockIdx*32 + i, frames l0 + tx and l0 + 32 + tx
-      const int vv = blockIdx.x * 32 + i;
-      __half2* row = reinterpret_cast<__half2*>(xp + (size_t)vv * KD);
-      if (l0 + tx < L2) row[l0 + tx] = tile[i][tx];
-      if (l0 + 32 + tx < L2) row[l0 + 32 + tx] = tile[i][32 + tx];
+    for (int q = 0; q < 4; ++q) {
+      const int l = l0 + g + 8 * q;
+      tile[g + 8 * q][lane] = (ok && l < L) ? __ldg(x + (size_t)l * V + v) : make_float2(0.f, 0.f);
     }
     __syncthreads();
+    // 16-frame fp32 chunks of this group's 8 coefficients, summed into float64
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      float cr[8], ci[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) cr[i] = ci[i] = 0.f;
+      for (int ll = 16 * h; ll < 16 * h + 16 && l0 + ll < L; ++ll) {
+        const float2 xv = tile[ll][lane];
+        if (g == 0) nrm += (double)xv.x * xv.x + (double)xv.y * xv.y;
+        const float4* pr = reinterpret_cast<const float4*>(phiT + (size_t)(l0 + ll) * RF + 8 * g);
+#pragma unroll
+        for (int i2 = 0; i2 < 4; ++i2) {
+          const float4 p = __ldg(pr + i2);   // phi_{8g+2i2}, phi_{8g+2i2+1}; u += conj(phi) x
+          cr[2 * i2] = fmaf(p.x, xv.x, fmaf(p.y, xv.y, cr[2 * i2]));
+          ci[2 * i2] = fmaf(p.x, xv.y, fmaf(-p.y, xv.x, ci[2 * i2]));
+          cr[2 * i2 + 1] = fmaf(p.z, xv.x, fmaf(p.w, xv.y, cr[2 * i2 + 1]));
+          ci[2 * i2 + 1] = fmaf(p.z, xv.y, fmaf(-p.w, xv.x, ci[2 * i2 + 1]));
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i) { ur[i] += (double)cr[i]; ui[i] += (double)ci[i]; }
+    }
+    // voxel-major copy: warp g writes voxels 4g .. 4g+3, 32 frames each (256 contiguous bytes)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int vv = blockIdx.x * 32 + 4 * g + q;
+      if (vv < V && l0 + lane < L) xT[(size_t)vv * L + l0 + lane] = tile[lane][4 * g + q];
+    }
+    __syncthreads();
+  }
+  // s_v = max-abs over the Rf complex coefficients (the rows past Rf are exactly zero)
+  double m = 0.0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) m = fmax(m, fmax(fabs(ur[i]), fabs(ui[i])));
+  red[g][lane] = m;
+  __syncthreads();
+  double s = 0.0;
+  for (int i = 0; i < 8; ++i) s = fmax(s, red[i][lane]);
+  if (!(s > 0.0)) s = 1.0;
+  if (!ok) return;
+  if (g == 0) {
+    xs[v] = (float)s;
+    xnorm[v] = sqrt(nrm);
+  }
+  const float sf = (float)s;   // the scale the GEMM epilogue sees
+  __half* row = xp + (size_t)v * KF;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int c = 2 * (8 * g + i);
+    __half hr, lr, hi, li;
+    split_h(ur[i] / (double)sf, hr, lr);
+    split_h(ui[i] / (double)sf, hi, li);
+    row[c] = hr; row[c + 1] = hi;                       // [u_hi
+    row[2 * RF + c] = lr; row[2 * RF + c + 1] = li;     //  | u_lo
+    row[4 * RF + c] = hr; row[4 * RF + c + 1] = hi;     //  | u_hi]
   }
 }
 
-// rho and LUT lookup for the chosen atoms: Re<d_k, x_v> in fp32 from the complex64 data.  A
-// CTA takes 32 voxels; 32-frame tiles of x ([l][v], coalesced over v) and of the 32 chosen atoms
-// ([v][l], coalesced over l) are staged in shared memory; warp w sums voxels 4w..4w+3 with one
-// frame per lane and a final shuffle reduction.
-__global__ void __launch_bounds__(256) k_dict_fix(const float2* __restrict__ x, const float2* __restrict__ atoms,
-                                                  const float* __restrict__ n2inv, const float* __restrict__ lut, int P,
-                                                  int L, int V, const unsigned long long* __restrict__ best,
-                                                  int* __restrict__ index,
-                                                  float* __restrict__ pd, float* __restrict__ params) {
-  __shared__ float2 xt[64][33];   // [l][v]
-  __shared__ float2 dt[32][65];   // [v][l]
-  __shared__ int ks[32];
-  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
-  const int v0 = blockIdx.x * 32;
-  if (threadIdx.x < 32) ks[tx] = v0 + tx < V ? (int)(0xFFFFFFFFu - (uint32_t)(best[v0 + tx] & 0xFFFFFFFFull)) : 0;
-  __syncthreads();
-  float acc[4] = {0.f, 0.f, 0.f, 0.f};
-  for (int l0 = 0; l0 < L; l0 += 64) {   // 64 frames per step, 16 loads in flight per thread
-#pragma unroll
-    for (int i = ty; i < 64; i += 8) {
-      const int l = l0 + i, v = v0 + tx;
-      xt[i][tx] = (l < L && v < V) ? __ldg(x + (size_t)l * V + v) : make_float2(0.f, 0.f);
-    }
-#pragma unroll
-    for (int i = ty; i < 32; i += 8) {
-      const float2* dr = atoms + (size_t)ks[i] * L + l0;
-      dt[i][tx] = (l0 + tx < L) ? __ldg(dr + tx) : make_float2(0.f, 0.f);
-      dt[i][32 + tx] = (l0 + 32 + tx < L) ? __ldg(dr + 32 + tx) : make_float2(0.f, 0.f);
-    }
-    __syncthreads();
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {   // Re(conj(d) x) = dr xr + di xi, frames l0 + tx and l0 + 32 + tx
-      const int j = ty * 4 + q;
-      const float2 d0 = dt[j][tx], x0 = xt[tx][j], d1 = dt[j][32 + tx], x1 = xt[32 + tx][j];
-      acc[q] = fmaf(d0.x, x0.x, fmaf(d0.y, x0.y, acc[q]));
-      acc[q] = fmaf(d1.x, x1.x, fmaf(d1.y, x1.y, acc[q]));
-    }
-    __syncthreads();
+// Basis coordinates: x = sum_i w_i d_i (w [r][V], the LLR basis d [r][L]) -> u = Phi x = sum_i w_i Mf_i
+// with Mf [r][RF] = Phi d_i (float64), ||x||^2 = w^H Gd w (Gd = d d^H, float64); one thread per voxel.
+__device__ __forceinline__ double2 proj_coef_f(const float2 (&wv)[32], int r, const double2* __restrict__ Mf, int f) {
+  double sr = 0.0, si = 0.0;
+  for (int i = 0; i < r; ++i) {
+    const double2 mm = __ldg(Mf + i * RF + f);
+    sr += (double)wv[i].x * mm.x - (double)wv[i].y * mm.y;
+    si += (double)wv[i].x * mm.y + (double)wv[i].y * mm.x;
   }
-#pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    float r = acc[q];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
-    const int v = v0 + ty * 4 + q;
-    if (tx == 0 && v < V) {
-      const int k = ks[ty * 4 + q];
-      index[v] = k;
-      pd[v] = fmaxf(r * __ldg(n2inv + k), 0.f);
-    }
-    if (params && v < V)
-      for (int c = tx; c < P; c += 32) params[(size_t)v * P + c] = __ldg(lut + (size_t)ks[ty * 4 + q] * P + c);
-  }
+  return make_double2(sr, si);
 }
 
-// Short time series (L <= 32: the basis-coordinate match, K = 64): one thread per voxel.
-// Pack: x [L][V] -> X~ [Vpad][KD] fp16 row v = (Re, Im) x_v / s_v, zero-padded; s_v = max |Re|, |Im|.
-__global__ void __launch_bounds__(256) k_dict_pack_short(const float2* __restrict__ x, int L, int V, int Vpad, int KD,
-                                                         __half* __restrict__ xp, float* __restrict__ s) {
-  const int v = blockIdx.x * blockDim.x + threadIdx.x;
-  if (v >= Vpad) return;
-  float2 a[32];
-  float m = 0.f;
-#pragma unroll
-  for (int l = 0; l < 32; ++l) {
-    a[l] = (l < L && v < V) ? __ldg(x + (size_t)l * V + v) : make_float2(0.f, 0.f);
-    m = fmaxf(m, fmaxf(fabsf(a[l].x), fabsf(a[l].y)));
-  }
-  const float sc = m > 0.f ? m : 1.f, inv = 1.f / sc;
-  if (v < V) s[v] = sc;
-  uint4* row = reinterpret_cast<uint4*>(xp + (size_t)v * KD);
-#pragma unroll
-  for (int q = 0; q < 8; ++q) {   // 8 x 16 bytes = 64 halves = 32 complex slots (KD == 64)
-    __half2 h[4];
-#pragma unroll
-    for (int t = 0; t < 4; ++t) h[t] = __floats2half2_rn(a[4 * q + t].x * inv, a[4 * q + t].y * inv);
-    row[q] = *reinterpret_cast<uint4*>(h);
-  }
-}
-
-// rho and LUT lookup for the chosen atoms, one thread per voxel (L <= 32): Re<d_k, x_v> in fp32.
-__global__ void __launch_bounds__(256) k_dict_fix_short(const float2* __restrict__ x, const float2* __restrict__ atoms,
-                                                        const float* __restrict__ n2inv, const float* __restrict__ lut,
-                                                        int P, int L, int V, const unsigned long long* __restrict__ best,
-                                                        int* __restrict__ index, float* __restrict__ pd,
-                                                        float* __restrict__ params) {
+__global__ void __launch_bounds__(128) k_dict_proj_coef(const float2* __restrict__ w, int r, int V,
+                                                        const double2* __restrict__ Mf, const double2* __restrict__ Gd,
+                                                        __half* __restrict__ xp, float* __restrict__ xs,
+                                                        double* __restrict__ xnorm) {
   const int v = blockIdx.x * blockDim.x + threadIdx.x;
   if (v >= V) return;
-  const int k = (int)(0xFFFFFFFFu - (uint32_t)(best[v] & 0xFFFFFFFFull));
-  const float2* d = atoms + (size_t)k * L;
-  float acc = 0.f;
-  for (int l = 0; l < L; ++l) {
-    const float2 dv = __ldg(d + l), xv = __ldg(x + (size_t)l * V + v);
-    acc = fmaf(dv.x, xv.x, fmaf(dv.y, xv.y, acc));
+  float2 wv[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) wv[i] = i < r ? __ldg(w + (size_t)i * V + v) : make_float2(0.f, 0.f);
+  double n2 = 0.0;
+  for (int i = 0; i < r; ++i)
+    for (int j = 0; j < r; ++j) {   // conj(w_i) Gd_ij w_j
+      const double2 gq = __ldg(Gd + i * r + j);
+      const double ar = (double)wv[i].x, ai = -(double)wv[i].y, br = wv[j].x, bi = wv[j].y;
+      const double pr = ar * br - ai * bi, pi = ar * bi + ai * br;
+      n2 += pr * gq.x - pi * gq.y;
+    }
+  double m = 0.0;   // pass 1: the scale; pass 2: the packed row (recomputed: no 128-double array)
+  for (int f = 0; f < RF; ++f) {
+    const double2 u = proj_coef_f(wv, r, Mf, f);
+    m = fmax(m, fmax(fabs(u.x), fabs(u.y)));
   }
-  index[v] = k;
-  pd[v] = fmaxf(acc * __ldg(n2inv + k), 0.f);
+  if (!(m > 0.0)) m = 1.0;
+  const float sf = (float)m;
+  xs[v] = sf;
+  xnorm[v] = sqrt(fmax(n2, 0.0));
+  __half* row = xp + (size_t)v * KF;
+  for (int f = 0; f < RF; ++f) {
+    const double2 u = proj_coef_f(wv, r, Mf, f);
+    __half hr, lr, hi, li;
+    split_h(u.x / (double)sf, hr, lr);
+    split_h(u.y / (double)sf, hi, li);
+    row[2 * f] = hr; row[2 * f + 1] = hi;
+    row[2 * RF + 2 * f] = lr; row[2 * RF + 2 * f + 1] = li;
+    row[4 * RF + 2 * f] = hr; row[4 * RF + 2 * f + 1] = hi;
+  }
+}
+
+// Certified band: thr_v = (max(0, sqrt(best_v) - 2 beta ||x_v|| / s_v))^2 on the filter score
+// scale (sqrt(score) = rho~ ||x|| / s_v); +inf for a zero voxel (every atom scores 0: index 0).
+__global__ void k_dict_thr(const unsigned long long* __restrict__ best, const double* __restrict__ xnorm,
+                           const float* __restrict__ xs, double beta, int V, float* __restrict__ thr,
+                           int* __restrict__ ncand) {
+  const int v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= V) return;
+  ncand[v] = 0;
+  if (!(xnorm[v] > 0.0)) {
+    thr[v] = INFINITY;
+    return;
+  }
+  const double sb = sqrt((double)__uint_as_float((uint32_t)(best[v] >> 32)));
+  const double t = sb - 2.0 * beta * xnorm[v] / (double)xs[v];
+  // rounded down so that the fp32 comparison in the epilogue can only admit more atoms
+  thr[v] = t > 0.0 ? __double2float_rd(t * t * (1.0 - 1e-6)) : 0.f;
+}
+
+// ------------------------------------------------------------------------------ exact rescoring
+struct Best {
+  double s;      // |c|^2 / ||d||^2
+  int k;
+  double cre;    // Re c of the best atom
+};
+__device__ __forceinline__ void best_update(Best& b, double s, int k, double cre) {
+  if (s > b.s || (s == b.s && k < b.k)) { b.s = s; b.k = k; b.cre = cre; }
+}
+
+__device__ __forceinline__ void finish_voxel(int v, const Best& b, const double* __restrict__ dn2,
+                                             const float* __restrict__ lut, int P, int* __restrict__ index,
+                                             float* __restrict__ pd, float* __restrict__ params) {
+  index[v] = b.k;
+  pd[v] = (float)fmax(b.cre / dn2[b.k], 0.0);
   if (params)
-    for (int c = 0; c < P; ++c) params[(size_t)v * P + c] = __ldg(lut + (size_t)k * P + c);
+    for (int c = 0; c < P; ++c) params[(size_t)v * P + c] = __ldg(lut + (size_t)b.k * P + c);
+}
+
+// exact <d_k, x_v> from the voxel-major frames: one warp, lanes over frames, float64 sums of the
+// (exact) products of fp32 values, fixed-order warp reduction
+__device__ __forceinline__ double2 warp_dot_frames(const float2* __restrict__ dk, const float2* __restrict__ xv, int L,
+                                                   int lane) {
+  double sr = 0.0, si = 0.0;
+  for (int l = lane; l < L; l += 32) {
+    const float2 a = __ldg(dk + l), b = __ldg(xv + l);
+    sr += (double)a.x * b.x + (double)a.y * b.y;
+    si += (double)a.x * b.y - (double)a.y * b.x;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    sr += __shfl_xor_sync(0xffffffffu, sr, o);
+    si += __shfl_xor_sync(0xffffffffu, si, o);
+  }
+  return make_double2(sr, si);
+}
+
+// Frames: one warp per voxel over its listed atoms; a voxel with an overflowing list, or every
+// atom in band, is queued for k_dict_exact_frames (ov / nov).
+__global__ void __launch_bounds__(256) k_dict_rescore_frames(const float2* __restrict__ xT, const float2* __restrict__ atoms,
+                                                             const double* __restrict__ dn2, const double* __restrict__ xnorm,
+                                                             const int* __restrict__ ncand, const int* __restrict__ cand,
+                                                             const float* __restrict__ lut, int P, int L, int V,
+                                                             int* __restrict__ index, float* __restrict__ pd,
+                                                             float* __restrict__ params, int* __restrict__ ov,
+                                                             int* __restrict__ nov) {
+  const int lane = threadIdx.x & 31;
+  const int v = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (v >= V) return;
+  Best b{-1.0, 0, 0.0};
+  if (!(xnorm[v] > 0.0)) {   // zero voxel: every score is 0 -> the lowest index, PD 0
+    b.s = 0.0;
+    if (lane == 0) finish_voxel(v, b, dn2, lut, P, index, pd, params);
+    return;
+  }
+  const int n = ncand[v];
+  if (n > kCand || n == 0) {   // (n == 0 cannot happen: the filter's best atom is always in band)
+    if (lane == 0) ov[atomicAdd(nov, 1)] = v;
+    return;
+  }
+  const float2* xv = xT + (size_t)v * L;
+  for (int i = 0; i < n; ++i) {
+    const int k = cand[(size_t)v * kCand + i];
+    const double2 c = warp_dot_frames(atoms + (size_t)k * L, xv, L, lane);
+    best_update(b, (c.x * c.x + c.y * c.y) / dn2[k], k, c.x);
+  }
+  if (lane == 0) finish_voxel(v, b, dn2, lut, P, index, pd, params);
+}
+
+// every atom, exactly, for the queued voxels (one block per voxel, warps over atoms)
+__global__ void __launch_bounds__(256) k_dict_exact_frames(const float2* __restrict__ xT, const float2* __restrict__ atoms,
+                                                           const double* __restrict__ dn2, int K, const float* __restrict__ lut,
+                                                           int P, int L, const int* __restrict__ ov,
+                                                           const int* __restrict__ nov, int* __restrict__ index,
+                                                           float* __restrict__ pd, float* __restrict__ params) {
+  __shared__ Best wb[8];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int n = *nov;
+  for (int q = blockIdx.x; q < n; q += gridDim.x) {
+    const int v = ov[q];
+    Best b{-1.0, 0, 0.0};
+    for (int k = w; k < K; k += 8) {
+      if (!(dn2[k] > 0.0)) continue;   // an all-zero atom is never matched
+      const double2 c = warp_dot_frames(atoms + (size_t)k * L, xT + (size_t)v * L, L, lane);
+      best_update(b, (c.x * c.x + c.y * c.y) / dn2[k], k, c.x);
+    }
+    if (lane == 0) wb[w] = b;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      Best t = wb[0];
+      for (int i = 1; i < 8; ++i) best_update(t, wb[i].s, wb[i].k, wb[i].cre);
+      finish_voxel(v, t, dn2, lut, P, index, pd, params);
+    }
+    __syncthreads();
+  }
+}
+
+// Basis coordinates: exact <d_k, x> = sum_i w_i conj(Dc[k][i]) (Dc = <d_i, d_k>, float64), one
+// thread per voxel over its listed atoms; overflow queued for k_dict_exact_coef.
+__device__ __forceinline__ double2 dot_coef(const double2* __restrict__ dck, const float2 (&wv)[32], int r) {
+  double sr = 0.0, si = 0.0;
+  for (int i = 0; i < r; ++i) {
+    const double2 d = __ldg(dck + i);
+    sr += wv[i].x * d.x + wv[i].y * d.y;
+    si += wv[i].y * d.x - wv[i].x * d.y;
+  }
+  return make_double2(sr, si);
+}
+
+__global__ void __launch_bounds__(128) k_dict_rescore_coef(const float2* __restrict__ w, int r, const double2* __restrict__ Dc,
+                                                           const double* __restrict__ dn2, const double* __restrict__ xnorm,
+                                                           const int* __restrict__ ncand, const int* __restrict__ cand,
+                                                           const float* __restrict__ lut, int P, int V,
+                                                           int* __restrict__ index, float* __restrict__ pd,
+                                                           float* __restrict__ params, int* __restrict__ ov,
+                                                           int* __restrict__ nov) {
+  const int v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= V) return;
+  Best b{-1.0, 0, 0.0};
+  if (!(xnorm[v] > 0.0)) {
+    b.s = 0.0;
+    finish_voxel(v, b, dn2, lut, P, index, pd, params);
+    return;
+  }
+  const int n = ncand[v];
+  if (n > kCand || n == 0) {
+    ov[atomicAdd(nov, 1)] = v;
+    return;
+  }
+  float2 wv[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) wv[i] = i < r ? __ldg(w + (size_t)i * V + v) : make_float2(0.f, 0.f);
+  for (int i = 0; i < n; ++i) {
+    const int k = cand[(size_t)v * kCand + i];
+    const double2 c = dot_coef(Dc + (size_t)k * r, wv, r);
+    best_update(b, (c.x * c.x + c.y * c.y) / dn2[k], k, c.x);
+  }
+  finish_voxel(v, b, dn2, lut, P, index, pd, params);
+}
+
+__global__ void __launch_bounds__(128) k_dict_exact_coef(const float2* __restrict__ w, int r, const double2* __restrict__ Dc,
+                                                         const double* __restrict__ dn2, int K, const float* __restrict__ lut,
+                                                         int P, int V, const int* __restrict__ ov, const int* __restrict__ nov,
+                                                         int* __restrict__ index, float* __restrict__ pd,
+                                                         float* __restrict__ params) {
+  const int n = *nov;
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < n; q += gridDim.x * blockDim.x) {
+    const int v = ov[q];
+    float2 wv[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) wv[i] = i < r ? __ldg(w + (size_t)i * V + v) : make_float2(0.f, 0.f);
+    Best b{-1.0, 0, 0.0};
+    for (int k = 0; k < K; ++k) {
+      if (!(dn2[k] > 0.0)) continue;
+      const double2 c = dot_coef(Dc + (size_t)k * r, wv, r);
+      best_update(b, (c.x * c.x + c.y * c.y) / dn2[k], k, c.x);
+    }
+    finish_voxel(v, b, dn2, lut, P, index, pd, params);
+  }
+}
+
+// ------------------------------------------------------------------------------ setup (float64)
+// Per atom (one block): a_k = Phi d_k (RF complex, float64 from the fp32 inputs), the residual
+// norm ||d_k - Phi^H a_k||^2 and ||a_k||_1, with phi [RF][L] (rows past Rf zero).
+__global__ void __launch_bounds__(256) k_dict_filter_atoms(const float2* __restrict__ atoms, const float2* __restrict__ phi,
+                                                           int L, double2* __restrict__ a, double* __restrict__ res2,
+                                                           double* __restrict__ a1) {
+  __shared__ double2 sa[RF];
+  __shared__ double red[8];
+  const int k = blockIdx.x, lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const float2* d = atoms + (size_t)k * L;
+  for (int f = w; f < RF; f += 8) {   // warp per filter row
+    double sr = 0.0, si = 0.0;
+    for (int l = lane; l < L; l += 32) {   // conj(phi) d
+      const float2 p = __ldg(phi + (size_t)f * L + l), x = __ldg(d + l);
+      sr += (double)p.x * x.x + (double)p.y * x.y;
+      si += (double)p.x * x.y - (double)p.y * x.x;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      sr += __shfl_xor_sync(0xffffffffu, sr, o);
+      si += __shfl_xor_sync(0xffffffffu, si, o);
+    }
+    if (lane == 0) sa[f] = make_double2(sr, si);
+  }
+  __syncthreads();
+  double r2 = 0.0;
+  for (int l = threadIdx.x; l < L; l += blockDim.x) {   // d_l - sum_f phi_fl a_f
+    const float2 x = __ldg(d + l);
+    double er = x.x, ei = x.y;
+    for (int f = 0; f < RF; ++f) {
+      const float2 p = __ldg(phi + (size_t)f * L + l);
+      er -= (double)p.x * sa[f].x - (double)p.y * sa[f].y;
+      ei -= (double)p.x * sa[f].y + (double)p.y * sa[f].x;
+    }
+    r2 += er * er + ei * ei;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) r2 += __shfl_xor_sync(0xffffffffu, r2, o);
+  if (lane == 0) red[w] = r2;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0, n1 = 0.0;
+    for (int i = 0; i < 8; ++i) t += red[i];
+    for (int f = 0; f < RF; ++f) n1 += sqrt(sa[f].x * sa[f].x + sa[f].y * sa[f].y);
+    res2[k] = t;
+    a1[k] = n1;
+  }
+  if (threadIdx.x < RF) a[(size_t)k * RF + threadIdx.x] = sa[threadIdx.x];
 }
 
 }  // namespace dm

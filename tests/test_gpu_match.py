@@ -1,23 +1,23 @@
-"""GPU parity of dictionary matching Phi_D (tcgen05 kernel) against the float64 oracle.
+"""GPU parity of dictionary matching Phi_D against the float64 oracle: the index must EQUAL the
+oracle's argmax for every checked voxel (Eq. (5), reading 21; ties -> lowest index).
 
-PAPER.md:76-92 Eq. (5), reading 21.  The tensor-core correlations use fp16 operands
-(scaled to [-1, 1]) with fp32 accumulation, so the argmax is compared as SURVEY/the task asks
-for results with several correct answers: the chosen atom must be exactly the oracle's wherever
-the oracle's best and second-best normalised correlations differ by more than TIE_REL, and
-otherwise must score within TIE_REL of the best (a valid near-tie).  pd = max(Re<d_k,x>/||d_k||^2, 0)
-is recomputed in fp32 for the chosen atom and compared with the oracle's value for that atom.
+The GPU path (match.cuh) is a certified tensor-core filter plus exact float64 rescoring of every
+atom inside the filter's error band, with a full exact scan for voxels whose band holds more than
+32 atoms; pd = max(Re<d_k,x>/||d_k||^2, 0) comes from the exact correlation of the chosen atom.
+Inputs: noisy voxel fingerprints (many near-ties: neighbouring atoms correlate to 0.999998) and
+rank-5 phantom time series (the CG solution's kind of voxels), on the paper's 3336-atom grid.
 """
 import numpy as np
 import pytest
 import torch
 
+import synth
 import synth.dictionary as sd
 from oracle import match as om
 
 pytestmark = pytest.mark.gpu
 
-TIE_REL = 2e-4    # fp16 operands, fp32 accumulation: measured deficit of near-tie picks < 2e-5
-PD_RTOL = 1e-4
+PD_RTOL = 1e-5
 
 
 @pytest.fixture(scope="module")
@@ -26,71 +26,103 @@ def binding():
     return b
 
 
-def run(binding, D, lut, X):
-    """X [V][L] complex128 -> GPU match on the frame-major layout [L][V]."""
+def run(binding, D, lut, X, keep=False):
+    """X [V][L] complex -> GPU match on the frame-major layout [L][V] (complex64 values)."""
     dic = binding.Dictionary(D, lut)
     x = torch.from_numpy(np.ascontiguousarray(X.T.astype(np.complex64))).cuda()
     idx, pd, par = dic.match(x)
     torch.cuda.synchronize()
+    ov = dic.overflow()
+    out = (idx.cpu().numpy(), pd.cpu().numpy(), None if par is None else par.cpu().numpy(), ov)
+    if keep:
+        return out + (dic,)
     dic.close()
-    return idx.cpu().numpy(), pd.cpu().numpy(), None if par is None else par.cpu().numpy()
+    return out
 
 
 def check(D, X, lut, idx, pd, par):
+    """Exact parity on the complex64 values the GPU saw."""
+    X = X.astype(np.complex64).astype(np.complex128)
+    D = D.astype(np.complex64).astype(np.complex128)
     k, _, rho, score = om.match(X, D, p=1)
-    V = X.shape[0]
-    s_best = score[np.arange(V), k]
-    s_gpu = score[np.arange(V), idx]
-    srt = np.sort(score, axis=1)
-    gap = (srt[:, -1] - srt[:, -2]) / np.maximum(srt[:, -1], 1e-300)
-    clear = gap > TIE_REL
-    assert np.array_equal(idx[clear], k[clear]), f"{np.sum(idx[clear] != k[clear])} clear-cut voxels differ"
-    deficit = np.max((s_best - s_gpu) / np.maximum(s_best, 1e-300))
-    print(f"clear-cut {clear.mean():.3f}, exact {np.mean(idx == k):.3f}, max relative deficit {deficit:.2e}")
-    assert deficit <= TIE_REL, "a near-tie pick scores below the tolerance"
-    c = om.correlations(X, D)[np.arange(V), idx]
-    n2 = np.sum(np.abs(D) ** 2, axis=1)[idx]
-    rho_pick = np.maximum(c.real / n2, 0.0)
-    assert np.allclose(pd, rho_pick, rtol=PD_RTOL, atol=PD_RTOL * np.abs(rho_pick).max())
+    bad = np.flatnonzero(idx != k)
+    assert bad.size == 0, (f"{bad.size} of {len(k)} voxels differ, e.g. voxel {bad[0]}: gpu {idx[bad[0]]} "
+                           f"oracle {k[bad[0]]}, scores {score[bad[0], idx[bad[0]]]:.17g} {score[bad[0], k[bad[0]]]:.17g}")
+    assert np.allclose(pd, rho, rtol=PD_RTOL, atol=PD_RTOL * max(np.abs(rho).max(), 1e-30))
     if par is not None:
         assert np.array_equal(par, lut[idx].astype(np.float32))
-    return clear.mean()
+    srt = np.sort(score, axis=1)
+    gap = (srt[:, -1] - srt[:, -2]) / np.maximum(srt[:, -1], 1e-300)
+    return float(np.mean(gap < 1e-5))
 
 
 def test_small_ragged(binding):
-    # K, L, V not multiples of the tile sizes (128 atoms, 32 frames, 128 voxels)
+    # K, L, V not multiples of the tile sizes (128 atoms, 64-wide K blocks, 128 voxels)
     g = sd.t1t2_grid()[::11]
     D = sd.surrogate_dictionary(200, g)
     X, k0, _ = sd.voxel_fingerprints(D, 1000, noise=0.01)
-    idx, pd, par = run(binding, D, g, X)
-    frac = check(D, X, g, idx, pd, par)
-    assert frac > 0.2
+    idx, pd, par, ov = run(binding, D, g, X)
+    check(D, X, g, idx, pd, par)
+
+
+def test_short_series_full_rank_filter(binding):
+    # L < 64: the filter spans every frame (residual 0)
+    g = sd.t1t2_grid()[::13]
+    D = sd.surrogate_dictionary(40, g)
+    X, _, _ = sd.voxel_fingerprints(D, 500, noise=0.05)
+    idx, pd, par, ov = run(binding, D, g, X)
+    check(D, X, g, idx, pd, par)
 
 
 def test_edge_voxels(binding):
     g = sd.t1t2_grid()[::29]
     D = sd.surrogate_dictionary(64, g)
-    Dn = D / np.linalg.norm(D, axis=1)[:, None]
-    X = np.stack([np.zeros(64), -3.0 * D[7], 2.5 * D[40], 1e-6 * D[3], 1e4 * D[90]]).astype(np.complex128)
-    idx, pd, par = run(binding, D, g, X)
+    X = np.stack([np.zeros(64), -3.0 * D[7], 2.5 * D[40], 1e-6 * D[3], 1e4 * D[90], D[5] + D[6]]).astype(np.complex128)
+    idx, pd, par, ov = run(binding, D, g, X)
     assert idx[0] == 0 and pd[0] == 0.0            # zero voxel: lowest index, PD 0
     assert idx[1] == 7 and pd[1] == 0.0            # negative atom: PD clamped
-    assert idx[2] == 40 and np.isclose(pd[2], 2.5, rtol=1e-5)
-    assert idx[3] == 3 and np.isclose(pd[3], 1e-6, rtol=1e-4)   # per-voxel scaling: no fp16 underflow
-    assert idx[4] == 90 and np.isclose(pd[4], 1e4, rtol=1e-5)
+    assert idx[2] == 40 and np.isclose(pd[2], 2.5, rtol=1e-6)
+    assert idx[3] == 3 and np.isclose(pd[3], 1e-6, rtol=1e-6)   # per-voxel scaling: no fp16 underflow
+    assert idx[4] == 90 and np.isclose(pd[4], 1e4, rtol=1e-6)
     assert np.array_equal(par, g[idx].astype(np.float32))
-    del Dn
+    check(D, X, g, idx, pd, par)
 
 
-def test_full_dictionary_sampled_voxels(binding):
-    # the bench configuration: 3336 atoms x 1000 frames, 65536 voxels; 256 voxels checked
+def test_duplicate_atoms_tie_to_lowest_index(binding):
+    g = sd.t1t2_grid()[::31]
+    D = sd.surrogate_dictionary(80, g)
+    D[9] = D[4]                                    # an exact tie: the lower index wins
+    X = np.stack([2.0 * D[4], D[9] + 0.01 * D[20]])
+    idx, pd, par, ov = run(binding, D, g, X)
+    assert idx[0] == 4 and idx[1] == 4
+    check(D, X, g, idx, pd, par)
+
+
+def test_full_dictionary_fingerprints_exact(binding):
+    # the bench dictionary: 3336 atoms x 1000 frames, 65536 noisy fingerprints (near-ties)
     g = sd.t1t2_grid()
     D = sd.surrogate_dictionary(1000, g)
-    X, k0, _ = sd.voxel_fingerprints(D, 65536, noise=0.01)
-    idx, pd, par = run(binding, D, g, X)
-    sel = np.random.default_rng(5).choice(65536, 256, replace=False)
-    frac = check(D, X[sel], g, idx[sel], pd[sel], par[sel])
-    assert frac > 0.1
+    X, _, _ = sd.voxel_fingerprints(D, 65536, noise=0.01)
+    idx, pd, par, ov, dic = run(binding, D, g, X, keep=True)
+    rf, beta, res = dic.filter_info()
+    dic.close()
+    sel = np.random.default_rng(5).choice(65536, 512, replace=False)
+    near = check(D, X[sel], g, idx[sel], pd[sel], par[sel])
+    print(f"filter Rf {rf}, beta {beta:.2e}, residual {res:.2e}; overflow voxels {ov}; near-ties (<1e-5) {near:.3f}")
+    assert near > 0.2                              # the case the fp16-only argmax got wrong
+    assert ov <= 65536 // 100                      # the full scans stay rare on this dictionary
+
+
+def test_full_dictionary_phantom_voxels_exact(binding):
+    # rank-5 phantom time series (the kind of voxels the CG solution holds), every 7th voxel
+    cfg = synth.get_config("mrf")
+    g = sd.t1t2_grid()
+    D = sd.surrogate_dictionary(cfg.L, g)
+    x = synth.images(cfg, list(range(cfg.L)))      # [L][N][N]
+    X = x.reshape(cfg.L, -1).T[::7]
+    idx, pd, par, ov = run(binding, D, g, X)
+    sel = np.random.default_rng(6).choice(len(X), 512, replace=False)
+    check(D, X[sel], g, idx[sel], pd[sel], par[sel])
 
 
 def test_invalid_calls(binding):
@@ -103,10 +135,10 @@ def test_invalid_calls(binding):
     dic.close()
 
 
-def test_match_in_basis_coordinates_equals_the_frame_match(binding):
-    """mrf_dict_match_coef(u) = mrf_dict_match(x) for x = sum_i u_i d_i in span(d): same atom
-    except valid near-ties (scores from the frame-domain correlations), pd to 1e-4.  Both sides
-    are the library's; the frame-domain match is parity-tested against the oracle above."""
+def test_match_in_basis_coordinates_is_exact(binding):
+    """mrf_dict_match_coef(u) returns the exact argmax of |<d_k, x>| / ||d_k|| for x = sum_i u_i d_i
+    (d the library's basis; the expected values are computed here in float64 from that x), and
+    equals the frame-domain match of the same x."""
     L = 300
     grid = sd.t1t2_grid()[::7]
     D = sd.surrogate_dictionary(L, grid)
@@ -114,18 +146,17 @@ def test_match_in_basis_coordinates_equals_the_frame_match(binding):
     d = dic.basis(0.9999, 32)                                    # [r][L]
     X, _, _ = sd.voxel_fingerprints(D, 777, noise=0.02)          # [V][L]
     u = (X @ np.conj(d).T).astype(np.complex64)                  # coefficients of P_S x: [V][r]
-    x = (u.astype(np.complex128) @ d.astype(np.complex128)).astype(np.complex64)   # x in span(d)
+    x = u.astype(np.complex128) @ d.astype(np.complex128)        # x in span(d), exactly
     ic, pc, qc = dic.match_coef(torch.from_numpy(np.ascontiguousarray(u.T)).cuda())
-    ix, px, qx = dic.match(torch.from_numpy(np.ascontiguousarray(x.T)).cuda())
-    ic, ix = ic.cpu().numpy(), ix.cpu().numpy()
-    # normalised correlations of x (plain numpy here: x is built from the library's basis, so the
-    # oracle is not run on it)
-    score = np.abs(x.astype(np.complex128) @ np.conj(D).T) / np.linalg.norm(D, axis=1)[None, :]
-    s_best = score.max(axis=1)
-    same = ic == ix
-    assert same.mean() > 0.95
-    V = len(ic)
-    assert np.all(score[np.arange(V), ic] >= (1 - TIE_REL) * s_best)
-    assert np.allclose(pc.cpu().numpy()[same], px.cpu().numpy()[same], rtol=1e-4, atol=1e-6 * px.max().item())
-    assert np.array_equal(qc.cpu().numpy()[same], qx.cpu().numpy()[same])
+    ic = ic.cpu().numpy()
+    Dq = D.astype(np.complex64).astype(np.complex128)
+    c = x @ np.conj(Dq).T
+    n2 = np.sum(np.abs(Dq) ** 2, axis=1)
+    k = np.argmax(np.abs(c) / np.sqrt(n2)[None, :], axis=1)
+    assert np.array_equal(ic, k)
+    rho = np.maximum(c[np.arange(len(k)), k].real / n2[k], 0.0)
+    assert np.allclose(pc.cpu().numpy(), rho, rtol=1e-5, atol=1e-6 * rho.max())
+    assert np.array_equal(qc.cpu().numpy(), grid[k].astype(np.float32))
+    ix, px, qx = dic.match(torch.from_numpy(np.ascontiguousarray(x.T.astype(np.complex64))).cuda())
+    assert np.mean(ix.cpu().numpy() == ic) > 0.99                # x rounded to complex64 for the frame match
     dic.close()

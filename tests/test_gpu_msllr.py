@@ -84,10 +84,12 @@ def _rel(a, b):
     return float(np.linalg.norm(np.asarray(a) - np.asarray(b)) / np.linalg.norm(np.asarray(b)))
 
 
-TIE_REL = 2e-4   # as tests/test_gpu_match.py
+# Phi_D is exact (tests/test_gpu_match.py); the GPU and oracle iterates differ by ~1e-6 (fp32), so a
+# voxel whose best and second-best scores on the oracle's x lie closer than that may flip
+TIE_REL = 1e-5
 
 
-@pytest.mark.parametrize("lam1,iters,which", [(0.0, 3, "problem"), (2e-3, 2, "problem1")])
+@pytest.mark.parametrize("lam1,iters,which", [(0.0, 3, "problem"), (2e-3, 2, "problem1"), (2e-3, 4, "problem1")])
 def test_solve_against_the_oracle(binding, request, lam1, iters, which):
     pr = request.getfixturevalue(which)
     lam2, beta = 0.05, 0.5
