@@ -63,6 +63,7 @@ static void dict_free(mrf_dict_s* d) {
   for (void* p : {(void*)d->atoms, (void*)d->dn2, (void*)d->lut, (void*)d->phi, (void*)d->phiT, (void*)d->dpf,
                   (void*)d->w2f, (void*)d->xp, (void*)d->xs, (void*)d->xnorm, (void*)d->best, (void*)d->thr,
                   (void*)d->ncand, (void*)d->cand, (void*)d->ov, (void*)d->nov, (void*)d->xT, (void*)d->basis,
+                  (void*)d->part_best, (void*)d->a64, (void*)d->beta2, (void*)d->u64,
                   (void*)d->Mf, (void*)d->Gd, (void*)d->Dc})
     if (p) cudaFree(p);
   delete d;
@@ -90,7 +91,7 @@ static mrf_status build_filter(mrf_dict d) {
   double2* a = nullptr;
   double *res2 = nullptr, *a1 = nullptr;
   auto cleanup = [&]() {
-    for (void* p : {(void*)a, (void*)res2, (void*)a1})
+    for (void* p : {(void*)res2, (void*)a1})
       if (p) cudaFree(p);
   };
   if (cudaMalloc((void**)&d->phi, ph.size() * sizeof(float2)) != cudaSuccess ||
@@ -99,8 +100,10 @@ static mrf_status build_filter(mrf_dict d) {
       cudaMalloc((void**)&res2, (size_t)K * sizeof(double)) != cudaSuccess ||
       cudaMalloc((void**)&a1, (size_t)K * sizeof(double)) != cudaSuccess) {
     cleanup();
+    if (a) cudaFree(a);
     return fail(MRF_ENOMEM, "mrf_dict_create: filter allocation failed");
   }
+  d->a64 = a;   // owned by the dictionary from here on
   cudaError_t e = cudaMemcpy(d->phi, ph.data(), ph.size() * sizeof(float2), cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMemcpy(d->phiT, phT.data(), phT.size() * sizeof(float2), cudaMemcpyHostToDevice);
   if (e == cudaSuccess) {
@@ -147,15 +150,26 @@ static mrf_status build_filter(mrf_dict d) {
     }
   }
   // beta (match.cuh): residual ||r_k|| / ||d_k|| (plus 1e-12 for its float64 evaluation) +
-  // projection rounding sqrt(2) 32 u32 ||a_k||_1 / ||d_k|| + split-operand rounding 3 u16^2 +
-  // subnormal half (2^-25 sqrt(2 RF) 2) + worst-case fp32 accumulation of the K = 384 products
-  // gamma_384, on both components (sqrt 2), + the fp32 score arithmetic (1e-6), x 1.05
+  // projection rounding eps_u ||a_k||_1 / ||d_k|| (eps_u = sqrt(2) gamma_{2 kProjChunk} (1 + 1e-4):
+  // kProjChunk-frame fp32 chunks, ||phi_f|| <= 1 + 1e-4) + split-operand rounding 3 u16^2 + subnormal half
+  // (2^-25 sqrt(2 RF) 2) + worst-case fp32 accumulation of the K = 384 products gamma_384, on both
+  // components (sqrt 2), + the fp32 score arithmetic (1e-6), x 1.05.  beta2_k (the float64
+  // coefficient score of the rescoring) keeps the residual and projection terms of atom k.
   const double u32 = std::ldexp(1.0, -24), u16 = std::ldexp(1.0, -11);
   const double g384 = 384.0 * u32 / (1.0 - 384.0 * u32);
+  const double nfma = 2.0 * dm::kProjChunk;
+  const double eps_u = std::sqrt(2.0) * (nfma * u32 / (1.0 - nfma * u32)) * (1.0 + 1e-4);
   const double gemm = std::sqrt(2.0) * ((3.0 * u16 * u16 + g384) * 1.001 + std::ldexp(1.0, -25) * std::sqrt(2.0 * dm::RF) * 2.0);
   d->beta_res = bres;
   d->beta_a1 = ba1;
-  d->beta = 1.05 * ((bres + 1e-12) + std::sqrt(2.0) * 32.0 * u32 * ba1 + gemm + 1e-6);
+  d->beta = 1.05 * ((bres + 1e-12) + eps_u * ba1 + gemm + 1e-6);
+  std::vector<double> b2(K, 0.0);
+  for (int kk = 0; kk < K; ++kk)
+    if (dn2[kk] > 0.0)
+      b2[kk] = 1.05 * (std::sqrt(std::max(r2h[kk], 0.0)) + eps_u * a1h[kk]) / std::sqrt(dn2[kk]) + 1e-12;
+  if (cudaMalloc((void**)&d->beta2, (size_t)K * sizeof(double)) != cudaSuccess)
+    return fail(MRF_ENOMEM, "mrf_dict_create: filter allocation failed");
+  CUDA_TRY(cudaMemcpy(d->beta2, b2.data(), (size_t)K * sizeof(double), cudaMemcpyHostToDevice));
   if (cudaMalloc((void**)&d->dpf, dp.size() * sizeof(__half)) != cudaSuccess ||
       cudaMalloc((void**)&d->w2f, w2.size() * sizeof(float)) != cudaSuccess)
     return fail(MRF_ENOMEM, "mrf_dict_create: filter allocation failed");
@@ -198,6 +212,8 @@ mrf_status mrf_dict_create(const void* atoms, const float* lut, int K, int L, in
     e = cudaFuncSetAttribute(dm::k_dict_gemm<2, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dm::SMEM);
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(dm::k_dict_gemm<2, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dm::SMEM);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(dm::k_dict_proj_frames, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dm::proj_smem());
   if (e != cudaSuccess) {
     dict_free(d);
     return fail(MRF_ECUDA, std::string("mrf_dict_create: ") + cudaGetErrorString(e));
@@ -221,7 +237,7 @@ static mrf_status grow(mrf_dict d, long long vpad, long long vt, int L, cudaStre
   if (vpad > d->vcap) {
     CUDA_TRY(cudaStreamSynchronize(st));
     for (void** p : {(void**)&d->xp, (void**)&d->xs, (void**)&d->xnorm, (void**)&d->best, (void**)&d->thr,
-                     (void**)&d->ncand, (void**)&d->cand, (void**)&d->ov})
+                     (void**)&d->ncand, (void**)&d->cand, (void**)&d->ov, &d->part_best, (void**)&d->u64})
       if (*p) { cudaFree(*p); *p = nullptr; }
     d->vcap = 0;
     if (cudaMalloc((void**)&d->xp, (size_t)vpad * dm::KF * sizeof(__half)) != cudaSuccess ||
@@ -231,7 +247,9 @@ static mrf_status grow(mrf_dict d, long long vpad, long long vt, int L, cudaStre
         cudaMalloc((void**)&d->thr, (size_t)vpad * sizeof(float)) != cudaSuccess ||
         cudaMalloc((void**)&d->ncand, (size_t)vpad * sizeof(int)) != cudaSuccess ||
         cudaMalloc((void**)&d->cand, (size_t)vpad * dm::kCand * sizeof(int)) != cudaSuccess ||
-        cudaMalloc((void**)&d->ov, (size_t)vpad * sizeof(int)) != cudaSuccess)
+        cudaMalloc((void**)&d->ov, (size_t)vpad * sizeof(int)) != cudaSuccess ||
+        cudaMalloc((void**)&d->part_best, (size_t)vpad * dm::kParts * sizeof(dm::PartBest)) != cudaSuccess ||
+        cudaMalloc((void**)&d->u64, (size_t)vpad * dm::RF * sizeof(double2)) != cudaSuccess)
       return fail(MRF_ENOMEM, std::string(who) + ": workspace allocation failed");
     if (!d->nov && cudaMalloc((void**)&d->nov, sizeof(int)) != cudaSuccess)
       return fail(MRF_ENOMEM, std::string(who) + ": workspace allocation failed");
@@ -307,17 +325,19 @@ mrf_status mrf_dict_match(mrf_dict d, const void* x, long long V, int* index, fl
     return MRF_OK;
   }
   CUDA_TRY(cudaMemsetAsync(d->xp + (size_t)V * dm::KF, 0, (size_t)(vpad - V) * dm::KF * sizeof(__half), st));
-  dm::k_dict_proj_frames<<<(unsigned)((V + 31) / 32), 256, 0, st>>>(xf, d->phiT, d->L, (int)V, d->xT, d->xp, d->xs, d->xnorm);
+  dm::k_dict_proj_frames<<<(unsigned)((V + 31) / 32), 256, dm::proj_smem(), st>>>(xf, d->phiT, d->L, (int)V, d->xT, d->xp, d->xs,
+                                                                     d->xnorm, d->u64);
   MRF_TRY(check_launch("k_dict_proj_frames"));
   MRF_TRY(filter_passes(d, V, vpad, st));
-  dm::k_dict_rescore_frames<<<(unsigned)((V + 7) / 8), 256, 0, st>>>(d->xT, d->atoms, d->dn2, d->xnorm, d->ncand, d->cand,
-                                                                    d->lut, d->P, d->L, (int)V, index, pd, params, d->ov,
-                                                                    d->nov);
+  dm::k_dict_rescore_frames<<<(unsigned)((V + 7) / 8), 256, 0, st>>>(d->xT, d->atoms, d->dn2, d->xnorm, d->u64, d->a64,
+                                                                    d->beta2, d->ncand, d->cand, d->lut, d->P, d->L, (int)V,
+                                                                    index, pd, params, d->ov, d->nov);
   MRF_TRY(check_launch("k_dict_rescore_frames"));
-  dm::k_dict_exact_frames<<<(unsigned)std::min<long long>(V, 1184), 256, 0, st>>>(d->xT, d->atoms, d->dn2, d->K, d->lut,
-                                                                                  d->P, d->L, d->ov, d->nov, index, pd,
-                                                                                  params);
-  return check_launch("k_dict_exact_frames");
+  dm::k_dict_exact_frames<<<1184, 256, 0, st>>>(d->xT, d->atoms, d->dn2, d->K, d->L, d->ov, d->nov,
+                                                (dm::PartBest*)d->part_best);
+  MRF_TRY(check_launch("k_dict_exact_frames"));
+  dm::k_dict_exact_finish<<<64, 128, 0, st>>>(d->ov, d->nov, (const dm::PartBest*)d->part_best, d->dn2, d->lut, d->P, index, pd, params);
+  return check_launch("k_dict_exact_finish");
 }
 
 mrf_status mrf_dict_match_coef(mrf_dict d, const void* u, long long V, int* index, float* pd, float* params,

@@ -24,18 +24,22 @@ struct mrf_dict_s {
   __half* dpf = nullptr;         // [NP][KF]
   float* w2f = nullptr;          // [NP / 2]
   CUtensorMap tmdf;
-  double beta = 0.0;             // |rho~_k - rho_k| <= beta for every atom and voxel
+  double beta = 0.0;             // |rho~_k - rho_k| <= beta for every atom and voxel (the GEMM filter)
+  double2* a64 = nullptr;        // [K][64] a_k = phi d_k (float64; the rescoring's second level)
+  double* beta2 = nullptr;       // [K] |rho^_k - rho_k| bound of the float64 coefficient score
   double beta_res = 0.0, beta_a1 = 0.0;   // max ||r_k|| / ||d_k||, max ||a_k||_1 / ||d_k|| (diagnostics)
   // per-voxel workspaces (grown on demand)
   __half* xp = nullptr;          // [vcap][KF] packed filter coefficients
   float* xs = nullptr;           // [vcap] per-voxel scale
   double* xnorm = nullptr;       // [vcap] ||x_v||
+  double2* u64 = nullptr;        // [vcap][64] u = phi x (float64 totals of fp32 chunks)
   unsigned long long* best = nullptr;   // [vcap] packed (score, ~atom) maxima of the filter pass
   float* thr = nullptr;          // [vcap] certified-band threshold
   int* ncand = nullptr;          // [vcap]
   int* cand = nullptr;           // [vcap][kCand]
   int* ov = nullptr;             // [vcap] voxels rescored against every atom
   int* nov = nullptr;            // [1]
+  void* part_best = nullptr;     // [vcap][16] per-part bests of the full scan (match.cuh PartBest)
   long long vcap = 0;
   float2* xT = nullptr;          // [vtcap][L] voxel-major frames (frame-domain match)
   long long vtcap = 0;

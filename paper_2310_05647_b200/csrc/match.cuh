@@ -62,7 +62,7 @@ __device__ __forceinline__ void mma_f16(uint32_t tmem_d, uint64_t a, uint64_t b,
 // w2[k] = (m_k / ||d_k||)^2 (0 for padding atoms).  X~ [Vpad][KD] and D~ [NP][KD] fp16 are read
 // through the tensor maps; m_tiles = Vpad / BM, n_tiles = NP / BN, kblocks = KD / BK.  The
 // grid is persistent (one CTA per SM), so the m_tiles x n_tiles units quantise to < 1 %.
-constexpr int kCand = 32;   // listed candidates per voxel (more: the voxel is rescored against every atom)
+constexpr int kCand = 128;  // listed candidates per voxel (more: the voxel is rescored against every atom)
 
 template <int NG, int EPI>
 __global__ void __launch_bounds__(threads<NG>(), 1)
@@ -207,61 +207,96 @@ __device__ __forceinline__ void split_h(double v, __half& hi, __half& lo) {
   lo = __double2half(v - (double)__half2float(hi));
 }
 
-// Frame domain: x [L][V] complex64 -> u = Phi x (float64 totals of 16-frame fp32 chunks), ||x||
-// (float64), the packed row [V][KF] and scale s_v, and the voxel-major copy xT [V][L].
-// Block = 32 voxels x 8 groups; group g owns filter rows 8g .. 8g+7 (phiT [L][RF] complex, rows
-// past Rf zero); lane = voxel, so phi loads are warp-uniform broadcasts and x loads coalesce.
-__global__ void __launch_bounds__(256) k_dict_proj_frames(const float2* __restrict__ x, const float2* __restrict__ phiT,
-                                                          int L, int V, float2* __restrict__ xT,
-                                                          __half* __restrict__ xp, float* __restrict__ xs,
-                                                          double* __restrict__ xnorm) {
-  __shared__ float2 tile[32][33];   // [frame][voxel] staging of the transpose
-  __shared__ double red[8][32];
+// Frame domain: x [L][V] complex64 -> u = Phi x, ||x|| (float64), the packed row [V][KF], scale s_v,
+// u itself in float64 [V][RF] (the second certification level of the rescoring) and the
+// voxel-major copy xT [V][L].  u accumulates fp32 FMAs over kProjChunk-frame chunks (2 kProjChunk
+// FMAs per component: error <= gamma_{2 kProjChunk} Sum |phi| |x| <= gamma ||x||), each chunk
+// added in float64.  Block = 32 voxels x 8 groups; group g owns filter rows 8g .. 8g+7; lane = voxel.
+// Per 32-frame tile the x values (zero past L) and the tile's phi rows [32][RF] are staged in shared
+// memory (constant trip counts; every phi read is a broadcast).
+constexpr int kProjChunk = 32;
+constexpr size_t proj_smem() { return 2 * 32 * RF * 8 + 2 * 32 * 33 * 8; }
+
+// cp.async of 8 / 16 bytes, zero-filled when `valid` is false (LDGSTS; Ampere+)
+__device__ __forceinline__ void cp_async8(void* dst, const void* src, bool valid) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(saddr(dst)), "l"(src), "r"(valid ? 8 : 0) : "memory");
+}
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, bool valid) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(saddr(dst)), "l"(src), "r"(valid ? 16 : 0) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+
+__global__ void __launch_bounds__(256, 3) k_dict_proj_frames(const float2* __restrict__ x, const float2* __restrict__ phiT,
+                                                             int L, int V, float2* __restrict__ xT,
+                                                             __half* __restrict__ xp, float* __restrict__ xs,
+                                                             double* __restrict__ xnorm, double2* __restrict__ u64) {
+  extern __shared__ __align__(16) unsigned char pj_raw[];   // proj_smem() bytes
+  auto ptile = reinterpret_cast<float2(*)[32][RF]>(pj_raw);                  // [buffer][frame][filter row]
+  auto tile = reinterpret_cast<float2(*)[32][33]>(pj_raw + 2 * 32 * RF * 8);  // [buffer][frame][voxel]
+  auto red = reinterpret_cast<double(*)[32]>(pj_raw + 2 * 32 * RF * 8);       // after the loop (aliases tile)
   const int lane = threadIdx.x & 31, g = threadIdx.x >> 5;
   const int v = blockIdx.x * 32 + lane;
   const bool ok = v < V;
   double ur[8], ui[8], nrm = 0.0;
 #pragma unroll
   for (int i = 0; i < 8; ++i) ur[i] = ui[i] = 0.0;
-  for (int l0 = 0; l0 < L; l0 += 32) {
-    // transpose tile: warp g loads frames l0 + g + 8q for the 32 voxels (coalesced over voxels)
+  const int ntiles = (L + 31) / 32;
+  auto stage = [&](int t) {   // tile t into buffer t & 1 (zero past L / V)
+    const int l0 = 32 * t, bi = t & 1;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {   // warp g: frames l0 + g + 8q, coalesced over the voxels
+      const int l = l0 + g + 8 * q;
+      cp_async8(&tile[bi][g + 8 * q][lane], x + (size_t)min(l, L - 1) * V + (ok ? v : 0), ok && l < L);
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {   // 32 x 64 complex phi rows: 1024 x 16 bytes, 4 per thread
+      const int i = threadIdx.x + 256 * q, l = l0 + i / (RF / 2);
+      cp_async16(reinterpret_cast<float4*>(&ptile[bi][0][0]) + i,
+                 reinterpret_cast<const float4*>(phiT + (size_t)min(l, L - 1) * RF) + (i % (RF / 2)), l < L);
+    }
+  };
+  stage(0);
+  cp_async_commit();
+  for (int t = 0; t < ntiles; ++t) {
+    const int l0 = 32 * t, bi = t & 1;
+    if (t + 1 < ntiles) stage(t + 1);
+    cp_async_commit();
+    cp_async_wait1();   // tile t has landed (t + 1 may still be in flight)
+    __syncthreads();
+    float cr[8], ci[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) cr[i] = ci[i] = 0.f;
+#pragma unroll
+    for (int ll = 0; ll < 32; ++ll) {   // one 32-frame fp32 chunk, added in float64 below
+      const float2 xv = tile[bi][ll][lane];
+      const float4* pr = reinterpret_cast<const float4*>(&ptile[bi][ll][8 * g]);
+#pragma unroll
+      for (int i2 = 0; i2 < 4; ++i2) {
+        const float4 p = pr[i2];   // phi_{8g+2i2}, phi_{8g+2i2+1}; u += conj(phi) x
+        cr[2 * i2] = fmaf(p.x, xv.x, fmaf(p.y, xv.y, cr[2 * i2]));
+        ci[2 * i2] = fmaf(p.x, xv.y, fmaf(-p.y, xv.x, ci[2 * i2]));
+        cr[2 * i2 + 1] = fmaf(p.z, xv.x, fmaf(p.w, xv.y, cr[2 * i2 + 1]));
+        ci[2 * i2 + 1] = fmaf(p.z, xv.y, fmaf(-p.w, xv.x, ci[2 * i2 + 1]));
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) { ur[i] += (double)cr[i]; ui[i] += (double)ci[i]; }
+    // ||x||^2: warp g sums frames g, g + 8, g + 16, g + 24 of the tile for its voxel
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      const int l = l0 + g + 8 * q;
-      tile[g + 8 * q][lane] = (ok && l < L) ? __ldg(x + (size_t)l * V + v) : make_float2(0.f, 0.f);
-    }
-    __syncthreads();
-    // 16-frame fp32 chunks of this group's 8 coefficients, summed into float64
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      float cr[8], ci[8];
-#pragma unroll
-      for (int i = 0; i < 8; ++i) cr[i] = ci[i] = 0.f;
-      for (int ll = 16 * h; ll < 16 * h + 16 && l0 + ll < L; ++ll) {
-        const float2 xv = tile[ll][lane];
-        if (g == 0) nrm += (double)xv.x * xv.x + (double)xv.y * xv.y;
-        const float4* pr = reinterpret_cast<const float4*>(phiT + (size_t)(l0 + ll) * RF + 8 * g);
-#pragma unroll
-        for (int i2 = 0; i2 < 4; ++i2) {
-          const float4 p = __ldg(pr + i2);   // phi_{8g+2i2}, phi_{8g+2i2+1}; u += conj(phi) x
-          cr[2 * i2] = fmaf(p.x, xv.x, fmaf(p.y, xv.y, cr[2 * i2]));
-          ci[2 * i2] = fmaf(p.x, xv.y, fmaf(-p.y, xv.x, ci[2 * i2]));
-          cr[2 * i2 + 1] = fmaf(p.z, xv.x, fmaf(p.w, xv.y, cr[2 * i2 + 1]));
-          ci[2 * i2 + 1] = fmaf(p.z, xv.y, fmaf(-p.w, xv.x, ci[2 * i2 + 1]));
-        }
-      }
-#pragma unroll
-      for (int i = 0; i < 8; ++i) { ur[i] += (double)cr[i]; ui[i] += (double)ci[i]; }
+      const float2 xv = tile[bi][g + 8 * q][lane];
+      nrm += (double)xv.x * xv.x + (double)xv.y * xv.y;
     }
     // voxel-major copy: warp g writes voxels 4g .. 4g+3, 32 frames each (256 contiguous bytes)
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       const int vv = blockIdx.x * 32 + 4 * g + q;
-      if (vv < V && l0 + lane < L) xT[(size_t)vv * L + l0 + lane] = tile[lane][4 * g + q];
+      if (vv < V && l0 + lane < L) xT[(size_t)vv * L + l0 + lane] = tile[bi][lane][4 * g + q];
     }
-    __syncthreads();
+    __syncthreads();   // buffer bi is refilled by the stage of tile t + 2
   }
-  // s_v = max-abs over the Rf complex coefficients (the rows past Rf are exactly zero)
+  // s_v = max-abs over the Rf complex coefficients (the rows past Rf are exactly zero); ||x||
   double m = 0.0;
 #pragma unroll
   for (int i = 0; i < 8; ++i) m = fmax(m, fmax(fabs(ur[i]), fabs(ui[i])));
@@ -270,16 +305,23 @@ __global__ void __launch_bounds__(256) k_dict_proj_frames(const float2* __restri
   double s = 0.0;
   for (int i = 0; i < 8; ++i) s = fmax(s, red[i][lane]);
   if (!(s > 0.0)) s = 1.0;
+  __syncthreads();
+  red[g][lane] = nrm;
+  __syncthreads();
   if (!ok) return;
   if (g == 0) {
+    double n2 = 0.0;
+    for (int i = 0; i < 8; ++i) n2 += red[i][lane];
     xs[v] = (float)s;
-    xnorm[v] = sqrt(nrm);
+    xnorm[v] = sqrt(n2);
   }
   const float sf = (float)s;   // the scale the GEMM epilogue sees
   __half* row = xp + (size_t)v * KF;
+  double2* uv = u64 + (size_t)v * RF + 8 * g;
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
     const int c = 2 * (8 * g + i);
+    uv[i] = make_double2(ur[i], ui[i]);
     __half hr, lr, hi, li;
     split_h(ur[i] / (double)sf, hr, lr);
     split_h(ui[i] / (double)sf, hi, li);
@@ -394,10 +436,15 @@ __device__ __forceinline__ double2 warp_dot_frames(const float2* __restrict__ dk
   return make_double2(sr, si);
 }
 
-// Frames: one warp per voxel over its listed atoms; a voxel with an overflowing list, or every
-// atom in band, is queued for k_dict_exact_frames (ov / nov).
+// Frames: one warp per voxel.  Level 2 (lane i = listed atom i): rho^_k = |<a_k, u>| / (||d_k|| ||x||)
+// in float64 from the float64 coefficients, |rho^_k - rho_k| <= beta2_k = (||r_k|| + eps_u ||a_k||_1)
+// / ||d_k|| (per atom, dict.cu); an atom stays a candidate only if rho^_k + beta2_k reaches
+// max_j (rho^_j - beta2_j).  Level 3: exact float64 <d_k, x> over the frames for the survivors.  A
+// voxel whose list overflowed is queued for the full scan (ov / nov).
 __global__ void __launch_bounds__(256) k_dict_rescore_frames(const float2* __restrict__ xT, const float2* __restrict__ atoms,
                                                              const double* __restrict__ dn2, const double* __restrict__ xnorm,
+                                                             const double2* __restrict__ u64, const double2* __restrict__ a64,
+                                                             const double* __restrict__ beta2,
                                                              const int* __restrict__ ncand, const int* __restrict__ cand,
                                                              const float* __restrict__ lut, int P, int L, int V,
                                                              int* __restrict__ index, float* __restrict__ pd,
@@ -407,7 +454,8 @@ __global__ void __launch_bounds__(256) k_dict_rescore_frames(const float2* __res
   const int v = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (v >= V) return;
   Best b{-1.0, 0, 0.0};
-  if (!(xnorm[v] > 0.0)) {   // zero voxel: every score is 0 -> the lowest index, PD 0
+  const double xn = xnorm[v];
+  if (!(xn > 0.0)) {   // zero voxel: every score is 0 -> the lowest index, PD 0
     b.s = 0.0;
     if (lane == 0) finish_voxel(v, b, dn2, lut, P, index, pd, params);
     return;
@@ -417,28 +465,69 @@ __global__ void __launch_bounds__(256) k_dict_rescore_frames(const float2* __res
     if (lane == 0) ov[atomicAdd(nov, 1)] = v;
     return;
   }
+  // level 2: lane i scores listed atoms i, i + 32, i + 64, i + 96
+  constexpr int RND = kCand / 32;
+  int kr[RND];
+  double hr[RND], m = -INFINITY;
+  const double2* uv = u64 + (size_t)v * RF;
+#pragma unroll
+  for (int rd = 0; rd < RND; ++rd) {
+    const int i = 32 * rd + lane;
+    kr[rd] = 0;
+    hr[rd] = -INFINITY;
+    if (i < n) {
+      const int k = cand[(size_t)v * kCand + i];
+      const double2* ak = a64 + (size_t)k * RF;
+      double sr = 0.0, si = 0.0;
+#pragma unroll 8
+      for (int f = 0; f < RF; ++f) {   // <a_k, u> = sum conj(a) u
+        const double2 a = __ldg(ak + f), u = __ldg(uv + f);
+        sr += a.x * u.x + a.y * u.y;
+        si += a.x * u.y - a.y * u.x;
+      }
+      const double rho = sqrt(sr * sr + si * si) / (sqrt(dn2[k]) * xn), bk = beta2[k];
+      kr[rd] = k;
+      hr[rd] = rho + bk;
+      m = fmax(m, rho - bk);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  // level 3: exact float64 <d_k, x> for the atoms whose upper bound reaches m
   const float2* xv = xT + (size_t)v * L;
-  for (int i = 0; i < n; ++i) {
-    const int k = cand[(size_t)v * kCand + i];
-    const double2 c = warp_dot_frames(atoms + (size_t)k * L, xv, L, lane);
-    best_update(b, (c.x * c.x + c.y * c.y) / dn2[k], k, c.x);
+#pragma unroll
+  for (int rd = 0; rd < RND; ++rd) {
+    unsigned keep = __ballot_sync(0xffffffffu, hr[rd] >= m);
+    while (keep) {
+      const int i = __ffs(keep) - 1;
+      keep &= keep - 1;
+      const int ki = __shfl_sync(0xffffffffu, kr[rd], i);
+      const double2 c = warp_dot_frames(atoms + (size_t)ki * L, xv, L, lane);
+      best_update(b, (c.x * c.x + c.y * c.y) / dn2[ki], ki, c.x);
+    }
   }
   if (lane == 0) finish_voxel(v, b, dn2, lut, P, index, pd, params);
 }
 
-// every atom, exactly, for the queued voxels (one block per voxel, warps over atoms)
+// Full exact scan for the queued voxels: item (queued voxel q, atom part) -> the part's best in
+// part_best[q][part]; k_dict_exact_finish merges the parts in order (deterministic).
+constexpr int kParts = 16;
+struct PartBest {
+  double s, cre;
+  int k, pad;
+};
 __global__ void __launch_bounds__(256) k_dict_exact_frames(const float2* __restrict__ xT, const float2* __restrict__ atoms,
-                                                           const double* __restrict__ dn2, int K, const float* __restrict__ lut,
-                                                           int P, int L, const int* __restrict__ ov,
-                                                           const int* __restrict__ nov, int* __restrict__ index,
-                                                           float* __restrict__ pd, float* __restrict__ params) {
+                                                           const double* __restrict__ dn2, int K, int L,
+                                                           const int* __restrict__ ov, const int* __restrict__ nov,
+                                                           PartBest* __restrict__ part_best) {
   __shared__ Best wb[8];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int n = *nov;
-  for (int q = blockIdx.x; q < n; q += gridDim.x) {
-    const int v = ov[q];
-    Best b{-1.0, 0, 0.0};
-    for (int k = w; k < K; k += 8) {
+  const int n = *nov, kp = (K + kParts - 1) / kParts;
+  for (int it = blockIdx.x; it < n * kParts; it += gridDim.x) {
+    const int q = it / kParts, part = it % kParts, v = ov[q];
+    const int k0 = part * kp, k1 = min(K, k0 + kp);
+    Best b{-1.0, 0x7fffffff, 0.0};
+    for (int k = k0 + w; k < k1; k += 8) {
       if (!(dn2[k] > 0.0)) continue;   // an all-zero atom is never matched
       const double2 c = warp_dot_frames(atoms + (size_t)k * L, xT + (size_t)v * L, L, lane);
       best_update(b, (c.x * c.x + c.y * c.y) / dn2[k], k, c.x);
@@ -448,9 +537,24 @@ __global__ void __launch_bounds__(256) k_dict_exact_frames(const float2* __restr
     if (threadIdx.x == 0) {
       Best t = wb[0];
       for (int i = 1; i < 8; ++i) best_update(t, wb[i].s, wb[i].k, wb[i].cre);
-      finish_voxel(v, t, dn2, lut, P, index, pd, params);
+      part_best[(size_t)q * kParts + part] = PartBest{t.s, t.cre, t.k, 0};
     }
     __syncthreads();
+  }
+}
+
+__global__ void k_dict_exact_finish(const int* __restrict__ ov, const int* __restrict__ nov,
+                                    const PartBest* __restrict__ part_best, const double* __restrict__ dn2,
+                                    const float* __restrict__ lut, int P, int* __restrict__ index, float* __restrict__ pd,
+                                    float* __restrict__ params) {
+  const int n = *nov;
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < n; q += gridDim.x * blockDim.x) {
+    Best b{-1.0, 0x7fffffff, 0.0};
+    for (int part = 0; part < kParts; ++part) {
+      const PartBest pb = part_best[(size_t)q * kParts + part];
+      best_update(b, pb.s, pb.k, pb.cre);
+    }
+    finish_voxel(ov[q], b, dn2, lut, P, index, pd, params);
   }
 }
 

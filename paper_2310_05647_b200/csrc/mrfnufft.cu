@@ -111,6 +111,7 @@ struct mrf_plan_s {
   int* achunks = nullptr;    // per (interleaf, strip) spread matrix in SELL-32 form
   int2* atab = nullptr;
   int* fil = nullptr;
+  int* perm = nullptr;       // [L] interleaf-ordered processing order within each batch (DevPlan::perm)
   // workspaces
   // Frame batches alternate between kLanes internal streams so one batch's kernel tail overlaps
   // the next batch's kernels; each lane owns its half-grid and k-space workspaces.
@@ -166,11 +167,19 @@ struct mrf_plan_s {
   unsigned long long cg_use[kGraphs] = {}, cg_clock = 0;
   size_t bytes = 0;
   Prof prof;
+  // the gridding column kernels keep the natural frame order (interleaf order measured 2 % slower
+  // there); the Toeplitz column kernel walks each batch in interleaf order (its PSF tables)
+  DevPlan dp_natural() const {
+    DevPlan d = dp();
+    d.perm = nullptr;
+    return d;
+  }
   DevPlan dp() const {
     DevPlan d;
     d.N = N; d.G = G; d.M = M; d.R = R; d.C = C; d.W = W; d.S = S; d.recw = recw;
     d.coils = coils; d.dap = dap; d.tw = tw; d.fchunks = fchunks; d.ftab = ftab; d.achunks = achunks; d.atab = atab;
     d.fil = fil;
+    d.perm = perm;
     d.dbg = dbg;
     d.dbgbuf = dbgbuf;
     return d;
@@ -288,7 +297,7 @@ static void free_plan(mrf_plan_s* pl) {
     if (pl->Hs[i]) cudaFree(pl->Hs[i]);
     if (pl->ybufs[i]) cudaFree(pl->ybufs[i]);
   }
-  void* ptrs[] = {pl->pc_lam, pl->z, pl->pc_tmp, pl->pc_part,
+  void* ptrs[] = {pl->perm, pl->pc_lam, pl->z, pl->pc_tmp, pl->pc_part,
                   pl->coils, pl->dap, pl->tw, pl->fchunks, pl->ftab, pl->achunks, pl->atab, pl->fil, pl->r, pl->p, pl->q,
                   pl->part, pl->dotp, pl->sc, pl->hist, pl->stg_x, pl->stg_y, pl->stg_z, pl->ax[0], pl->ax[1],
                   pl->ay[0], pl->ay[1]};
@@ -485,7 +494,7 @@ template <int G>
 static mrf_status launch_fwd_cols(mrf_plan_s* pl, const float2* H, float2* y, int l0, int nb, cudaStream_t st) {
   const long long items = (long long)nb * pl->C * pl->S;
   ProfScope ps(pl, MRF_K_FWD_COLS, st);
-  CUDA_TRY(launch_pdl(k_fwd_cols<G>, pgrid(pl, pl->occ_fc, items), cols_threads<G>(), pl->col_smem, st, pl->dp(), H, y,
+  CUDA_TRY(launch_pdl(k_fwd_cols<G>, pgrid(pl, pl->occ_fc, items), cols_threads<G>(), pl->col_smem, st, pl->dp_natural(), H, y,
                       l0, nb, pl->fc_stage));
   return MRF_OK;
 }
@@ -496,7 +505,7 @@ static mrf_status launch_adj_cols(mrf_plan_s* pl, const float2* y, float2* H, in
   const int stage = ys ? pl->ac_stage : (int)(((size_t)pl->acol_smem - adj_cols_fixed<G>(0, pl->adj_sep)) & ~size_t(15));
   ProfScope ps(pl, MRF_K_ADJ_COLS, st);
   auto adj_kernel = pl->adj_sep ? k_adj_cols<G, (G <= 512)> : k_adj_cols<G, false>;
-  CUDA_TRY(launch_pdl(adj_kernel, pgrid(pl, pl->occ_ac, items), cols_threads<G>(), pl->acol_smem, st, pl->dp(), y, H,
+  CUDA_TRY(launch_pdl(adj_kernel, pgrid(pl, pl->occ_ac, items), cols_threads<G>(), pl->acol_smem, st, pl->dp_natural(), y, H,
                       l0, nb, ys, stage));
   return MRF_OK;
 }
@@ -1537,6 +1546,20 @@ mrf_status mrf_plan_create(const mrf_plan_desc* d, mrf_plan* out) {
   if (!ce) ce = up(pl->achunks, ach.data(), ach.size() * sizeof(int));
   if (!ce) ce = up(pl->atab, atab.data(), atab.size() * sizeof(int2));
   if (!ce) ce = up(pl->fil, fil.data(), fil.size() * sizeof(int));
+  std::vector<int> perm(L);   // (lives until the uploads below have completed)
+  if (!ce) {   // column passes: each batch's frames in interleaf order (shared plan tables read from L2)
+    for (int l0 = 0; l0 < L; l0 += bf) {
+      const int nb = std::min(bf, L - l0);
+      std::vector<int> ord(nb);
+      for (int i = 0; i < nb; ++i) ord[i] = i;
+      std::stable_sort(ord.begin(), ord.end(), [&](int a, int b) { return fil[l0 + a] < fil[l0 + b]; });
+      for (int i = 0; i < nb; ++i) perm[l0 + i] = ord[i];
+    }
+    if (std::getenv("MRF_NO_PERM") == nullptr) {
+      if (cudaMalloc((void**)&pl->perm, (size_t)L * sizeof(int)) != cudaSuccess) ce = cudaErrorMemoryAllocation;
+      else ce = up(pl->perm, perm.data(), perm.size() * sizeof(int));
+    }
+  }
   if (!ce && pl->coils) ce = up(pl->coils, d->coils, (size_t)C * N * N * sizeof(float2));
   if (!ce && (pl->flags & MRF_DCF)) {
     std::vector<double> wr((size_t)M);

@@ -105,6 +105,19 @@ def test_operators_stress_subset(mrf):
     assert rel(xa_gpu, xa_ref) <= OP_TOL
 
 
+def test_normal_stress_subset(mrf):
+    """The stress normal operator A^H A + mu I (16 coils, W = 8, 280 points in the DC cell:
+    reduction slices in the spread) on 3 frames, two of them in one batch, vs the oracle."""
+    cfg, traj, coils, frames, x = setup("stress", frames=[5, 6, 1500])
+    fil = synth.frame_interleaf(frames, cfg.R)
+    pl = plan_for(mrf, cfg, traj, coils, frames, batch_frames=2)
+    xn_gpu = host(pl.normal(dev(x), mu=cfg.mu))
+    xn_ref = on.normal(x, traj, coils, cfg.W, mu=cfg.mu, frame_interleaf=fil, workers=WORKERS)
+    assert rel(xn_gpu, xn_ref) <= OP_TOL
+    for i in range(len(frames)):   # and frame by frame (no frame hides behind another's norm)
+        assert rel(xn_gpu[i], xn_ref[i]) <= OP_TOL
+
+
 def test_full_mrf_launch_config_sampled_frames(mrf):
     """MRF-shaped config at full size (L = 1000, the bench launch configuration): sampled frames
     of forward / normal vs the oracle computed frame by frame."""
@@ -273,6 +286,22 @@ def test_cg_cfg2(mrf):
 
 def test_cg_sense_subset(mrf):
     _cg_case(mrf, "sense", frames=range(10))
+
+
+def test_cg_sense_multi_batch(mrf):
+    """SENSE CG (8 coils, 1 % noise, 10 iterations) over 16 frames in 4-frame batches on both
+    lanes, frames 40..55 (16 distinct interleaves), vs the oracle's CG."""
+    cfg, traj, coils, frames, x = setup("sense", frames=range(40, 56))
+    fil = synth.frame_interleaf(frames, cfg.R)
+    y = on.forward(x, traj, coils, cfg.W, frame_interleaf=fil, workers=WORKERS)
+    y = (y + cfg.noise * np.sqrt(np.mean(np.abs(y) ** 2)) * synth.unit_noise(cfg.C, cfg.M, frames, cfg.seed)).astype(np.complex64)
+    H = lambda v: on.normal(v, traj, coils, cfg.W, mu=cfg.mu, frame_interleaf=fil, workers=WORKERS)
+    rhs = ocg.dc_rhs(on.adjoint(y, traj, coils, cfg.N, cfg.W, frame_interleaf=fil, workers=WORKERS), None, cfg.mu)
+    x_ref, h_ref = ocg.cg(H, rhs, np.zeros_like(rhs), cfg.cg_iters)
+    pl = plan_for(mrf, cfg, traj, coils, frames, batch_frames=4)
+    xg, info = pl.dc_cg(dev(y), mu=cfg.mu, n_iter=cfg.cg_iters, zero_init=True)
+    assert rel(host(xg), x_ref) <= CG_TOL
+    assert np.allclose(info["history"], h_ref, rtol=1e-3, atol=0)
 
 
 def test_cg_x0_z(mrf):
