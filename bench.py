@@ -51,6 +51,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-pcg", action="store_true", help="skip the preconditioned-CG measurement")
     ap.add_argument("--pcg-tol", type=float, default=1e-3)
+    ap.add_argument("--flush-l2", default="auto", choices=["auto", "on", "off"],
+                    help="flush L2 between timed steps (auto: when the working set is < 4x L2)")
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target CPU work of the oracle sample")
     ap.add_argument("--batch-frames", type=int, default=0)
     return ap.parse_args()
@@ -324,15 +326,29 @@ def run_ours(args):
     barrier()
     torch.cuda.synchronize()
     clocks.start()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    ev0.record(stream)
-    for _ in range(args.steps):
-        step()
-    ev1.record(stream)
+    # L2 flush between steps when the step's working set is not far beyond the 126 MB L2
+    # (SURVEY.md §8(d) timing protocol): a 512 MB write outside the per-step events
+    work_set = 4.0 * L * cfg.N * cfg.N * 8 + 2.0 * L * cfg.C * cfg.M * 8
+    flush = args.flush_l2 == "on" or (args.flush_l2 == "auto" and work_set < 4 * 126e6)
+    scratch = torch.empty(512 << 20, dtype=torch.uint8, device=dev) if flush else None
+    if flush:   # per-step events around each step, the flush between them untimed
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+        for i in range(args.steps):
+            scratch.fill_(i & 0xFF)
+            evs[i][0].record(stream)
+            step()
+            evs[i][1].record(stream)
+    else:       # one bracket around the K steps
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))]
+        evs[0][0].record(stream)
+        for _ in range(args.steps):
+            step()
+        evs[0][1].record(stream)
     torch.cuda.synchronize()
     barrier()
-    ms_total = max_over_ranks(ev0.elapsed_time(ev1))
+    ms_total = max_over_ranks(sum(a.elapsed_time(b) for a, b in evs))
     clk = clocks.stop()
+    del scratch
     # per-kernel-class CUDA events (the library brackets every launch): the same steps again,
     # outside the timed region -- profiling replaces the solve's CUDA graph by direct launches
     plan.profile(True)
@@ -614,7 +630,9 @@ def run_ours(args):
         "config": {"workload": cfg.name, "N": cfg.N, "L": cfg.L, "M": cfg.M, "C": cfg.C, "R": cfg.R, "W": cfg.W,
                    "sigma": cfg.sigma, "cg_iters": n_iter, "mu": cfg.mu, "parallelism": f"frames/{world}",
                    "step": "mrf_dc_cg_ex(MRF_CG_ZERO_INIT), x0 = 0: 1 adjoint + n_iter normals + CG vector ops",
-                   "l2": "working set > L2 (x, r, p, q each %.0f MB); no flush" % (cfg.L * cfg.N ** 2 * 8 / 1e6),
+                   "l2": (f"L2 flushed between steps (512 MB write outside the per-step events; step working set "
+                          f"{work_set / 1e6:.0f} MB)" if flush else
+                          f"working set {work_set / 1e6:.0f} MB (x, r, p, q each {L * cfg.N ** 2 * 8 / 1e6:.0f} MB) > L2; no flush"),
                    "batch_frames": args.batch_frames or "auto"},
         "ms_per_AHA": ms_normal, "ms_per_forward": ms_fwd, "ms_per_adjoint": ms_adj,
         "ms_per_cg_iter_est": ms_cg_iter,

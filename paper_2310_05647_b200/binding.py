@@ -18,6 +18,8 @@ import numpy as np
 import torch
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libmrfnufft.so")
+if os.environ.get("MRF_LIB_PATH"):   # A/B experiments against another in-tree build (never the default)
+    LIB_PATH = os.environ["MRF_LIB_PATH"]
 
 MRF_DEAPOD_ANALYTIC = 0
 MRF_DEAPOD_DISCRETE = 1
@@ -131,7 +133,11 @@ def _load() -> ctypes.CDLL:
                              vp], ci),
     }
     for name, (args, res) in sig.items():
-        fn = getattr(lib, name)
+        fn = getattr(lib, name, None)
+        if fn is None:   # only an A/B build (MRF_LIB_PATH) may lack symbols; tests/test_abi_cpu.py checks the exports
+            if not os.environ.get("MRF_LIB_PATH"):
+                raise ImportError(f"{LIB_PATH} does not export {name}")
+            continue
         fn.argtypes = args
         fn.restype = res
     return lib

@@ -263,13 +263,14 @@ __device__ __forceinline__ void gather_rec_any(const int* rp, int W, const float
   atomicAdd(&yf[word(0)].y, acc.y);
 }
 
-// Column-pass items walk a batch's (frame, coil) pairs in interleaf order: perm[l0 + slot] is the
-// batch-local frame processed in slot `slot`, so the frames that share an interleaf (and its
-// plan tables) are processed together and read the tables from L2.  Returns fc = frame * C + c.
-__device__ __forceinline__ int item_fc(const DevPlan& p, int item, int S, int l0) {
-  const int slot = item / S, C = p.C;
+// Toeplitz column-pass items walk a batch's (frame, coil) pairs in interleaf order: perm[l0 + slot]
+// is the batch-local frame processed in slot `slot`, so the frames that share an interleaf (and its
+// PSF spectrum) are processed together and read it from L2.  Returns fc = frame * C + c.  (The
+// gridding column kernels keep the natural order: measured 3-6 % faster there.)
+__device__ __forceinline__ int item_fc(const int* __restrict__ perm, int C, int item, int S, int l0) {
+  const int slot = item / S;
   const int f = slot / C;
-  return (p.perm ? __ldg(p.perm + l0 + f) : f) * C + slot % C;
+  return (perm ? __ldg(perm + l0 + f) : f) * C + slot % C;
 }
 
 // ============================================================================ forward rows
@@ -424,12 +425,12 @@ k_fwd_cols(DevPlan p, const float2* __restrict__ H, float2* __restrict__ y, int 
   pdl_launch_dependents();
   pdl_wait();
   auto chunk_of = [&](int item) -> int2 {
-    const int fc = item_fc(p, item, S, l0), s = item % S;
+    const int fc = item / S, s = item % S;
     return __ldg(p.ftab + __ldg(p.fil + l0 + fc / C) * S + s);
   };
   auto issue_in = [&](int item) {
     mbar_expect_tx(&bars[0], STRIP_IN);
-    bulk_g2s(inb, H + ((size_t)item_fc(p, item, S, l0) * S + item % S) * (N * SW), STRIP_IN, &bars[0]);
+    bulk_g2s(inb, H + (size_t)item * (N * SW), STRIP_IN, &bars[0]);
   };
   auto issue_chunk = [&](int2 ow) {   // records beyond the staging capacity are read from L2
     const uint32_t bytes = (uint32_t)min(stage_cap, ow.y * 4) & ~15u;
@@ -449,7 +450,7 @@ k_fwd_cols(DevPlan p, const float2* __restrict__ H, float2* __restrict__ y, int 
     if (item + (int)gridDim.x < n_items) off_next = chunk_of(item + gridDim.x);
   }
   for (int k = 0; item < n_items; item += gridDim.x, ++k) {
-    const int fc = item_fc(p, item, S, l0);
+    const int fc = item / S;
     const int next = item + gridDim.x;
     mbar_wait(&bars[0], k & 1);
     pt.mark(0);
@@ -652,7 +653,7 @@ k_adj_cols(DevPlan p, const float2* __restrict__ y, float2* __restrict__ H, int 
   pdl_launch_dependents();
   pdl_wait();
   auto chunk_of = [&](int item) -> int2 {
-    const int fc = item_fc(p, item, S, l0), s = item % S;
+    const int fc = item / S, s = item % S;
     return __ldg(p.atab + __ldg(p.fil + l0 + fc / C) * S + s);
   };
   auto issue = [&](int item, int2 ow) {   // the part of a chunk beyond the staging buffer is read from L2
@@ -662,7 +663,7 @@ k_adj_cols(DevPlan p, const float2* __restrict__ y, float2* __restrict__ H, int 
     chunk_words = ow.y;
     mbar_expect_tx(&bars[0], bytes + (uint32_t)ystage);
     bulk_g2s(stage, p.achunks + ow.x, bytes, &bars[0]);
-    if (ystage) bulk_g2s(ys, y + (size_t)item_fc(p, item, S, l0) * M, (uint32_t)ystage, &bars[0]);
+    if (ystage) bulk_g2s(ys, y + (size_t)(item / S) * M, (uint32_t)ystage, &bars[0]);
   };
   int item = blockIdx.x;
   int2 off_next = make_int2(0, 0);
@@ -674,7 +675,7 @@ k_adj_cols(DevPlan p, const float2* __restrict__ y, float2* __restrict__ H, int 
     if (item + (int)gridDim.x < n_items) off_next = chunk_of(item + gridDim.x);
   }
   for (int k = 0; item < n_items; item += gridDim.x, ++k) {
-    const int fc = item_fc(p, item, S, l0);
+    const int fc = item / S;
     const int next = item + gridDim.x;
     mbar_wait(&bars[0], k & 1);
     pt.mark(0);
@@ -852,12 +853,12 @@ k_toep_cols(DevPlan p, const float2* __restrict__ Hf, float2* __restrict__ Ha, c
   pdl_wait();
   auto issue_in = [&](int item) {
     mbar_expect_tx(bar, STRIP_IN);
-    bulk_g2s(inb, Hf + ((size_t)item_fc(p, item, S, l0) * S + item % S) * (N * SW), STRIP_IN, bar);
+    bulk_g2s(inb, Hf + ((size_t)item_fc(p.perm, C, item, S, l0) * S + item % S) * (N * SW), STRIP_IN, bar);
   };
   int item = blockIdx.x;
   if (tid == 0 && item < n_items) issue_in(item);
   for (int k = 0; item < n_items; item += gridDim.x, ++k) {
-    const int fc = item_fc(p, item, S, l0), s = item % S;
+    const int fc = item_fc(p.perm, C, item, S, l0), s = item % S;
     const int next = item + gridDim.x;
     // PSF values at this thread's forward-output rows k1 + P k2: issued now, used after the FFT
     const int r = __ldg(p.fil + l0 + fc / C);

@@ -167,13 +167,6 @@ struct mrf_plan_s {
   unsigned long long cg_use[kGraphs] = {}, cg_clock = 0;
   size_t bytes = 0;
   Prof prof;
-  // the gridding column kernels keep the natural frame order (interleaf order measured 2 % slower
-  // there); the Toeplitz column kernel walks each batch in interleaf order (its PSF tables)
-  DevPlan dp_natural() const {
-    DevPlan d = dp();
-    d.perm = nullptr;
-    return d;
-  }
   DevPlan dp() const {
     DevPlan d;
     d.N = N; d.G = G; d.M = M; d.R = R; d.C = C; d.W = W; d.S = S; d.recw = recw;
@@ -494,7 +487,7 @@ template <int G>
 static mrf_status launch_fwd_cols(mrf_plan_s* pl, const float2* H, float2* y, int l0, int nb, cudaStream_t st) {
   const long long items = (long long)nb * pl->C * pl->S;
   ProfScope ps(pl, MRF_K_FWD_COLS, st);
-  CUDA_TRY(launch_pdl(k_fwd_cols<G>, pgrid(pl, pl->occ_fc, items), cols_threads<G>(), pl->col_smem, st, pl->dp_natural(), H, y,
+  CUDA_TRY(launch_pdl(k_fwd_cols<G>, pgrid(pl, pl->occ_fc, items), cols_threads<G>(), pl->col_smem, st, pl->dp(), H, y,
                       l0, nb, pl->fc_stage));
   return MRF_OK;
 }
@@ -505,7 +498,7 @@ static mrf_status launch_adj_cols(mrf_plan_s* pl, const float2* y, float2* H, in
   const int stage = ys ? pl->ac_stage : (int)(((size_t)pl->acol_smem - adj_cols_fixed<G>(0, pl->adj_sep)) & ~size_t(15));
   ProfScope ps(pl, MRF_K_ADJ_COLS, st);
   auto adj_kernel = pl->adj_sep ? k_adj_cols<G, (G <= 512)> : k_adj_cols<G, false>;
-  CUDA_TRY(launch_pdl(adj_kernel, pgrid(pl, pl->occ_ac, items), cols_threads<G>(), pl->acol_smem, st, pl->dp_natural(), y, H,
+  CUDA_TRY(launch_pdl(adj_kernel, pgrid(pl, pl->occ_ac, items), cols_threads<G>(), pl->acol_smem, st, pl->dp(), y, H,
                       l0, nb, ys, stage));
   return MRF_OK;
 }
