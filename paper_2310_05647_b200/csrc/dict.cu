@@ -64,7 +64,7 @@ static void dict_free(mrf_dict_s* d) {
                   (void*)d->w2f, (void*)d->xp, (void*)d->xs, (void*)d->xnorm, (void*)d->best, (void*)d->thr,
                   (void*)d->ncand, (void*)d->cand, (void*)d->ov, (void*)d->nov, (void*)d->xT, (void*)d->basis,
                   (void*)d->part_best, (void*)d->a64, (void*)d->beta2, (void*)d->u64,
-                  (void*)d->Mf, (void*)d->Gd, (void*)d->Dc})
+                  (void*)d->Gd, (void*)d->Dc, (void*)d->dpc, (void*)d->w2c})
     if (p) cudaFree(p);
   delete d;
 }
@@ -269,9 +269,11 @@ static mrf_status grow(mrf_dict d, long long vpad, long long vt, int L, cudaStre
 
 // The two filter GEMM passes over the packed voxel rows d->xp (match.cuh steps 3): best score,
 // certified band, candidate lists.
-static mrf_status filter_passes(mrf_dict d, long long V, long long vpad, cudaStream_t st) {
+static mrf_status filter_passes(mrf_dict d, long long V, long long vpad, int kf, const CUtensorMap& tmd, const float* w2,
+                                double beta, cudaStream_t st) {
   CUtensorMap tmx;
-  MRF_TRY(make_tmap(&tmx, d->xp, (uint64_t)dm::KF, (uint64_t)vpad, (uint32_t)dm::BM));
+  MRF_TRY(tmap_2d(&tmx, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, d->xp, (uint64_t)kf, (uint64_t)vpad, (uint64_t)kf * sizeof(__half),
+                  (uint32_t)dm::BK, (uint32_t)dm::BM));
   const int m_tiles = (int)(vpad / dm::BM), n_tiles = d->NP / dm::BN;
   int n_sm = 148;
   CUDA_TRY(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, d->device));
@@ -285,13 +287,13 @@ static mrf_status filter_passes(mrf_dict d, long long V, long long vpad, cudaStr
     }
     CUDA_TRY(cudaEventRecord(d->ev[d->ev_used], st));
   }
-  dm::k_dict_gemm<2, 0><<<grid, dm::threads<2>(), dm::SMEM, st>>>(tmx, d->tmdf, d->w2f, m_tiles, n_tiles, dm::KF / dm::BK,
-                                                                  (int)V, d->best, nullptr, nullptr, nullptr);
+  dm::k_dict_gemm<2, 0><<<grid, dm::threads<2>(), dm::SMEM, st>>>(tmx, tmd, w2, m_tiles, n_tiles, kf / dm::BK, (int)V,
+                                                                  d->best, nullptr, nullptr, nullptr);
   MRF_TRY(check_launch("k_dict_gemm"));
-  dm::k_dict_thr<<<(unsigned)((V + 255) / 256), 256, 0, st>>>(d->best, d->xnorm, d->xs, d->beta, (int)V, d->thr, d->ncand);
+  dm::k_dict_thr<<<(unsigned)((V + 255) / 256), 256, 0, st>>>(d->best, d->xnorm, d->xs, beta, (int)V, d->thr, d->ncand);
   MRF_TRY(check_launch("k_dict_thr"));
-  dm::k_dict_gemm<2, 1><<<grid, dm::threads<2>(), dm::SMEM, st>>>(tmx, d->tmdf, d->w2f, m_tiles, n_tiles, dm::KF / dm::BK,
-                                                                  (int)V, nullptr, d->thr, d->ncand, d->cand);
+  dm::k_dict_gemm<2, 1><<<grid, dm::threads<2>(), dm::SMEM, st>>>(tmx, tmd, w2, m_tiles, n_tiles, kf / dm::BK, (int)V,
+                                                                  nullptr, d->thr, d->ncand, d->cand);
   MRF_TRY(check_launch("k_dict_gemm"));
   if (d->prof) {
     CUDA_TRY(cudaEventRecord(d->ev[d->ev_used + 1], st));
@@ -328,7 +330,7 @@ mrf_status mrf_dict_match(mrf_dict d, const void* x, long long V, int* index, fl
   dm::k_dict_proj_frames<<<(unsigned)((V + 31) / 32), 256, dm::proj_smem(), st>>>(xf, d->phiT, d->L, (int)V, d->xT, d->xp, d->xs,
                                                                      d->xnorm, d->u64);
   MRF_TRY(check_launch("k_dict_proj_frames"));
-  MRF_TRY(filter_passes(d, V, vpad, st));
+  MRF_TRY(filter_passes(d, V, vpad, dm::KF, d->tmdf, d->w2f, d->beta, st));
   dm::k_dict_rescore_frames<<<(unsigned)((V + 7) / 8), 256, 0, st>>>(d->xT, d->atoms, d->dn2, d->xnorm, d->u64, d->a64,
                                                                     d->beta2, d->ncand, d->cand, d->lut, d->P, d->L, (int)V,
                                                                     index, pd, params, d->ov, d->nov);
@@ -343,17 +345,16 @@ mrf_status mrf_dict_match(mrf_dict d, const void* x, long long V, int* index, fl
 mrf_status mrf_dict_match_coef(mrf_dict d, const void* u, long long V, int* index, float* pd, float* params,
                                void* stream) {
   MRF_TRY(check_args(d, "mrf_dict_match_coef", u, V, index, pd, params));
-  if (!d->rank || !d->Dc) return fail(MRF_EINVAL, "mrf_dict_match_coef: no basis (call mrf_dict_basis)");
+  if (!d->rank || !d->Dc || !d->dpc) return fail(MRF_EINVAL, "mrf_dict_match_coef: no basis (call mrf_dict_basis)");
   CUDA_TRY(cudaSetDevice(d->device));
   cudaStream_t st = (cudaStream_t)stream;
   const long long vpad = ((V + dm::BM - 1) / dm::BM) * dm::BM;
   MRF_TRY(grow(d, vpad, 0, d->L, st, "mrf_dict_match_coef"));
   const float2* w = reinterpret_cast<const float2*>(u);
-  CUDA_TRY(cudaMemsetAsync(d->xp + (size_t)V * dm::KF, 0, (size_t)(vpad - V) * dm::KF * sizeof(__half), st));
-  dm::k_dict_proj_coef<<<(unsigned)((V + 127) / 128), 128, 0, st>>>(w, d->rank, (int)V, d->Mf, d->Gd, d->xp, d->xs,
-                                                                     d->xnorm);
+  CUDA_TRY(cudaMemsetAsync(d->xp + (size_t)V * dm::KFC, 0, (size_t)(vpad - V) * dm::KFC * sizeof(__half), st));
+  dm::k_dict_proj_coef<<<(unsigned)((V + 127) / 128), 128, 0, st>>>(w, d->rank, (int)V, d->Gd, d->xp, d->xs, d->xnorm);
   MRF_TRY(check_launch("k_dict_proj_coef"));
-  MRF_TRY(filter_passes(d, V, vpad, st));
+  MRF_TRY(filter_passes(d, V, vpad, dm::KFC, d->tmdc, d->w2c, d->beta_c, st));
   dm::k_dict_rescore_coef<<<(unsigned)((V + 127) / 128), 128, 0, st>>>(w, d->rank, d->Dc, d->dn2, d->xnorm, d->ncand,
                                                                         d->cand, d->lut, d->P, (int)V, index, pd, params,
                                                                         d->ov, d->nov);
@@ -429,37 +430,67 @@ static void host_jacobi_eig(int n, std::vector<std::complex<double>>& H, std::ve
 }
 
 // The match in basis coordinates (mrf_dict_match_coef; x = sum_i w_i d_i for the basis rows d_i):
-// Dc[k][i] = <d_i, d_k> (exact scores <d_k, x> = sum_i w_i conj(Dc[k][i])), Mf[i][f] = <phi_f, d_i>
-// (the filter coefficients u = phi x = sum_i w_i Mf[i]) and Gd[i][j] = <d_i, d_j> (||x||^2 =
-// w^H Gd w), all float64 on the device from the fp32 basis (k_cgemm, float64 accumulation).
+// Dc[k][i] = <d_i, d_k> (exact scores <d_k, x> = sum_i w_i conj(Dc[k][i])) and Gd[i][j] = <d_i, d_j>
+// (||x||^2 = w^H Gd w), float64 on the device from the fp32 basis (k_cgemm, float64 accumulation),
+// and the r-dimensional certified filter: rows [Dc_hi | Dc_hi | Dc_lo] / m'_k (blocks of 64 halves,
+// 2r <= 64), weights (m'_k / ||d_k||)^2 with the FULL atom norms, and beta_c = split-operand
+// rounding + worst-case fp32 accumulation of the K = 192 products (no residual: the identity is exact).
 static mrf_status build_coef_dict(mrf_dict d, int r) {
   const int K = d->K, L = d->L;
-  for (void* p : {(void*)d->Mf, (void*)d->Gd, (void*)d->Dc})
+  for (void* p : {(void*)d->Gd, (void*)d->Dc, (void*)d->dpc, (void*)d->w2c})
     if (p) cudaFree(p);
-  d->Mf = nullptr; d->Gd = nullptr; d->Dc = nullptr;
+  d->Gd = nullptr; d->Dc = nullptr; d->dpc = nullptr; d->w2c = nullptr;
   if (cudaMalloc((void**)&d->Dc, (size_t)K * r * sizeof(double2)) != cudaSuccess ||
-      cudaMalloc((void**)&d->Mf, (size_t)r * dm::RF * sizeof(double2)) != cudaSuccess ||
-      cudaMalloc((void**)&d->Gd, (size_t)r * r * sizeof(double2)) != cudaSuccess)
+      cudaMalloc((void**)&d->Gd, (size_t)r * r * sizeof(double2)) != cudaSuccess ||
+      cudaMalloc((void**)&d->dpc, (size_t)d->NP * dm::KFC * sizeof(__half)) != cudaSuccess ||
+      cudaMalloc((void**)&d->w2c, (size_t)d->NP / 2 * sizeof(float)) != cudaSuccess)
     return fail(MRF_ENOMEM, "mrf_dict_basis: allocation failed");
   const dim3 blk(16, 16);
   auto grid = [](int M, int N) { return dim3((unsigned)((N + 15) / 16), (unsigned)((M + 15) / 16)); };
   // Dc^* = conj(D) d^T, i.e. conj(Dc[k][i]) = sum_l conj(d_kl) d_il  (conjugated on the host below)
   llr::k_cgemm<<<grid(K, r), blk>>>(d->atoms, L, 1, 1, d->basis, 1, L, K, r, L, nullptr, d->Dc);
   MRF_TRY(check_launch("k_cgemm"));
-  // Mf^* [r][RF]: conj(Mf[i][f]) = sum_l conj(d_il) phi_fl
-  llr::k_cgemm<<<grid(r, dm::RF), blk>>>(d->basis, L, 1, 1, d->phi, 1, L, r, dm::RF, L, nullptr, d->Mf);
-  MRF_TRY(check_launch("k_cgemm"));
   // Gd [r][r]: Gd[i][j] = sum_l conj(d_il) d_jl = <d_i, d_j>
   llr::k_cgemm<<<grid(r, r), blk>>>(d->basis, L, 1, 1, d->basis, 1, L, r, r, L, nullptr, d->Gd);
   MRF_TRY(check_launch("k_cgemm"));
-  for (double2* p : {d->Dc, d->Mf}) {
-    const size_t n = p == d->Dc ? (size_t)K * r : (size_t)r * dm::RF;
-    std::vector<double2> h(n);
-    CUDA_TRY(cudaMemcpy(h.data(), p, n * sizeof(double2), cudaMemcpyDeviceToHost));
-    for (auto& v : h) v.y = -v.y;
-    CUDA_TRY(cudaMemcpy(p, h.data(), n * sizeof(double2), cudaMemcpyHostToDevice));
+  std::vector<double2> dc((size_t)K * r);
+  CUDA_TRY(cudaMemcpy(dc.data(), d->Dc, dc.size() * sizeof(double2), cudaMemcpyDeviceToHost));
+  for (auto& v : dc) v.y = -v.y;
+  CUDA_TRY(cudaMemcpy(d->Dc, dc.data(), dc.size() * sizeof(double2), cudaMemcpyHostToDevice));
+  std::vector<double> dn2(K);
+  CUDA_TRY(cudaMemcpy(dn2.data(), d->dn2, (size_t)K * sizeof(double), cudaMemcpyDeviceToHost));
+  std::vector<__half> dp((size_t)d->NP * dm::KFC, __float2half(0.f));
+  std::vector<float> w2((size_t)d->NP / 2, 0.f);
+  for (int k = 0; k < K; ++k) {
+    if (!(dn2[k] > 0.0)) continue;
+    double m = 0.0;
+    for (int i = 0; i < r; ++i) m = std::max({m, std::fabs(dc[(size_t)k * r + i].x), std::fabs(dc[(size_t)k * r + i].y)});
+    if (!(m > 0.0)) continue;
+    w2[k] = (float)(m * m / dn2[k]);
+    __half* r0 = &dp[(size_t)(2 * k) * dm::KFC];
+    __half* r1 = r0 + dm::KFC;
+    for (int i = 0; i < r; ++i) {
+      const double2 v = dc[(size_t)k * r + i];
+      const double comp[4] = {v.x / m, v.y / m, -v.y / m, v.x / m};   // r0: (re, im), r1: (-im, re)
+      for (int c = 0; c < 4; ++c) {
+        const __half hi = __double2half(comp[c]);
+        const __half lo = __double2half(comp[c] - (double)__half2float(hi));
+        __half* row = c < 2 ? r0 : r1;
+        const int col = 2 * i + (c & 1);
+        row[col] = hi;
+        row[64 + col] = hi;
+        row[128 + col] = lo;
+      }
+    }
   }
-  return MRF_OK;
+  const double u32 = std::ldexp(1.0, -24), u16 = std::ldexp(1.0, -11);
+  const double g192 = 192.0 * u32 / (1.0 - 192.0 * u32);
+  // ||w|| <= ||x|| (1 + 1e-6): the basis rows are orthonormal to fp32 rounding
+  d->beta_c = 1.05 * std::sqrt(2.0) * ((3.0 * u16 * u16 + g192) * 1.001 + std::ldexp(1.0, -25) * 8.0 * 2.0) + 1e-6;
+  CUDA_TRY(cudaMemcpy(d->dpc, dp.data(), dp.size() * sizeof(__half), cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(d->w2c, w2.data(), w2.size() * sizeof(float), cudaMemcpyHostToDevice));
+  return tmap_2d(&d->tmdc, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, d->dpc, (uint64_t)dm::KFC, (uint64_t)d->NP,
+                 (uint64_t)dm::KFC * sizeof(__half), (uint32_t)dm::BK, (uint32_t)dm::BN);
 }
 
 // Leading right singular vectors of D by subspace iteration on D^H D (GEMMs on the device, double

@@ -51,11 +51,14 @@ struct mrf_dict_s {
   unsigned basis_gen = 0;        // process-wide generation of the basis (mrf_dict_basis)
   float2* basis = nullptr;       // device [rank][L]
   std::vector<float2> basis_h;   // host copy
-  // the match in basis coordinates (mrf_dict_match_coef, x = sum_i w_i d_i): Mf = phi d_i
-  // [rank][64], Gd = d d^H [rank][rank] and Dc [K][rank] = <d_i, d_k>, all float64
-  double2* Mf = nullptr;
+  // the match in basis coordinates (mrf_dict_match_coef, x = sum_i w_i d_i): Gd = d d^H
+  // [rank][rank] and Dc [K][rank] = <d_i, d_k> (float64), and the r-dimensional filter
   double2* Gd = nullptr;
   double2* Dc = nullptr;
+  __half* dpc = nullptr;         // [NP][KFC] packed [Dc_hi | Dc_hi | Dc_lo] / m'_k rows (the coefficient filter)
+  float* w2c = nullptr;          // [NP / 2] (m'_k / ||d_k||)^2
+  CUtensorMap tmdc;
+  double beta_c = 0.0;           // the coefficient filter's bound on |rho~_k - rho_k|
   // last match: voxels rescored against every atom (diagnostics)
   int last_overflow = 0;
 };

@@ -331,27 +331,23 @@ __global__ void __launch_bounds__(256, 3) k_dict_proj_frames(const float2* __res
   }
 }
 
-// Basis coordinates: x = sum_i w_i d_i (w [r][V], the LLR basis d [r][L]) -> u = Phi x = sum_i w_i Mf_i
-// with Mf [r][RF] = Phi d_i (float64), ||x||^2 = w^H Gd w (Gd = d d^H, float64); one thread per voxel.
-__device__ __forceinline__ double2 proj_coef_f(const float2 (&wv)[32], int r, const double2* __restrict__ Mf, int f) {
-  double sr = 0.0, si = 0.0;
-  for (int i = 0; i < r; ++i) {
-    const double2 mm = __ldg(Mf + i * RF + f);
-    sr += (double)wv[i].x * mm.x - (double)wv[i].y * mm.y;
-    si += (double)wv[i].x * mm.y + (double)wv[i].y * mm.x;
-  }
-  return make_double2(sr, si);
-}
-
+// Basis coordinates: x = sum_i w_i d_i (w [r][V], the LLR basis rows d_i, r <= 32).  Here the exact
+// scores are r-dimensional, <d_k, x> = sum_i w_i conj(Dc[k][i]) (Dc = <d_i, d_k>, float64), so the
+// filter runs on w itself: rows [w_hi | w_lo | w_hi] / s_v of KFC = 3 x 64 halves (2r <= 64, zero
+// padded) against the packed Dc rows; ||x||^2 = w^H Gd w (Gd = d d^H, float64).  One thread per voxel.
+constexpr int KFC = 3 * 64;
 __global__ void __launch_bounds__(128) k_dict_proj_coef(const float2* __restrict__ w, int r, int V,
-                                                        const double2* __restrict__ Mf, const double2* __restrict__ Gd,
-                                                        __half* __restrict__ xp, float* __restrict__ xs,
-                                                        double* __restrict__ xnorm) {
+                                                        const double2* __restrict__ Gd, __half* __restrict__ xp,
+                                                        float* __restrict__ xs, double* __restrict__ xnorm) {
   const int v = blockIdx.x * blockDim.x + threadIdx.x;
   if (v >= V) return;
   float2 wv[32];
+  float m = 0.f;
 #pragma unroll
-  for (int i = 0; i < 32; ++i) wv[i] = i < r ? __ldg(w + (size_t)i * V + v) : make_float2(0.f, 0.f);
+  for (int i = 0; i < 32; ++i) {
+    wv[i] = i < r ? __ldg(w + (size_t)i * V + v) : make_float2(0.f, 0.f);
+    m = fmaxf(m, fmaxf(fabsf(wv[i].x), fabsf(wv[i].y)));
+  }
   double n2 = 0.0;
   for (int i = 0; i < r; ++i)
     for (int j = 0; j < r; ++j) {   // conj(w_i) Gd_ij w_j
@@ -360,24 +356,18 @@ __global__ void __launch_bounds__(128) k_dict_proj_coef(const float2* __restrict
       const double pr = ar * br - ai * bi, pi = ar * bi + ai * br;
       n2 += pr * gq.x - pi * gq.y;
     }
-  double m = 0.0;   // pass 1: the scale; pass 2: the packed row (recomputed: no 128-double array)
-  for (int f = 0; f < RF; ++f) {
-    const double2 u = proj_coef_f(wv, r, Mf, f);
-    m = fmax(m, fmax(fabs(u.x), fabs(u.y)));
-  }
-  if (!(m > 0.0)) m = 1.0;
-  const float sf = (float)m;
+  const float sf = m > 0.f ? m : 1.f;
   xs[v] = sf;
   xnorm[v] = sqrt(fmax(n2, 0.0));
-  __half* row = xp + (size_t)v * KF;
-  for (int f = 0; f < RF; ++f) {
-    const double2 u = proj_coef_f(wv, r, Mf, f);
+  __half* row = xp + (size_t)v * KFC;
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
     __half hr, lr, hi, li;
-    split_h(u.x / (double)sf, hr, lr);
-    split_h(u.y / (double)sf, hi, li);
-    row[2 * f] = hr; row[2 * f + 1] = hi;
-    row[2 * RF + 2 * f] = lr; row[2 * RF + 2 * f + 1] = li;
-    row[4 * RF + 2 * f] = hr; row[4 * RF + 2 * f + 1] = hi;
+    split_h((double)wv[i].x / (double)sf, hr, lr);
+    split_h((double)wv[i].y / (double)sf, hi, li);
+    row[2 * i] = hr; row[2 * i + 1] = hi;
+    row[64 + 2 * i] = lr; row[64 + 2 * i + 1] = li;
+    row[128 + 2 * i] = hr; row[128 + 2 * i + 1] = hi;
   }
 }
 
@@ -558,8 +548,9 @@ __global__ void k_dict_exact_finish(const int* __restrict__ ov, const int* __res
   }
 }
 
-// Basis coordinates: exact <d_k, x> = sum_i w_i conj(Dc[k][i]) (Dc = <d_i, d_k>, float64), one
-// thread per voxel over its listed atoms; overflow queued for k_dict_exact_coef.
+// Basis coordinates: exact <d_k, x> = sum_i w_i conj(Dc[k][i]) (Dc = <d_i, d_k>, float64: products of
+// fp32 w and float64 Dc, float64 sums), one thread per voxel over its listed atoms; overflow queued
+// for k_dict_exact_coef.
 __device__ __forceinline__ double2 dot_coef(const double2* __restrict__ dck, const float2 (&wv)[32], int r) {
   double sr = 0.0, si = 0.0;
   for (int i = 0; i < r; ++i) {
