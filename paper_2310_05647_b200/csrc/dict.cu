@@ -327,7 +327,7 @@ mrf_status mrf_dict_match(mrf_dict d, const void* x, long long V, int* index, fl
     return MRF_OK;
   }
   CUDA_TRY(cudaMemsetAsync(d->xp + (size_t)V * dm::KF, 0, (size_t)(vpad - V) * dm::KF * sizeof(__half), st));
-  dm::k_dict_proj_frames<<<(unsigned)((V + 31) / 32), 256, dm::proj_smem(), st>>>(xf, d->phiT, d->L, (int)V, d->xT, d->xp, d->xs,
+  dm::k_dict_proj_frames<<<(unsigned)((V + dm::PJV - 1) / dm::PJV), 256, dm::proj_smem(), st>>>(xf, d->phiT, d->L, (int)V, d->xT, d->xp, d->xs,
                                                                      d->xnorm, d->u64);
   MRF_TRY(check_launch("k_dict_proj_frames"));
   MRF_TRY(filter_passes(d, V, vpad, dm::KF, d->tmdf, d->w2f, d->beta, st));

@@ -209,15 +209,17 @@ __device__ __forceinline__ void split_h(double v, __half& hi, __half& lo) {
 
 // Frame domain: x [L][V] complex64 -> u = Phi x, ||x|| (float64), the packed row [V][KF], scale s_v,
 // u itself in float64 [V][RF] (the second certification level of the rescoring) and the
-// voxel-major copy xT [V][L].  u accumulates fp32 FMAs over kProjChunk-frame chunks (2 kProjChunk
-// FMAs per component: error <= gamma_{2 kProjChunk} Sum |phi| |x| <= gamma ||x||), each chunk
-// added in float64.  Block = 32 voxels x 8 groups; group g owns filter rows 8g .. 8g+7; lane = voxel.
-// Per 32-frame tile the x values (zero past L) and the tile's phi rows [32][RF] are staged in shared
-// memory (constant trip counts; every phi read is a broadcast).
-constexpr int kProjChunk = 32;
-constexpr size_t proj_smem() { return 2 * 32 * RF * 8 + 2 * 32 * 33 * 8; }
+// voxel-major copy xT [V][L].  A register-tiled complex GEMM on the CUDA cores: block = 64 voxels
+// x 64 coefficients, thread = 4 voxels x 4 coefficients (16 complex accumulators), K streamed in
+// 16-frame tiles (x tile [16][64] and phi tile [16][64] complex in shared memory, cp.async double
+// buffered; per frame 4 LDS.128 feed 64 FMAs).  Each 16-frame tile is one fp32 chunk (2 x 16 FMAs
+// per component: error <= gamma_32 Sum |phi| |x| <= gamma_32 ||x||), added into float64 totals.
+constexpr int kProjChunk = 16;   // frames per fp32 chunk = frames per K tile
+constexpr int PJV = 64;          // voxels per block
+constexpr int PJX = PJV + 2;     // padded x-tile row (16-byte aligned pairs, conflict-light transposed reads)
+constexpr size_t proj_smem() { return (size_t)2 * kProjChunk * RF * 8 + (size_t)2 * kProjChunk * PJX * 8; }
 
-// cp.async of 8 / 16 bytes, zero-filled when `valid` is false (LDGSTS; Ampere+)
+// cp.async of 8 / 16 bytes, zero-filled when `valid` is false (LDGSTS)
 __device__ __forceinline__ void cp_async8(void* dst, const void* src, bool valid) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(saddr(dst)), "l"(src), "r"(valid ? 8 : 0) : "memory");
 }
@@ -227,31 +229,35 @@ __device__ __forceinline__ void cp_async16(void* dst, const void* src, bool vali
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
 
-__global__ void __launch_bounds__(256, 3) k_dict_proj_frames(const float2* __restrict__ x, const float2* __restrict__ phiT,
+__global__ void __launch_bounds__(256, 2) k_dict_proj_frames(const float2* __restrict__ x, const float2* __restrict__ phiT,
                                                              int L, int V, float2* __restrict__ xT,
                                                              __half* __restrict__ xp, float* __restrict__ xs,
                                                              double* __restrict__ xnorm, double2* __restrict__ u64) {
   extern __shared__ __align__(16) unsigned char pj_raw[];   // proj_smem() bytes
-  auto ptile = reinterpret_cast<float2(*)[32][RF]>(pj_raw);                  // [buffer][frame][filter row]
-  auto tile = reinterpret_cast<float2(*)[32][33]>(pj_raw + 2 * 32 * RF * 8);  // [buffer][frame][voxel]
-  auto red = reinterpret_cast<double(*)[32]>(pj_raw + 2 * 32 * RF * 8);       // after the loop (aliases tile)
-  const int lane = threadIdx.x & 31, g = threadIdx.x >> 5;
-  const int v = blockIdx.x * 32 + lane;
-  const bool ok = v < V;
-  double ur[8], ui[8], nrm = 0.0;
+  auto ptile = reinterpret_cast<float2(*)[kProjChunk][RF]>(pj_raw);                              // [buf][frame][f]
+  auto tile = reinterpret_cast<float2(*)[kProjChunk][PJX]>(pj_raw + 2 * kProjChunk * RF * 8);    // [buf][frame][voxel]
+  auto red = reinterpret_cast<double(*)[16]>(pj_raw);   // after the loop: [voxel][tx] (aliases ptile)
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;   // coefficients 4tx.., voxels 4ty..
+  const int vb = blockIdx.x * PJV;
+  double ur[4][4], ui[4][4], nrm[4];
 #pragma unroll
-  for (int i = 0; i < 8; ++i) ur[i] = ui[i] = 0.0;
-  const int ntiles = (L + 31) / 32;
+  for (int a = 0; a < 4; ++a) {
+    nrm[a] = 0.0;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) ur[a][b] = ui[a][b] = 0.0;
+  }
+  const int ntiles = (L + kProjChunk - 1) / kProjChunk;
   auto stage = [&](int t) {   // tile t into buffer t & 1 (zero past L / V)
-    const int l0 = 32 * t, bi = t & 1;
+    const int l0 = kProjChunk * t, bi = t & 1;
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {   // warp g: frames l0 + g + 8q, coalesced over the voxels
-      const int l = l0 + g + 8 * q;
-      cp_async8(&tile[bi][g + 8 * q][lane], x + (size_t)min(l, L - 1) * V + (ok ? v : 0), ok && l < L);
+    for (int q = 0; q < kProjChunk * PJV / 256; ++q) {   // x: [16 frames][64 voxels], 8 bytes each
+      const int i = tid + 256 * q, fl = i / PJV, vv = i % PJV;
+      const int l = l0 + fl, v = vb + vv;
+      cp_async8(&tile[bi][fl][vv], x + (size_t)min(l, L - 1) * V + min(v, V - 1), l < L && v < V);
     }
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {   // 32 x 64 complex phi rows: 1024 x 16 bytes, 4 per thread
-      const int i = threadIdx.x + 256 * q, l = l0 + i / (RF / 2);
+    for (int q = 0; q < kProjChunk * RF / 2 / 256; ++q) {   // phi rows: [16][64] complex = 512 x 16 bytes
+      const int i = tid + 256 * q, fl = i / (RF / 2), l = l0 + fl;
       cp_async16(reinterpret_cast<float4*>(&ptile[bi][0][0]) + i,
                  reinterpret_cast<const float4*>(phiT + (size_t)min(l, L - 1) * RF) + (i % (RF / 2)), l < L);
     }
@@ -259,75 +265,95 @@ __global__ void __launch_bounds__(256, 3) k_dict_proj_frames(const float2* __res
   stage(0);
   cp_async_commit();
   for (int t = 0; t < ntiles; ++t) {
-    const int l0 = 32 * t, bi = t & 1;
+    const int l0 = kProjChunk * t, bi = t & 1;
     if (t + 1 < ntiles) stage(t + 1);
     cp_async_commit();
     cp_async_wait1();   // tile t has landed (t + 1 may still be in flight)
     __syncthreads();
-    float cr[8], ci[8];
+    float cr[4][4], ci[4][4];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) cr[i] = ci[i] = 0.f;
+    for (int a = 0; a < 4; ++a)
 #pragma unroll
-    for (int ll = 0; ll < 32; ++ll) {   // one 32-frame fp32 chunk, added in float64 below
-      const float2 xv = tile[bi][ll][lane];
-      const float4* pr = reinterpret_cast<const float4*>(&ptile[bi][ll][8 * g]);
+      for (int b = 0; b < 4; ++b) cr[a][b] = ci[a][b] = 0.f;
+#pragma unroll 4
+    for (int fl = 0; fl < kProjChunk; ++fl) {
+      const float4 x01 = *reinterpret_cast<const float4*>(&tile[bi][fl][4 * ty]);       // voxels 4ty, 4ty+1
+      const float4 x23 = *reinterpret_cast<const float4*>(&tile[bi][fl][4 * ty + 2]);
+      const float4 p01 = *reinterpret_cast<const float4*>(&ptile[bi][fl][4 * tx]);
+      const float4 p23 = *reinterpret_cast<const float4*>(&ptile[bi][fl][4 * tx + 2]);
+      const float2 xv[4] = {make_float2(x01.x, x01.y), make_float2(x01.z, x01.w), make_float2(x23.x, x23.y),
+                            make_float2(x23.z, x23.w)};
+      const float2 pv[4] = {make_float2(p01.x, p01.y), make_float2(p01.z, p01.w), make_float2(p23.x, p23.y),
+                            make_float2(p23.z, p23.w)};
 #pragma unroll
-      for (int i2 = 0; i2 < 4; ++i2) {
-        const float4 p = pr[i2];   // phi_{8g+2i2}, phi_{8g+2i2+1}; u += conj(phi) x
-        cr[2 * i2] = fmaf(p.x, xv.x, fmaf(p.y, xv.y, cr[2 * i2]));
-        ci[2 * i2] = fmaf(p.x, xv.y, fmaf(-p.y, xv.x, ci[2 * i2]));
-        cr[2 * i2 + 1] = fmaf(p.z, xv.x, fmaf(p.w, xv.y, cr[2 * i2 + 1]));
-        ci[2 * i2 + 1] = fmaf(p.z, xv.y, fmaf(-p.w, xv.x, ci[2 * i2 + 1]));
-      }
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {   // u += conj(phi) x
+          cr[a][b] = fmaf(pv[b].x, xv[a].x, fmaf(pv[b].y, xv[a].y, cr[a][b]));
+          ci[a][b] = fmaf(pv[b].x, xv[a].y, fmaf(-pv[b].y, xv[a].x, ci[a][b]));
+        }
     }
 #pragma unroll
-    for (int i = 0; i < 8; ++i) { ur[i] += (double)cr[i]; ui[i] += (double)ci[i]; }
-    // ||x||^2: warp g sums frames g, g + 8, g + 16, g + 24 of the tile for its voxel
+    for (int a = 0; a < 4; ++a)
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const float2 xv = tile[bi][g + 8 * q][lane];
-      nrm += (double)xv.x * xv.x + (double)xv.y * xv.y;
+      for (int b = 0; b < 4; ++b) { ur[a][b] += (double)cr[a][b]; ui[a][b] += (double)ci[a][b]; }
+    // ||x||^2: thread tx adds frame tx of the tile for its 4 voxels
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+      const float2 xv = tile[bi][tx][4 * ty + a];
+      nrm[a] += (double)xv.x * xv.x + (double)xv.y * xv.y;
     }
-    // voxel-major copy: warp g writes voxels 4g .. 4g+3, 32 frames each (256 contiguous bytes)
+    // voxel-major copy: 64 voxels x 16 frames, each voxel's 128-byte run coalesced
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int vv = blockIdx.x * 32 + 4 * g + q;
-      if (vv < V && l0 + lane < L) xT[(size_t)vv * L + l0 + lane] = tile[bi][lane][4 * g + q];
+    for (int q = 0; q < kProjChunk * PJV / 256; ++q) {
+      const int i = tid + 256 * q, vv = i / kProjChunk, fl = i % kProjChunk;
+      if (vb + vv < V && l0 + fl < L) xT[(size_t)(vb + vv) * L + l0 + fl] = tile[bi][fl][vv];
     }
     __syncthreads();   // buffer bi is refilled by the stage of tile t + 2
   }
-  // s_v = max-abs over the Rf complex coefficients (the rows past Rf are exactly zero); ||x||
-  double m = 0.0;
+  // per voxel: s_v = max-abs of its 64 complex coefficients (16 threads), ||x|| (16 threads)
 #pragma unroll
-  for (int i = 0; i < 8; ++i) m = fmax(m, fmax(fabs(ur[i]), fabs(ui[i])));
-  red[g][lane] = m;
-  __syncthreads();
-  double s = 0.0;
-  for (int i = 0; i < 8; ++i) s = fmax(s, red[i][lane]);
-  if (!(s > 0.0)) s = 1.0;
-  __syncthreads();
-  red[g][lane] = nrm;
-  __syncthreads();
-  if (!ok) return;
-  if (g == 0) {
-    double n2 = 0.0;
-    for (int i = 0; i < 8; ++i) n2 += red[i][lane];
-    xs[v] = (float)s;
-    xnorm[v] = sqrt(n2);
+  for (int a = 0; a < 4; ++a) {
+    double m = 0.0;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) m = fmax(m, fmax(fabs(ur[a][b]), fabs(ui[a][b])));
+    red[4 * ty + a][tx] = m;
   }
-  const float sf = (float)s;   // the scale the GEMM epilogue sees
-  __half* row = xp + (size_t)v * KF;
-  double2* uv = u64 + (size_t)v * RF + 8 * g;
+  __syncthreads();
+  double sv[4];
 #pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const int c = 2 * (8 * g + i);
-    uv[i] = make_double2(ur[i], ui[i]);
-    __half hr, lr, hi, li;
-    split_h(ur[i] / (double)sf, hr, lr);
-    split_h(ui[i] / (double)sf, hi, li);
-    row[c] = hr; row[c + 1] = hi;                       // [u_hi
-    row[2 * RF + c] = lr; row[2 * RF + c + 1] = li;     //  | u_lo
-    row[4 * RF + c] = hr; row[4 * RF + c + 1] = hi;     //  | u_hi]
+  for (int a = 0; a < 4; ++a) {
+    double m = 0.0;
+    for (int i = 0; i < 16; ++i) m = fmax(m, red[4 * ty + a][i]);
+    sv[a] = m > 0.0 ? m : 1.0;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int a = 0; a < 4; ++a) red[4 * ty + a][tx] = nrm[a];
+  __syncthreads();
+#pragma unroll
+  for (int a = 0; a < 4; ++a) {
+    const int v = vb + 4 * ty + a;
+    if (v >= V) continue;
+    if (tx == 0) {
+      double n2 = 0.0;
+      for (int i = 0; i < 16; ++i) n2 += red[4 * ty + a][i];
+      xs[v] = (float)sv[a];
+      xnorm[v] = sqrt(n2);
+    }
+    const float sf = (float)sv[a];   // the scale the GEMM epilogue sees
+    __half* row = xp + (size_t)v * KF;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int f = 4 * tx + b, c = 2 * f;
+      u64[(size_t)v * RF + f] = make_double2(ur[a][b], ui[a][b]);
+      __half hr, lr, hi, li;
+      split_h(ur[a][b] / (double)sf, hr, lr);
+      split_h(ui[a][b] / (double)sf, hi, li);
+      row[c] = hr; row[c + 1] = hi;                       // [u_hi
+      row[2 * RF + c] = lr; row[2 * RF + c + 1] = li;     //  | u_lo
+      row[4 * RF + c] = hr; row[4 * RF + c + 1] = hi;     //  | u_hi]
+    }
   }
 }
 
