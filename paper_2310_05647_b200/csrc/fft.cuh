@@ -35,8 +35,8 @@ template <int R, int K, int SIGN>
 struct Tw {
   static constexpr int Kr = (K % R) > R / 2 ? (K % R) - R : (K % R);
   static constexpr double ang = SIGN * 2.0 * c_pi() * double(Kr) / double(R);
-  static constexpr float c = float(c_cos(ang));
-  static constexpr float s = float(c_sin(ang));
+  static constexpr double c = c_cos(ang);
+  static constexpr double s = c_sin(ang);
 };
 
 __device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
@@ -67,8 +67,55 @@ __device__ __forceinline__ float2 twmul(float2 a) {
   } else if constexpr (4 * k == 3 * R) {
     return mul_i<-SIGN>(a);
   } else {
-    constexpr float c = Tw<R, K, SIGN>::c, s = Tw<R, K, SIGN>::s;
+    constexpr float c = float(Tw<R, K, SIGN>::c), s = float(Tw<R, K, SIGN>::s);
     return make_float2(fmaf(a.x, c, -a.y * s), fmaf(a.x, s, a.y * c));
+  }
+}
+
+// a + W_R^K b and a - W_R^K b with the twiddle multiplication folded into fused multiply-adds:
+// for W = c + i s, factor the larger of |c|, |s| out (tangent form, |t| <= 1): W b = c (b + i t b)
+// or s (u b + i b), so the pair costs 6 FP instructions (2 FMA for the scaled b, 4 FMA for the sum
+// and the difference) instead of 8 (a complex multiply and two complex additions).  The trivial
+// angles stay additions / swaps.
+template <int R, int K, int SIGN>
+__device__ __forceinline__ void bfly_w(float2 a, float2 b, float2& sum, float2& diff) {
+  constexpr int k = ((K % R) + R) % R;
+  if constexpr (k == 0 || 2 * k == R || 4 * k == R || 4 * k == 3 * R) {
+    const float2 t = twmul<R, K, SIGN>(b);
+    sum = cadd(a, t);
+    diff = csub(a, t);
+  } else {
+    constexpr double c = Tw<R, K, SIGN>::c, s = Tw<R, K, SIGN>::s;
+    if constexpr ((c < 0 ? -c : c) >= (s < 0 ? -s : s)) {
+      constexpr float t = float(s / c), cf = float(c);
+      const float bx = fmaf(-t, b.y, b.x), by = fmaf(t, b.x, b.y);   // b (1 + i t)
+      sum = make_float2(fmaf(cf, bx, a.x), fmaf(cf, by, a.y));
+      diff = make_float2(fmaf(-cf, bx, a.x), fmaf(-cf, by, a.y));
+    } else {
+      constexpr float u = float(c / s), sf = float(s);
+      const float bx = fmaf(u, b.x, -b.y), by = fmaf(u, b.y, b.x);   // b (u + i)
+      sum = make_float2(fmaf(sf, bx, a.x), fmaf(sf, by, a.y));
+      diff = make_float2(fmaf(-sf, bx, a.x), fmaf(-sf, by, a.y));
+    }
+  }
+}
+// a + W_R^K b alone (4 FP instructions for a generic angle)
+template <int R, int K, int SIGN>
+__device__ __forceinline__ float2 madd_w(float2 a, float2 b) {
+  constexpr int k = ((K % R) + R) % R;
+  if constexpr (k == 0 || 2 * k == R || 4 * k == R || 4 * k == 3 * R) {
+    return cadd(a, twmul<R, K, SIGN>(b));
+  } else {
+    constexpr double c = Tw<R, K, SIGN>::c, s = Tw<R, K, SIGN>::s;
+    if constexpr ((c < 0 ? -c : c) >= (s < 0 ? -s : s)) {
+      constexpr float t = float(s / c), cf = float(c);
+      const float bx = fmaf(-t, b.y, b.x), by = fmaf(t, b.x, b.y);
+      return make_float2(fmaf(cf, bx, a.x), fmaf(cf, by, a.y));
+    } else {
+      constexpr float u = float(c / s), sf = float(s);
+      const float bx = fmaf(u, b.x, -b.y), by = fmaf(u, b.y, b.x);
+      return make_float2(fmaf(sf, bx, a.x), fmaf(sf, by, a.y));
+    }
   }
 }
 
@@ -76,30 +123,26 @@ template <int R, int SIGN>
 __device__ __forceinline__ void dft(float2 (&v)[R]);
 
 namespace detail {
-// radix-4 DIT combine: X[k + m R/4] = sum_q W_R^{qk} W_4^{qm} D_q[k]
+// radix-4 DIT combine: X[k + m R/4] = sum_q W_R^{qk} W_4^{qm} D_q[k], with W_R^{3K} = W_R^K W_R^{2K}
+// and SIGN i = W_R^{R/4} folded into FMA butterflies (bfly_w):
+//   s02, d02 = D0 +- W^{2K} D2;  f, g = D1 +- W^{2K} D3;
+//   X[K], X[K + R/2] = s02 +- W^K f;  X[K + R/4], X[K + 3R/4] = d02 +- W^{K + R/4} g
 template <int R, int SIGN, int K>
 __device__ __forceinline__ void r4_combine(float2 (&v)[R], const float2 (&d0)[R / 4], const float2 (&d1)[R / 4],
                                            const float2 (&d2)[R / 4], const float2 (&d3)[R / 4]) {
   if constexpr (K < R / 4) {
-    const float2 a0 = d0[K];
-    const float2 a1 = twmul<R, K, SIGN>(d1[K]);
-    const float2 a2 = twmul<R, 2 * K, SIGN>(d2[K]);
-    const float2 a3 = twmul<R, 3 * K, SIGN>(d3[K]);
-    const float2 s02 = cadd(a0, a2), d02 = csub(a0, a2);
-    const float2 s13 = cadd(a1, a3), d13 = mul_i<SIGN>(csub(a1, a3));
-    v[K] = cadd(s02, s13);
-    v[K + R / 2] = csub(s02, s13);
-    v[K + R / 4] = cadd(d02, d13);
-    v[K + 3 * R / 4] = csub(d02, d13);
+    float2 s02, d02, f, g;
+    bfly_w<R, 2 * K, SIGN>(d0[K], d2[K], s02, d02);
+    bfly_w<R, 2 * K, SIGN>(d1[K], d3[K], f, g);
+    bfly_w<R, K, SIGN>(s02, f, v[K], v[K + R / 2]);
+    bfly_w<R, K + R / 4, SIGN>(d02, g, v[K + R / 4], v[K + 3 * R / 4]);
     r4_combine<R, SIGN, K + 1>(v, d0, d1, d2, d3);
   }
 }
 template <int R, int SIGN, int K>
 __device__ __forceinline__ void r2_combine(float2 (&v)[R], const float2 (&e)[R / 2], const float2 (&o)[R / 2]) {
   if constexpr (K < R / 2) {
-    const float2 t = twmul<R, K, SIGN>(o[K]);
-    v[K] = cadd(e[K], t);
-    v[K + R / 2] = csub(e[K], t);
+    bfly_w<R, K, SIGN>(e[K], o[K], v[K], v[K + R / 2]);
     r2_combine<R, SIGN, K + 1>(v, e, o);
   }
 }
@@ -177,19 +220,16 @@ __device__ __forceinline__ void dft_halfzero(float2 (&v)[P]) {
 }
 
 namespace detail {
-// radix-4 DIT combine producing only X[K] and X[K + 3R/4]
+// radix-4 DIT combine producing only X[K] and X[K + 3R/4] (folded as r4_combine)
 template <int R, int SIGN, int K>
 __device__ __forceinline__ void r4_combine_halfout(float2 (&v)[R], const float2 (&d0)[R / 4], const float2 (&d1)[R / 4],
                                                    const float2 (&d2)[R / 4], const float2 (&d3)[R / 4]) {
   if constexpr (K < R / 4) {
-    const float2 a0 = d0[K];
-    const float2 a1 = twmul<R, K, SIGN>(d1[K]);
-    const float2 a2 = twmul<R, 2 * K, SIGN>(d2[K]);
-    const float2 a3 = twmul<R, 3 * K, SIGN>(d3[K]);
-    const float2 s02 = cadd(a0, a2), d02 = csub(a0, a2);
-    const float2 s13 = cadd(a1, a3), d13 = mul_i<SIGN>(csub(a1, a3));
-    v[K] = cadd(s02, s13);
-    v[K + 3 * R / 4] = csub(d02, d13);
+    float2 s02, d02, f, g;
+    bfly_w<R, 2 * K, SIGN>(d0[K], d2[K], s02, d02);
+    bfly_w<R, 2 * K, SIGN>(d1[K], d3[K], f, g);
+    v[K] = madd_w<R, K, SIGN>(s02, f);
+    v[K + 3 * R / 4] = madd_w<R, K + 3 * R / 4, SIGN>(d02, g);   // d02 - W^{K + R/4} g
     r4_combine_halfout<R, SIGN, K + 1>(v, d0, d1, d2, d3);
   }
 }
@@ -207,9 +247,9 @@ __device__ __forceinline__ void dft_halfout(float2 (&v)[R]) {
     dft<4, SIGN>(e);
     dft<4, SIGN>(o);
     v[0] = cadd(e[0], o[0]);
-    v[1] = cadd(e[1], twmul<8, 1, SIGN>(o[1]));
-    v[6] = csub(e[2], twmul<8, 2, SIGN>(o[2]));
-    v[7] = csub(e[3], twmul<8, 3, SIGN>(o[3]));
+    v[1] = madd_w<8, 1, SIGN>(e[1], o[1]);
+    v[6] = madd_w<8, 6, SIGN>(e[2], o[2]);   // e - W^2 o = e + W^6 o
+    v[7] = madd_w<8, 7, SIGN>(e[3], o[3]);   // e - W^3 o = e + W^7 o
   } else if constexpr (R >= 16) {
     static_assert(R % 4 == 0, "R must be a power of two");
     float2 d0[R / 4], d1[R / 4], d2[R / 4], d3[R / 4];
