@@ -242,6 +242,13 @@ mrf_status mrf_dict_create(const void* atoms, const float* lut, int K, int L, in
  * voxel gets index 0, pd 0.  Errors: MRF_EINVAL, MRF_ENOMEM, MRF_ECUDA. */
 mrf_status mrf_dict_match(mrf_dict dict, const void* x, long long V, int* index, float* pd, float* params,
                           void* stream);
+/* mrf_dict_match with flags.  MRF_MATCH_NORM2: Eq. (5) as printed, k = argmax |<d_k, x>| /
+ * ||d_k||_2^2 (reading 21 uses ||d_k||_2: with atoms of unequal norm the printed
+ * form prefers low-norm atoms).  Same exact-argmax machinery (the band is widened by 1/min ||d_k||).
+ * Unknown flags: MRF_EINVAL. */
+#define MRF_MATCH_NORM2 1u
+mrf_status mrf_dict_match_ex(mrf_dict dict, const void* x, long long V, unsigned flags, int* index, float* pd,
+                             float* params, void* stream);
 /* Voxels of the last match that were rescored against every atom (more than 32 atoms inside the
  * certified band); synchronises.  The filter: *rank = Rf, *beta = the bound on the normalised
  * correlation, *residual = max_k ||r_k|| / ||d_k|| (nullable outputs). */
@@ -270,6 +277,8 @@ mrf_status mrf_dict_basis_copy(mrf_dict dict, void* basis_out);
  * atom norms ||d_k|| are kept).  Needs mrf_dict_basis; otherwise as mrf_dict_match. */
 mrf_status mrf_dict_match_coef(mrf_dict dict, const void* u, long long V, int* index, float* pd, float* params,
                                void* stream);
+mrf_status mrf_dict_match_coef_ex(mrf_dict dict, const void* u, long long V, unsigned flags, int* index, float* pd,
+                                  float* params, void* stream);
 
 /* An LLR operator on N x N images of the dictionary's L frames, p x p patches with stride s
  * (11 x 11, 5), patch corners 0, s, 2s, ... and N - p.  Needs mrf_dict_basis; the
@@ -365,6 +374,17 @@ typedef struct {
 } mrf_msllr_info;
 mrf_status mrf_msllr_solve(mrf_llr llr, mrf_dict dict, mrf_plan plan, const void* b, const mrf_msllr_params* prm,
                            void* x, int* index, float* pd, float* params, mrf_msllr_info* info, void* stream);
+/* Printed-form switches of the LLR / MS-LLR operator (the defaults are DESIGN.md's readings; these
+ * reproduce the formulas as printed): MRF_LLR_LITERAL_EQ23 -- the update divides by the scalar
+ * 1 + mu lambda2 beta of Eq. (23) instead of 1 + gamma c(v) (reading 25, exact
+ * with overlapping patches); MRF_LLR_RAW_MAPS -- the manifold weights of Eq. (8)
+ * use the raw (T1, T2, PD) patches instead of standardised ones (reading 26); MRF_LLR_MATCH_NORM2 --
+ * Phi_D inside mrf_msllr_solve uses Eq. (5)'s printed ||d||^2 denominator (reading 21).  Applies to
+ * every later call on the operator.  Unknown bits: MRF_EINVAL. */
+#define MRF_LLR_LITERAL_EQ23 1u
+#define MRF_LLR_RAW_MAPS 2u
+#define MRF_LLR_MATCH_NORM2 4u
+mrf_status mrf_llr_set_options(mrf_llr llr, unsigned options);
 mrf_status mrf_llr_destroy(mrf_llr llr);
 
 /* enable != 0 brackets every subsequent tensor-core GEMM launch (k_dict_gemm) of mrf_dict_match

@@ -57,9 +57,12 @@ def svt(C: np.ndarray, tau: float) -> np.ndarray:
     return (u * np.maximum(s - tau, 0.0)) @ vh
 
 
-def llr_prox(Z: np.ndarray, tau: float, gamma: float, p: int = 11, s: int = 5):
+def llr_prox(Z: np.ndarray, tau: float, gamma: float, p: int = 11, s: int = 5, literal: bool = False):
     """Eqs. (20)-(21): P_q = SVT_tau(Q_q(Z)) for all patches, then
-    X = (Z + gamma Q^*(P)) / (1 + gamma c).  Returns (X, nuclear norm sum of Q_q(Z))."""
+    X = (Z + gamma Q^*(P)) / (1 + gamma c) (reading 25: c(v) = number of patches covering v, the
+    exact minimiser with overlapping patches).  literal=True: the printed scalar form
+    X = (Z + gamma Q^*(P)) / (1 + gamma) of Eq. (23) (exact only when the
+    patches do not overlap).  Returns (X, nuclear norm sum of Q_q(Z))."""
     L, N, _ = Z.shape
     acc = np.zeros(Z.shape, dtype=np.complex128)
     cnt = np.zeros((N, N))
@@ -72,11 +75,12 @@ def llr_prox(Z: np.ndarray, tau: float, gamma: float, p: int = 11, s: int = 5):
             P = svt(C, tau)
             acc[:, y0:y0 + p, x0:x0 + p] += P.T.reshape(L, p, p)
             cnt[y0:y0 + p, x0:x0 + p] += 1.0
-    return (np.asarray(Z, np.complex128) + gamma * acc) / (1.0 + gamma * cnt)[None], nuc
+    den = (1.0 + gamma) * np.ones_like(cnt) if literal else (1.0 + gamma * cnt)
+    return (np.asarray(Z, np.complex128) + gamma * acc) / den[None], nuc
 
 
 def llr_step(X, rhs, normal, d, mu: float, lam2: float, beta: float, p: int = 11, s: int = 5,
-             lam1: float = 0.0, lap=None):
+             lam1: float = 0.0, lap=None, literal: bool = False):
     """One iteration of Algorithm 1: Eq. (15) -> Eq. (20) -> Eq. (21).  normal(v) = A^H A v;
     rhs = A^H b; lam1, lap: the manifold term lam1 Q^*(Q(X) L) of Eq. (15) (``oracle.manifold``),
     omitted when lam1 = 0 (the LLR ablation).  Returns (X+, Z)."""
@@ -85,5 +89,5 @@ def llr_step(X, rhs, normal, d, mu: float, lam2: float, beta: float, p: int = 11
         from .manifold import gradient
         G = G + lam1 * gradient(np.asarray(X, np.complex128), lap, X.shape[1], p, s)
     Z = project(np.asarray(X, np.complex128) - mu * G, d)
-    Xn, _ = llr_prox(Z, 1.0 / beta, mu * lam2 * beta, p, s)
+    Xn, _ = llr_prox(Z, 1.0 / beta, mu * lam2 * beta, p, s, literal=literal)
     return Xn, Z

@@ -53,10 +53,12 @@ def standardise(maps: np.ndarray) -> np.ndarray:
     return out
 
 
-def weights(maps: np.ndarray, N: int, p: int = 11, s: int = 5, sigma2: float | None = None):
-    """(W [n][n], sigma^2) from the parameter maps (Eq. 8)."""
+def weights(maps: np.ndarray, N: int, p: int = 11, s: int = 5, sigma2: float | None = None, raw: bool = False):
+    """(W [n][n], sigma^2) from the parameter maps (Eq. 8).  The distances use the standardised
+    maps (reading 26); raw=True: the printed form, Euclidean distances of the raw (T1, T2, PD)
+    patches (PAPER.md:151)."""
     P = patches(N, p, s)
-    V = casorati_all(standardise(maps), P, p)                   # [3 p^2][n]
+    V = casorati_all(np.asarray(maps, np.float64) if raw else standardise(maps), P, p)   # [3 p^2][n]
     sq = np.sum(V * V, axis=0)
     d2 = np.maximum(sq[:, None] + sq[None, :] - 2.0 * (V.T @ V), 0.0)
     n = d2.shape[0]

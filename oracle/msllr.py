@@ -44,21 +44,25 @@ def cost(X, b, A, lam1: float, lam2: float, lap=None, p: int = 11, s: int = 5):
     return data + lam1 * trace + lam2 * nuc, (data, trace, nuc)
 
 
-def maps_of(X, D, lut):
-    """Phi_D(X) for X [L][N][N]: (k [V], eta [V][P], rho [V]) and the map stack (T1, T2, PD) [3][N][N]."""
+def maps_of(X, D, lut, match_p: int = 1):
+    """Phi_D(X) for X [L][N][N]: (k [V], eta [V][P], rho [V]) and the map stack (T1, T2, PD) [3][N][N].
+    match_p = 2: Eq. (5)'s printed ||d||^2 denominator (reading 21 uses ||d||)."""
     L, N, _ = X.shape
-    k, eta, rho, _ = omatch.match(np.asarray(X).reshape(L, -1).T, D, lut)
+    k, eta, rho, _ = omatch.match(np.asarray(X).reshape(L, -1).T, D, lut, p=match_p)
     m = np.stack([eta[:, 0].reshape(N, N), eta[:, 1].reshape(N, N), rho.reshape(N, N)])
     return (k, eta, rho), m
 
 
 def solve(b, traj, D, lut, d, mu: float, lam1_0: float, lam2: float, beta: float, max_iter: int,
           tol: float = 1e-5, W: int = 6, N: int | None = None, p: int = 11, s: int = 5,
-          sigma2: float | None = None, workers: int = 1, op: str = "grid", coils=None):
+          sigma2: float | None = None, workers: int = 1, op: str = "grid", coils=None, literal_update: bool = False,
+          raw_maps: bool = False, match_p: int = 1):
     """Algorithm 1.  b [L][C][M] k-space, traj [R][M][2], D [K][L] atoms, lut [K][2] (T1, T2),
     d [r][L] the basis of P_S, coils [C][N][N] or None (A = F_u C).  op = "grid":
     A is the KB gridding NUFFT; op = "nudft": A is the plain definition (the direct non-uniform DFT).
-    Returns dict(x, k, eta, rho, iters, cost, lambda1)."""
+    The printed-form switches (readings 21, 25, 26): literal_update -> Eq. (21)'s scalar
+    1 + mu lambda2 beta denominator; raw_maps -> Eq. (8) on the raw maps; match_p = 2 -> Eq. (5)'s
+    ||d||^2 denominator in Phi_D.  Returns dict(x, k, eta, rho, iters, cost, lambda1)."""
     b = np.asarray(b, np.complex128)
     S = coils
     if op == "nudft":
@@ -74,8 +78,8 @@ def solve(b, traj, D, lut, d, mu: float, lam1_0: float, lam2: float, beta: float
 
     def update_maps(X):
         nonlocal lam1, lap
-        _, m = maps_of(X, D, lut)
-        Wm, _ = om.weights(m, N, p, s, sigma2)
+        _, m = maps_of(X, D, lut, match_p)
+        Wm, _ = om.weights(m, N, p, s, sigma2, raw=raw_maps)
         lap = om.laplacian(Wm)
         lam1 = lam1_0 * float(lap.max())                              # lambda_1^0 max(L)
 
@@ -83,7 +87,7 @@ def solve(b, traj, D, lut, d, mu: float, lam1_0: float, lam2: float, beta: float
         update_maps(X)                                                 # M^0, L^0
     costs, prev, it = [], 0.0, 0
     for n in range(1, max_iter + 1):
-        X, _ = ol.llr_step(X, rhs, normal, d, mu, lam2, beta, p, s, lam1=lam1, lap=lap)
+        X, _ = ol.llr_step(X, rhs, normal, d, mu, lam2, beta, p, s, lam1=lam1, lap=lap, literal=literal_update)
         c, _ = cost(X, b, A, lam1, lam2, lap, p, s)
         costs.append(c)
         it = n
@@ -92,5 +96,5 @@ def solve(b, traj, D, lut, d, mu: float, lam1_0: float, lam2: float, beta: float
         prev = c
         if lam1_0 > 0 and n < max_iter:
             update_maps(X)
-    (k, eta, rho), _ = maps_of(X, D, lut)
+    (k, eta, rho), _ = maps_of(X, D, lut, match_p)
     return {"x": X, "k": k, "eta": eta, "rho": rho, "iters": it, "cost": costs, "lambda1": lam1}

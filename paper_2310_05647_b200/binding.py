@@ -38,7 +38,10 @@ EXPORTED = [
     "mrf_llr_step", "mrf_llr_destroy", "mrf_llr_laplacian", "mrf_llr_cost", "mrf_msllr_solve", "mrf_plan_wait",
     "mrf_dict_match_coef", "mrf_llr_create_basis", "mrf_llr_subspace_normal", "mrf_llr_create_shard",
     "mrf_plan_set_host_allreduce", "mrf_plan_set_precond_shift", "mrf_dict_overflow", "mrf_dict_filter_info",
+    "mrf_dict_match_ex", "mrf_dict_match_coef_ex", "mrf_llr_set_options",
 ]
+MRF_MATCH_NORM2 = 1
+MRF_LLR_LITERAL_EQ23, MRF_LLR_RAW_MAPS, MRF_LLR_MATCH_NORM2 = 1, 2, 4
 
 MRF_DTYPE_F32 = 0
 MRF_DTYPE_F64 = 1
@@ -110,6 +113,9 @@ def _load() -> ctypes.CDLL:
         "mrf_dict_create": ([vp, vp, ci, ci, ci, ci, ctypes.POINTER(vp)], ci),
         "mrf_dict_match": ([vp, vp, ctypes.c_longlong, vp, vp, vp, vp], ci),
         "mrf_dict_match_coef": ([vp, vp, ctypes.c_longlong, vp, vp, vp, vp], ci),
+        "mrf_dict_match_ex": ([vp, vp, ctypes.c_longlong, ctypes.c_uint, vp, vp, vp, vp], ci),
+        "mrf_dict_match_coef_ex": ([vp, vp, ctypes.c_longlong, ctypes.c_uint, vp, vp, vp, vp], ci),
+        "mrf_llr_set_options": ([vp, ctypes.c_uint], ci),
         "mrf_dict_destroy": ([vp], ci),
         "mrf_dict_overflow": ([vp, ctypes.POINTER(ci)], ci),
         "mrf_dict_filter_info": ([vp, ctypes.POINTER(ci), ctypes.POINTER(ctypes.c_double),
@@ -414,7 +420,9 @@ class Dictionary:
                                    self.K, self.L, self.P, self.device, ctypes.byref(h)))
         self._h = h
 
-    def match(self, x: torch.Tensor):
+    def match(self, x: torch.Tensor, norm2: bool = False):
+        """Exact Phi_D of the frame-major stack x [L][...voxels]; norm2=True: Eq. (5) as printed
+        (||d||^2 denominator, mrf_dict_match_ex with MRF_MATCH_NORM2)."""
         if not (isinstance(x, torch.Tensor) and x.is_cuda and x.dtype == torch.complex64 and x.is_contiguous()):
             raise TypeError("x must be a contiguous CUDA complex64 tensor [L][...]")
         if x.shape[0] != self.L:
@@ -424,10 +432,11 @@ class Dictionary:
         pd = torch.empty(V, dtype=torch.float32, device=x.device)
         params = torch.empty((V, self.P), dtype=torch.float32, device=x.device) if self.P else None
         st = torch.cuda.current_stream(x.device).cuda_stream
-        _check(lib.mrf_dict_match(self._h, _ptr(x), V, _ptr(index), _ptr(pd), _ptr(params), ctypes.c_void_p(st)))
+        _check(lib.mrf_dict_match_ex(self._h, _ptr(x), V, MRF_MATCH_NORM2 if norm2 else 0, _ptr(index), _ptr(pd),
+                                     _ptr(params), ctypes.c_void_p(st)))
         return index, pd, params
 
-    def match_coef(self, u: torch.Tensor):
+    def match_coef(self, u: torch.Tensor, norm2: bool = False):
         """Phi_D of voxels in basis coordinates u [r][...voxels] (CUDA complex64), x_v = sum_i u[i, v] d_i
         (mrf_dict_match_coef; needs basis())."""
         if not (isinstance(u, torch.Tensor) and u.is_cuda and u.dtype == torch.complex64 and u.is_contiguous()):
@@ -437,7 +446,8 @@ class Dictionary:
         pd = torch.empty(V, dtype=torch.float32, device=u.device)
         params = torch.empty((V, self.P), dtype=torch.float32, device=u.device) if self.P else None
         st = torch.cuda.current_stream(u.device).cuda_stream
-        _check(lib.mrf_dict_match_coef(self._h, _ptr(u), V, _ptr(index), _ptr(pd), _ptr(params), ctypes.c_void_p(st)))
+        _check(lib.mrf_dict_match_coef_ex(self._h, _ptr(u), V, MRF_MATCH_NORM2 if norm2 else 0, _ptr(index), _ptr(pd),
+                                          _ptr(params), ctypes.c_void_p(st)))
         return index, pd, params
 
     def overflow(self) -> int:
@@ -525,6 +535,13 @@ class LLR:
         self._h = h
         self.N, self.L, self.r = int(N), int(L_local), None
         return self
+
+    def set_options(self, literal_eq23: bool = False, raw_maps: bool = False, match_norm2: bool = False):
+        """The printed-form switches (mrf_llr_set_options): Eq. (23)'s scalar denominator, Eq. (8)
+        on raw maps, Eq. (5)'s ||d||^2 denominator in Phi_D (readings 25, 26, 21)."""
+        o = (MRF_LLR_LITERAL_EQ23 if literal_eq23 else 0) | (MRF_LLR_RAW_MAPS if raw_maps else 0) | \
+            (MRF_LLR_MATCH_NORM2 if match_norm2 else 0)
+        _check(lib.mrf_llr_set_options(self._h, o))
 
     def subspace_normal(self, plan: "Plan", u, z=None):
         """Coefficients of P_S A^H A (sum_i u_i d_i) for u [r][N][N] on a Toeplitz plan (mrf_llr_subspace_normal)."""

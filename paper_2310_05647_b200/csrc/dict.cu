@@ -64,7 +64,7 @@ static void dict_free(mrf_dict_s* d) {
                   (void*)d->w2f, (void*)d->xp, (void*)d->xs, (void*)d->xnorm, (void*)d->best, (void*)d->thr,
                   (void*)d->ncand, (void*)d->cand, (void*)d->ov, (void*)d->nov, (void*)d->xT, (void*)d->basis,
                   (void*)d->part_best, (void*)d->a64, (void*)d->beta2, (void*)d->u64,
-                  (void*)d->Gd, (void*)d->Dc, (void*)d->dpc, (void*)d->w2c})
+                  (void*)d->Gd, (void*)d->Dc, (void*)d->dpc, (void*)d->w2c, (void*)d->w2f2, (void*)d->w2c2})
     if (p) cudaFree(p);
   delete d;
 }
@@ -121,7 +121,7 @@ static mrf_status build_filter(mrf_dict d) {
   // packed atom rows: 2k = (ar, ai) and 2k+1 = (-ai, ar) per coefficient, scaled by 1/m_k, split
   // into fp16 hi + lo: [hi | hi | lo] against the voxel rows [u_hi | u_lo | u_hi]
   std::vector<__half> dp((size_t)d->NP * dm::KF, __float2half(0.f));
-  std::vector<float> w2((size_t)d->NP / 2, 0.f);
+  std::vector<float> w2((size_t)d->NP / 2, 0.f), w2p((size_t)d->NP / 2, 0.f);
   double bres = 0.0, ba1 = 0.0;
   for (int kk = 0; kk < K; ++kk) {
     if (!(dn2[kk] > 0.0)) continue;   // zero atom: w2 = 0, never listed
@@ -132,6 +132,7 @@ static mrf_status build_filter(mrf_dict d) {
     ba1 = std::max(ba1, a1h[kk] / nd);
     if (!(m > 0.0)) continue;         // no component in the filter space: its score is 0 (+ band)
     w2[kk] = (float)(m * m / dn2[kk]);
+    w2p[kk] = (float)(m * m / (dn2[kk] * dn2[kk]));
     __half* r0 = &dp[(size_t)(2 * kk) * dm::KF];
     __half* r1 = r0 + dm::KF;
     for (int f = 0; f < dm::RF; ++f) {
@@ -170,11 +171,16 @@ static mrf_status build_filter(mrf_dict d) {
   if (cudaMalloc((void**)&d->beta2, (size_t)K * sizeof(double)) != cudaSuccess)
     return fail(MRF_ENOMEM, "mrf_dict_create: filter allocation failed");
   CUDA_TRY(cudaMemcpy(d->beta2, b2.data(), (size_t)K * sizeof(double), cudaMemcpyHostToDevice));
+  d->dmin = 0.0;
+  for (int kk = 0; kk < K; ++kk)
+    if (dn2[kk] > 0.0 && (d->dmin == 0.0 || std::sqrt(dn2[kk]) < d->dmin)) d->dmin = std::sqrt(dn2[kk]);
   if (cudaMalloc((void**)&d->dpf, dp.size() * sizeof(__half)) != cudaSuccess ||
-      cudaMalloc((void**)&d->w2f, w2.size() * sizeof(float)) != cudaSuccess)
+      cudaMalloc((void**)&d->w2f, w2.size() * sizeof(float)) != cudaSuccess ||
+      cudaMalloc((void**)&d->w2f2, w2p.size() * sizeof(float)) != cudaSuccess)
     return fail(MRF_ENOMEM, "mrf_dict_create: filter allocation failed");
   CUDA_TRY(cudaMemcpy(d->dpf, dp.data(), dp.size() * sizeof(__half), cudaMemcpyHostToDevice));
   CUDA_TRY(cudaMemcpy(d->w2f, w2.data(), w2.size() * sizeof(float), cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(d->w2f2, w2p.data(), w2p.size() * sizeof(float), cudaMemcpyHostToDevice));
   return make_tmap(&d->tmdf, d->dpf, (uint64_t)dm::KF, (uint64_t)d->NP, (uint32_t)dm::BN);
 }
 
@@ -314,6 +320,13 @@ static mrf_status check_args(mrf_dict d, const char* who, const void* x, long lo
 extern "C" {
 
 mrf_status mrf_dict_match(mrf_dict d, const void* x, long long V, int* index, float* pd, float* params, void* stream) {
+  return mrf_dict_match_ex(d, x, V, 0u, index, pd, params, stream);
+}
+
+mrf_status mrf_dict_match_ex(mrf_dict d, const void* x, long long V, unsigned flags, int* index, float* pd, float* params,
+                             void* stream) {
+  if (flags & ~MRF_MATCH_NORM2) return fail(MRF_EINVAL, "mrf_dict_match: unknown flags");
+  const int pw = (flags & MRF_MATCH_NORM2) ? 2 : 1;
   MRF_TRY(check_args(d, "mrf_dict_match", x, V, index, pd, params));
   CUDA_TRY(cudaSetDevice(d->device));
   cudaStream_t st = (cudaStream_t)stream;
@@ -330,12 +343,13 @@ mrf_status mrf_dict_match(mrf_dict d, const void* x, long long V, int* index, fl
   dm::k_dict_proj_frames<<<(unsigned)((V + dm::PJV - 1) / dm::PJV), 256, dm::proj_smem(), st>>>(xf, d->phiT, d->L, (int)V, d->xT, d->xp, d->xs,
                                                                      d->xnorm, d->u64);
   MRF_TRY(check_launch("k_dict_proj_frames"));
-  MRF_TRY(filter_passes(d, V, vpad, dm::KF, d->tmdf, d->w2f, d->beta, st));
+  // the printed form's scores |c| / ||d||^2 carry the band beta ||d|| ||x|| / ||d||^2 <= beta ||x|| / dmin
+  MRF_TRY(filter_passes(d, V, vpad, dm::KF, d->tmdf, pw == 2 ? d->w2f2 : d->w2f, pw == 2 ? d->beta / d->dmin : d->beta, st));
   dm::k_dict_rescore_frames<<<(unsigned)((V + 7) / 8), 256, 0, st>>>(d->xT, d->atoms, d->dn2, d->xnorm, d->u64, d->a64,
-                                                                    d->beta2, d->ncand, d->cand, d->lut, d->P, d->L, (int)V,
+                                                                    d->beta2, pw, d->ncand, d->cand, d->lut, d->P, d->L, (int)V,
                                                                     index, pd, params, d->ov, d->nov);
   MRF_TRY(check_launch("k_dict_rescore_frames"));
-  dm::k_dict_exact_frames<<<1184, 256, 0, st>>>(d->xT, d->atoms, d->dn2, d->K, d->L, d->ov, d->nov,
+  dm::k_dict_exact_frames<<<1184, 256, 0, st>>>(d->xT, d->atoms, d->dn2, pw, d->K, d->L, d->ov, d->nov,
                                                 (dm::PartBest*)d->part_best);
   MRF_TRY(check_launch("k_dict_exact_frames"));
   dm::k_dict_exact_finish<<<64, 128, 0, st>>>(d->ov, d->nov, (const dm::PartBest*)d->part_best, d->dn2, d->lut, d->P, index, pd, params);
@@ -344,6 +358,13 @@ mrf_status mrf_dict_match(mrf_dict d, const void* x, long long V, int* index, fl
 
 mrf_status mrf_dict_match_coef(mrf_dict d, const void* u, long long V, int* index, float* pd, float* params,
                                void* stream) {
+  return mrf_dict_match_coef_ex(d, u, V, 0u, index, pd, params, stream);
+}
+
+mrf_status mrf_dict_match_coef_ex(mrf_dict d, const void* u, long long V, unsigned flags, int* index, float* pd,
+                                  float* params, void* stream) {
+  if (flags & ~MRF_MATCH_NORM2) return fail(MRF_EINVAL, "mrf_dict_match_coef: unknown flags");
+  const int pw = (flags & MRF_MATCH_NORM2) ? 2 : 1;
   MRF_TRY(check_args(d, "mrf_dict_match_coef", u, V, index, pd, params));
   if (!d->rank || !d->Dc || !d->dpc) return fail(MRF_EINVAL, "mrf_dict_match_coef: no basis (call mrf_dict_basis)");
   CUDA_TRY(cudaSetDevice(d->device));
@@ -354,12 +375,13 @@ mrf_status mrf_dict_match_coef(mrf_dict d, const void* u, long long V, int* inde
   CUDA_TRY(cudaMemsetAsync(d->xp + (size_t)V * dm::KFC, 0, (size_t)(vpad - V) * dm::KFC * sizeof(__half), st));
   dm::k_dict_proj_coef<<<(unsigned)((V + 127) / 128), 128, 0, st>>>(w, d->rank, (int)V, d->Gd, d->xp, d->xs, d->xnorm);
   MRF_TRY(check_launch("k_dict_proj_coef"));
-  MRF_TRY(filter_passes(d, V, vpad, dm::KFC, d->tmdc, d->w2c, d->beta_c, st));
-  dm::k_dict_rescore_coef<<<(unsigned)((V + 127) / 128), 128, 0, st>>>(w, d->rank, d->Dc, d->dn2, d->xnorm, d->ncand,
+  MRF_TRY(filter_passes(d, V, vpad, dm::KFC, d->tmdc, pw == 2 ? d->w2c2 : d->w2c, pw == 2 ? d->beta_c / d->dmin : d->beta_c,
+                        st));
+  dm::k_dict_rescore_coef<<<(unsigned)((V + 127) / 128), 128, 0, st>>>(w, d->rank, d->Dc, d->dn2, pw, d->xnorm, d->ncand,
                                                                         d->cand, d->lut, d->P, (int)V, index, pd, params,
                                                                         d->ov, d->nov);
   MRF_TRY(check_launch("k_dict_rescore_coef"));
-  dm::k_dict_exact_coef<<<64, 128, 0, st>>>(w, d->rank, d->Dc, d->dn2, d->K, d->lut, d->P, (int)V, d->ov, d->nov, index,
+  dm::k_dict_exact_coef<<<64, 128, 0, st>>>(w, d->rank, d->Dc, d->dn2, pw, d->K, d->lut, d->P, (int)V, d->ov, d->nov, index,
                                             pd, params);
   return check_launch("k_dict_exact_coef");
 }
@@ -437,13 +459,14 @@ static void host_jacobi_eig(int n, std::vector<std::complex<double>>& H, std::ve
 // rounding + worst-case fp32 accumulation of the K = 192 products (no residual: the identity is exact).
 static mrf_status build_coef_dict(mrf_dict d, int r) {
   const int K = d->K, L = d->L;
-  for (void* p : {(void*)d->Gd, (void*)d->Dc, (void*)d->dpc, (void*)d->w2c})
+  for (void* p : {(void*)d->Gd, (void*)d->Dc, (void*)d->dpc, (void*)d->w2c, (void*)d->w2c2})
     if (p) cudaFree(p);
-  d->Gd = nullptr; d->Dc = nullptr; d->dpc = nullptr; d->w2c = nullptr;
+  d->Gd = nullptr; d->Dc = nullptr; d->dpc = nullptr; d->w2c = nullptr; d->w2c2 = nullptr;
   if (cudaMalloc((void**)&d->Dc, (size_t)K * r * sizeof(double2)) != cudaSuccess ||
       cudaMalloc((void**)&d->Gd, (size_t)r * r * sizeof(double2)) != cudaSuccess ||
       cudaMalloc((void**)&d->dpc, (size_t)d->NP * dm::KFC * sizeof(__half)) != cudaSuccess ||
-      cudaMalloc((void**)&d->w2c, (size_t)d->NP / 2 * sizeof(float)) != cudaSuccess)
+      cudaMalloc((void**)&d->w2c, (size_t)d->NP / 2 * sizeof(float)) != cudaSuccess ||
+      cudaMalloc((void**)&d->w2c2, (size_t)d->NP / 2 * sizeof(float)) != cudaSuccess)
     return fail(MRF_ENOMEM, "mrf_dict_basis: allocation failed");
   const dim3 blk(16, 16);
   auto grid = [](int M, int N) { return dim3((unsigned)((N + 15) / 16), (unsigned)((M + 15) / 16)); };
@@ -460,13 +483,14 @@ static mrf_status build_coef_dict(mrf_dict d, int r) {
   std::vector<double> dn2(K);
   CUDA_TRY(cudaMemcpy(dn2.data(), d->dn2, (size_t)K * sizeof(double), cudaMemcpyDeviceToHost));
   std::vector<__half> dp((size_t)d->NP * dm::KFC, __float2half(0.f));
-  std::vector<float> w2((size_t)d->NP / 2, 0.f);
+  std::vector<float> w2((size_t)d->NP / 2, 0.f), w2p((size_t)d->NP / 2, 0.f);
   for (int k = 0; k < K; ++k) {
     if (!(dn2[k] > 0.0)) continue;
     double m = 0.0;
     for (int i = 0; i < r; ++i) m = std::max({m, std::fabs(dc[(size_t)k * r + i].x), std::fabs(dc[(size_t)k * r + i].y)});
     if (!(m > 0.0)) continue;
     w2[k] = (float)(m * m / dn2[k]);
+    w2p[k] = (float)(m * m / (dn2[k] * dn2[k]));
     __half* r0 = &dp[(size_t)(2 * k) * dm::KFC];
     __half* r1 = r0 + dm::KFC;
     for (int i = 0; i < r; ++i) {
@@ -489,6 +513,7 @@ static mrf_status build_coef_dict(mrf_dict d, int r) {
   d->beta_c = 1.05 * std::sqrt(2.0) * ((3.0 * u16 * u16 + g192) * 1.001 + std::ldexp(1.0, -25) * 8.0 * 2.0) + 1e-6;
   CUDA_TRY(cudaMemcpy(d->dpc, dp.data(), dp.size() * sizeof(__half), cudaMemcpyHostToDevice));
   CUDA_TRY(cudaMemcpy(d->w2c, w2.data(), w2.size() * sizeof(float), cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(d->w2c2, w2p.data(), w2p.size() * sizeof(float), cudaMemcpyHostToDevice));
   return tmap_2d(&d->tmdc, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, d->dpc, (uint64_t)dm::KFC, (uint64_t)d->NP,
                  (uint64_t)dm::KFC * sizeof(__half), (uint32_t)dm::BK, (uint32_t)dm::BN);
 }

@@ -22,7 +22,9 @@ struct mrf_dict_s {
   float2* phi = nullptr;         // [64][L] (rows past Rf zero)
   float2* phiT = nullptr;        // [L][64]
   __half* dpf = nullptr;         // [NP][KF]
-  float* w2f = nullptr;          // [NP / 2]
+  float* w2f = nullptr;          // [NP / 2] (m_k / ||d_k||)^2 (normalised correlation, reading 21)
+  float* w2f2 = nullptr;         // [NP / 2] (m_k / ||d_k||^2)^2 (Eq. 5 as printed, MRF_MATCH_NORM2)
+  double dmin = 0.0;             // smallest non-zero atom norm (the printed form's band)
   CUtensorMap tmdf;
   double beta = 0.0;             // |rho~_k - rho_k| <= beta for every atom and voxel (the GEMM filter)
   double2* a64 = nullptr;        // [K][64] a_k = phi d_k (float64; the rescoring's second level)
@@ -57,6 +59,7 @@ struct mrf_dict_s {
   double2* Dc = nullptr;
   __half* dpc = nullptr;         // [NP][KFC] packed [Dc_hi | Dc_hi | Dc_lo] / m'_k rows (the coefficient filter)
   float* w2c = nullptr;          // [NP / 2] (m'_k / ||d_k||)^2
+  float* w2c2 = nullptr;         // [NP / 2] (m'_k / ||d_k||^2)^2
   CUtensorMap tmdc;
   double beta_c = 0.0;           // the coefficient filter's bound on |rho~_k - rho_k|
   // last match: voxels rescored against every atom (diagnostics)

@@ -31,6 +31,7 @@ struct mrf_llr_s {
   // hook; the coefficient partials are all-reduced through it), else nullptr
   int frame0 = 0, Lg = 0;
   mrf_plan comm = nullptr;
+  unsigned opts = 0;   // mrf_llr_set_options: printed-form switches (readings 21, 25, 26)
   float2* dT = nullptr;       // [L][R] transposed basis, rows zero-padded to R = 16 or 32
   int* corners = nullptr;     // [nc]
   float2* Y = nullptr;        // [N*N][r] coefficients of Z
@@ -382,7 +383,7 @@ mrf_status mrf_llr_laplacian(mrf_llr h, const float* params, const float* pd, do
   CUDA_TRY(cudaMemsetAsync(pdmax, 0, sizeof(unsigned), st));
   mfd::k_mfd_max<<<kStatBlocks, 256, 0, st>>>(pd, V, pdmax);
   mfd::k_mfd_stats<<<kStatBlocks, 256, 0, st>>>(params, pd, V, pdmax, h->stats);
-  mfd::k_mfd_stats_final<<<1, 256, 0, st>>>(h->stats, kStatBlocks, sel);
+  mfd::k_mfd_stats_final<<<1, 256, 0, st>>>(h->stats, kStatBlocks, sel, (h->opts & MRF_LLR_RAW_MAPS) ? 1 : 0);
   MRF_TRY(check_launch("k_mfd_stats"));
   mfd::k_mfd_patchvec<<<n, 128, 0, st>>>(params, pd, sel, h->corners, h->nc, h->N, h->p, h->pv);
   const dim3 gd((unsigned)((n + 127) / 128), (unsigned)((n + 127) / 128));
@@ -481,13 +482,14 @@ static mrf_status step_impl(mrf_llr h, mrf_plan plan, const void* x, const void*
   }
   MRF_TRY(svt(h, h->Y, 1.f / beta, st));
   const float gamma = mu * lambda2 * beta;
+  const int lit = (h->opts & MRF_LLR_LITERAL_EQ23) ? 1 : 0;
   const unsigned gv = (unsigned)((V + 31) / 32);
   if (h->r <= 16)
     llr::k_llr_update<16><<<gv, 256, 0, st>>>(h->Y, h->P, h->corners, h->nc, h->N, h->p, h->r, h->dT, h->L, gamma,
-                                              (float2*)x_out, h->xcv, h->xcr);
+                                              (float2*)x_out, h->xcv, h->xcr, lit);
   else
     llr::k_llr_update<32><<<gv, 256, 0, st>>>(h->Y, h->P, h->corners, h->nc, h->N, h->p, h->r, h->dT, h->L, gamma,
-                                              (float2*)x_out, h->xcv, h->xcr);
+                                              (float2*)x_out, h->xcv, h->xcr, lit);
   MRF_TRY(check_launch("k_llr_update"));
   h->q_fresh = false;   // the coefficients moved on
   // Tr(Q(P_S x) L Q(P_S x)^H) and sum_q ||Q_q(Z)||_*: patches summed in a fixed order (synchronise)
@@ -590,7 +592,7 @@ static mrf_status sub_step(mrf_llr_s* h, float mu, float lambda1, float lambda2,
   MRF_TRY(svt(h, h->Y, 1.f / beta, st));
   const float gamma = mu * lambda2 * beta;
   llr::k_llr_update_coef<<<(unsigned)(((long long)V * h->r + 255) / 256), 256, 0, st>>>(
-      h->Y, h->P, h->corners, h->nc, h->N, h->p, h->r, gamma, h->xcv, h->xcr);
+      h->Y, h->P, h->corners, h->nc, h->N, h->p, h->r, gamma, h->xcv, h->xcr, (h->opts & MRF_LLR_LITERAL_EQ23) ? 1 : 0);
   h->q_fresh = false;   // the coefficients moved on
   return check_launch("k_llr_update_coef");
 }
@@ -721,8 +723,9 @@ mrf_status mrf_msllr_solve(mrf_llr h, mrf_dict dict, mrf_plan plan, const void* 
   }
   bool have_coef = false;
   auto maps = [&](const void* cur, void* ms) -> mrf_status {
-    if (have_coef && coef_ok) return mrf_dict_match_coef(dict, h->xcr, V, index, pd, params, ms);
-    return mrf_dict_match(dict, cur, V, index, pd, params, ms);
+    const unsigned mf = (h->opts & MRF_LLR_MATCH_NORM2) ? MRF_MATCH_NORM2 : 0u;
+    if (have_coef && coef_ok) return mrf_dict_match_coef_ex(dict, h->xcr, V, mf, index, pd, params, ms);
+    return mrf_dict_match_ex(dict, cur, V, mf, index, pd, params, ms);
   };
   auto update_maps = [&](const void* cur, void* ms) -> mrf_status {
     MRF_TRY(maps(cur, ms));
@@ -808,10 +811,10 @@ mrf_status mrf_msllr_solve(mrf_llr h, mrf_dict dict, mrf_plan plan, const void* 
     const unsigned gv = (unsigned)((V + 31) / 32);
     if (h->r <= 16)
       llr::k_llr_update<16><<<gv, 256, 0, st>>>(h->xcv, h->P, h->corners, h->nc, h->N, h->p, h->r, h->dT, h->L, 0.f,
-                                                (float2*)x, nullptr, nullptr);
+                                                (float2*)x, nullptr, nullptr, 0);
     else
       llr::k_llr_update<32><<<gv, 256, 0, st>>>(h->xcv, h->P, h->corners, h->nc, h->N, h->p, h->r, h->dT, h->L, 0.f,
-                                                (float2*)x, nullptr, nullptr);
+                                                (float2*)x, nullptr, nullptr, 0);
     MRF_TRY(check_launch("k_llr_update"));
   } else if (cur != x) {
     CUDA_TRY(cudaMemcpyAsync(x, cur, xbytes, cudaMemcpyDeviceToDevice, st));
@@ -836,6 +839,14 @@ mrf_status mrf_llr_subspace_normal(mrf_llr h, mrf_plan plan, const void* u, void
   cudaStream_t st = (cudaStream_t)stream;
   MRF_TRY(ensure_sn(h, plan, st, false));
   return sn_apply(plan, h->Ksn, h->r, (const float2*)u, (float2*)z, h->spa, h->spb, st);
+}
+
+mrf_status mrf_llr_set_options(mrf_llr h, unsigned options) {
+  if (!h) return fail(MRF_EINVAL, "mrf_llr_set_options: null operator");
+  if (options & ~(MRF_LLR_LITERAL_EQ23 | MRF_LLR_RAW_MAPS | MRF_LLR_MATCH_NORM2))
+    return fail(MRF_EINVAL, "mrf_llr_set_options: unknown options");
+  h->opts = options;
+  return MRF_OK;
 }
 
 mrf_status mrf_llr_destroy(mrf_llr h) {

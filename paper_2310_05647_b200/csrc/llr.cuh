@@ -320,7 +320,7 @@ __global__ void __launch_bounds__(256) k_llr_update(const float2* __restrict__ Y
                                                     const int* __restrict__ corners, int nc, int N, int p, int r,
                                                     const float2* __restrict__ dT, int L, float gamma,
                                                     float2* __restrict__ xout, float2* __restrict__ xcv,
-                                                    float2* __restrict__ xcr) {
+                                                    float2* __restrict__ xcr, int lit) {
   // xcv [V][r] / xcr [r][V] (nullable): the coefficients Xc of x+ in both layouts (x+ = Xc d
   // lies in span(d): the next step's manifold term, the cost and Phi_D read them instead of x+)
   __shared__ float2 xcs[R][33];
@@ -351,7 +351,7 @@ __global__ void __launch_bounds__(256) k_llr_update(const float2* __restrict__ Y
           ++cnt;
         }
       }
-      const float inv = 1.f / (1.f + gamma * (float)cnt);
+      const float inv = 1.f / (1.f + gamma * (lit ? 1.f : (float)cnt));   // lit: Eq. (23) as printed
 #pragma unroll
       for (int i = 0; i < R; ++i)
         if (i < r) {
@@ -394,7 +394,7 @@ static __global__ void __launch_bounds__(256) k_llr_update_coef(const float2* __
                                                                 const float2* __restrict__ P,
                                                                 const int* __restrict__ corners, int nc, int N, int p,
                                                                 int r, float gamma, float2* __restrict__ xcv,
-                                                                float2* __restrict__ xcr) {
+                                                                float2* __restrict__ xcr, int lit) {
   const int V = N * N;
   const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (t >= (long long)V * r) return;
@@ -414,7 +414,7 @@ static __global__ void __launch_bounds__(256) k_llr_update_coef(const float2* __
       ++cnt;
     }
   }
-  const float inv = 1.f / (1.f + gamma * (float)cnt);
+  const float inv = 1.f / (1.f + gamma * (lit ? 1.f : (float)cnt));   // lit: Eq. (23) as printed
   const float2 y = __ldg(Y + t);
   const float2 xc = make_float2((y.x + gamma * acc.x) * inv, (y.y + gamma * acc.y) * inv);
   xcv[t] = xc;
@@ -561,7 +561,8 @@ struct LapSel {
 
 // ms from the per-block partials of k_mfd_stats: each of the 7 sums is reduced by 32 lanes of one
 // warp (fixed strided partial sums, then a fixed xor tree: deterministic), one warp per sum
-static __global__ void k_mfd_stats_final(const double* __restrict__ part, int nblk, LapSel* __restrict__ sel) {
+// raw != 0: Eq. (8) on the raw maps (mean 0, std 1 recorded: the patch vectors are the raw values)
+static __global__ void k_mfd_stats_final(const double* __restrict__ part, int nblk, LapSel* __restrict__ sel, int raw) {
   __shared__ double a[8];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (w < 7) {
@@ -575,8 +576,8 @@ static __global__ void k_mfd_stats_final(const double* __restrict__ part, int nb
     const int c = threadIdx.x;
     const double cnt = a[6] > 0.0 ? a[6] : 1.0;
     const double mean = a[2 * c] / cnt, var = fmax(a[2 * c + 1] / cnt - mean * mean, 0.0);
-    sel->ms[2 * c] = mean;
-    sel->ms[2 * c + 1] = var > 0.0 ? sqrt(var) : 1.0;
+    sel->ms[2 * c] = raw ? 0.0 : mean;
+    sel->ms[2 * c + 1] = raw ? 1.0 : (var > 0.0 ? sqrt(var) : 1.0);
   }
   if (threadIdx.x == 0) {
     sel->count = a[6];

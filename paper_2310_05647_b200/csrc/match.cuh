@@ -460,7 +460,7 @@ __device__ __forceinline__ double2 warp_dot_frames(const float2* __restrict__ dk
 __global__ void __launch_bounds__(256) k_dict_rescore_frames(const float2* __restrict__ xT, const float2* __restrict__ atoms,
                                                              const double* __restrict__ dn2, const double* __restrict__ xnorm,
                                                              const double2* __restrict__ u64, const double2* __restrict__ a64,
-                                                             const double* __restrict__ beta2,
+                                                             const double* __restrict__ beta2, int pw,
                                                              const int* __restrict__ ncand, const int* __restrict__ cand,
                                                              const float* __restrict__ lut, int P, int L, int V,
                                                              int* __restrict__ index, float* __restrict__ pd,
@@ -501,7 +501,9 @@ __global__ void __launch_bounds__(256) k_dict_rescore_frames(const float2* __res
         sr += a.x * u.x + a.y * u.y;
         si += a.x * u.y - a.y * u.x;
       }
-      const double rho = sqrt(sr * sr + si * si) / (sqrt(dn2[k]) * xn), bk = beta2[k];
+      // pw = 2 (Eq. 5 as printed): score |c| / ||d||^2 = rho / ||d||, bound beta2 / ||d||
+      const double nd = sqrt(dn2[k]), sc = pw == 2 ? nd : 1.0;
+      const double rho = sqrt(sr * sr + si * si) / (nd * xn) / sc, bk = beta2[k] / sc;
       kr[rd] = k;
       hr[rd] = rho + bk;
       m = fmax(m, rho - bk);
@@ -519,7 +521,7 @@ __global__ void __launch_bounds__(256) k_dict_rescore_frames(const float2* __res
       keep &= keep - 1;
       const int ki = __shfl_sync(0xffffffffu, kr[rd], i);
       const double2 c = warp_dot_frames(atoms + (size_t)ki * L, xv, L, lane);
-      best_update(b, (c.x * c.x + c.y * c.y) / dn2[ki], ki, c.x);
+      best_update(b, (c.x * c.x + c.y * c.y) / (pw == 2 ? dn2[ki] * dn2[ki] : dn2[ki]), ki, c.x);
     }
   }
   if (lane == 0) finish_voxel(v, b, dn2, lut, P, index, pd, params);
@@ -533,7 +535,7 @@ struct PartBest {
   int k, pad;
 };
 __global__ void __launch_bounds__(256) k_dict_exact_frames(const float2* __restrict__ xT, const float2* __restrict__ atoms,
-                                                           const double* __restrict__ dn2, int K, int L,
+                                                           const double* __restrict__ dn2, int pw, int K, int L,
                                                            const int* __restrict__ ov, const int* __restrict__ nov,
                                                            PartBest* __restrict__ part_best) {
   __shared__ Best wb[8];
@@ -546,7 +548,7 @@ __global__ void __launch_bounds__(256) k_dict_exact_frames(const float2* __restr
     for (int k = k0 + w; k < k1; k += 8) {
       if (!(dn2[k] > 0.0)) continue;   // an all-zero atom is never matched
       const double2 c = warp_dot_frames(atoms + (size_t)k * L, xT + (size_t)v * L, L, lane);
-      best_update(b, (c.x * c.x + c.y * c.y) / dn2[k], k, c.x);
+      best_update(b, (c.x * c.x + c.y * c.y) / (pw == 2 ? dn2[k] * dn2[k] : dn2[k]), k, c.x);
     }
     if (lane == 0) wb[w] = b;
     __syncthreads();
@@ -588,7 +590,7 @@ __device__ __forceinline__ double2 dot_coef(const double2* __restrict__ dck, con
 }
 
 __global__ void __launch_bounds__(128) k_dict_rescore_coef(const float2* __restrict__ w, int r, const double2* __restrict__ Dc,
-                                                           const double* __restrict__ dn2, const double* __restrict__ xnorm,
+                                                           const double* __restrict__ dn2, int pw, const double* __restrict__ xnorm,
                                                            const int* __restrict__ ncand, const int* __restrict__ cand,
                                                            const float* __restrict__ lut, int P, int V,
                                                            int* __restrict__ index, float* __restrict__ pd,
@@ -613,13 +615,13 @@ __global__ void __launch_bounds__(128) k_dict_rescore_coef(const float2* __restr
   for (int i = 0; i < n; ++i) {
     const int k = cand[(size_t)v * kCand + i];
     const double2 c = dot_coef(Dc + (size_t)k * r, wv, r);
-    best_update(b, (c.x * c.x + c.y * c.y) / dn2[k], k, c.x);
+    best_update(b, (c.x * c.x + c.y * c.y) / (pw == 2 ? dn2[k] * dn2[k] : dn2[k]), k, c.x);
   }
   finish_voxel(v, b, dn2, lut, P, index, pd, params);
 }
 
 __global__ void __launch_bounds__(128) k_dict_exact_coef(const float2* __restrict__ w, int r, const double2* __restrict__ Dc,
-                                                         const double* __restrict__ dn2, int K, const float* __restrict__ lut,
+                                                         const double* __restrict__ dn2, int pw, int K, const float* __restrict__ lut,
                                                          int P, int V, const int* __restrict__ ov, const int* __restrict__ nov,
                                                          int* __restrict__ index, float* __restrict__ pd,
                                                          float* __restrict__ params) {
@@ -633,7 +635,7 @@ __global__ void __launch_bounds__(128) k_dict_exact_coef(const float2* __restric
     for (int k = 0; k < K; ++k) {
       if (!(dn2[k] > 0.0)) continue;
       const double2 c = dot_coef(Dc + (size_t)k * r, wv, r);
-      best_update(b, (c.x * c.x + c.y * c.y) / dn2[k], k, c.x);
+      best_update(b, (c.x * c.x + c.y * c.y) / (pw == 2 ? dn2[k] * dn2[k] : dn2[k]), k, c.x);
     }
     finish_voxel(v, b, dn2, lut, P, index, pd, params);
   }

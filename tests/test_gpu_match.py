@@ -3,7 +3,7 @@ oracle's argmax for every checked voxel (Eq. (5), reading 21; tie
 
 The GPU path (match.cuh) is a certified tensor-core filter plus exact float64 rescoring of every
 atom inside the filter's error band, with a full exact scan for voxels whose band holds more than
-32 atoms; pd = max(Re<d_k,x>/||d_k||^2, 0) comes from the exact correlation of the chosen atom.
+128 atoms; pd = max(Re<d_k,x>/||d_k||^2, 0) comes from the exact correlation of the chosen atom.
 Inputs: noisy voxel fingerprints (many near-ties: neighbouring atoms correlate to 0.999998) and
 rank-5 phantom time series (the CG solution's kind of voxels), on the paper's 3336-atom grid.
 """
@@ -159,4 +159,30 @@ def test_match_in_basis_coordinates_is_exact(binding):
     assert np.array_equal(qc.cpu().numpy(), grid[k].astype(np.float32))
     ix, px, qx = dic.match(torch.from_numpy(np.ascontiguousarray(x.T.astype(np.complex64))).cuda())
     assert np.mean(ix.cpu().numpy() == ic) > 0.99                # x rounded to complex64 for the frame match
+    dic.close()
+
+
+def test_printed_eq5_norm2_is_exact(binding):
+    """MRF_MATCH_NORM2 (Eq. 5 as printed, argmax |<d,x>| / ||d||^2; reading 21 uses ||d||): the index
+    equals the oracle's p = 2 argmax, frames and basis coordinates."""
+    L = 300
+    g = sd.t1t2_grid()[::7]
+    D = sd.surrogate_dictionary(L, g)
+    X, _, _ = sd.voxel_fingerprints(D, 1500, noise=0.02)
+    dic = binding.Dictionary(D, g.astype(np.float32))
+    x = torch.from_numpy(np.ascontiguousarray(X.T.astype(np.complex64))).cuda()
+    idx, pd, _ = dic.match(x, norm2=True)
+    Xq = X.astype(np.complex64).astype(np.complex128)
+    Dq = D.astype(np.complex64).astype(np.complex128)
+    k2, _, rho2, _ = om.match(Xq, Dq, p=2)
+    k1, _, _, _ = om.match(Xq, Dq, p=1)
+    assert np.array_equal(idx.cpu().numpy(), k2) and not np.array_equal(k1, k2)
+    assert np.allclose(pd.cpu().numpy(), rho2, rtol=PD_RTOL, atol=PD_RTOL * rho2.max())
+    d = dic.basis(0.9999, 32)
+    u = (X @ np.conj(d).T).astype(np.complex64)
+    xs = u.astype(np.complex128) @ d.astype(np.complex128)
+    ic, _, _ = dic.match_coef(torch.from_numpy(np.ascontiguousarray(u.T)).cuda(), norm2=True)
+    c = xs @ np.conj(Dq).T
+    kc = np.argmax(np.abs(c) / np.sum(np.abs(Dq) ** 2, axis=1)[None, :], axis=1)
+    assert np.array_equal(ic.cpu().numpy(), kc)
     dic.close()

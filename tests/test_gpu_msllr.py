@@ -364,3 +364,25 @@ def test_sharded_solve_through_a_single_rank_communicator(binding, problem):
             o.close()
     finally:
         binding.nccl_comm_destroy(comm)
+
+
+def test_printed_form_switches_against_the_oracle(binding, problem1):
+    """Algorithm 1 with every printed-form switch on (mrf_llr_set_options): Eq. (23)'s scalar
+    denominator, Eq. (8) on raw maps, Eq. (5)'s ||d||^2 in Phi_D -- against the oracle's loop with
+    literal_update, raw_maps, match_p = 2; and the switched loop differs from the default one."""
+    pr = problem1
+    lam1, lam2, beta, iters = 2e-3, 0.05, 0.5, 2
+    ref = oms.solve(pr["b"], pr["traj"], pr["D"], pr["lut"], pr["d"], pr["mu"], lam1, lam2, beta, iters, tol=0.0,
+                    W=W, N=N, p=P, s=S, literal_update=True, raw_maps=True, match_p=2)
+    dic, op, pl, b = _gpu(binding, pr)
+    op.set_options(literal_eq23=True, raw_maps=True, match_norm2=True)
+    out = op.solve(dic, pl, b, mu=pr["mu"], lam1=lam1, lam2=lam2, beta=beta, max_iter=iters, tol=0.0)
+    torch.cuda.synchronize()
+    assert _rel(out["x"].cpu().numpy(), ref["x"]) <= 1e-4
+    assert np.allclose(out["cost"], ref["cost"], rtol=1e-4, atol=0)
+    assert abs(out["lambda1"] - ref["lambda1"]) <= 1e-4 * ref["lambda1"]
+    op.set_options()
+    dflt = op.solve(dic, pl, b, mu=pr["mu"], lam1=lam1, lam2=lam2, beta=beta, max_iter=iters, tol=0.0)
+    assert _rel(dflt["x"].cpu().numpy(), ref["x"]) > 1e-3
+    assert binding.lib.mrf_llr_set_options(op._h, 8) == 1          # unknown option: MRF_EINVAL
+    pl.close(), op.close(), dic.close()

@@ -97,3 +97,28 @@ def test_step_without_regularisation_is_the_projected_gradient():
     Xn, Z = llr.llr_step(X, rhs, normal, d, mu=1.0, lam2=0.0, beta=0.2)
     assert np.allclose(Z, llr.project(X - (0.5 * X - rhs), d), atol=1e-12)
     assert np.allclose(Xn, Z, atol=1e-12)
+
+
+def test_literal_eq23_update():
+    """The printed Eq. (23) update X = (Z + g Q*(P)) / (1 + g): equal to the
+    overlap-exact reading 25 when the patches do not overlap (stride = patch size: every voxel is
+    covered once), and on an overlapping tiling equal to the formula written out by hand for a
+    voxel covered by several patches."""
+    rng = np.random.default_rng(9)
+    L, N, p = 6, 8, 4
+    Z = rand_c(rng, L, N, N)
+    g = 0.7
+    a, _ = llr.llr_prox(Z, 0.3, g, p, p, literal=True)
+    b, _ = llr.llr_prox(Z, 0.3, g, p, p, literal=False)
+    assert np.allclose(a, b, rtol=0, atol=1e-12)
+    # overlapping (stride 2): voxel (3, 3) lies in the patches with corners {0, 2} x {0, 2}
+    lit, _ = llr.llr_prox(Z, 0.3, g, p, 2, literal=True)
+    exact, _ = llr.llr_prox(Z, 0.3, g, p, 2, literal=False)
+    acc = np.zeros(L, complex)
+    for y0 in (0, 2):
+        for x0 in (0, 2):
+            P = llr.svt(llr.casorati(Z, y0, x0, p), 0.3)
+            acc += P[(3 - y0) * p + (3 - x0)]
+    assert np.allclose(lit[:, 3, 3], (Z[:, 3, 3] + g * acc) / (1 + g), atol=1e-12)
+    assert np.allclose(exact[:, 3, 3], (Z[:, 3, 3] + g * acc) / (1 + 4 * g), atol=1e-12)
+    assert not np.allclose(lit, exact)

@@ -82,3 +82,27 @@ def test_trace_form_equals_half_the_ordered_pair_sum():
     t = 1e-6
     num = (om.penalty(X + t * E, Lp, N, p, s) - om.penalty(X - t * E, Lp, N, p, s)) / (2 * t)
     assert np.isclose(num, 2 * np.real(np.vdot(om.gradient(X, Lp, N, p, s), E)), rtol=1e-6)
+
+
+def test_raw_map_weights_printed_eq8():
+    """Eq. (8) on the raw maps (reading 26 standardises them first): the weights
+    equal an explicit loop over patch pairs of the raw (T1, T2, PD) values with the same median
+    bandwidth, and equal the standardised weights when the maps are already standardised."""
+    import synth.dictionary as sd
+    N, p, s = 16, 5, 3
+    maps = sd.parameter_maps(N)
+    W, s2 = om.weights(maps, N, p, s, raw=True)
+    P = om.patches(N, p, s)
+    vec = [np.concatenate([maps[c][y0:y0 + p, x0:x0 + p].ravel() for c in range(3)]) for (y0, x0) in P]
+    n = len(vec)
+    d2 = np.array([[np.sum((vec[i] - vec[j]) ** 2) for j in range(n)] for i in range(n)])
+    nz = d2[np.triu_indices(n, 1)]
+    nz = nz[nz > 0]
+    assert np.isclose(s2, np.median(nz), rtol=1e-12)
+    ref = np.exp(-d2 / s2)
+    np.fill_diagonal(ref, 0.0)
+    assert np.allclose(W, ref, rtol=1e-12, atol=1e-15)
+    st = om.standardise(maps)
+    Ws, _ = om.weights(st, N, p, s, raw=True)
+    Wr, _ = om.weights(maps, N, p, s, raw=False)
+    assert np.allclose(Ws, Wr, atol=1e-12)
