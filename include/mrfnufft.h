@@ -169,6 +169,14 @@ const char* mrf_last_error(void);
 /* Bytes of device memory the plan owns (tables, coils, workspaces, CG vectors). */
 size_t mrf_plan_device_bytes(mrf_plan plan);
 
+/* Test hook (stage-wise parity): copies the half-grid workspace of the plan's first
+ * batch lane into dst (host or device, `bytes` = batch_frames * C * N * G * 8, else MRF_EINVAL) after
+ * synchronising the device.  After mrf_forward on a one-batch plan it holds the row-FFT'd padded
+ * image, strip-major [frame * C + c][G/16][N][16] (image row iy, grid column 16 s + j); after
+ * mrf_adjoint the column-iFFT'd spread grid at the N kept rows, row-major [frame * C + c][N][G].
+ * Not part of the computation's API: nothing reads it back. */
+mrf_status mrf_plan_debug_halfgrid(mrf_plan plan, void* dst, size_t bytes);
+
 /* ---- per-kernel timing (CUDA events on the launching stream) ----------------------------- */
 /* Kernel classes for mrf_profile_query. */
 #define MRF_K_FWD_ROWS      0   /* deapod . coil . pad . row FFT                                */

@@ -38,7 +38,7 @@ EXPORTED = [
     "mrf_llr_step", "mrf_llr_destroy", "mrf_llr_laplacian", "mrf_llr_cost", "mrf_msllr_solve", "mrf_plan_wait",
     "mrf_dict_match_coef", "mrf_llr_create_basis", "mrf_llr_subspace_normal", "mrf_llr_create_shard",
     "mrf_plan_set_host_allreduce", "mrf_plan_set_precond_shift", "mrf_dict_overflow", "mrf_dict_filter_info",
-    "mrf_dict_match_ex", "mrf_dict_match_coef_ex", "mrf_llr_set_options",
+    "mrf_dict_match_ex", "mrf_dict_match_coef_ex", "mrf_llr_set_options", "mrf_plan_debug_halfgrid",
 ]
 MRF_MATCH_NORM2 = 1
 MRF_LLR_LITERAL_EQ23, MRF_LLR_RAW_MAPS, MRF_LLR_MATCH_NORM2 = 1, 2, 4
@@ -116,6 +116,7 @@ def _load() -> ctypes.CDLL:
         "mrf_dict_match_ex": ([vp, vp, ctypes.c_longlong, ctypes.c_uint, vp, vp, vp, vp], ci),
         "mrf_dict_match_coef_ex": ([vp, vp, ctypes.c_longlong, ctypes.c_uint, vp, vp, vp, vp], ci),
         "mrf_llr_set_options": ([vp, ctypes.c_uint], ci),
+        "mrf_plan_debug_halfgrid": ([vp, vp, ctypes.c_size_t], ci),
         "mrf_dict_destroy": ([vp], ci),
         "mrf_dict_overflow": ([vp, ctypes.POINTER(ci)], ci),
         "mrf_dict_filter_info": ([vp, ctypes.POINTER(ci), ctypes.POINTER(ctypes.c_double),
@@ -339,6 +340,13 @@ class Plan:
 
         self._host_ar = HOST_ALLREDUCE_FN(tramp)   # keep the trampoline alive with the plan
         _check(lib.mrf_plan_set_host_allreduce(self._h, self._host_ar, None))
+
+    def debug_halfgrid(self, frames: int) -> np.ndarray:
+        """The first lane's half-grid workspace (mrf_plan_debug_halfgrid; test hook), `frames` =
+        the plan's batch size: complex64 [frames * C * N * G]."""
+        out = np.empty(frames * self.C * self.N * int(round(self.sigma * self.N)), dtype=np.complex64)
+        _check(lib.mrf_plan_debug_halfgrid(self._h, out.ctypes.data_as(ctypes.c_void_p), out.nbytes))
+        return out
 
     def wait(self):
         """Waits for the result copies of async_host solves (mrf_plan_wait)."""

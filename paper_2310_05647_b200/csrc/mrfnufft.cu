@@ -1758,6 +1758,16 @@ mrf_status mrf_profile_query(mrf_plan pl, int cls, double* total_ms, long long* 
   return MRF_OK;
 }
 
+mrf_status mrf_plan_debug_halfgrid(mrf_plan pl, void* dst, size_t bytes) {
+  if (!pl || !dst) return fail(MRF_EINVAL, "null plan/dst");
+  const size_t need = (size_t)pl->bf * pl->C * pl->N * pl->G * sizeof(float2);
+  if (bytes != need) return fail(MRF_EINVAL, "bytes must be batch_frames * C * N * G * 8");
+  DeviceGuard guard(pl->device);
+  CUDA_TRY(cudaDeviceSynchronize());
+  CUDA_TRY(cudaMemcpy(dst, pl->Hs[0], need, cudaMemcpyDefault));
+  return MRF_OK;
+}
+
 mrf_status mrf_plan_set_precond_shift(mrf_plan pl, double shift) {
   if (!pl) return fail(MRF_EINVAL, "null plan");
   if (!(shift >= 0.0) || !std::isfinite(shift)) return fail(MRF_EINVAL, "shift must be finite and >= 0");

@@ -562,3 +562,30 @@ def test_cg_async_host_pipeline(mrf):
     with pytest.raises(mrf.MrfError):
         pl.dc_cg(dev(ys[0]), mu=cfg.mu, n_iter=2, zero_init=True, async_host=True)
     pl.close()
+
+
+# ------------------------------------------------------------------------ stage-wise parity
+@pytest.mark.parametrize("name,over", [("pr1", {}), ("sense", {"N": 64, "M": 700, "R": 4})])
+def test_stagewise_half_grids(mrf, name, over):
+    """Stage-wise parity: the half grid between the row and the column pass, against
+    the oracle's own stages (oracle.nufft grid_*_frame(stages=True)).  Forward: the row FFT of the
+    deapodised, coil-weighted, zero-padded image (image row iy, all G columns); adjoint: the spread
+    grid after the column inverse DFT at the N kept rows."""
+    cfg, traj, coils, frames, x = setup(name, frames=range(3), **over)
+    fil = synth.frame_interleaf(frames, cfg.R)
+    L, N, G, C = len(frames), cfg.N, cfg.G, cfg.C
+    pl = plan_for(mrf, cfg, traj, coils, frames, batch_frames=L)
+    gp = on.GridParams(N, cfg.W)
+    pl.forward(dev(x))
+    Hf = pl.debug_halfgrid(L).reshape(L * C, G // 16, N, 16).transpose(0, 2, 1, 3).reshape(L, C, N, G)
+    yr = synth.random_kspace(C, cfg.M, frames, cfg.seed).astype(np.complex64)
+    pl.adjoint(dev(yr))
+    Ha = pl.debug_halfgrid(L).reshape(L, C, N, G)
+    for l in range(L):
+        k = traj[fil[l]]
+        _, st = on.grid_forward_frame(x[l], coils, k, gp, stages=True)
+        assert rel(Hf[l], st["half"]) <= OP_TOL
+        _, sa = on.grid_adjoint_frame(yr[l], coils, k, gp, stages=True)
+        col = np.fft.ifft(sa["spread"], axis=1, norm="forward")[:, gp.idx, :]   # columns only, kept rows
+        assert rel(Ha[l], col) <= OP_TOL
+    pl.close()
