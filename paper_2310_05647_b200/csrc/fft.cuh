@@ -39,19 +39,68 @@ struct Tw {
   static constexpr double s = c_sin(ang);
 };
 
-__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
-__device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
+// ---- complex arithmetic on the packed FP32x2 pipe (sm_100: FADD2 / FMUL2 / FFMA2) -------------
+// One instruction operates on both halves of a 64-bit register pair, so a complex addition is one
+// instruction instead of two, a complex multiplication two instead of four, and the folded twiddle
+// butterfly three instead of six.  ptxas folds the operand swaps / partial negations / scalar
+// broadcasts written below into the instruction's operand modifiers (.F32x2.LO_HI.NP, .F32), so the
+// pk() shuffles cost nothing.  Each half is an IEEE fp32 add / mul / fma, exactly as the scalar
+// forms.
+typedef unsigned long long f32x2_t;
+__device__ __forceinline__ f32x2_t pk(float x, float y) {
+  f32x2_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(x), "f"(y));
+  return r;
+}
+__device__ __forceinline__ f32x2_t pk(float2 a) { return pk(a.x, a.y); }
+__device__ __forceinline__ float2 upk(f32x2_t r) {
+  float2 a;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a.x), "=f"(a.y) : "l"(r));
+  return a;
+}
+__device__ __forceinline__ f32x2_t add2(f32x2_t a, f32x2_t b) {
+  f32x2_t d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ f32x2_t sub2(f32x2_t a, f32x2_t b) {
+  f32x2_t d;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ f32x2_t mul2(f32x2_t a, f32x2_t b) {
+  f32x2_t d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ f32x2_t fma2(f32x2_t a, f32x2_t b, f32x2_t c) {   // a * b + c per half
+  f32x2_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return upk(add2(pk(a), pk(b))); }
+__device__ __forceinline__ float2 csub(float2 a, float2 b) { return upk(sub2(pk(a), pk(b))); }
+// a * b = b a.x + (-b.y, b.x) a.y
 __device__ __forceinline__ float2 cmul(float2 a, float2 b) {
-  return make_float2(fmaf(a.x, b.x, -a.y * b.y), fmaf(a.x, b.y, a.y * b.x));
+  return upk(fma2(pk(b.y, b.x), pk(-a.y, a.y), mul2(pk(b), pk(a.x, a.x))));
 }
-__device__ __forceinline__ float2 cmulc(float2 a, float2 b) {   // a * conj(b)
-  return make_float2(fmaf(a.x, b.x, a.y * b.y), fmaf(a.y, b.x, -a.x * b.y));
+// a * conj(b) = a b.x + (a.y, -a.x) b.y
+__device__ __forceinline__ float2 cmulc(float2 a, float2 b) {
+  return upk(fma2(pk(a.y, a.x), pk(b.y, -b.y), mul2(pk(a), pk(b.x, b.x))));
 }
-__device__ __forceinline__ float2 cscale(float2 a, float s) { return make_float2(a.x * s, a.y * s); }
+__device__ __forceinline__ float2 cscale(float2 a, float s) { return upk(mul2(pk(a), pk(s, s))); }
+// acc + w * v (real weight w)
+__device__ __forceinline__ float2 caxpy(float w, float2 v, float2 acc) { return upk(fma2(pk(w, w), pk(v), pk(acc))); }
 // multiply by SIGN * i
 template <int SIGN>
 __device__ __forceinline__ float2 mul_i(float2 a) {
   return SIGN > 0 ? make_float2(-a.y, a.x) : make_float2(a.y, -a.x);
+}
+// a + SIGN i b in one instruction (b swapped, one half negated, times 1)
+template <int SIGN>
+__device__ __forceinline__ float2 cadd_i(float2 a, float2 b) {
+  return SIGN > 0 ? upk(fma2(pk(b.y, b.x), pk(-1.f, 1.f), pk(a))) : upk(fma2(pk(b.y, b.x), pk(1.f, -1.f), pk(a)));
 }
 
 // a * W_R^K with the trivial angles special-cased.
@@ -68,53 +117,59 @@ __device__ __forceinline__ float2 twmul(float2 a) {
     return mul_i<-SIGN>(a);
   } else {
     constexpr float c = float(Tw<R, K, SIGN>::c), s = float(Tw<R, K, SIGN>::s);
-    return make_float2(fmaf(a.x, c, -a.y * s), fmaf(a.x, s, a.y * c));
+    return upk(fma2(pk(a.y, a.x), pk(-s, s), mul2(pk(a), pk(c, c))));   // a c + (-a.y, a.x) s
   }
 }
 
 // a + W_R^K b and a - W_R^K b with the twiddle multiplication folded into fused multiply-adds:
 // for W = c + i s, factor the larger of |c|, |s| out (tangent form, |t| <= 1): W b = c (b + i t b)
-// or s (u b + i b), so the pair costs 6 FP instructions (2 FMA for the scaled b, 4 FMA for the sum
-// and the difference) instead of 8 (a complex multiply and two complex additions).  The trivial
-// angles stay additions / swaps.
+// or s (u b + i b), so the pair costs 3 packed instructions (1 FFMA2 for the scaled b, 2 for the
+// sum and the difference) instead of 8 scalar ones (a complex multiply and two complex additions).
+// The trivial angles stay additions / swaps.
 template <int R, int K, int SIGN>
 __device__ __forceinline__ void bfly_w(float2 a, float2 b, float2& sum, float2& diff) {
   constexpr int k = ((K % R) + R) % R;
-  if constexpr (k == 0 || 2 * k == R || 4 * k == R || 4 * k == 3 * R) {
+  if constexpr (k == 0 || 2 * k == R) {
     const float2 t = twmul<R, K, SIGN>(b);
     sum = cadd(a, t);
     diff = csub(a, t);
+  } else if constexpr (4 * k == R || 4 * k == 3 * R) {   // W = +-i: a + W b, a - W b
+    constexpr int S = (4 * k == R) ? SIGN : -SIGN;
+    sum = cadd_i<S>(a, b);
+    diff = cadd_i<-S>(a, b);
   } else {
     constexpr double c = Tw<R, K, SIGN>::c, s = Tw<R, K, SIGN>::s;
     if constexpr ((c < 0 ? -c : c) >= (s < 0 ? -s : s)) {
       constexpr float t = float(s / c), cf = float(c);
-      const float bx = fmaf(-t, b.y, b.x), by = fmaf(t, b.x, b.y);   // b (1 + i t)
-      sum = make_float2(fmaf(cf, bx, a.x), fmaf(cf, by, a.y));
-      diff = make_float2(fmaf(-cf, bx, a.x), fmaf(-cf, by, a.y));
+      const f32x2_t bb = fma2(pk(b.y, b.x), pk(-t, t), pk(b));   // b (1 + i t)
+      sum = upk(fma2(pk(cf, cf), bb, pk(a)));
+      diff = upk(fma2(pk(-cf, -cf), bb, pk(a)));
     } else {
       constexpr float u = float(c / s), sf = float(s);
-      const float bx = fmaf(u, b.x, -b.y), by = fmaf(u, b.y, b.x);   // b (u + i)
-      sum = make_float2(fmaf(sf, bx, a.x), fmaf(sf, by, a.y));
-      diff = make_float2(fmaf(-sf, bx, a.x), fmaf(-sf, by, a.y));
+      const f32x2_t bb = fma2(pk(b), pk(u, u), pk(-b.y, b.x));   // b (u + i)
+      sum = upk(fma2(pk(sf, sf), bb, pk(a)));
+      diff = upk(fma2(pk(-sf, -sf), bb, pk(a)));
     }
   }
 }
-// a + W_R^K b alone (4 FP instructions for a generic angle)
+// a + W_R^K b alone (2 packed instructions for a generic angle)
 template <int R, int K, int SIGN>
 __device__ __forceinline__ float2 madd_w(float2 a, float2 b) {
   constexpr int k = ((K % R) + R) % R;
-  if constexpr (k == 0 || 2 * k == R || 4 * k == R || 4 * k == 3 * R) {
+  if constexpr (k == 0 || 2 * k == R) {
     return cadd(a, twmul<R, K, SIGN>(b));
+  } else if constexpr (4 * k == R || 4 * k == 3 * R) {
+    return cadd_i<(4 * k == R) ? SIGN : -SIGN>(a, b);
   } else {
     constexpr double c = Tw<R, K, SIGN>::c, s = Tw<R, K, SIGN>::s;
     if constexpr ((c < 0 ? -c : c) >= (s < 0 ? -s : s)) {
       constexpr float t = float(s / c), cf = float(c);
-      const float bx = fmaf(-t, b.y, b.x), by = fmaf(t, b.x, b.y);
-      return make_float2(fmaf(cf, bx, a.x), fmaf(cf, by, a.y));
+      const f32x2_t bb = fma2(pk(b.y, b.x), pk(-t, t), pk(b));
+      return upk(fma2(pk(cf, cf), bb, pk(a)));
     } else {
       constexpr float u = float(c / s), sf = float(s);
-      const float bx = fmaf(u, b.x, -b.y), by = fmaf(u, b.y, b.x);
-      return make_float2(fmaf(sf, bx, a.x), fmaf(sf, by, a.y));
+      const f32x2_t bb = fma2(pk(b), pk(u, u), pk(-b.y, b.x));
+      return upk(fma2(pk(sf, sf), bb, pk(a)));
     }
   }
 }
@@ -159,11 +214,11 @@ __device__ __forceinline__ void dft(float2 (&v)[R]) {
     v[1] = csub(a, b);
   } else if constexpr (R == 4) {
     const float2 s02 = cadd(v[0], v[2]), d02 = csub(v[0], v[2]);
-    const float2 s13 = cadd(v[1], v[3]), d13 = mul_i<SIGN>(csub(v[1], v[3]));
+    const float2 s13 = cadd(v[1], v[3]), d13 = csub(v[1], v[3]);
     v[0] = cadd(s02, s13);
     v[2] = csub(s02, s13);
-    v[1] = cadd(d02, d13);
-    v[3] = csub(d02, d13);
+    v[1] = cadd_i<SIGN>(d02, d13);    // d02 + SIGN i d13
+    v[3] = cadd_i<-SIGN>(d02, d13);
   } else if constexpr (R == 8) {
     float2 e[4], o[4];
 #pragma unroll

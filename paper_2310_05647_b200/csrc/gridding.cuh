@@ -229,14 +229,9 @@ __device__ __forceinline__ void gather_rec(const int* rp, const float2* strip, f
     float2 racc = make_float2(0.f, 0.f);
 #pragma unroll
     for (int i = 0; i < W; ++i) {
-      const float2 g = row[i];
-      const float w = __int_as_float(wd[2 + i]);
-      racc.x = fmaf(w, g.x, racc.x);
-      racc.y = fmaf(w, g.y, racc.y);
+      racc = caxpy(__int_as_float(wd[2 + i]), row[i], racc);
     }
-    const float wy = __int_as_float(wd[2 + W + ty]);
-    acc.x = fmaf(wy, racc.x, acc.x);
-    acc.y = fmaf(wy, racc.y, acc.y);
+    acc = caxpy(__int_as_float(wd[2 + W + ty]), racc, acc);
   }
   atomicAdd(&yf[wd[0]].x, acc.x);
   atomicAdd(&yf[wd[0]].y, acc.y);
@@ -252,12 +247,9 @@ __device__ __forceinline__ void gather_rec_any(const int* rp, int W, const float
     const float2* row = strip + ((gy0 + ty) & (G - 1)) * SWG + cx0;
     float2 racc = make_float2(0.f, 0.f);
     for (int i = 0; i < W; ++i) {
-      const float2 g = row[i];
-      racc.x = fmaf(wt(2 + i), g.x, racc.x);
-      racc.y = fmaf(wt(2 + i), g.y, racc.y);
+      racc = caxpy(wt(2 + i), row[i], racc);
     }
-    acc.x = fmaf(wt(2 + W + ty), racc.x, acc.x);
-    acc.y = fmaf(wt(2 + W + ty), racc.y, acc.y);
+    acc = caxpy(wt(2 + W + ty), racc, acc);
   }
   atomicAdd(&yf[word(0)].x, acc.x);
   atomicAdd(&yf[word(0)].y, acc.y);
@@ -348,10 +340,10 @@ k_fwd_rows(DevPlan p, const float2* __restrict__ x, float2* __restrict__ H, int 
             img = xs[rloc * N + ix];
           } else {   // fused CG vector update
             const float2 rv = xs[rloc * N + ix], pv = xs[RPC * N + rloc * N + ix], xv = xs[2 * RPC * N + rloc * N + ix];
-            img = make_float2(fmaf(beta, pv.x, rv.x), fmaf(beta, pv.y, rv.y));
+            img = caxpy(beta, pv, rv);
             const size_t gi = ((size_t)(l0 + bl) * N + iy) * N + ix;
             cg_p[gi] = img;
-            cg_x[gi] = make_float2(fmaf(alpha, pv.x, xv.x), fmaf(alpha, pv.y, xv.y));
+            cg_x[gi] = caxpy(alpha, pv, xv);
           }
           float2 val = cscale(img, dy * sdap[ix]);
           if (p.coils) val = cmul(val, cs[rloc * N + ix]);
@@ -559,7 +551,7 @@ __device__ __forceinline__ void spread_cells(const int2* sl_tab, const unsigned 
       const int2 e = i < n_staged ? ents[i] : __ldg(gents + i);
       const float wgt = __int_as_float(e.y);
       const float2 v = YS ? ys[e.x] : __ldg(yf + e.x);
-      if (cell != 0xFFFF) strip[cell] = make_float2(wgt * v.x, wgt * v.y);
+      if (cell != 0xFFFF) strip[cell] = cscale(v, wgt);
     }
     sl_lo = 0;
     sl_hi = n_multi;
@@ -575,9 +567,7 @@ __device__ __forceinline__ void spread_cells(const int2* sl_tab, const unsigned 
       for (int kk = 0; kk < width; ++kk) {
         const int2 e = ep[kk * 32];
         const float wgt = __int_as_float(e.y);
-        const float2 v = YS ? ys[e.x] : __ldg(yf + e.x);
-        acc.x = fmaf(wgt, v.x, acc.x);
-        acc.y = fmaf(wgt, v.y, acc.y);
+        acc = caxpy(wgt, YS ? ys[e.x] : __ldg(yf + e.x), acc);
       }
     } else {
       const int2* ep = gents + si.x + lane;
@@ -585,9 +575,7 @@ __device__ __forceinline__ void spread_cells(const int2* sl_tab, const unsigned 
       for (int kk = 0; kk < width; ++kk) {
         const int2 e = __ldg(ep + kk * 32);
         const float wgt = __int_as_float(e.y);
-        const float2 v = YS ? ys[e.x] : __ldg(yf + e.x);
-        acc.x = fmaf(wgt, v.x, acc.x);
-        acc.y = fmaf(wgt, v.y, acc.y);
+        acc = caxpy(wgt, YS ? ys[e.x] : __ldg(yf + e.x), acc);
       }
     }
     if (si.y < 0) {   // warp-uniform
@@ -1288,8 +1276,7 @@ k_adj_rows(DevPlan p, const float2* __restrict__ H, float2* __restrict__ out, co
         float2 o = cscale(acc[b][kk], dy * sdap[ix]);
         if (xin) {
           const float2 xv = xrow[ix];
-          o.x = fmaf(mu, xv.x, o.x);
-          o.y = fmaf(mu, xv.y, o.y);
+          o = caxpy(mu, xv, o);
           if (dot) {
             d.x += (double)xv.x * o.x + (double)xv.y * o.y;
             d.y += (double)xv.x * o.y - (double)xv.y * o.x;
