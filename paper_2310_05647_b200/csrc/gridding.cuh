@@ -546,7 +546,26 @@ __device__ __forceinline__ void spread_cells(const int2* sl_tab, const unsigned 
   if (PASS == 0) {
     const int n1 = (nsl - n_multi) * 32;
     const unsigned short* cells1 = cells + n_multi * 32;
-    for (int i = tid; i < n1; i += nthreads) {
+    // four cells per thread in flight: all index / entry loads, then the y loads, then the stores
+    // (the strip and the staged tables are disjoint, so hoisting the loads is safe)
+    int i = tid;
+    for (; i + 3 * nthreads < n1; i += 4 * nthreads) {
+      int cl[4];
+      int2 e[4];
+      float2 v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int ii = i + u * nthreads;
+        cl[u] = cells1[ii];
+        e[u] = ii < n_staged ? ents[ii] : __ldg(gents + ii);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[u] = YS ? ys[e[u].x] : __ldg(yf + e[u].x);
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (cl[u] != 0xFFFF) strip[cl[u]] = cscale(v[u], __int_as_float(e[u].y));
+    }
+    for (; i < n1; i += nthreads) {
       const int cell = cells1[i];
       const int2 e = i < n_staged ? ents[i] : __ldg(gents + i);
       const float wgt = __int_as_float(e.y);
@@ -564,7 +583,18 @@ __device__ __forceinline__ void spread_cells(const int2* sl_tab, const unsigned 
     float2 acc = make_float2(0.f, 0.f);
     if (!from_l2) {
       const int2* ep = ents + (si.x - e0) + lane;
-      for (int kk = 0; kk < width; ++kk) {
+      int kk = 0;
+      for (; kk + 3 < width; kk += 4) {   // loads first, the sum in entry order (deterministic)
+        int2 e[4];
+        float2 v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) e[u] = ep[(kk + u) * 32];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) v[u] = YS ? ys[e[u].x] : __ldg(yf + e[u].x);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) acc = caxpy(__int_as_float(e[u].y), v[u], acc);
+      }
+      for (; kk < width; ++kk) {
         const int2 e = ep[kk * 32];
         const float wgt = __int_as_float(e.y);
         acc = caxpy(wgt, YS ? ys[e.x] : __ldg(yf + e.x), acc);

@@ -1528,6 +1528,19 @@ mrf_status mrf_plan_create(const mrf_plan_desc* d, mrf_plan* out) {
     for (int i = 0; i < pl->nlanes; ++i)
       if ((s = dev_alloc(pl, &pl->Has[i], (size_t)bf * C * N * G))) return bail(s);
   }
+  if (std::getenv("MRF_PLAN_STATS")) {   // chunk size distribution (bytes) against the staging buffers
+    std::vector<int> a, f;
+    for (const int2& ow : atab) a.push_back(ow.y * 4);
+    for (const int2& ow : ftab) f.push_back(ow.y * 4);
+    std::sort(a.begin(), a.end());
+    std::sort(f.begin(), f.end());
+    auto q = [](const std::vector<int>& v, double p) { return v[(size_t)(p * (v.size() - 1))]; };
+    double sa = 0, sf = 0;
+    for (int v : a) sa += v;
+    for (int v : f) sf += v;
+    std::fprintf(stderr, "[plan] adj chunks: mean %.0f p50 %d p90 %d max %d (stage %d) | fwd chunks: mean %.0f p90 %d max %d (stage %d)\n",
+                 sa / a.size(), q(a, 0.5), q(a, 0.9), a.back(), pl->ac_stage, sf / f.size(), q(f, 0.9), f.back(), pl->fc_stage);
+  }
   for (const int2& ow : atab)   // the spread kernel needs every chunk's header, slices and cells staged
     if ((size_t)ach[ow.x + 2] * 4 > (size_t)pl->ac_stage)
       return bail(fail(MRF_EUNSUPPORTED, "a grid strip has too many occupied cells for the staging buffer"));
