@@ -1,6 +1,7 @@
 // cg.cuh -- CG vector kernels with float64 inner products.
 #pragma once
 #include <cuda_runtime.h>
+#include <stdint.h>
 
 #include "fft.cuh"
 
@@ -127,6 +128,34 @@ __global__ void __launch_bounds__(kReduceThreads) k_reduce(const double2* __rest
   }
 }
 
+// dst = sum a[0..na) + mu * sum b[0..nb) (each summed in a fixed order), then alpha (OP ==
+// kRedAlpha) -- the split-phase CG's <p, (A^H A + mu I) p> = ||A p||^2 + mu ||p||^2.
+template <int OP>
+__global__ void __launch_bounds__(kReduceThreads) k_reduce_pq(const double2* __restrict__ a, int na,
+                                                              const double2* __restrict__ b, int nb, double mu,
+                                                              double2* __restrict__ dst, CGScalars* sc, double* hx, int k) {
+  __shared__ double red[2][kReduceThreads / 32];
+  double sa = 0.0, sb = 0.0;
+  for (int i = threadIdx.x; i < na; i += kReduceThreads) sa += a[i].x;
+  for (int i = threadIdx.x; i < nb; i += kReduceThreads) sb += b[i].x;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    sa += __shfl_xor_sync(0xffffffffu, sa, o);
+    sb += __shfl_xor_sync(0xffffffffu, sb, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    red[0][threadIdx.x >> 5] = sa;
+    red[1][threadIdx.x >> 5] = sb;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double ta = 0.0, tb = 0.0;
+    for (int w = 0; w < kReduceThreads / 32; ++w) { ta += red[0][w]; tb += red[1][w]; }
+    *dst = make_double2(ta + mu * tb, 0.0);
+    if (OP == kRedAlpha) cg_alpha(sc, hx, k);
+  }
+}
+
 // The vector kernels treat the complex64 arrays as float4 (two elements; n is even and the arrays
 // are 16-byte aligned) and keep 4 independent float4 per operand in flight per thread (a
 // grid-stride loop unrolled by 4), enough outstanding bytes per SM to stream at HBM rate.
@@ -150,6 +179,26 @@ __device__ __forceinline__ double norm2d(float4 v) {
   return ((double)v.x * v.x + (double)v.y * v.y) + ((double)v.z * v.z + (double)v.w * v.w);
 }
 
+
+// partial ||v||^2 per block (v: n complex64 values, 8-byte aligned; any n)
+__global__ void __launch_bounds__(kVecThreads) k_sqnorm(const float2* __restrict__ v, size_t n, double2* __restrict__ part) {
+  double2 s = make_double2(0.0, 0.0);
+  const float4* v4 = reinterpret_cast<const float4*>(v);
+  if (reinterpret_cast<uintptr_t>(v) % 16 == 0) {
+    MRF_VEC4_LOOP(n / 2, { s.x += norm2d(v4[i]); })
+    if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+      const float2 t = v[n - 1];
+      s.x += (double)t.x * t.x + (double)t.y * t.y;
+    }
+  } else {
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+      const float2 t = v[i];
+      s.x += (double)t.x * t.x + (double)t.y * t.y;
+    }
+  }
+  s = block_sum2(s);
+  if (threadIdx.x == 0) part[blockIdx.x] = s;
+}
 
 // r = rhs - q ; p = r  (initial residual; q == nullptr: x0 = 0, r = rhs); partial <r,r>
 __global__ void __launch_bounds__(kVecThreads) k_cg_init(const float2* __restrict__ rhs, const float2* __restrict__ q,

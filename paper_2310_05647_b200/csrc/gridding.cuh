@@ -267,12 +267,14 @@ __device__ __forceinline__ int item_fc(const int* __restrict__ perm, int C, int 
 
 // ============================================================================ forward rows
 // Items (bl, rowblock, c), c fastest.  MODE 0: image block = x.  MODE 1 (CG, C == 1): image block
-// = p' = r + beta p with x' = x + alpha p, both written back (one pass over r, p, x per iteration).
+// = p' = r + beta p with x' = x + alpha p, both written back (one pass over r, p, x per iteration);
+// with pn != nullptr also the float64 partials of ||p'||^2, one per warp and item (split-phase CG).
 template <int G, int MODE>
 __global__ void __launch_bounds__(kRowThreads)
 k_fwd_rows(DevPlan p, const float2* __restrict__ x, float2* __restrict__ H, int l0, int nb,
            float2* __restrict__ cg_r, float2* __restrict__ cg_p, float2* __restrict__ cg_x,
-           const double* __restrict__ cg_ab, float2* __restrict__ yzero, long long nyzero) {
+           const double* __restrict__ cg_ab, float2* __restrict__ yzero, long long nyzero,
+           double2* __restrict__ pn = nullptr) {
   using Rc = RowCfg<G>;
   constexpr int P = Rc::P, Q = Rc::Q, T = Rc::T, N = Rc::N, RPC = Rc::RPC, A = Q / T, B = P / T;
   constexpr int NRB = N / RPC, S = G / SW, NST = MODE == 1 ? 3 : 1;
@@ -328,6 +330,7 @@ k_fwd_rows(DevPlan p, const float2* __restrict__ x, float2* __restrict__ H, int 
     mbar_wait(bar, ph);
     ph ^= 1;
     float2 v[A][P];
+    double pp = 0.0;   // ||p'||^2 of this thread's pixels (MODE 1)
 #pragma unroll
     for (int a = 0; a < A; ++a) {
       const int n2 = t + T * a;
@@ -344,6 +347,7 @@ k_fwd_rows(DevPlan p, const float2* __restrict__ x, float2* __restrict__ H, int 
             const size_t gi = ((size_t)(l0 + bl) * N + iy) * N + ix;
             cg_p[gi] = img;
             cg_x[gi] = caxpy(alpha, pv, xv);
+            pp += (double)img.x * img.x + (double)img.y * img.y;
           }
           float2 val = cscale(img, dy * sdap[ix]);
           if (p.coils) val = cmul(val, cs[rloc * N + ix]);
@@ -352,6 +356,11 @@ k_fwd_rows(DevPlan p, const float2* __restrict__ x, float2* __restrict__ H, int 
           v[a][n1] = make_float2(0.f, 0.f);
         }
       }
+    }
+    if (MODE == 1 && pn) {   // per-warp partial of ||p'||^2 (summed in a fixed order by k_reduce_pq)
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) pp += __shfl_xor_sync(0xffffffffu, pp, o);
+      if ((tid & 31) == 0) pn[((size_t)l0 * NRB + item) * (kRowThreads / 32) + (tid >> 5)] = make_double2(pp, 0.0);
     }
     __syncthreads();   // staging consumed: prefetch the next item behind this item's FFT
     if (tid == 0 && item + (int)gridDim.x < n_items) {
@@ -1172,10 +1181,15 @@ __global__ void k_psf_store(const double* __restrict__ Tm, int G, float* __restr
 // Items (bl, rowblock); coils accumulated in registers.  out = sum_c conj(S_c) crop(rowIFFT(H))
 // . dap dap (+ mu xin).  With dot != nullptr also writes the item's float64 partial of
 // <xin, out> (the CG inner product <p, q>, fused).
-template <int G>
+// Split-phase CG (rres != nullptr, C == 1): q = out is not stored; the residual is advanced in
+// place, r -= alpha q with alpha = *cg_alpha (computed from ||A p||^2 + mu ||p||^2 before this
+// pass), and dot receives the partial of <r, r> of the new residual.  p and r are staged
+// single-buffered in the two x slots, prefetched after the previous item's epilogue.
+template <int G, bool RU>
 __global__ void __launch_bounds__(kRowThreads)
 k_adj_rows(DevPlan p, const float2* __restrict__ H, float2* __restrict__ out, const float2* __restrict__ xin,
-           float mu, int l0, int nb, double2* __restrict__ dot) {
+           float mu, int l0, int nb, double2* __restrict__ dot, float2* __restrict__ rres,
+           const double* __restrict__ cg_alpha) {
   using Rc = RowCfg<G>;
   constexpr int P = Rc::P, Q = Rc::Q, T = Rc::T, N = Rc::N, RPC = Rc::RPC, A = Q / T, B = P / T;
   constexpr int NRB = N / RPC;
@@ -1217,16 +1231,28 @@ k_adj_rows(DevPlan p, const float2* __restrict__ H, float2* __restrict__ out, co
     mbar_expect_tx(&bars[1 + xb], XBLK);
     bulk_g2s(xs + xb * RPC * N, xin + ((size_t)(l0 + bl) * N + (size_t)rb * RPC) * N, XBLK, &bars[1 + xb]);
   };
+  auto issue_pr = [&](int item) {   // split-phase CG: p -> slot 0, r -> slot 1 (thread 0)
+    const int rb = item % NRB, bl = item / NRB;
+    const size_t off = ((size_t)(l0 + bl) * N + (size_t)rb * RPC) * N;
+    mbar_expect_tx(&bars[1], XBLK);
+    bulk_g2s(xs, xin + off, XBLK, &bars[1]);
+    mbar_expect_tx(&bars[2], XBLK);
+    bulk_g2s(xs + RPC * N, rres + off, XBLK, &bars[2]);
+  };
+  const float alpha = RU ? (float)*cg_alpha : 0.f;   // after pdl_wait: written by the alpha step
   int item = blockIdx.x;
   if (warp == 0 && item < n_items) issue_h(item, 0);
-  if (tid == 0 && xin && item < n_items) issue_x(item, 0);
+  if (tid == 0 && item < n_items) {
+    if (RU) issue_pr(item);
+    else if (xin) issue_x(item, 0);
+  }
   uint32_t hph = 0;
   float2* myex = ex + rloc * Rc::EX;
   for (int k = 0; item < n_items; item += gridDim.x, ++k) {
     const int rb = item % NRB, bl = item / NRB;
     const int iy = rb * RPC + rloc;
     const int next = item + gridDim.x;
-    if (tid == 0 && xin && next < n_items) issue_x(next, (k + 1) & 1);   // buffer freed by item k-1
+    if (!RU && tid == 0 && xin && next < n_items) issue_x(next, (k + 1) & 1);   // buffer freed by item k-1
     float2 acc[B][Q / 2];
 #pragma unroll
     for (int b = 0; b < B; ++b)
@@ -1292,9 +1318,16 @@ k_adj_rows(DevPlan p, const float2* __restrict__ H, float2* __restrict__ out, co
     }
     // a6 epilogue: deapodise, (+ mu x), store, CG partial <xin, out>
     const float dy = sdap[iy];
-    float2* orow = out + ((size_t)(l0 + bl) * N + iy) * N;
-    const float2* xrow = xs + (k & 1) * RPC * N + rloc * N;
-    if (xin) mbar_wait(&bars[1 + (k & 1)], (k >> 1) & 1);
+    const size_t orow0 = ((size_t)(l0 + bl) * N + iy) * N;
+    float2* orow = (RU ? rres : out) + orow0;
+    const float2* xrow = xs + (RU ? 0 : (k & 1)) * RPC * N + rloc * N;
+    const float2* rrow = xs + RPC * N + rloc * N;
+    if (RU) {
+      mbar_wait(&bars[1], k & 1);
+      mbar_wait(&bars[2], k & 1);
+    } else if (xin) {
+      mbar_wait(&bars[1 + (k & 1)], (k >> 1) & 1);
+    }
     double2 d = make_double2(0.0, 0.0);
 #pragma unroll
     for (int b = 0; b < B; ++b) {
@@ -1304,7 +1337,11 @@ k_adj_rows(DevPlan p, const float2* __restrict__ H, float2* __restrict__ out, co
         const int k2 = kk < Q / 4 ? kk : kk + Q / 2;
         const int ix = grid_to_img<G>(k1 + P * k2);
         float2 o = cscale(acc[b][kk], dy * sdap[ix]);
-        if (xin) {
+        if (RU) {   // r' = r - alpha (A^H A p + mu p); <r', r'>
+          o = caxpy(mu, xrow[ix], o);
+          o = caxpy(-alpha, o, rrow[ix]);
+          d.x += (double)o.x * o.x + (double)o.y * o.y;
+        } else if (xin) {
           const float2 xv = xrow[ix];
           o = caxpy(mu, xv, o);
           if (dot) {
@@ -1324,6 +1361,10 @@ k_adj_rows(DevPlan p, const float2* __restrict__ H, float2* __restrict__ out, co
       if (lane == 0) red[warp] = d;
     }
     __syncthreads();   // x block consumed; red complete
+    if (RU && tid == 0 && next < n_items) {   // p, r slots free: prefetch the next item's
+      fence_proxy_async();
+      issue_pr(next);
+    }
     if (dot && tid == 0) {
       double2 s = make_double2(0.0, 0.0);
       for (int i = 0; i < kRowThreads / 32; ++i) { s.x += red[i].x; s.y += red[i].y; }

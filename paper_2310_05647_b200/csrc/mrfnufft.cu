@@ -131,6 +131,9 @@ struct mrf_plan_s {
   float2* q = nullptr;
   double2* part = nullptr;   // [kPartBlocks] vector-kernel partials
   double2* dotp = nullptr;   // [L * rowblocks] fused <p, q> partials of k_adj_rows
+  // split-phase CG (C == 1): y = A p of all local frames and the ||p||^2 partials of the row pass
+  float2* ycg = nullptr;     // [L][M]
+  double2* pnp = nullptr;    // [L * rowblocks * 4]
   size_t ndotp = 0;
   CGScalars* sc = nullptr;
   float2* cg_rin = nullptr;  // the vector the fused CG row pass adds to beta p: r (CG) or z (PCG)
@@ -290,7 +293,7 @@ static void free_plan(mrf_plan_s* pl) {
     if (pl->Hs[i]) cudaFree(pl->Hs[i]);
     if (pl->ybufs[i]) cudaFree(pl->ybufs[i]);
   }
-  void* ptrs[] = {pl->perm, pl->pc_lam, pl->z, pl->pc_tmp, pl->pc_part,
+  void* ptrs[] = {pl->ycg, pl->pnp, pl->perm, pl->pc_lam, pl->z, pl->pc_tmp, pl->pc_part,
                   pl->coils, pl->dap, pl->tw, pl->fchunks, pl->ftab, pl->achunks, pl->atab, pl->fil, pl->r, pl->p, pl->q,
                   pl->part, pl->dotp, pl->sc, pl->hist, pl->stg_x, pl->stg_y, pl->stg_z, pl->ax[0], pl->ax[1],
                   pl->ay[0], pl->ay[1]};
@@ -414,13 +417,14 @@ static mrf_status setup_kernels(mrf_plan_s* pl) {
   pl->ac_stage = (int)((s_acol - adj_cols_fixed<G>((size_t)pl->ystage, pl->adj_sep)) & ~size_t(15));
   CUDA_TRY(cudaFuncSetAttribute(k_fwd_rows<G, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s_fr0));
   CUDA_TRY(cudaFuncSetAttribute(k_fwd_rows<G, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s_fr1));
-  CUDA_TRY(cudaFuncSetAttribute(k_adj_rows<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s_ar));
+  CUDA_TRY(cudaFuncSetAttribute(k_adj_rows<G, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s_ar));
+  CUDA_TRY(cudaFuncSetAttribute(k_adj_rows<G, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s_ar));
   CUDA_TRY(cudaFuncSetAttribute(k_fwd_cols<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s_col));
   auto adj_kernel = pl->adj_sep ? k_adj_cols<G, (G <= 512)> : k_adj_cols<G, false>;
   CUDA_TRY(cudaFuncSetAttribute(adj_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s_acol));
   CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pl->occ_fr0, k_fwd_rows<G, 0>, kRowThreads, s_fr0));
   CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pl->occ_fr1, k_fwd_rows<G, 1>, kRowThreads, s_fr1));
-  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pl->occ_ar, k_adj_rows<G>, kRowThreads, s_ar));
+  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pl->occ_ar, k_adj_rows<G, false>, kRowThreads, s_ar));
   CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pl->occ_fc, k_fwd_cols<G>, ncol, s_col));
   CUDA_TRY(cudaFuncSetAttribute(k_toep_cols<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)toep_cols_smem<G>()));
   CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pl->occ_tc, k_toep_cols<G>, ncol, toep_cols_smem<G>()));
@@ -471,16 +475,16 @@ static mrf_status launch_fwd_rows(mrf_plan_s* pl, const float2* x, float2* H, in
   const long long items = (long long)nb * (pl->N / RowCfg<G>::RPC) * pl->C;
   ProfScope ps(pl, MRF_K_FWD_ROWS, st);
   CUDA_TRY(launch_pdl(k_fwd_rows<G, 0>, pgrid(pl, pl->occ_fr0, items), kRowThreads, fwd_rows_smem<G>(1), st, pl->dp(),
-                      x, H, l0, nb, nullptr, nullptr, nullptr, nullptr, yzero, nyzero));
+                      x, H, l0, nb, nullptr, nullptr, nullptr, nullptr, yzero, nyzero, (double2*)nullptr));
   return MRF_OK;
 }
 template <int G>
 static mrf_status launch_fwd_rows_cg(mrf_plan_s* pl, float2* x, float2* H, int l0, int nb, cudaStream_t st,
-                                     float2* yzero, long long nyzero) {
+                                     float2* yzero, long long nyzero, double2* pn = nullptr) {
   const long long items = (long long)nb * (pl->N / RowCfg<G>::RPC) * pl->C;
   ProfScope ps(pl, MRF_K_FWD_ROWS, st);
   CUDA_TRY(launch_pdl(k_fwd_rows<G, 1>, pgrid(pl, pl->occ_fr1, items), kRowThreads, fwd_rows_smem<G>(3), st, pl->dp(),
-                      nullptr, H, l0, nb, pl->cg_rin ? pl->cg_rin : pl->r, pl->p, x, &pl->sc->alpha, yzero, nyzero));
+                      nullptr, H, l0, nb, pl->cg_rin ? pl->cg_rin : pl->r, pl->p, x, &pl->sc->alpha, yzero, nyzero, pn));
   return MRF_OK;
 }
 template <int G>
@@ -504,11 +508,15 @@ static mrf_status launch_adj_cols(mrf_plan_s* pl, const float2* y, float2* H, in
 }
 template <int G>
 static mrf_status launch_adj_rows(mrf_plan_s* pl, const float2* H, float2* out, const float2* xin, float mu, int l0,
-                                  int nb, double2* dot, cudaStream_t st) {
+                                  int nb, double2* dot, cudaStream_t st, float2* rres = nullptr) {
   const long long items = (long long)nb * (pl->N / RowCfg<G>::RPC);
   ProfScope ps(pl, MRF_K_ADJ_ROWS, st);
-  CUDA_TRY(launch_pdl(k_adj_rows<G>, pgrid(pl, pl->occ_ar, items), kRowThreads, adj_rows_smem<G>(), st, pl->dp(), H, out,
-                      xin, mu, l0, nb, dot));
+  if (rres)
+    CUDA_TRY(launch_pdl(k_adj_rows<G, true>, pgrid(pl, pl->occ_ar, items), kRowThreads, adj_rows_smem<G>(), st, pl->dp(),
+                        H, out, xin, mu, l0, nb, dot, rres, (const double*)&pl->sc->alpha));
+  else
+    CUDA_TRY(launch_pdl(k_adj_rows<G, false>, pgrid(pl, pl->occ_ar, items), kRowThreads, adj_rows_smem<G>(), st, pl->dp(),
+                        H, out, xin, mu, l0, nb, dot, (float2*)nullptr, (const double*)nullptr));
   return MRF_OK;
 }
 
@@ -607,6 +615,40 @@ static mrf_status run_normal(mrf_plan_s* pl, const float2* x, float2* out, float
   return ln.end();
 }
 
+// Split-phase CG iteration (C == 1, gridding plans): the forward half of the
+// normal operator for every batch -- the fused row pass (p = r + beta p, x += alpha p, ||p||^2
+// partials) and the column pass into y = A p of all frames -- then, once alpha = rho /
+// (||A p||^2 + mu ||p||^2) is known, the adjoint half whose row pass advances r -= alpha
+// (A^H A p + mu p) in place and emits the <r, r> partials.  q is never stored and the separate
+// r-update pass disappears: 8 image passes per iteration instead of 10.
+template <int G>
+static mrf_status run_cg_split_fwd(mrf_plan_s* pl, float2* xsol, cudaStream_t st) {
+  Lanes ln(pl, st, n_batches(pl));
+  MRF_TRY(ln.begin());
+  for (int b = 0, l0 = 0; l0 < pl->L; ++b, l0 += pl->bf) {
+    const int nb = std::min(pl->bf, pl->L - l0);
+    cudaStream_t s = ln.stream(b);
+    float2* H = pl->Hs[ln.slot(b)];
+    float2* yb = pl->ycg + (size_t)l0 * pl->M;
+    MRF_TRY(launch_fwd_rows_cg<G>(pl, xsol, H, l0, nb, s, yb, (long long)nb * pl->M, pl->pnp));
+    MRF_TRY(launch_fwd_cols<G>(pl, H, yb, l0, nb, s));
+  }
+  return ln.end();
+}
+template <int G>
+static mrf_status run_cg_split_adj(mrf_plan_s* pl, float mu, cudaStream_t st) {
+  Lanes ln(pl, st, n_batches(pl));
+  MRF_TRY(ln.begin());
+  for (int b = 0, l0 = 0; l0 < pl->L; ++b, l0 += pl->bf) {
+    const int nb = std::min(pl->bf, pl->L - l0);
+    cudaStream_t s = ln.stream(b);
+    float2* H = pl->Hs[ln.slot(b)];
+    MRF_TRY(launch_adj_cols<G>(pl, pl->ycg + (size_t)l0 * pl->M, H, l0, nb, s));
+    MRF_TRY(launch_adj_rows<G>(pl, H, nullptr, pl->p, mu, l0, nb, pl->dotp, s, pl->r));
+  }
+  return ln.end();
+}
+
 // Toeplitz form of run_normal (plans with MRF_NORMAL_TOEPLITZ): row FFT of pad(S_c x) (no
 // deapodisation), k_toep_cols (column FFT, x PSF spectrum, column iFFT), row iFFT + conj-coil sum.
 template <int G>
@@ -657,6 +699,12 @@ static mrf_status do_normal(mrf_plan_s* pl, const float2* x, float2* out, float 
   DISPATCH_G(pl, run_normal, pl, x, out, mu, cg, xsol, st);
 }
 static mrf_status do_setup(mrf_plan_s* pl) { DISPATCH_G(pl, setup_kernels, pl); }
+static mrf_status do_cg_split_fwd(mrf_plan_s* pl, float2* xsol, cudaStream_t st) {
+  DISPATCH_G(pl, run_cg_split_fwd, pl, xsol, st);
+}
+static mrf_status do_cg_split_adj(mrf_plan_s* pl, float mu, cudaStream_t st) {
+  DISPATCH_G(pl, run_cg_split_adj, pl, mu, st);
+}
 
 // ---------------------------------------------------------------------------- CG (device scalars)
 static int vec_blocks(size_t n) {
@@ -896,6 +944,8 @@ static mrf_status run_cg_launch(mrf_plan_s* pl, const float2* y, const float2* z
     CUDA_TRY(cudaStreamSynchronize(st));
   }
   *iters_done = n_iter;
+  const bool comm = pl->nccl_comm || pl->host_ar;
+  const bool split = pl->ycg && !pc && pl->C == 1 && !(pl->flags & MRF_NORMAL_TOEPLITZ);
   for (int k = 0; k < n_iter; ++k) {
     if (tol > 0.f && res0 == 0.0) { *iters_done = 0; break; }
     if (pl->C > 1) {   // unfused p / x update (the multi-coil row pass reads the image once per coil)
@@ -903,6 +953,28 @@ static mrf_status run_cg_launch(mrf_plan_s* pl, const float2* y, const float2* z
       k_cg_px<<<nblk, kVecThreads, 0, st>>>(x, pl->p, rin, n, pl->sc);
       MRF_TRY(vec_launch_check("k_cg_px"));
     }
+    if (split) {   // alpha from ||A p||^2 + mu ||p||^2; the adjoint half advances r and emits <r, r>
+      MRF_TRY(do_cg_split_fwd(pl, x, st));
+      const size_t ny = (size_t)pl->L * pl->M;
+      const int nbly = vec_blocks(ny);
+      {
+        ProfScope ps(pl, MRF_K_CG_VEC, st);
+        k_sqnorm<<<nbly, kVecThreads, 0, st>>>(pl->ycg, ny, pl->part);
+        MRF_TRY(vec_launch_check("k_sqnorm"));
+        const int npn = (int)(pl->ndotp * (kRowThreads / 32));
+        if (comm) k_reduce_pq<kRedPlain><<<1, kReduceThreads, 0, st>>>(pl->part, nbly, pl->pnp, npn, (double)mu, &pl->sc->pq, pl->sc, hist_a, k);
+        else k_reduce_pq<kRedAlpha><<<1, kReduceThreads, 0, st>>>(pl->part, nbly, pl->pnp, npn, (double)mu, &pl->sc->pq, pl->sc, hist_a, k);
+        MRF_TRY(vec_launch_check("k_reduce_pq"));
+      }
+      if (comm) {
+        MRF_TRY(allreduce2(pl, &pl->sc->pq, st));
+        ProfScope ps(pl, MRF_K_CG_VEC, st);
+        k_cg_alpha<<<1, 1, 0, st>>>(pl->sc, hist_a, k);
+        MRF_TRY(vec_launch_check("k_cg_alpha"));
+      }
+      MRF_TRY(do_cg_split_adj(pl, mu, st));
+      MRF_TRY(reduce_step<kRedBeta>(pl, pl->dotp, (int)pl->ndotp, &pl->sc->rr, hist_b, k, st));
+    } else {
     MRF_TRY(do_normal(pl, pl->p, pl->q, mu, st, 1, x));
     MRF_TRY(reduce_step<kRedAlpha>(pl, pl->dotp, (int)pl->ndotp, &pl->sc->pq, hist_a, k, st));
     {
@@ -917,6 +989,7 @@ static mrf_status run_cg_launch(mrf_plan_s* pl, const float2* y, const float2* z
       MRF_TRY(reduce_step<kRedBetaPc>(pl, pl->pc_part, npart, &pl->sc->rz, hist_b, k, st));
     } else {
       MRF_TRY(reduce_step<kRedBeta>(pl, pl->part, nblk, &pl->sc->rr, hist_b, k, st));
+    }
     }
     if (tol > 0.f) {
       double res = 0.0;
@@ -1507,6 +1580,12 @@ mrf_status mrf_plan_create(const mrf_plan_desc* d, mrf_plan* out) {
     return bail(s);
   if (d->coils && C >= 1) {
     if ((s = dev_alloc(pl, &pl->coils, (size_t)C * N * N))) return bail(s);
+  }
+  if (C == 1 && !(d->flags & MRF_NORMAL_TOEPLITZ)) {   // split-phase CG (MRF_CG_SPLIT=0 disables)
+    const char* e = std::getenv("MRF_CG_SPLIT");
+    if (!(e && e[0] == '0'))
+      if ((s = dev_alloc(pl, &pl->ycg, (size_t)L * M)) || (s = dev_alloc(pl, &pl->pnp, pl->ndotp * (kRowThreads / 32))))
+        return bail(s);
   }
   pl->nlanes = std::min(kDefaultLanes, (L + bf - 1) / bf);
   if (const char* e = std::getenv("MRF_LANES")) pl->nlanes = std::max(1, std::min(kMaxLanes, std::atoi(e)));
