@@ -50,6 +50,7 @@ def parse():
     ap.add_argument("--no-llr", action="store_true", help="skip the LLR outer-step measurement")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-pcg", action="store_true", help="skip the preconditioned-CG measurement")
+    ap.add_argument("--no-fft-stages", action="store_true", help="skip the per-stage comparison with cuFFT")
     ap.add_argument("--pcg-tol", type=float, default=1e-3)
     ap.add_argument("--flush-l2", default="auto", choices=["auto", "on", "off"],
                     help="flush L2 between timed steps (auto: when the working set is < 4x L2)")
@@ -396,6 +397,57 @@ def run_ours(args):
     except Exception:
         cufft_ms = None
 
+    # ---------------------------------------------------------------- FFT stages vs cuFFT (reference only)
+    # Each of the four gridding kernels timed on its own (a one-lane plan, per-kernel-class events,
+    # forward then adjoint), beside cuFFT doing the same stage's transforms unpruned: the row stage
+    # = N length-G FFTs per frame-coil (torch.fft.fft over the last axis of [B, N, G]), the column
+    # stage = G length-G FFTs per frame-coil (axis -2 of [B, G, G]).  Ours includes the fused
+    # deapodisation / gather / spread / crop work of its stage; cuFFT's includes its own HBM passes.
+    fft_stages = None
+    if not args.no_fft_stages and world == 1:   # (time_op synchronises ranks)
+        try:
+            prev_lanes = os.environ.get("MRF_LANES")
+            os.environ["MRF_LANES"] = "1"
+            try:
+                p1 = binding.Plan(cfg.N, traj, L, coils=coils, W=cfg.W, frame_offset=off, device=local,
+                                  batch_frames=args.batch_frames)
+            finally:
+                if prev_lanes is None:
+                    os.environ.pop("MRF_LANES", None)
+                else:
+                    os.environ["MRF_LANES"] = prev_lanes
+            p1.forward(xin, y=yout)
+            p1.adjoint(y, x=xout)
+            torch.cuda.synchronize()
+            p1.profile(True)
+            for _ in range(reps):
+                p1.forward(xin, y=yout)
+                p1.adjoint(y, x=xout)
+            torch.cuda.synchronize()
+            ours = {k: p1.profile_query(k)[0] / reps for k in ("fwd_rows", "fwd_cols", "adj_cols", "adj_rows")}
+            p1.profile(False)
+            p1.close()
+            FB = max(1, min(32, L * cfg.C))
+            nch = math.ceil(L * cfg.C / FB)
+            bufr = torch.randn((FB, cfg.N, cfg.G), dtype=torch.complex64, device=dev)
+            bufc = torch.randn((FB, cfg.G, cfg.G), dtype=torch.complex64, device=dev)
+            cuf = {
+                "rows_fwd": time_op(lambda: [torch.fft.fft(bufr, dim=-1) for _ in range(nch)], 3),
+                "cols_fwd": time_op(lambda: [torch.fft.fft(bufc, dim=-2) for _ in range(nch)], 3),
+                "cols_inv": time_op(lambda: [torch.fft.ifft(bufc, dim=-2) for _ in range(nch)], 3),
+                "rows_inv": time_op(lambda: [torch.fft.ifft(bufr, dim=-1) for _ in range(nch)], 3),
+            }
+            del bufr, bufc
+            fft_stages = {"ours_ms": {"fwd_rows": ours["fwd_rows"], "fwd_cols": ours["fwd_cols"],
+                                      "adj_cols": ours["adj_cols"], "adj_rows": ours["adj_rows"]},
+                          "cufft_ms": cuf,
+                          "note": "ours: one-lane plan, per-kernel-class CUDA events, stage = pruned transforms + the "
+                                  "fused deapod/gather/spread/crop of that kernel; cuFFT: unpruned batched 1D C2C "
+                                  "transforms of the same stage (rows: N x G per frame-coil, columns: G x G), "
+                                  "out-of-place, timing reference only"}
+        except Exception as e:  # reference timing only
+            fft_stages = {"error": str(e)[:200]}
+
     # ---------------------------------------------------------------- Toeplitz normal operator
     toep = None
     if not args.no_toeplitz:
@@ -435,8 +487,11 @@ def run_ours(args):
         dic.profile(False)
         gemm_ms /= max(gemm_n, 1)
         Vm, Km = xm.shape[1], atoms.shape[0]
-        vpad, np_, kd = -(-Vm // 128) * 128, -(-2 * Km // 256) * 256, -(-2 * cfg.L // 64) * 64
-        gemm_fl = 2.0 * vpad * np_ * kd
+        # the profiled bracket holds the certified filter's two k_dict_gemm passes over the packed
+        # fp16 rows [u_hi | u_lo | u_hi] of the r-dimensional projection: K = KF = 384
+        # (csrc/match.cuh), M = voxels padded to 128, N = 2 x atoms padded to 256
+        vpad, np_, kd = -(-Vm // 128) * 128, -(-2 * Km // 256) * 256, 384
+        gemm_fl = 2 * 2.0 * vpad * np_ * kd
         peak_tc = float(peaks().get("bf16_tflops", 2250.0))
         match = {"ms": ms_match, "voxels": Vm, "atoms": Km, "frames": cfg.L,
                  "useful_tflops": 8.0 * Vm * Km * cfg.L / (ms_match * 1e-3) / 1e12,
@@ -444,9 +499,11 @@ def run_ours(args):
                               "peak": peak_tc, "unit": "TFLOP/s",
                               "frac": gemm_fl / (gemm_ms * 1e-3) / 1e12 / peak_tc, "avg_launch_ms": gemm_ms,
                               "peak_note": "measured bf16 dense burst (MEASURED_PEAKS.json); fp16 runs at the same rate"},
-                 "note": "mrf_dict_match on the CG solution: fp16 tcgen05 GEMM (pads to 128 voxels, 128 atoms, "
-                         "32 frames) + fused argmax, then exact fp32 PD; synthetic 3336-atom dictionary "
-                         "(PAPER.md:319 grid, surrogate fingerprints)"}
+                 "note": "mrf_dict_match on the CG solution (exact Eq. 5 argmax): r-dimensional projection, "
+                         "certified 3xFP16 tcgen05 filter (two GEMM passes, K = 384; 'roofline' covers them), "
+                         "float64 rescoring of every admissible atom; useful_tflops = the dense complex "
+                         "correlation 8 V K L it replaces, per second of the whole match; synthetic 3336-atom "
+                         "dictionary (PAPER.md:319 grid, surrogate fingerprints)"}
         dic.close()
 
     # ---------------------------------------------------------------- preconditioned CG
@@ -639,7 +696,7 @@ def run_ours(args):
         "fwd_pts_s": cfg.L * cfg.C * cfg.M / (ms_fwd * 1e-3), "adj_pts_s": cfg.L * cfg.C * cfg.M / (ms_adj * 1e-3),
         "hbm": {"algorithmic_bytes_per_step": hbm_bytes, "achieved_GBs": hbm_achieved, "peak_GBs": hbm_peak,
                 "frac": hbm_achieved / hbm_peak},
-        "cufft_ref_ms_fft2_LC": cufft_ms,
+        "cufft_ref_ms_fft2_LC": cufft_ms, "fft_stages": fft_stages,
         "roofline": roofline, "roofline_AHA": roofline_aha, "toeplitz": toep, "match": match, "dcf": dcf_res, "pcg": pcg_res, "llr": llr_res, "kernel_share": share, "kernel_share_of_kernel_time": share_k, "gpu_launches": gpu_launches,
         "clocks": clk, "e2e": e2e, "cpu_baseline": cpu,
     }

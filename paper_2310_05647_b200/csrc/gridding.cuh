@@ -858,7 +858,7 @@ k_adj_cols(DevPlan p, const float2* __restrict__ y, float2* __restrict__ H, int 
 template <int G>
 __global__ void __launch_bounds__(SW * FFTShape<G>::T, (G >= 1024 ? 1 : 2))
 k_toep_cols(DevPlan p, const float2* __restrict__ Hf, float2* __restrict__ Ha, const float* __restrict__ psf, int l0,
-            int nb) {
+            int nb, double2* __restrict__ tq) {
   using F = FFTShape<G>;
   constexpr int P = F::P, Q = F::Q, T = F::T, N = G / 2, A = Q / T, B = P / T, S = G / SW;
   constexpr uint32_t STRIP_IN = N * SW * sizeof(float2);
@@ -886,6 +886,7 @@ k_toep_cols(DevPlan p, const float2* __restrict__ Hf, float2* __restrict__ Ha, c
   if (tid == 0 && item < n_items) issue_in(item);
   for (int k = 0; item < n_items; item += gridDim.x, ++k) {
     const int fc = item_fc(p.perm, C, item, S, l0), s = item % S;
+    double tpx = 0.0;
     const int next = item + gridDim.x;
     // PSF values at this thread's forward-output rows k1 + P k2: issued now, used after the FFT
     const int r = __ldg(p.fil + l0 + fc / C);
@@ -935,11 +936,22 @@ k_toep_cols(DevPlan p, const float2* __restrict__ Hf, float2* __restrict__ Ha, c
     for (int b = 0; b < B; ++b) {
       const int k1 = t + T * b;
       dft<Q, -1>(w[b]);                          // w[b][k2] = X[k1 + P k2]
+      if (tq) {   // Parseval: <p, A^H A p> = sum_k T(k) |X(k)|^2 (split-phase CG, reading 30)
+#pragma unroll
+        for (int k2 = 0; k2 < Q; ++k2)
+          tpx += (double)tp[b][k2] * ((double)w[b][k2].x * w[b][k2].x + (double)w[b][k2].y * w[b][k2].y);
+      }
 #pragma unroll
       for (int k2 = 0; k2 < Q; ++k2) w[b][k2] = cscale(w[b][k2], tp[b][k2]);
       dft<Q, +1>(w[b]);                          // stage A of the inverse: index n2
 #pragma unroll
       for (int n2 = 0; n2 < Q; ++n2) ex[(n2 * P + k1) * SW + c] = cmulc(w[b][n2], stw[n2 * P + k1]);
+    }
+    if (tq) {   // one partial per warp and item, summed in a fixed order by k_reduce_pq
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) tpx += __shfl_xor_sync(0xffffffffu, tpx, o);
+      if ((tid & 31) == 0) tq[((size_t)l0 * C * S + item) * (blockDim.x >> 5) + (tid >> 5)] = make_double2(tpx, 0.0);
+      tpx = 0.0;
     }
     __syncthreads();
     float2* Hc = Ha + (size_t)fc * N * G + (size_t)s * SW + c;    // row-major [fc][iy][G]

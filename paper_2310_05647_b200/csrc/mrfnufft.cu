@@ -134,6 +134,8 @@ struct mrf_plan_s {
   // split-phase CG (C == 1): y = A p of all local frames and the ||p||^2 partials of the row pass
   float2* ycg = nullptr;     // [L][M]
   double2* pnp = nullptr;    // [L * rowblocks * 4]
+  float2* hacg = nullptr;    // Toeplitz plans: [L][N][G] adjoint-side half grids of all frames
+  double2* tqp = nullptr;    // Toeplitz plans: [L * S * warps] Parseval partials of <p, A^H A p>
   size_t ndotp = 0;
   CGScalars* sc = nullptr;
   float2* cg_rin = nullptr;  // the vector the fused CG row pass adds to beta p: r (CG) or z (PCG)
@@ -258,6 +260,11 @@ static void fft_shape(int G, int* P, int* Q, int* T) {
   }
 }
 
+static int cols_threads_rt(int G) {   // threads of a column-kernel CTA (SW x T)
+  int P = 0, Q = 0, T = 0;
+  fft_shape(G, &P, &Q, &T);
+  return SW * T;
+}
 template <typename T>
 static mrf_status dev_alloc(mrf_plan_s* pl, T** ptr, size_t count) {
   if (count == 0) count = 1;
@@ -293,7 +300,7 @@ static void free_plan(mrf_plan_s* pl) {
     if (pl->Hs[i]) cudaFree(pl->Hs[i]);
     if (pl->ybufs[i]) cudaFree(pl->ybufs[i]);
   }
-  void* ptrs[] = {pl->ycg, pl->pnp, pl->perm, pl->pc_lam, pl->z, pl->pc_tmp, pl->pc_part,
+  void* ptrs[] = {pl->ycg, pl->pnp, pl->hacg, pl->tqp, pl->perm, pl->pc_lam, pl->z, pl->pc_tmp, pl->pc_part,
                   pl->coils, pl->dap, pl->tw, pl->fchunks, pl->ftab, pl->achunks, pl->atab, pl->fil, pl->r, pl->p, pl->q,
                   pl->part, pl->dotp, pl->sc, pl->hist, pl->stg_x, pl->stg_y, pl->stg_z, pl->ax[0], pl->ax[1],
                   pl->ay[0], pl->ay[1]};
@@ -521,11 +528,12 @@ static mrf_status launch_adj_rows(mrf_plan_s* pl, const float2* H, float2* out, 
 }
 
 template <int G>
-static mrf_status launch_toep_cols(mrf_plan_s* pl, const float2* Hf, float2* Ha, int l0, int nb, cudaStream_t st) {
+static mrf_status launch_toep_cols(mrf_plan_s* pl, const float2* Hf, float2* Ha, int l0, int nb, cudaStream_t st,
+                                   double2* tq = nullptr) {
   const long long items = (long long)nb * pl->C * pl->S;
   ProfScope ps(pl, MRF_K_FWD_COLS, st);
   CUDA_TRY(launch_pdl(k_toep_cols<G>, pgrid(pl, pl->occ_tc, items), cols_threads<G>(), toep_cols_smem<G>(), st, pl->dp(),
-                      Hf, Ha, pl->psf, l0, nb));
+                      Hf, Ha, pl->psf, l0, nb, tq));
   return MRF_OK;
 }
 
@@ -649,6 +657,44 @@ static mrf_status run_cg_split_adj(mrf_plan_s* pl, float mu, cudaStream_t st) {
   return ln.end();
 }
 
+// The same split on Toeplitz plans (C == 1): the forward half (row pass + k_toep_cols) keeps the
+// adjoint-side half grids of every frame and emits the Parseval partials of <p, A^H A p> =
+// sum_k T(k) |FFT(pad p)(k)|^2; the adjoint half is the residual-update row pass.
+template <int G>
+static mrf_status run_cg_split_fwd_toep(mrf_plan_s* pl, float2* xsol, cudaStream_t st) {
+  Lanes ln(pl, st, n_batches(pl));
+  MRF_TRY(ln.begin());
+  float* dap = pl->dap;
+  pl->dap = pl->ones;   // dp() copies: unit deapodisation
+  mrf_status rc = MRF_OK;
+  for (int b = 0, l0 = 0; l0 < pl->L && rc == MRF_OK; ++b, l0 += pl->bf) {
+    const int nb = std::min(pl->bf, pl->L - l0);
+    cudaStream_t s = ln.stream(b);
+    float2* Hf = pl->Hs[ln.slot(b)];
+    rc = launch_fwd_rows_cg<G>(pl, xsol, Hf, l0, nb, s, nullptr, 0, pl->pnp);
+    if (rc == MRF_OK) rc = launch_toep_cols<G>(pl, Hf, pl->hacg + (size_t)l0 * pl->N * pl->G, l0, nb, s, pl->tqp);
+  }
+  pl->dap = dap;
+  MRF_TRY(rc);
+  return ln.end();
+}
+template <int G>
+static mrf_status run_cg_split_adj_toep(mrf_plan_s* pl, float mu, cudaStream_t st) {
+  Lanes ln(pl, st, n_batches(pl));
+  MRF_TRY(ln.begin());
+  float* dap = pl->dap;
+  pl->dap = pl->ones;
+  mrf_status rc = MRF_OK;
+  for (int b = 0, l0 = 0; l0 < pl->L && rc == MRF_OK; ++b, l0 += pl->bf) {
+    const int nb = std::min(pl->bf, pl->L - l0);
+    rc = launch_adj_rows<G>(pl, pl->hacg + (size_t)l0 * pl->N * pl->G, nullptr, pl->p, mu, l0, nb, pl->dotp, ln.stream(b),
+                            pl->r);
+  }
+  pl->dap = dap;
+  MRF_TRY(rc);
+  return ln.end();
+}
+
 // Toeplitz form of run_normal (plans with MRF_NORMAL_TOEPLITZ): row FFT of pad(S_c x) (no
 // deapodisation), k_toep_cols (column FFT, x PSF spectrum, column iFFT), row iFFT + conj-coil sum.
 template <int G>
@@ -700,9 +746,15 @@ static mrf_status do_normal(mrf_plan_s* pl, const float2* x, float2* out, float 
 }
 static mrf_status do_setup(mrf_plan_s* pl) { DISPATCH_G(pl, setup_kernels, pl); }
 static mrf_status do_cg_split_fwd(mrf_plan_s* pl, float2* xsol, cudaStream_t st) {
+  if (pl->flags & MRF_NORMAL_TOEPLITZ) {
+    DISPATCH_G(pl, run_cg_split_fwd_toep, pl, xsol, st);
+  }
   DISPATCH_G(pl, run_cg_split_fwd, pl, xsol, st);
 }
 static mrf_status do_cg_split_adj(mrf_plan_s* pl, float mu, cudaStream_t st) {
+  if (pl->flags & MRF_NORMAL_TOEPLITZ) {
+    DISPATCH_G(pl, run_cg_split_adj_toep, pl, mu, st);
+  }
   DISPATCH_G(pl, run_cg_split_adj, pl, mu, st);
 }
 
@@ -945,7 +997,8 @@ static mrf_status run_cg_launch(mrf_plan_s* pl, const float2* y, const float2* z
   }
   *iters_done = n_iter;
   const bool comm = pl->nccl_comm || pl->host_ar;
-  const bool split = pl->ycg && !pc && pl->C == 1 && !(pl->flags & MRF_NORMAL_TOEPLITZ);
+  const bool toep = (pl->flags & MRF_NORMAL_TOEPLITZ) != 0;
+  const bool split = !pc && pl->C == 1 && (toep ? pl->hacg != nullptr : pl->ycg != nullptr);
   for (int k = 0; k < n_iter; ++k) {
     if (tol > 0.f && res0 == 0.0) { *iters_done = 0; break; }
     if (pl->C > 1) {   // unfused p / x update (the multi-coil row pass reads the image once per coil)
@@ -953,17 +1006,24 @@ static mrf_status run_cg_launch(mrf_plan_s* pl, const float2* y, const float2* z
       k_cg_px<<<nblk, kVecThreads, 0, st>>>(x, pl->p, rin, n, pl->sc);
       MRF_TRY(vec_launch_check("k_cg_px"));
     }
-    if (split) {   // alpha from ||A p||^2 + mu ||p||^2; the adjoint half advances r and emits <r, r>
+    if (split) {   // alpha from <p, A^H A p> + mu ||p||^2; the adjoint half advances r and emits <r, r>
       MRF_TRY(do_cg_split_fwd(pl, x, st));
-      const size_t ny = (size_t)pl->L * pl->M;
-      const int nbly = vec_blocks(ny);
       {
         ProfScope ps(pl, MRF_K_CG_VEC, st);
-        k_sqnorm<<<nbly, kVecThreads, 0, st>>>(pl->ycg, ny, pl->part);
-        MRF_TRY(vec_launch_check("k_sqnorm"));
+        const double2* pa = pl->part;   // gridding: ||y||^2 partials of y = A p; Toeplitz: Parseval partials
+        int na = 0;
+        if (toep) {
+          pa = pl->tqp;
+          na = pl->L * pl->C * pl->S * (cols_threads_rt(pl->G) / 32);
+        } else {
+          const size_t ny = (size_t)pl->L * pl->M;
+          na = vec_blocks(ny);
+          k_sqnorm<<<na, kVecThreads, 0, st>>>(pl->ycg, ny, pl->part);
+          MRF_TRY(vec_launch_check("k_sqnorm"));
+        }
         const int npn = (int)(pl->ndotp * (kRowThreads / 32));
-        if (comm) k_reduce_pq<kRedPlain><<<1, kReduceThreads, 0, st>>>(pl->part, nbly, pl->pnp, npn, (double)mu, &pl->sc->pq, pl->sc, hist_a, k);
-        else k_reduce_pq<kRedAlpha><<<1, kReduceThreads, 0, st>>>(pl->part, nbly, pl->pnp, npn, (double)mu, &pl->sc->pq, pl->sc, hist_a, k);
+        if (comm) k_reduce_pq<kRedPlain><<<1, kReduceThreads, 0, st>>>(pa, na, pl->pnp, npn, (double)mu, &pl->sc->pq, pl->sc, hist_a, k);
+        else k_reduce_pq<kRedAlpha><<<1, kReduceThreads, 0, st>>>(pa, na, pl->pnp, npn, (double)mu, &pl->sc->pq, pl->sc, hist_a, k);
         MRF_TRY(vec_launch_check("k_reduce_pq"));
       }
       if (comm) {
@@ -1555,6 +1615,8 @@ mrf_status mrf_plan_create(const mrf_plan_desc* d, mrf_plan* out) {
   // ---- batch size: frames per launch (per lane) ---------------------------------------------------
   const size_t per_frame = (size_t)C * N * G * sizeof(float2);
   int bf = d->batch_frames;
+  if (bf == 0)
+    if (const char* e = std::getenv("MRF_BF")) bf = std::max(0, std::atoi(e));   // experiment knob
   if (bf == 0) {
     // per lane; measured: launch-tail amortisation beats L2 residency (MRF: 128 MB); multi-coil
     // batches hold C x the half grid per frame, and 1 GB keeps their row passes (the coil sum is
@@ -1581,11 +1643,17 @@ mrf_status mrf_plan_create(const mrf_plan_desc* d, mrf_plan* out) {
   if (d->coils && C >= 1) {
     if ((s = dev_alloc(pl, &pl->coils, (size_t)C * N * N))) return bail(s);
   }
-  if (C == 1 && !(d->flags & MRF_NORMAL_TOEPLITZ)) {   // split-phase CG (MRF_CG_SPLIT=0 disables)
+  if (C == 1) {   // split-phase CG (MRF_CG_SPLIT=0 disables)
     const char* e = std::getenv("MRF_CG_SPLIT");
-    if (!(e && e[0] == '0'))
-      if ((s = dev_alloc(pl, &pl->ycg, (size_t)L * M)) || (s = dev_alloc(pl, &pl->pnp, pl->ndotp * (kRowThreads / 32))))
+    if (!(e && e[0] == '0')) {
+      if ((s = dev_alloc(pl, &pl->pnp, pl->ndotp * (kRowThreads / 32)))) return bail(s);
+      if (!(d->flags & MRF_NORMAL_TOEPLITZ)) {
+        if ((s = dev_alloc(pl, &pl->ycg, (size_t)L * M))) return bail(s);
+      } else if ((s = dev_alloc(pl, &pl->hacg, (size_t)L * N * G)) ||
+                 (s = dev_alloc(pl, &pl->tqp, (size_t)L * (G / SW) * (SW * 32 / 32)))) {   // S items x warps
         return bail(s);
+      }
+    }
   }
   pl->nlanes = std::min(kDefaultLanes, (L + bf - 1) / bf);
   if (const char* e = std::getenv("MRF_LANES")) pl->nlanes = std::max(1, std::min(kMaxLanes, std::atoi(e)));
