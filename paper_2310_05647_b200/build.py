@@ -32,20 +32,29 @@ def up_to_date() -> bool:
     return all(os.path.getmtime(d) <= t for d in DEPS if os.path.exists(d))
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and up_to_date():
-        return LIB
-    cmd = [nvcc(), *NVCC_FLAGS, "-o", LIB + ".tmp", *SOURCES, "-ldl"]
+CHECKS_LIB = os.path.join(HERE, "libmrfnufft_checks.so")
+
+
+def build(force: bool = False, verbose: bool = False, checks: bool = False) -> str:
+    """checks=True: the bounds-checked variant libmrfnufft_checks.so (-DMRF_CHECKS: every index read
+    from a plan table or a staged chunk is tested in the kernels, a failure traps).
+    Test infrastructure only (tests/test_gpu_checks.py loads it through MRF_LIB_PATH)."""
+    lib = CHECKS_LIB if checks else LIB
+    if not force and os.path.exists(lib) and all(os.path.getmtime(d) <= os.path.getmtime(lib) for d in DEPS
+                                                 if os.path.exists(d)):
+        return lib
+    cmd = [nvcc(), *NVCC_FLAGS, "-o", lib + ".tmp", *SOURCES, "-ldl"]
+    if checks:
+        cmd.insert(1, "-DMRF_CHECKS")
     if os.environ.get("MRF_EXPERIMENTS"):
         cmd.insert(1, "-DMRF_EXPERIMENTS")
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
         print(" ".join(cmd), flush=True)
     subprocess.run(cmd, check=True)
-    os.replace(LIB + ".tmp", LIB)
-    return LIB
+    os.replace(lib + ".tmp", lib)
+    return lib
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose="-v" in sys.argv)
-    print(LIB)
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, checks="--checks" in sys.argv))

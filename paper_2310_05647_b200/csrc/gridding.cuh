@@ -21,6 +21,26 @@
 
 #include "fft.cuh"
 
+// Device-side bounds checks (the checks build, -DMRF_CHECKS: libmrfnufft_checks.so):
+// every index that comes from a plan table or a staged chunk is tested before use; a failure
+// prints the condition and traps (the launch fails, the host sees MRF_ECUDA).  Compiled out of
+// the production build.
+#ifdef MRF_CHECKS
+#include <cstdio>
+#define MRF_CHECK(cond)                                                                       \
+  do {                                                                                        \
+    if (!(cond)) {                                                                            \
+      printf("MRF_CHECK failed at %s:%d: %s (block %d thread %d)\n", __FILE__, __LINE__, #cond, \
+             (int)blockIdx.x, (int)threadIdx.x);                                              \
+      __trap();                                                                               \
+    }                                                                                         \
+  } while (0)
+#else
+#define MRF_CHECK(cond) \
+  do {                  \
+  } while (0)
+#endif
+
 namespace mrf {
 
 constexpr int SW = 16;             // columns per strip (>= W: a point's x-taps touch <= 2 strips)
@@ -210,7 +230,7 @@ struct PhaseTimer {
 // last column (weight 0 by construction) read finite values.  Each y_j receives
 // at most two strip partials, added with fp32 atomics onto 0 (order independent).
 template <int G, int W, bool GL>
-__device__ __forceinline__ void gather_rec(const int* rp, const float2* strip, float2* __restrict__ yf) {
+__device__ __forceinline__ void gather_rec(const int* rp, const float2* strip, float2* __restrict__ yf, int M) {
   constexpr int RW = (2 + 2 * W + 3) & ~3;
   int wd[RW];
 #pragma unroll
@@ -222,6 +242,7 @@ __device__ __forceinline__ void gather_rec(const int* rp, const float2* strip, f
     wd[4 * k + 3] = q.w;
   }
   const int gy0 = wd[1] & 2047, cx0 = (wd[1] >> 11) & 31;
+  MRF_CHECK((unsigned)wd[0] < (unsigned)M && gy0 < G && cx0 < SW);
   float2 acc = make_float2(0.f, 0.f);
 #pragma unroll
   for (int ty = 0; ty < W; ++ty) {
@@ -238,10 +259,11 @@ __device__ __forceinline__ void gather_rec(const int* rp, const float2* strip, f
 }
 // The same for any W in [2, 16] (run-time loops; rp may point to shared or global memory).
 template <int G>
-__device__ __forceinline__ void gather_rec_any(const int* rp, int W, const float2* strip, float2* __restrict__ yf) {
+__device__ __forceinline__ void gather_rec_any(const int* rp, int W, const float2* strip, float2* __restrict__ yf, int M) {
   auto word = [&](int w) { return rp[(w >> 2) * 128 + (w & 3)]; };   // record word w (interleaved layout)
   auto wt = [&](int w) { return __int_as_float(word(w)); };
   const int gy0 = word(1) & 2047, cx0 = (word(1) >> 11) & 31;
+  MRF_CHECK((unsigned)word(0) < (unsigned)M && gy0 < G && cx0 < SW);
   float2 acc = make_float2(0.f, 0.f);
   for (int ty = 0; ty < W; ++ty) {
     const float2* row = strip + ((gy0 + ty) & (G - 1)) * SWG + cx0;
@@ -517,13 +539,13 @@ k_fwd_cols(DevPlan p, const float2* __restrict__ H, float2* __restrict__ y, int 
       for (int e = tid; e < n_rec; e += blockDim.x) {
         const int ro = (e >> 5) * recw * 32 + (e & 31) * 4;   // word offset of the record's piece 0
         if (W == 6) {
-          if (e < n_st) gather_rec<G, 6, false>(recs + ro, strip, yf);
-          else gather_rec<G, 6, true>(grecs + ro, strip, yf);
+          if (e < n_st) gather_rec<G, 6, false>(recs + ro, strip, yf, p.M);
+          else gather_rec<G, 6, true>(grecs + ro, strip, yf, p.M);
         } else if (W == 8) {
-          if (e < n_st) gather_rec<G, 8, false>(recs + ro, strip, yf);
-          else gather_rec<G, 8, true>(grecs + ro, strip, yf);
+          if (e < n_st) gather_rec<G, 8, false>(recs + ro, strip, yf, p.M);
+          else gather_rec<G, 8, true>(grecs + ro, strip, yf, p.M);
         } else {
-          gather_rec_any<G>((e < n_st ? recs : grecs) + ro, W, strip, yf);
+          gather_rec_any<G>((e < n_st ? recs : grecs) + ro, W, strip, yf, p.M);
         }
       }
     }
@@ -551,7 +573,8 @@ __device__ __forceinline__ void spread_cells(const int2* sl_tab, const unsigned 
                                              const int2* __restrict__ gents, int n_staged, int e0, int sl_lo,
                                              int sl_hi, bool from_l2, int nsl, int n_multi, const float2* ys,
                                              const float2* __restrict__ yf, float2* strip, int tid, int nthreads,
-                                             int warp, int nwarps, int lane) {
+                                             int warp, int nwarps, int lane, int M, int ncell, int nent) {
+  (void)M; (void)ncell; (void)nent;   // bounds of the checks build (MRF_CHECK)
   if (PASS == 0) {
     const int n1 = (nsl - n_multi) * 32;
     const unsigned short* cells1 = cells + n_multi * 32;
@@ -565,8 +588,10 @@ __device__ __forceinline__ void spread_cells(const int2* sl_tab, const unsigned 
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const int ii = i + u * nthreads;
+        MRF_CHECK(ii < nent);
         cl[u] = cells1[ii];
         e[u] = ii < n_staged ? ents[ii] : __ldg(gents + ii);
+        MRF_CHECK((unsigned)e[u].x < (unsigned)M && (cl[u] == 0xFFFF || cl[u] < ncell));
       }
 #pragma unroll
       for (int u = 0; u < 4; ++u) v[u] = YS ? ys[e[u].x] : __ldg(yf + e[u].x);
@@ -575,8 +600,10 @@ __device__ __forceinline__ void spread_cells(const int2* sl_tab, const unsigned 
         if (cl[u] != 0xFFFF) strip[cl[u]] = cscale(v[u], __int_as_float(e[u].y));
     }
     for (; i < n1; i += nthreads) {
+      MRF_CHECK(i < nent);
       const int cell = cells1[i];
       const int2 e = i < n_staged ? ents[i] : __ldg(gents + i);
+      MRF_CHECK((unsigned)e.x < (unsigned)M && (cell == 0xFFFF || cell < ncell));
       const float wgt = __int_as_float(e.y);
       const float2 v = YS ? ys[e.x] : __ldg(yf + e.x);
       if (cell != 0xFFFF) strip[cell] = cscale(v, wgt);
@@ -589,6 +616,8 @@ __device__ __forceinline__ void spread_cells(const int2* sl_tab, const unsigned 
     const int width = abs(si.y);   // si.y < 0: the 32 lanes share one cell (warp reduction)
     if (PASS == 0 && si.x + 32 * width > n_staged) break;   // firsts increase with sl
     const int cell = cells[sl * 32 + lane];
+    MRF_CHECK(cell == 0xFFFF || cell < ncell);
+    MRF_CHECK(si.x + 32 * width <= nent);
     float2 acc = make_float2(0.f, 0.f);
     if (!from_l2) {
       const int2* ep = ents + (si.x - e0) + lane;
@@ -597,7 +626,10 @@ __device__ __forceinline__ void spread_cells(const int2* sl_tab, const unsigned 
         int2 e[4];
         float2 v[4];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) e[u] = ep[(kk + u) * 32];
+        for (int u = 0; u < 4; ++u) {
+          e[u] = ep[(kk + u) * 32];
+          MRF_CHECK((unsigned)e[u].x < (unsigned)M);
+        }
 #pragma unroll
         for (int u = 0; u < 4; ++u) v[u] = YS ? ys[e[u].x] : __ldg(yf + e[u].x);
 #pragma unroll
@@ -719,14 +751,16 @@ k_adj_cols(DevPlan p, const float2* __restrict__ y, float2* __restrict__ H, int 
       const int2* sl_tab = reinterpret_cast<const int2*>(stage + kAdjHdr);
       const unsigned short* cells = reinterpret_cast<const unsigned short*>(stage + cells_off);
       const int2* ents = reinterpret_cast<const int2*>(stage + ent_off);
+      MRF_CHECK(cells_off >= kAdjHdr && ent_off >= cells_off && ent_off * 4 <= copied && copied <= chunk_words * 4);
+      MRF_CHECK(nsl >= n_multi && n_multi >= 0 && (chunk_words - ent_off) / 2 >= 32 * (nsl - n_multi));
       const int n_staged = (copied / 4 - ent_off) / 2;          // entries in shared memory
       const int2* gents = reinterpret_cast<const int2*>(p.achunks + chunk_off + ent_off);
       if (ystage)
         spread_cells<true, 0>(sl_tab, cells, ents, gents, n_staged, 0, 0, 0, false, nsl, n_multi, ys, yf, strip, tid,
-                              blockDim.x, warp, nwarps, lane);
+                              blockDim.x, warp, nwarps, lane, M, G * SW, (chunk_words - ent_off) / 2);
       else
         spread_cells<false, 0>(sl_tab, cells, ents, gents, n_staged, 0, 0, 0, false, nsl, n_multi, ys, yf, strip,
-                               tid, blockDim.x, warp, nwarps, lane);
+                               tid, blockDim.x, warp, nwarps, lane, M, G * SW, (chunk_words - ent_off) / 2);
       if (copied < chunk_words * 4) {   // chunk larger than the staging buffer (block-uniform)
         // The wide slices past the staged prefix: windows of whole slices brought in by further
         // bulk copies over the (consumed) entry region; a slice wider than the region reads L2.
@@ -757,10 +791,10 @@ k_adj_cols(DevPlan p, const float2* __restrict__ y, float2* __restrict__ H, int 
           }
           if (ystage)
             spread_cells<true, 1>(sl_tab, cells, ents, gents, n_staged, wv.x, sl0, wv.y, wv.z != 0, nsl, n_multi, ys,
-                                  yf, strip, tid, blockDim.x, warp, nwarps, lane);
+                                  yf, strip, tid, blockDim.x, warp, nwarps, lane, M, G * SW, (chunk_words - ent_off) / 2);
           else
             spread_cells<false, 1>(sl_tab, cells, ents, gents, n_staged, wv.x, sl0, wv.y, wv.z != 0, nsl, n_multi, ys,
-                                   yf, strip, tid, blockDim.x, warp, nwarps, lane);
+                                   yf, strip, tid, blockDim.x, warp, nwarps, lane, M, G * SW, (chunk_words - ent_off) / 2);
           sl0 = wv.y;
         }
       }

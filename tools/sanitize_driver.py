@@ -28,8 +28,10 @@ def dev(a):
 def ops():
     # pr1 (G = 64), a 64^2 multi-batch plan (G = 128, two lanes), a 128^2 stress-like spiral
     # (G = 256, cells with > 128 spread entries -> reduction slices) with 4 coils
+    # plus the MRF shape (G = 512), G = 1024 and the W extremes 2 and 16
     cases = [("pr1", {}, None, 0), ("cfg2", dict(N=64, L=24), None, 8),
-             ("stress", dict(N=128, L=6, C=4), 4, 3)]
+             ("stress", dict(N=128, L=6, C=4), 4, 3), ("mrf", dict(L=8), None, 4),
+             ("cfg2", dict(N=512, L=2), None, 0), ("pr1", dict(W=2), None, 0), ("pr1", dict(W=16), None, 0)]
     for name, over, C, bf in cases:
         cfg = synth.get_config(name, **over)
         traj = synth.spiral_trajectory(cfg.M, cfg.R, cfg.turns, cfg.p)
@@ -47,7 +49,7 @@ def ops():
             pl.dc_cg(y, mu=cfg.mu, n_iter=2, tol=1e-3)
             torch.cuda.synchronize()
             pl.close()
-        print(f"ops {name}: ok", flush=True)
+        print(f"ops {name} N={cfg.N} W={cfg.W}: ok", flush=True)
 
 
 def dictionary():
