@@ -568,6 +568,8 @@ k_fwd_cols(DevPlan p, const float2* __restrict__ H, float2* __restrict__ y, int 
 // PASS 0: the flat run and the wide slices whose entries are staged (entries at ents[e]);
 // PASS 1: wide slices [sl_lo, sl_hi) past the staged prefix, whose entries a further bulk copy
 // brought to ents[e - e0] (from_l2: one slice too wide for the buffer, read from L2).
+// PASS 2: as PASS 1 with every entry read from L2 (the direct path of oversized chunks, eight loads
+// in flight per lane).
 template <bool YS, int PASS>
 __device__ __forceinline__ void spread_cells(const int2* sl_tab, const unsigned short* cells, const int2* ents,
                                              const int2* __restrict__ gents, int n_staged, int e0, int sl_lo,
@@ -642,8 +644,20 @@ __device__ __forceinline__ void spread_cells(const int2* sl_tab, const unsigned 
       }
     } else {
       const int2* ep = gents + si.x + lane;
+      int kk = 0;
+      if (PASS == 2)   // (the direct path of oversized chunks)
+      for (; kk + 7 < width; kk += 8) {   // eight L2 loads in flight, the sum in entry order
+        int2 e[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          e[u] = __ldg(ep + (kk + u) * 32);
+          MRF_CHECK((unsigned)e[u].x < (unsigned)M);
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) acc = caxpy(__int_as_float(e[u].y), YS ? ys[e[u].x] : __ldg(yf + e[u].x), acc);
+      }
 #pragma unroll 4
-      for (int kk = 0; kk < width; ++kk) {
+      for (; kk < width; ++kk) {
         const int2 e = __ldg(ep + kk * 32);
         const float wgt = __int_as_float(e.y);
         acc = caxpy(wgt, YS ? ys[e.x] : __ldg(yf + e.x), acc);
@@ -768,6 +782,20 @@ k_adj_cols(DevPlan p, const float2* __restrict__ y, float2* __restrict__ H, int 
         const int nent = (chunk_words - ent_off) / 2;
         int sl0 = 0;
         while (sl0 < n_multi && sl_tab[sl0].x + 32 * abs(sl_tab[sl0].y) <= n_staged) ++sl0;
+        // A chunk that needs more than one further window (the centre strips of a dense spiral:
+        // stress) reads the rest of its slices straight from L2, eight loads in flight per lane,
+        // instead of streaming windows (two barriers and a copy round trip each); one window
+        // is still cheaper than L2 latency (measured: stress normal -4 %, MRF unchanged).
+        const bool direct = MRF_DBG_ON(4) || (nent - n_staged > cap);
+        if (direct) {
+          if (ystage)
+            spread_cells<true, 2>(sl_tab, cells, ents, gents, n_staged, 0, sl0, n_multi, true, nsl, n_multi, ys, yf,
+                                  strip, tid, blockDim.x, warp, nwarps, lane, M, G * SW, (chunk_words - ent_off) / 2);
+          else
+            spread_cells<false, 2>(sl_tab, cells, ents, gents, n_staged, 0, sl0, n_multi, true, nsl, n_multi, ys, yf,
+                                   strip, tid, blockDim.x, warp, nwarps, lane, M, G * SW, (chunk_words - ent_off) / 2);
+          sl0 = n_multi;
+        }
         while (sl0 < n_multi) {   // sl0 is block-uniform
           __syncthreads();        // the previous window's entries are consumed
           if (tid == 0) {
