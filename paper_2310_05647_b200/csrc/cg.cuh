@@ -261,10 +261,12 @@ __global__ void __launch_bounds__(kVecThreads) k_cg_xfin(float2* __restrict__ x,
   })
 }
 
-// x += alpha p_old ; p = r + beta p_old   (unfused form, used when C > 1)
+// x += alpha p_old ; p = r + beta p_old   (unfused form, used when C > 1); with part != nullptr
+// also the block partials of ||p||^2 (split-phase CG)
 __global__ void __launch_bounds__(kVecThreads) k_cg_px(float2* __restrict__ x, float2* __restrict__ pv,
                                                        const float2* __restrict__ r, size_t n,
-                                                       const CGScalars* __restrict__ sc) {
+                                                       const CGScalars* __restrict__ sc, double2* __restrict__ part) {
+  double2 s = make_double2(0.0, 0.0);
   const float alpha = (float)sc->alpha, beta = (float)sc->beta;
   float4* p4 = reinterpret_cast<float4*>(pv);
   float4* x4 = reinterpret_cast<float4*>(x);
@@ -277,8 +279,14 @@ __global__ void __launch_bounds__(kVecThreads) k_cg_px(float2* __restrict__ x, f
     xi.z = fmaf(alpha, pi.z, xi.z);
     xi.w = fmaf(alpha, pi.w, xi.w);
     x4[i] = xi;
-    p4[i] = make_float4(fmaf(beta, pi.x, ri.x), fmaf(beta, pi.y, ri.y), fmaf(beta, pi.z, ri.z), fmaf(beta, pi.w, ri.w));
+    const float4 pn = make_float4(fmaf(beta, pi.x, ri.x), fmaf(beta, pi.y, ri.y), fmaf(beta, pi.z, ri.z), fmaf(beta, pi.w, ri.w));
+    p4[i] = pn;
+    s.x += norm2d(pn);
   })
+  if (part) {
+    s = block_sum2(s);
+    if (threadIdx.x == 0) part[blockIdx.x] = s;
+  }
 }
 
 __global__ void k_cg_beta(CGScalars* sc, double* hist, double* hb, int k) { cg_beta(sc, hist, hb, k); }

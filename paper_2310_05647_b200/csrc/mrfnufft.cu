@@ -637,8 +637,10 @@ static mrf_status run_cg_split_fwd(mrf_plan_s* pl, float2* xsol, cudaStream_t st
     const int nb = std::min(pl->bf, pl->L - l0);
     cudaStream_t s = ln.stream(b);
     float2* H = pl->Hs[ln.slot(b)];
-    float2* yb = pl->ycg + (size_t)l0 * pl->M;
-    MRF_TRY(launch_fwd_rows_cg<G>(pl, xsol, H, l0, nb, s, yb, (long long)nb * pl->M, pl->pnp));
+    float2* yb = pl->ycg + (size_t)l0 * pl->C * pl->M;
+    const long long ny = (long long)nb * pl->C * pl->M;   // zeroed by the row pass for the gather
+    if (pl->C == 1) MRF_TRY(launch_fwd_rows_cg<G>(pl, xsol, H, l0, nb, s, yb, ny, pl->pnp));
+    else MRF_TRY(launch_fwd_rows<G>(pl, pl->p, H, l0, nb, s, yb, ny));   // p, x formed by k_cg_px
     MRF_TRY(launch_fwd_cols<G>(pl, H, yb, l0, nb, s));
   }
   return ln.end();
@@ -651,7 +653,7 @@ static mrf_status run_cg_split_adj(mrf_plan_s* pl, float mu, cudaStream_t st) {
     const int nb = std::min(pl->bf, pl->L - l0);
     cudaStream_t s = ln.stream(b);
     float2* H = pl->Hs[ln.slot(b)];
-    MRF_TRY(launch_adj_cols<G>(pl, pl->ycg + (size_t)l0 * pl->M, H, l0, nb, s));
+    MRF_TRY(launch_adj_cols<G>(pl, pl->ycg + (size_t)l0 * pl->C * pl->M, H, l0, nb, s));
     MRF_TRY(launch_adj_rows<G>(pl, H, nullptr, pl->p, mu, l0, nb, pl->dotp, s, pl->r));
   }
   return ln.end();
@@ -998,12 +1000,12 @@ static mrf_status run_cg_launch(mrf_plan_s* pl, const float2* y, const float2* z
   *iters_done = n_iter;
   const bool comm = pl->nccl_comm || pl->host_ar;
   const bool toep = (pl->flags & MRF_NORMAL_TOEPLITZ) != 0;
-  const bool split = !pc && pl->C == 1 && (toep ? pl->hacg != nullptr : pl->ycg != nullptr);
+  const bool split = !pc && (toep ? pl->C == 1 && pl->hacg != nullptr : pl->ycg != nullptr);
   for (int k = 0; k < n_iter; ++k) {
     if (tol > 0.f && res0 == 0.0) { *iters_done = 0; break; }
     if (pl->C > 1) {   // unfused p / x update (the multi-coil row pass reads the image once per coil)
       ProfScope ps(pl, MRF_K_CG_VEC, st);
-      k_cg_px<<<nblk, kVecThreads, 0, st>>>(x, pl->p, rin, n, pl->sc);
+      k_cg_px<<<nblk, kVecThreads, 0, st>>>(x, pl->p, rin, n, pl->sc, split ? pl->pnp : nullptr);
       MRF_TRY(vec_launch_check("k_cg_px"));
     }
     if (split) {   // alpha from <p, A^H A p> + mu ||p||^2; the adjoint half advances r and emits <r, r>
@@ -1016,12 +1018,14 @@ static mrf_status run_cg_launch(mrf_plan_s* pl, const float2* y, const float2* z
           pa = pl->tqp;
           na = pl->L * pl->C * pl->S * (cols_threads_rt(pl->G) / 32);
         } else {
-          const size_t ny = (size_t)pl->L * pl->M;
+          const size_t ny = (size_t)pl->L * pl->C * pl->M;
           na = vec_blocks(ny);
           k_sqnorm<<<na, kVecThreads, 0, st>>>(pl->ycg, ny, pl->part);
           MRF_TRY(vec_launch_check("k_sqnorm"));
         }
-        const int npn = (int)(pl->ndotp * (kRowThreads / 32));
+        // ||p||^2 partials: per warp and row item from the fused row pass (C == 1), per block from
+        // k_cg_px (C > 1)
+        const int npn = pl->C == 1 ? (int)(pl->ndotp * (kRowThreads / 32)) : nblk;
         if (comm) k_reduce_pq<kRedPlain><<<1, kReduceThreads, 0, st>>>(pa, na, pl->pnp, npn, (double)mu, &pl->sc->pq, pl->sc, hist_a, k);
         else k_reduce_pq<kRedAlpha><<<1, kReduceThreads, 0, st>>>(pa, na, pl->pnp, npn, (double)mu, &pl->sc->pq, pl->sc, hist_a, k);
         MRF_TRY(vec_launch_check("k_reduce_pq"));
@@ -1643,12 +1647,12 @@ mrf_status mrf_plan_create(const mrf_plan_desc* d, mrf_plan* out) {
   if (d->coils && C >= 1) {
     if ((s = dev_alloc(pl, &pl->coils, (size_t)C * N * N))) return bail(s);
   }
-  if (C == 1) {   // split-phase CG (MRF_CG_SPLIT=0 disables)
+  {   // split-phase CG (MRF_CG_SPLIT=0 disables): gridding plans of any C, Toeplitz plans with C == 1
     const char* e = std::getenv("MRF_CG_SPLIT");
-    if (!(e && e[0] == '0')) {
-      if ((s = dev_alloc(pl, &pl->pnp, pl->ndotp * (kRowThreads / 32)))) return bail(s);
+    if (!(e && e[0] == '0') && (C == 1 || !(d->flags & MRF_NORMAL_TOEPLITZ))) {
+      if ((s = dev_alloc(pl, &pl->pnp, std::max<size_t>(pl->ndotp * (kRowThreads / 32), kPartBlocks)))) return bail(s);
       if (!(d->flags & MRF_NORMAL_TOEPLITZ)) {
-        if ((s = dev_alloc(pl, &pl->ycg, (size_t)L * M))) return bail(s);
+        if ((s = dev_alloc(pl, &pl->ycg, (size_t)L * C * M))) return bail(s);
       } else if ((s = dev_alloc(pl, &pl->hacg, (size_t)L * N * G)) ||
                  (s = dev_alloc(pl, &pl->tqp, (size_t)L * (G / SW) * (SW * 32 / 32)))) {   // S items x warps
         return bail(s);

@@ -592,14 +592,14 @@ def test_stagewise_half_grids(mrf, name, over):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("normal", ["gridding", "toeplitz"])
-def test_split_phase_cg_matches_textbook_cg(mrf, monkeypatch, normal):
+@pytest.mark.parametrize("name,normal", [("cfg2", "gridding"), ("cfg2", "toeplitz"), ("sense", "gridding")])
+def test_split_phase_cg_matches_textbook_cg(mrf, monkeypatch, name, normal):
     """The split-phase CG (alpha = rho / (<p, A^H A p> + mu ||p||^2) with <p, A^H A p> = ||A p||^2 on
     gridding plans and sum_k T(k) |FFT(pad p)|^2 (Parseval) on Toeplitz plans, r advanced inside the
     adjoint row pass; reading 30) against the textbook loop (alpha = rho / Re<p, q>,
     separate r update; MRF_CG_SPLIT=0) on the same plan inputs: the two are the same iteration in
     exact arithmetic, so their iterates agree to fp32 rounding."""
-    cfg, traj, coils, frames, x = setup("cfg2", frames=range(40))
+    cfg, traj, coils, frames, x = setup(name, frames=range(40 if name == "cfg2" else 12))
     y = host(plan_for(mrf, cfg, traj, coils, frames).forward(dev(x)))
     out = {}
     for split in ("1", "0"):
