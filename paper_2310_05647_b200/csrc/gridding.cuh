@@ -681,9 +681,14 @@ __device__ __forceinline__ void spread_cells(const int2* sl_tab, const unsigned 
 // summing w * y_j over its (j, w) list (SELL-32 slices, no atomics, deterministic);
 // a5: column iFFT, then the N kept rows are stored strip-major H[fc][strip][iy][16].
 // Pipeline: y[fc] and the chunk of the next item are fetched right after this item's spread.
-template <int G, bool SEP>
+template <int G, bool SEP, bool DYN>
 __global__ void __launch_bounds__(SW * FFTShape<G>::T, (SEP || G >= 1024) ? 1 : 2)
-k_adj_cols(DevPlan p, const float2* __restrict__ y, float2* __restrict__ H, int l0, int nb, int ystage, int stage_cap) {
+k_adj_cols(DevPlan p, const float2* __restrict__ y, float2* __restrict__ H, int l0, int nb, int ystage, int stage_cap,
+           int* __restrict__ ctr) {
+  // DYN: after its first item (blockIdx.x) a CTA takes the next unclaimed item from the
+  // counter ctr[0] (dynamic hand-out: the strips differ in spread work, and a static round-robin
+  // left the SMs' busy time spread 69 k .. 95 k cycles around an 82 k mean); the last CTA to exit
+  // (ctr[1]) resets both words for the next launch on this lane.
   using F = FFTShape<G>;
   constexpr int P = F::P, Q = F::Q, T = F::T, N = G / 2, A = Q / T, B = P / T, S = G / SW;
   // SEP (G <= 512): the spread strip S and the FFT exchange buffer E are separate, so S only ever
@@ -738,18 +743,31 @@ k_adj_cols(DevPlan p, const float2* __restrict__ y, float2* __restrict__ H, int 
     bulk_g2s(stage, p.achunks + ow.x, bytes, &bars[0]);
     if (ystage) bulk_g2s(ys, y + (size_t)(item / S) * M, (uint32_t)ystage, &bars[0]);
   };
+  __shared__ int s_next[2];   // the CTA's next item, by item parity (written by thread 0)
   int item = blockIdx.x;
   int2 off_next = make_int2(0, 0);
   PhaseTimer pt;
   pt.start(MRF_DBG_ON(2) && tid == 0);
   int nit = 0;
-  if (tid == 0 && item < n_items) {
+  int pend = 0;   // (thread 0, DYN) the hand-out claimed two items ahead: its latency hides behind an item
+  if constexpr (DYN) {
+    if (tid == 0) {
+      const int nx = (int)gridDim.x + atomicAdd(ctr, 1);
+      pend = (int)gridDim.x + atomicAdd(ctr, 1);
+      s_next[0] = nx;
+      if (item < n_items) {
+        issue(item, chunk_of(item));
+        if (nx < n_items) off_next = chunk_of(nx);
+      }
+    }
+  } else if (tid == 0 && item < n_items) {
     issue(item, chunk_of(item));
     if (item + (int)gridDim.x < n_items) off_next = chunk_of(item + gridDim.x);
   }
   for (int k = 0; item < n_items; item += gridDim.x, ++k) {
     const int fc = item / S;
-    const int next = item + gridDim.x;
+    const int snext = item + gridDim.x;   // the static round-robin's next item
+    int next = snext;
     mbar_wait(&bars[0], k & 1);
     pt.mark(0);
     ++nit;
@@ -830,10 +848,18 @@ k_adj_cols(DevPlan p, const float2* __restrict__ y, float2* __restrict__ H, int 
     pt.mark(1);
     __syncthreads();
     pt.mark(2);
+    if (DYN) next = s_next[k & 1];   // written by thread 0 before the barrier above
     if (tid == 0 && next < n_items) {
       fence_proxy_async();
       issue(next, off_next);
-      if (next + (int)gridDim.x < n_items) off_next = chunk_of(next + gridDim.x);
+      if constexpr (DYN) {
+        const int nn = pend;
+        pend = (int)gridDim.x + atomicAdd(ctr, 1);
+        s_next[(k + 1) & 1] = nn;
+        if (nn < n_items) off_next = chunk_of(nn);
+      } else {
+        if (next + (int)gridDim.x < n_items) off_next = chunk_of(next + gridDim.x);
+      }
     }
     // a5: column inverse FFT (e^{+i}, unnormalised); only the N kept rows are stored
     float2 v[A][P];
@@ -905,8 +931,17 @@ k_adj_cols(DevPlan p, const float2* __restrict__ y, float2* __restrict__ H, int 
     // ordered by its own first barrier (every thread is past its stage-2 loads by then).
     if constexpr (!SEP) __syncthreads();
     pt.mark(7);
+    if constexpr (DYN) item = next - (int)gridDim.x;   // (the loop adds gridDim.x back)
   }
   pt.report(p.dbgbuf ? p.dbgbuf + 16 : nullptr, nit);
+  if (DYN && tid == 0) {   // the last CTA out resets the hand-out counter
+    __threadfence();
+    if (atomicAdd(ctr + 1, 1) == (int)gridDim.x - 1) {
+      ctr[0] = 0;
+      ctr[1] = 0;
+      __threadfence();
+    }
+  }
 }
 
 // ============================================================================ Toeplitz columns

@@ -112,6 +112,8 @@ struct mrf_plan_s {
   int2* atab = nullptr;
   int* fil = nullptr;
   int* perm = nullptr;       // [L] interleaf-ordered processing order within each batch (DevPlan::perm)
+  int* ctrs = nullptr;       // [kMaxLanes][8] dynamic item hand-out counters of the column kernels (self-resetting)
+  bool adj_dyn = false;      // k_adj_cols hands items out dynamically (set at plan creation from the chunk sizes)
   // workspaces
   // Frame batches alternate between kLanes internal streams so one batch's kernel tail overlaps
   // the next batch's kernels; each lane owns its half-grid and k-space workspaces.
@@ -300,7 +302,7 @@ static void free_plan(mrf_plan_s* pl) {
     if (pl->Hs[i]) cudaFree(pl->Hs[i]);
     if (pl->ybufs[i]) cudaFree(pl->ybufs[i]);
   }
-  void* ptrs[] = {pl->ycg, pl->pnp, pl->hacg, pl->tqp, pl->perm, pl->pc_lam, pl->z, pl->pc_tmp, pl->pc_part,
+  void* ptrs[] = {pl->ctrs, pl->ycg, pl->pnp, pl->hacg, pl->tqp, pl->perm, pl->pc_lam, pl->z, pl->pc_tmp, pl->pc_part,
                   pl->coils, pl->dap, pl->tw, pl->fchunks, pl->ftab, pl->achunks, pl->atab, pl->fil, pl->r, pl->p, pl->q,
                   pl->part, pl->dotp, pl->sc, pl->hist, pl->stg_x, pl->stg_y, pl->stg_z, pl->ax[0], pl->ax[1],
                   pl->ay[0], pl->ay[1]};
@@ -404,6 +406,19 @@ __global__ void k_dcf_scale(float2* __restrict__ yw, const float2* __restrict__ 
   }
 }
 
+// k_adj_cols variant of the plan: SEP (separate exchange buffer, G <= 512, one CTA per SM) and DYN
+// (dynamic item hand-out; plans whose spread chunks mostly overflow the staging buffer)
+template <int G>
+static void (*adj_cols_kernel(const mrf_plan_s* pl))(DevPlan, const float2*, float2*, int, int, int, int, int*) {
+  if (pl->adj_sep) return pl->adj_dyn ? k_adj_cols<G, (G <= 512), true> : k_adj_cols<G, (G <= 512), false>;
+  return pl->adj_dyn ? k_adj_cols<G, false, true> : k_adj_cols<G, false, false>;
+}
+
+template <int G>
+static mrf_status adj_cols_attr(mrf_plan_s* pl) {   // (after a change of the variant)
+  CUDA_TRY(cudaFuncSetAttribute(adj_cols_kernel<G>(pl), cudaFuncAttributeMaxDynamicSharedMemorySize, pl->acol_smem));
+  return MRF_OK;
+}
 template <int G>
 static mrf_status setup_kernels(mrf_plan_s* pl) {
   const int ncol = cols_threads<G>();
@@ -427,7 +442,7 @@ static mrf_status setup_kernels(mrf_plan_s* pl) {
   CUDA_TRY(cudaFuncSetAttribute(k_adj_rows<G, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s_ar));
   CUDA_TRY(cudaFuncSetAttribute(k_adj_rows<G, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s_ar));
   CUDA_TRY(cudaFuncSetAttribute(k_fwd_cols<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s_col));
-  auto adj_kernel = pl->adj_sep ? k_adj_cols<G, (G <= 512)> : k_adj_cols<G, false>;
+  auto adj_kernel = adj_cols_kernel<G>(pl);
   CUDA_TRY(cudaFuncSetAttribute(adj_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s_acol));
   CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pl->occ_fr0, k_fwd_rows<G, 0>, kRowThreads, s_fr0));
   CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pl->occ_fr1, k_fwd_rows<G, 1>, kRowThreads, s_fr1));
@@ -503,14 +518,15 @@ static mrf_status launch_fwd_cols(mrf_plan_s* pl, const float2* H, float2* y, in
   return MRF_OK;
 }
 template <int G>
-static mrf_status launch_adj_cols(mrf_plan_s* pl, const float2* y, float2* H, int l0, int nb, cudaStream_t st) {
+static mrf_status launch_adj_cols(mrf_plan_s* pl, const float2* y, float2* H, int l0, int nb, cudaStream_t st,
+                                  int slot = 0) {
   const long long items = (long long)nb * pl->C * pl->S;
   const int ys = ((uintptr_t)y % 16 == 0) ? pl->ystage : 0;
   const int stage = ys ? pl->ac_stage : (int)(((size_t)pl->acol_smem - adj_cols_fixed<G>(0, pl->adj_sep)) & ~size_t(15));
   ProfScope ps(pl, MRF_K_ADJ_COLS, st);
-  auto adj_kernel = pl->adj_sep ? k_adj_cols<G, (G <= 512)> : k_adj_cols<G, false>;
+  auto adj_kernel = adj_cols_kernel<G>(pl);
   CUDA_TRY(launch_pdl(adj_kernel, pgrid(pl, pl->occ_ac, items), cols_threads<G>(), pl->acol_smem, st, pl->dp(), y, H,
-                      l0, nb, ys, stage));
+                      l0, nb, ys, stage, pl->adj_dyn ? pl->ctrs + 8 * slot : (int*)nullptr));
   return MRF_OK;
 }
 template <int G>
@@ -594,7 +610,7 @@ static mrf_status run_adjoint(mrf_plan_s* pl, const float2* y, float2* x, cudaSt
     const int nb = std::min(pl->bf, pl->L - l0);
     cudaStream_t s = ln.stream(b);
     float2* H = pl->Hs[ln.slot(b)];
-    MRF_TRY(launch_adj_cols<G>(pl, y + (size_t)l0 * pl->C * pl->M, H, l0, nb, s));
+    MRF_TRY(launch_adj_cols<G>(pl, y + (size_t)l0 * pl->C * pl->M, H, l0, nb, s, ln.slot(b)));
     MRF_TRY(launch_adj_rows<G>(pl, H, x, nullptr, 0.f, l0, nb, nullptr, s));
   }
   return ln.end();
@@ -617,7 +633,7 @@ static mrf_status run_normal(mrf_plan_s* pl, const float2* x, float2* out, float
     if (cg && pl->C == 1) MRF_TRY(launch_fwd_rows_cg<G>(pl, xsol, H, l0, nb, s, yb, ny));
     else MRF_TRY(launch_fwd_rows<G>(pl, x, H, l0, nb, s, yb, ny));
     MRF_TRY(launch_fwd_cols<G>(pl, H, yb, l0, nb, s));
-    MRF_TRY(launch_adj_cols<G>(pl, yb, H, l0, nb, s));
+    MRF_TRY(launch_adj_cols<G>(pl, yb, H, l0, nb, s, ln.slot(b)));
     MRF_TRY(launch_adj_rows<G>(pl, H, out, (mu != 0.f || cg) ? x : nullptr, mu, l0, nb, cg ? pl->dotp : nullptr, s));
   }
   return ln.end();
@@ -653,7 +669,7 @@ static mrf_status run_cg_split_adj(mrf_plan_s* pl, float mu, cudaStream_t st) {
     const int nb = std::min(pl->bf, pl->L - l0);
     cudaStream_t s = ln.stream(b);
     float2* H = pl->Hs[ln.slot(b)];
-    MRF_TRY(launch_adj_cols<G>(pl, pl->ycg + (size_t)l0 * pl->C * pl->M, H, l0, nb, s));
+    MRF_TRY(launch_adj_cols<G>(pl, pl->ycg + (size_t)l0 * pl->C * pl->M, H, l0, nb, s, ln.slot(b)));
     MRF_TRY(launch_adj_rows<G>(pl, H, nullptr, pl->p, mu, l0, nb, pl->dotp, s, pl->r));
   }
   return ln.end();
@@ -1673,11 +1689,28 @@ mrf_status mrf_plan_create(const mrf_plan_desc* d, mrf_plan* out) {
     if (cudaEventCreateWithFlags(&pl->ev_fork, cudaEventDisableTiming) != cudaSuccess)
       return bail(fail(MRF_ECUDA, "event creation failed"));
   }
+  {   // item hand-out counters of k_adj_cols (DYN variant), one pair per lane, self-resetting
+    if ((s = dev_alloc(pl, &pl->ctrs, (size_t)kMaxLanes * 8))) return bail(s);
+    if (cudaMemset(pl->ctrs, 0, (size_t)kMaxLanes * 8 * sizeof(int)) != cudaSuccess) return bail(fail(MRF_ECUDA, "memset"));
+  }
   if ((s = do_setup(pl))) return bail(s);
   if (pl->flags & MRF_NORMAL_TOEPLITZ) {
     if ((s = build_psf(pl, d->traj, st))) return bail(s);
     for (int i = 0; i < pl->nlanes; ++i)
       if ((s = dev_alloc(pl, &pl->Has[i], (size_t)bf * C * N * G))) return bail(s);
+  }
+  {   // dynamic item hand-out in k_adj_cols when the mean spread chunk exceeds half the staging
+      // buffer (the item costs then vary several-fold: stress normal -14 %; on the MRF plan, mean
+      // chunk 24 KB of an 85 KB buffer, the static round-robin is 5 % faster).  MRF_ADJ_DYN=0/1 overrides.
+    double mean = 0.0;
+    for (const int2& ow : atab) mean += ow.y * 4.0;
+    mean /= (double)atab.size();
+    pl->adj_dyn = pl->ctrs && mean > 0.5 * pl->ac_stage;
+    if (const char* e = std::getenv("MRF_ADJ_DYN")) pl->adj_dyn = pl->ctrs && e[0] == '1';
+    if (pl->adj_dyn) {
+      auto k = [&]() { DISPATCH_G(pl, adj_cols_attr, pl); };
+      if ((s = k())) return bail(s);
+    }
   }
   if (std::getenv("MRF_PLAN_STATS")) {   // chunk size distribution (bytes) against the staging buffers
     std::vector<int> a, f;

@@ -610,3 +610,23 @@ def test_split_phase_cg_matches_textbook_cg(mrf, monkeypatch, name, normal):
         pl.close()
     assert rel(out["1"][0], out["0"][0]) < 1e-5
     assert np.allclose(out["1"][1], out["0"][1], rtol=1e-5, atol=0)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["cfg2", "stress"])
+def test_dynamic_item_handout_is_bitwise_identical(mrf, monkeypatch, name):
+    """k_adj_cols hands its items out dynamically on plans whose spread chunks overflow the
+    staging buffer (MRF_ADJ_DYN overrides the plan's choice).  Every item is computed the same
+    whichever CTA takes it, so the adjoint and the normal operator must agree bit for bit between
+    the static round-robin and the dynamic hand-out, on several batches and both lanes."""
+    over = dict(frames=range(3)) if name == "stress" else dict(frames=range(60))
+    cfg, traj, coils, frames, x = setup(name, **over)
+    yr = synth.random_kspace(cfg.C, cfg.M, frames, cfg.seed)
+    out = {}
+    for dyn in ("0", "1"):
+        monkeypatch.setenv("MRF_ADJ_DYN", dyn)
+        pl = plan_for(mrf, cfg, traj, coils, frames, batch_frames=max(1, len(frames) // 3))
+        out[dyn] = (host(pl.adjoint(dev(yr))), host(pl.normal(dev(x), mu=cfg.mu)))
+        pl.close()
+    assert np.array_equal(out["0"][0], out["1"][0])
+    assert np.array_equal(out["0"][1], out["1"][1])
