@@ -290,6 +290,29 @@ __device__ __forceinline__ void r4_combine_halfout(float2 (&v)[R], const float2 
 }
 }  // namespace detail
 
+namespace detail {
+// r4_combine_halfout split over a lane pair (l, l ^ 16): lane half h = 0 holds D0, D2 (da, db),
+// h = 1 holds D1, D3.  Each forms its first butterfly (s02, d02 or f, g), the pair swaps d02 and
+// f by shuffle, and h = 0 produces X[K] = s02 + W^K f, h = 1 X[K + 3R/4] = d02 + W^{K + 3R/4} g
+// -- operation for operation what r4_combine_halfout computes in one thread.
+template <int R, int SIGN, int K>
+__device__ __forceinline__ void t2_combine(float2 (&out)[R / 4], const float2 (&da)[R / 4], const float2 (&db)[R / 4],
+                                           int h) {
+  if constexpr (K < R / 4) {
+    float2 s, d;
+    bfly_w<R, 2 * K, SIGN>(da[K], db[K], s, d);   // h = 0: s02, d02;  h = 1: f, g
+    const float2 send = h ? s : d;                // h = 0 gives d02 away, h = 1 gives f away
+    float2 recv;
+    recv.x = __shfl_xor_sync(0xffffffffu, send.x, 16);
+    recv.y = __shfl_xor_sync(0xffffffffu, send.y, 16);
+    const float2 lo = madd_w<R, K, SIGN>(s, recv);               // (h = 0) s02 + W^K f
+    const float2 hi = madd_w<R, K + 3 * R / 4, SIGN>(recv, d);   // (h = 1) d02 + W^{K + 3R/4} g
+    out[K] = h ? hi : lo;
+    t2_combine<R, SIGN, K + 1>(out, da, db, h);
+  }
+}
+}  // namespace detail
+
 // R-point DFT (natural order) that produces only the outputs k < R/4 and k >= 3R/4 -- the kept
 // (cropped) half of the oversampled grid in the adjoint.  The other
 // entries of v are left unspecified.  The last butterfly stage skips the two dropped outputs.

@@ -681,8 +681,14 @@ __device__ __forceinline__ void spread_cells(const int2* sl_tab, const unsigned 
 // summing w * y_j over its (j, w) list (SELL-32 slices, no atomics, deterministic);
 // a5: column iFFT, then the N kept rows are stored strip-major H[fc][strip][iy][16].
 // Pipeline: y[fc] and the chunk of the next item are fetched right after this item's spread.
-template <int G, bool SEP, bool DYN>
-__global__ void __launch_bounds__(SW * FFTShape<G>::T, (SEP || G >= 1024) ? 1 : 2)
+// T2 (G = 512, SEP): two threads per stage-2 transform, 32 threads per column (16 warps per CTA
+// instead of 8 at the same shared-memory footprint).  Stage 1 is one P-point DFT per thread; in
+// stage 2 the lane pair (l, l ^ 16) splits the radix-4 decimation of the Q-point DFT -- lane half
+// h owns the sub-transforms of n2 = h, h + 2 (mod 4) -- and exchanges the half-combined values by
+// shuffle; the operations and their order per output are those of dft_halfout, so the two
+// variants agree bit for bit.
+template <int G, bool SEP, bool DYN, bool T2 = false>
+__global__ void __launch_bounds__(SW * FFTShape<G>::T * (T2 ? 2 : 1), (SEP || G >= 1024) ? 1 : 2)
 k_adj_cols(DevPlan p, const float2* __restrict__ y, float2* __restrict__ H, int l0, int nb, int ystage, int stage_cap,
            int* __restrict__ ctr) {
   // DYN: after its first item (blockIdx.x) a CTA takes the next unclaimed item from the
@@ -690,7 +696,8 @@ k_adj_cols(DevPlan p, const float2* __restrict__ y, float2* __restrict__ H, int 
   // left the SMs' busy time spread 69 k .. 95 k cycles around an 82 k mean); the last CTA to exit
   // (ctr[1]) resets both words for the next launch on this lane.
   using F = FFTShape<G>;
-  constexpr int P = F::P, Q = F::Q, T = F::T, N = G / 2, A = Q / T, B = P / T, S = G / SW;
+  constexpr int P = F::P, Q = F::Q, T = F::T * (T2 ? 2 : 1), N = G / 2, A = Q / T, B = T2 ? 1 : P / T, S = G / SW;
+  static_assert(!T2 || (SEP && T == Q && Q == 32 && 2 * P == T), "T2: G = 512 with the separate exchange buffer");
   // SEP (G <= 512): the spread strip S and the FFT exchange buffer E are separate, so S only ever
   // holds spread values and zeros: the stage-1 loads skip the row pairs the chunk's row mask marks
   // untouched and re-zero only the touched ones, and the stage-1 twiddles live in registers.
@@ -773,7 +780,10 @@ k_adj_cols(DevPlan p, const float2* __restrict__ y, float2* __restrict__ H, int 
     ++nit;
     // row-pair mask of this warp's stage-1 loads: bit a*P + n1 <=> rows Q n1 + T a + 2 warp + {0,1}
     // received spread values (read before the staging buffer is refilled)
-    const uint32_t rmask = SEP ? (uint32_t)stage[kChunkHdr + warp] : ~0u;
+    // (T2: warp w holds n2 = 2w + {0,1} = T' a + 2w' + {0,1} of the 8-warp layout, a = w >> 3, w' = w & 7)
+    const uint32_t rmask = !SEP ? ~0u
+                           : T2 ? ((uint32_t)stage[kChunkHdr + (warp & 7)] >> (P * (warp >> 3))) & ((1u << P) - 1u)
+                                : (uint32_t)stage[kChunkHdr + warp];
     {
       // Staged prefix of the chunk: header, slice table and cells always fit (checked at plan
       // time); a slice whose entries lie past the staged prefix reads them from L2.
@@ -904,6 +914,28 @@ k_adj_cols(DevPlan p, const float2* __restrict__ y, float2* __restrict__ H, int 
     }
     __syncthreads();
     pt.mark(4);
+    float2* Hc = H + (size_t)fc * N * G + (size_t)(item % S) * SW + c;    // row-major [fc][iy][G]
+    if constexpr (T2) {
+      // lane half h = t & 1 (lanes l and l ^ 16 share k1 = t >> 1): sub-transforms q = h and h + 2 of
+      // the radix-4 decimation in time, D_q[K] = sum_i ex[n2 = 4 i + q] W_8^{iK}
+      const int h = t & 1, k1 = t >> 1;
+      float2 da[Q / 4], db[Q / 4];
+#pragma unroll
+      for (int i = 0; i < Q / 4; ++i) {
+        da[i] = ex[((4 * i + h) * P + k1) * SW + c];
+        db[i] = ex[((4 * i + h + 2) * P + k1) * SW + c];
+      }
+      pt.mark(5);
+      dft<Q / 4, +1>(da);
+      dft<Q / 4, +1>(db);
+      float2 out[Q / 4];
+      detail::t2_combine<Q, +1, 0>(out, da, db, h);
+#pragma unroll
+      for (int K = 0; K < Q / 4; ++K) {
+        const int k2 = h ? K + 3 * Q / 4 : K;
+        Hc[(size_t)grid_to_img<G>(k1 + P * k2) * G] = out[K];
+      }
+    } else {
     float2 w[B][Q];
 #pragma unroll
     for (int b = 0; b < B; ++b) {
@@ -916,7 +948,6 @@ k_adj_cols(DevPlan p, const float2* __restrict__ y, float2* __restrict__ H, int 
       }
     }
     pt.mark(5);
-    float2* Hc = H + (size_t)fc * N * G + (size_t)(item % S) * SW + c;    // row-major [fc][iy][G]
 #pragma unroll
     for (int b = 0; b < B; ++b) {
       const int k1 = t + T * b;
@@ -925,6 +956,7 @@ k_adj_cols(DevPlan p, const float2* __restrict__ y, float2* __restrict__ H, int 
       for (int k2 = 0; k2 < Q; ++k2) {
         if (k2 < Q / 4 || k2 >= 3 * Q / 4) Hc[(size_t)grid_to_img<G>(k1 + P * k2) * G] = w[b][k2];
       }
+    }
     }
     pt.mark(6);
     // !SEP: zero-fill visible before the next spread.  SEP: the next item's spread and exchange are

@@ -66,7 +66,7 @@ struct DeviceGuard {
 
 }  // namespace
 
-static constexpr int kMaxLanes = 4;
+static constexpr int kMaxLanes = 8;
 
 struct CgKey {   // the arguments a captured CG graph bakes in
   const void *x = nullptr, *y = nullptr, *z = nullptr;
@@ -79,6 +79,7 @@ struct CgKey {   // the arguments a captured CG graph bakes in
   }
 };
 static constexpr int kDefaultLanes = 2;
+static int cols_threads_rt(int G);
 
 struct mrf_plan_s {
   // sizes
@@ -89,6 +90,8 @@ struct mrf_plan_s {
   int bf = 1;               // frames per batch
   int nsm = 148;            // SMs of the device
   bool adj_sep = false;      // k_adj_cols variant with the separate exchange buffer (one CTA per SM)
+  bool adj_t2 = false;       // k_adj_cols with two threads per stage-2 transform (G = 512: 16 warps per CTA)
+  int adj_threads() const { return cols_threads_rt(G) * (adj_t2 ? 2 : 1); }
   int ystage = 0;           // bytes of y[fc] k_adj_cols stages in shared memory (M*8 if M even, M*8 <= kYBytes)
   int occ_fr0 = 1, occ_fr1 = 1, occ_fc = 1, occ_ac = 1, occ_ar = 1;   // resident CTAs per SM
   int fc_stage = 0, ac_stage = 0;   // chunk staging bytes of the column kernels
@@ -410,6 +413,9 @@ __global__ void k_dcf_scale(float2* __restrict__ yw, const float2* __restrict__ 
 // (dynamic item hand-out; plans whose spread chunks mostly overflow the staging buffer)
 template <int G>
 static void (*adj_cols_kernel(const mrf_plan_s* pl))(DevPlan, const float2*, float2*, int, int, int, int, int*) {
+  if constexpr (G == 512) {
+    if (pl->adj_sep && pl->adj_t2) return pl->adj_dyn ? k_adj_cols<G, true, true, true> : k_adj_cols<G, true, false, true>;
+  }
   if (pl->adj_sep) return pl->adj_dyn ? k_adj_cols<G, (G <= 512), true> : k_adj_cols<G, (G <= 512), false>;
   return pl->adj_dyn ? k_adj_cols<G, false, true> : k_adj_cols<G, false, false>;
 }
@@ -436,6 +442,8 @@ static mrf_status setup_kernels(mrf_plan_s* pl) {
   pl->acol_smem = (int)s_acol;
   pl->fc_stage = (int)((s_col - fwd_cols_fixed<G>()) & ~size_t(15));
   pl->adj_sep = G <= 512 && actas == 1;
+  pl->adj_t2 = false;
+  if (const char* e = std::getenv("MRF_ADJ_T2")) pl->adj_t2 = G == 512 && pl->adj_sep && e[0] == '1';
   pl->ac_stage = (int)((s_acol - adj_cols_fixed<G>((size_t)pl->ystage, pl->adj_sep)) & ~size_t(15));
   CUDA_TRY(cudaFuncSetAttribute(k_fwd_rows<G, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s_fr0));
   CUDA_TRY(cudaFuncSetAttribute(k_fwd_rows<G, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s_fr1));
@@ -450,7 +458,7 @@ static mrf_status setup_kernels(mrf_plan_s* pl) {
   CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pl->occ_fc, k_fwd_cols<G>, ncol, s_col));
   CUDA_TRY(cudaFuncSetAttribute(k_toep_cols<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)toep_cols_smem<G>()));
   CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pl->occ_tc, k_toep_cols<G>, ncol, toep_cols_smem<G>()));
-  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pl->occ_ac, adj_kernel, ncol, s_acol));
+  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pl->occ_ac, adj_kernel, pl->adj_threads(), s_acol));
   CUDA_TRY(cudaFuncSetAttribute(k_sn_fcols<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sn_cols_smem<G>()));
   CUDA_TRY(cudaFuncSetAttribute(k_sn_icols<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sn_cols_smem<G>()));
   if (pl->occ_fr0 < 1 || pl->occ_fr1 < 1 || pl->occ_ar < 1 || pl->occ_fc < 1 || pl->occ_ac < 1)
@@ -487,8 +495,20 @@ static cudaError_t launch_pdl(void (*kern)(KArgs...), int grid, int block, size_
   return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
 }
 
-static int pgrid(mrf_plan_s* pl, int occ, long long items) {
-  return (int)std::max<long long>(1, std::min<long long>(items, (long long)occ * pl->nsm));
+// Experiment knobs MRF_GCAP_FR / _FC / _AC / _AR: upper bound on the CTAs of one launch of the forward-row,
+// forward-column, adjoint-column and adjoint-row kernels (0 = resident CTAs x SMs, the default), so that
+// kernels of several lanes can share the SMs side by side.
+static int g_gcap[4] = {0, 0, 0, 0};
+static bool g_gcap_init = [] {
+  const char* names[4] = {"MRF_GCAP_FR", "MRF_GCAP_FC", "MRF_GCAP_AC", "MRF_GCAP_AR"};
+  for (int i = 0; i < 4; ++i)
+    if (const char* e = std::getenv(names[i])) g_gcap[i] = std::max(0, std::atoi(e));
+  return true;
+}();
+static int pgrid(mrf_plan_s* pl, int occ, long long items, int cls = -1) {
+  long long g = std::min<long long>(items, (long long)occ * pl->nsm);
+  if (cls >= 0 && g_gcap[cls] > 0) g = std::min<long long>(g, g_gcap[cls]);
+  return (int)std::max<long long>(1, g);
 }
 
 template <int G>
@@ -496,7 +516,7 @@ static mrf_status launch_fwd_rows(mrf_plan_s* pl, const float2* x, float2* H, in
                                   float2* yzero = nullptr, long long nyzero = 0) {
   const long long items = (long long)nb * (pl->N / RowCfg<G>::RPC) * pl->C;
   ProfScope ps(pl, MRF_K_FWD_ROWS, st);
-  CUDA_TRY(launch_pdl(k_fwd_rows<G, 0>, pgrid(pl, pl->occ_fr0, items), kRowThreads, fwd_rows_smem<G>(1), st, pl->dp(),
+  CUDA_TRY(launch_pdl(k_fwd_rows<G, 0>, pgrid(pl, pl->occ_fr0, items, 0), kRowThreads, fwd_rows_smem<G>(1), st, pl->dp(),
                       x, H, l0, nb, nullptr, nullptr, nullptr, nullptr, yzero, nyzero, (double2*)nullptr));
   return MRF_OK;
 }
@@ -505,7 +525,7 @@ static mrf_status launch_fwd_rows_cg(mrf_plan_s* pl, float2* x, float2* H, int l
                                      float2* yzero, long long nyzero, double2* pn = nullptr) {
   const long long items = (long long)nb * (pl->N / RowCfg<G>::RPC) * pl->C;
   ProfScope ps(pl, MRF_K_FWD_ROWS, st);
-  CUDA_TRY(launch_pdl(k_fwd_rows<G, 1>, pgrid(pl, pl->occ_fr1, items), kRowThreads, fwd_rows_smem<G>(3), st, pl->dp(),
+  CUDA_TRY(launch_pdl(k_fwd_rows<G, 1>, pgrid(pl, pl->occ_fr1, items, 0), kRowThreads, fwd_rows_smem<G>(3), st, pl->dp(),
                       nullptr, H, l0, nb, pl->cg_rin ? pl->cg_rin : pl->r, pl->p, x, &pl->sc->alpha, yzero, nyzero, pn));
   return MRF_OK;
 }
@@ -513,7 +533,7 @@ template <int G>
 static mrf_status launch_fwd_cols(mrf_plan_s* pl, const float2* H, float2* y, int l0, int nb, cudaStream_t st) {
   const long long items = (long long)nb * pl->C * pl->S;
   ProfScope ps(pl, MRF_K_FWD_COLS, st);
-  CUDA_TRY(launch_pdl(k_fwd_cols<G>, pgrid(pl, pl->occ_fc, items), cols_threads<G>(), pl->col_smem, st, pl->dp(), H, y,
+  CUDA_TRY(launch_pdl(k_fwd_cols<G>, pgrid(pl, pl->occ_fc, items, 1), cols_threads<G>(), pl->col_smem, st, pl->dp(), H, y,
                       l0, nb, pl->fc_stage));
   return MRF_OK;
 }
@@ -525,7 +545,7 @@ static mrf_status launch_adj_cols(mrf_plan_s* pl, const float2* y, float2* H, in
   const int stage = ys ? pl->ac_stage : (int)(((size_t)pl->acol_smem - adj_cols_fixed<G>(0, pl->adj_sep)) & ~size_t(15));
   ProfScope ps(pl, MRF_K_ADJ_COLS, st);
   auto adj_kernel = adj_cols_kernel<G>(pl);
-  CUDA_TRY(launch_pdl(adj_kernel, pgrid(pl, pl->occ_ac, items), cols_threads<G>(), pl->acol_smem, st, pl->dp(), y, H,
+  CUDA_TRY(launch_pdl(adj_kernel, pgrid(pl, pl->occ_ac, items, 2), pl->adj_threads(), pl->acol_smem, st, pl->dp(), y, H,
                       l0, nb, ys, stage, pl->adj_dyn ? pl->ctrs + 8 * slot : (int*)nullptr));
   return MRF_OK;
 }
@@ -535,10 +555,10 @@ static mrf_status launch_adj_rows(mrf_plan_s* pl, const float2* H, float2* out, 
   const long long items = (long long)nb * (pl->N / RowCfg<G>::RPC);
   ProfScope ps(pl, MRF_K_ADJ_ROWS, st);
   if (rres)
-    CUDA_TRY(launch_pdl(k_adj_rows<G, true>, pgrid(pl, pl->occ_ar, items), kRowThreads, adj_rows_smem<G>(), st, pl->dp(),
+    CUDA_TRY(launch_pdl(k_adj_rows<G, true>, pgrid(pl, pl->occ_ar, items, 3), kRowThreads, adj_rows_smem<G>(), st, pl->dp(),
                         H, out, xin, mu, l0, nb, dot, rres, (const double*)&pl->sc->alpha));
   else
-    CUDA_TRY(launch_pdl(k_adj_rows<G, false>, pgrid(pl, pl->occ_ar, items), kRowThreads, adj_rows_smem<G>(), st, pl->dp(),
+    CUDA_TRY(launch_pdl(k_adj_rows<G, false>, pgrid(pl, pl->occ_ar, items, 3), kRowThreads, adj_rows_smem<G>(), st, pl->dp(),
                         H, out, xin, mu, l0, nb, dot, (float2*)nullptr, (const double*)nullptr));
   return MRF_OK;
 }
@@ -548,7 +568,7 @@ static mrf_status launch_toep_cols(mrf_plan_s* pl, const float2* Hf, float2* Ha,
                                    double2* tq = nullptr) {
   const long long items = (long long)nb * pl->C * pl->S;
   ProfScope ps(pl, MRF_K_FWD_COLS, st);
-  CUDA_TRY(launch_pdl(k_toep_cols<G>, pgrid(pl, pl->occ_tc, items), cols_threads<G>(), toep_cols_smem<G>(), st, pl->dp(),
+  CUDA_TRY(launch_pdl(k_toep_cols<G>, pgrid(pl, pl->occ_tc, items, 1), cols_threads<G>(), toep_cols_smem<G>(), st, pl->dp(),
                       Hf, Ha, pl->psf, l0, nb, tq));
   return MRF_OK;
 }
@@ -1558,7 +1578,10 @@ mrf_status mrf_plan_create(const mrf_plan_desc* d, mrf_plan* out) {
       // slices last.  Slices [0, n_multi) are the ones wider than 1.
       // measured: 128 (stress normal 254 -> 83 ms); a lower threshold costs more in per-slice
       // reductions than it saves (MRF, where no cell exceeds 120 entries, is unaffected)
-      constexpr int kSplitEntries = 128;
+      static const int kSplitEntries = [] {   // MRF_SPLIT: experiment knob
+        const char* e = std::getenv("MRF_SPLIT");
+        return e ? std::max(32, std::atoi(e)) : 128;
+      }();
       std::vector<int2> slices;   // {first row index, width (< 0: reduction slice of one row)}
       size_t r0 = 0;
       while (r0 < rows.size() && rows[r0].y > kSplitEntries) {
@@ -1707,7 +1730,12 @@ mrf_status mrf_plan_create(const mrf_plan_desc* d, mrf_plan* out) {
     mean /= (double)atab.size();
     pl->adj_dyn = pl->ctrs && mean > 0.5 * pl->ac_stage;
     if (const char* e = std::getenv("MRF_ADJ_DYN")) pl->adj_dyn = pl->ctrs && e[0] == '1';
-    if (pl->adj_dyn) {
+    // The same plans (spread-heavy items) take the 16-warp variant of the kernel (two threads per
+    // stage-2 transform, k_adj_cols<.., T2>): measured stress A^H A 69.9 -> 68.0 ms, while the MRF
+    // adjoint, whose items are bound by the FFT's shared-memory traffic, loses 14 % with it
+    // (0.920 -> 1.049 ms).  MRF_ADJ_T2=0/1 overrides.
+    if (std::getenv("MRF_ADJ_T2") == nullptr) pl->adj_t2 = pl->adj_dyn && G == 512 && pl->adj_sep;
+    if (pl->adj_dyn || pl->adj_t2) {
       auto k = [&]() { DISPATCH_G(pl, adj_cols_attr, pl); };
       if ((s = k())) return bail(s);
     }

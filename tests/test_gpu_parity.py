@@ -613,6 +613,27 @@ def test_split_phase_cg_matches_textbook_cg(mrf, monkeypatch, name, normal):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("name", ["mrf", "stress"])
+def test_two_thread_stage2_variant_is_bitwise_identical(mrf, monkeypatch, name):
+    """k_adj_cols<G = 512> has a 16-warp variant (two threads per stage-2 transform, the lane pair
+    exchanging its half-combined radix-4 values by shuffle; chosen for spread-heavy plans,
+    MRF_ADJ_T2 overrides).  It performs the same floating-point operations in the same order per
+    output as the 8-warp kernel, so adjoint, normal operator and CG must agree bit for bit."""
+    over = dict(frames=range(3)) if name == "stress" else dict(frames=range(40))
+    cfg, traj, coils, frames, x = setup(name, **over)
+    yr = synth.random_kspace(cfg.C, cfg.M, frames, cfg.seed)
+    out = {}
+    for t2 in ("0", "1"):
+        monkeypatch.setenv("MRF_ADJ_T2", t2)
+        pl = plan_for(mrf, cfg, traj, coils, frames, batch_frames=max(1, len(frames) // 3))
+        xs, _ = pl.dc_cg(dev(yr), mu=cfg.mu, n_iter=3)
+        out[t2] = (host(pl.adjoint(dev(yr))), host(pl.normal(dev(x), mu=cfg.mu)), host(xs))
+        pl.close()
+    for a, b in zip(out["0"], out["1"]):
+        assert np.array_equal(a, b)
+
+
+@pytest.mark.gpu
 @pytest.mark.parametrize("name", ["cfg2", "stress"])
 def test_dynamic_item_handout_is_bitwise_identical(mrf, monkeypatch, name):
     """k_adj_cols hands its items out dynamically on plans whose spread chunks overflow the
