@@ -508,6 +508,15 @@ static bool g_gcap_init = [] {
 static int pgrid(mrf_plan_s* pl, int occ, long long items, int cls = -1) {
   long long g = std::min<long long>(items, (long long)occ * pl->nsm);
   if (cls >= 0 && g_gcap[cls] > 0) g = std::min<long long>(g, g_gcap[cls]);
+  // Column kernels walk items (fc, strip) round-robin, item % S = strip: a grid that shares a factor
+  // with S confines each CTA to the strips of one residue class, and the strips next to DC carry
+  // several times the mean gather / spread work (a grid of 128 CTAs, a multiple of the 32 strips,
+  // measured 2.28 ms for the MRF normal operator against 1.59 ms).  Take the next smaller grid
+  // coprime with S (148 SMs: 147 and 295 CTAs; adjoint 0.919 -> 0.906 ms).
+  if ((cls == 1 || cls == 2) && items > g && pl->S > 1) {
+    auto gcd = [](long long a, long long b) { while (b) { const long long t = a % b; a = b; b = t; } return a; };
+    while (g > 1 && gcd(g, pl->S) != 1) --g;
+  }
   return (int)std::max<long long>(1, g);
 }
 
