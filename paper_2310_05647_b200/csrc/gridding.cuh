@@ -645,16 +645,30 @@ __device__ __forceinline__ void spread_cells(const int2* sl_tab, const unsigned 
     } else {
       const int2* ep = gents + si.x + lane;
       int kk = 0;
-      if (PASS == 2)   // (the direct path of oversized chunks)
-      for (; kk + 7 < width; kk += 8) {   // eight L2 loads in flight, the sum in entry order
-        int2 e[8];
+      if (PASS == 2) {   // (the direct path of oversized chunks)
+        for (; kk + 7 < width; kk += 8) {   // eight L2 loads in flight, the sum in entry order
+          int2 e[8];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          e[u] = __ldg(ep + (kk + u) * 32);
-          MRF_CHECK((unsigned)e[u].x < (unsigned)M);
+          for (int u = 0; u < 8; ++u) {
+            e[u] = __ldg(ep + (kk + u) * 32);
+            MRF_CHECK((unsigned)e[u].x < (unsigned)M);
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u) acc = caxpy(__int_as_float(e[u].y), YS ? ys[e[u].x] : __ldg(yf + e[u].x), acc);
         }
+        if (kk < width) {   // the last (width % 8) steps: their loads in flight together as well
+          int2 e[7];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) acc = caxpy(__int_as_float(e[u].y), YS ? ys[e[u].x] : __ldg(yf + e[u].x), acc);
+          for (int u = 0; u < 7; ++u)
+            if (kk + u < width) e[u] = __ldg(ep + (kk + u) * 32);
+#pragma unroll
+          for (int u = 0; u < 7; ++u)
+            if (kk + u < width) {
+              MRF_CHECK((unsigned)e[u].x < (unsigned)M);
+              acc = caxpy(__int_as_float(e[u].y), YS ? ys[e[u].x] : __ldg(yf + e[u].x), acc);
+            }
+          kk = width;
+        }
       }
 #pragma unroll 4
       for (; kk < width; ++kk) {
@@ -808,8 +822,15 @@ k_adj_cols(DevPlan p, const float2* __restrict__ y, float2* __restrict__ H, int 
         // bulk copies over the (consumed) entry region; a slice wider than the region reads L2.
         const int cap = (copied / 4 - ent_off) / 2;          // entries that fit
         const int nent = (chunk_words - ent_off) / 2;
+        // first wide slice whose entries are not all staged (slice ends increase with the slice
+        // index: binary search, a dense chunk has hundreds of slices)
         int sl0 = 0;
-        while (sl0 < n_multi && sl_tab[sl0].x + 32 * abs(sl_tab[sl0].y) <= n_staged) ++sl0;
+        for (int hi = n_multi; sl0 < hi;) {
+          const int mid = (sl0 + hi) >> 1;
+          const int2 sm = sl_tab[mid];
+          if (sm.x + 32 * abs(sm.y) <= n_staged) sl0 = mid + 1;
+          else hi = mid;
+        }
         // A chunk that needs more than one further window (the centre strips of a dense spiral:
         // stress) reads the rest of its slices straight from L2, eight loads in flight per lane,
         // instead of streaming windows (two barriers and a copy round trip each); one window

@@ -1739,11 +1739,10 @@ mrf_status mrf_plan_create(const mrf_plan_desc* d, mrf_plan* out) {
     mean /= (double)atab.size();
     pl->adj_dyn = pl->ctrs && mean > 0.5 * pl->ac_stage;
     if (const char* e = std::getenv("MRF_ADJ_DYN")) pl->adj_dyn = pl->ctrs && e[0] == '1';
-    // The same plans (spread-heavy items) take the 16-warp variant of the kernel (two threads per
-    // stage-2 transform, k_adj_cols<.., T2>): measured stress A^H A 69.9 -> 68.0 ms, while the MRF
-    // adjoint, whose items are bound by the FFT's shared-memory traffic, loses 14 % with it
-    // (0.920 -> 1.049 ms).  MRF_ADJ_T2=0/1 overrides.
-    if (std::getenv("MRF_ADJ_T2") == nullptr) pl->adj_t2 = pl->adj_dyn && G == 512 && pl->adj_sep;
+    // The 16-warp variant of the kernel (two threads per stage-2 transform, k_adj_cols<.., T2>) is
+    // an option only (MRF_ADJ_T2=1): it gained 2.7 % on stress before the direct path's remainder
+    // loads were batched and nothing after (65.0 vs 64.9 ms), and loses 14 % on MRF, whose items are
+    // bound by the FFT's shared-memory traffic (adjoint 0.920 -> 1.049 ms).
     if (pl->adj_dyn || pl->adj_t2) {
       auto k = [&]() { DISPATCH_G(pl, adj_cols_attr, pl); };
       if ((s = k())) return bail(s);

@@ -616,8 +616,7 @@ def test_split_phase_cg_matches_textbook_cg(mrf, monkeypatch, name, normal):
 @pytest.mark.parametrize("name", ["mrf", "stress"])
 def test_two_thread_stage2_variant_is_bitwise_identical(mrf, monkeypatch, name):
     """k_adj_cols<G = 512> has a 16-warp variant (two threads per stage-2 transform, the lane pair
-    exchanging its half-combined radix-4 values by shuffle; chosen for spread-heavy plans,
-    MRF_ADJ_T2 overrides).  It performs the same floating-point operations in the same order per
+    exchanging its half-combined radix-4 values by shuffle; an option, MRF_ADJ_T2=1).  It performs the same floating-point operations in the same order per
     output as the 8-warp kernel, so adjoint, normal operator and CG must agree bit for bit."""
     over = dict(frames=range(3)) if name == "stress" else dict(frames=range(40))
     cfg, traj, coils, frames, x = setup(name, **over)
