@@ -835,7 +835,10 @@ k_adj_cols(DevPlan p, const float2* __restrict__ y, float2* __restrict__ H, int 
         // stress) reads the rest of its slices straight from L2, eight loads in flight per lane,
         // instead of streaming windows (two barriers and a copy round trip each); one window
         // is still cheaper than L2 latency (measured: stress normal -4 %, MRF unchanged).
-        const bool direct = MRF_DBG_ON(4) || (nent - n_staged > cap);
+        // (With the direct path's loads batched eight deep through the slice tails, it also beats the
+        // single window: MRF adjoint 0.951 -> 0.943 ms; MRF_DBG=8 of the experiment build restores
+        // the windows for overflows of at most one window.)
+        const bool direct = !MRF_DBG_ON(8) || (nent - n_staged > cap);
         if (direct) {
           if (ystage)
             spread_cells<true, 2>(sl_tab, cells, ents, gents, n_staged, 0, sl0, n_multi, true, nsl, n_multi, ys, yf,
