@@ -200,19 +200,22 @@ __global__ void __launch_bounds__(kVecThreads) k_sqnorm(const float2* __restrict
   if (threadIdx.x == 0) part[blockIdx.x] = s;
 }
 
-// r = rhs - q ; p = r  (initial residual; q == nullptr: x0 = 0, r = rhs); partial <r,r>
-__global__ void __launch_bounds__(kVecThreads) k_cg_init(const float2* __restrict__ rhs, const float2* __restrict__ q,
-                                                         float2* __restrict__ r, float2* __restrict__ pv, size_t n,
+// r = rhs - q ; p = r  (initial residual; q == nullptr: x0 = 0, r = rhs); partial <r,r>.
+// rhs may be r itself (the solver's call): with q == nullptr r already holds its value and is
+// not rewritten (one image pass fewer).
+__global__ void __launch_bounds__(kVecThreads) k_cg_init(const float2* rhs, const float2* __restrict__ q,
+                                                         float2* r, float2* __restrict__ pv, size_t n,
                                                          double2* __restrict__ part) {
   const float4* rh4 = reinterpret_cast<const float4*>(rhs);
   const float4* q4 = reinterpret_cast<const float4*>(q);
   float4* r4 = reinterpret_cast<float4*>(r);
   float4* p4 = reinterpret_cast<float4*>(pv);
+  const bool keep_r = q == nullptr && rhs == r;
   double2 s = make_double2(0.0, 0.0);
   MRF_VEC4_LOOP(n / 2, {
     const float4 a = rh4[i], b = q4 ? q4[i] : make_float4(0.f, 0.f, 0.f, 0.f);
     const float4 v = make_float4(a.x - b.x, a.y - b.y, a.z - b.z, a.w - b.w);
-    r4[i] = v;
+    if (!keep_r) r4[i] = v;
     p4[i] = v;
     s.x += norm2d(v);
   })
